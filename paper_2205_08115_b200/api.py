@@ -1,0 +1,401 @@
+"""Python mirror of the reference solver interface (``gw::`` namespace).
+
+Names, argument meaning, validation order and exception classes follow
+``/root/reference/proj/include/gw/{types,solvers,projections,diagnostics}.hpp``
+so parity tests read like the reference's own tests.  Every compute call goes
+through the C-ABI in ``libgwb.so`` (include/gwb.h); there is no Python or CPU
+fallback for the solver path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import abi
+from .abi import (ConfigError, DimensionMismatchError, NumericalInstabilityError,  # noqa: F401
+                  UnsupportedError, ZeroSumLineError, DomainError)
+
+ROWS, COLS = abi.ROWS, abi.COLS
+
+
+def _f64(a, order="F") -> np.ndarray:
+    return np.require(np.asarray(a, dtype=np.float64), requirements=[order[0] + "_CONTIGUOUS", "ALIGNED"])
+
+
+def _ptr(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ---------------------------------------------------------------------------
+# Value types (types.hpp:62-118, types.cpp:68-153)
+# ---------------------------------------------------------------------------
+class DistanceMatrix:
+    """Symmetric nonnegative structure matrix; construction symmetrizes
+    (A + Aᵀ)/2 and rejects negative or non-finite entries (types.cpp:68-84)."""
+
+    def __init__(self, entries):
+        a = np.asarray(entries, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            r, c = (a.shape + (0, 0))[:2] if a.ndim == 2 else (a.size, 1)
+            raise DimensionMismatchError(f"distance matrix must be square, got {r}x{c}")
+        if a.shape[0] == 0:
+            raise DimensionMismatchError("distance matrix must be nonempty")
+        e = 0.5 * (a + a.T)
+        if not np.all(np.isfinite(e)):
+            raise ValueError("distance matrix has non-finite entries")
+        if np.any(e < 0.0):
+            raise ValueError("distance matrix has negative entries")
+        self._e = np.asfortranarray(e)
+
+    @classmethod
+    def trusted(cls, entries: np.ndarray) -> "DistanceMatrix":
+        """Wrap an already-symmetric, validated matrix without the O(n²) copy."""
+        obj = cls.__new__(cls)
+        obj._e = _f64(entries)
+        return obj
+
+    def size(self) -> int:
+        return self._e.shape[0]
+
+    def entries(self) -> np.ndarray:
+        return self._e
+
+
+class ProbabilityVector:
+    """Strictly positive weights summing to 1 within 1e-12 (types.cpp:86-108)."""
+
+    def __init__(self, weights):
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).ravel())
+        if w.size == 0:
+            raise ValueError("probability vector must be nonempty")
+        if not np.all(np.isfinite(w)):
+            raise ValueError("probability vector has non-finite entries")
+        if np.any(w <= 0.0):
+            raise ValueError("probability vector entries must be strictly positive; remove "
+                             "zero-mass points before construction")
+        mass = float(np.sum(w))
+        if abs(mass - 1.0) > 1e-12:
+            raise ValueError(f"probability vector sums to {mass:g}, expected 1 within 1e-12")
+        self._w = w
+
+    @staticmethod
+    def uniform(n: int) -> "ProbabilityVector":
+        return ProbabilityVector(np.full(n, 1.0 / n))
+
+    def size(self) -> int:
+        return self._w.size
+
+    def weights(self) -> np.ndarray:
+        return self._w
+
+
+class Coupling:
+    """Nonnegative matrix of total mass 1 within 1e-9 (types.cpp:110-126)."""
+
+    def __init__(self, entries):
+        e = np.asarray(entries, dtype=np.float64)
+        if e.ndim != 2 or e.shape[0] == 0 or e.shape[1] == 0:
+            raise DimensionMismatchError("coupling must be nonempty")
+        if not np.all(np.isfinite(e)):
+            raise ValueError("coupling has non-finite entries")
+        if np.any(e < 0.0):
+            raise ValueError("coupling has negative entries")
+        mass = float(np.sum(e))
+        if abs(mass - 1.0) > 1e-9:
+            raise ValueError(f"coupling total mass is {mass:g}, expected 1 within 1e-9")
+        self._e = e
+
+    def rows(self) -> int:
+        return self._e.shape[0]
+
+    def cols(self) -> int:
+        return self._e.shape[1]
+
+    def entries(self) -> np.ndarray:
+        return self._e
+
+
+@dataclass
+class SolverConfig:
+    """gw::SolverConfig with the protocol defaults (types.hpp:132-147)."""
+
+    algorithm: str = "bapg"
+    geometry: str = "entropy"
+    rho: float = 0.1
+    step: float = 5.0
+    epsilon_reg: float = 0.1
+    inner_iters: int = 1000
+    inner_tol: float = 1e-9
+    rel_tol: float = 1e-6
+    max_iters: int = 2000
+    perturbation: float = 0.0
+    switch_iters: int = 200
+    seed: int = 0
+    log_domain: bool = False
+    record_residual: bool = False
+    # B200 extensions
+    precision: str = "auto"   # auto | tf32 | 3xtf32
+    quiet: bool = False
+
+    def to_abi(self) -> abi.Config:
+        prec = {"auto": abi.PREC_AUTO, "tf32": abi.PREC_TF32, "3xtf32": abi.PREC_3XTF32}
+        if self.algorithm not in abi.ALGORITHMS:
+            raise ConfigError(f"unknown solver '{self.algorithm}' (expected bapg|bpg|ebpg|hbpg|fw)")
+        if self.geometry not in ("entropy", "quadratic"):
+            raise ConfigError(f"unknown geometry '{self.geometry}' (expected entropy|quadratic)")
+        return abi.default_config(
+            algorithm=abi.ALGORITHMS[self.algorithm],
+            geometry=abi.ENTROPY if self.geometry == "entropy" else abi.QUADRATIC,
+            rho=self.rho, step=self.step, epsilon_reg=self.epsilon_reg,
+            inner_iters=self.inner_iters, inner_tol=self.inner_tol, rel_tol=self.rel_tol,
+            max_iters=self.max_iters, perturbation=self.perturbation,
+            switch_iters=self.switch_iters, seed=self.seed, log_domain=int(self.log_domain),
+            record_residual=int(self.record_residual), precision=prec[self.precision],
+            quiet=int(self.quiet))
+
+
+def validate(config: SolverConfig) -> None:
+    """gw::validate (types.cpp:176-188)."""
+    st = abi.Status()
+    abi.load().gwb_validate_config(C.byref(config.to_abi()), C.byref(st))
+    abi.raise_for(st)
+
+
+def validate_inputs(d_x: DistanceMatrix, d_y: DistanceMatrix, mu: ProbabilityVector,
+                    nu: ProbabilityVector) -> None:
+    """gw::validate_inputs (types.cpp:190-202)."""
+    if d_x.size() != mu.size():
+        raise DimensionMismatchError(
+            f"D_X is {d_x.size()}x{d_x.size()} but mu has length {mu.size()}")
+    if d_y.size() != nu.size():
+        raise DimensionMismatchError(
+            f"D_Y is {d_y.size()}x{d_y.size()} but nu has length {nu.size()}")
+
+
+@dataclass
+class IterationRecord:
+    iter: int = 0
+    objective: float = 0.0
+    marginal_infeasibility: float = 0.0
+    split_gap: float = 0.0
+    residual: Optional[float] = None
+    rel_change: float = 0.0
+    elapsed_seconds: float = 0.0
+    phase: int = 0
+
+
+@dataclass
+class SolveReport:
+    final_coupling: Coupling
+    pi_half: Optional[Coupling] = None
+    w_half: Optional[Coupling] = None
+    trace: List[IterationRecord] = field(default_factory=list)
+    converged: bool = False
+    iterations_used: int = 0
+
+
+@dataclass
+class SolveOptions:
+    initial: Optional[np.ndarray] = None
+    observer: Optional[Callable[[int, np.ndarray, Optional[np.ndarray]], None]] = None
+
+
+_ENTRY = {None: "gwb_solve", "bapg": "gwb_bapg_solve", "bpg": "gwb_bpg_solve",
+          "ebpg": "gwb_ebpg_solve", "hbpg": "gwb_hbpg_solve"}
+
+
+def _solve(entry, d_x, d_y, mu, nu, config, opts):
+    lib = abi.load()
+    opts = opts or SolveOptions()
+    cfg = config.to_abi()
+    # Validation order of the reference (solvers.cpp:141-143): the algorithm
+    # and config checks run in the C-ABI; dimension checks need the objects.
+    if entry is not None and cfg.algorithm != abi.ALGORITHMS[entry]:
+        raise ConfigError(f"{entry}_solve called with algorithm '{config.algorithm}'")
+    validate(config)
+    validate_inputs(d_x, d_y, mu, nu)
+    n, m = d_x.size(), d_y.size()
+    init = None
+    if opts.initial is not None:
+        init = _f64(opts.initial)
+        if init.shape != (n, m):
+            raise DimensionMismatchError("initial coupling shape mismatch")
+    out_final = np.empty((n, m), dtype=np.float64, order="F")
+    is_bapg = cfg.algorithm == abi.BAPG
+    out_pi = np.empty((n, m), dtype=np.float64, order="F") if is_bapg else None
+    out_w = np.empty((n, m), dtype=np.float64, order="F") if is_bapg else None
+    cap = max(1, config.max_iters)
+    trace = (abi.Record * cap)()
+    n_rec, conv, used = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    st = abi.Status()
+
+    cb = abi.OBSERVER()
+    if opts.observer is not None:
+        def _obs(_user, it, pi_p, w_p, nn, mm):
+            pi = np.ctypeslib.as_array(pi_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
+            w = None
+            if w_p:
+                w = np.ctypeslib.as_array(w_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
+            opts.observer(int(it), pi, w)
+            return 0
+        cb = abi.OBSERVER(_obs)
+    fn = getattr(lib, _ENTRY[entry])
+    fn(C.byref(cfg), _ptr(d_x.entries()), n, _ptr(d_y.entries()), m, _ptr(mu.weights()),
+       _ptr(nu.weights()), _ptr(init), cb, None, _ptr(out_final), _ptr(out_pi), _ptr(out_w),
+       trace, cap, C.byref(n_rec), C.byref(conv), C.byref(used), C.byref(st))
+    abi.raise_for(st)
+    recs = [IterationRecord(iter=r.iter, objective=r.objective,
+                            marginal_infeasibility=r.marginal_infeasibility,
+                            split_gap=r.split_gap,
+                            residual=r.residual if r.has_residual else None,
+                            rel_change=r.rel_change, elapsed_seconds=r.elapsed_seconds,
+                            phase=r.phase) for r in trace[: n_rec.value]]
+    return SolveReport(final_coupling=Coupling(out_final),
+                       pi_half=Coupling(out_pi) if is_bapg else None,
+                       w_half=Coupling(out_w) if is_bapg else None,
+                       trace=recs, converged=bool(conv.value), iterations_used=used.value)
+
+
+def solve(d_x, d_y, mu, nu, config: SolverConfig, opts: Optional[SolveOptions] = None):
+    """gw::solve (solvers.cpp:499-515)."""
+    return _solve(None, d_x, d_y, mu, nu, config, opts)
+
+
+def bapg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
+    """gw::bapg_solve (solvers.cpp:138-217)."""
+    return _solve("bapg", d_x, d_y, mu, nu, config, opts)
+
+
+def bpg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
+    """gw::bpg_solve (solvers.cpp:219-293)."""
+    return _solve("bpg", d_x, d_y, mu, nu, config, opts)
+
+
+def ebpg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
+    """gw::ebpg_solve (solvers.cpp:295-363)."""
+    return _solve("ebpg", d_x, d_y, mu, nu, config, opts)
+
+
+def hbpg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
+    """gw::hbpg_solve (solvers.cpp:365-426)."""
+    return _solve("hbpg", d_x, d_y, mu, nu, config, opts)
+
+
+def gw_objective(d_x: DistanceMatrix, d_y: DistanceMatrix, pi) -> float:
+    """gw::gw_objective (solvers.cpp:64-69)."""
+    p = _f64(pi)
+    out = C.c_double(0.0)
+    st = abi.Status()
+    abi.load().gwb_gw_objective(_ptr(d_x.entries()), d_x.size(), _ptr(d_y.entries()), d_y.size(),
+                                _ptr(p), p.shape[0], p.shape[1], C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def product_coupling(mu: ProbabilityVector, nu: ProbabilityVector) -> Coupling:
+    """gw::product_coupling (types.cpp:204-207)."""
+    out = np.empty((mu.size(), nu.size()), order="F")
+    st = abi.Status()
+    abi.load().gwb_product_coupling(_ptr(mu.weights()), mu.size(), _ptr(nu.weights()), nu.size(),
+                                    _ptr(out), C.byref(st))
+    abi.raise_for(st)
+    return Coupling(out)
+
+
+def lipschitz_bound(d_x: DistanceMatrix, d_y: DistanceMatrix) -> float:
+    """gw::lipschitz_bound (solvers.cpp:133-136)."""
+    out = C.c_double(0.0)
+    st = abi.Status()
+    abi.load().gwb_lipschitz_bound(_ptr(d_x.entries()), d_x.size(), _ptr(d_y.entries()),
+                                   d_y.size(), C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def kl_scale(pi, target: ProbabilityVector, axis: int) -> np.ndarray:
+    """gw::kl_scale (projections.cpp:12-34)."""
+    p = _f64(pi)
+    out = np.empty_like(p, order="F")
+    st = abi.Status()
+    abi.load().gwb_kl_scale(_ptr(p), p.shape[0], p.shape[1], _ptr(target.weights()),
+                            target.size(), axis, _ptr(out), C.byref(st))
+    abi.raise_for(st)
+    return out
+
+
+@dataclass
+class SinkhornResult:
+    coupling: np.ndarray
+    iterations: int = 0
+    marginal_error: float = 0.0
+    converged: bool = False
+
+
+def _sinkhorn(k, mu, nu, tol, max_iters, log_domain):
+    a = _f64(k)
+    n, m = a.shape
+    if n != mu.size() or m != nu.size():
+        name = "sinkhorn_project_log: exponent/marginal" if log_domain else "sinkhorn_project: kernel/marginal"
+        raise DimensionMismatchError(f"{name} shape mismatch")
+    out = np.empty_like(a, order="F")
+    it, err, conv = C.c_int32(0), C.c_double(0.0), C.c_int32(0)
+    st = abi.Status()
+    abi.load().gwb_sinkhorn_project(_ptr(a), n, m, _ptr(mu.weights()), _ptr(nu.weights()), tol,
+                                    max_iters, int(log_domain), _ptr(out), C.byref(it),
+                                    C.byref(err), C.byref(conv), C.byref(st))
+    abi.raise_for(st)
+    return SinkhornResult(out, it.value, err.value, bool(conv.value))
+
+
+def sinkhorn_project(kernel, mu, nu, tol, max_iters) -> SinkhornResult:
+    """gw::sinkhorn_project (projections.cpp:92-116)."""
+    return _sinkhorn(kernel, mu, nu, tol, max_iters, False)
+
+
+def sinkhorn_project_log(exponent, mu, nu, tol, max_iters) -> SinkhornResult:
+    """gw::sinkhorn_project_log (projections.cpp:129-163)."""
+    return _sinkhorn(exponent, mu, nu, tol, max_iters, True)
+
+
+def marginal_infeasibility(pi, mu: ProbabilityVector, nu: ProbabilityVector) -> float:
+    """gw::marginal_infeasibility (diagnostics.cpp:9-20)."""
+    p = _f64(pi)
+    out = C.c_double(0.0)
+    st = abi.Status()
+    abi.load().gwb_marginal_infeasibility(_ptr(p), p.shape[0], p.shape[1], _ptr(mu.weights()),
+                                          mu.size(), _ptr(nu.weights()), nu.size(),
+                                          C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def split_gap(pi, w) -> float:
+    """gw::split_gap (diagnostics.cpp:22-27)."""
+    p, q = _f64(pi), _f64(w)
+    if p.shape != q.shape:
+        raise DimensionMismatchError("split_gap: shape mismatch")
+    out = C.c_double(0.0)
+    st = abi.Status()
+    abi.load().gwb_split_gap(_ptr(p), _ptr(q), p.shape[0], p.shape[1], C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def hard_assignment(pi) -> np.ndarray:
+    """gw::hard_assignment (tasks.cpp:190-200)."""
+    p = _f64(pi)
+    out = np.empty(p.shape[0], dtype=np.int32)
+    st = abi.Status()
+    abi.load().gwb_hard_assignment(_ptr(p), p.shape[0], p.shape[1],
+                                   out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(st))
+    abi.raise_for(st)
+    return out
+
+
+def version() -> str:
+    return abi.load().gwb_version().decode()

@@ -1,0 +1,568 @@
+// capi.cu — the extern "C" boundary (include/gwb.h).
+//
+// Host-side responsibilities only: argument validation in the reference's
+// order (require_algorithm → validate → validate_inputs → initial shape →
+// positivity, solvers.cpp:141-151), error mapping to the reference's
+// exception classes and message formats (types.cpp:54-66), and driving the
+// device engines.  All arithmetic on the solver path runs in the sm_100a
+// kernels; when no device is present every compute entry point fails with
+// GWB_ERR_RUNTIME (there is no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gwb.h"
+#include "../../include/gwb_ext.h"
+#include "solver.cuh"
+#include "standalone.cuh"
+
+#define GWB_STR2(x) #x
+#define GWB_STR(x) GWB_STR2(x)
+
+namespace {
+
+using gwb::BapgEngine;
+
+struct ApiError {
+  int32_t code;
+  std::string msg;
+  int32_t iteration = 0;
+  std::string solver;
+  int32_t axis = 0;
+  int64_t index = 0;
+};
+
+int32_t fill(gwb_status* st, const ApiError& e) {
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->code = e.code;
+    st->iteration = e.iteration;
+    st->axis = e.axis;
+    st->index = e.index;
+    std::snprintf(st->solver, sizeof(st->solver), "%s", e.solver.c_str());
+    std::snprintf(st->message, sizeof(st->message), "%s", e.msg.c_str());
+  }
+  return e.code;
+}
+
+int32_t ok(gwb_status* st) {
+  if (st) std::memset(st, 0, sizeof(*st));
+  return GWB_OK;
+}
+
+std::string fmt(const char* f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  std::vsnprintf(buf, sizeof(buf), f, ap);
+  va_end(ap);
+  return buf;
+}
+
+[[noreturn]] void fail(int32_t code, const std::string& msg) { throw ApiError{code, msg}; }
+
+// NumericalInstabilityError(solver, iter, detail), types.cpp:60-66.
+[[noreturn]] void numerical(const char* solver, int iter, const std::string& detail) {
+  ApiError e{GWB_ERR_NUMERICAL,
+             fmt("numerical instability in %s at iteration %d: %s", solver, iter, detail.c_str())};
+  e.iteration = iter;
+  e.solver = solver;
+  throw e;
+}
+
+// ZeroSumLineError message, types.cpp:54-58.
+std::string zero_sum_msg(int axis, int64_t index) {
+  return fmt("%s %lld has nonpositive sum; cannot rescale", axis == GWB_ROWS ? "row" : "column",
+             static_cast<long long>(index));
+}
+
+template <class F>
+int32_t guarded(gwb_status* st, F&& f) {
+  try {
+    f();
+    return ok(st);
+  } catch (const ApiError& e) {
+    return fill(st, e);
+  } catch (const gwb::CudaError& e) {
+    return fill(st, ApiError{GWB_ERR_RUNTIME, e.what()});
+  } catch (const std::bad_alloc&) {
+    return fill(st, ApiError{GWB_ERR_RUNTIME, "host allocation failed"});
+  } catch (const std::exception& e) {
+    return fill(st, ApiError{GWB_ERR_RUNTIME, e.what()});
+  }
+}
+
+// ---- device selection (side channel; the reference API has none) ----------
+std::mutex g_dev_mu;
+std::vector<int> g_devices;
+
+int primary_device() {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_devices.empty()) {
+    if (const char* env = std::getenv("GWB_DEVICES")) {
+      const char* p = env;
+      while (*p) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) break;
+        g_devices.push_back(static_cast<int>(v));
+        p = *end == ',' ? end + 1 : end;
+      }
+    }
+    if (g_devices.empty()) g_devices.push_back(0);
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(GWB_ERR_RUNTIME, "no CUDA device available: the GW solver path runs only on sm_100 GPUs");
+  }
+  if (g_devices[0] >= count) fail(GWB_ERR_RUNTIME, fmt("device %d not present", g_devices[0]));
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, g_devices[0]);
+  if (prop.major != 10)
+    fail(GWB_ERR_RUNTIME, fmt("device %d is sm_%d%d; this build targets sm_100a", g_devices[0],
+                              prop.major, prop.minor));
+  return g_devices[0];
+}
+
+const char* algo_name(int32_t a) {
+  switch (a) {
+    case GWB_BAPG: return "bapg";
+    case GWB_BPG: return "bpg";
+    case GWB_EBPG: return "ebpg";
+    case GWB_HBPG: return "hbpg";
+    case GWB_FW: return "fw";
+  }
+  return "?";
+}
+
+// validate(SolverConfig), types.cpp:176-188.
+void validate_config(const gwb_config* c) {
+  if (!c) fail(GWB_ERR_CONFIG, "null config");
+  if (c->rho <= 0.0) fail(GWB_ERR_CONFIG, "rho must be positive");
+  if (c->step <= 0.0) fail(GWB_ERR_CONFIG, "step must be positive");
+  if (c->epsilon_reg <= 0.0) fail(GWB_ERR_CONFIG, "eps must be positive");
+  if (c->inner_iters < 1) fail(GWB_ERR_CONFIG, "inner-iters must be >= 1");
+  if (c->inner_tol <= 0.0) fail(GWB_ERR_CONFIG, "inner-tol must be positive");
+  if (c->rel_tol <= 0.0) fail(GWB_ERR_CONFIG, "rel-tol must be positive");
+  if (c->max_iters < 1) fail(GWB_ERR_CONFIG, "max-iters must be >= 1");
+  if (c->perturbation < 0.0 || c->perturbation >= 1.0)
+    fail(GWB_ERR_CONFIG, "perturbation must lie in [0, 1)");
+  if (c->switch_iters < 0) fail(GWB_ERR_CONFIG, "switch-iters must be >= 0");
+}
+
+void require_algorithm(const gwb_config* c, int32_t expected, const char* who) {
+  if (c->algorithm != expected)
+    fail(GWB_ERR_CONFIG, fmt("%s called with algorithm '%s'", who, algo_name(c->algorithm)));
+}
+
+struct SolveOut {
+  double* out_final;
+  double* out_pi;
+  double* out_w;
+  gwb_record* trace;
+  int32_t trace_cap;
+  int32_t* n_records;
+  int32_t* converged;
+  int32_t* iterations_used;
+};
+
+// Decodes DevStatus flags in the reference's precedence (solvers.cpp:164-189).
+void raise_device_flags(const gwb::DevStatus& s, const char* solver) {
+  using namespace gwb;
+  if (s.flags == 0) return;
+  const int it = s.err_iter;
+  if (s.flags & kFlagOverflowA) numerical(solver, it, "exp overflow; increase rho");
+  if (s.flags & kFlagZeroA) numerical(solver, it, zero_sum_msg(GWB_ROWS, s.zero_index));
+  if (s.flags & kFlagOverflowB) numerical(solver, it, "exp overflow; increase rho");
+  if (s.flags & kFlagZeroB) numerical(solver, it, zero_sum_msg(GWB_COLS, s.zero_index));
+  numerical(solver, it, "non-finite iterate");
+}
+
+// bapg_solve (solvers.cpp:138-217) on the device engine.
+void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, int64_t m,
+          const double* mu, const double* nu, const double* initial, gwb_observer observer,
+          void* user, const SolveOut& o) {
+  if (cfg->geometry != GWB_ENTROPY)
+    fail(GWB_ERR_UNSUPPORTED, "quadratic-geometry BAPG is outside the B200 path (DESIGN.md)");
+  if (cfg->record_residual)
+    fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
+  const size_t len = static_cast<size_t>(n) * static_cast<size_t>(m);
+  std::vector<double> w0;
+  if (initial) {
+    // initial_coupling + positivity (solvers.cpp:146-151), w0 = kl_scale(π0, ν, Cols)
+    // (solvers.cpp:152; projections.cpp:23-31) — an O(nm) host pass, once.
+    for (size_t k = 0; k < len; ++k)
+      if (!(initial[k] > 0.0))
+        fail(GWB_ERR_CONFIG,
+             "bapg entropy geometry requires a strictly positive initialization (the product "
+             "coupling qualifies)");
+    w0.assign(initial, initial + len);
+    for (int64_t j = 0; j < m; ++j) {
+      double s = 0.0;
+      for (int64_t i = 0; i < n; ++i) s += w0[j * n + i];
+      if (!(s > 0.0) || !std::isfinite(s)) {
+        ApiError e{GWB_ERR_ZERO_SUM, zero_sum_msg(GWB_COLS, j)};
+        e.axis = GWB_COLS;
+        e.index = j;
+        throw e;
+      }
+      const double f = nu[j] / s;
+      for (int64_t i = 0; i < n; ++i) w0[j * n + i] *= f;
+    }
+  }
+  if (o.trace_cap < cfg->max_iters && o.trace)
+    fail(GWB_ERR_CAPACITY, fmt("trace capacity %d < max_iters %d", o.trace_cap, cfg->max_iters));
+  const int device = primary_device();
+  BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
+  eng.load_host(dx, dy, mu, nu);
+  eng.reset(initial ? w0.data() : nullptr);
+  gwb::DevStatus s;
+  if (!observer) {
+    eng.run(cfg->max_iters, cfg->rel_tol);
+    s = eng.status();
+    raise_device_flags(s, "bapg");
+  } else {
+    // Slow path: host-synchronous iterations so the observer sees π, w.
+    std::vector<double> hp(len), hw(len);
+    for (int k = 0; k < cfg->max_iters; ++k) {
+      eng.iterate(1, cfg->rel_tol, false);
+      s = eng.status();
+      raise_device_flags(s, "bapg");
+      eng.outputs(nullptr, hp.data(), hw.data());
+      if (observer(user, s.iter - 1, hp.data(), hw.data(), n, m) != 0)
+        fail(GWB_ERR_RUNTIME, "observer requested abort");
+      if (s.converged) break;
+    }
+  }
+  const int used = s.iter - 1;
+  eng.tail();
+  const std::vector<gwb::HostRecord> recs = eng.records(used);
+  if (o.trace) {
+    for (int k = 0; k < used; ++k) {
+      gwb_record& r = o.trace[k];
+      std::memset(&r, 0, sizeof(r));
+      r.iter = k + 1;
+      r.objective = recs[k].objective;
+      r.marginal_infeasibility = recs[k].marginal_infeasibility;
+      r.split_gap = recs[k].split_gap;
+      r.rel_change = recs[k].rel_change;
+      r.elapsed_seconds = recs[k].elapsed;
+      r.phase = 0;
+    }
+  }
+  if (o.n_records) *o.n_records = o.trace ? used : 0;
+  if (o.converged) *o.converged = s.converged;
+  if (o.iterations_used) *o.iterations_used = used;
+  eng.outputs(o.out_final, o.out_pi, o.out_w);
+}
+
+int32_t solve_impl(int32_t expected, const gwb_config* cfg, const double* dx, int64_t n,
+                   const double* dy, int64_t m, const double* mu, const double* nu,
+                   const double* initial, gwb_observer observer, void* user, double* out_final,
+                   double* out_pi, double* out_w, gwb_record* trace, int32_t trace_cap,
+                   int32_t* n_records, int32_t* converged, int32_t* iterations_used,
+                   gwb_status* st) {
+  return guarded(st, [&] {
+    if (!cfg) fail(GWB_ERR_CONFIG, "null config");
+    const int32_t algo = expected >= 0 ? expected : cfg->algorithm;
+    if (expected >= 0) {
+      static const char* names[] = {"bapg_solve", "bpg_solve", "ebpg_solve", "hbpg_solve", "fw_solve"};
+      require_algorithm(cfg, expected, names[expected]);
+    }
+    validate_config(cfg);
+    if (n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "distance matrix must be nonempty");
+    if (!dx || !dy || !mu || !nu || !out_final) fail(GWB_ERR_INVALID, "null input/output buffer");
+    if (n_records) *n_records = 0;
+    const SolveOut o{out_final, out_pi, out_w, trace, trace_cap, n_records, converged, iterations_used};
+    switch (algo) {
+      case GWB_BAPG:
+        bapg(cfg, dx, n, dy, m, mu, nu, initial, observer, user, o);
+        return;
+      case GWB_EBPG:
+      case GWB_BPG:
+      case GWB_HBPG:
+        gwb::bregman_solve(cfg, algo, dx, n, dy, m, mu, nu, initial, observer, user, out_final,
+                           trace, trace_cap, n_records, converged, iterations_used);
+        return;
+      case GWB_FW:
+        fail(GWB_ERR_UNSUPPORTED,
+             "Frank-Wolfe (transportation-simplex LMO) is outside the B200 path (DESIGN.md)");
+      default:
+        fail(GWB_ERR_CONFIG, "unknown algorithm");
+    }
+  });
+}
+
+}  // namespace
+
+// Exceptions from the standalone / Bregman modules surface as these.
+namespace gwb {
+[[noreturn]] void api_fail(int32_t code, const std::string& msg) { fail(code, msg); }
+[[noreturn]] void api_numerical(const char* solver, int iter, const std::string& detail) {
+  numerical(solver, iter, detail);
+}
+[[noreturn]] void api_zero_sum(int axis, int64_t index) {
+  ApiError e{GWB_ERR_ZERO_SUM, zero_sum_msg(axis, index)};
+  e.axis = axis;
+  e.index = index;
+  throw e;
+}
+int api_device() { return primary_device(); }
+}  // namespace gwb
+
+extern "C" {
+
+void gwb_config_default(gwb_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->algorithm = GWB_BAPG;
+  c->geometry = GWB_ENTROPY;
+  c->rho = 0.1;
+  c->step = 5.0;
+  c->epsilon_reg = 0.1;
+  c->inner_iters = 1000;
+  c->inner_tol = 1e-9;
+  c->rel_tol = 1e-6;
+  c->max_iters = 2000;
+  c->perturbation = 0.0;
+  c->switch_iters = 200;
+  c->seed = 0;
+  c->log_domain = 0;
+  c->record_residual = 0;
+  c->precision = GWB_PREC_AUTO;
+  c->quiet = 0;
+}
+
+int32_t gwb_validate_config(const gwb_config* cfg, gwb_status* st) {
+  return guarded(st, [&] { validate_config(cfg); });
+}
+
+#define GWB_SOLVE_ARGS                                                                        \
+  cfg, dx, n, dy, m, mu, nu, initial, observer, user, out_final, out_pi, out_w, trace,        \
+      trace_cap, n_records, converged, iterations_used, st
+
+int32_t gwb_solve GWB_SOLVE_SIGNATURE { return solve_impl(-1, GWB_SOLVE_ARGS); }
+int32_t gwb_bapg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_BAPG, GWB_SOLVE_ARGS); }
+int32_t gwb_bpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_BPG, GWB_SOLVE_ARGS); }
+int32_t gwb_ebpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_EBPG, GWB_SOLVE_ARGS); }
+int32_t gwb_hbpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_HBPG, GWB_SOLVE_ARGS); }
+
+int32_t gwb_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
+                         const double* pi, int64_t pi_rows, int64_t pi_cols, double* out,
+                         gwb_status* st) {
+  return guarded(st, [&] {
+    if (pi_rows != n || pi_cols != m)
+      fail(GWB_ERR_DIMENSION, "gw_objective: coupling shape mismatch");
+    *out = gwb::device_gw_objective(dx, n, dy, m, pi);
+  });
+}
+
+int32_t gwb_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
+                             double* out, gwb_status* st) {
+  return guarded(st, [&] { gwb::device_product_coupling(mu, n, nu, m, out); });
+}
+
+int32_t gwb_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m, double* out,
+                            gwb_status* st) {
+  return guarded(st, [&] { *out = gwb::device_lipschitz_bound(dx, n, dy, m); });
+}
+
+int32_t gwb_kl_scale(const double* pi, int64_t n, int64_t m, const double* target,
+                     int64_t target_len, int32_t axis, double* out, gwb_status* st) {
+  return guarded(st, [&] {
+    if (axis == GWB_ROWS && n != target_len)
+      fail(GWB_ERR_DIMENSION, "kl_scale: row count does not match target");
+    if (axis != GWB_ROWS && m != target_len)
+      fail(GWB_ERR_DIMENSION, "kl_scale: column count does not match target");
+    gwb::device_kl_scale(pi, n, m, target, axis, out);
+  });
+}
+
+int32_t gwb_sinkhorn_project(const double* kernel, int64_t n, int64_t m, const double* mu,
+                             const double* nu, double tol, int32_t max_iters, int32_t log_domain,
+                             double* out, int32_t* iterations, double* marginal_error,
+                             int32_t* converged, gwb_status* st) {
+  return guarded(st, [&] {
+    gwb::device_sinkhorn(kernel, n, m, mu, nu, tol, max_iters, log_domain, out, iterations,
+                         marginal_error, converged);
+  });
+}
+
+int32_t gwb_marginal_infeasibility(const double* pi, int64_t n, int64_t m, const double* mu,
+                                   int64_t mu_len, const double* nu, int64_t nu_len, double* out,
+                                   gwb_status* st) {
+  return guarded(st, [&] {
+    if (mu_len != n || nu_len != m)
+      fail(GWB_ERR_DIMENSION, "marginal_infeasibility: shape mismatch");
+    *out = gwb::device_marginal_infeasibility(pi, n, m, mu, nu);
+  });
+}
+
+int32_t gwb_split_gap(const double* pi, const double* w, int64_t n, int64_t m, double* out,
+                      gwb_status* st) {
+  return guarded(st, [&] { *out = gwb::device_split_gap(pi, w, n, m); });
+}
+
+int32_t gwb_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out,
+                            gwb_status* st) {
+  return guarded(st, [&] { gwb::device_hard_assignment(pi, n, m, out); });
+}
+
+int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
+                               const double* dy, int64_t m, const double* mu, const double* nu,
+                               double* out_final, double* out_pi, double* out_w,
+                               gwb_record* trace, int32_t trace_cap, int32_t* n_records,
+                               int32_t* converged, int32_t* iterations_used, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!cfg) fail(GWB_ERR_CONFIG, "null config");
+    require_algorithm(cfg, GWB_BAPG, "bapg_solve");
+    validate_config(cfg);
+    if (cfg->geometry != GWB_ENTROPY) fail(GWB_ERR_UNSUPPORTED, "quadratic geometry unsupported");
+    if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual unsupported");
+    if (batch < 1 || n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "empty batch or problem");
+    gwb::device_bapg_batched(cfg, batch, dx, n, dy, m, mu, nu, out_final, out_pi, out_w, trace,
+                             trace_cap, n_records, converged, iterations_used);
+  });
+}
+
+int32_t gwb_set_devices(int32_t count, const int32_t* ids, gwb_status* st) {
+  return guarded(st, [&] {
+    if (count < 1 || !ids) fail(GWB_ERR_CONFIG, "gwb_set_devices needs at least one id");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    g_devices.assign(ids, ids + count);
+  });
+}
+
+// ---- device-resident session ---------------------------------------------
+struct gwb_session {
+  std::unique_ptr<BapgEngine> eng;
+  gwb_config cfg;
+};
+
+int32_t gwb_session_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t device,
+                           gwb_session** out, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!cfg) fail(GWB_ERR_CONFIG, "null config");
+    require_algorithm(cfg, GWB_BAPG, "bapg_solve");
+    validate_config(cfg);
+    if (n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "distance matrix must be nonempty");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device >= count) {
+      cudaGetLastError();
+      fail(GWB_ERR_RUNTIME, "no CUDA device available");
+    }
+    auto* s = new gwb_session();
+    s->cfg = *cfg;
+    s->eng.reset(new BapgEngine(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr));
+    *out = s;
+  });
+}
+
+int32_t gwb_session_load_device(gwb_session* s, const float* dx, int64_t ldx, const float* dy,
+                                int64_t ldy, const float* mu, const float* nu, void* stream,
+                                gwb_status* st) {
+  return guarded(st, [&] {
+    (void)stream;
+    s->eng->load_device(dx, ldx, dy, ldy, mu, nu);
+  });
+}
+
+int32_t gwb_session_reset(gwb_session* s, void* stream, gwb_status* st) {
+  return guarded(st, [&] {
+    (void)stream;
+    s->eng->reset(nullptr);
+  });
+}
+
+int32_t gwb_session_iterate(gwb_session* s, int32_t iters, void* stream, int64_t* launches,
+                            gwb_status* st) {
+  return guarded(st, [&] {
+    (void)stream;
+    const bool timing = launches != nullptr && *launches < 0;
+    s->eng->set_timing(timing);
+    const int64_t l = s->eng->iterate(iters, s->cfg.rel_tol, !timing);
+    if (launches) *launches = l;
+  });
+}
+
+int32_t gwb_session_stream(gwb_session* s, void** stream, gwb_status* st) {
+  return guarded(st, [&] { *stream = static_cast<void*>(s->eng->stream()); });
+}
+
+int32_t gwb_session_info(gwb_session* s, int32_t* precision, double* gemm_flops_per_iter,
+                         gwb_status* st) {
+  return guarded(st, [&] {
+    *precision = s->eng->precision();
+    *gemm_flops_per_iter = s->eng->gemm_flops_per_iter();
+  });
+}
+
+int32_t gwb_session_pi(gwb_session* s, float** pi, int64_t* ld, gwb_status* st) {
+  return guarded(st, [&] {
+    *pi = s->eng->pi_dev();
+    *ld = s->eng->ld();
+  });
+}
+
+int32_t gwb_session_kernel_ms(gwb_session* s, int32_t kind, double* avg_ms, int64_t* count,
+                              gwb_status* st) {
+  return guarded(st, [&] { s->eng->kernel_ms(kind, avg_ms, count); });
+}
+
+int32_t gwb_session_destroy(gwb_session* s) {
+  delete s;
+  return GWB_OK;
+}
+
+int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                       int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t precision,
+                       void* stream, gwb_status* st) {
+  return guarded(st, [&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    gwb::GemmDesc d;
+    d.M = M;
+    d.N = N;
+    d.K = K;
+    d.a = a;
+    d.lda = lda;
+    d.b = b;
+    d.ldb = ldb;
+    d.c = c;
+    d.ldc = ldc;
+    float* alo = nullptr;
+    float* blo = nullptr;
+    if (precision == GWB_PREC_3XTF32) {
+      GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&alo), sizeof(float) * M * lda + 256, s));
+      GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blo), sizeof(float) * N * ldb + 256, s));
+      gwb::launch_tf32_aux(a, M, K, lda, alo, 2, s);
+      gwb::launch_tf32_aux(b, N, K, ldb, blo, 2, s);
+      d.a_lo = alo;
+      d.b_lo = blo;
+      d.three_pass = true;
+    }
+    gwb::GemmPlan* p = gwb::gemm_plan_create(d);
+    const cudaError_t e = gwb::gemm_launch(p, s);
+    gwb::gemm_plan_destroy(p);
+    if (alo) cudaFreeAsync(alo, s);
+    if (blo) cudaFreeAsync(blo, s);
+    GWB_CUDA(e);
+  });
+}
+
+const char* gwb_version(void) {
+  return "gwb 0.1 (sm_100a: tcgen05 kind::tf32 GEMM chain, CUDA " GWB_STR(__CUDACC_VER_MAJOR__) "."
+      GWB_STR(__CUDACC_VER_MINOR__) ")";
+}
+
+}  // extern "C"

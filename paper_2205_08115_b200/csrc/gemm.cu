@@ -1,0 +1,353 @@
+// gemm.cu — tcgen05 / TMEM / TMA GEMM for sm_100a, kind::tf32 with optional
+// 3xTF32 split-precision passes (see gemm.cuh).
+//
+// Structure (one CTA per 128×256 output tile, 576 threads, 1 CTA / SM):
+//   warp 0   : TMA producer — 4-stage ring of {A 128×32, B 256×32} fp32 tiles
+//              in the 128-byte-swizzled K-major layout, mbarrier full/empty
+//   warp 1   : TMEM allocator + MMA issuer — one elected lane issues
+//              tcgen05.mma.kind::tf32 (M=128, N=256, K=8) ×4 per stage into
+//              one of two 256-column TMEM accumulators (512 columns total)
+//   warps 2-17: epilogue — drain each finished K-chunk with tcgen05.ld
+//              32x32b into fp32 registers (RN adds), then scale and store
+// Tiles are rasterised in groups of kGroupM row-blocks so concurrently
+// resident CTAs share A and B panels in L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace gwb {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 32;  // 32 fp32 = 128 B = one swizzle row
+constexpr int kStages = 4;
+constexpr int kGroupM = 8;
+constexpr int kEpiWarps = 16;             // 4 lane quadrants × 4 column slices
+constexpr int kSliceCols = kBN / 4;       // 64 accumulator columns per thread
+constexpr int kThreads = 32 * (2 + kEpiWarps);
+constexpr uint32_t kABytes = kBM * kBK * 4;
+constexpr uint32_t kBBytes = kBN * kBK * 4;
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTmemCols = 2 * kBN;   // double-buffered accumulator
+constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+
+struct __align__(64) GemmParams {
+  CUtensorMap a_map[2];
+  CUtensorMap b_map[2];
+  int32_t M, N, K;
+  int32_t passes;
+  int32_t a_sel[3];
+  int32_t b_sel[3];
+  int32_t tiles_m, tiles_n;
+  int32_t chunk;  // k-blocks accumulated in TMEM before promotion to registers
+  float* c;
+  float* c_aux;
+  int64_t ldc;
+  int32_t aux_mode;
+  const float* row_scale;
+  const float* col_scale;
+  const int* skip;
+};
+
+__device__ __forceinline__ float trunc_tf32(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// The tensor core's fp32 accumulation truncates (measured: relative bias
+// ≈ −3.6e-8 per accumulated term, linear in K).  The MMA warp therefore
+// restarts accumulation every `chunk` k-blocks in one of two TMEM buffers
+// and the epilogue warps add each finished chunk into fp32 registers with
+// round-to-nearest adds ("promotion"), bounding the bias by the chunk length.
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32_kernel(const __grid_constant__ GemmParams p) {
+  if (p.skip != nullptr && *p.skip != 0) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  float* sA = reinterpret_cast<float*>(smem);
+  float* sB = reinterpret_cast<float*>(smem + kStages * kABytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;  // [2] chunk accumulated
+  uint64_t* tempty = tfull + 2;       // [2] chunk drained by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_idx();
+  const uint32_t lane = threadIdx.x & 31;
+
+  // Grouped rasterisation: consecutive blocks sweep kGroupM row tiles.
+  const int bid = blockIdx.x;
+  const int per_group = kGroupM * p.tiles_n;
+  const int group = bid / per_group;
+  const int first_m = group * kGroupM;
+  const int gsize = min(p.tiles_m - first_m, kGroupM);
+  const int in_group = bid % per_group;
+  const int tm = first_m + in_group % gsize;
+  const int tn = in_group / gsize;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&p.a_map[0]);
+    ptx::tma_prefetch(&p.b_map[0]);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], kEpiWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int kblocks = (p.K + kBK - 1) / kBK;
+  const int total = p.passes * kblocks;
+  const int chunk = p.chunk;
+  const int nchunks = (total + chunk - 1) / chunk;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      for (int it = 0; it < total; ++it) {
+        const int s = it % kStages;
+        const uint32_t ph = (it / kStages) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        const int pass = it / kblocks;
+        const int kb = it - pass * kblocks;
+        ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+        ptx::tma_load_2d(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], &full[s], kb * kBK,
+                         tm * kBM);
+        ptx::tma_load_2d(sB + s * (kBN * kBK), &p.b_map[p.b_sel[pass]], &full[s], kb * kBK,
+                         tn * kBN);
+      }
+    }
+  } else if (warp == 1) {
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_tf32(kBM, kBN);
+      for (int c = 0; c < nchunks; ++c) {
+        const int b = c & 1;
+        ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
+        const int it0 = c * chunk;
+        const int it1 = min(total, it0 + chunk);
+        for (int it = it0; it < it1; ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
+          const uint32_t b_base = ptx::smem_u32(sB + s * (kBN * kBK));
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            ptx::mma_tf32(acc, ptx::umma_desc_sw128(a_base + k * 32),
+                          ptx::umma_desc_sw128(b_base + k * 32), idesc,
+                          (it != it0 || k != 0) ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty[s]);
+        }
+        ptx::mma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    // Epilogue: warp w (2..17) owns TMEM lanes 32·(w%4).. and columns
+    // [64·slice, 64·slice + 64) of the 128×256 tile.
+    const uint32_t quad = warp & 3;
+    const uint32_t slice = (warp - 2) >> 2;
+    const uint32_t lane_base = quad * 32;
+    const uint32_t col_base = slice * kSliceCols;
+    float acc[kSliceCols];
+#pragma unroll
+    for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1;
+      ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t taddr = tmem + (lane_base << 16) + static_cast<uint32_t>(b * kBN) + col_base;
+#pragma unroll
+      for (int h = 0; h < kSliceCols / 32; ++h) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(taddr + h * 32, v);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], __uint_as_float(v[j]));
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+    }
+    const int row = tm * kBM + static_cast<int>(lane_base + lane);
+    if (row < p.M) {
+      const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
+      float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+      float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
+      const bool round_out = p.aux_mode == 1;
+      const int col0 = tn * kBN + static_cast<int>(col_base);
+#pragma unroll
+      for (int j = 0; j < kSliceCols; ++j) {
+        float x = acc[j] * rs;
+        if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
+        acc[j] = round_out ? rna_tf32(x) : x;
+      }
+      if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < kSliceCols; j += 4) {
+          *reinterpret_cast<float4*>(crow + col0 + j) =
+              make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+          if (clo)
+            *reinterpret_cast<float4*>(clo + col0 + j) = make_float4(
+                acc[j] - trunc_tf32(acc[j]), acc[j + 1] - trunc_tf32(acc[j + 1]),
+                acc[j + 2] - trunc_tf32(acc[j + 2]), acc[j + 3] - trunc_tf32(acc[j + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kSliceCols; ++j) {
+          if (col0 + j < p.N) {
+            crow[col0 + j] = acc[j];
+            if (clo) clo[col0 + j] = acc[j] - trunc_tf32(acc[j]);
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+// Row-major rows×cols fp32 matrix (leading dim ld), box = box_rows × 32 cols.
+CUtensorMap make_map(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  if ((ld * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
+    throw std::runtime_error("gemm: TMA needs 16-B aligned base and row pitch");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld ld=%lld",
+                  static_cast<int>(r), (long long)rows, (long long)cols, (long long)ld);
+    throw std::runtime_error(buf);
+  }
+  return m;
+}
+
+}  // namespace
+
+struct GemmPlan {
+  GemmParams params;
+  int grid = 0;
+  double flops = 0.0;
+};
+
+GemmPlan* gemm_plan_create(const GemmDesc& d) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
+  });
+  auto* p = new GemmPlan();
+  GemmParams& g = p->params;
+  std::memset(&g, 0, sizeof(g));
+  g.M = static_cast<int32_t>(d.M);
+  g.N = static_cast<int32_t>(d.N);
+  g.K = static_cast<int32_t>(d.K);
+  g.a_map[0] = make_map(d.a, d.M, d.K, d.lda, kBM);
+  g.b_map[0] = make_map(d.b, d.N, d.K, d.ldb, kBN);
+  g.a_map[1] = d.a_lo ? make_map(d.a_lo, d.M, d.K, d.lda, kBM) : g.a_map[0];
+  g.b_map[1] = d.b_lo ? make_map(d.b_lo, d.N, d.K, d.ldb, kBN) : g.b_map[0];
+  g.passes = 1;
+  g.a_sel[0] = 0;
+  g.b_sel[0] = 0;
+  if (d.three_pass) {
+    // A·B + A·B_lo + A_lo·B; a missing residual means that operand is exact
+    // in TF32 (e.g. 0/1 adjacency), so its pass is dropped.
+    if (d.b_lo) {
+      g.a_sel[g.passes] = 0;
+      g.b_sel[g.passes] = 1;
+      ++g.passes;
+    }
+    if (d.a_lo) {
+      g.a_sel[g.passes] = 1;
+      g.b_sel[g.passes] = 0;
+      ++g.passes;
+    }
+  }
+  g.tiles_m = static_cast<int32_t>((d.M + kBM - 1) / kBM);
+  g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
+  g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
+  g.c = d.c;
+  g.c_aux = d.c_aux;
+  g.ldc = d.ldc;
+  g.aux_mode = d.aux_mode;
+  g.row_scale = d.row_scale;
+  g.col_scale = d.col_scale;
+  g.skip = d.skip;
+  p->grid = g.tiles_m * g.tiles_n;
+  p->flops = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
+  return p;
+}
+
+void gemm_plan_destroy(GemmPlan* p) { delete p; }
+
+cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
+  gemm_tf32_kernel<<<p->grid, kThreads, kSmemBytes, s>>>(p->params);
+  return cudaGetLastError();
+}
+
+double gemm_flops(const GemmPlan* p) { return p->flops; }
+int gemm_passes(const GemmPlan* p) { return p->params.passes; }
+
+}  // namespace gwb

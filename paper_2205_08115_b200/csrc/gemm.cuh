@@ -1,0 +1,52 @@
+// gemm.cuh — host interface of the tcgen05 TF32 / 3xTF32 GEMM ("TN": both
+// operands K-major, i.e. row-major M×K and N×K with K contiguous).
+//
+//   C[M×N] = Σ_pass A_pass · B_passᵀ   (fp32 accumulate in TMEM)
+//   epilogue: C *= row_scale[i] · col_scale[j]; optionally rounds the
+//             output to TF32 (rna) or emits the residual C − trunc_tf32(C)
+//             for a following 1xTF32 / 3xTF32 GEMM.
+//
+// This is the K1 kernel of SURVEY.md §2.3: each BAPG half-step issues two of
+// these for the D_X·π·D_Y chain (reference: structure_product,
+// proj/src/solvers.cpp:16-19, where Eigen's dense GEMM does the work).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gwb {
+
+struct GemmDesc {
+  int64_t M = 0, N = 0, K = 0;
+  const float* a = nullptr;     // M×K row-major, leading dim lda
+  const float* a_lo = nullptr;  // optional residual A − trunc_tf32(A)
+  int64_t lda = 0;
+  const float* b = nullptr;     // N×K row-major, leading dim ldb
+  const float* b_lo = nullptr;
+  int64_t ldb = 0;
+  float* c = nullptr;           // M×N row-major, leading dim ldc
+  float* c_aux = nullptr;       // optional second output, see aux_mode
+  int64_t ldc = 0;
+  int aux_mode = 0;             // 0: none; 1: c holds rna_tf32(C) (for a
+                                // following 1xTF32 GEMM), c_aux unused;
+                                // 2: c holds C, c_aux = C − trunc_tf32(C)
+  const float* row_scale = nullptr;  // length M
+  const float* col_scale = nullptr;  // length N
+  const int* skip = nullptr;         // device flag: nonzero ⇒ kernel is a no-op
+  bool three_pass = false;           // 3xTF32 (drops A_lo·B_lo); needs *_lo
+  int promote_every = 2;             // k-blocks (×32) per TMEM chunk; 0 = never
+};
+
+// Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).
+struct GemmPlan;
+
+GemmPlan* gemm_plan_create(const GemmDesc& d);
+void gemm_plan_destroy(GemmPlan* p);
+cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s);
+// Algorithmic FLOPs of one launch (2·M·N·K, independent of the pass count).
+double gemm_flops(const GemmPlan* p);
+int gemm_passes(const GemmPlan* p);
+
+}  // namespace gwb

@@ -1,0 +1,581 @@
+// kernels.cu — HBM-bound BAPG half-step kernels, fused diagnostics and the
+// boundary conversions (see kernels.cuh).  All row-major buffers have a
+// leading dimension that is a multiple of 32 floats with zeroed padding, so
+// float4 accesses never leave the allocation.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace gwb {
+
+namespace {
+
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ float trunc_tf32(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Operand copy for the next GEMM: 1 → TF32 round-to-nearest-away (unbiased
+// 1xTF32 input), 2 → residual x − trunc_tf32(x) (3xTF32 low part).
+__device__ __forceinline__ float aux_of(float x, int mode) {
+  return mode == 1 ? rna_tf32(x) : x - trunc_tf32(x);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// (max, Σ v·e^{x−max}) online accumulator.
+struct MaxSum {
+  float mx;
+  float s;
+};
+
+__device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) {
+  if (e > a.mx) {
+    a.s = a.s * __expf(a.mx - e) + v;
+    a.mx = e;
+  } else {
+    a.s += v * __expf(e - a.mx);
+  }
+}
+
+__device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) {
+  if (b.mx == -INFINITY) return a;
+  if (a.mx == -INFINITY) return b;
+  const float M = fmaxf(a.mx, b.mx);
+  MaxSum r;
+  r.mx = M;
+  r.s = a.s * __expf(a.mx - M) + b.s * __expf(b.mx - M);
+  // NaN propagation: any NaN max poisons the sum.
+  if (isnan(a.mx) || isnan(b.mx)) {
+    r.mx = NAN;
+    r.s = NAN;
+  }
+  return r;
+}
+
+__device__ __forceinline__ MaxSum warp_merge(MaxSum a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MaxSum b;
+    b.mx = __shfl_xor_sync(0xffffffffu, a.mx, o);
+    b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
+    a = ms_merge(a, b);
+  }
+  return a;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide (max,sum) merge + up to 5 fp64 sums; result broadcast to all.
+template <int kThreads, int kSums>
+__device__ void block_reduce(MaxSum& ms, double (&sums)[kSums]) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ float s_mx[kWarps], s_s[kWarps];
+  __shared__ double s_d[kSums][kWarps];
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  ms = warp_merge(ms);
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = warp_sum(sums[k]);
+  if (l == 0) {
+    s_mx[w] = ms.mx;
+    s_s[w] = ms.s;
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) s_d[k][w] = sums[k];
+  }
+  __syncthreads();
+  MaxSum r{-INFINITY, 0.f};
+  double t[kSums];
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) t[k] = 0.0;
+  for (int q = 0; q < kWarps; ++q) {  // fixed order ⇒ deterministic
+    r = ms_merge(r, MaxSum{s_mx[q], s_s[q]});
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) t[k] += s_d[k][q];
+  }
+  ms = r;
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = t[k];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Half-step a: one CTA per row.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int write, int tail) {
+  if (tail ? d.st->flags != 0 : d.st->done != 0) return;
+  const int64_t i = blockIdx.x;
+  const float* g = d.G + i * d.ld;
+  const float* w = d.W + i * d.ld;
+  const int64_t m = d.m;
+  const float inv_rho = d.inv_rho;
+
+  MaxSum ms{-INFINITY, 0.f};
+  double sums[2] = {0.0, 0.0};  // ⟨G,W⟩, ΣW
+  for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
+    const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+    const float4 w4 = *reinterpret_cast<const float4*>(w + j);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < m) {
+        ms_add(ms, gv[q] * inv_rho, wv[q]);
+        sums[0] += static_cast<double>(gv[q]) * wv[q];
+        sums[1] += wv[q];
+      }
+    }
+  }
+  block_reduce<kRowThreads, 2>(ms, sums);
+
+  if (threadIdx.x == 0) {
+    d.row_part[i].gw = sums[0];
+    const double dev = sums[1] - d.mu64[i];
+    d.row_part[i].rowdev = dev * dev;
+  }
+  if (!write) return;
+  const float S = ms.s;
+  const float r = ms.mx;
+  if (threadIdx.x == 0) {
+    if (r > 700.0f) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (!(S > 0.0f) || !isfinite(S) || isnan(r)) {
+      atomicOr(&d.st->flags, kFlagZeroA);
+      atomicMin(&d.st->zero_index, static_cast<int>(i));
+    }
+  }
+  const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
+  float* p = d.P + i * d.ld;
+  float* plo = d.P_aux ? d.P_aux + i * d.ld : nullptr;
+  const int am = d.aux_mode;
+  for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
+    const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+    const float4 w4 = *reinterpret_cast<const float4*>(w + j);
+    float4 o;
+    o.x = (j + 0 < m) ? scale * w4.x * __expf(g4.x * inv_rho - r) : 0.f;
+    o.y = (j + 1 < m) ? scale * w4.y * __expf(g4.y * inv_rho - r) : 0.f;
+    o.z = (j + 2 < m) ? scale * w4.z * __expf(g4.z * inv_rho - r) : 0.f;
+    o.w = (j + 3 < m) ? scale * w4.w * __expf(g4.w * inv_rho - r) : 0.f;
+    *reinterpret_cast<float4*>(p + j) = o;
+    if (plo)
+      *reinterpret_cast<float4*>(plo + j) =
+          make_float4(aux_of(o.x, am), aux_of(o.y, am), aux_of(o.z, am), aux_of(o.w, am));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Half-step b, pass 1: per (row chunk, 128-column block) partials.
+// ---------------------------------------------------------------------------
+constexpr int kColThreads = 256;
+constexpr int kColWidth = 128;  // columns per CTA (32 lanes × float4)
+
+__global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int rows_per_chunk) {
+  if (d.st->done) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
+  const float inv_rho = d.inv_rho;
+  MaxSum ms[4] = {{-INFINITY, 0.f}, {-INFINITY, 0.f}, {-INFINITY, 0.f}, {-INFINITY, 0.f}};
+  double ps[4] = {0.0, 0.0, 0.0, 0.0};
+  if (c0 < d.m) {
+    for (int64_t i = r0 + warp; i < r1; i += kColThreads / 32) {
+      const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
+      const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + c0);
+      ms_add(ms[0], g4.x * inv_rho, p4.x);
+      ms_add(ms[1], g4.y * inv_rho, p4.y);
+      ms_add(ms[2], g4.z * inv_rho, p4.z);
+      ms_add(ms[3], g4.w * inv_rho, p4.w);
+      ps[0] += p4.x;
+      ps[1] += p4.y;
+      ps[2] += p4.z;
+      ps[3] += p4.w;
+    }
+  }
+  __shared__ float s_mx[kColThreads / 32][kColWidth];
+  __shared__ float s_s[kColThreads / 32][kColWidth];
+  __shared__ double s_p[kColThreads / 32][kColWidth];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    s_mx[warp][lane * 4 + q] = ms[q].mx;
+    s_s[warp][lane * 4 + q] = ms[q].s;
+    s_p[warp][lane * 4 + q] = ps[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < kColWidth) {
+    const int c = threadIdx.x;
+    const int64_t col = static_cast<int64_t>(blockIdx.x) * kColWidth + c;
+    if (col < d.m) {
+      MaxSum r{-INFINITY, 0.f};
+      double p = 0.0;
+      for (int q = 0; q < kColThreads / 32; ++q) {
+        r = ms_merge(r, MaxSum{s_mx[q][c], s_s[q][c]});
+        p += s_p[q][c];
+      }
+      const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + col;
+      d.col_pmax[o] = r.mx;
+      d.col_psum[o] = r.s;
+      d.col_psump[o] = p;
+    }
+  }
+}
+
+// Half-step b, pass 2: merge chunk partials per column, raise errors.
+__global__ void col_combine_kernel(BapgDev d) {
+  if (d.st->done) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= d.m) return;
+  MaxSum r{-INFINITY, 0.f};
+  double p = 0.0;
+  for (int c = 0; c < d.chunks; ++c) {
+    const int64_t o = static_cast<int64_t>(c) * d.m + j;
+    r = ms_merge(r, MaxSum{d.col_pmax[o], d.col_psum[o]});
+    p += d.col_psump[o];
+  }
+  if (r.mx > 700.0f) atomicOr(&d.st->flags, kFlagOverflowB);
+  if (!(r.s > 0.0f) || !isfinite(r.s) || isnan(r.mx)) {
+    atomicOr(&d.st->flags, kFlagZeroB);
+    atomicMin(&d.st->zero_index, static_cast<int>(j));
+  }
+  d.col_max[j] = r.mx;
+  d.col_scale[j] = static_cast<float>(d.nu64[j] / static_cast<double>(r.s));
+  const double dev = p - d.nu64[j];
+  d.col_dev[j] = dev * dev;
+}
+
+// Half-step b, pass 3: write W_new, fused diagnostics. One CTA per row.
+__global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
+  if (d.st->done) return;
+  if (d.st->flags != 0) return;
+  const int64_t i = blockIdx.x;
+  const float* g = d.G + i * d.ld;
+  const float* p = d.P + i * d.ld;
+  const float* wo = d.W + i * d.ld;
+  float* wn = d.W_new + i * d.ld;
+  float* wlo = d.W_aux ? d.W_aux + i * d.ld : nullptr;
+  const int am = d.aux_mode;
+  const float inv_rho = d.inv_rho;
+  const int64_t m = d.m;
+  double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
+  bool finite = true;
+  for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
+    const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+    const float4 p4 = *reinterpret_cast<const float4*>(p + j);
+    const float4 w4 = *reinterpret_cast<const float4*>(wo + j);
+    const float4 cm = *reinterpret_cast<const float4*>(d.col_max + j);
+    const float4 cs = *reinterpret_cast<const float4*>(d.col_scale + j);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+    const float mv[4] = {cm.x, cm.y, cm.z, cm.w};
+    const float sv[4] = {cs.x, cs.y, cs.z, cs.w};
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < m) {
+        o[q] = sv[q] * pv[q] * __expf(gv[q] * inv_rho - mv[q]);
+        finite = finite && isfinite(o[q]);
+        sums[0] += static_cast<double>(gv[q]) * o[q];
+        const double sp = static_cast<double>(pv[q]) - o[q];
+        sums[1] += sp * sp;
+        const double df = static_cast<double>(o[q]) - wv[q];
+        sums[2] += df * df;
+        sums[3] += static_cast<double>(wv[q]) * wv[q];
+        sums[4] += static_cast<double>(gv[q]) * pv[q];
+      } else {
+        o[q] = 0.f;
+      }
+    }
+    *reinterpret_cast<float4*>(wn + j) = make_float4(o[0], o[1], o[2], o[3]);
+    if (wlo)
+      *reinterpret_cast<float4*>(wlo + j) =
+          make_float4(aux_of(o[0], am), aux_of(o[1], am), aux_of(o[2], am), aux_of(o[3], am));
+  }
+  MaxSum dummy{-INFINITY, 0.f};
+  block_reduce<kRowThreads, 5>(dummy, sums);
+  if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
+    atomicOr(&d.st->flags, kFlagNonFinite);
+  if (threadIdx.x == 0) {
+    ColWritePart& c = d.cw_part[i];
+    c.gw = sums[0];
+    c.split = sums[1];
+    c.diff = sums[2];
+    c.wold = sums[3];
+    c.gp = sums[4];
+  }
+}
+
+// Flags raised by a kernel: mark the solve finished at the current iteration.
+__global__ void flag_check_kernel(DevStatus* st) {
+  if (st->done) return;
+  if (st->flags != 0) {
+    st->done = 1;
+    st->err_iter = st->iter;
+  }
+}
+
+constexpr int kFinThreads = 512;
+
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(BapgDev d, double rel_tol, int tail) {
+  DevStatus* st = d.st;
+  if (tail ? st->flags != 0 : st->done != 0) return;
+  const int k = tail ? st->iter - 1 : st->iter;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // acc: 0 gw_row, 1 rowdev, 2 cw.gw, 3 split, 4 diff, 5 wold, 6 gp, 7 coldev
+  for (int64_t i = threadIdx.x; i < d.n; i += kFinThreads) {
+    acc[0] += d.row_part[i].gw;
+    acc[1] += d.row_part[i].rowdev;
+    if (!tail) {
+      const ColWritePart c = d.cw_part[i];
+      acc[2] += c.gw;
+      acc[3] += c.split;
+      acc[4] += c.diff;
+      acc[5] += c.wold;
+      acc[6] += c.gp;
+    }
+  }
+  if (!tail)
+    for (int64_t j = threadIdx.x; j < d.m; j += kFinThreads) acc[7] += d.col_dev[j];
+  __shared__ double s[8][kFinThreads / 32];
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double v = warp_sum(acc[q]);
+    if (l == 0) s[q][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double t[8];
+  for (int q = 0; q < 8; ++q) {
+    t[q] = 0.0;
+    for (int r = 0; r < kFinThreads / 32; ++r) t[q] += s[q][r];
+  }
+  if (tail) {
+    d.rec[k].mw_w = t[0];
+    d.rec[k].row_sq = t[1];
+    return;
+  }
+  if (k >= 2) {  // the row pass of iteration k saw w^{k-1}
+    d.rec[k - 1].mw_w = t[0];
+    d.rec[k - 1].row_sq = t[1];
+  }
+  DevRecord& r = d.rec[k];
+  r.mpi_w = t[2];
+  r.split_sq = t[3];
+  r.diff_sq = t[4];
+  r.wold_sq = t[5];
+  r.mpi_pi = t[6];
+  r.col_sq = t[7];
+  r.elapsed = 1e-9 * static_cast<double>(globaltimer() - st->t0);
+  const double rel = sqrt(t[4]) / sqrt(t[5]);
+  st->iter = k + 1;
+  if (rel <= rel_tol) {
+    st->converged = 1;
+    st->done = 1;
+  }
+}
+
+__global__ void status_reset_kernel(DevStatus* st) {
+  st->done = 0;
+  st->flags = 0;
+  st->iter = 1;
+  st->err_iter = 0;
+  st->converged = 0;
+  st->zero_index = 0x7fffffff;
+  st->sink_sweeps = 0;
+  st->sink_err_sweep = 0;
+  st->t0 = globaltimer();
+}
+
+// ---------------------------------------------------------------------------
+// Conversions.
+// ---------------------------------------------------------------------------
+__global__ void c64_to_r32_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
+                                  float* __restrict__ dst, int64_t ld) {
+  __shared__ float tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;  // row block
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * 32;  // col block
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, j = j0 + y;
+    if (i < rows && j < cols) tile[y][threadIdx.x] = static_cast<float>(src[j * rows + i]);
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t i = i0 + y, j = j0 + threadIdx.x;
+    if (i < rows && j < cols) dst[i * ld + j] = tile[threadIdx.x][y];
+  }
+}
+
+__global__ void row_sums64_kernel(const float* src, int64_t rows, int64_t cols, int64_t ld,
+                                  double* out) {
+  const int64_t i = blockIdx.x;
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) s += src[i * ld + j];
+  s = warp_sum(s);
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t += sh[q];
+    out[i] = t;
+  }
+}
+
+__global__ void col_sums64_kernel(const float* src, int64_t rows, int64_t cols, int64_t ld,
+                                  double* out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < rows; ++i) s += src[i * ld + j];
+  out[j] = s;
+}
+
+__global__ void r32_to_c64_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                  int64_t ld, double* __restrict__ dst, int axis,
+                                  const double* __restrict__ target,
+                                  const double* __restrict__ sums) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t i = i0 + y, j = j0 + threadIdx.x;
+    if (i < rows && j < cols) {
+      double v = static_cast<double>(src[i * ld + j]);
+      if (axis == 0) v *= target[i] / sums[i];
+      if (axis == 1) v *= target[j] / sums[j];
+      tile[y][threadIdx.x] = v;
+    }
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t j = j0 + y, i = i0 + threadIdx.x;
+    if (i < rows && j < cols) dst[j * rows + i] = tile[threadIdx.x][y];
+  }
+}
+
+__global__ void average64_kernel(const double* a, const double* b, double* dst, int64_t len) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = 0.5 * (a[k] + b[k]);
+}
+
+__global__ void tf32_aux_kernel(const float* x, int64_t rows, int64_t cols, int64_t ld,
+                                float* out, int mode) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) out[i * ld + j] = aux_of(x[i * ld + j], mode);
+}
+
+__global__ void product_coupling_kernel(const float* mu, const float* nu, int64_t n, int64_t m,
+                                        int64_t ld, float* P) {
+  const int64_t i = blockIdx.x;
+  const float a = mu[i];
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) P[i * ld + j] = a * nu[j];
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
+  // valid for v >= 0 (structure matrices are nonnegative)
+  atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+}
+
+__global__ void analyze_kernel(const float* D, int64_t rows, int64_t cols, int64_t ld,
+                               float* out_max, int* out_inexact) {
+  const int64_t i = blockIdx.x;
+  float mx = 0.f;
+  int inexact = 0;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    const float v = D[i * ld + j];
+    mx = fmaxf(mx, v);
+    inexact |= (v != trunc_tf32(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    inexact |= __shfl_xor_sync(0xffffffffu, inexact, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(out_max, mx);
+    if (inexact) atomicOr(out_inexact, 1);
+  }
+}
+
+inline unsigned grid1d(int64_t work, int threads) {
+  return static_cast<unsigned>((work + threads - 1) / threads);
+}
+
+}  // namespace
+
+void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
+  row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
+                                                                       write ? 0 : 1);
+  if (write) flag_check_kernel<<<1, 1, 0, s>>>(d.st);
+}
+
+void launch_col_update(const BapgDev& d, cudaStream_t s) {
+  const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
+  dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
+            static_cast<unsigned>(d.chunks));
+  col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
+  col_combine_kernel<<<grid1d(d.m, 256), 256, 0, s>>>(d);
+  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
+  col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
+}
+
+void launch_finalize(const BapgDev& d, double rel_tol, bool tail, cudaStream_t s) {
+  finalize_kernel<<<1, kFinThreads, 0, s>>>(d, rel_tol, tail ? 1 : 0);
+}
+
+void launch_status_reset(DevStatus* st, cudaStream_t s) { status_reset_kernel<<<1, 1, 0, s>>>(st); }
+
+void launch_colmajor64_to_rowmajor32(const double* src, int64_t rows, int64_t cols, float* dst,
+                                     int64_t ld, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  c64_to_r32_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, dst, ld);
+}
+
+void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t cols, int64_t ld,
+                                     double* dst, int axis, const double* target, double* work,
+                                     cudaStream_t s) {
+  if (axis == 0) row_sums64_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(src, rows, cols, ld, work);
+  if (axis == 1) col_sums64_kernel<<<grid1d(cols, 256), 256, 0, s>>>(src, rows, cols, ld, work);
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  r32_to_c64_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld, dst, axis, target, work);
+}
+
+void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s) {
+  average64_kernel<<<1184, 256, 0, s>>>(a, b, dst, len);
+}
+
+void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
+                     cudaStream_t s) {
+  tf32_aux_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld, out, mode);
+}
+
+void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
+                    int* out_inexact, cudaStream_t s) {
+  analyze_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(D, rows, cols, ld, out_max, out_inexact);
+}
+
+void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,
+                             float* P, cudaStream_t s) {
+  product_coupling_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(mu, nu, n, m, ld, P);
+}
+
+}  // namespace gwb

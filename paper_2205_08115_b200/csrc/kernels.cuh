@@ -1,0 +1,133 @@
+// kernels.cuh — HBM-bound kernels around the GEMM chain: the BAPG row/column
+// KL projections (kl_scale of the multiplicative update, projections.cpp:12-34
+// as used by solvers.cpp:164-177), the per-iteration diagnostics fused into
+// those passes, the Sinkhorn sweeps for eBPG/BPG, and layout conversions at
+// the C-ABI boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gwb {
+
+// Error bits raised by device kernels (decoded on the host in reference
+// precedence order, solvers.cpp:164-189).
+enum DevFlag : int {
+  kFlagOverflowA = 1,   // max(D_X w D_Y / rho) > 700 in half-step a
+  kFlagZeroA = 2,       // a row of w ⊙ exp(E) has nonpositive / non-finite sum
+  kFlagOverflowB = 4,   // same checks in half-step b
+  kFlagZeroB = 8,
+  kFlagNonFinite = 16,  // non-finite iterate
+  kFlagDeadLine = 32,   // eBPG: kernel row/column underflowed to zero
+  kFlagOverflowK = 64,  // BPG: max(2t·M(π)) > 700
+  kFlagSinkNonFinite = 128,
+};
+
+// Device-resident solver status; every kernel returns immediately when
+// `done` is set, so a converged or failed solve turns the remainder of an
+// already-enqueued CUDA graph into no-ops.
+struct DevStatus {
+  int done;        // read by every kernel's prologue
+  int flags;       // DevFlag bits
+  int iter;        // current 1-based outer iteration
+  int err_iter;    // iteration at which flags were first raised
+  int converged;
+  int zero_index;  // lowest offending line (atomicMin)
+  int sink_sweeps; // last Sinkhorn sweep count
+  int sink_err_sweep;
+  unsigned long long t0;  // %globaltimer at reset
+};
+
+// Per-iteration trace record kept on the device (fp64).
+struct DevRecord {
+  double mpi_pi;     // ⟨M(π), π⟩
+  double mpi_w;      // ⟨M(π), w⟩
+  double mw_w;       // ⟨M(w), w⟩   (filled one half-step later)
+  double col_sq;     // Σ_j (colsum(π)_j − ν_j)²
+  double row_sq;     // Σ_i (rowsum(w)_i − μ_i)²  (filled one half-step later)
+  double split_sq;   // ‖π − w‖²
+  double diff_sq;    // ‖w' − w‖²
+  double wold_sq;    // ‖w‖²
+  double elapsed;    // seconds since reset
+};
+
+struct RowPart {     // per-row fp64 partials of the half-step-a pass
+  double gw;         // ⟨G_i, W_i⟩
+  double rowdev;     // (Σ_j W_ij − μ_i)²
+};
+
+struct ColWritePart {  // per-row fp64 partials of the half-step-b write pass
+  double gw;         // ⟨G_i, W'_i⟩
+  double split;      // ‖P_i − W'_i‖²
+  double diff;       // ‖W'_i − W_i‖²
+  double wold;       // ‖W_i‖²
+  double gp;         // ⟨G_i, P_i⟩
+};
+
+struct BapgDev {
+  int64_t n, m, ld;         // P/W/G are n×m row-major, leading dim ld
+  float inv_rho;
+  const float* G;
+  const float* mu;          // fp32 marginals
+  const float* nu;
+  const double* mu64;
+  const double* nu64;
+  float* P;
+  float* P_aux;             // GEMM copy of P, see aux_mode (nullable)
+  float* W;                 // current w (read in both half-steps)
+  float* W_new;             // next w (written by half-step b)
+  float* W_aux;             // GEMM copy of W_new, see aux_mode (nullable)
+  int aux_mode;             // 1: aux = rna_tf32(x) (1xTF32 operand)
+                            // 2: aux = x − trunc_tf32(x) (3xTF32 residual)
+  RowPart* row_part;        // n
+  ColWritePart* cw_part;    // n
+  float* col_pmax;          // chunks × m
+  float* col_psum;          // chunks × m
+  double* col_psump;        // chunks × m : Σ_i P_ij partials
+  float* col_max;           // m
+  float* col_scale;         // m
+  double* col_dev;          // m : (colsum(P)_j − ν_j)²
+  int chunks;
+  DevStatus* st;
+  DevRecord* rec;           // [max_iters + 1]
+};
+
+// Half-step a (solvers.cpp:164-170): E = G/ρ, P = diag(μ/rowsum)·(W ⊙ e^E),
+// with per-row max shift; also ⟨G,W⟩ and rowsum(W) diagnostics for the
+// previous iteration's record.  `write` = false computes diagnostics only.
+void launch_row_update(const BapgDev& d, bool write, cudaStream_t s);
+// Half-step b (solvers.cpp:171-177): column (max, Σ P e^{E−max}) partials,
+// combine + checks, then W_new = P ⊙ e^E · diag(ν/colsum) with fused
+// split-gap / rel-change / objective partials.
+void launch_col_update(const BapgDev& d, cudaStream_t s);
+// Reduces the per-line partials in fixed order into rec[iter] / rec[iter-1],
+// evaluates the stop rule (solvers.cpp:191,208) and advances st->iter.
+void launch_finalize(const BapgDev& d, double rel_tol, bool tail, cudaStream_t s);
+void launch_status_reset(DevStatus* st, cudaStream_t s);
+
+// Layout conversions at the boundary.
+// dst (rows×cols row-major fp32, ld) = src (rows×cols column-major fp64)
+void launch_colmajor64_to_rowmajor32(const double* src, int64_t rows, int64_t cols, float* dst,
+                                     int64_t ld, cudaStream_t s);
+// dst (column-major fp64) = src (row-major fp32) with optional fp64 exact
+// re-projection of rows (axis 0, target mu) or columns (axis 1, target nu):
+// the K8 fix-up that restores the fp64 marginal invariants of the reference
+// (types.cpp:120-152).  axis = -1: plain widening.
+void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t cols, int64_t ld,
+                                     double* dst, int axis, const double* target, double* work,
+                                     cudaStream_t s);
+// dst = 0.5 (a + b), column-major fp64 of len elements.
+void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s);
+// out = aux_of(x, mode) (1: rna_tf32(x), 2: x − trunc_tf32(x)), row-major.
+void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
+                     cudaStream_t s);
+// Scans a structure matrix: *out_max = max entry, *out_inexact = 1 if any
+// entry is not exactly representable in TF32 (0/1 adjacency is exact).
+void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
+                    int* out_inexact, cudaStream_t s);
+// P = μ νᵀ (product coupling, types.cpp:204-207) in row-major fp32.
+void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,
+                             float* P, cudaStream_t s);
+
+}  // namespace gwb

@@ -1,0 +1,535 @@
+// solver.cu — BAPG device engine (see solver.cuh).
+//
+// One iteration (reference solvers.cpp:159-212) is 12 launches:
+//   half a: GEMM1 Vᵀ = D_Y·Wᵀ, GEMM2 G = D_X·V, row_update (+flag check)
+//   half b: GEMM1 Vᵀ = D_Y·Pᵀ, GEMM2 G = D_X·V, col partial/combine/write
+//           (+2 flag checks), finalize (trace record + stop rule)
+// Every kernel returns immediately once DevStatus::done is set, so chunks of
+// iterations are captured once as CUDA graphs and replayed without host
+// synchronisation; the host polls `done` two chunks behind.
+#include "solver.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+namespace gwb {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s at %s", cudaGetErrorString(e), what);
+    throw CudaError(buf);
+  }
+}
+
+namespace {
+
+constexpr int kChunkIters = 16;  // iterations per captured graph (even)
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  GWB_CUDA(cudaMalloc(&p, count * sizeof(T) + 256));
+  GWB_CUDA(cudaMemset(p, 0, count * sizeof(T) + 256));
+  return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+}  // namespace
+
+int resolve_precision(int requested, bool d_exact, double dmax_x, double dmax_y, double rho) {
+  if (requested == GWB_PREC_TF32 || requested == GWB_PREC_3XTF32) return requested;
+  // AUTO: 3xTF32.  Measured on B200: 1xTF32 with rna-rounded
+  // operands keeps π within 1e-4 on graph problems but misses the 1e-5 GW
+  // objective bound (4.7e-5 .. 1.1e-4), so it stays an explicit opt-in.
+  (void)d_exact;
+  (void)dmax_x;
+  (void)dmax_y;
+  (void)rho;
+  return GWB_PREC_3XTF32;
+}
+
+BapgEngine::BapgEngine(int device, int64_t n, int64_t m, double rho, int precision,
+                       int max_iters, cudaStream_t stream)
+    : device_(device),
+      n_(n),
+      m_(m),
+      ldn_(round_up(n, 32)),
+      ldm_(round_up(m, 32)),
+      rho_(rho),
+      precision_(precision),
+      max_iters_(max_iters),
+      stream_(stream) {
+  GWB_CUDA(cudaSetDevice(device_));
+  if (!stream_) {
+    GWB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    own_stream_ = true;
+  }
+  alloc();
+}
+
+BapgEngine::~BapgEngine() {
+  cudaSetDevice(device_);
+  cudaStreamSynchronize(stream_);
+  destroy_graphs();
+  for (int q = 0; q < 2; ++q) {
+    gemm_plan_destroy(g1_[q][0]);
+    if (q == 0) gemm_plan_destroy(g1_[q][1]);
+    gemm_plan_destroy(g1_tail_[q]);
+  }
+  gemm_plan_destroy(g2_);
+  gemm_plan_destroy(g2_tail_);
+  for (void* p : std::initializer_list<void*>{
+           Dx_, Dx_aux_, Dy_, Dy_aux_, P_, P_aux_, W_[0], W_[1], W_aux_[0], W_aux_[1], Vt_,
+           Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
+           col_max_, col_scale_, col_psump_, col_dev_, st_, rec_})
+    dfree(p);
+  if (h_done_) cudaFreeHost(h_done_);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto& mk : ev_marks_) {
+    cudaEventDestroy(mk.second.first);
+    cudaEventDestroy(mk.second.second);
+  }
+  if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+void BapgEngine::alloc() {
+  const size_t nm = static_cast<size_t>(n_) * ldm_;
+  Dx_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
+  Dy_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
+  P_ = dalloc<float>(nm);
+  P_aux_ = dalloc<float>(nm);
+  for (int q = 0; q < 2; ++q) {
+    W_[q] = dalloc<float>(nm);
+    W_aux_[q] = dalloc<float>(nm);
+  }
+  Vt_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+  if (precision_ == GWB_PREC_3XTF32) Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+  G_ = dalloc<float>(nm);
+  mu32_ = dalloc<float>(ldn_);
+  nu32_ = dalloc<float>(ldm_);
+  mu64_ = dalloc<double>(ldn_);
+  nu64_ = dalloc<double>(ldm_);
+  row_part_ = dalloc<RowPart>(n_);
+  cw_part_ = dalloc<ColWritePart>(n_);
+  // Column-pass chunking: enough CTAs to fill the chip (≥ 2 waves of 148).
+  const int64_t col_blocks = (m_ + 127) / 128;
+  chunks_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n_ + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks)));
+  col_pmax_ = dalloc<float>(static_cast<size_t>(chunks_) * m_);
+  col_psum_ = dalloc<float>(static_cast<size_t>(chunks_) * m_);
+  col_psump_ = dalloc<double>(static_cast<size_t>(chunks_) * m_);
+  col_max_ = dalloc<float>(ldm_);
+  col_scale_ = dalloc<float>(ldm_);
+  col_dev_ = dalloc<double>(ldm_);
+  st_ = dalloc<DevStatus>(1);
+  rec_ = dalloc<DevRecord>(static_cast<size_t>(max_iters_) + 2);
+  GWB_CUDA(cudaMallocHost(&h_done_, 4 * sizeof(int)));
+}
+
+BapgDev BapgEngine::dev_view(int q) const {
+  BapgDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.n = n_;
+  d.m = m_;
+  d.ld = ldm_;
+  d.inv_rho = static_cast<float>(1.0 / rho_);
+  d.G = G_;
+  d.mu = mu32_;
+  d.nu = nu32_;
+  d.mu64 = mu64_;
+  d.nu64 = nu64_;
+  d.P = P_;
+  d.P_aux = P_aux_;
+  d.W = W_[q];
+  d.W_new = W_[1 - q];
+  d.W_aux = W_aux_[1 - q];
+  d.aux_mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
+  d.row_part = row_part_;
+  d.cw_part = cw_part_;
+  d.col_pmax = col_pmax_;
+  d.col_psum = col_psum_;
+  d.col_psump = col_psump_;
+  d.col_max = col_max_;
+  d.col_scale = col_scale_;
+  d.col_dev = col_dev_;
+  d.chunks = chunks_;
+  d.st = st_;
+  d.rec = rec_;
+  return d;
+}
+
+void BapgEngine::prepare_d() {
+  // Exactness / max of each structure matrix decides the operand copies.
+  float* d_max = dalloc<float>(2);
+  int* d_inexact = dalloc<int>(2);
+  launch_analyze(Dx_, n_, n_, ldn_, d_max, d_inexact, stream_);
+  launch_analyze(Dy_, m_, m_, ldm_, d_max + 1, d_inexact + 1, stream_);
+  float h_max[2];
+  int h_inexact[2];
+  GWB_CUDA(cudaMemcpyAsync(h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaMemcpyAsync(h_inexact, d_inexact, sizeof(h_inexact), cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  dfree(d_max);
+  dfree(d_inexact);
+  dx_exact_ = h_inexact[0] == 0;
+  dy_exact_ = h_inexact[1] == 0;
+  if (precision_ == GWB_PREC_AUTO)
+    precision_ = resolve_precision(GWB_PREC_AUTO, dx_exact_ && dy_exact_, h_max[0], h_max[1], rho_);
+  if (precision_ == GWB_PREC_3XTF32 && !Vt_aux_)
+    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+  const int mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
+  if (!dx_exact_) {
+    if (!Dx_aux_) Dx_aux_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
+    launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_aux_, mode, stream_);
+  }
+  if (!dy_exact_) {
+    if (!Dy_aux_) Dy_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
+    launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_aux_, mode, stream_);
+  }
+  build_plans();
+}
+
+void BapgEngine::build_plans() {
+  destroy_graphs();
+  for (int q = 0; q < 2; ++q) {
+    gemm_plan_destroy(g1_[q][0]);
+    if (q == 0) gemm_plan_destroy(g1_[q][1]);
+    g1_[q][1] = nullptr;
+    gemm_plan_destroy(g1_tail_[q]);
+  }
+  gemm_plan_destroy(g2_);
+  gemm_plan_destroy(g2_tail_);
+
+  const bool tf32 = precision_ == GWB_PREC_TF32;
+  // A operands (structure matrices).
+  const float* ax = Dx_;
+  const float* ax_lo = nullptr;
+  const float* ay = Dy_;
+  const float* ay_lo = nullptr;
+  if (!dx_exact_) {
+    if (tf32) ax = Dx_aux_;
+    else ax_lo = Dx_aux_;
+  }
+  if (!dy_exact_) {
+    if (tf32) ay = Dy_aux_;
+    else ay_lo = Dy_aux_;
+  }
+  auto gemm1 = [&](float* X, float* X_aux, const int* skip) {
+    GemmDesc d;
+    d.M = m_;
+    d.N = n_;
+    d.K = m_;
+    d.a = ay;
+    d.a_lo = ay_lo;
+    d.lda = ldm_;
+    d.b = tf32 ? X_aux : X;
+    d.b_lo = tf32 ? nullptr : X_aux;
+    d.ldb = ldm_;
+    d.c = Vt_;
+    d.c_aux = Vt_aux_;
+    d.ldc = ldn_;
+    d.aux_mode = tf32 ? 1 : 2;
+    d.skip = skip;
+    d.three_pass = !tf32;
+    return gemm_plan_create(d);
+  };
+  auto gemm2 = [&](const int* skip) {
+    GemmDesc d;
+    d.M = n_;
+    d.N = m_;
+    d.K = n_;
+    d.a = ax;
+    d.a_lo = ax_lo;
+    d.lda = ldn_;
+    d.b = Vt_;
+    d.b_lo = tf32 ? nullptr : Vt_aux_;
+    d.ldb = ldn_;
+    d.c = G_;
+    d.ldc = ldm_;
+    d.aux_mode = 0;
+    d.skip = skip;
+    d.three_pass = !tf32;
+    return gemm_plan_create(d);
+  };
+  const int* done = &st_->done;
+  const int* flags = &st_->flags;
+  for (int q = 0; q < 2; ++q) {
+    g1_[q][0] = gemm1(W_[q], W_aux_[q], done);
+    g1_tail_[q] = gemm1(W_[q], W_aux_[q], flags);
+  }
+  g1_[0][1] = gemm1(P_, P_aux_, done);
+  g1_[1][1] = g1_[0][1];
+  g2_ = gemm2(done);
+  g2_tail_ = gemm2(flags);
+}
+
+void BapgEngine::load_host(const double* dx, const double* dy, const double* mu,
+                           const double* nu) {
+  GWB_CUDA(cudaSetDevice(device_));
+  const int64_t big = std::max(n_ * n_, m_ * m_);
+  double* stage = nullptr;
+  GWB_CUDA(cudaMalloc(&stage, static_cast<size_t>(big) * sizeof(double)));
+  GWB_CUDA(cudaMemcpyAsync(stage, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, stream_));
+  launch_colmajor64_to_rowmajor32(stage, n_, n_, Dx_, ldn_, stream_);
+  GWB_CUDA(cudaMemcpyAsync(stage, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, stream_));
+  launch_colmajor64_to_rowmajor32(stage, m_, m_, Dy_, ldm_, stream_);
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  GWB_CUDA(cudaFree(stage));
+  std::vector<float> mu32(n_), nu32(m_);
+  for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
+  for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
+  GWB_CUDA(cudaMemcpyAsync(mu64_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(nu64_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(mu32_, mu32.data(), sizeof(float) * n_, cudaMemcpyHostToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(nu32_, nu32.data(), sizeof(float) * m_, cudaMemcpyHostToDevice, stream_));
+  prepare_d();
+}
+
+void BapgEngine::load_device(const float* dx, int64_t ldx, const float* dy, int64_t ldy,
+                             const float* mu, const float* nu) {
+  GWB_CUDA(cudaSetDevice(device_));
+  GWB_CUDA(cudaMemcpy2DAsync(Dx_, ldn_ * 4, dx, ldx * 4, n_ * 4, n_, cudaMemcpyDeviceToDevice, stream_));
+  GWB_CUDA(cudaMemcpy2DAsync(Dy_, ldm_ * 4, dy, ldy * 4, m_ * 4, m_, cudaMemcpyDeviceToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(mu32_, mu, sizeof(float) * n_, cudaMemcpyDeviceToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(nu32_, nu, sizeof(float) * m_, cudaMemcpyDeviceToDevice, stream_));
+  std::vector<float> mu32(n_), nu32(m_);
+  GWB_CUDA(cudaMemcpyAsync(mu32.data(), mu, sizeof(float) * n_, cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaMemcpyAsync(nu32.data(), nu, sizeof(float) * m_, cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  std::vector<double> mu64(mu32.begin(), mu32.end()), nu64(nu32.begin(), nu32.end());
+  GWB_CUDA(cudaMemcpyAsync(mu64_, mu64.data(), sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
+  GWB_CUDA(cudaMemcpyAsync(nu64_, nu64.data(), sizeof(double) * m_, cudaMemcpyHostToDevice, stream_));
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  prepare_d();
+}
+
+void BapgEngine::reset(const double* w0_host) {
+  GWB_CUDA(cudaSetDevice(device_));
+  launch_status_reset(st_, stream_);
+  if (w0_host) {
+    double* stage = nullptr;
+    GWB_CUDA(cudaMalloc(&stage, sizeof(double) * n_ * m_));
+    GWB_CUDA(cudaMemcpyAsync(stage, w0_host, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, stream_));
+    launch_colmajor64_to_rowmajor32(stage, n_, m_, W_[0], ldm_, stream_);
+    GWB_CUDA(cudaStreamSynchronize(stream_));
+    GWB_CUDA(cudaFree(stage));
+  } else {
+    launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, W_[0], stream_);
+  }
+  launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], precision_ == GWB_PREC_TF32 ? 1 : 2, stream_);
+  parity_ = 0;
+  GWB_CUDA(cudaGetLastError());
+}
+
+cudaEvent_t BapgEngine::ev_get() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GWB_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
+  const BapgDev d = dev_view(q);
+  int64_t launches = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  if (timing_) {
+    e0 = ev_get();
+    e1 = ev_get();
+    e2 = ev_get();
+    GWB_CUDA(cudaEventRecord(e0, stream_));
+  }
+  GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
+  GWB_CUDA(gemm_launch(g2_, stream_));
+  launches += 2;
+  if (timing_) GWB_CUDA(cudaEventRecord(e1, stream_));
+  if (!half_b) {
+    launch_row_update(d, true, stream_);
+    launches += 2;
+  } else {
+    launch_col_update(d, stream_);
+    launch_finalize(d, rel_tol, false, stream_);
+    launches += 6;
+  }
+  if (timing_) {
+    GWB_CUDA(cudaEventRecord(e2, stream_));
+    ev_marks_.push_back({0, {e0, e1}});
+    ev_marks_.push_back({1, {e1, e2}});
+  }
+  GWB_CUDA(cudaGetLastError());
+  return launches;
+}
+
+int64_t BapgEngine::enqueue_iteration(int q, double rel_tol) {
+  return enqueue_half(q, false, rel_tol) + enqueue_half(q, true, rel_tol);
+}
+
+void BapgEngine::destroy_graphs() {
+  for (auto& g : graph_) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
+
+int64_t BapgEngine::iterate(int iters, double rel_tol, bool use_graph) {
+  GWB_CUDA(cudaSetDevice(device_));
+  int64_t launches = 0;
+  int done = 0;
+  if (use_graph && !timing_) {
+    while (iters - done >= kChunkIters) {
+      cudaGraphExec_t& ge = graph_[parity_];
+      if (!ge) {
+        cudaGraph_t g;
+        GWB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        int q = parity_;
+        for (int k = 0; k < kChunkIters; ++k) {
+          enqueue_iteration(q, rel_tol);
+          q ^= 1;
+        }
+        GWB_CUDA(cudaStreamEndCapture(stream_, &g));
+        GWB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        GWB_CUDA(cudaGraphDestroy(g));
+        graph_iters_ = kChunkIters;
+      }
+      GWB_CUDA(cudaGraphLaunch(ge, stream_));
+      launches += kChunkIters * 12;
+      done += kChunkIters;  // even ⇒ parity unchanged
+    }
+  }
+  for (; done < iters; ++done) {
+    launches += enqueue_iteration(parity_, rel_tol);
+    parity_ ^= 1;
+  }
+  return launches;
+}
+
+void BapgEngine::run(int max_iters, double rel_tol) {
+  GWB_CUDA(cudaSetDevice(device_));
+  int remaining = max_iters;
+  int c = 0;
+  cudaEvent_t ev[4];
+  for (auto& e : ev) GWB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  bool stop = false;
+  while (remaining > 0 && !stop) {
+    const int chunk = std::min(remaining, kChunkIters);
+    iterate(chunk, rel_tol, true);
+    remaining -= chunk;
+    GWB_CUDA(cudaMemcpyAsync(&h_done_[c % 4], &st_->done, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    GWB_CUDA(cudaEventRecord(ev[c % 4], stream_));
+    if (c >= 2) {
+      GWB_CUDA(cudaEventSynchronize(ev[(c - 2) % 4]));
+      if (h_done_[(c - 2) % 4]) stop = true;
+    }
+    ++c;
+  }
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  for (auto& e : ev) cudaEventDestroy(e);
+  // The current w lives in W_[iterations_used % 2] (iteration k writes it).
+  const DevStatus s = status();
+  parity_ = (s.iter - 1) & 1;
+}
+
+void BapgEngine::tail() {
+  GWB_CUDA(cudaSetDevice(device_));
+  const BapgDev d = dev_view(parity_);
+  GWB_CUDA(gemm_launch(g1_tail_[parity_], stream_));
+  GWB_CUDA(gemm_launch(g2_tail_, stream_));
+  launch_row_update(d, false, stream_);
+  launch_finalize(d, 0.0, true, stream_);
+  GWB_CUDA(cudaGetLastError());
+}
+
+DevStatus BapgEngine::status() {
+  DevStatus s;
+  GWB_CUDA(cudaMemcpyAsync(&s, st_, sizeof(s), cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  return s;
+}
+
+std::vector<HostRecord> BapgEngine::records(int count) {
+  std::vector<DevRecord> r(static_cast<size_t>(count) + 1);
+  GWB_CUDA(cudaMemcpyAsync(r.data(), rec_, sizeof(DevRecord) * (count + 1), cudaMemcpyDeviceToHost, stream_));
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  std::vector<HostRecord> out(static_cast<size_t>(count));
+  for (int k = 1; k <= count; ++k) {
+    const DevRecord& d = r[k];
+    HostRecord& h = out[k - 1];
+    // f(½(π+w)) = −¼[⟨Mπ,π⟩ + 2⟨Mπ,w⟩ + ⟨Mw,w⟩]  (D_X, D_Y symmetric)
+    h.objective = -0.25 * (d.mpi_pi + 2.0 * d.mpi_w + d.mw_w);
+    h.marginal_infeasibility = 0.5 * std::sqrt(d.col_sq) / static_cast<double>(m_) +
+                               0.5 * std::sqrt(d.row_sq) / static_cast<double>(n_);
+    h.split_gap = std::sqrt(d.split_sq);
+    h.rel_change = std::sqrt(d.diff_sq) / std::sqrt(d.wold_sq);
+    h.elapsed = d.elapsed;
+  }
+  return out;
+}
+
+void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
+  GWB_CUDA(cudaSetDevice(device_));
+  const size_t len = static_cast<size_t>(n_) * m_;
+  double* pi64 = nullptr;
+  double* w64 = nullptr;
+  double* work = nullptr;
+  GWB_CUDA(cudaMalloc(&pi64, len * sizeof(double)));
+  GWB_CUDA(cudaMalloc(&w64, len * sizeof(double)));
+  GWB_CUDA(cudaMalloc(&work, sizeof(double) * std::max(n_, m_)));
+  // K8 fix-up: exact fp64 row (π) / column (w) re-projection.
+  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+  launch_rowmajor32_to_colmajor64(W_[parity_], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  if (out_pi) GWB_CUDA(cudaMemcpyAsync(out_pi, pi64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  if (out_w) GWB_CUDA(cudaMemcpyAsync(out_w, w64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  if (out_final) {
+    launch_average64(pi64, w64, pi64, static_cast<int64_t>(len), stream_);
+    GWB_CUDA(cudaMemcpyAsync(out_final, pi64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  }
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(pi64);
+  cudaFree(w64);
+  cudaFree(work);
+}
+
+void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  double total = 0.0;
+  int64_t cnt = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
+  for (auto& mk : ev_marks_) {
+    if (mk.first == kind) {
+      float ms = 0.f;
+      GWB_CUDA(cudaEventElapsedTime(&ms, mk.second.first, mk.second.second));
+      total += ms;
+      ++cnt;
+    }
+  }
+  // Return all events to the pool (events are shared between marks).
+  std::vector<cudaEvent_t> evs;
+  for (auto& mk : ev_marks_) {
+    evs.push_back(mk.second.first);
+    evs.push_back(mk.second.second);
+  }
+  std::sort(evs.begin(), evs.end());
+  evs.erase(std::unique(evs.begin(), evs.end()), evs.end());
+  for (auto e : evs) ev_pool_.push_back(e);
+  ev_marks_.clear();
+  // One mark per half-step of each kind; GEMM marks cover two launches.
+  *avg_ms = cnt ? total / static_cast<double>(cnt) : 0.0;
+  *count = cnt;
+}
+
+double BapgEngine::gemm_flops_per_iter() const {
+  // Two half-steps × (m·n·m + n·m·n) MACs × 2.
+  return 2.0 * 2.0 * static_cast<double>(n_) * m_ * static_cast<double>(n_ + m_);
+}
+
+}  // namespace gwb

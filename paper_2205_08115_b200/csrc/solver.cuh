@@ -1,0 +1,134 @@
+// solver.cuh — device-side BAPG engine: workspace in HBM, the per-iteration
+// launch sequence (2×2 GEMMs + row/column projection passes + finalize),
+// CUDA-graph capture of iteration chunks, device-side stop rule, and the
+// fp64 boundary conversions.  Reference loop: bapg_solve,
+// proj/src/solvers.cpp:138-217.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gwb.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace gwb {
+
+struct CudaError : std::exception {
+  std::string msg;
+  explicit CudaError(std::string m) : msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+void check_cuda(cudaError_t e, const char* what);
+#define GWB_CUDA(x) ::gwb::check_cuda((x), #x)
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Host-side view of one finished trace record (IterationRecord fields).
+struct HostRecord {
+  double objective, marginal_infeasibility, split_gap, rel_change, elapsed;
+};
+
+class BapgEngine {
+ public:
+  // n×n D_X, m×m D_Y; `precision` resolved to PREC_TF32 or PREC_3XTF32.
+  BapgEngine(int device, int64_t n, int64_t m, double rho, int precision, int max_iters,
+             cudaStream_t stream);
+  ~BapgEngine();
+  BapgEngine(const BapgEngine&) = delete;
+  BapgEngine& operator=(const BapgEngine&) = delete;
+
+  int64_t n() const { return n_; }
+  int64_t m() const { return m_; }
+  cudaStream_t stream() const { return stream_; }
+
+  // Inputs from host fp64 column-major (symmetric D: layout-free) or from
+  // device fp32 row-major.
+  void load_host(const double* dx, const double* dy, const double* mu, const double* nu);
+  void load_device(const float* dx, int64_t ldx, const float* dy, int64_t ldy, const float* mu,
+                   const float* nu);
+  // π0 = μνᵀ or `initial` (host fp64 col-major); w0 = kl_scale(π0, ν, Cols)
+  // computed by the caller in fp64 and passed as w0 (nullable ⇒ w0 = π0,
+  // exact for the product coupling).
+  void reset(const double* w0_host);
+  // Enqueues `iters` iterations (no host sync); returns kernel launches.
+  int64_t iterate(int iters, double rel_tol, bool use_graph);
+  // Polls convergence between chunks; returns when done or all enqueued.
+  void run(int max_iters, double rel_tol);
+  // Objective / row-infeasibility of the last iteration (one more chain).
+  void tail();
+  DevStatus status();
+  std::vector<HostRecord> records(int count);
+  // Outputs as host fp64 column-major (nullable pointers are skipped).
+  void outputs(double* out_final, double* out_pi, double* out_w);
+  // Device pointers (session API).
+  float* pi_dev() const { return P_; }
+  int64_t ld() const { return ldm_; }
+  int precision() const { return precision_; }
+  // CUDA-event timing of kernel classes inside iterate() (enabled on demand).
+  void set_timing(bool on) { timing_ = on; }
+  void kernel_ms(int kind, double* avg_ms, int64_t* count);
+  double gemm_flops_per_iter() const;
+  bool d_exact() const { return dx_exact_ && dy_exact_; }
+  int parity() const { return parity_; }
+
+ private:
+  void alloc();
+  void build_plans();
+  void prepare_d();
+  int64_t enqueue_iteration(int parity, double rel_tol);
+  int64_t enqueue_half(int parity, bool half_b, double rel_tol);
+  void destroy_graphs();
+
+  int device_;
+  int64_t n_, m_, ldn_, ldm_;
+  double rho_;
+  int precision_;
+  int max_iters_;
+  cudaStream_t stream_;
+  bool own_stream_ = false;
+  int parity_ = 0;  // which W buffer holds the current w
+  bool dx_exact_ = true, dy_exact_ = true;
+
+  // device buffers
+  float *Dx_ = nullptr, *Dx_aux_ = nullptr, *Dy_ = nullptr, *Dy_aux_ = nullptr;
+  float *P_ = nullptr, *P_aux_ = nullptr, *W_[2] = {nullptr, nullptr},
+        *W_aux_[2] = {nullptr, nullptr};
+  float *Vt_ = nullptr, *Vt_aux_ = nullptr, *G_ = nullptr;
+  float *mu32_ = nullptr, *nu32_ = nullptr;
+  double *mu64_ = nullptr, *nu64_ = nullptr;
+  RowPart* row_part_ = nullptr;
+  ColWritePart* cw_part_ = nullptr;
+  float *col_pmax_ = nullptr, *col_psum_ = nullptr, *col_max_ = nullptr, *col_scale_ = nullptr;
+  double *col_psump_ = nullptr, *col_dev_ = nullptr;
+  DevStatus* st_ = nullptr;
+  DevRecord* rec_ = nullptr;
+  int chunks_ = 1;
+  int* h_done_ = nullptr;  // pinned
+
+  // GEMM plans: [parity][half] for GEMM1 (operand W[parity] or P), GEMM2;
+  // tail plans skip only on errors.
+  GemmPlan* g1_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  GemmPlan* g2_ = nullptr;
+  GemmPlan* g1_tail_[2] = {nullptr, nullptr};
+  GemmPlan* g2_tail_ = nullptr;
+
+  cudaGraphExec_t graph_[2] = {nullptr, nullptr};  // chunk graph per start parity
+  int graph_iters_ = 0;
+
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks_;
+  cudaEvent_t ev_get();
+
+  BapgDev dev_view(int parity) const;
+};
+
+// Resolves GWB_PREC_AUTO (see gwb.h).
+int resolve_precision(int requested, bool d_exact, double dmax_x, double dmax_y, double rho);
+
+}  // namespace gwb

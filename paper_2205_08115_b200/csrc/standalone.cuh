@@ -1,0 +1,49 @@
+// standalone.cuh — device implementations of the single-shot entry points
+// on the path (gw_objective, product_coupling, lipschitz_bound, kl_scale,
+// Sinkhorn, diagnostics, hard_assignment), the eBPG/BPG/hBPG solvers and the
+// batched small-problem BAPG.  Errors are raised through api_* (capi.cu).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/gwb.h"
+
+namespace gwb {
+
+[[noreturn]] void api_fail(int32_t code, const std::string& msg);
+[[noreturn]] void api_numerical(const char* solver, int iter, const std::string& detail);
+[[noreturn]] void api_zero_sum(int axis, int64_t index);
+int api_device();
+
+double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
+                           const double* pi);
+void device_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
+                             double* out);
+double device_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m);
+void device_kl_scale(const double* pi, int64_t n, int64_t m, const double* target, int32_t axis,
+                     double* out);
+void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* mu,
+                     const double* nu, double tol, int32_t max_iters, int32_t log_domain,
+                     double* out, int32_t* iterations, double* marginal_error,
+                     int32_t* converged);
+double device_marginal_infeasibility(const double* pi, int64_t n, int64_t m, const double* mu,
+                                     const double* nu);
+double device_split_gap(const double* pi, const double* w, int64_t n, int64_t m);
+void device_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out);
+
+// eBPG / BPG / hBPG (solvers.cpp:219-426) on the device.
+void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_t n,
+                   const double* dy, int64_t m, const double* mu, const double* nu,
+                   const double* initial, gwb_observer observer, void* user, double* out_final,
+                   gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
+                   int32_t* iterations_used);
+
+// Batched BAPG over independent small problems (config 5).
+void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
+                         const double* dy, int64_t m, const double* mu, const double* nu,
+                         double* out_final, double* out_pi, double* out_w, gwb_record* trace,
+                         int32_t trace_cap, int32_t* n_records, int32_t* converged,
+                         int32_t* iterations_used);
+
+}  // namespace gwb

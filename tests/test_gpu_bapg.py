@@ -1,0 +1,81 @@
+"""BAPG parity: the B200 path through the C-ABI against the CPU oracle
+(oracle/gw_oracle.c, pinned to the reference TUs) on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star): final coupling within 1e-4 max-abs
+relative to its scale, GW objective within 1e-5 relative, identical argmax
+matching on rows whose oracle top-2 margin exceeds the fp32 error bound.
+"""
+import numpy as np
+import pytest
+
+import paper_2205_08115_b200 as gw
+from paper_2205_08115_b200 import abi, instances as I
+
+pytestmark = pytest.mark.gpu
+
+PI_TOL = 1e-4
+OBJ_TOL = 1e-5
+
+
+def run_both(port, inst, precision, **over):
+    solver = dict(inst.solver)
+    solver.update(over)
+    cfg = gw.SolverConfig(precision=precision, quiet=True, **solver)
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu), cfg)
+    ores = port.solve(cfg.to_abi(), inst.dx, inst.dy, inst.mu, inst.nu)
+    assert ores.code == 0, ores.message
+    return rep, ores
+
+
+def rel_scale(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def check_argmax(pi, pi_ref, tol):
+    ref_idx = np.argmax(pi_ref, axis=1)
+    got = gw.hard_assignment(pi)
+    srt = np.sort(pi_ref, axis=1)
+    margin = (srt[:, -1] - srt[:, -2]) / np.abs(pi_ref).max()
+    decided = margin > 4 * tol
+    assert np.array_equal(got[decided], ref_idx[decided]), \
+        f"{np.sum(got[decided] != ref_idx[decided])} decided rows differ"
+    return decided.mean()
+
+
+@pytest.mark.parametrize("precision", ["tf32", "3xtf32"])
+def test_bapg_er_small(gpu, port, precision):
+    inst = I.config1(seed=3, n=256)
+    rep, o = run_both(port, inst, precision, max_iters=60)
+    assert rep.iterations_used == o.iterations_used == 60
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL
+    assert rel_scale(rep.w_half.entries(), o.w) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+    check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
+    for r, q in zip(rep.trace, o.trace):
+        assert r.iter == q["iter"]
+        assert abs(r.objective - q["objective"]) <= 1e-4 * abs(q["objective"])
+        assert abs(r.rel_change - q["rel_change"]) <= 1e-3 * q["rel_change"] + 1e-7
+        assert abs(r.split_gap - q["split_gap"]) <= 1e-3 * q["split_gap"] + 1e-9
+
+
+def test_bapg_gmm_small_3xtf32(gpu, port):
+    inst = I.config2(seed=1, n=320, m=256)
+    rep, o = run_both(port, inst, "3xtf32", max_iters=40)
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+
+
+def test_bapg_marginal_invariants(gpu):
+    inst = I.config1(seed=5, n=160)
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu),
+                   gw.SolverConfig(max_iters=20, rel_tol=1e-30))
+    pi, w = rep.pi_half.entries(), rep.w_half.entries()
+    # SPEC.md:329 / types.cpp:137-152: each half satisfies its own marginal.
+    assert np.abs(pi.sum(axis=1) - inst.mu).max() <= 1e-10
+    assert np.abs(w.sum(axis=0) - inst.nu).max() <= 1e-10
+    assert abs(rep.final_coupling.entries().sum() - 1.0) <= 1e-9

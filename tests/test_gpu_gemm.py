@@ -1,0 +1,56 @@
+"""K1: the tcgen05 TF32 / 3xTF32 GEMM against an fp64 torch reference."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(a, b, precision, c=None):
+    import torch
+    from paper_2205_08115_b200 import abi
+    M, K = a.shape
+    N = b.shape[0]
+    ld = lambda k: (k + 31) // 32 * 32
+    A = torch.zeros((M, ld(K)), device="cuda", dtype=torch.float32); A[:, :K] = a
+    B = torch.zeros((N, ld(K)), device="cuda", dtype=torch.float32); B[:, :K] = b
+    Cm = torch.full((M, ld(N)), float("nan"), device="cuda", dtype=torch.float32)
+    lib = abi.load()
+    fn = lib.gwb_debug_gemm
+    fn.restype = C.c_int32
+    fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                   C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.POINTER(abi.Status)]
+    st = abi.Status()
+    torch.cuda.synchronize()
+    rc = fn(A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1], Cm.data_ptr(), Cm.shape[1],
+            M, N, K, precision, None, C.byref(st))
+    torch.cuda.synchronize()
+    assert rc == 0, st.message
+    return Cm[:, :N].double().cpu().numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 32), (256, 512, 256), (1000, 1000, 1000),
+                                   (200, 72, 40), (20, 4000, 20), (4000, 20, 4000)])
+def test_gemm_tf32_exact_operands(gpu, M, N, K):
+    # Integer-valued operands are exact in TF32 and sums stay < 2^24: the
+    # tensor-core result must be bit-exact.
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    a = rng.integers(0, 3, size=(M, K)).astype(np.float32)
+    b = rng.integers(0, 3, size=(N, K)).astype(np.float32)
+    import torch
+    c = _gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 1)
+    np.testing.assert_array_equal(c, a.astype(np.float64) @ b.astype(np.float64).T)
+
+
+@pytest.mark.parametrize("precision,tol", [(1, 2e-3), (2, 2e-6)])
+def test_gemm_precision(gpu, precision, tol):
+    import torch
+    rng = np.random.default_rng(1)
+    M, N, K = 384, 640, 1024
+    a = rng.random((M, K)).astype(np.float32)
+    b = rng.random((N, K)).astype(np.float32)
+    c = _gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), precision)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    rel = np.abs(c - ref).max() / np.abs(ref).max()
+    assert rel < tol, rel
