@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: BAPG iterations/sec at n=m=20000 (BASELINE.json config 4).
+
+One "step" = one BAPG iteration (two half-steps, each a D_X·π·D_Y chain on
+the tcgen05 GEMM + the fused KL projection passes) over the resident
+problem.  value = iterations/s with inputs in HBM (timed with CUDA events on
+the solver's stream, max over ranks); e2e = the same metric through the
+C-ABI (gwb_solve) with host fp64 buffers, host↔device copies included.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BAPG iterations/sec at n=m=20000"
+WORKLOAD = ("c4: BAPG, Barabasi-Albert n=m=20000 (m_attach=5) vs permuted copy with 2% edge "
+            "noise, uniform marginals, rho=0.1, fp32 dense D")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=20000)
+    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32"])
+    ap.add_argument("--e2e-iters", type=int, default=200)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=2500)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "B200_PROFILING.md fallback"
+
+
+def measure_tf32_peak(torch):
+    """cuBLAS TF32 dense 8192³ (2·N³ FLOP), best of 10, CUDA events."""
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    for _ in range(3):
+        torch.matmul(a, b)
+    best = 1e9
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+# ---------------------------------------------------------------------------
+def build_instance(n, seed=0):
+    from paper_2205_08115_b200 import instances as I
+    e = I.barabasi_albert(n, 5, I.mix_seed(seed, 41))
+    noisy = I.edge_noise(n, e, 0.02, 0.02, I.mix_seed(I.mix_seed(seed, 41), 1))
+    tgt, perm = I.permute_graph(n, noisy, I.mix_seed(I.mix_seed(seed, 41), 2))
+    return e, tgt, perm
+
+
+def dense_dev(torch, n, edges):
+    d = torch.zeros((n, (n + 31) // 32 * 32), device="cuda", dtype=torch.float32)
+    t = torch.from_numpy(edges.astype(np.int64)).cuda()
+    d[t[:, 0], t[:, 1]] = 1.0
+    d[t[:, 1], t[:, 0]] = 1.0
+    return d
+
+
+def cpu_reference_sample(n_target, cpu_n, budget_s=20.0):
+    """Reference BAPG (oracle/_ref: reference TUs + eigen_lite + OpenBLAS fp64)
+    on a BA(cpu_n) instance; iterations/s extrapolated to n_target by the
+    FLOP ratio of the GEMM-dominated iteration (6·n·m·(n+m), n=m ⇒ ∝ n³)."""
+    from oracle.bindings import Oracle
+    from paper_2205_08115_b200 import abi
+    from paper_2205_08115_b200 import instances as I
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    ref = Oracle("reference")
+    e = I.barabasi_albert(cpu_n, 5, I.mix_seed(0, 41))
+    inst = I.alignment_instance(e, cpu_n, 0.02, I.mix_seed(0, 41), "cpu", {})
+    cfg = abi.default_config(rho=0.1, max_iters=1, rel_tol=1e-30)
+    t0 = time.perf_counter()
+    r = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    t1 = time.perf_counter() - t0
+    iters = max(1, min(50, int(budget_s / max(t1, 1e-3))))
+    cfg.max_iters = iters
+    t0 = time.perf_counter()
+    r = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    dt = time.perf_counter() - t0
+    assert r.code == 0, r.message
+    its = iters / dt
+    scale = (cpu_n / n_target) ** 3
+    return {"value": its * scale, "unit": "it/s", "cores": cores, "kind": "reference",
+            "sample": f"reference bapg_solve (oracle/_ref, OpenBLAS fp64, {cores} threads) on "
+                      f"BA n=m={cpu_n}: {iters} iterations in {dt:.2f}s = {its:.3f} it/s, "
+                      f"scaled by (n/{n_target})^3 to n={n_target}"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cb = cpu_reference_sample(args.n, args.cpu_n)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BA graphs)",
+            "config": {"workload": WORKLOAD, "parallelism": "cpu threads"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, world, rank, local, dist):
+    import torch
+    import paper_2205_08115_b200 as gw
+    from paper_2205_08115_b200 import abi
+
+    torch.cuda.set_device(local)
+    lib = abi.load()
+    n = args.n
+    edges, tgt, perm = build_instance(n)
+    dx = dense_dev(torch, n, edges)
+    dy = dense_dev(torch, n, tgt)
+    mu = torch.full((n,), 1.0 / n, device="cuda", dtype=torch.float32)
+    nu = mu.clone()
+
+    prec = {"auto": abi.PREC_AUTO, "tf32": abi.PREC_TF32, "3xtf32": abi.PREC_3XTF32}[args.precision]
+    cfg = abi.default_config(rho=0.1, max_iters=args.steps + args.warmup + 4, rel_tol=1e-30,
+                             precision=prec)
+    st = abi.Status()
+    sess = C.c_void_p()
+    rc = lib.gwb_session_create(C.byref(cfg), n, n, local, C.byref(sess), C.byref(st))
+    abi.raise_for(st)
+    torch.cuda.synchronize()
+    lib.gwb_session_load_device(sess, dx.data_ptr(), dx.shape[1], dy.data_ptr(), dy.shape[1],
+                                mu.data_ptr(), nu.data_ptr(), None, C.byref(st))
+    abi.raise_for(st)
+    lib.gwb_session_reset(sess, None, C.byref(st))
+    abi.raise_for(st)
+    sp = C.c_void_p()
+    lib.gwb_session_stream(sess, C.byref(sp), C.byref(st))
+    stream = torch.cuda.ExternalStream(sp.value)
+    rprec, flops_it = C.c_int32(0), C.c_double(0)
+    lib.gwb_session_info(sess, C.byref(rprec), C.byref(flops_it), C.byref(st))
+
+    launches = C.c_int64(-1)  # eager with per-kernel-class CUDA events
+    lib.gwb_session_iterate(sess, args.warmup, None, C.byref(launches), C.byref(st))
+    abi.raise_for(st)
+    gms, gcnt = C.c_double(0), C.c_int64(0)
+    lib.gwb_session_kernel_ms(sess, 0, C.byref(gms), C.byref(gcnt), C.byref(st))  # reset marks
+    lib.gwb_session_kernel_ms(sess, 1, C.byref(gms), C.byref(gcnt), C.byref(st))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    with clocks:
+        with torch.cuda.stream(stream):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            launches = C.c_int64(-1)
+            lib.gwb_session_iterate(sess, args.steps, None, C.byref(launches), C.byref(st))
+            ev1.record(stream)
+            ev1.synchronize()
+    abi.raise_for(st)
+    ms = ev0.elapsed_time(ev1)
+    # per-launch GEMM time: one mark per half-step covers GEMM1+GEMM2
+    lib.gwb_session_kernel_ms(sess, 0, C.byref(gms), C.byref(gcnt), C.byref(st))
+    chain_ms = gms.value
+    sms, scnt = C.c_double(0), C.c_int64(0)
+    lib.gwb_session_kernel_ms(sess, 1, C.byref(sms), C.byref(scnt), C.byref(st))
+    torch.cuda.synchronize()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value_rank = args.steps / (ms * 1e-3)
+    value = value_rank * world  # replicas: every rank runs the full problem
+
+    peaks, peak_src = measured_peaks()
+    tf32_peak = measure_tf32_peak(torch) if rank == 0 else None
+    chain_flops = flops_it.value / 2.0           # one half-step = one D_X·π·D_Y chain
+    achieved = chain_flops / (chain_ms * 1e-3) / 1e12 if chain_ms > 0 else None
+    passes = 2 if rprec.value == abi.PREC_3XTF32 else 1
+    roofline = {
+        "bound": "tensor", "kernel": "gemm_tf32_kernel (D_Y·πᵀ then D_X·V per half-step)",
+        "achieved": achieved, "unit": "TFLOP/s",
+        "peak": tf32_peak, "peak_source": "cuBLAS TF32 8192^3 measured in this run "
+        f"(MEASURED_PEAKS has bf16 only: {peaks.get('bf16_tflops')} TF/s burst, {peak_src})",
+        "frac": (achieved / tf32_peak) if (achieved and tf32_peak) else None,
+        "executed_frac": (achieved * passes / tf32_peak) if (achieved and tf32_peak) else None,
+        "algorithmic_flops_per_launch_pair": chain_flops,
+        "passes": passes, "traffic": None,
+        "scaling_kernels_ms_per_half_step": sms.value,
+    }
+    sess_destroy = lib.gwb_session_destroy
+    sess_destroy(sess)
+    del dx, dy
+    torch.cuda.empty_cache()
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e(args, edges, tgt, n, prec)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        try:
+            cpu = cpu_reference_sample(n, args.cpu_n)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "error": str(ex)}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (3xTF32 tensor cores, fp32 accumulate)" if passes == 2 else "f32 (1xTF32)",
+            "data": "synthetic (seeded BA graphs, reference RNG)",
+            "config": {"workload": WORKLOAD, "n": n, "m": n,
+                       "precision": "3xtf32" if passes == 2 else "tf32",
+                       "l2": "no flush: each operand (1.6 GB) exceeds the 126 MB L2",
+                       "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+            "tflops": {"algorithmic_per_iteration": flops_it.value,
+                       "achieved_whole_step": flops_it.value * value_rank / 1e12},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches.value), "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, edges, tgt, n, prec):
+    """gwb_solve through the C-ABI from host fp64 (column-major) buffers:
+    H2D of D_X, D_Y, μ, ν and D2H of the final coupling + trace inside the
+    timed region.  Iterations/s = e2e_iters / wall time of the call."""
+    import paper_2205_08115_b200 as gw
+    from paper_2205_08115_b200 import abi, instances as I
+    dx = I.adjacency(n, edges)
+    dy = I.adjacency(n, tgt)
+    u = np.full(n, 1.0 / n)
+    out = np.empty((n, n), order="F")
+    cfg = abi.default_config(rho=0.1, max_iters=args.e2e_iters, rel_tol=1e-30, precision=prec)
+    trace = (abi.Record * cfg.max_iters)()
+    nr, cv, used = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    st = abi.Status()
+    lib = abi.load()
+    D = C.POINTER(C.c_double)
+    p = lambda a: a.ctypes.data_as(D)
+    t0 = time.perf_counter()
+    lib.gwb_solve(C.byref(cfg), p(dx), n, p(dy), n, p(u), p(u), None, abi.OBSERVER(), None,
+                  p(out), None, None, trace, cfg.max_iters, C.byref(nr), C.byref(cv),
+                  C.byref(used), C.byref(st))
+    dt = time.perf_counter() - t0
+    abi.raise_for(st)
+    return {"value": used.value / dt, "unit": "it/s", "iterations": used.value,
+            "seconds": dt, "h2d_bytes_per_step": int(dx.nbytes + dy.nbytes + 2 * u.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes + used.value * C.sizeof(abi.Record)),
+            "note": "one gwb_solve call = one e2e step (pageable host fp64 buffers)"}
+
+
+def main():
+    args = parse()
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -367,16 +367,18 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(BapgDev d, double
     t[q] = 0.0;
     for (int r = 0; r < kFinThreads / 32; ++r) t[q] += s[q][r];
   }
+  // Iterations past max_rec (session API) share a scratch slot.
+  auto slot = [&](int it) { return it <= d.max_rec ? it : d.max_rec + 1; };
   if (tail) {
-    d.rec[k].mw_w = t[0];
-    d.rec[k].row_sq = t[1];
+    d.rec[slot(k)].mw_w = t[0];
+    d.rec[slot(k)].row_sq = t[1];
     return;
   }
   if (k >= 2) {  // the row pass of iteration k saw w^{k-1}
-    d.rec[k - 1].mw_w = t[0];
-    d.rec[k - 1].row_sq = t[1];
+    d.rec[slot(k - 1)].mw_w = t[0];
+    d.rec[slot(k - 1)].row_sq = t[1];
   }
-  DevRecord& r = d.rec[k];
+  DevRecord& r = d.rec[slot(k)];
   r.mpi_w = t[2];
   r.split_sq = t[3];
   r.diff_sq = t[4];

@@ -90,7 +90,8 @@ struct BapgDev {
   double* col_dev;          // m : (colsum(P)_j − ν_j)²
   int chunks;
   DevStatus* st;
-  DevRecord* rec;           // [max_iters + 1]
+  DevRecord* rec;           // [max_rec + 2]
+  int max_rec;              // records beyond this iteration are not kept
 };
 
 // Half-step a (solvers.cpp:164-170): E = G/ρ, P = diag(μ/rowsum)·(W ⊙ e^E),

@@ -162,6 +162,7 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.chunks = chunks_;
   d.st = st_;
   d.rec = rec_;
+  d.max_rec = max_iters_;
   return d;
 }
 
@@ -501,17 +502,25 @@ void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
 
 void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
   GWB_CUDA(cudaStreamSynchronize(stream_));
-  double total = 0.0;
-  int64_t cnt = 0;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
-  for (auto& mk : ev_marks_) {
-    if (mk.first == kind) {
-      float ms = 0.f;
-      GWB_CUDA(cudaEventElapsedTime(&ms, mk.second.first, mk.second.second));
-      total += ms;
-      ++cnt;
-    }
+  if (ev_marks_.empty()) {  // already harvested: report the cached class
+    *avg_ms = kind >= 0 && kind < 2 ? last_ms_[kind] : 0.0;
+    *count = kind >= 0 && kind < 2 ? last_cnt_[kind] : 0;
+    return;
   }
+  double tot[2] = {0.0, 0.0};
+  int64_t cnts[2] = {0, 0};
+  for (auto& mk : ev_marks_) {
+    float ms = 0.f;
+    GWB_CUDA(cudaEventElapsedTime(&ms, mk.second.first, mk.second.second));
+    tot[mk.first] += ms;
+    ++cnts[mk.first];
+  }
+  for (int k = 0; k < 2; ++k) {
+    last_ms_[k] = cnts[k] ? tot[k] / static_cast<double>(cnts[k]) : 0.0;
+    last_cnt_[k] = cnts[k];
+  }
+  const double total = kind >= 0 && kind < 2 ? tot[kind] : 0.0;
+  const int64_t cnt = kind >= 0 && kind < 2 ? cnts[kind] : 0;
   // Return all events to the pool (events are shared between marks).
   std::vector<cudaEvent_t> evs;
   for (auto& mk : ev_marks_) {

@@ -121,6 +121,8 @@ class BapgEngine {
   int graph_iters_ = 0;
 
   bool timing_ = false;
+  double last_ms_[2] = {0.0, 0.0};
+  int64_t last_cnt_[2] = {0, 0};
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks_;
   cudaEvent_t ev_get();
