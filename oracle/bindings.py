@@ -76,12 +76,12 @@ class Oracle:
                 self.lib.gwo_set_dgemm(C.cast(self._blas.scipy_cblas_dgemm64_, C.c_void_p))
         self.pre = pre
         L = self.lib
-        L[pre + "solve"].argtypes = _SOLVE
-        L[pre + "solve"].restype = C.c_int32
-        L[pre + "gw_objective"].argtypes = [_D, C.c_int64, _D, C.c_int64, _D, C.c_int64, C.c_int64, _D, _ST]
-        L[pre + "product_coupling"].argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _ST]
-        L[pre + "kl_scale"].argtypes = [_D, C.c_int64, C.c_int64, _D, C.c_int64, C.c_int32, _D, _ST]
-        L[pre + "sinkhorn_project"].argtypes = [_D, C.c_int64, C.c_int64, _D, _D, C.c_double,
+        getattr(L, pre + "solve").argtypes = _SOLVE
+        getattr(L, pre + "solve").restype = C.c_int32
+        getattr(L, pre + "gw_objective").argtypes = [_D, C.c_int64, _D, C.c_int64, _D, C.c_int64, C.c_int64, _D, _ST]
+        getattr(L, pre + "product_coupling").argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _ST]
+        getattr(L, pre + "kl_scale").argtypes = [_D, C.c_int64, C.c_int64, _D, C.c_int64, C.c_int32, _D, _ST]
+        getattr(L, pre + "sinkhorn_project").argtypes = [_D, C.c_int64, C.c_int64, _D, _D, C.c_double,
                                                 C.c_int32, C.c_int32, _D, _I, _D, _I, _ST]
         if kind == "reference":
             L.gwref_lipschitz_bound.argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _ST]
@@ -110,7 +110,7 @@ class Oracle:
         trace = (abi.Record * cap)()
         nr, cv, used = C.c_int32(0), C.c_int32(0), C.c_int32(0)
         st = abi.Status()
-        rc = self.lib[self.pre + "solve"](C.byref(cfg), _p(dx), n, _p(dy), m, _p(mu), _p(nu),
+        rc = getattr(self.lib, self.pre + "solve")(C.byref(cfg), _p(dx), n, _p(dy), m, _p(mu), _p(nu),
                                           _p(init), _p(final), _p(pi), _p(w), trace, cap,
                                           C.byref(nr), C.byref(cv), C.byref(used), C.byref(st))
         res = OracleResult(rc, st.message.decode(errors="replace"), status=st)
@@ -129,20 +129,20 @@ class Oracle:
     def gw_objective(self, dx, dy, pi):
         dx, dy, pi = _f(dx), _f(dy), _f(pi)
         out, st = C.c_double(0), abi.Status()
-        rc = self.lib[self.pre + "gw_objective"](_p(dx), dx.shape[0], _p(dy), dy.shape[0], _p(pi),
+        rc = getattr(self.lib, self.pre + "gw_objective")(_p(dx), dx.shape[0], _p(dy), dy.shape[0], _p(pi),
                                                  pi.shape[0], pi.shape[1], C.byref(out), C.byref(st))
         return rc, out.value, st
 
     def product_coupling(self, mu, nu):
         mu, nu = np.ascontiguousarray(mu, float), np.ascontiguousarray(nu, float)
         out, st = np.empty((mu.size, nu.size), order="F"), abi.Status()
-        rc = self.lib[self.pre + "product_coupling"](_p(mu), mu.size, _p(nu), nu.size, _p(out), C.byref(st))
+        rc = getattr(self.lib, self.pre + "product_coupling")(_p(mu), mu.size, _p(nu), nu.size, _p(out), C.byref(st))
         return rc, out, st
 
     def kl_scale(self, pi, target, axis):
         pi, t = _f(pi), np.ascontiguousarray(target, float)
         out, st = np.empty_like(pi, order="F"), abi.Status()
-        rc = self.lib[self.pre + "kl_scale"](_p(pi), pi.shape[0], pi.shape[1], _p(t), t.size, axis,
+        rc = getattr(self.lib, self.pre + "kl_scale")(_p(pi), pi.shape[0], pi.shape[1], _p(t), t.size, axis,
                                              _p(out), C.byref(st))
         return rc, out, st
 
@@ -151,7 +151,7 @@ class Oracle:
         mu, nu = np.ascontiguousarray(mu, float), np.ascontiguousarray(nu, float)
         out, st = np.empty_like(k, order="F"), abi.Status()
         it, err, cv = C.c_int32(0), C.c_double(0), C.c_int32(0)
-        rc = self.lib[self.pre + "sinkhorn_project"](_p(k), k.shape[0], k.shape[1], _p(mu), _p(nu),
+        rc = getattr(self.lib, self.pre + "sinkhorn_project")(_p(k), k.shape[0], k.shape[1], _p(mu), _p(nu),
                                                      tol, max_iters, int(log_domain), _p(out),
                                                      C.byref(it), C.byref(err), C.byref(cv), C.byref(st))
         return rc, dict(coupling=out, iterations=it.value, marginal_error=err.value,

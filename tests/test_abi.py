@@ -1,0 +1,111 @@
+"""C-ABI surface (CPU): the library loads, exports every symbol the headers
+declare, and the host-side validation mirrors the reference; compute entry
+points fail loudly (no CPU fallback) when no GPU is visible."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2205_08115_b200 as gw
+from paper_2205_08115_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("gwb.h", "gwb_ext.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"\b(gwb_[a-z0-9_]+)\s*(?:\(|GWB_SOLVE_SIGNATURE)", txt))
+    names.discard("gwb_solve_fn")
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = abi.load()
+    syms = declared_symbols()
+    assert len(syms) >= 35
+    for s in sorted(syms):
+        assert hasattr(lib, s), s
+
+
+def test_version_names_arch():
+    assert "sm_100a" in gw.version()
+
+
+def test_config_defaults_match_reference():
+    c = abi.Config()
+    abi.load().gwb_config_default(C.byref(c))
+    # test_core.cpp:145-159
+    assert (c.rel_tol, c.max_iters, c.rho, c.step, c.epsilon_reg) == (1e-6, 2000, 0.1, 5.0, 0.1)
+    assert (c.perturbation, c.inner_tol, c.inner_iters, c.switch_iters) == (0.0, 1e-9, 1000, 200)
+
+
+@pytest.mark.parametrize("field,val,msg", [
+    ("rho", 0.0, "rho must be positive"), ("step", -1.0, "step must be positive"),
+    ("epsilon_reg", 0.0, "eps must be positive"), ("inner_iters", 0, "inner-iters must be >= 1"),
+    ("inner_tol", 0.0, "inner-tol must be positive"), ("rel_tol", 0.0, "rel-tol must be positive"),
+    ("max_iters", 0, "max-iters must be >= 1"), ("perturbation", -0.1, "perturbation must lie in [0, 1)"),
+    ("switch_iters", -2, "switch-iters must be >= 0")])
+def test_validate_messages(field, val, msg):
+    cfg = gw.SolverConfig(**{field: val})
+    with pytest.raises(gw.ConfigError, match=re.escape(msg)):
+        gw.validate(cfg)
+
+
+def test_require_algorithm_before_validation():
+    d = gw.DistanceMatrix(np.zeros((2, 2)))
+    u = gw.ProbabilityVector.uniform(2)
+    with pytest.raises(gw.ConfigError, match="bapg_solve called with algorithm 'hbpg'"):
+        gw.bapg_solve(d, d, u, u, gw.SolverConfig(algorithm="hbpg", rho=0.0))
+
+
+def test_value_types():
+    # test_core.cpp:91-132
+    sym = np.array([[0, 1], [1, 0]], float)
+    np.testing.assert_array_equal(gw.DistanceMatrix(sym).entries(), sym)
+    fixed = gw.DistanceMatrix(np.array([[0, 2], [4, 0]], float)).entries()
+    assert fixed[0, 1] == 3.0 and fixed[1, 0] == 3.0
+    with pytest.raises(gw.DimensionMismatchError):
+        gw.DistanceMatrix(np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        gw.DistanceMatrix(np.array([[0, -1], [-1, 0]], float))
+    with pytest.raises(ValueError):
+        gw.DistanceMatrix(np.array([[np.nan, 1], [1, 0]]))
+    gw.ProbabilityVector([0.5, 0.5])
+    for bad in ([1.0, 0.0], [0.6, 0.6], [-0.5, 1.5]):
+        with pytest.raises(ValueError):
+            gw.ProbabilityVector(bad)
+    assert gw.ProbabilityVector.uniform(4).weights()[3] == 0.25
+    gw.Coupling(np.array([[0.5, 0.0], [0.0, 0.5]]))
+    with pytest.raises(ValueError):
+        gw.Coupling(np.array([[0.6, 0.0], [0.0, 0.5]]))
+
+
+def test_validate_inputs_names_pair():
+    d3 = gw.DistanceMatrix(np.zeros((3, 3)))
+    d4 = gw.DistanceMatrix(np.zeros((4, 4)))
+    gw.validate_inputs(d3, d4, gw.ProbabilityVector.uniform(3), gw.ProbabilityVector.uniform(4))
+    with pytest.raises(gw.DimensionMismatchError, match="D_X"):
+        gw.validate_inputs(d3, d4, gw.ProbabilityVector.uniform(4), gw.ProbabilityVector.uniform(3))
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    d = gw.DistanceMatrix(np.zeros((2, 2)))
+    u = gw.ProbabilityVector.uniform(2)
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        gw.solve(d, d, u, u, gw.SolverConfig(max_iters=2))
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        gw.product_coupling(u, u)
+
+
+def test_unsupported_paths_are_explicit():
+    d = gw.DistanceMatrix(np.zeros((2, 2)))
+    u = gw.ProbabilityVector.uniform(2)
+    with pytest.raises(gw.UnsupportedError):
+        gw.solve(d, d, u, u, gw.SolverConfig(algorithm="fw", max_iters=2))

@@ -1,0 +1,70 @@
+"""The C restatement (oracle/gw_oracle.c) against the reference's own
+translation units (oracle/_ref) on seeded instances: every algorithm on the
+path, traces, and error semantics.  Pins the oracle used by the GPU parity
+tests.  Skipped where the reference is not buildable (the GPU box)."""
+import numpy as np
+import pytest
+
+from paper_2205_08115_b200 import abi
+from paper_2205_08115_b200 import instances as I
+
+CASES = [
+    ("bapg-er", lambda: I.config1(seed=1, n=96), dict(algorithm=abi.BAPG, rho=0.1, max_iters=40)),
+    ("bapg-gmm", lambda: I.config2(seed=2, n=80, m=64), dict(algorithm=abi.BAPG, rho=0.05, max_iters=30)),
+    ("bapg-sbm", lambda: I.config3(seed=3, n=120, k=6), dict(algorithm=abi.BAPG, rho=0.5, max_iters=30)),
+    ("bapg-stop", lambda: I.config1(seed=4, n=64), dict(algorithm=abi.BAPG, rho=0.1, max_iters=500, rel_tol=1e-6)),
+    ("ebpg", lambda: I.config1(seed=5, n=64), dict(algorithm=abi.EBPG, epsilon_reg=0.1, max_iters=15, inner_iters=10)),
+    ("ebpg-log", lambda: I.config1(seed=6, n=64), dict(algorithm=abi.EBPG, epsilon_reg=0.01, log_domain=1, max_iters=10, inner_iters=20)),
+    ("bpg", lambda: I.config1(seed=7, n=64), dict(algorithm=abi.BPG, step=5.0, max_iters=12, inner_iters=10)),
+    ("hbpg", lambda: I.config1(seed=8, n=64), dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10, switch_iters=6, max_iters=14)),
+    ("bpg-perturb", lambda: I.config1(seed=9, n=48), dict(algorithm=abi.BPG, perturbation=0.01, max_iters=8, inner_iters=20)),
+]
+
+
+@pytest.mark.parametrize("name,make,over", CASES, ids=[c[0] for c in CASES])
+def test_port_matches_reference(port, ref, name, make, over):
+    inst = make()
+    kw = dict(rel_tol=1e-30, quiet=1)
+    kw.update(over)
+    cfg = abi.default_config(**kw)
+    a = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    b = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert a.code == b.code == 0, (a.message, b.message)
+    assert a.iterations_used == b.iterations_used and a.converged == b.converged
+    scale = np.abs(b.final).max()
+    assert np.abs(a.final - b.final).max() <= 1e-12 * scale
+    assert len(a.trace) == len(b.trace)
+    for x, y in zip(a.trace, b.trace):
+        assert x["iter"] == y["iter"] and x["phase"] == y["phase"]
+        for k in ("objective", "marginal_infeasibility", "split_gap", "rel_change"):
+            assert x[k] == pytest.approx(y[k], rel=1e-9, abs=1e-15), (k, x[k], y[k])
+
+
+@pytest.mark.parametrize("over,solver", [
+    (dict(rho=1e-7), "bapg"),
+    (dict(algorithm=abi.BPG, step=1e7, inner_iters=5), "bpg"),
+    (dict(algorithm=abi.EBPG, epsilon_reg=1e-5, inner_iters=5), "ebpg"),
+])
+def test_error_semantics_match(port, ref, over, solver):
+    inst = I.config1(seed=2, n=48)
+    cfg = abi.default_config(rel_tol=1e-30, max_iters=5, quiet=1, **over)
+    a = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    b = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert a.code == b.code and a.message == b.message, (a.message, b.message)
+    assert a.code == abi.ERR_NUMERICAL
+    assert a.status.solver.decode() == solver
+
+
+def test_initial_coupling_and_positivity(port, ref):
+    inst = I.config1(seed=3, n=40)
+    rng = np.random.default_rng(0)
+    init = rng.random((40, 40)) + 0.1
+    init /= init.sum()
+    cfg = abi.default_config(rel_tol=1e-30, max_iters=5)
+    a = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
+    b = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
+    assert np.abs(a.final - b.final).max() <= 1e-13
+    init[3, 4] = 0.0
+    a = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
+    b = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
+    assert a.code == b.code == abi.ERR_CONFIG and a.message == b.message
