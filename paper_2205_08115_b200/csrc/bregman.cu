@@ -1,1 +1,937 @@
-// bregman.cu — eBPG / BPG / hBPG device solvers (placeholder until built).
+// bregman.cu — eBPG / BPG / hBPG on the device (reference solvers.cpp:219-426).
+//
+// Per outer iteration k (π = current coupling, P[q]):
+//   GEMM chain            G = D_X·π·D_Y                       (tcgen05, 3xTF32)
+//   form   (row pass)     ⟨G,π⟩ for record k−1's objective;
+//                         eBPG: E = (2/ε)G, BPG: E = 2t·G, log-kernel
+//                         LK = E (eBPG) or log π + E (BPG); stores the
+//                         row-shifted LKs = LK − max_j LK in place of G
+//   check                 BPG overflow (max E > 700), eBPG dead lines,
+//                         reset of the Sinkhorn potentials
+//   sweeps s=1..inner     row LSE → f (fp64), early-exit decision for sweep
+//                         s−1 (the reference's ∞-norm marginal test after a
+//                         full ROWS→COLS sweep, projections.cpp:101-113),
+//                         column LSE (chunked partials + fixed-order merge) → g
+//   write                 π' = exp(max(LKs, clamp) + f + g) (+ perturbation),
+//                         row/column sums, ‖π'−π‖², ‖π‖²
+//   finalize              trace record, stop rule, hBPG phase switch.
+// The Sinkhorn runs in the log domain with fp64 potentials over an fp32
+// row-shifted log-kernel: identical to the reference's plain-domain
+// alternating scaling (rows first) whenever the latter is finite, with the
+// reference's 1e-300 kernel clamp applied as a log-space floor and its error
+// semantics (dead lines, zero-sum lines, overflow, non-finite) emulated.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "devutil.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "solver.cuh"
+#include "standalone.cuh"
+
+namespace gwb {
+
+namespace {
+
+using namespace dev;
+
+constexpr double kLogClamp = -690.7755278982137;     // log(1e-300)
+constexpr double kExpUnderflow = -745.1332191019412;  // fp64 exp(x) == 0 below
+constexpr int kThreads = 256;
+constexpr int kColWidth = 128;
+
+enum BFlag : int {
+  kBOverflow = 1,   // BPG: max(2t·D_X π D_Y) > 700
+  kBDeadLine = 2,   // eBPG (plain): a kernel line underflowed to zero
+  kBZeroRow = 4,    // Sinkhorn row with zero sum   (index: zero_index)
+  kBZeroCol = 8,    // Sinkhorn column with zero sum
+  kBNonFinite = 16, // Sinkhorn produced non-finite values (sweep: err_sweep)
+};
+
+struct BState {
+  int done, flags, iter, err_iter, converged;
+  int zero_index, err_sweep;
+  int phase;      // 1 = eBPG, 2 = BPG
+  int used1, conv1;
+  int sink_done, sweeps;
+  int gmax_bits;  // max of E over the matrix (E ≥ 0), float bits
+  unsigned long long t0;
+};
+
+struct BRecord {
+  double obj;      // ⟨M(π), π⟩, filled one iteration later
+  double rel, infeas, elapsed;
+  int phase, sweeps;
+};
+
+struct BDev {
+  int64_t n, m, ld;
+  float* G;             // chain output, overwritten by LKs
+  const float* P;       // π_k
+  float* P_new;
+  float* P_aux_new;
+  int aux_mode;
+  const double* mu64;
+  const double* nu64;
+  double* f;
+  double* f_new;
+  double* g;
+  float* rowmax;
+  double* row_err;
+  double* col_err;
+  double* col_pm;       // chunks × m  (max, fp64)
+  double* col_ps;       // chunks × m  (Σ exp, fp64)
+  float* col_pemax;     // chunks × m  (max of unshifted E; sweep 1, eBPG plain)
+  double* col_sum;      // chunks × m  (write-pass column sums)
+  double* row_sum;      // colblocks × n
+  double* obj_part;     // n
+  double* wpart;        // (colblocks·chunks) × 2
+  int chunks, colblocks;
+  float eb_scale;       // 2/ε
+  float bp_scale;       // 2t
+  int log_domain;
+  double perturb, uniform_mass;
+  int budget1, max_iters, has_phase2;
+  double rel_tol, inner_tol;
+  BState* st;
+  BRecord* rec;
+  int max_rec;
+};
+
+__device__ __forceinline__ bool skip(const BDev& d) { return d.st->done != 0; }
+__device__ __forceinline__ bool skip_sink(const BDev& d) {
+  return d.st->done != 0 || d.st->sink_done != 0;
+}
+
+// Per-row clamp floor in shifted log space: the reference clamps the kernel
+// at 1e-300 (solvers.cpp:252, :331); eBPG's kernel is exp(E − max E).
+__device__ __forceinline__ double clamp_floor(const BDev& d, int64_t i) {
+  if (d.st->phase == 1) {
+    if (d.log_domain) return -INFINITY;
+    return kLogClamp + static_cast<double>(__int_as_float(d.st->gmax_bits)) - d.rowmax[i];
+  }
+  return kLogClamp - d.rowmax[i];
+}
+
+__device__ double block_sum(double v) {
+  __shared__ double sh[32];
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t += sh[q];
+  return t;
+}
+
+__device__ float block_max(float v) {
+  __shared__ float sh[32];
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = -INFINITY;
+  for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t = fmaxf(t, sh[q]);
+  return t;
+}
+
+// (max, Σ e^{x−max}) in fp64 state with fp32 exponentials of small arguments.
+struct LseAcc {
+  double mx;
+  double s;
+};
+__device__ __forceinline__ void lse_add(LseAcc& a, double x) {
+  if (x > a.mx) {
+    a.s = a.s * static_cast<double>(__expf(static_cast<float>(a.mx - x))) + 1.0;
+    a.mx = x;
+  } else if (x > -INFINITY) {
+    a.s += static_cast<double>(__expf(static_cast<float>(x - a.mx)));
+  } else if (isnan(x)) {
+    a.mx = NAN;
+  }
+}
+__device__ __forceinline__ LseAcc lse_merge(LseAcc a, LseAcc b) {
+  if (isnan(a.mx) || isnan(b.mx)) return LseAcc{NAN, NAN};
+  if (b.mx == -INFINITY) return a;
+  if (a.mx == -INFINITY) return b;
+  const double M = fmax(a.mx, b.mx);
+  return LseAcc{M, a.s * exp(a.mx - M) + b.s * exp(b.mx - M)};
+}
+
+// ---------------------------------------------------------------------------
+// form: one CTA per row.
+__global__ void __launch_bounds__(kThreads) form_kernel(BDev d, int tail) {
+  if (tail ? d.st->flags != 0 : skip(d)) return;
+  const int64_t i = blockIdx.x;
+  float* g = d.G + i * d.ld;
+  const float* p = d.P + i * d.ld;
+  const bool ebpg = d.st->phase == 1;
+  const float sc = ebpg ? d.eb_scale : d.bp_scale;
+  double obj = 0.0;
+  float rmax = -INFINITY, emax = 0.0f;
+  for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
+    const float gv = g[j], pv = p[j];
+    obj += static_cast<double>(gv) * pv;
+    const float e = sc * gv;
+    emax = fmaxf(emax, e);
+    const float lk = ebpg ? e : e + logf(pv);
+    rmax = fmaxf(rmax, lk);
+  }
+  obj = block_sum(obj);
+  if (threadIdx.x == 0) d.obj_part[i] = obj;
+  if (tail) return;
+  rmax = block_max(rmax);
+  emax = block_max(emax);
+  if (threadIdx.x == 0) {
+    d.rowmax[i] = rmax;
+    atomicMax(&d.st->gmax_bits, __float_as_int(emax));
+  }
+  for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
+    const float e = sc * g[j];
+    const float lk = ebpg ? e : e + logf(p[j]);
+    g[j] = lk - rmax;
+  }
+}
+
+// Checks after the form pass + Sinkhorn reset.  One block.
+__global__ void form_check_kernel(BDev d) {
+  BState* st = d.st;
+  if (skip(d)) return;
+  const float gmax = __int_as_float(st->gmax_bits);
+  float rmin = INFINITY;
+  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) rmin = fminf(rmin, d.rowmax[i]);
+  rmin = -block_max(-rmin);
+  for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) d.g[j] = 0.0;
+  if (threadIdx.x == 0) {
+    st->sink_done = 0;
+    st->sweeps = 0;
+    if (st->phase == 2 && gmax > 700.0f) {
+      atomicOr(&st->flags, kBOverflow);
+    } else if (st->phase == 1 && !d.log_domain &&
+               static_cast<double>(rmin) - gmax < kExpUnderflow) {
+      atomicOr(&st->flags, kBDeadLine);
+    }
+    if (st->flags) {
+      st->done = 1;
+      st->err_iter = st->iter;
+    }
+  }
+}
+
+// Sinkhorn row update for sweep s: f_new = log μ − LSE_j(max(LKs, floor) + g).
+__global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
+  if (skip_sink(d)) return;
+  const int64_t i = blockIdx.x;
+  const float* lk = d.G + i * d.ld;
+  const double floor_i = clamp_floor(d, i);
+  LseAcc a{-INFINITY, 0.0};
+  for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
+    const double x = fmax(static_cast<double>(lk[j]), floor_i) + d.g[j];
+    lse_add(a, x);
+  }
+  // block merge (fixed order)
+  __shared__ double smx[kThreads / 32], ss[kThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    LseAcc b{__shfl_xor_sync(0xffffffffu, a.mx, o), __shfl_xor_sync(0xffffffffu, a.s, o)};
+    a = lse_merge(a, b);
+  }
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  if (l == 0) {
+    smx[w] = a.mx;
+    ss[w] = a.s;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  LseAcc r{-INFINITY, 0.0};
+  for (int q = 0; q < kThreads / 32; ++q) r = lse_merge(r, LseAcc{smx[q], ss[q]});
+  const double lse = r.mx + log(r.s);
+  const double fn = log(d.mu64[i]) - lse;
+  d.f_new[i] = fn;
+  if (s >= 2) d.row_err[i] = fabs(d.mu64[i] * expm1(d.f[i] - fn));
+  if (isnan(lse) || !(r.s > 0.0) || r.mx == -INFINITY) {
+    const bool plain = !(d.st->phase == 1 && d.log_domain);
+    if (plain && !isnan(lse)) {
+      atomicOr(&d.st->flags, kBZeroRow);
+      atomicMin(&d.st->zero_index, static_cast<int>(i));
+    } else {
+      atomicOr(&d.st->flags, kBNonFinite);
+    }
+  }
+}
+
+// Early-exit decision for sweep s−1 and f ← f_new.  One block.
+__global__ void row_decide_kernel(BDev d, int s) {
+  BState* st = d.st;
+  if (skip_sink(d)) return;
+  if (st->flags) {
+    if (threadIdx.x == 0) {
+      st->done = 1;
+      st->err_iter = st->iter;
+      st->err_sweep = s;
+    }
+    return;
+  }
+  __shared__ int conv;
+  if (s >= 2) {
+    double e = 0.0;
+    for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) e = fmax(e, d.row_err[i]);
+    for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) e = fmax(e, d.col_err[j]);
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t = fmax(t, sh[q]);
+      conv = t <= d.inner_tol;
+    }
+    __syncthreads();
+    if (conv) {
+      if (threadIdx.x == 0) {
+        st->sink_done = 1;
+        st->sweeps = s - 1;
+      }
+      return;
+    }
+  }
+  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) d.f[i] = d.f_new[i];
+  if (threadIdx.x == 0) st->sweeps = s;
+}
+
+// Column LSE partials: (128-column block, row chunk) per CTA.
+__global__ void __launch_bounds__(kThreads) col_lse_partial_kernel(BDev d, int rows_per_chunk,
+                                                                   int first_sweep) {
+  if (skip_sink(d)) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
+  const bool want_emax = first_sweep && d.st->phase == 1 && !d.log_domain;
+  LseAcc a[4] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}};
+  float emax[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (c0 < d.m) {
+    for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
+      const float4 v = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
+      const double fl = clamp_floor(d, i), fi = d.f[i];
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lse_add(a[q], fmax(static_cast<double>(vv[q]), fl) + fi);
+        if (want_emax) emax[q] = fmaxf(emax[q], vv[q] + d.rowmax[i]);
+      }
+    }
+  }
+  __shared__ double s_mx[kThreads / 32][kColWidth];
+  __shared__ double s_s[kThreads / 32][kColWidth];
+  __shared__ float s_e[kThreads / 32][kColWidth];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    s_mx[warp][lane * 4 + q] = a[q].mx;
+    s_s[warp][lane * 4 + q] = a[q].s;
+    s_e[warp][lane * 4 + q] = emax[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < kColWidth) {
+    const int c = threadIdx.x;
+    const int64_t col = static_cast<int64_t>(blockIdx.x) * kColWidth + c;
+    if (col < d.m) {
+      LseAcc r{-INFINITY, 0.0};
+      float e = -INFINITY;
+      for (int q = 0; q < kThreads / 32; ++q) {
+        r = lse_merge(r, LseAcc{s_mx[q][c], s_s[q][c]});
+        e = fmaxf(e, s_e[q][c]);
+      }
+      const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + col;
+      d.col_pm[o] = r.mx;
+      d.col_ps[o] = r.s;
+      d.col_pemax[o] = e;
+    }
+  }
+}
+
+__global__ void col_lse_combine_kernel(BDev d, int first_sweep) {
+  if (skip_sink(d)) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= d.m) return;
+  LseAcc r{-INFINITY, 0.0};
+  float e = -INFINITY;
+  for (int c = 0; c < d.chunks; ++c) {
+    const int64_t o = static_cast<int64_t>(c) * d.m + j;
+    r = lse_merge(r, LseAcc{d.col_pm[o], d.col_ps[o]});
+    e = fmaxf(e, d.col_pemax[o]);
+  }
+  const double lse = r.mx + log(r.s);
+  const double gn = log(d.nu64[j]) - lse;
+  d.g[j] = gn;
+  d.col_err[j] = fabs(exp(gn + lse) - d.nu64[j]);
+  const bool plain = !(d.st->phase == 1 && d.log_domain);
+  if (first_sweep && d.st->phase == 1 && !d.log_domain &&
+      static_cast<double>(e) - __int_as_float(d.st->gmax_bits) < kExpUnderflow)
+    atomicOr(&d.st->flags, kBDeadLine);
+  if (isnan(lse) || !(r.s > 0.0) || r.mx == -INFINITY) {
+    if (plain && !isnan(lse)) {
+      atomicOr(&d.st->flags, kBZeroCol);
+      atomicMin(&d.st->zero_index, static_cast<int>(j));
+    } else {
+      atomicOr(&d.st->flags, kBNonFinite);
+    }
+  }
+}
+
+__global__ void col_flag_kernel(BDev d, int s) {
+  BState* st = d.st;
+  if (skip_sink(d)) return;
+  if (st->flags) {
+    st->done = 1;
+    st->err_iter = st->iter;
+    st->err_sweep = s;
+  }
+}
+
+// π' = exp(max(LKs, floor) + f + g) (+ perturbation), fused sums.
+__global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_chunk) {
+  if (skip(d)) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
+  // Remark-1 perturbation applies to BPG iterations only (solvers.cpp:263-267).
+  const bool perturb = d.perturb > 0.0 && d.st->phase == 2;
+  const float keep = static_cast<float>(1.0 - d.perturb);
+  const float add = static_cast<float>(d.perturb * d.uniform_mass);
+  double cs[4] = {0.0, 0.0, 0.0, 0.0};
+  double diff = 0.0, old = 0.0;
+  const bool ok = c0 < d.m;
+  double gj[4] = {0.0, 0.0, 0.0, 0.0};
+  if (ok)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) gj[q] = (c0 + q < d.m) ? d.g[c0 + q] : 0.0;
+  for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
+    double rs = 0.0;
+    if (ok) {
+      const float4 v = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
+      const float4 pv = *reinterpret_cast<const float4*>(d.P + i * d.ld + c0);
+      const double fl = clamp_floor(d, i), fi = d.f[i];
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      const float po[4] = {pv.x, pv.y, pv.z, pv.w};
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (c0 + q < d.m) {
+          const double x = fmax(static_cast<double>(vv[q]), fl) + fi + gj[q];
+          float val = static_cast<float>(exp(x));
+          if (perturb) val = keep * val + add;
+          o[q] = val;
+          cs[q] += val;
+          rs += val;
+          const double df = static_cast<double>(val) - po[q];
+          diff += df * df;
+          old += static_cast<double>(po[q]) * po[q];
+        } else {
+          o[q] = 0.0f;
+        }
+      }
+      *reinterpret_cast<float4*>(d.P_new + i * d.ld + c0) = make_float4(o[0], o[1], o[2], o[3]);
+      if (d.P_aux_new)
+        *reinterpret_cast<float4*>(d.P_aux_new + i * d.ld + c0) =
+            make_float4(aux_of(o[0], d.aux_mode), aux_of(o[1], d.aux_mode),
+                        aux_of(o[2], d.aux_mode), aux_of(o[3], d.aux_mode));
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) d.row_sum[static_cast<int64_t>(blockIdx.x) * d.n + i] = rs;
+  }
+  __shared__ double s_c[kThreads / 32][kColWidth];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s_c[warp][lane * 4 + q] = cs[q];
+  diff = block_sum(diff);
+  old = block_sum(old);
+  __syncthreads();
+  if (threadIdx.x < kColWidth) {
+    const int64_t col = static_cast<int64_t>(blockIdx.x) * kColWidth + threadIdx.x;
+    if (col < d.m) {
+      double t = 0.0;
+      for (int q = 0; q < kThreads / 32; ++q) t += s_c[q][threadIdx.x];
+      d.col_sum[static_cast<int64_t>(blockIdx.y) * d.m + col] = t;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int64_t cta = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+    d.wpart[2 * cta] = diff;
+    d.wpart[2 * cta + 1] = old;
+  }
+}
+
+// Record k, stop rule, phase logic.  One block.
+__global__ void breg_finalize_kernel(BDev d, int tail) {
+  BState* st = d.st;
+  if (tail ? st->flags != 0 : skip(d)) return;
+  const int k = tail ? st->iter - 1 : st->iter;
+  auto slot = [&](int it) { return it <= d.max_rec ? it : d.max_rec + 1; };
+  double obj = 0.0;
+  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) obj += d.obj_part[i];
+  obj = block_sum(obj);
+  if (tail) {
+    if (threadIdx.x == 0) d.rec[slot(k)].obj = obj;
+    return;
+  }
+  double rowdev = 0.0, coldev = 0.0, diff = 0.0, old = 0.0;
+  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < d.colblocks; ++b) s += d.row_sum[static_cast<int64_t>(b) * d.n + i];
+    rowdev += (s - d.mu64[i]) * (s - d.mu64[i]);
+  }
+  for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < d.chunks; ++c) s += d.col_sum[static_cast<int64_t>(c) * d.m + j];
+    coldev += (s - d.nu64[j]) * (s - d.nu64[j]);
+  }
+  const int64_t ctas = static_cast<int64_t>(d.chunks) * d.colblocks;
+  for (int64_t c = threadIdx.x; c < ctas; c += blockDim.x) {
+    diff += d.wpart[2 * c];
+    old += d.wpart[2 * c + 1];
+  }
+  rowdev = block_sum(rowdev);
+  coldev = block_sum(coldev);
+  diff = block_sum(diff);
+  old = block_sum(old);
+  if (threadIdx.x != 0) return;
+  if (k >= 2) d.rec[slot(k - 1)].obj = obj;
+  BRecord& r = d.rec[slot(k)];
+  r.rel = sqrt(diff) / sqrt(old);
+  r.infeas = sqrt(coldev) / static_cast<double>(d.m) + sqrt(rowdev) / static_cast<double>(d.n);
+  r.elapsed = 1e-9 * static_cast<double>(globaltimer() - st->t0);
+  r.phase = st->phase;
+  r.sweeps = st->sweeps;
+  const bool conv = dev::stop_rule(r.rel, d.rel_tol);
+  st->iter = k + 1;
+  st->gmax_bits = 0;
+  if (st->phase == 1) {
+    if (conv || k >= d.budget1) {
+      st->used1 = k;
+      st->conv1 = conv;
+      if (!d.has_phase2 || d.max_iters - k < 1) {
+        st->done = 1;
+        st->converged = conv;
+      } else {
+        st->phase = 2;
+      }
+    }
+  } else if (conv) {
+    st->done = 1;
+    st->converged = 1;
+  }
+  if (k >= d.max_iters) st->done = 1;
+}
+
+__global__ void breg_reset_kernel(BState* st, int phase) {
+  st->done = 0;
+  st->flags = 0;
+  st->iter = 1;
+  st->err_iter = 0;
+  st->converged = 0;
+  st->zero_index = 0x7fffffff;
+  st->err_sweep = 0;
+  st->phase = phase;
+  st->used1 = 0;
+  st->conv1 = 0;
+  st->sink_done = 0;
+  st->sweeps = 0;
+  st->gmax_bits = 0;
+  st->t0 = globaltimer();
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  GWB_CUDA(cudaMalloc(&p, count * sizeof(T) + 256));
+  GWB_CUDA(cudaMemset(p, 0, count * sizeof(T) + 256));
+  GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // see solver.cu dalloc
+  return static_cast<T*>(p);
+}
+
+struct DevFree {
+  void operator()(void* p) const {
+    if (p) cudaFree(p);
+  }
+};
+
+// ---------------------------------------------------------------------------
+class BregmanEngine {
+ public:
+  BregmanEngine(int device, int64_t n, int64_t m, const gwb_config& cfg, int algo)
+      : dev_(device), n_(n), m_(m), ldn_(round_up(n, 32)), ldm_(round_up(m, 32)), cfg_(cfg),
+        algo_(algo) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    const size_t nm = static_cast<size_t>(n_) * ldm_;
+    Dx_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_));
+    Dy_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
+    Dx_lo_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_));
+    Dy_lo_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
+    for (int q = 0; q < 2; ++q) {
+      P_[q] = keep(dalloc<float>(nm));
+      Pa_[q] = keep(dalloc<float>(nm));
+    }
+    Vt_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
+    Vta_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
+    G_ = keep(dalloc<float>(nm));
+    mu_ = keep(dalloc<double>(n_));
+    nu_ = keep(dalloc<double>(m_));
+    f_ = keep(dalloc<double>(n_));
+    fn_ = keep(dalloc<double>(n_));
+    g_ = keep(dalloc<double>(m_));
+    rowmax_ = keep(dalloc<float>(n_));
+    row_err_ = keep(dalloc<double>(n_));
+    col_err_ = keep(dalloc<double>(m_));
+    colblocks_ = static_cast<int>((m_ + kColWidth - 1) / kColWidth);
+    chunks_ = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>((n_ + 63) / 64, (4 * 148 + colblocks_ - 1) / colblocks_)));
+    col_pm_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_ps_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_pe_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
+    col_sum_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
+    row_sum_ = keep(dalloc<double>(static_cast<size_t>(colblocks_) * n_));
+    obj_part_ = keep(dalloc<double>(n_));
+    wpart_ = keep(dalloc<double>(2 * static_cast<size_t>(chunks_) * colblocks_));
+    st_ = keep(dalloc<BState>(1));
+    rec_ = keep(dalloc<BRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
+  }
+  ~BregmanEngine() {
+    cudaSetDevice(dev_);
+    cudaStreamSynchronize(s_);
+    for (auto* p : plans_) gemm_plan_destroy(p);
+    for (void* p : bufs_) cudaFree(p);
+    cudaStreamDestroy(s_);
+  }
+
+  void load(const double* dx, const double* dy, const double* mu, const double* nu,
+            const double* initial) {
+    const int64_t big = std::max(std::max(n_ * n_, m_ * m_), n_ * m_);
+    std::unique_ptr<void, DevFree> stage(dalloc<double>(static_cast<size_t>(big)));
+    double* sp = static_cast<double*>(stage.get());
+    GWB_CUDA(cudaMemcpyAsync(sp, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, s_));
+    launch_colmajor64_to_rowmajor32(sp, n_, n_, Dx_, ldn_, s_);
+    launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_lo_, 2, s_);
+    GWB_CUDA(cudaMemcpyAsync(sp, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, s_));
+    launch_colmajor64_to_rowmajor32(sp, m_, m_, Dy_, ldm_, s_);
+    launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
+    GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
+    if (initial) {
+      GWB_CUDA(cudaMemcpyAsync(sp, initial, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, s_));
+      launch_colmajor64_to_rowmajor32(sp, n_, m_, P_[0], ldm_, s_);
+    } else {
+      std::vector<float> mu32(n_), nu32(m_);
+      for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
+      for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
+      std::unique_ptr<void, DevFree> a(dalloc<float>(n_)), b(dalloc<float>(m_));
+      GWB_CUDA(cudaMemcpyAsync(a.get(), mu32.data(), 4 * n_, cudaMemcpyHostToDevice, s_));
+      GWB_CUDA(cudaMemcpyAsync(b.get(), nu32.data(), 4 * m_, cudaMemcpyHostToDevice, s_));
+      launch_product_coupling(static_cast<float*>(a.get()), static_cast<float*>(b.get()), n_, m_,
+                              ldm_, P_[0], s_);
+      GWB_CUDA(cudaStreamSynchronize(s_));
+    }
+    launch_tf32_aux(P_[0], n_, m_, ldm_, Pa_[0], 2, s_);
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    build_plans();
+  }
+
+  // Runs the whole solve; returns iterations used.
+  void run(gwb_observer observer, void* user, std::vector<double>* host_pi) {
+    const int budget1 = algo_ == GWB_EBPG ? cfg_.max_iters
+                        : algo_ == GWB_BPG ? 0
+                                           : std::min(cfg_.switch_iters, cfg_.max_iters);
+    breg_reset_kernel<<<1, 1, 0, s_>>>(st_, budget1 >= 1 ? 1 : 2);
+    GWB_CUDA(cudaGetLastError());
+    BDev d = view(0);
+    d.budget1 = budget1;
+    d.has_phase2 = algo_ != GWB_EBPG;
+    base_ = d;
+    const int rows_per_chunk = static_cast<int>((n_ + chunks_ - 1) / chunks_);
+    for (int k = 1; k <= cfg_.max_iters; ++k) {
+      const int q = (k - 1) & 1;
+      BDev v = base_;
+      rebind(v, q);
+      GWB_CUDA(gemm_launch(g1_[q], s_));
+      GWB_CUDA(gemm_launch(g2_, s_));
+      form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 0);
+      form_check_kernel<<<1, 1024, 0, s_>>>(v);
+      for (int sw = 1; sw <= cfg_.inner_iters; ++sw) {
+        row_lse_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, sw);
+        row_decide_kernel<<<1, 1024, 0, s_>>>(v, sw);
+        dim3 grid(static_cast<unsigned>(colblocks_), static_cast<unsigned>(chunks_));
+        col_lse_partial_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk, sw == 1);
+        col_lse_combine_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(v, sw == 1);
+        col_flag_kernel<<<1, 1, 0, s_>>>(v, sw);
+        if (cfg_.inner_iters > 64 && (sw % 32) == 0) {
+          // Long inner loops: stop enqueueing once the device has converged.
+          BState h;
+          GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
+          GWB_CUDA(cudaStreamSynchronize(s_));
+          if (h.done || h.sink_done) break;
+        }
+      }
+      dim3 grid(static_cast<unsigned>(colblocks_), static_cast<unsigned>(chunks_));
+      write_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk);
+      breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 0);
+      GWB_CUDA(cudaGetLastError());
+      BState h;
+      GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
+      GWB_CUDA(cudaStreamSynchronize(s_));
+      if (h.flags) break;
+      if (observer && h.iter - 1 == k) {
+        to_host(P_[k & 1], 1, host_pi);
+        if (observer(user, k, host_pi->data(), nullptr, n_, m_) != 0)
+          api_fail(GWB_ERR_RUNTIME, "observer requested abort");
+      }
+      if (h.done) break;
+    }
+  }
+
+  BState status() {
+    BState h;
+    GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    return h;
+  }
+
+  // Objective of the last record: one more chain on the final π.
+  void tail(int used) {
+    const int q = used & 1;
+    BDev v = base_;
+    rebind(v, q);
+    GWB_CUDA(gemm_launch(g1t_[q], s_));
+    GWB_CUDA(gemm_launch(g2t_, s_));
+    form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 1);
+    breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 1);
+    GWB_CUDA(cudaGetLastError());
+  }
+
+  std::vector<BRecord> records(int count) {
+    std::vector<BRecord> r(static_cast<size_t>(count) + 1);
+    GWB_CUDA(cudaMemcpyAsync(r.data(), rec_, sizeof(BRecord) * (count + 1), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    return r;
+  }
+
+  // Final π to host fp64 column-major with exact fp64 column re-projection
+  // onto `col_target` (the reference's last Sinkhorn step is a column scaling).
+  void output(int used, double* out, const std::vector<double>& col_target) {
+    std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_)),
+        w(dalloc<double>(std::max(n_, m_))), t(dalloc<double>(m_));
+    GWB_CUDA(cudaMemcpyAsync(t.get(), col_target.data(), sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
+    launch_rowmajor32_to_colmajor64(P_[used & 1], n_, m_, ldm_, static_cast<double*>(o.get()), 1,
+                                    static_cast<double*>(t.get()), static_cast<double*>(w.get()), s_);
+    GWB_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * n_ * m_, cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+  }
+
+ private:
+  template <class T>
+  T* keep(T* p) {
+    bufs_.push_back(p);
+    return p;
+  }
+
+  void to_host(float* P, int, std::vector<double>* out) {
+    out->resize(static_cast<size_t>(n_) * m_);
+    std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_));
+    launch_rowmajor32_to_colmajor64(P, n_, m_, ldm_, static_cast<double*>(o.get()), -1, nullptr,
+                                    nullptr, s_);
+    GWB_CUDA(cudaMemcpyAsync(out->data(), o.get(), sizeof(double) * n_ * m_, cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+  }
+
+  BDev view(int q) {
+    BDev d;
+    std::memset(&d, 0, sizeof(d));
+    d.n = n_;
+    d.m = m_;
+    d.ld = ldm_;
+    d.G = G_;
+    d.aux_mode = 2;
+    d.mu64 = mu_;
+    d.nu64 = nu_;
+    d.f = f_;
+    d.f_new = fn_;
+    d.g = g_;
+    d.rowmax = rowmax_;
+    d.row_err = row_err_;
+    d.col_err = col_err_;
+    d.col_pm = col_pm_;
+    d.col_ps = col_ps_;
+    d.col_pemax = col_pe_;
+    d.col_sum = col_sum_;
+    d.row_sum = row_sum_;
+    d.obj_part = obj_part_;
+    d.wpart = wpart_;
+    d.chunks = chunks_;
+    d.colblocks = colblocks_;
+    d.eb_scale = static_cast<float>(2.0 / cfg_.epsilon_reg);
+    d.bp_scale = static_cast<float>(2.0 * cfg_.step);
+    d.log_domain = cfg_.log_domain;
+    d.perturb = cfg_.perturbation;
+    d.uniform_mass = 1.0 / (static_cast<double>(n_) * static_cast<double>(m_));
+    d.max_iters = cfg_.max_iters;
+    d.rel_tol = cfg_.rel_tol;
+    d.inner_tol = cfg_.inner_tol;
+    d.st = st_;
+    d.rec = rec_;
+    d.max_rec = cfg_.max_iters;
+    rebind(d, q);
+    return d;
+  }
+
+  void rebind(BDev& d, int q) {
+    d.P = P_[q];
+    d.P_new = P_[1 - q];
+    d.P_aux_new = Pa_[1 - q];
+  }
+
+  void build_plans() {
+    auto g1 = [&](int q, const int* skip) {
+      GemmDesc d;
+      d.M = m_; d.N = n_; d.K = m_;
+      d.a = Dy_; d.a_lo = Dy_lo_; d.lda = ldm_;
+      d.b = P_[q]; d.b_lo = Pa_[q]; d.ldb = ldm_;
+      d.c = Vt_; d.c_aux = Vta_; d.ldc = ldn_; d.aux_mode = 2;
+      d.skip = skip;
+      d.three_pass = true;
+      GemmPlan* p = gemm_plan_create(d);
+      plans_.push_back(p);
+      return p;
+    };
+    auto g2 = [&](const int* skip) {
+      GemmDesc d;
+      d.M = n_; d.N = m_; d.K = n_;
+      d.a = Dx_; d.a_lo = Dx_lo_; d.lda = ldn_;
+      d.b = Vt_; d.b_lo = Vta_; d.ldb = ldn_;
+      d.c = G_; d.ldc = ldm_;
+      d.skip = skip;
+      d.three_pass = true;
+      GemmPlan* p = gemm_plan_create(d);
+      plans_.push_back(p);
+      return p;
+    };
+    for (int q = 0; q < 2; ++q) {
+      g1_[q] = g1(q, &st_->done);
+      g1t_[q] = g1(q, &st_->flags);
+    }
+    g2_ = g2(&st_->done);
+    g2t_ = g2(&st_->flags);
+  }
+
+  int dev_;
+  int64_t n_, m_, ldn_, ldm_;
+  gwb_config cfg_;
+  int algo_;
+  cudaStream_t s_ = nullptr;
+  std::vector<void*> bufs_;
+  std::vector<GemmPlan*> plans_;
+  float *Dx_, *Dy_, *Dx_lo_, *Dy_lo_, *P_[2], *Pa_[2], *Vt_, *Vta_, *G_, *rowmax_;
+  double *mu_, *nu_, *f_, *fn_, *g_, *row_err_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
+      *row_sum_, *obj_part_, *wpart_;
+  float* col_pe_;
+  int chunks_ = 1, colblocks_ = 1;
+  BState* st_;
+  BRecord* rec_;
+  BDev base_;
+  GemmPlan *g1_[2], *g1t_[2], *g2_, *g2t_;
+};
+
+// Error precedence and wrapping of ebpg_solve / bpg_solve (solvers.cpp:246-261,
+// :312-336): eBPG rethrows only ZeroSumLineError; BPG wraps both.
+void raise_breg(const BState& s, bool log_domain) {
+  const int it = s.err_iter;
+  const bool bpg_phase = s.phase == 2;
+  const char* solver = bpg_phase ? "bpg" : "ebpg";
+  char detail[400];
+  if (s.flags & kBOverflow) api_numerical("bpg", it, "exp overflow; reduce step");
+  if (s.flags & kBDeadLine)
+    api_numerical("ebpg", it,
+                  "kernel line underflowed to zero; increase eps or enable the log-domain solver");
+  if (s.flags & (kBZeroRow | kBZeroCol)) {
+    std::snprintf(detail, sizeof(detail), "%s %d has nonpositive sum; cannot rescale",
+                  (s.flags & kBZeroRow) ? "row" : "column", s.zero_index);
+    api_numerical(solver, it, detail);
+  }
+  // non-finite entries after a sweep (projections.cpp:104-107 / 151-154)
+  const bool logd = !bpg_phase && log_domain;
+  std::snprintf(detail, sizeof(detail),
+                "numerical instability in %s at iteration %d: non-finite entries after scaling sweep",
+                logd ? "sinkhorn-log" : "sinkhorn", s.err_sweep);
+  if (bpg_phase) api_numerical("bpg", it, detail);
+  api_numerical(logd ? "sinkhorn-log" : "sinkhorn", s.err_sweep,
+                "non-finite entries after scaling sweep");
+}
+
+}  // namespace
+
+void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_t n,
+                   const double* dy, int64_t m, const double* mu, const double* nu,
+                   const double* initial, gwb_observer observer, void* user, double* out_final,
+                   gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
+                   int32_t* iterations_used) {
+  if (cfg->record_residual)
+    api_fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
+  if (trace && trace_cap < cfg->max_iters) api_fail(GWB_ERR_CAPACITY, "trace capacity < max_iters");
+  if (initial) {
+    const size_t len = static_cast<size_t>(n) * m;
+    for (size_t k = 0; k < len; ++k)
+      if (!(initial[k] >= 0.0) || !std::isfinite(initial[k]))
+        api_fail(GWB_ERR_INVALID, "initial coupling must be finite and nonnegative");
+  }
+  const int device = api_device();
+  // BPG step-size warning (solvers.cpp:226-234), only if a BPG phase can run.
+  const bool bpg_may_run =
+      algo == GWB_BPG || (algo == GWB_HBPG && cfg->max_iters >= 1);
+  BregmanEngine eng(device, n, m, *cfg, algo);
+  eng.load(dx, dy, mu, nu, initial);
+  std::vector<double> host_pi;
+  eng.run(observer, user, &host_pi);
+  const BState s = eng.status();
+  if (s.flags) raise_breg(s, cfg->log_domain != 0);
+  const int used = s.iter - 1;
+  if (bpg_may_run && (algo == GWB_BPG || s.used1 < used || s.phase == 2) && !cfg->quiet) {
+    const double lip = device_lipschitz_bound(dx, n, dy, m);
+    if (lip > 0.0 && cfg->step > 1.0 / lip)
+      std::fprintf(stderr,
+                   "bpg: step %g exceeds sigma/L_f = %g; descent is not guaranteed at this step "
+                   "size\n",
+                   cfg->step, 1.0 / lip);
+  }
+  eng.tail(used);
+  const std::vector<BRecord> r = eng.records(used);
+  if (trace) {
+    for (int k = 1; k <= used; ++k) {
+      gwb_record& o = trace[k - 1];
+      std::memset(&o, 0, sizeof(o));
+      o.iter = k;
+      o.objective = -r[k].obj;
+      o.marginal_infeasibility = r[k].infeas;
+      o.rel_change = r[k].rel;
+      o.elapsed_seconds = r[k].elapsed;
+      o.phase = algo == GWB_HBPG ? r[k].phase : 0;
+    }
+  }
+  if (n_records) *n_records = trace ? used : 0;
+  if (converged) *converged = s.converged;
+  if (iterations_used) *iterations_used = used;
+  // Column sums of the returned coupling: ν after a Sinkhorn column step, or
+  // (1−p)ν + p/m after a perturbed BPG step.
+  const bool last_bpg = used >= 1 && r[used].phase == 2;
+  const double p = last_bpg ? cfg->perturbation : 0.0;
+  std::vector<double> target(m);
+  for (int64_t j = 0; j < m; ++j) target[j] = (1.0 - p) * nu[j] + p / static_cast<double>(m);
+  eng.output(used, out_final, target);
+}
+
+}  // namespace gwb

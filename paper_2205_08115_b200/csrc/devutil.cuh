@@ -1,0 +1,125 @@
+// devutil.cuh — device helpers shared by the projection / Sinkhorn kernels:
+// TF32 operand splitting, %globaltimer, and the (max, Σ v·e^{x−max}) online
+// accumulator with deterministic (fixed-order) warp and block reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+namespace gwb {
+namespace dev {
+
+// Stop rule rel_change ≤ rel_tol (solvers.cpp:208, :284, :354) evaluated on
+// fp32 iterates.  An fp32 iterate can become exactly stationary
+// (rel_change == 0) where the fp64 reference still moves by ~1e-14; that
+// only counts as convergence when rel_tol is above fp32 resolution.
+constexpr double kFp32Resolution = 1e-7;
+__device__ __forceinline__ bool stop_rule(double rel, double rel_tol) {
+  return rel <= rel_tol && (rel > 0.0 || rel_tol >= kFp32Resolution);
+}
+
+__device__ __forceinline__ float trunc_tf32(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Operand copy for the next GEMM: 1 → TF32 round-to-nearest-away (unbiased
+// 1xTF32 input), 2 → residual x − trunc_tf32(x) (3xTF32 low part).
+__device__ __forceinline__ float aux_of(float x, int mode) {
+  return mode == 1 ? rna_tf32(x) : x - trunc_tf32(x);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// (max, Σ v·e^{x−max}) online accumulator.
+struct MaxSum {
+  float mx;
+  float s;
+};
+
+__device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) {
+  if (e > a.mx) {
+    a.s = a.s * __expf(a.mx - e) + v;
+    a.mx = e;
+  } else {
+    a.s += v * __expf(e - a.mx);
+  }
+}
+
+__device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) {
+  if (b.mx == -INFINITY) return a;
+  if (a.mx == -INFINITY) return b;
+  const float M = fmaxf(a.mx, b.mx);
+  MaxSum r;
+  r.mx = M;
+  r.s = a.s * __expf(a.mx - M) + b.s * __expf(b.mx - M);
+  // NaN propagation: any NaN max poisons the sum.
+  if (isnan(a.mx) || isnan(b.mx)) {
+    r.mx = NAN;
+    r.s = NAN;
+  }
+  return r;
+}
+
+__device__ __forceinline__ MaxSum warp_merge(MaxSum a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MaxSum b;
+    b.mx = __shfl_xor_sync(0xffffffffu, a.mx, o);
+    b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
+    a = ms_merge(a, b);
+  }
+  return a;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide (max,sum) merge + up to 5 fp64 sums; result broadcast to all.
+template <int kThreads, int kSums>
+__device__ void block_reduce(MaxSum& ms, double (&sums)[kSums]) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ float s_mx[kWarps], s_s[kWarps];
+  __shared__ double s_d[kSums][kWarps];
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  ms = warp_merge(ms);
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = warp_sum(sums[k]);
+  if (l == 0) {
+    s_mx[w] = ms.mx;
+    s_s[w] = ms.s;
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) s_d[k][w] = sums[k];
+  }
+  __syncthreads();
+  MaxSum r{-INFINITY, 0.f};
+  double t[kSums];
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) t[k] = 0.0;
+  for (int q = 0; q < kWarps; ++q) {  // fixed order ⇒ deterministic
+    r = ms_merge(r, MaxSum{s_mx[q], s_s[q]});
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) t[k] += s_d[k][q];
+  }
+  ms = r;
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = t[k];
+  __syncthreads();
+}
+
+}  // namespace dev
+}  // namespace gwb

@@ -34,7 +34,10 @@ template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   GWB_CUDA(cudaMalloc(&p, count * sizeof(T) + 256));
+  // The engines run on non-blocking streams, which do not order against the
+  // legacy stream cudaMemset uses: wait for the zero-fill before returning.
   GWB_CUDA(cudaMemset(p, 0, count * sizeof(T) + 256));
+  GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   return static_cast<T*>(p);
 }
 
