@@ -1,16 +1,22 @@
 // gemm.cu — tcgen05 / TMEM / TMA GEMM for sm_100a, kind::tf32 with optional
 // 3xTF32 split-precision passes (see gemm.cuh).
 //
-// Structure (one CTA per 128×256 output tile, 576 threads, 1 CTA / SM):
-//   warp 0   : TMA producer — 4-stage ring of {A 128×32, B 256×32} fp32 tiles
-//              in the 128-byte-swizzled K-major layout, mbarrier full/empty
-//   warp 1   : TMEM allocator + MMA issuer — one elected lane issues
-//              tcgen05.mma.kind::tf32 (M=128, N=256, K=8) ×4 per stage into
-//              one of two 256-column TMEM accumulators (512 columns total)
-//   warps 2-17: epilogue — drain each finished K-chunk with tcgen05.ld
-//              32x32b into fp32 registers (RN adds), then scale and store
+// One CTA PAIR (cluster of 2, cta_group::2) per 256×256 output tile; each CTA
+// owns 128 rows of the tile (its TMEM lanes) and loads its half of A (128
+// rows) and its half of B (128 of the 256 N rows), so per CTA and k-block the
+// TMA writes and the MMA reads 32 KB of shared memory instead of 48 KB.
+//   warp 0    : TMA producer (both CTAs) — 6-stage ring of {A 128×32, B 128×32}
+//               fp32 tiles, 128-B swizzle; completion counted on the LEADER's
+//               full barrier (cp.async.bulk.tensor.cta_group::2)
+//   warp 1    : TMEM allocation (cta_group::2, 512 columns) and, in the leader
+//               only, the single-thread tcgen05.mma.cta_group::2.kind::tf32
+//               issuer (M=256, N=256, K=8, 4 per stage); commits multicast to
+//               both CTAs' empty / tmem-full barriers
+//   warps 2-17: epilogue (both CTAs) — drain each finished K-chunk from TMEM
+//               (tcgen05.ld 32x32b) into fp32 registers (RN adds), then scale
+//               and store; drain completion is reported to the leader
 // Tiles are rasterised in groups of kGroupM row-blocks so concurrently
-// resident CTAs share A and B panels in L2.
+// resident pairs share A and B panels in L2.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -26,18 +32,20 @@ namespace gwb {
 
 namespace {
 
-constexpr int kBM = 128;
-constexpr int kBN = 256;
-constexpr int kBK = 32;  // 32 fp32 = 128 B = one swizzle row
-constexpr int kStages = 4;
+constexpr int kBM = 128;                   // rows per CTA
+constexpr int kPairM = 2 * kBM;            // rows per CTA pair (MMA M)
+constexpr int kBN = 256;                   // columns per tile (MMA N)
+constexpr int kHalfN = kBN / 2;            // B rows loaded per CTA
+constexpr int kBK = 32;                    // 32 fp32 = 128 B = one swizzle row
+constexpr int kStages = 6;
 constexpr int kGroupM = 8;
-constexpr int kEpiWarps = 16;             // 4 lane quadrants × 4 column slices
-constexpr int kSliceCols = kBN / 4;       // 64 accumulator columns per thread
+constexpr int kEpiWarps = 16;              // 4 lane quadrants × 4 column slices
+constexpr int kSliceCols = kBN / 4;        // 64 accumulator columns per thread
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kABytes = kBM * kBK * 4;
-constexpr uint32_t kBBytes = kBN * kBK * 4;
-constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr uint32_t kTmemCols = 2 * kBN;   // double-buffered accumulator
+constexpr uint32_t kBBytes = kHalfN * kBK * 4;
+constexpr uint32_t kStageBytes = kABytes + kBBytes;  // per CTA
+constexpr uint32_t kTmemCols = 2 * kBN;    // double-buffered accumulator
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
 struct __align__(64) GemmParams {
@@ -47,7 +55,7 @@ struct __align__(64) GemmParams {
   int32_t passes;
   int32_t a_sel[3];
   int32_t b_sel[3];
-  int32_t tiles_m, tiles_n;
+  int32_t tiles_m, tiles_n;  // tiles_m counts 256-row pair tiles
   int32_t chunk;  // k-blocks accumulated in TMEM before promotion to registers
   float* c;
   float* c_aux;
@@ -73,7 +81,7 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // restarts accumulation every `chunk` k-blocks in one of two TMEM buffers
 // and the epilogue warps add each finished chunk into fp32 registers with
 // round-to-nearest adds ("promotion"), bounding the bias by the chunk length.
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ GemmParams p) {
   if (p.skip != nullptr && *p.skip != 0) return;
 
@@ -84,20 +92,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sB = reinterpret_cast<float*>(smem + kStages * kABytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // [2] chunk accumulated
-  uint64_t* tempty = tfull + 2;       // [2] chunk drained by the epilogue
+  uint64_t* tfull = empty + kStages;  // [2] chunk accumulated (per CTA)
+  uint64_t* tempty = tfull + 2;       // [2] chunk drained (leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = ptx::warp_idx();
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
 
-  // Grouped rasterisation: consecutive blocks sweep kGroupM row tiles.
-  const int bid = blockIdx.x;
+  // Grouped rasterisation over pair tiles.
+  const int pid = blockIdx.x >> 1;
   const int per_group = kGroupM * p.tiles_n;
-  const int group = bid / per_group;
+  const int group = pid / per_group;
   const int first_m = group * kGroupM;
   const int gsize = min(p.tiles_m - first_m, kGroupM);
-  const int in_group = bid % per_group;
+  const int in_group = pid % per_group;
   const int tm = first_m + in_group % gsize;
   const int tn = in_group / gsize;
 
@@ -110,13 +120,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], kEpiWarps);
+      ptx::mbar_init(&tempty[b], 2 * kEpiWarps);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc_2sm<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -124,6 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = p.passes * kblocks;
   const int chunk = p.chunk;
   const int nchunks = (total + chunk - 1) / chunk;
+  const int a_row = tm * kPairM + static_cast<int>(rank) * kBM;
+  const int b_row = tn * kBN + static_cast<int>(rank) * kHalfN;
 
   if (warp == 0) {
     if (ptx::elect_one()) {
@@ -133,16 +145,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&empty[s], ph ^ 1);
         const int pass = it / kblocks;
         const int kb = it - pass * kblocks;
-        ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
-        ptx::tma_load_2d(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], &full[s], kb * kBK,
-                         tm * kBM);
-        ptx::tma_load_2d(sB + s * (kBN * kBK), &p.b_map[p.b_sel[pass]], &full[s], kb * kBK,
-                         tn * kBN);
+        const uint32_t fbar = ptx::mapa(&full[s], 0);
+        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kBK, a_row);
+        ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kBK,
+                             b_row);
       }
     }
   } else if (warp == 1) {
-    if (ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_tf32(kBM, kBN);
+    if (leader && ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_tf32(kPairM, kBN);
       for (int c = 0; c < nchunks; ++c) {
         const int b = c & 1;
         ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
@@ -156,21 +168,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
-          const uint32_t b_base = ptx::smem_u32(sB + s * (kBN * kBK));
+          const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN * kBK));
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
-            ptx::mma_tf32(acc, ptx::umma_desc_sw128(a_base + k * 32),
-                          ptx::umma_desc_sw128(b_base + k * 32), idesc,
-                          (it != it0 || k != 0) ? 1u : 0u);
+            ptx::mma_tf32_2sm(acc, ptx::umma_desc_sw128(a_base + k * 32),
+                              ptx::umma_desc_sw128(b_base + k * 32), idesc,
+                              (it != it0 || k != 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[s]);
+          ptx::mma_commit_2sm(&empty[s], 0x3);
         }
-        ptx::mma_commit(&tfull[b]);
+        ptx::mma_commit_2sm(&tfull[b], 0x3);
       }
     }
   } else {
     // Epilogue: warp w (2..17) owns TMEM lanes 32·(w%4).. and columns
-    // [64·slice, 64·slice + 64) of the 128×256 tile.
+    // [64·slice, 64·slice + 64) of this CTA's 128×256 accumulator.
     const uint32_t quad = warp & 3;
     const uint32_t slice = (warp - 2) >> 2;
     const uint32_t lane_base = quad * 32;
@@ -178,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float acc[kSliceCols];
 #pragma unroll
     for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+    const uint32_t tempty_leader[2] = {ptx::mapa(&tempty[0], 0), ptx::mapa(&tempty[1], 0)};
     for (int c = 0; c < nchunks; ++c) {
       const int b = c & 1;
       ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
@@ -193,9 +206,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
     }
-    const int row = tm * kBM + static_cast<int>(lane_base + lane);
+    const int row = a_row + static_cast<int>(lane_base + lane);
     if (row < p.M) {
       const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
       float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
@@ -231,10 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem);
+    ptx::tmem_dealloc_2sm<kTmemCols>(tmem);
   }
 }
 
@@ -305,9 +318,9 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.N = static_cast<int32_t>(d.N);
   g.K = static_cast<int32_t>(d.K);
   g.a_map[0] = make_map(d.a, d.M, d.K, d.lda, kBM);
-  g.b_map[0] = make_map(d.b, d.N, d.K, d.ldb, kBN);
+  g.b_map[0] = make_map(d.b, d.N, d.K, d.ldb, kHalfN);
   g.a_map[1] = d.a_lo ? make_map(d.a_lo, d.M, d.K, d.lda, kBM) : g.a_map[0];
-  g.b_map[1] = d.b_lo ? make_map(d.b_lo, d.N, d.K, d.ldb, kBN) : g.b_map[0];
+  g.b_map[1] = d.b_lo ? make_map(d.b_lo, d.N, d.K, d.ldb, kHalfN) : g.b_map[0];
   g.passes = 1;
   g.a_sel[0] = 0;
   g.b_sel[0] = 0;
@@ -325,7 +338,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       ++g.passes;
     }
   }
-  g.tiles_m = static_cast<int32_t>((d.M + kBM - 1) / kBM);
+  g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
   g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
   g.c = d.c;
@@ -335,7 +348,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.row_scale = d.row_scale;
   g.col_scale = d.col_scale;
   g.skip = d.skip;
-  p->grid = g.tiles_m * g.tiles_n;
+  p->grid = 2 * g.tiles_m * g.tiles_n;  // two CTAs (one cluster) per tile
   p->flops = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
   return p;
 }
