@@ -37,10 +37,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=20000)
-    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2"])
     ap.add_argument("--e2e-iters", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=2500)
     return ap.parse_args()
 
@@ -209,26 +210,20 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
-def run_ours(args, world, rank, local, dist):
-    import torch
-    import paper_2205_08115_b200 as gw
-    from paper_2205_08115_b200 import abi
+PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4}
+PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2"}
+# tensor passes per chain GEMM for 0/1 structure matrices, and the MMA kind
+PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16")}
 
-    torch.cuda.set_device(local)
-    lib = abi.load()
-    n = args.n
-    edges, tgt, perm = build_instance(n)
-    dx = dense_dev(torch, n, edges)
-    dy = dense_dev(torch, n, tgt)
-    mu = torch.full((n,), 1.0 / n, device="cuda", dtype=torch.float32)
-    nu = mu.clone()
 
-    prec = {"auto": abi.PREC_AUTO, "tf32": abi.PREC_TF32, "3xtf32": abi.PREC_3XTF32}[args.precision]
+def time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks=None):
+    """Device-resident BAPG: `steps` iterations timed with CUDA events on the
+    session stream (eager launches, per-kernel-class events)."""
     cfg = abi.default_config(rho=0.1, max_iters=args.steps + args.warmup + 4, rel_tol=1e-30,
                              precision=prec)
     st = abi.Status()
     sess = C.c_void_p()
-    rc = lib.gwb_session_create(C.byref(cfg), n, n, local, C.byref(sess), C.byref(st))
+    lib.gwb_session_create(C.byref(cfg), n, n, local, C.byref(sess), C.byref(st))
     abi.raise_for(st)
     torch.cuda.synchronize()
     lib.gwb_session_load_device(sess, dx.data_ptr(), dx.shape[1], dy.data_ptr(), dy.shape[1],
@@ -241,60 +236,100 @@ def run_ours(args, world, rank, local, dist):
     stream = torch.cuda.ExternalStream(sp.value)
     rprec, flops_it = C.c_int32(0), C.c_double(0)
     lib.gwb_session_info(sess, C.byref(rprec), C.byref(flops_it), C.byref(st))
-
-    launches = C.c_int64(-1)  # eager with per-kernel-class CUDA events
+    launches = C.c_int64(-1)
     lib.gwb_session_iterate(sess, args.warmup, None, C.byref(launches), C.byref(st))
     abi.raise_for(st)
     gms, gcnt = C.c_double(0), C.c_int64(0)
-    lib.gwb_session_kernel_ms(sess, 0, C.byref(gms), C.byref(gcnt), C.byref(st))  # reset marks
-    lib.gwb_session_kernel_ms(sess, 1, C.byref(gms), C.byref(gcnt), C.byref(st))
+    lib.gwb_session_kernel_ms(sess, 0, C.byref(gms), C.byref(gcnt), C.byref(st))  # drop warm-up marks
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = ClockSampler(local)
-    with clocks:
-        with torch.cuda.stream(stream):
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            ev0.record(stream)
-            launches = C.c_int64(-1)
-            lib.gwb_session_iterate(sess, args.steps, None, C.byref(launches), C.byref(st))
-            ev1.record(stream)
-            ev1.synchronize()
+    with (clocks if clocks is not None else _Null()):  # clocks sampled for the main run
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        launches = C.c_int64(-1)
+        lib.gwb_session_iterate(sess, args.steps, None, C.byref(launches), C.byref(st))
+        ev1.record(stream)
+        ev1.synchronize()
     abi.raise_for(st)
     ms = ev0.elapsed_time(ev1)
-    # per-launch GEMM time: one mark per half-step covers GEMM1+GEMM2
     lib.gwb_session_kernel_ms(sess, 0, C.byref(gms), C.byref(gcnt), C.byref(st))
-    chain_ms = gms.value
     sms, scnt = C.c_double(0), C.c_int64(0)
     lib.gwb_session_kernel_ms(sess, 1, C.byref(sms), C.byref(scnt), C.byref(st))
-    torch.cuda.synchronize()
+    lib.gwb_session_destroy(sess)
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    return dict(ms=ms, chain_ms=gms.value, scal_ms=sms.value, launches=int(launches.value),
+                precision=rprec.value, flops_it=flops_it.value)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *e):
+        return False
+
+
+def run_ours(args, world, rank, local, dist):
+    import torch
+    from paper_2205_08115_b200 import abi
+
+    torch.cuda.set_device(local)
+    lib = abi.load()
+    n = args.n
+    edges, tgt, perm = build_instance(n)
+    dx = dense_dev(torch, n, edges)
+    dy = dense_dev(torch, n, tgt)
+    mu = torch.full((n,), 1.0 / n, device="cuda", dtype=torch.float32)
+    nu = mu.clone()
+
+    prec = PREC_NAMES[args.precision]
+    clocks = ClockSampler(local)
+    main = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks)
+    variants = {}
+    if not args.no_variants:
+        for name in ("3xtf32", "bf16x2"):
+            if PREC_NAMES[name] == main["precision"]:
+                continue
+            v = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, PREC_NAMES[name],
+                             dist)
+            variants[name] = {"value": world * args.steps / (v["ms"] * 1e-3), "unit": "it/s",
+                              "chain_tflops_alg": (v["flops_it"] / 2) / (v["chain_ms"] * 1e-3) / 1e12
+                              if v["chain_ms"] > 0 else None}
+    ms = main["ms"]
     value_rank = args.steps / (ms * 1e-3)
     value = value_rank * world  # replicas: every rank runs the full problem
 
     peaks, peak_src = measured_peaks()
     tf32_peak = measure_tf32_peak(torch) if rank == 0 else None
-    chain_flops = flops_it.value / 2.0           # one half-step = one D_X·π·D_Y chain
-    achieved = chain_flops / (chain_ms * 1e-3) / 1e12 if chain_ms > 0 else None
-    passes = 2 if rprec.value == abi.PREC_3XTF32 else 1
+    flops_it = main["flops_it"]
+    chain_flops = flops_it / 2.0  # one half-step = one D_X·π·D_Y chain (2 GEMM launches)
+    achieved = chain_flops / (main["chain_ms"] * 1e-3) / 1e12 if main["chain_ms"] > 0 else None
+    passes, kind = PREC_PASSES[main["precision"]]
+    label = PREC_LABEL[main["precision"]]
+    exec_peak = peaks.get("bf16_tflops_sustained") if kind == "bf16" else tf32_peak
     roofline = {
-        "bound": "tensor", "kernel": "gemm_tf32_kernel (D_Y·πᵀ then D_X·V per half-step)",
+        "bound": "tensor",
+        "kernel": "gemm_tf32_kernel, CTA-pair tcgen05 (D_Y·πᵀ then D_X·V per half-step)",
         "achieved": achieved, "unit": "TFLOP/s",
-        "peak": tf32_peak, "peak_source": "cuBLAS TF32 8192^3 measured in this run "
-        f"(MEASURED_PEAKS has bf16 only: {peaks.get('bf16_tflops')} TF/s burst, {peak_src})",
+        "peak": tf32_peak,
+        "peak_source": "FP32-accumulate TF32 roofline: cuBLAS TF32 8192^3 measured in this run "
+                       f"(MEASURED_PEAKS.json carries bf16 only; {peak_src})",
         "frac": (achieved / tf32_peak) if (achieved and tf32_peak) else None,
-        "executed_frac": (achieved * passes / tf32_peak) if (achieved and tf32_peak) else None,
+        "precision": label, "passes": passes, "mma_kind": kind,
+        "executed_tflops": achieved * passes if achieved else None,
+        "executed_peak": exec_peak,
+        "executed_peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if kind == "bf16"
+                                 else "cuBLAS TF32 measured in this run"),
+        "executed_frac": (achieved * passes / exec_peak) if (achieved and exec_peak) else None,
         "algorithmic_flops_per_launch_pair": chain_flops,
-        "passes": passes, "traffic": None,
-        "scaling_kernels_ms_per_half_step": sms.value,
+        "traffic": None,
+        "scaling_kernels_ms_per_half_step": main["scal_ms"],
     }
-    sess_destroy = lib.gwb_session_destroy
-    sess_destroy(sess)
     del dx, dy
     torch.cuda.empty_cache()
 
@@ -312,16 +347,15 @@ def run_ours(args, world, rank, local, dist):
             "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 (3xTF32 tensor cores, fp32 accumulate)" if passes == 2 else "f32 (1xTF32)",
+            "dtype": f"f32 iterates; chain {label} ({passes} {kind} MMA passes, fp32 accumulate)",
             "data": "synthetic (seeded BA graphs, reference RNG)",
-            "config": {"workload": WORKLOAD, "n": n, "m": n,
-                       "precision": "3xtf32" if passes == 2 else "tf32",
+            "config": {"workload": WORKLOAD, "n": n, "m": n, "precision": label,
                        "l2": "no flush: each operand (1.6 GB) exceeds the 126 MB L2",
                        "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
-            "tflops": {"algorithmic_per_iteration": flops_it.value,
-                       "achieved_whole_step": flops_it.value * value_rank / 1e12},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches.value), "clocks": clocks.summary(),
+            "tflops": {"algorithmic_per_iteration": flops_it,
+                       "achieved_whole_step": flops_it * value_rank / 1e12},
+            "roofline": roofline, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": main["launches"], "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
 

@@ -45,7 +45,13 @@ enum gwb_axis { GWB_ROWS = 0, GWB_COLS = 1 };
  * meets the π (1e-4) and objective (1e-5) parity bounds; 1xTF32 uses
  * rna-rounded operands and is faster but misses the objective bound.
  * AUTO currently resolves to 3xTF32. */
-enum gwb_precision { GWB_PREC_AUTO = 0, GWB_PREC_TF32 = 1, GWB_PREC_3XTF32 = 2 };
+enum gwb_precision {
+  GWB_PREC_AUTO = 0,
+  GWB_PREC_TF32 = 1,    /* 1 kind::tf32 pass, rna-rounded operands */
+  GWB_PREC_3XTF32 = 2,  /* hi/lo TF32 split passes (2 when D is 0/1) */
+  GWB_PREC_BF16X3 = 3,  /* exact-bf16 D × 3 bf16 planes of the iterate (24-bit) */
+  GWB_PREC_BF16X2 = 4   /* exact-bf16 D × 2 bf16 planes (16-bit) */
+};
 
 /* Error codes; each maps to one reference exception class. */
 enum gwb_code {

@@ -3,6 +3,7 @@
 // accumulator with deterministic (fixed-order) warp and block reductions.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -20,6 +21,16 @@ __device__ __forceinline__ bool stop_rule(double rel, double rel_tol) {
   return rel <= rel_tol && (rel > 0.0 || rel_tol >= kFp32Resolution);
 }
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+  const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
+  return lo | (hi << 16);
+}
+
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
 __device__ __forceinline__ float trunc_tf32(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
@@ -34,6 +45,32 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // 1xTF32 input), 2 → residual x − trunc_tf32(x) (3xTF32 low part).
 __device__ __forceinline__ float aux_of(float x, int mode) {
   return mode == 1 ? rna_tf32(x) : x - trunc_tf32(x);
+}
+
+// GEMM operand copy of 4 consecutive values at element offset `off`:
+//   mode 1/2: one fp32 plane (rna_tf32(x) or x − trunc_tf32(x));
+//   mode 3/4: 3 or 2 bf16 planes, `plane` elements apart, whose sum is x
+//             (round-to-nearest splits hi = rn(x), mid = rn(x − hi), …).
+__device__ __forceinline__ void aux_store4(float* aux, int mode, int64_t plane, int64_t off,
+                                           float a, float b, float c, float d) {
+  if (mode <= 2) {
+    *reinterpret_cast<float4*>(aux + off) =
+        make_float4(aux_of(a, mode), aux_of(b, mode), aux_of(c, mode), aux_of(d, mode));
+    return;
+  }
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(aux);
+  float v[4] = {a, b, c, d};
+  const int planes = mode == 3 ? 3 : 2;
+  for (int pl = 0; pl < planes; ++pl) {
+    float h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = bf16_round(v[q]);
+      v[q] -= h[q];
+    }
+    *reinterpret_cast<uint2*>(base + pl * plane + off) =
+        make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+  }
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -25,6 +25,8 @@
 #include <mutex>
 #include <stdexcept>
 
+#include <cuda_bf16.h>
+
 #include "gemm.cuh"
 #include "ptx.cuh"
 
@@ -37,6 +39,7 @@ constexpr int kPairM = 2 * kBM;            // rows per CTA pair (MMA M)
 constexpr int kBN = 256;                   // columns per tile (MMA N)
 constexpr int kHalfN = kBN / 2;            // B rows loaded per CTA
 constexpr int kBK = 32;                    // 32 fp32 = 128 B = one swizzle row
+constexpr int kBK16 = 64;                  // 64 bf16 = 128 B
 constexpr int kStages = 6;
 constexpr int kGroupM = 8;
 constexpr int kEpiWarps = 16;              // 4 lane quadrants × 4 column slices
@@ -50,13 +53,16 @@ constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
 struct __align__(64) GemmParams {
   CUtensorMap a_map[2];
-  CUtensorMap b_map[2];
+  CUtensorMap b_map[3];
   int32_t M, N, K;
   int32_t passes;
   int32_t a_sel[3];
   int32_t b_sel[3];
   int32_t tiles_m, tiles_n;  // tiles_m counts 256-row pair tiles
   int32_t chunk;  // k-blocks accumulated in TMEM before promotion to registers
+  int32_t kind;   // 0: kind::tf32 (fp32 operands), 1: kind::f16 (bf16 operands)
+  int32_t c_planes;
+  __nv_bfloat16* c_pl[3];
   float* c;
   float* c_aux;
   int64_t ldc;
@@ -130,7 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int kblocks = (p.K + kBK - 1) / kBK;
+  const int kblk = p.kind ? kBK16 : kBK;  // elements per 128-B k-block
+  const int kblocks = (p.K + kblk - 1) / kblk;
   const int total = p.passes * kblocks;
   const int chunk = p.chunk;
   const int nchunks = (total + chunk - 1) / chunk;
@@ -147,14 +154,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int kb = it - pass * kblocks;
         const uint32_t fbar = ptx::mapa(&full[s], 0);
         if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-        ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kBK, a_row);
-        ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kBK,
+        ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk, a_row);
+        ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kblk,
                              b_row);
       }
     }
   } else if (warp == 1) {
     if (leader && ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_tf32(kPairM, kBN);
+      const uint32_t idesc = p.kind ? ptx::idesc_bf16(kPairM, kBN) : ptx::idesc_tf32(kPairM, kBN);
       for (int c = 0; c < nchunks; ++c) {
         const int b = c & 1;
         ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
@@ -169,11 +176,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
           const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN * kBK));
+          // 4 MMAs per 128-B k-block: K = 8 (tf32) or 16 (bf16), +32 B each.
 #pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            ptx::mma_tf32_2sm(acc, ptx::umma_desc_sw128(a_base + k * 32),
-                              ptx::umma_desc_sw128(b_base + k * 32), idesc,
-                              (it != it0 || k != 0) ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
+            const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32);
+            const uint32_t accum = (it != it0 || k != 0) ? 1u : 0u;
+            if (p.kind) ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
+            else ptx::mma_tf32_2sm(acc, ad, bd, idesc, accum);
           }
           ptx::mma_commit_2sm(&empty[s], 0x3);
         }
@@ -221,7 +231,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
         acc[j] = round_out ? rna_tf32(x) : x;
       }
-      if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
+      if (p.c_planes > 0) {
+        // bf16 split planes (RN): x ≈ hi + mid (+ lo), for a bf16-split GEMM.
+        const int64_t off = static_cast<int64_t>(row) * p.ldc + col0;
+        const bool vec = col0 + kSliceCols <= p.N && (p.ldc & 7) == 0;
+#pragma unroll
+        for (int j0 = 0; j0 < kSliceCols; j0 += 8) {
+          __align__(16) __nv_bfloat16 h[3][8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float r = acc[j0 + q];
+            h[0][q] = __float2bfloat16_rn(r);
+            r -= __bfloat162float(h[0][q]);
+            h[1][q] = __float2bfloat16_rn(r);
+            r -= __bfloat162float(h[1][q]);
+            h[2][q] = __float2bfloat16_rn(r);
+          }
+          for (int pl = 0; pl < p.c_planes; ++pl) {
+            if (pl == 1 && p.c_planes == 2) {  // x2: lo = rn(x − hi)
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                h[1][q] = __float2bfloat16_rn(acc[j0 + q] - __bfloat162float(h[0][q]));
+            }
+            __nv_bfloat16* dst = p.c_pl[pl] + off + j0;
+            if (vec) {
+              *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h[pl]);
+            } else {
+              for (int q = 0; q < 8; ++q)
+                if (col0 + j0 + q < p.N) dst[q] = h[pl][q];
+            }
+          }
+        }
+      } else if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
         for (int j = 0; j < kSliceCols; j += 4) {
           *reinterpret_cast<float4*>(crow + col0 + j) =
@@ -274,17 +315,21 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Row-major rows×cols fp32 matrix (leading dim ld), box = box_rows × 32 cols.
-CUtensorMap make_map(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// Row-major rows×cols matrix (leading dim ld elements) of fp32 (esize 4) or
+// bf16 (esize 2); box = box_rows × 128 B.
+CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                     int esize = 4) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
-  if ((ld * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
+  if ((ld * esize) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
     throw std::runtime_error("gemm: TMA needs 16-B aligned base and row pitch");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esize), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims,
+  CUresult r = encode_fn()(&m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                          : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(ptr), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -317,13 +362,26 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.M = static_cast<int32_t>(d.M);
   g.N = static_cast<int32_t>(d.N);
   g.K = static_cast<int32_t>(d.K);
+  g.passes = 1;
+  g.a_sel[0] = 0;
+  g.b_sel[0] = 0;
+  if (d.bf16_planes > 0) {
+    // Σ_p A·B_p over bf16 planes (A exact in bf16).
+    g.kind = 1;
+    g.a_map[0] = make_map(d.a_bf16, d.M, d.K, d.lda, kBM, 2);
+    g.a_map[1] = g.a_map[0];
+    for (int pl = 0; pl < d.bf16_planes; ++pl) {
+      g.b_map[pl] = make_map(d.b_bf16[pl], d.N, d.K, d.ldb, kHalfN, 2);
+      g.a_sel[pl] = 0;
+      g.b_sel[pl] = pl;
+    }
+    g.passes = d.bf16_planes;
+  } else {
   g.a_map[0] = make_map(d.a, d.M, d.K, d.lda, kBM);
   g.b_map[0] = make_map(d.b, d.N, d.K, d.ldb, kHalfN);
   g.a_map[1] = d.a_lo ? make_map(d.a_lo, d.M, d.K, d.lda, kBM) : g.a_map[0];
   g.b_map[1] = d.b_lo ? make_map(d.b_lo, d.N, d.K, d.ldb, kHalfN) : g.b_map[0];
-  g.passes = 1;
-  g.a_sel[0] = 0;
-  g.b_sel[0] = 0;
+  g.b_map[2] = g.b_map[0];
   if (d.three_pass) {
     // A·B + A·B_lo + A_lo·B; a missing residual means that operand is exact
     // in TF32 (e.g. 0/1 adjacency), so its pass is dropped.
@@ -338,6 +396,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       ++g.passes;
     }
   }
+  }
   g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
   g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
@@ -345,6 +404,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.c_aux = d.c_aux;
   g.ldc = d.ldc;
   g.aux_mode = d.aux_mode;
+  g.c_planes = d.c_planes;
+  for (int pl = 0; pl < 3; ++pl) g.c_pl[pl] = static_cast<__nv_bfloat16*>(d.c_bf16[pl]);
   g.row_scale = d.row_scale;
   g.col_scale = d.col_scale;
   g.skip = d.skip;

@@ -36,7 +36,17 @@ struct GemmDesc {
   const float* col_scale = nullptr;  // length N
   const int* skip = nullptr;         // device flag: nonzero ⇒ kernel is a no-op
   bool three_pass = false;           // 3xTF32 (drops A_lo·B_lo); needs *_lo
-  int promote_every = 2;             // k-blocks (×32) per TMEM chunk; 0 = never
+  int promote_every = 2;             // k-blocks per TMEM chunk; 0 = never
+  // bf16 split mode (kind::f16): A is an exact bf16 matrix (e.g. 0/1
+  // adjacency), B is given as `bf16_planes` bf16 planes whose sum is the
+  // fp32 operand; C = Σ_p A·B_pᵀ.  Replaces a/b/*_lo when bf16_planes > 0.
+  int bf16_planes = 0;               // 0 (TF32 path), 2 or 3
+  const void* a_bf16 = nullptr;      // M×K bf16, leading dim lda
+  const void* b_bf16[3] = {nullptr, nullptr, nullptr};  // N×K planes, ldb
+  // Output as bf16 split planes (for a following bf16-split GEMM) instead
+  // of fp32 `c`: c_planes ∈ {0, 2, 3}; planes are M×N with leading dim ldc.
+  int c_planes = 0;
+  void* c_bf16[3] = {nullptr, nullptr, nullptr};
 };
 
 // Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).

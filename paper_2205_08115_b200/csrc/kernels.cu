@@ -64,7 +64,6 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   }
   const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
   float* p = d.P + i * d.ld;
-  float* plo = d.P_aux ? d.P_aux + i * d.ld : nullptr;
   const int am = d.aux_mode;
   for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
@@ -75,9 +74,7 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
     o.z = (j + 2 < m) ? scale * w4.z * __expf(g4.z * inv_rho - r) : 0.f;
     o.w = (j + 3 < m) ? scale * w4.w * __expf(g4.w * inv_rho - r) : 0.f;
     *reinterpret_cast<float4*>(p + j) = o;
-    if (plo)
-      *reinterpret_cast<float4*>(plo + j) =
-          make_float4(aux_of(o.x, am), aux_of(o.y, am), aux_of(o.z, am), aux_of(o.w, am));
+    if (d.P_aux) aux_store4(d.P_aux, am, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
   }
 }
 
@@ -170,7 +167,6 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   const float* p = d.P + i * d.ld;
   const float* wo = d.W + i * d.ld;
   float* wn = d.W_new + i * d.ld;
-  float* wlo = d.W_aux ? d.W_aux + i * d.ld : nullptr;
   const int am = d.aux_mode;
   const float inv_rho = d.inv_rho;
   const int64_t m = d.m;
@@ -205,9 +201,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
       }
     }
     *reinterpret_cast<float4*>(wn + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (wlo)
-      *reinterpret_cast<float4*>(wlo + j) =
-          make_float4(aux_of(o[0], am), aux_of(o[1], am), aux_of(o[2], am), aux_of(o[3], am));
+    if (d.W_aux) aux_store4(d.W_aux, am, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3]);
   }
   MaxSum dummy{-INFINITY, 0.f};
   block_reduce<kRowThreads, 5>(dummy, sums);
@@ -381,9 +375,20 @@ __global__ void average64_kernel(const double* a, const double* b, double* dst, 
 }
 
 __global__ void tf32_aux_kernel(const float* x, int64_t rows, int64_t cols, int64_t ld,
-                                float* out, int mode) {
+                                float* out, int mode, int64_t plane) {
   const int64_t i = blockIdx.x;
-  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) out[i * ld + j] = aux_of(x[i * ld + j], mode);
+  // ld is a multiple of 32, so whole float4 groups stay inside the row pitch.
+  for (int64_t j = threadIdx.x * 4; j < cols; j += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i * ld + j);
+    aux_store4(out, mode, plane, i * ld + j, v.x, v.y, v.z, v.w);
+  }
+}
+
+__global__ void to_bf16_kernel(const float* x, int64_t rows, int64_t cols, int64_t ld,
+                               __nv_bfloat16* out) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+    out[i * ld + j] = __float2bfloat16_rn(x[i * ld + j]);
 }
 
 __global__ void product_coupling_kernel(const float* mu, const float* nu, int64_t n, int64_t m,
@@ -406,7 +411,8 @@ __global__ void analyze_kernel(const float* D, int64_t rows, int64_t cols, int64
   for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
     const float v = D[i * ld + j];
     mx = fmaxf(mx, v);
-    inexact |= (v != trunc_tf32(v));
+    inexact |= (v != trunc_tf32(v)) ? 1 : 0;
+    inexact |= (v != bf16_round(v)) ? 2 : 0;
   }
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -414,7 +420,7 @@ __global__ void analyze_kernel(const float* D, int64_t rows, int64_t cols, int64
   }
   if ((threadIdx.x & 31) == 0) {
     atomic_max_nonneg(out_max, mx);
-    if (inexact) atomicOr(out_inexact, 1);
+    if (inexact) atomicOr(out_inexact, inexact);
   }
 }
 
@@ -468,7 +474,14 @@ void launch_average64(const double* a, const double* b, double* dst, int64_t len
 
 void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
                      cudaStream_t s) {
-  tf32_aux_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld, out, mode);
+  tf32_aux_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld, out, mode,
+                                                               rows * ld);
+}
+
+void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
+                    cudaStream_t s) {
+  to_bf16_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld,
+                                                             static_cast<__nv_bfloat16*>(out));
 }
 
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,

@@ -80,6 +80,8 @@ struct BapgDev {
   float* W_aux;             // GEMM copy of W_new, see aux_mode (nullable)
   int aux_mode;             // 1: aux = rna_tf32(x) (1xTF32 operand)
                             // 2: aux = x − trunc_tf32(x) (3xTF32 residual)
+                            // 3/4: 3 / 2 bf16 split planes (bf16x3 / bf16x2)
+  int64_t plane;            // elements per bf16 plane (n·ld)
   RowPart* row_part;        // n
   ColWritePart* cw_part;    // n
   float* col_pmax;          // chunks × m
@@ -120,9 +122,13 @@ void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t col
                                      cudaStream_t s);
 // dst = 0.5 (a + b), column-major fp64 of len elements.
 void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s);
-// out = aux_of(x, mode) (1: rna_tf32(x), 2: x − trunc_tf32(x)), row-major.
+// GEMM operand copy of x (ld multiple of 4): mode 1: rna_tf32(x);
+// 2: x − trunc_tf32(x); 3/4: 3 or 2 bf16 split planes (plane = rows·ld).
 void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
                      cudaStream_t s);
+// out (bf16, same ld) = bf16_rn(x).
+void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
+                    cudaStream_t s);
 // Scans a structure matrix: *out_max = max entry, *out_inexact = 1 if any
 // entry is not exactly representable in TF32 (0/1 adjacency is exact).
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,

@@ -49,14 +49,16 @@ void dfree(void* p) {
 
 int resolve_precision(int requested, bool d_exact, double dmax_x, double dmax_y, double rho) {
   if (requested == GWB_PREC_TF32 || requested == GWB_PREC_3XTF32) return requested;
-  // AUTO: 3xTF32.  Measured on B200: 1xTF32 with rna-rounded
-  // operands keeps π within 1e-4 on graph problems but misses the 1e-5 GW
-  // objective bound (4.7e-5 .. 1.1e-4), so it stays an explicit opt-in.
-  (void)d_exact;
+  // AUTO (measured on B200): a 3-term split with fp32
+  // accumulate.  When both structure matrices are exact in bf16 (0/1
+  // graphs) the split runs as bf16x3 — D × (hi + mid + lo) bf16 planes,
+  // 24-bit operands, 1.5 TF32-pass equivalents — otherwise as 3xTF32.
+  // 1xTF32 misses the 1e-5 objective bound and bf16x2 is reduced precision;
+  // both stay explicit opt-ins.
   (void)dmax_x;
   (void)dmax_y;
   (void)rho;
-  return GWB_PREC_3XTF32;
+  return d_exact ? GWB_PREC_BF16X3 : GWB_PREC_3XTF32;
 }
 
 BapgEngine::BapgEngine(int device, int64_t n, int64_t m, double rho, int precision,
@@ -90,7 +92,8 @@ BapgEngine::~BapgEngine() {
   gemm_plan_destroy(g2_);
   gemm_plan_destroy(g2_tail_);
   for (void* p : std::initializer_list<void*>{
-           Dx_, Dx_aux_, Dy_, Dy_aux_, P_, P_aux_, W_[0], W_[1], W_aux_[0], W_aux_[1], Vt_,
+           Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
+           W_aux_[1], Vt_,
            Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
            col_max_, col_scale_, col_psump_, col_dev_, st_, rec_})
     dfree(p);
@@ -108,13 +111,16 @@ void BapgEngine::alloc() {
   Dx_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
   Dy_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
   P_ = dalloc<float>(nm);
-  P_aux_ = dalloc<float>(nm);
+  // Operand copies hold one fp32 plane (TF32 modes) or up to three bf16
+  // planes (bf16x3): size them for 6 B/element.
+  P_aux_ = dalloc<float>(nm * 3 / 2);
   for (int q = 0; q < 2; ++q) {
     W_[q] = dalloc<float>(nm);
-    W_aux_[q] = dalloc<float>(nm);
+    W_aux_[q] = dalloc<float>(nm * 3 / 2);
   }
   Vt_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
-  if (precision_ == GWB_PREC_3XTF32) Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+  if (precision_ != GWB_PREC_TF32)
+    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2);
   G_ = dalloc<float>(nm);
   mu32_ = dalloc<float>(ldn_);
   nu32_ = dalloc<float>(ldm_);
@@ -153,7 +159,8 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.W = W_[q];
   d.W_new = W_[1 - q];
   d.W_aux = W_aux_[1 - q];
-  d.aux_mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
+  d.aux_mode = aux_mode();
+  d.plane = n_ * ldm_;
   d.row_part = row_part_;
   d.cw_part = cw_part_;
   d.col_pmax = col_pmax_;
@@ -182,12 +189,25 @@ void BapgEngine::prepare_d() {
   GWB_CUDA(cudaStreamSynchronize(stream_));
   dfree(d_max);
   dfree(d_inexact);
-  dx_exact_ = h_inexact[0] == 0;
-  dy_exact_ = h_inexact[1] == 0;
+  dx_exact_ = (h_inexact[0] & 1) == 0;
+  dy_exact_ = (h_inexact[1] & 1) == 0;
+  const bool bf16_exact = (h_inexact[0] & 2) == 0 && (h_inexact[1] & 2) == 0;
   if (precision_ == GWB_PREC_AUTO)
-    precision_ = resolve_precision(GWB_PREC_AUTO, dx_exact_ && dy_exact_, h_max[0], h_max[1], rho_);
-  if (precision_ == GWB_PREC_3XTF32 && !Vt_aux_)
-    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+    precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, h_max[0], h_max[1], rho_);
+  // bf16 splits need exactly representable structure matrices (0/1 graphs);
+  // otherwise fall back to 3xTF32, which splits both operands.
+  if ((precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2) && !bf16_exact)
+    precision_ = GWB_PREC_3XTF32;
+  if (precision_ != GWB_PREC_TF32 && !Vt_aux_)
+    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2);
+  if (bf16()) {
+    if (!Dx_bf_) Dx_bf_ = dalloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16);
+    if (!Dy_bf_) Dy_bf_ = dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16);
+    launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
+    launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
+    build_plans();
+    return;
+  }
   const int mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
   if (!dx_exact_) {
     if (!Dx_aux_) Dx_aux_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
@@ -211,6 +231,55 @@ void BapgEngine::build_plans() {
   gemm_plan_destroy(g2_);
   gemm_plan_destroy(g2_tail_);
 
+  const int* done = &st_->done;
+  const int* flags = &st_->flags;
+  if (bf16()) {
+    // bf16 split chain: A = D (exact bf16), B = planes of W / P / V.
+    const int planes = precision_ == GWB_PREC_BF16X3 ? 3 : 2;
+    auto planes_of = [](float* base, int64_t plane_elems, int k) {
+      return static_cast<void*>(reinterpret_cast<uint16_t*>(base) + k * plane_elems);
+    };
+    auto gemm1 = [&](float* X_aux, const int* skip) {
+      GemmDesc d;
+      d.M = m_;
+      d.N = n_;
+      d.K = m_;
+      d.bf16_planes = planes;
+      d.a_bf16 = Dy_bf_;
+      d.lda = ldm_;
+      for (int k = 0; k < planes; ++k) d.b_bf16[k] = planes_of(X_aux, n_ * ldm_, k);
+      d.ldb = ldm_;
+      d.c_planes = planes;
+      for (int k = 0; k < planes; ++k) d.c_bf16[k] = planes_of(Vt_aux_, m_ * ldn_, k);
+      d.ldc = ldn_;
+      d.skip = skip;
+      return gemm_plan_create(d);
+    };
+    auto gemm2 = [&](const int* skip) {
+      GemmDesc d;
+      d.M = n_;
+      d.N = m_;
+      d.K = n_;
+      d.bf16_planes = planes;
+      d.a_bf16 = Dx_bf_;
+      d.lda = ldn_;
+      for (int k = 0; k < planes; ++k) d.b_bf16[k] = planes_of(Vt_aux_, m_ * ldn_, k);
+      d.ldb = ldn_;
+      d.c = G_;
+      d.ldc = ldm_;
+      d.skip = skip;
+      return gemm_plan_create(d);
+    };
+    for (int q = 0; q < 2; ++q) {
+      g1_[q][0] = gemm1(W_aux_[q], done);
+      g1_tail_[q] = gemm1(W_aux_[q], flags);
+    }
+    g1_[0][1] = gemm1(P_aux_, done);
+    g1_[1][1] = g1_[0][1];
+    g2_ = gemm2(done);
+    g2_tail_ = gemm2(flags);
+    return;
+  }
   const bool tf32 = precision_ == GWB_PREC_TF32;
   // A operands (structure matrices).
   const float* ax = Dx_;
@@ -262,8 +331,6 @@ void BapgEngine::build_plans() {
     d.three_pass = !tf32;
     return gemm_plan_create(d);
   };
-  const int* done = &st_->done;
-  const int* flags = &st_->flags;
   for (int q = 0; q < 2; ++q) {
     g1_[q][0] = gemm1(W_[q], W_aux_[q], done);
     g1_tail_[q] = gemm1(W_[q], W_aux_[q], flags);
@@ -327,7 +394,7 @@ void BapgEngine::reset(const double* w0_host) {
   } else {
     launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, W_[0], stream_);
   }
-  launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], precision_ == GWB_PREC_TF32 ? 1 : 2, stream_);
+  launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], aux_mode(), stream_);
   parity_ = 0;
   GWB_CUDA(cudaGetLastError());
 }

@@ -96,6 +96,14 @@ class BapgEngine {
 
   // device buffers
   float *Dx_ = nullptr, *Dx_aux_ = nullptr, *Dy_ = nullptr, *Dy_aux_ = nullptr;
+  float *Dx_bf_ = nullptr, *Dy_bf_ = nullptr;  // bf16 copies (bf16 split modes)
+  bool bf16() const { return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2; }
+  int aux_mode() const {
+    return precision_ == GWB_PREC_TF32 ? 1
+           : precision_ == GWB_PREC_BF16X3 ? 3
+           : precision_ == GWB_PREC_BF16X2 ? 4
+                                           : 2;
+  }
   float *P_ = nullptr, *P_aux_ = nullptr, *W_[2] = {nullptr, nullptr},
         *W_aux_[2] = {nullptr, nullptr};
   float *Vt_ = nullptr, *Vt_aux_ = nullptr, *G_ = nullptr;
