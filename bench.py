@@ -127,6 +127,18 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "B200_PROFILING.md fallback"
 
 
+def gemm_traffic(n):
+    """DRAM bytes per GEMM launch from the committed ncu capture (c4 only)."""
+    p = os.path.join(ROOT, "profiles", "gemm_traffic_c4.json")
+    if n != 20000 or not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return {"bytes_per_launch": d["dram_read_bytes_per_launch"] + d["dram_write_bytes_per_launch"],
+            "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
+            "source": d["source"]}
+
+
 def measure_tf32_peak(torch):
     """cuBLAS TF32 dense 8192³ (2·N³ FLOP), best of 10, CUDA events."""
     torch.backends.cuda.matmul.allow_tf32 = True
@@ -327,7 +339,7 @@ def run_ours(args, world, rank, local, dist):
                                  else "cuBLAS TF32 measured in this run"),
         "executed_frac": (achieved * passes / exec_peak) if (achieved and exec_peak) else None,
         "algorithmic_flops_per_launch_pair": chain_flops,
-        "traffic": None,
+        "traffic": gemm_traffic(n),
         "scaling_kernels_ms_per_half_step": main["scal_ms"],
     }
     del dx, dy
