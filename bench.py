@@ -36,13 +36,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=20000)
+    ap.add_argument("--size", dest="n", type=int, default=20000)
     ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2"])
     ap.add_argument("--e2e-iters", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--cpu-n", type=int, default=2500)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded NCCL path even at one rank (testing)")
+    ap.add_argument("--cpu-size", dest="cpu_n", type=int, default=2500)
     return ap.parse_args()
 
 
@@ -372,6 +374,84 @@ def run_ours(args, world, rank, local, dist):
         print(json.dumps(line), flush=True)
 
 
+def dense_rows_dev(torch, n, edges, r0, rows):
+    """Rows [r0, r0+rows) of the 0/1 adjacency, built on the device."""
+    d = torch.zeros((max(rows, 1), (n + 31) // 32 * 32), device="cuda", dtype=torch.float32)
+    e = np.concatenate([edges, edges[:, ::-1]])
+    e = e[(e[:, 0] >= r0) & (e[:, 0] < r0 + rows)]
+    t = torch.from_numpy(e.astype(np.int64)).cuda()
+    if len(e):
+        d[t[:, 0] - r0, t[:, 1]] = 1.0
+    return d
+
+
+def run_sharded_bench(args, world, rank, local, dist):
+    """N > 1: c4 rows of π, w, D_X sharded over the ranks (strong scaling of
+    the fixed n=m=20000 problem); Vᵀ all-gathers, column-statistics
+    all-gathers and diagnostic all-reduces over NCCL (NVLink/NVSwitch)."""
+    import torch
+    from paper_2205_08115_b200 import abi
+    from paper_2205_08115_b200 import dist as D
+    torch.cuda.set_device(local)
+    n = args.n
+    edges, tgt, _ = build_instance(n)
+    plan = D.ShardPlan(n, world)
+    rb, rv = plan.row_begin(rank), plan.rows_valid(rank)
+    dx_rows = dense_rows_dev(torch, n, edges, rb, rv)
+    dy = dense_dev(torch, n, tgt)
+    mu = torch.full((n,), 1.0 / n, device="cuda", dtype=torch.float32)
+    prec = PREC_NAMES[args.precision] or abi.PREC_BF16X3  # 0/1 graphs: AUTO = bf16x3
+    cfg = abi.default_config(rho=0.1, max_iters=args.steps + args.warmup + 4, rel_tol=1e-30,
+                             precision=prec)
+    shard = D.GpuShard(cfg, n, n, rank, world, local)
+    shard.load(dx_rows, dy, mu[rb:rb + max(rv, 1)].contiguous(), mu)
+    shard.reset()
+    del dx_rows, dy
+    comm = D.TorchComm(dist, rank, world)
+    D.iterate_sharded([shard], comm, args.warmup, poll_every=0)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local)
+    with clocks:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(shard.stream)
+        D.iterate_sharded([shard], comm, args.steps, poll_every=0)
+        ev1.record(shard.stream)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    st = shard.status()
+    if st["flags"]:
+        D.raise_shard_flags(st)
+    value = args.steps / (ms * 1e-3)  # whole-job iterations/s of the one sharded problem
+    passes, kind = PREC_PASSES[prec]
+    nr = plan.rows_per_shard
+    flops_it = 4.0 * n * n * (n + n)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": f"f32 iterates; chain {PREC_LABEL[prec]} ({passes} {kind} MMA passes, fp32 accumulate)",
+            "data": "synthetic (seeded BA graphs, reference RNG)",
+            "config": {"workload": WORKLOAD, "n": n, "m": n, "precision": PREC_LABEL[prec],
+                       "l2": "no flush: operands exceed the 126 MB L2",
+                       "parallelism": f"row-sharded over {world} GPUs (NCCL all-gather of Vᵀ "
+                                      "blocks, all-gather of column stats, all-reduce of "
+                                      "diagnostics)",
+                       "rows_per_shard": nr},
+            "tflops": {"algorithmic_per_iteration": flops_it,
+                       "achieved_whole_step": flops_it * value / 1e12},
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    shard.close()
+
+
 def run_e2e(args, edges, tgt, n, prec):
     """gwb_solve through the C-ABI from host fp64 (column-major) buffers:
     H2D of D_X, D_Y, μ, ν and D2H of the final coupling + trace inside the
@@ -407,7 +487,18 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:
-        run_ours(args, world, rank, local, dist)
+        if world > 1 or args.sharded:
+            if dist is None:  # one-rank process group so the NCCL calls are real
+                import torch
+                import torch.distributed as tdist
+                torch.cuda.set_device(local)
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                tdist.init_process_group("nccl", rank=0, world_size=1)
+                dist = tdist
+            run_sharded_bench(args, world, rank, local, dist)
+        else:
+            run_ours(args, world, rank, local, dist)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

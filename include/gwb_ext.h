@@ -21,6 +21,54 @@ GWB_API int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b,
                                int64_t N, int64_t K, int32_t precision,
                                void* stream, gwb_status* st);
 
+/* ---------------------------------------------------------------------------
+ * Row-sharded multi-GPU BAPG, one shard per rank (csrc/shard.cu).  The
+ * caller owns the communication buffers (e.g. torch tensors used with
+ * torch.distributed/NCCL) and issues the collectives between phases on the
+ * shard's stream:
+ *   per iteration: phase 0, all-gather(vt), phase 1, phase 2,
+ *                  all-gather(vt), phase 3, all-gather(col_stats), phase 4,
+ *                  all-reduce-sum(diag[8]), all-reduce-max(err[8]), phase 5
+ *   after the loop: phase 6, all-gather(vt), phase 7, all-reduce-sum(diag),
+ *                   all-reduce-max(err), phase 8, then gwb_shard_finish.
+ * vt is world × planes × m × rows_per_shard elements, rank r's chunk being
+ * its block of Vᵀ (the all-gather is in place, one collective for all
+ * planes); col_stats is world × 3 × m fp64; diag and err are 8 fp64 each.
+ * ------------------------------------------------------------------------- */
+typedef struct gwb_shard gwb_shard;
+
+GWB_API int32_t gwb_shard_create(const gwb_config* cfg, int64_t n, int64_t m,
+                                 int32_t rank, int32_t world, int32_t device,
+                                 void* stream, gwb_shard** out,
+                                 gwb_status* st);
+GWB_API int32_t gwb_shard_layout(gwb_shard* s, int64_t* rows_per_shard,
+                                 int64_t* row_begin, int64_t* rows_valid,
+                                 int32_t* planes, int32_t* elem_bytes,
+                                 int64_t* vt_bytes, int64_t* stats_bytes,
+                                 gwb_status* st);
+GWB_API int32_t gwb_shard_set_comm(gwb_shard* s, void* vt_gather,
+                                   void* col_stats, double* diag, double* err,
+                                   gwb_status* st);
+/* dx_rows: rows_valid × n fp32 rows of D_X owned by this rank (device). */
+GWB_API int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows,
+                                      int64_t ldx, const float* dy,
+                                      int64_t ldy, const float* mu_rows,
+                                      const float* nu, gwb_status* st);
+GWB_API int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st);
+GWB_API int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st);
+GWB_API int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st);
+GWB_API int32_t gwb_shard_status(gwb_shard* s, int32_t* done, int32_t* iter,
+                                 int32_t* flags, int32_t* converged,
+                                 int32_t* err_iter, int32_t* zero_index,
+                                 gwb_status* st);
+GWB_API int32_t gwb_shard_finish(gwb_shard* s, gwb_status* st);
+GWB_API int32_t gwb_shard_records(gwb_shard* s, int32_t count,
+                                  gwb_record* out, gwb_status* st);
+/* Local rows of π and w, row-major fp64 rows_valid × m (nullable). */
+GWB_API int32_t gwb_shard_rows(gwb_shard* s, double* pi_rows, double* w_rows,
+                               gwb_status* st);
+GWB_API int32_t gwb_shard_destroy(gwb_shard* s);
+
 /* Instance generators (paper_2205_08115_b200/csrc/instances.cpp).  Edge
  * lists are int32 pairs (a < b), canonical order; return the edge count
  * (the buffer holds min(count, cap) edges) or -1 on invalid arguments. */

@@ -61,6 +61,7 @@ struct __align__(64) GemmParams {
   int32_t tiles_m, tiles_n;  // tiles_m counts 256-row pair tiles
   int32_t chunk;  // k-blocks accumulated in TMEM before promotion to registers
   int32_t kind;   // 0: kind::tf32 (fp32 operands), 1: kind::f16 (bf16 operands)
+  int32_t b_block_k;  // > 0: B maps are 3-D [K/b_block_k][N][b_block_k]
   int32_t c_planes;
   __nv_bfloat16* c_pl[3];
   float* c;
@@ -155,8 +156,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t fbar = ptx::mapa(&full[s], 0);
         if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
         ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk, a_row);
-        ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kblk,
-                             b_row);
+        if (p.b_block_k > 0) {
+          const int kk = kb * kblk;
+          ptx::tma_load_3d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
+                               kk % p.b_block_k, b_row, kk / p.b_block_k);
+        } else {
+          ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kblk,
+                               b_row);
+        }
       }
     }
   } else if (warp == 1) {
@@ -342,6 +349,31 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
   return m;
 }
 
+// Blocked-K operand [blocks][rows][block_k] (contiguous), box = box_rows ×
+// 128 B within one block.
+CUtensorMap make_map_blocked(const void* ptr, int64_t rows, int64_t block_k, int64_t blocks,
+                             int box_rows, int esize, int64_t block_stride = 0) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  if (block_stride == 0) block_stride = block_k * rows;
+  if ((block_k * esize) % 16 != 0 || (block_stride * esize) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
+    throw std::runtime_error("gemm: blocked TMA needs 16-B aligned base and block pitch");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(block_k), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(blocks)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(block_k) * esize,
+                           static_cast<cuuint64_t>(block_stride) * esize};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / esize), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                          : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed");
+  return m;
+}
+
 }  // namespace
 
 struct GemmPlan {
@@ -371,16 +403,24 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     g.a_map[0] = make_map(d.a_bf16, d.M, d.K, d.lda, kBM, 2);
     g.a_map[1] = g.a_map[0];
     for (int pl = 0; pl < d.bf16_planes; ++pl) {
-      g.b_map[pl] = make_map(d.b_bf16[pl], d.N, d.K, d.ldb, kHalfN, 2);
+      g.b_map[pl] = d.b_block_k > 0
+                        ? make_map_blocked(d.b_bf16[pl], d.N, d.b_block_k, d.K / d.b_block_k,
+                                           kHalfN, 2, d.b_block_stride)
+                        : make_map(d.b_bf16[pl], d.N, d.K, d.ldb, kHalfN, 2);
       g.a_sel[pl] = 0;
       g.b_sel[pl] = pl;
     }
     g.passes = d.bf16_planes;
   } else {
+  auto bmap = [&](const float* b) {
+    return d.b_block_k > 0 ? make_map_blocked(b, d.N, d.b_block_k, d.K / d.b_block_k, kHalfN, 4,
+                                              d.b_block_stride)
+                           : make_map(b, d.N, d.K, d.ldb, kHalfN);
+  };
   g.a_map[0] = make_map(d.a, d.M, d.K, d.lda, kBM);
-  g.b_map[0] = make_map(d.b, d.N, d.K, d.ldb, kHalfN);
+  g.b_map[0] = bmap(d.b);
   g.a_map[1] = d.a_lo ? make_map(d.a_lo, d.M, d.K, d.lda, kBM) : g.a_map[0];
-  g.b_map[1] = d.b_lo ? make_map(d.b_lo, d.N, d.K, d.ldb, kHalfN) : g.b_map[0];
+  g.b_map[1] = d.b_lo ? bmap(d.b_lo) : g.b_map[0];
   g.b_map[2] = g.b_map[0];
   if (d.three_pass) {
     // A·B + A·B_lo + A_lo·B; a missing residual means that operand is exact
@@ -400,6 +440,10 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
   g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
+  g.b_block_k = static_cast<int32_t>(d.b_block_k);
+  if (d.b_block_k > 0 &&
+      (d.K % d.b_block_k != 0 || d.b_block_k % (d.bf16_planes > 0 ? kBK16 : kBK) != 0))
+    throw std::runtime_error("gemm: blocked K must tile K and be a multiple of the k-block");
   g.c = d.c;
   g.c_aux = d.c_aux;
   g.ldc = d.ldc;

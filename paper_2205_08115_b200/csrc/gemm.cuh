@@ -47,6 +47,12 @@ struct GemmDesc {
   // of fp32 `c`: c_planes ∈ {0, 2, 3}; planes are M×N with leading dim ldc.
   int c_planes = 0;
   void* c_bf16[3] = {nullptr, nullptr, nullptr};
+  // Blocked-K B operand (multi-GPU all-gather layout): when b_block_k > 0,
+  // every B plane is stored as [K / b_block_k][N][b_block_k] (leading dim of
+  // a block row = b_block_k); b_block_k must be a multiple of the k-block
+  // (32 fp32 / 64 bf16 elements).
+  int64_t b_block_k = 0;
+  int64_t b_block_stride = 0;        // elements between blocks (0 ⇒ N·b_block_k)
 };
 
 // Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).

@@ -298,6 +298,7 @@ __global__ void status_reset_kernel(DevStatus* st) {
   st->zero_index = 0x7fffffff;
   st->sink_sweeps = 0;
   st->sink_err_sweep = 0;
+  st->gdone = 0;
   st->t0 = globaltimer();
 }
 
@@ -431,8 +432,9 @@ inline unsigned grid1d(int64_t work, int threads) {
 }  // namespace
 
 void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
-  row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
-                                                                       write ? 0 : 1);
+  if (d.n >= 1)
+    row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
+                                                                         write ? 0 : 1);
   if (write) flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 
@@ -444,6 +446,20 @@ void launch_col_update(const BapgDev& d, cudaStream_t s) {
   col_combine_kernel<<<grid1d(d.m, 256), 256, 0, s>>>(d);
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
   col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
+}
+
+void launch_col_partial(const BapgDev& d, cudaStream_t s) {
+  if (d.n < 1) return;
+  const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
+  dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
+            static_cast<unsigned>(d.chunks));
+  col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
+}
+
+void launch_col_write(const BapgDev& d, cudaStream_t s) {
+  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
+  if (d.n >= 1) col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 

@@ -36,6 +36,7 @@ struct DevStatus {
   int zero_index;  // lowest offending line (atomicMin)
   int sink_sweeps; // last Sinkhorn sweep count
   int sink_err_sweep;
+  int gdone;       // sharded solver: globally agreed done (set by the finalize)
   unsigned long long t0;  // %globaltimer at reset
 };
 
@@ -104,6 +105,11 @@ void launch_row_update(const BapgDev& d, bool write, cudaStream_t s);
 // combine + checks, then W_new = P ⊙ e^E · diag(ν/colsum) with fused
 // split-gap / rel-change / objective partials.
 void launch_col_update(const BapgDev& d, cudaStream_t s);
+// The two data passes of half-step b separately (sharded solver): chunk
+// partials of (max, Σ π e^{E−max}, Σ π) per column, and — once col_max /
+// col_scale / col_dev hold the global merge — the W' write pass.
+void launch_col_partial(const BapgDev& d, cudaStream_t s);
+void launch_col_write(const BapgDev& d, cudaStream_t s);
 // Reduces the per-line partials in fixed order into rec[iter] / rec[iter-1],
 // evaluates the stop rule (solvers.cpp:191,208) and advances st->iter.
 void launch_finalize(const BapgDev& d, double rel_tol, bool tail, cudaStream_t s);

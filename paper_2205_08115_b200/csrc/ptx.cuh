@@ -101,6 +101,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem, const CUtensorMap* m
       : "memory");
 }
 
+// 3-D variant: box at (c0 inner, c1 row, c2 block).
+__device__ __forceinline__ void tma_load_3d_2sm(void* smem, const CUtensorMap* map,
+                                                uint32_t bar_cluster, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

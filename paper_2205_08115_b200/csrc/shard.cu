@@ -1,0 +1,703 @@
+// shard.cu — one rank of the row-sharded multi-GPU BAPG.
+//
+// Rank r owns rows [r·n_r, r·n_r + n_r) of π, w and D_X (n_r = ceil(n/P)
+// rounded up to 64; rows ≥ n are zero padding).  D_Y is replicated.  Per
+// half-step (reference solvers.cpp:164-177):
+//   GEMM1   Vᵀ[:, rows_r] = D_Y · X_rᵀ       → slot r of the gather buffer
+//   ── all-gather (NCCL, in place): the buffer is Vᵀ as [P][m][n_r] blocks ──
+//   GEMM2   G_r = D_X[rows_r, :] · V          (B read through a blocked-K
+//                                              3-D TMA map over the P blocks)
+//   a: row projection, fully local
+//   b: local column (max, Σ, Σπ) partials → slot r
+//   ── all-gather of the column partials; merged in fixed rank order ──
+//      column write pass, local fp64 diagnostic partial sums
+//   ── all-reduce (sum) of 8 diagnostic scalars, all-reduce (max) of flags ──
+//   finalize: identical record / stop rule / error decision on every rank.
+// The collectives are issued by the caller (torch.distributed over NCCL, or
+// the single-GPU emulation in tests) between gwb_shard_phase() calls on the
+// shard's stream; every kernel is a no-op once the solve is done, while the
+// collectives always run, so ranks never diverge in their collective calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/gwb.h"
+#include "../../include/gwb_ext.h"
+#include "devutil.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "solver.cuh"
+#include "standalone.cuh"
+
+namespace gwb {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kDiag = 8;  // ⟨G,W⟩, rowdev, ⟨G,W'⟩, split, diff, ‖W‖², ⟨G,P⟩, coldev
+constexpr int kErr = 8;   // ovfA, zeroA, ovfB, zeroB, nonfinite, −row idx, −col idx, unused
+
+__global__ void shard_col_local_kernel(BapgDev d, double* slot, int64_t m) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double mx = -INFINITY, s = 0.0, p = 0.0;
+  if (!d.st->done && d.n >= 1) {
+    for (int c = 0; c < d.chunks; ++c) {
+      const int64_t o = static_cast<int64_t>(c) * m + j;
+      const double cm = d.col_pmax[o], cs = d.col_psum[o];
+      if (cm > -INFINITY) {
+        if (cm > mx) {
+          s = s * exp(mx - cm) + cs;
+          mx = cm;
+        } else {
+          s += cs * exp(cm - mx);
+        }
+      } else if (isnan(cm)) {
+        mx = NAN;
+      }
+      p += d.col_psump[o];
+    }
+  }
+  slot[j] = mx;
+  slot[m + j] = s;
+  slot[2 * m + j] = p;
+}
+
+// Merge the P rank slots in rank order (deterministic), raise column errors.
+__global__ void shard_col_global_kernel(BapgDev d, const double* stats, int P) {
+  if (d.st->done) return;
+  const int64_t m = d.m;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double mx = -INFINITY, s = 0.0, p = 0.0;
+  bool nan = false;
+  for (int r = 0; r < P; ++r) {
+    const double* sl = stats + static_cast<int64_t>(r) * 3 * m;
+    const double cm = sl[j], cs = sl[m + j];
+    if (isnan(cm)) nan = true;
+    if (cm > -INFINITY) {
+      if (cm > mx) {
+        s = s * exp(mx - cm) + cs;
+        mx = cm;
+      } else {
+        s += cs * exp(cm - mx);
+      }
+    }
+    p += sl[2 * m + j];
+  }
+  if (mx > 700.0) atomicOr(&d.st->flags, kFlagOverflowB);
+  if (nan || !(s > 0.0) || !isfinite(s)) {
+    atomicOr(&d.st->flags, kFlagZeroB);
+    atomicMin(&d.st->zero_index, static_cast<int>(j));
+  }
+  d.col_max[j] = static_cast<float>(mx);
+  d.col_scale[j] = static_cast<float>(d.nu64[j] / s);
+  const double dev = p - d.nu64[j];
+  d.col_dev[j] = dev * dev;
+}
+
+__device__ double block_sum_d(double v) {
+  __shared__ double sh[32];
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t += sh[q];
+  return t;
+}
+
+// Local fp64 partial sums + local error flags (always written: the
+// all-reduce that follows runs on every rank unconditionally).
+__global__ void shard_diag_kernel(BapgDev d, double* diag, double* err, int rank,
+                                  int64_t row_begin, int tail) {
+  const DevStatus* st = d.st;
+  // The tail pass runs after convergence (gdone set) but not after errors.
+  const bool active = tail ? st->flags == 0 : !st->gdone;
+  double acc[kDiag] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (active) {
+    for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) {
+      acc[0] += d.row_part[i].gw;
+      acc[1] += d.row_part[i].rowdev;
+      if (!tail) {
+        const ColWritePart c = d.cw_part[i];
+        acc[2] += c.gw;
+        acc[3] += c.split;
+        acc[4] += c.diff;
+        acc[5] += c.wold;
+        acc[6] += c.gp;
+      }
+    }
+    if (!tail && rank == 0)
+      for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) acc[7] += d.col_dev[j];
+  }
+  for (int q = 0; q < kDiag; ++q) {
+    const double t = block_sum_d(acc[q]);
+    if (threadIdx.x == 0) diag[q] = t;
+  }
+  if (threadIdx.x == 0) {
+    const int f = active ? st->flags : 0;
+    err[0] = (f & kFlagOverflowA) ? 1.0 : 0.0;
+    err[1] = (f & kFlagZeroA) ? 1.0 : 0.0;
+    err[2] = (f & kFlagOverflowB) ? 1.0 : 0.0;
+    err[3] = (f & kFlagZeroB) ? 1.0 : 0.0;
+    err[4] = (f & kFlagNonFinite) ? 1.0 : 0.0;
+    err[5] = (f & kFlagZeroA) ? -static_cast<double>(row_begin + st->zero_index) : -1e18;
+    err[6] = (f & kFlagZeroB) ? -static_cast<double>(st->zero_index) : -1e18;
+    err[7] = 0.0;
+  }
+}
+
+// Global record / stop rule / error decision from the all-reduced vectors.
+__global__ void shard_finalize_kernel(BapgDev d, const double* diag, const double* err,
+                                      double rel_tol, int tail) {
+  DevStatus* st = d.st;
+  if (st->gdone) {
+    st->done = 1;
+    if (!tail || st->flags) return;
+  }
+  auto slot = [&](int it) { return it <= d.max_rec ? it : d.max_rec + 1; };
+  if (tail) {
+    const int k = st->iter - 1;
+    d.rec[slot(k)].mw_w = diag[0];
+    d.rec[slot(k)].row_sq = diag[1];
+    return;
+  }
+  const int k = st->iter;
+  int gflags = 0;
+  if (err[0] > 0.5) gflags |= kFlagOverflowA;
+  if (err[1] > 0.5) gflags |= kFlagZeroA;
+  if (err[2] > 0.5) gflags |= kFlagOverflowB;
+  if (err[3] > 0.5) gflags |= kFlagZeroB;
+  if (err[4] > 0.5) gflags |= kFlagNonFinite;
+  if (gflags) {
+    st->flags = gflags;
+    st->zero_index = static_cast<int>((gflags & kFlagZeroA) ? -err[5] : -err[6]);
+    st->err_iter = k;
+    st->done = st->gdone = 1;
+    return;
+  }
+  if (k >= 2) {
+    d.rec[slot(k - 1)].mw_w = diag[0];
+    d.rec[slot(k - 1)].row_sq = diag[1];
+  }
+  DevRecord& r = d.rec[slot(k)];
+  r.mpi_w = diag[2];
+  r.split_sq = diag[3];
+  r.diff_sq = diag[4];
+  r.wold_sq = diag[5];
+  r.mpi_pi = diag[6];
+  r.col_sq = diag[7];
+  r.elapsed = 1e-9 * static_cast<double>(globaltimer() - st->t0);
+  st->iter = k + 1;
+  // Local flags (if any) were all clean; keep the local done in sync.
+  st->flags = 0;
+  st->done = 0;
+  if (stop_rule(sqrt(diag[4]) / sqrt(diag[5]), rel_tol)) {
+    st->converged = 1;
+    st->done = st->gdone = 1;
+  }
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  GWB_CUDA(cudaMalloc(&p, count * sizeof(T) + 256));
+  GWB_CUDA(cudaMemset(p, 0, count * sizeof(T) + 256));
+  GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+class ShardEngine {
+ public:
+  ShardEngine(const gwb_config& cfg, int64_t n, int64_t m, int rank, int world, int device,
+              cudaStream_t stream)
+      : cfg_(cfg), n_(n), m_(m), rank_(rank), world_(world), dev_(device), s_(stream) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    if (!s_) {
+      GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+      own_stream_ = true;
+    }
+    prec_ = cfg.precision;
+    if (prec_ == GWB_PREC_AUTO) prec_ = GWB_PREC_BF16X3;
+    bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2;
+    planes_ = prec_ == GWB_PREC_BF16X3 ? 3 : (prec_ == GWB_PREC_TF32 ? 1 : 2);
+    esize_ = bf16_ ? 2 : 4;
+    aux_mode_ = prec_ == GWB_PREC_TF32 ? 1 : prec_ == GWB_PREC_3XTF32 ? 2
+                : prec_ == GWB_PREC_BF16X3 ? 3 : 4;
+    nr_ = round_up((n_ + world_ - 1) / world_, 64);
+    row_begin_ = static_cast<int64_t>(rank_) * nr_;
+    rows_valid_ = std::max<int64_t>(0, std::min<int64_t>(nr_, n_ - row_begin_));
+    ldk_ = round_up(nr_ * world_, 64);
+    ldm_ = round_up(m_, 64);
+    const size_t nm = static_cast<size_t>(nr_) * ldm_;
+    Dx_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_));
+    Dy_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
+    Dx_aux_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_));
+    Dy_aux_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
+    P_ = keep(dalloc<float>(nm));
+    P_aux_ = keep(dalloc<float>(nm * 3 / 2));
+    for (int q = 0; q < 2; ++q) {
+      W_[q] = keep(dalloc<float>(nm));
+      W_aux_[q] = keep(dalloc<float>(nm * 3 / 2));
+    }
+    G_ = keep(dalloc<float>(nm));
+    mu32_ = keep(dalloc<float>(nr_));
+    nu32_ = keep(dalloc<float>(ldm_));
+    mu64_ = keep(dalloc<double>(nr_));
+    nu64_ = keep(dalloc<double>(ldm_));
+    row_part_ = keep(dalloc<RowPart>(nr_));
+    cw_part_ = keep(dalloc<ColWritePart>(nr_));
+    const int64_t col_blocks = (m_ + 127) / 128;
+    chunks_ = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>((std::max<int64_t>(rows_valid_, 1) + 63) / 64,
+                             (4 * 148 + col_blocks - 1) / col_blocks)));
+    col_pmax_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
+    col_psum_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
+    col_psump_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_max_ = keep(dalloc<float>(ldm_));
+    col_scale_ = keep(dalloc<float>(ldm_));
+    col_dev_ = keep(dalloc<double>(ldm_));
+    st_ = keep(dalloc<DevStatus>(1));
+    rec_ = keep(dalloc<DevRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
+  }
+  ~ShardEngine() {
+    cudaSetDevice(dev_);
+    cudaStreamSynchronize(s_);
+    for (auto* p : plans_) gemm_plan_destroy(p);
+    for (void* p : bufs_) cudaFree(p);
+    if (own_stream_) cudaStreamDestroy(s_);
+  }
+
+  int64_t rows_per_shard() const { return nr_; }
+  int64_t row_begin() const { return row_begin_; }
+  int64_t rows_valid() const { return rows_valid_; }
+  int planes() const { return planes_; }
+  int esize() const { return esize_; }
+  int64_t vt_bytes() const {
+    return static_cast<int64_t>(planes_) * world_ * m_ * nr_ * esize_;
+  }
+  int64_t stats_bytes() const { return static_cast<int64_t>(world_) * 3 * m_ * 8; }
+  cudaStream_t stream() const { return s_; }
+
+  void set_comm(void* vt, void* stats, double* diag, double* err) {
+    vt_ = static_cast<uint8_t*>(vt);
+    stats_ = static_cast<double*>(stats);
+    diag_ = diag;
+    err_ = err;
+  }
+
+  // dx_rows: rows_valid × n fp32 (leading dim ldx) = D_X[row_begin : …, :];
+  // dy: m × m; mu_rows: rows_valid; nu: m.  Device pointers.
+  void load(const float* dx_rows, int64_t ldx, const float* dy, int64_t ldy, const float* mu_rows,
+            const float* nu) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    if (!vt_) throw CudaError("gwb_shard: set_comm must precede load");
+    if (rows_valid_ > 0)
+      GWB_CUDA(cudaMemcpy2DAsync(Dx_, ldk_ * 4, dx_rows, ldx * 4, n_ * 4, rows_valid_,
+                                 cudaMemcpyDeviceToDevice, s_));
+    GWB_CUDA(cudaMemcpy2DAsync(Dy_, ldm_ * 4, dy, ldy * 4, m_ * 4, m_, cudaMemcpyDeviceToDevice, s_));
+    if (rows_valid_ > 0)
+      GWB_CUDA(cudaMemcpyAsync(mu32_, mu_rows, 4 * rows_valid_, cudaMemcpyDeviceToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(nu32_, nu, 4 * m_, cudaMemcpyDeviceToDevice, s_));
+    std::vector<float> h_mu(std::max<int64_t>(rows_valid_, 1)), h_nu(m_);
+    if (rows_valid_ > 0)
+      GWB_CUDA(cudaMemcpyAsync(h_mu.data(), mu_rows, 4 * rows_valid_, cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaMemcpyAsync(h_nu.data(), nu, 4 * m_, cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    std::vector<double> d_mu(h_mu.begin(), h_mu.end()), d_nu(h_nu.begin(), h_nu.end());
+    GWB_CUDA(cudaMemcpyAsync(mu64_, d_mu.data(), 8 * std::max<int64_t>(rows_valid_, 1),
+                             cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(nu64_, d_nu.data(), 8 * m_, cudaMemcpyHostToDevice, s_));
+    // Operand copies of the structure matrices.
+    if (bf16_) {
+      launch_to_bf16(Dx_, nr_, ldk_, ldk_, Dx_aux_, s_);
+      launch_to_bf16(Dy_, m_, ldm_, ldm_, Dy_aux_, s_);
+    } else {
+      launch_tf32_aux(Dx_, nr_, ldk_, ldk_, Dx_aux_, aux_mode_, s_);
+      launch_tf32_aux(Dy_, m_, ldm_, ldm_, Dy_aux_, aux_mode_, s_);
+    }
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    build_plans();
+  }
+
+  void reset() {
+    GWB_CUDA(cudaSetDevice(dev_));
+    launch_status_reset(st_, s_);
+    if (rows_valid_ > 0) {
+      launch_product_coupling(mu32_, nu32_, rows_valid_, m_, ldm_, W_[0], s_);
+      launch_tf32_aux(W_[0], nr_, m_, ldm_, W_aux_[0], aux_mode_, s_);
+    }
+    parity_ = 0;
+    GWB_CUDA(cudaGetLastError());
+  }
+
+  // Phases between collectives (see file comment).
+  void phase(int ph) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    const int q = parity_;
+    BapgDev d = view(q);
+    switch (ph) {
+      case 0:  // A1: Vᵀ slot ← D_Y · W_rᵀ
+        GWB_CUDA(gemm_launch(g1_[q], s_));
+        break;
+      case 1:  // A2: G_r, row projection
+        GWB_CUDA(gemm_launch(g2_, s_));
+        launch_row_update(d, true, s_);
+        break;
+      case 2:  // B1
+        GWB_CUDA(gemm_launch(g1p_, s_));
+        break;
+      case 3:  // B2: G_r, local column partials → stats slot
+        GWB_CUDA(gemm_launch(g2_, s_));
+        launch_col_partial(d, s_);
+        shard_col_local_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
+            d, stats_ + static_cast<int64_t>(rank_) * 3 * m_, m_);
+        break;
+      case 4:  // B3: global column merge, write pass, local diagnostics
+        shard_col_global_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
+            d, stats_, world_);
+        launch_col_write(d, s_);
+        shard_diag_kernel<<<1, 512, 0, s_>>>(d, diag_, err_, rank_, row_begin_, 0);
+        break;
+      case 5:  // F: global finalize; w' becomes w
+        shard_finalize_kernel<<<1, 1, 0, s_>>>(d, diag_, err_, cfg_.rel_tol, 0);
+        parity_ ^= 1;
+        break;
+      case 6:  // tail A1 (chain on the final w; runs after convergence)
+        GWB_CUDA(gemm_launch(g1t_[q], s_));
+        break;
+      case 7:  // tail A2: diagnostics-only row pass
+        GWB_CUDA(gemm_launch(g2t_, s_));
+        launch_row_update(d, false, s_);
+        shard_diag_kernel<<<1, 512, 0, s_>>>(d, diag_, err_, rank_, row_begin_, 1);
+        break;
+      case 8:  // tail F
+        shard_finalize_kernel<<<1, 1, 0, s_>>>(d, diag_, err_, 0.0, 1);
+        break;
+      default:
+        throw CudaError("gwb_shard_phase: unknown phase");
+    }
+    GWB_CUDA(cudaGetLastError());
+  }
+
+  DevStatus status() {
+    DevStatus h;
+    GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    return h;
+  }
+
+  // After the loop the current w is W[(iterations used) % 2].
+  void sync_parity() {
+    const DevStatus h = status();
+    parity_ = (h.iter - 1) & 1;
+  }
+
+  std::vector<DevRecord> records(int count) {
+    std::vector<DevRecord> r(static_cast<size_t>(count) + 1);
+    GWB_CUDA(cudaMemcpyAsync(r.data(), rec_, sizeof(DevRecord) * (count + 1), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    return r;
+  }
+
+  // Local rows of π and w as row-major fp64 (rows_valid × m).
+  void rows(double* pi, double* w) {
+    std::vector<float> buf(static_cast<size_t>(nr_) * ldm_);
+    auto get = [&](const float* src, double* dst) {
+      if (!dst || rows_valid_ == 0) return;
+      GWB_CUDA(cudaMemcpyAsync(buf.data(), src, 4 * nr_ * ldm_, cudaMemcpyDeviceToHost, s_));
+      GWB_CUDA(cudaStreamSynchronize(s_));
+      for (int64_t i = 0; i < rows_valid_; ++i)
+        for (int64_t j = 0; j < m_; ++j) dst[i * m_ + j] = buf[i * ldm_ + j];
+    };
+    get(P_, pi);
+    get(W_[parity_], w);
+  }
+
+ private:
+  template <class T>
+  T* keep(T* p) {
+    bufs_.push_back(p);
+    return p;
+  }
+
+  BapgDev view(int q) const {
+    BapgDev d;
+    std::memset(&d, 0, sizeof(d));
+    d.n = rows_valid_;
+    d.m = m_;
+    d.ld = ldm_;
+    d.inv_rho = static_cast<float>(1.0 / cfg_.rho);
+    d.G = G_;
+    d.mu = mu32_;
+    d.nu = nu32_;
+    d.mu64 = mu64_;
+    d.nu64 = nu64_;
+    d.P = P_;
+    d.P_aux = P_aux_;
+    d.W = W_[q];
+    d.W_new = W_[1 - q];
+    d.W_aux = W_aux_[1 - q];
+    d.aux_mode = aux_mode_;
+    d.plane = nr_ * ldm_;
+    d.row_part = row_part_;
+    d.cw_part = cw_part_;
+    d.col_pmax = col_pmax_;
+    d.col_psum = col_psum_;
+    d.col_psump = col_psump_;
+    d.col_max = col_max_;
+    d.col_scale = col_scale_;
+    d.col_dev = col_dev_;
+    d.chunks = chunks_;
+    d.st = st_;
+    d.rec = rec_;
+    d.max_rec = cfg_.max_iters;
+    return d;
+  }
+
+  // Gather buffer layout [world][planes][m][n_r]: rank r's planes are one
+  // contiguous chunk, so a single in-place all-gather moves every plane.
+  void* slot(int plane, int rank) const {
+    return vt_ + ((static_cast<int64_t>(rank) * planes_ + plane) * m_ * nr_) * esize_;
+  }
+  void* plane_base(int plane) const {
+    return vt_ + (static_cast<int64_t>(plane) * m_ * nr_) * esize_;
+  }
+  void* aux_plane(float* aux, int p) const {
+    return reinterpret_cast<uint8_t*>(aux) + static_cast<int64_t>(p) * nr_ * ldm_ * 2;
+  }
+
+  GemmPlan* make1(float* X, float* X_aux, const int* skip) {
+    GemmDesc d;
+    d.M = m_;
+    d.N = nr_;
+    d.K = m_;
+    d.ldb = ldm_;
+    d.lda = ldm_;
+    d.ldc = nr_;
+    d.skip = skip;
+    if (bf16_) {
+      d.bf16_planes = planes_;
+      d.a_bf16 = Dy_aux_;
+      for (int p = 0; p < planes_; ++p) d.b_bf16[p] = aux_plane(X_aux, p);
+      d.c_planes = planes_;
+      for (int p = 0; p < planes_; ++p) d.c_bf16[p] = slot(p, rank_);
+    } else {
+      const bool tf32 = prec_ == GWB_PREC_TF32;
+      d.a = tf32 ? Dy_aux_ : Dy_;
+      d.a_lo = tf32 ? nullptr : Dy_aux_;
+      d.b = tf32 ? X_aux : X;
+      d.b_lo = tf32 ? nullptr : X_aux;
+      d.c = static_cast<float*>(slot(0, rank_));
+      d.c_aux = tf32 ? nullptr : static_cast<float*>(slot(1, rank_));
+      d.aux_mode = tf32 ? 1 : 2;
+      d.three_pass = !tf32;
+    }
+    GemmPlan* p = gemm_plan_create(d);
+    plans_.push_back(p);
+    return p;
+  }
+
+  GemmPlan* make2(const int* skip) {
+    GemmDesc d;
+    d.M = nr_;
+    d.N = m_;
+    d.K = nr_ * world_;
+    d.lda = ldk_;
+    d.b_block_k = nr_;
+    d.b_block_stride = static_cast<int64_t>(planes_) * m_ * nr_;
+    d.c = G_;
+    d.ldc = ldm_;
+    d.skip = skip;
+    if (bf16_) {
+      d.bf16_planes = planes_;
+      d.a_bf16 = Dx_aux_;
+      for (int p = 0; p < planes_; ++p) d.b_bf16[p] = plane_base(p);
+    } else {
+      const bool tf32 = prec_ == GWB_PREC_TF32;
+      d.a = tf32 ? Dx_aux_ : Dx_;
+      d.a_lo = tf32 ? nullptr : Dx_aux_;
+      d.b = static_cast<const float*>(plane_base(0));
+      d.b_lo = tf32 ? nullptr : static_cast<const float*>(plane_base(1));
+      d.three_pass = !tf32;
+    }
+    GemmPlan* p = gemm_plan_create(d);
+    plans_.push_back(p);
+    return p;
+  }
+
+  void build_plans() {
+    for (int q = 0; q < 2; ++q) {
+      g1_[q] = make1(W_[q], W_aux_[q], &st_->done);
+      g1t_[q] = make1(W_[q], W_aux_[q], &st_->flags);
+    }
+    g1p_ = make1(P_, P_aux_, &st_->done);
+    g2_ = make2(&st_->done);
+    g2t_ = make2(&st_->flags);
+  }
+
+  gwb_config cfg_;
+  int64_t n_, m_;
+  int rank_, world_, dev_;
+  cudaStream_t s_;
+  bool own_stream_ = false;
+  int prec_, planes_, esize_, aux_mode_;
+  bool bf16_;
+  int64_t nr_, row_begin_, rows_valid_, ldk_, ldm_;
+  int parity_ = 0;
+  std::vector<void*> bufs_;
+  std::vector<GemmPlan*> plans_;
+  float *Dx_, *Dy_, *Dx_aux_, *Dy_aux_, *P_, *P_aux_, *W_[2], *W_aux_[2], *G_;
+  float *mu32_, *nu32_;
+  double *mu64_, *nu64_;
+  RowPart* row_part_;
+  ColWritePart* cw_part_;
+  float *col_pmax_, *col_psum_, *col_max_, *col_scale_;
+  double *col_psump_, *col_dev_;
+  int chunks_ = 1;
+  DevStatus* st_;
+  DevRecord* rec_;
+  uint8_t* vt_ = nullptr;
+  double* stats_ = nullptr;
+  double* diag_ = nullptr;
+  double* err_ = nullptr;
+  GemmPlan *g1_[2] = {nullptr, nullptr}, *g1t_[2] = {nullptr, nullptr}, *g1p_ = nullptr,
+           *g2_ = nullptr, *g2t_ = nullptr;
+};
+
+}  // namespace gwb
+
+// ---------------------------------------------------------------------------
+// C-ABI (include/gwb_ext.h)
+// ---------------------------------------------------------------------------
+struct gwb_shard {
+  std::unique_ptr<gwb::ShardEngine> eng;
+  int64_t n, m;
+};
+
+namespace {
+template <class F>
+int32_t shard_guard(gwb_status* st, F&& f) {
+  try {
+    f();
+    if (st) std::memset(st, 0, sizeof(*st));
+    return GWB_OK;
+  } catch (const std::exception& e) {
+    if (st) {
+      std::memset(st, 0, sizeof(*st));
+      st->code = GWB_ERR_RUNTIME;
+      std::snprintf(st->message, sizeof(st->message), "%s", e.what());
+    }
+    return GWB_ERR_RUNTIME;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int32_t gwb_shard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t rank, int32_t world,
+                         int32_t device, void* stream, gwb_shard** out, gwb_status* st) {
+  return shard_guard(st, [&] {
+    if (!cfg || n < 1 || m < 1 || world < 1 || rank < 0 || rank >= world)
+      throw std::invalid_argument("gwb_shard_create: bad arguments");
+    auto* s = new gwb_shard();
+    s->n = n;
+    s->m = m;
+    s->eng.reset(new gwb::ShardEngine(*cfg, n, m, rank, world, device,
+                                      static_cast<cudaStream_t>(stream)));
+    *out = s;
+  });
+}
+
+int32_t gwb_shard_layout(gwb_shard* s, int64_t* rows_per_shard, int64_t* row_begin,
+                         int64_t* rows_valid, int32_t* planes, int32_t* elem_bytes,
+                         int64_t* vt_bytes, int64_t* stats_bytes, gwb_status* st) {
+  return shard_guard(st, [&] {
+    *rows_per_shard = s->eng->rows_per_shard();
+    *row_begin = s->eng->row_begin();
+    *rows_valid = s->eng->rows_valid();
+    *planes = s->eng->planes();
+    *elem_bytes = s->eng->esize();
+    *vt_bytes = s->eng->vt_bytes();
+    *stats_bytes = s->eng->stats_bytes();
+  });
+}
+
+int32_t gwb_shard_set_comm(gwb_shard* s, void* vt_gather, void* col_stats, double* diag,
+                           double* err, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->set_comm(vt_gather, col_stats, diag, err); });
+}
+
+int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows, int64_t ldx, const float* dy,
+                              int64_t ldy, const float* mu_rows, const float* nu, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->load(dx_rows, ldx, dy, ldy, mu_rows, nu); });
+}
+
+int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->reset(); });
+}
+
+int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->phase(phase); });
+}
+
+int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st) {
+  return shard_guard(st, [&] { *stream = static_cast<void*>(s->eng->stream()); });
+}
+
+int32_t gwb_shard_status(gwb_shard* s, int32_t* done, int32_t* iter, int32_t* flags,
+                         int32_t* converged, int32_t* err_iter, int32_t* zero_index,
+                         gwb_status* st) {
+  return shard_guard(st, [&] {
+    const gwb::DevStatus h = s->eng->status();
+    *done = h.done;
+    *iter = h.iter;
+    *flags = h.flags;
+    *converged = h.converged;
+    *err_iter = h.err_iter;
+    *zero_index = h.zero_index;
+  });
+}
+
+int32_t gwb_shard_finish(gwb_shard* s, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->sync_parity(); });
+}
+
+int32_t gwb_shard_records(gwb_shard* s, int32_t count, gwb_record* out, gwb_status* st) {
+  return shard_guard(st, [&] {
+    const std::vector<gwb::DevRecord> r = s->eng->records(count);
+    for (int k = 1; k <= count; ++k) {
+      const gwb::DevRecord& d = r[k];
+      gwb_record& o = out[k - 1];
+      std::memset(&o, 0, sizeof(o));
+      o.iter = k;
+      o.objective = -0.25 * (d.mpi_pi + 2.0 * d.mpi_w + d.mw_w);
+      o.marginal_infeasibility = 0.5 * std::sqrt(d.col_sq) / static_cast<double>(s->m) +
+                                 0.5 * std::sqrt(d.row_sq) / static_cast<double>(s->n);
+      o.split_gap = std::sqrt(d.split_sq);
+      o.rel_change = std::sqrt(d.diff_sq) / std::sqrt(d.wold_sq);
+      o.elapsed_seconds = d.elapsed;
+    }
+  });
+}
+
+int32_t gwb_shard_rows(gwb_shard* s, double* pi_rows, double* w_rows, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->rows(pi_rows, w_rows); });
+}
+
+int32_t gwb_shard_destroy(gwb_shard* s) {
+  delete s;
+  return GWB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,348 @@
+"""Row-sharded multi-GPU BAPG orchestration.
+
+One process per GPU (torchrun).  Each rank owns a contiguous block of rows of
+π, w and D_X; D_Y is replicated.  The device work runs in ``libgwb.so``
+(``gwb_shard_*``, csrc/shard.cu); this module owns the communication
+buffers as torch tensors and issues the collectives between the phases on
+the shard's CUDA stream, so NCCL (NVLink/NVSwitch) transfers are ordered
+with the kernels without host synchronisation:
+
+  per iteration   phase 0 · all-gather(Vᵀ) · phase 1 · phase 2 ·
+                  all-gather(Vᵀ) · phase 3 · all-gather(col stats) · phase 4 ·
+                  all-reduce-sum(diag) · all-reduce-max(err) · phase 5
+  after the loop  phase 6 · all-gather(Vᵀ) · phase 7 · all-reduce(diag, err) ·
+                  phase 8
+
+`run_sharded` drives any list of shard engines with any `Comm`: real ranks
+(`TorchComm`, one local shard), several virtual ranks on one GPU
+(`EmuComm`, used by the GPU tests — there is only one GPU per box here), or
+the CPU mirror used by the gloo tests (tests/shard_mirror.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+from . import abi
+
+KBLOCK_ROWS = 64  # shard rows are padded to a multiple of the bf16 k-block
+
+
+@dataclass
+class ShardPlan:
+    """Row ownership, identical to ShardEngine (csrc/shard.cu)."""
+
+    n: int
+    world: int
+
+    @property
+    def rows_per_shard(self) -> int:
+        r = -(-self.n // self.world)
+        return -(-r // KBLOCK_ROWS) * KBLOCK_ROWS
+
+    def row_begin(self, rank: int) -> int:
+        return rank * self.rows_per_shard
+
+    def rows_valid(self, rank: int) -> int:
+        return max(0, min(self.rows_per_shard, self.n - self.row_begin(rank)))
+
+
+_P = C.c_void_p
+_I64P = C.POINTER(C.c_int64)
+_I32P = C.POINTER(C.c_int32)
+_ST = C.POINTER(abi.Status)
+_SIGS = {
+    "gwb_shard_create": (C.c_int32, [C.POINTER(abi.Config), C.c_int64, C.c_int64, C.c_int32,
+                                     C.c_int32, C.c_int32, _P, C.POINTER(_P), _ST]),
+    "gwb_shard_layout": (C.c_int32, [_P, _I64P, _I64P, _I64P, _I32P, _I32P, _I64P, _I64P, _ST]),
+    "gwb_shard_set_comm": (C.c_int32, [_P, _P, _P, _P, _P, _ST]),
+    "gwb_shard_load_device": (C.c_int32, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, _ST]),
+    "gwb_shard_reset": (C.c_int32, [_P, _ST]),
+    "gwb_shard_phase": (C.c_int32, [_P, C.c_int32, _ST]),
+    "gwb_shard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
+    "gwb_shard_status": (C.c_int32, [_P, _I32P, _I32P, _I32P, _I32P, _I32P, _I32P, _ST]),
+    "gwb_shard_finish": (C.c_int32, [_P, _ST]),
+    "gwb_shard_records": (C.c_int32, [_P, C.c_int32, C.POINTER(abi.Record), _ST]),
+    "gwb_shard_rows": (C.c_int32, [_P, _P, _P, _ST]),
+    "gwb_shard_destroy": (C.c_int32, [_P]),
+}
+
+
+def _lib():
+    lib = abi.load()
+    if not getattr(lib, "_shard_ready", False):
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        lib._shard_ready = True
+    return lib
+
+
+def _check(st: abi.Status):
+    abi.raise_for(st)
+
+
+class GpuShard:
+    """One rank's ShardEngine plus its torch-owned communication buffers."""
+
+    def __init__(self, cfg: abi.Config, n: int, m: int, rank: int, world: int,
+                 device: int = 0, stream=None):
+        import torch
+        self.torch = torch
+        self.lib = _lib()
+        self.n, self.m, self.rank, self.world = n, m, rank, world
+        st = abi.Status()
+        self.h = _P()
+        sp = None if stream is None else stream.cuda_stream
+        self.lib.gwb_shard_create(C.byref(cfg), n, m, rank, world, device, sp, C.byref(self.h),
+                                  C.byref(st))
+        _check(st)
+        rps, rb, rv = C.c_int64(), C.c_int64(), C.c_int64()
+        pl, es, vb, sb = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        self.lib.gwb_shard_layout(self.h, C.byref(rps), C.byref(rb), C.byref(rv), C.byref(pl),
+                                  C.byref(es), C.byref(vb), C.byref(sb), C.byref(st))
+        _check(st)
+        self.rows_per_shard, self.row_begin, self.rows_valid = rps.value, rb.value, rv.value
+        self.planes, self.elem_bytes = pl.value, es.value
+        dev = torch.device("cuda", device)
+        self.vt = torch.zeros(vb.value, dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(world * 3 * m, dtype=torch.float64, device=dev)
+        self.diag = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.err = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.lib.gwb_shard_set_comm(self.h, self.vt.data_ptr(), self.stats.data_ptr(),
+                                    self.diag.data_ptr(), self.err.data_ptr(), C.byref(st))
+        _check(st)
+        sp = _P()
+        self.lib.gwb_shard_stream(self.h, C.byref(sp), C.byref(st))
+        self.stream = torch.cuda.ExternalStream(sp.value, device=dev)
+        self.max_iters = cfg.max_iters
+
+    def load(self, dx_rows, dy, mu_rows, nu):
+        """Device fp32 tensors: dx_rows (rows_valid × n, any leading dim),
+        dy (m × m), mu_rows (rows_valid), nu (m)."""
+        st = abi.Status()
+        self.torch.cuda.synchronize()
+        self.lib.gwb_shard_load_device(self.h, dx_rows.data_ptr(), dx_rows.stride(0),
+                                       dy.data_ptr(), dy.stride(0), mu_rows.data_ptr(),
+                                       nu.data_ptr(), C.byref(st))
+        _check(st)
+
+    def reset(self):
+        st = abi.Status()
+        self.lib.gwb_shard_reset(self.h, C.byref(st))
+        _check(st)
+
+    def phase(self, k: int):
+        st = abi.Status()
+        self.lib.gwb_shard_phase(self.h, k, C.byref(st))
+        _check(st)
+
+    def status(self) -> dict:
+        st = abi.Status()
+        v = [C.c_int32() for _ in range(6)]
+        self.lib.gwb_shard_status(self.h, *[C.byref(x) for x in v], C.byref(st))
+        _check(st)
+        keys = ("done", "iter", "flags", "converged", "err_iter", "zero_index")
+        return {k: x.value for k, x in zip(keys, v)}
+
+    def finish(self):
+        st = abi.Status()
+        self.lib.gwb_shard_finish(self.h, C.byref(st))
+        _check(st)
+
+    def records(self, count: int):
+        st = abi.Status()
+        out = (abi.Record * max(count, 1))()
+        self.lib.gwb_shard_records(self.h, count, out, C.byref(st))
+        _check(st)
+        return list(out[:count])
+
+    def rows(self):
+        import numpy as np
+        st = abi.Status()
+        pi = np.zeros((self.rows_valid, self.m))
+        w = np.zeros((self.rows_valid, self.m))
+        self.lib.gwb_shard_rows(self.h, pi.ctypes.data, w.ctypes.data, C.byref(st))
+        _check(st)
+        return pi, w
+
+    def close(self):
+        if self.h:
+            self.lib.gwb_shard_destroy(self.h)
+            self.h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+class TorchComm:
+    """Collectives for one local shard per process via torch.distributed
+    (NCCL on the GPU — NVLink/NVSwitch — or gloo for the CPU mirror)."""
+
+    def __init__(self, dist, rank: int, world: int, inplace_gather: bool = True):
+        self.dist, self.rank, self.world = dist, rank, world
+        self.inplace = inplace_gather
+
+    def _gather(self, buf):
+        view = buf.view(self.world, -1)
+        if self.inplace:
+            self.dist.all_gather_into_tensor(view, view[self.rank])
+        else:
+            parts = list(view.unbind(0))
+            self.dist.all_gather(parts, view[self.rank].clone())
+
+    def gather_vt(self, shards):
+        s = shards[0]
+        with _stream(s):
+            self._gather(s.vt)
+
+    def gather_stats(self, shards):
+        s = shards[0]
+        with _stream(s):
+            self._gather(s.stats)
+
+    def reduce_diag(self, shards):
+        s = shards[0]
+        with _stream(s):
+            self.dist.all_reduce(s.diag, op=self.dist.ReduceOp.SUM)
+            self.dist.all_reduce(s.err, op=self.dist.ReduceOp.MAX)
+
+
+class EmuComm:
+    """All `world` shards live in this process (one GPU, shared stream):
+    collectives become device copies / reductions in rank order."""
+
+    def gather_vt(self, shards):
+        self._gather(shards, "vt")
+
+    def gather_stats(self, shards):
+        self._gather(shards, "stats")
+
+    @staticmethod
+    def _gather(shards, attr):
+        world = len(shards)
+        with _stream(shards[0]):
+            views = [getattr(s, attr).view(world, -1) for s in shards]
+            for r in range(world):
+                for q in range(world):
+                    if q != r:
+                        views[q][r].copy_(views[r][r])
+
+    @staticmethod
+    def reduce_diag(shards):
+        with _stream(shards[0]):
+            total = shards[0].diag.clone()
+            mx = shards[0].err.clone()
+            for s in shards[1:]:
+                total += s.diag
+                mx = mx.maximum(s.err)
+            for s in shards:
+                s.diag.copy_(total)
+                s.err.copy_(mx)
+
+
+class _stream:
+    def __init__(self, shard):
+        self.s = getattr(shard, "stream", None)
+
+    def __enter__(self):
+        if self.s is not None:
+            import torch
+            self.ctx = torch.cuda.stream(self.s)
+            self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *e):
+        if self.s is not None:
+            self.ctx.__exit__(*e)
+        return False
+
+
+def _all_phase(shards, k):
+    for s in shards:
+        s.phase(k)
+
+
+def iterate_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> None:
+    """Enqueue up to `iters` iterations of the phase / collective schedule.
+    Every rank issues the same collectives every iteration (kernels no-op
+    once done); the globally agreed `done` flag is polled every
+    `poll_every` iterations (poll_every=0: never, no host synchronisation)."""
+    for it in range(1, iters + 1):
+        _all_phase(shards, 0)
+        comm.gather_vt(shards)
+        _all_phase(shards, 1)
+        _all_phase(shards, 2)
+        comm.gather_vt(shards)
+        _all_phase(shards, 3)
+        comm.gather_stats(shards)
+        _all_phase(shards, 4)
+        comm.reduce_diag(shards)
+        _all_phase(shards, 5)
+        if poll_every and (it % poll_every == 0 or it == iters):
+            if shards[0].status()["done"]:
+                break
+
+
+def finish_sharded(shards: List, comm) -> dict:
+    """Objective of the last record (one more chain) and final parity."""
+    st = shards[0].status()
+    if not st["flags"]:
+        _all_phase(shards, 6)
+        comm.gather_vt(shards)
+        _all_phase(shards, 7)
+        comm.reduce_diag(shards)
+        _all_phase(shards, 8)
+    for s in shards:
+        s.finish()
+    return shards[0].status()
+
+
+def run_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> dict:
+    """Full sharded solve: iterations, then the tail record."""
+    iterate_sharded(shards, comm, iters, poll_every)
+    return finish_sharded(shards, comm)
+
+
+def raise_shard_flags(st: dict):
+    """Reference error semantics from the agreed flags (solvers.cpp:164-189)."""
+    f, it = st["flags"], st["err_iter"]
+    if not f:
+        return
+
+    def num(detail):
+        raise abi.NumericalInstabilityError(
+            f"numerical instability in bapg at iteration {it}: {detail}", "bapg", it)
+
+    if f & 1:
+        num("exp overflow; increase rho")
+    if f & 2:
+        num(f"row {st['zero_index']} has nonpositive sum; cannot rescale")
+    if f & 4:
+        num("exp overflow; increase rho")
+    if f & 8:
+        num(f"column {st['zero_index']} has nonpositive sum; cannot rescale")
+    num("non-finite iterate")
+
+
+def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, device=0,
+                      stream=None) -> List[GpuShard]:
+    """Build shard engines from full device tensors (tests / emulation)."""
+    import torch
+    n, m = dx.shape[0], dy.shape[0]
+    shards = []
+    for r in (range(world) if ranks is None else ranks):
+        s = GpuShard(cfg, n, m, r, world, device, stream)
+        rb, rv = s.row_begin, s.rows_valid
+        rows = dx[rb:rb + max(rv, 1)].contiguous()
+        murows = mu[rb:rb + max(rv, 1)].contiguous()
+        s.load(rows, dy.contiguous(), murows, nu.contiguous())
+        shards.append(s)
+    torch.cuda.synchronize()
+    return shards

@@ -1,0 +1,95 @@
+"""Multi-rank host logic on CPU: world_size 2 and 3 over gloo.
+
+Each rank runs the CPU mirror of its shard (tests/shard_mirror.py) through
+the product's orchestrator (`dist.run_sharded` + `dist.TorchComm`) with real
+torch.distributed collectives; the assembled coupling and trace must equal
+the single-process oracle.  This pins the sharding plan, the blocked Vᵀ
+all-gather layout, the rank-ordered column merge and the agreed stop rule.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2205_08115_b200 import abi
+from paper_2205_08115_b200 import instances as I
+from paper_2205_08115_b200.dist import ShardPlan
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, iters, rel_tol, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2205_08115_b200.dist import TorchComm, run_sharded
+    from tests.shard_mirror import CpuShard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = I.config1(seed=9, n=n)
+    s = CpuShard(inst.dx, inst.dy, inst.mu, inst.nu, 0.1, rank, world, iters, rel_tol)
+    s.reset()
+    st = run_sharded([s], TorchComm(dist, rank, world, inplace_gather=False), iters, poll_every=4)
+    used = st["iter"] - 1
+    pi, w = s.rows()
+    q.put((rank, pi, w, s.trace(used), st))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, n, iters, rel_tol):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, iters, rel_tol, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda x: x[0])
+    pi = np.vstack([o[1] for o in out])
+    w = np.vstack([o[2] for o in out])
+    return pi, w, out[0][3], [o[4] for o in out]
+
+
+@pytest.mark.parametrize("world,n", [(2, 150), (3, 130)])
+def test_sharded_bapg_matches_oracle_gloo(port, world, n):
+    iters = 12
+    pi, w, trace, sts = _run(world, n, iters, 1e-30)
+    inst = I.config1(seed=9, n=n)
+    o = port.solve(abi.default_config(rho=0.1, max_iters=iters, rel_tol=1e-30), inst.dx, inst.dy,
+                   inst.mu, inst.nu)
+    assert o.code == 0
+    assert all(s["iter"] - 1 == iters for s in sts)
+    np.testing.assert_allclose(pi, o.pi, rtol=0, atol=1e-12 * np.abs(o.pi).max())
+    np.testing.assert_allclose(w, o.w, rtol=0, atol=1e-12 * np.abs(o.w).max())
+    for r, q in zip(trace, o.trace):
+        for k in ("objective", "marginal_infeasibility", "split_gap", "rel_change"):
+            assert r[k] == pytest.approx(q[k], rel=1e-9, abs=1e-14), k
+
+
+def test_sharded_stop_rule_agreed_gloo(port):
+    # every rank must stop at the oracle's convergence iteration
+    n, iters = 64, 1200
+    pi, w, trace, sts = _run(2, n, iters, 1e-6)
+    inst = I.config1(seed=9, n=n)
+    o = port.solve(abi.default_config(rho=0.1, max_iters=iters, rel_tol=1e-6), inst.dx, inst.dy,
+                   inst.mu, inst.nu)
+    assert o.converged
+    assert all(s["converged"] == 1 and s["iter"] - 1 == o.iterations_used for s in sts)
+    np.testing.assert_allclose(pi, o.pi, rtol=0, atol=1e-12)
+
+
+def test_shard_plan():
+    p = ShardPlan(20000, 8)
+    assert p.rows_per_shard == 2560 and p.rows_per_shard % 64 == 0
+    assert sum(p.rows_valid(r) for r in range(8)) == 20000
+    p = ShardPlan(100, 3)
+    assert [p.rows_valid(r) for r in range(3)] == [64, 36, 0]

@@ -1,0 +1,67 @@
+"""Row-sharded BAPG on the device: P shard engines on one GPU (the box has
+one GPU; `dist.EmuComm` stands in for NCCL with in-order device copies),
+driven by the same orchestrator as the multi-process path.  The assembled
+coupling must match the CPU oracle (north-star tolerances)."""
+import numpy as np
+import pytest
+
+from paper_2205_08115_b200 import abi, dist
+from paper_2205_08115_b200 import instances as I
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2, "3xtf32": abi.PREC_3XTF32,
+        "tf32": abi.PREC_TF32}
+
+
+def _run(inst, world, prec, iters, rel_tol=1e-30):
+    import torch
+    cfg = abi.default_config(rho=inst.solver["rho"], max_iters=iters, rel_tol=rel_tol,
+                             precision=PREC[prec])
+    t = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+    dx, dy, mu, nu = t(inst.dx), t(inst.dy), t(inst.mu), t(inst.nu)
+    stream = torch.cuda.Stream()
+    shards = dist.shards_from_dense(cfg, dx, dy, mu, nu, world, stream=stream)
+    for s in shards:
+        s.reset()
+    st = dist.run_sharded(shards, dist.EmuComm(), iters, poll_every=8)
+    dist.raise_shard_flags(st)
+    rows = [s.rows() for s in shards]
+    pi = np.vstack([r[0] for r in rows])
+    w = np.vstack([r[1] for r in rows])
+    used = st["iter"] - 1
+    recs = shards[0].records(used)
+    for s in shards:
+        s.close()
+    return pi, w, recs, st, cfg
+
+
+@pytest.mark.parametrize("world,prec,case", [
+    (2, "bf16x3", "er"), (3, "bf16x3", "er"), (4, "bf16x2", "er"), (2, "3xtf32", "gmm"),
+    (3, "tf32", "er")])
+def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case):
+    inst = I.config1(seed=4, n=300) if case == "er" else I.config2(seed=2, n=260, m=200)
+    iters = 30
+    pi, w, recs, st, cfg = _run(inst, world, prec, iters)
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert o.code == 0 and st["iter"] - 1 == iters
+    assert np.abs(pi - o.pi).max() <= 1e-4 * np.abs(o.pi).max()
+    assert np.abs(w - o.w).max() <= 1e-4 * np.abs(o.w).max()
+    obj, obj_ref = recs[-1].objective, o.trace[-1]["objective"]
+    tol = 2e-4 if prec == "tf32" else 1e-5
+    assert abs(obj - obj_ref) <= tol * abs(obj_ref)
+    for r, q in zip(recs, o.trace):
+        assert abs(r.rel_change - q["rel_change"]) <= 2e-3 * q["rel_change"] + 1e-7
+
+
+def test_sharded_stop_rule_and_errors(gpu, port):
+    inst = I.config1(seed=9, n=64)
+    pi, w, recs, st, cfg = _run(inst, 2, "bf16x3", 1200, rel_tol=1e-6)
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert o.converged and st["converged"]
+    assert abs((st["iter"] - 1) - o.iterations_used) <= 1
+    # overflow → NumericalInstabilityError agreed by every rank
+    inst2 = I.config1(seed=2, n=96)
+    inst2.solver["rho"] = 1e-7
+    with pytest.raises(abi.NumericalInstabilityError, match="exp overflow; increase rho"):
+        _run(inst2, 2, "bf16x3", 5)
