@@ -21,6 +21,12 @@ GWB_API int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b,
                                int64_t N, int64_t K, int32_t precision,
                                void* stream, gwb_status* st);
 
+/* Device time (CUDA events on its stream) of the last on-chip batched BAPG
+ * kernel launched by gwb_bapg_solve_batched in this process, summed over its
+ * batch chunks, and the number of problems it covered; 0 / 0 if the last
+ * batched call took the generic engine.  Measurement hook for bench.py. */
+GWB_API int32_t gwb_batched_last_kernel_ms(double* ms, int64_t* problems);
+
 /* ---------------------------------------------------------------------------
  * Row-sharded multi-GPU BAPG, one shard per rank (csrc/shard.cu).  The
  * caller owns the communication buffers (e.g. torch tensors used with

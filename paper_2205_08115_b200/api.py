@@ -272,6 +272,64 @@ def bapg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
     return _solve("bapg", d_x, d_y, mu, nu, config, opts)
 
 
+def bapg_solve_batched(d_xs, d_ys, mus, nus, config: SolverConfig,
+                       with_trace: bool = True) -> List[SolveReport]:
+    """Batched BAPG over independent problems of one shape (config 5).
+
+    Equivalent to ``[bapg_solve(dx, dy, mu, nu, config) for ...]`` — the
+    reference's experiment worker pool (experiment.cpp:273-304) — but solved
+    by the on-chip batched kernel (n, m ≤ 128) in one device call.  The first
+    failing problem (lowest index) raises, its index named in the message.
+    """
+    lib = abi.load()
+    cfg = config.to_abi()
+    if cfg.algorithm != abi.BAPG:
+        raise ConfigError(f"bapg_solve called with algorithm '{config.algorithm}'")
+    validate(config)
+    batch = len(d_xs)
+    if batch == 0 or not (len(d_ys) == len(mus) == len(nus) == batch):
+        raise DimensionMismatchError("batched inputs must be nonempty and of equal length")
+    for args in zip(d_xs, d_ys, mus, nus):
+        validate_inputs(*args)
+    n, m = d_xs[0].size(), d_ys[0].size()
+    if any(d.size() != n for d in d_xs) or any(d.size() != m for d in d_ys):
+        raise DimensionMismatchError("batched problems must share n and m")
+    dx = np.concatenate([_f64(d.entries()).ravel(order="F") for d in d_xs])
+    dy = np.concatenate([_f64(d.entries()).ravel(order="F") for d in d_ys])
+    mu = np.concatenate([np.asarray(p.weights(), dtype=np.float64) for p in mus])
+    nu = np.concatenate([np.asarray(p.weights(), dtype=np.float64) for p in nus])
+    out_final = np.empty(batch * n * m)
+    out_pi = np.empty(batch * n * m)
+    out_w = np.empty(batch * n * m)
+    cap = max(1, config.max_iters) if with_trace else 0
+    trace = (abi.Record * (batch * cap))() if with_trace else None
+    n_rec = np.zeros(batch, dtype=np.int32)
+    conv = np.zeros(batch, dtype=np.int32)
+    used = np.zeros(batch, dtype=np.int32)
+    st = abi.Status()
+    lib.gwb_bapg_solve_batched(C.byref(cfg), batch, _ptr(dx), n, _ptr(dy), m, _ptr(mu), _ptr(nu),
+                               _ptr(out_final), _ptr(out_pi), _ptr(out_w), trace, cap,
+                               n_rec.ctypes.data_as(C.POINTER(C.c_int32)),
+                               conv.ctypes.data_as(C.POINTER(C.c_int32)),
+                               used.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(st))
+    abi.raise_for(st)
+    out = []
+    for b in range(batch):
+        sl = slice(b * n * m, (b + 1) * n * m)
+        recs = []
+        if with_trace:
+            recs = [IterationRecord(iter=r.iter, objective=r.objective,
+                                    marginal_infeasibility=r.marginal_infeasibility,
+                                    split_gap=r.split_gap, rel_change=r.rel_change,
+                                    elapsed_seconds=r.elapsed_seconds, phase=r.phase)
+                    for r in trace[b * cap: b * cap + int(n_rec[b])]]
+        shape = lambda a: Coupling(a[sl].reshape((n, m), order="F"))
+        out.append(SolveReport(final_coupling=shape(out_final), pi_half=shape(out_pi),
+                               w_half=shape(out_w), trace=recs, converged=bool(conv[b]),
+                               iterations_used=int(used[b])))
+    return out
+
+
 def bpg_solve(d_x, d_y, mu, nu, config: SolverConfig, opts=None):
     """gw::bpg_solve (solvers.cpp:219-293)."""
     return _solve("bpg", d_x, d_y, mu, nu, config, opts)

@@ -13,12 +13,15 @@ namespace gwb {
 namespace dev {
 
 // Stop rule rel_change ≤ rel_tol (solvers.cpp:208, :284, :354) evaluated on
-// fp32 iterates.  An fp32 iterate can become exactly stationary
-// (rel_change == 0) where the fp64 reference still moves by ~1e-14; that
-// only counts as convergence when rel_tol is above fp32 resolution.
-constexpr double kFp32Resolution = 1e-7;
-__device__ __forceinline__ bool stop_rule(double rel, double rel_tol) {
-  return rel <= rel_tol && (rel > 0.0 || rel_tol >= kFp32Resolution);
+// fp32 iterates.  Near a fixed point the fp32 iterate stops moving (rel_change
+// exactly 0, or only underflowed entries still change, rel ~1e-40) while the
+// fp64 reference keeps moving at its own noise floor (~1e-16).  A tolerance
+// below that floor (the pinned-benchmark idiom rel_tol = 1e-30) therefore
+// never triggers in the reference and never triggers here; any tolerance at
+// or above it is compared directly.
+constexpr double kFp64Floor = 1e-15;
+__host__ __device__ __forceinline__ bool stop_rule(double rel, double rel_tol) {
+  return rel_tol >= kFp64Floor && rel <= rel_tol;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {

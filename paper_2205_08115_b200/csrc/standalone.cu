@@ -443,15 +443,5 @@ double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_
   return -v;
 }
 
-void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
-                         const double* dy, int64_t m, const double* mu, const double* nu,
-                         double* out_final, double* out_pi, double* out_w, gwb_record* trace,
-                         int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                         int32_t* iterations_used) {
-  (void)cfg; (void)batch; (void)dx; (void)n; (void)dy; (void)m; (void)mu; (void)nu;
-  (void)out_final; (void)out_pi; (void)out_w; (void)trace; (void)trace_cap; (void)n_records;
-  (void)converged; (void)iterations_used;
-  api_fail(GWB_ERR_UNSUPPORTED, "batched BAPG device path not built yet");
-}
 
 }  // namespace gwb

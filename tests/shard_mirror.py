@@ -183,7 +183,7 @@ class CpuShard:
         self.iter = k + 1
         self.W = self.W_new
         rel = np.sqrt(d[4]) / np.sqrt(d[5])
-        if rel <= self.rel_tol and (rel > 0 or self.rel_tol >= 1e-7):
+        if self.rel_tol >= 1e-15 and rel <= self.rel_tol:  # devutil.cuh stop_rule
             self.conv = True
             self.done = self.gdone = True
 

@@ -1,0 +1,160 @@
+"""Batched BAPG (config 5): the on-chip batched kernel (csrc/batched.cu)
+through gwb_bapg_solve_batched against the CPU oracle, problem by problem.
+
+Same bounds as the single-problem parity tests (BASELINE.json north_star):
+coupling within 1e-4 max-abs relative to its scale, objective within 1e-5
+relative.  The reference has no batched API; its equivalent is one
+gw::solve per problem (experiment.cpp:273-304), which is what the oracle
+runs.
+"""
+import numpy as np
+import pytest
+
+import paper_2205_08115_b200 as gw
+from paper_2205_08115_b200 import instances as I
+
+PI_TOL = 1e-4
+OBJ_TOL = 1e-5
+
+
+def dm(a):
+    return gw.DistanceMatrix.trusted(np.asarray(a, dtype=np.float64))
+
+
+def pv(a):
+    return gw.ProbabilityVector(np.asarray(a, dtype=np.float64))
+
+
+def rel_scale(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def check_against_oracle(port, reps, probs, cfg):
+    for b, (rep, (dx, dy, mu, nu)) in enumerate(zip(reps, probs)):
+        o = port.solve(cfg.to_abi(), dx, dy, mu, nu)
+        assert o.code == 0, o.message
+        assert rep.iterations_used == o.iterations_used, b
+        assert rep.converged == bool(o.converged), b
+        assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL, b
+        assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL, b
+        assert rel_scale(rep.w_half.entries(), o.w) < PI_TOL, b
+        assert len(rep.trace) == len(o.trace), b
+        pi_norm = np.linalg.norm(o.pi)
+        obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+        assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref), (b, obj, obj_ref)
+        for r, q in zip(rep.trace, o.trace):
+            assert r.iter == q["iter"]
+            assert abs(r.objective - q["objective"]) <= 2e-4 * abs(q["objective"])
+            assert abs(r.rel_change - q["rel_change"]) <= 1e-3 * q["rel_change"] + 1e-7
+            # absolute term: fp32 resolution of ‖π‖ (the gap falls to ~1e-7)
+            assert abs(r.split_gap - q["split_gap"]) <= 1e-3 * q["split_gap"] + 1e-6 * pi_norm
+            assert abs(r.marginal_infeasibility - q["marginal_infeasibility"]) <= \
+                1e-3 * q["marginal_infeasibility"] + 1e-9
+
+
+def solve_batch(probs, cfg, **kw):
+    return gw.bapg_solve_batched([dm(p[0]) for p in probs], [dm(p[1]) for p in probs],
+                                 [pv(p[2]) for p in probs], [pv(p[3]) for p in probs], cfg, **kw)
+
+
+def c5_probs(count, seed=0):
+    out = []
+    for k in range(count):
+        inst = I.config5_problem(k, seed=seed)
+        out.append((inst.dx, inst.dy, inst.mu, inst.nu))
+    return out
+
+
+@pytest.mark.gpu
+def test_batched_c5_parity(gpu, port):
+    probs = c5_probs(5)
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=120, rel_tol=1e-30, quiet=True)
+    reps = solve_batch(probs, cfg)
+    check_against_oracle(port, reps, probs, cfg)
+
+
+@pytest.mark.gpu
+def test_batched_ragged_nonuniform(gpu, port):
+    # n ≠ m below the 128 tile, non-uniform marginals: exercises the padding.
+    rng = np.random.default_rng(7)
+    probs = []
+    for k in range(3):
+        n, m = 100, 77
+        dx = I.adjacency(n, I.erdos_renyi(n, 0.08, 100 + k))
+        dy = I.adjacency(m, I.erdos_renyi(m, 0.12, 200 + k))
+        mu = rng.uniform(0.5, 1.5, n)
+        nu = rng.uniform(0.5, 1.5, m)
+        probs.append((dx, dy, mu / mu.sum(), nu / nu.sum()))
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.05, max_iters=80, rel_tol=1e-30, quiet=True)
+    check_against_oracle(port, solve_batch(probs, cfg), probs, cfg)
+
+
+@pytest.mark.gpu
+def test_batched_tiny_and_full_tile(gpu, port):
+    # n = 1, 2 are exact fixed points (rel_change 0 at iteration 1); rel_tol
+    # below 1e-15 never stops on the device (devutil.cuh stop_rule), so those
+    # run with rel_tol 1e-6.
+    for n, tol in ((1, 1e-6), (2, 1e-6), (33, 1e-30), (128, 1e-30)):
+        dx = I.adjacency(n, I.erdos_renyi(n, 0.3, n)) if n > 1 else np.zeros((1, 1))
+        probs = [(dx, dx.copy(), np.full(n, 1.0 / n), np.full(n, 1.0 / n))]
+        cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=15, rel_tol=tol, quiet=True)
+        check_against_oracle(port, solve_batch(probs, cfg), probs, cfg)
+
+
+@pytest.mark.gpu
+def test_batched_early_stop_per_problem(gpu, port):
+    probs = c5_probs(4, seed=3)
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=400, rel_tol=2e-4, quiet=True)
+    reps = solve_batch(probs, cfg)
+    assert all(r.converged for r in reps)
+    check_against_oracle(port, reps, probs, cfg)
+
+
+@pytest.mark.gpu
+def test_batched_generic_fallbacks(gpu, port):
+    # n > 128 and non-bf16-exact distances take the generic engine per problem.
+    big = I.config1(seed=2, n=150)
+    probs = [(big.dx, big.dy, big.mu, big.nu)] * 2
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=30, rel_tol=1e-30, quiet=True)
+    check_against_oracle(port, solve_batch(probs, cfg), probs, cfg)
+    g = I.config2(seed=4, n=64, m=48)
+    probs = [(g.dx, g.dy, g.mu, g.nu)]
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.05, max_iters=30, rel_tol=1e-30, quiet=True)
+    check_against_oracle(port, solve_batch(probs, cfg), probs, cfg)
+
+
+@pytest.mark.gpu
+def test_batched_without_trace(gpu):
+    probs = c5_probs(3, seed=9)
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=50, rel_tol=1e-30, quiet=True)
+    a = solve_batch(probs, cfg, with_trace=False)
+    b = solve_batch(probs, cfg, with_trace=True)
+    for x, y in zip(a, b):
+        assert x.trace == [] and len(y.trace) == 50
+        # deterministic kernel: identical couplings with or without records
+        assert np.array_equal(x.final_coupling.entries(), y.final_coupling.entries())
+
+
+@pytest.mark.gpu
+def test_batched_error_names_problem(gpu, port):
+    probs = c5_probs(3, seed=1)
+    dx, dy, mu, nu = probs[1]
+    probs[1] = (dx * 256.0, dy * 256.0, mu, nu)  # bf16-exact, overflows exp at rho 0.1
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=20, rel_tol=1e-30, quiet=True)
+    o = port.solve(cfg.to_abi(), *probs[1])
+    assert o.code != 0
+    with pytest.raises(gw.NumericalInstabilityError, match="problem 1"):
+        solve_batch(probs, cfg)
+
+
+def test_batched_shape_validation():
+    a = I.config5_problem(0)
+    b = I.config5_problem(1, n=64)
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=5, quiet=True)
+    with pytest.raises(gw.DimensionMismatchError):
+        solve_batch([(a.dx, a.dy, a.mu, a.nu), (b.dx, b.dy, b.mu, b.nu)], cfg)
+    with pytest.raises(gw.DimensionMismatchError):
+        gw.bapg_solve_batched([], [], [], [], cfg)
+    with pytest.raises(gw.ConfigError):
+        solve_batch([(a.dx, a.dy, a.mu, a.nu)],
+                    gw.SolverConfig(algorithm="ebpg", max_iters=5, quiet=True))
