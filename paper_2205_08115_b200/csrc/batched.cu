@@ -81,12 +81,23 @@ __host__ __device__ __forceinline__ uint32_t sw_off(int row, int k) {
          (static_cast<uint32_t>(k & 7) << 1);
 }
 
-__device__ __forceinline__ void split3(float x, __nv_bfloat16& a, __nv_bfloat16& b,
-                                       __nv_bfloat16& c) {
-  a = __float2bfloat16_rn(x);
-  const float r1 = x - __bfloat162float(a);
-  b = __float2bfloat16_rn(r1);
-  c = __float2bfloat16_rn(r1 - __bfloat162float(b));
+// Two fp32 values → three packed bf16x2 planes whose sum is exact
+// (hi = rn(x), mid = rn(x − hi), lo = rn(x − hi − mid)).  One F2FP per plane
+// pair; a bf16 is the upper half of the fp32 with the same value.
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+__device__ __forceinline__ void split3x2(float a, float b, uint32_t& p0, uint32_t& p1,
+                                         uint32_t& p2) {
+  p0 = cvt_bf16x2(a, b);
+  a -= __uint_as_float(p0 << 16);
+  b -= __uint_as_float(p0 & 0xFFFF0000u);
+  p1 = cvt_bf16x2(a, b);
+  a -= __uint_as_float(p1 << 16);
+  b -= __uint_as_float(p1 & 0xFFFF0000u);
+  p2 = cvt_bf16x2(a, b);
 }
 
 // Transpose-reduce: lane l holds v[0..31] (one row, 32 columns); afterwards
@@ -204,6 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
   const uint32_t sD_a = ptx::smem_u32(sD), sPl_a = ptx::smem_u32(sPl);
   uint32_t load_ph = 0, mma_ph = 0;
 
+  // TMEM loads are issued back to back and waited once per phase.
+  auto ld = [&](uint32_t col, uint32_t (&r)[32]) { ptx::tmem_ld_32x32b_x32(tl + col, r); };
   auto load_cols = [&](uint32_t col, float (&v)[32]) {
     uint32_t r[32];
     ptx::tmem_ld_32x32b_x32(tl + col, r);
@@ -232,17 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
     for (int c8 = 0; c8 < 4; ++c8) {
       uint32_t pk[3][4];
 #pragma unroll
-      for (int e = 0; e < 8; e += 2) {
-        __nv_bfloat16 a0, a1, a2, b0, b1, b2;
-        split3(v[c8 * 8 + e], a0, a1, a2);
-        split3(v[c8 * 8 + e + 1], b0, b1, b2);
-        pk[0][e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(a0)) |
-                       (static_cast<uint32_t>(__bfloat16_as_ushort(b0)) << 16);
-        pk[1][e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(a1)) |
-                       (static_cast<uint32_t>(__bfloat16_as_ushort(b1)) << 16);
-        pk[2][e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(a2)) |
-                       (static_cast<uint32_t>(__bfloat16_as_ushort(b2)) << 16);
-      }
+      for (int e = 0; e < 4; ++e)
+        split3x2(v[c8 * 8 + 2 * e], v[c8 * 8 + 2 * e + 1], pk[0][e], pk[1][e], pk[2][e]);
       const uint32_t off = sw_off(i, col + 8 * c8);
 #pragma unroll
       for (int p = 0; p < 3; ++p)
@@ -357,9 +361,17 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         double gw = 0.0, rw = 0.0;
 #pragma unroll 1
         for (int g = 0; g < 2; ++g) {
+          uint32_t ha[32], la[32], wr[32];
+          ld(kAccHi + c0 + 32 * g, ha);
+          ld(kAccLo + c0 + 32 * g, la);
+          ld(kW + c0 + 32 * g, wr);
+          ptx::tmem_wait_ld();
           float gv[32], wv[32];
-          load_acc(g, gv);
-          load_cols(kW + c0 + 32 * g, wv);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            gv[t] = __fadd_rn(__uint_as_float(ha[t]), __uint_as_float(la[t]));
+            wv[t] = __uint_as_float(wr[t]);
+          }
           float gwf = 0.f;
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
@@ -387,12 +399,14 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
           float S = 0.f;
 #pragma unroll 1
           for (int g = 0; g < 2; ++g) {
-            float gv[32], wv[32];
-            load_cols(kAccHi + c0 + 32 * g, gv);
-            load_cols(kW + c0 + 32 * g, wv);
+            uint32_t gr[32], wr[32];
+            ld(kAccHi + c0 + 32 * g, gr);
+            ld(kW + c0 + 32 * g, wr);
+            ptx::tmem_wait_ld();
+            float gv[32];
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
-              gv[t] = wv[t] * __expf(gv[t] * inv_rho - r);
+              gv[t] = __uint_as_float(wr[t]) * __expf(__uint_as_float(gr[t]) * inv_rho - r);
               S += gv[t];
             }
             store_cols(kPi + c0 + 32 * g, gv);
@@ -463,14 +477,17 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       // B2: t = π e^{G/ρ − c} (kept in kAccLo); column sums of t (fp32) and π (fp64).
 #pragma unroll 1
       for (int g = 0; g < 2; ++g) {
-        float gv[32], pv[32];
-        load_cols(kAccHi + c0 + 32 * g, gv);
-        load_cols(kPi + c0 + 32 * g, pv);
+        uint32_t gr[32], pr[32];
+        ld(kAccHi + c0 + 32 * g, gr);
+        ld(kPi + c0 + 32 * g, pr);
+        ptx::tmem_wait_ld();
+        float gv[32];
         double pd[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          gv[t] = pv[t] * __expf(gv[t] * inv_rho - col_c[c0 + 32 * g + t]);
-          pd[t] = static_cast<double>(pv[t]);
+          const float pv = __uint_as_float(pr[t]);
+          gv[t] = pv * __expf(__uint_as_float(gr[t]) * inv_rho - col_c[c0 + 32 * g + t]);
+          pd[t] = static_cast<double>(pv);
         }
         store_cols(kAccLo + c0 + 32 * g, gv);
         const float cs = xreduce32(gv, lane, FAdd{});
@@ -512,25 +529,33 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       bool finite = true;
 #pragma unroll 1
       for (int g = 0; g < 2; ++g) {
-        float gv[32], pv[32], wv[32], tv[32];
-        load_cols(kAccHi + c0 + 32 * g, gv);
-        load_cols(kPi + c0 + 32 * g, pv);
-        load_cols(kW + c0 + 32 * g, wv);
-        load_cols(kAccLo + c0 + 32 * g, tv);
+        uint32_t gr[32], pr[32], wr[32], tr[32];
+        ld(kAccHi + c0 + 32 * g, gr);
+        ld(kPi + c0 + 32 * g, pr);
+        ld(kW + c0 + 32 * g, wr);
+        ld(kAccLo + c0 + 32 * g, tr);
+        ptx::tmem_wait_ld();
+        float tv[32];
+#define gv(t) __uint_as_float(gr[t])
+#define pv(t) __uint_as_float(pr[t])
+#define wv(t) __uint_as_float(wr[t])
         float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          const float o = col_s[c0 + 32 * g + t] * tv[t];
+          const float o = col_s[c0 + 32 * g + t] * __uint_as_float(tr[t]);
           finite = finite && isfinite(o);
-          f[0] = fmaf(gv[t], o, f[0]);
-          const float sp = pv[t] - o;
+          f[0] = fmaf(gv(t), o, f[0]);
+          const float sp = pv(t) - o;
           f[1] = fmaf(sp, sp, f[1]);
-          const float df = o - wv[t];
+          const float df = o - wv(t);
           f[2] = fmaf(df, df, f[2]);
-          f[3] = fmaf(wv[t], wv[t], f[3]);
-          f[4] = fmaf(gv[t], pv[t], f[4]);
+          f[3] = fmaf(wv(t), wv(t), f[3]);
+          f[4] = fmaf(gv(t), pv(t), f[4]);
           tv[t] = o;
         }
+#undef gv
+#undef pv
+#undef wv
 #pragma unroll
         for (int s = 0; s < 5; ++s) dsum[s] += static_cast<double>(f[s]);
         store_cols(kW + c0 + 32 * g, tv);
@@ -572,9 +597,16 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       float* W = a.W + static_cast<int64_t>(b) * kT * kT + static_cast<int64_t>(i) * kT + c0;
 #pragma unroll 1
       for (int g = 0; g < 2; ++g) {
+        uint32_t pr[32], wr[32];
+        ld(kPi + c0 + 32 * g, pr);
+        ld(kW + c0 + 32 * g, wr);
+        ptx::tmem_wait_ld();
         float pv[32], wv[32];
-        load_cols(kPi + c0 + 32 * g, pv);
-        load_cols(kW + c0 + 32 * g, wv);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          pv[t] = __uint_as_float(pr[t]);
+          wv[t] = __uint_as_float(wr[t]);
+        }
 #pragma unroll
         for (int t = 0; t < 32; t += 4) {
           *reinterpret_cast<float4*>(P + 32 * g + t) = make_float4(pv[t], pv[t + 1], pv[t + 2], pv[t + 3]);
