@@ -76,7 +76,8 @@ struct BDev {
   const float* P;       // π_k
   float* P_new;
   float* P_aux_new;
-  int aux_mode;
+  int aux_mode;         // GEMM operand copy of P_new: 2 = 3xTF32 residual, 3/4 = bf16 planes
+  int64_t plane;        // elements per bf16 plane (n·ld)
   const double* mu64;
   const double* nu64;
   double* f;
@@ -441,9 +442,7 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
       }
       *reinterpret_cast<float4*>(d.P_new + i * d.ld + c0) = make_float4(o[0], o[1], o[2], o[3]);
       if (d.P_aux_new)
-        *reinterpret_cast<float4*>(d.P_aux_new + i * d.ld + c0) =
-            make_float4(aux_of(o[0], d.aux_mode), aux_of(o[1], d.aux_mode),
-                        aux_of(o[2], d.aux_mode), aux_of(o[3], d.aux_mode));
+        aux_store4(d.P_aux_new, d.aux_mode, d.plane, i * d.ld + c0, o[0], o[1], o[2], o[3]);
     }
     rs = warp_sum(rs);
     if (lane == 0) d.row_sum[static_cast<int64_t>(blockIdx.x) * d.n + i] = rs;
@@ -578,10 +577,10 @@ class BregmanEngine {
     Dy_lo_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
     for (int q = 0; q < 2; ++q) {
       P_[q] = keep(dalloc<float>(nm));
-      Pa_[q] = keep(dalloc<float>(nm));
+      Pa_[q] = keep(dalloc<float>(nm * 3 / 2));  // fp32 residual or up to 3 bf16 planes
     }
     Vt_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
-    Vta_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
+    Vta_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
     G_ = keep(dalloc<float>(nm));
     mu_ = keep(dalloc<double>(n_));
     nu_ = keep(dalloc<double>(m_));
@@ -619,10 +618,10 @@ class BregmanEngine {
     double* sp = static_cast<double*>(stage.get());
     GWB_CUDA(cudaMemcpyAsync(sp, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, s_));
     launch_colmajor64_to_rowmajor32(sp, n_, n_, Dx_, ldn_, s_);
-    launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_lo_, 2, s_);
+
     GWB_CUDA(cudaMemcpyAsync(sp, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, s_));
     launch_colmajor64_to_rowmajor32(sp, m_, m_, Dy_, ldm_, s_);
-    launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
+    choose_precision();
     GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
     if (initial) {
@@ -639,7 +638,7 @@ class BregmanEngine {
                               ldm_, P_[0], s_);
       GWB_CUDA(cudaStreamSynchronize(s_));
     }
-    launch_tf32_aux(P_[0], n_, m_, ldm_, Pa_[0], 2, s_);
+    launch_tf32_aux(P_[0], n_, m_, ldm_, Pa_[0], aux_mode_, s_);
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_plans();
   }
@@ -757,7 +756,8 @@ class BregmanEngine {
     d.m = m_;
     d.ld = ldm_;
     d.G = G_;
-    d.aux_mode = 2;
+    d.aux_mode = aux_mode_;
+    d.plane = n_ * ldm_;
     d.mu64 = mu_;
     d.nu64 = nu_;
     d.f = f_;
@@ -796,7 +796,76 @@ class BregmanEngine {
     d.P_aux_new = Pa_[1 - q];
   }
 
+  // Chain precision, as for BAPG: bf16 planes of the
+  // iterate against exact bf16 structure matrices when both are 0/1-like,
+  // otherwise 3xTF32 (both operands split).
+  void choose_precision() {
+    std::unique_ptr<void, DevFree> mx(dalloc<float>(2)), ix(dalloc<int>(2));
+    float* d_max = static_cast<float*>(mx.get());
+    int* d_inexact = static_cast<int*>(ix.get());
+    launch_analyze(Dx_, n_, n_, ldn_, d_max, d_inexact, s_);
+    launch_analyze(Dy_, m_, m_, ldm_, d_max + 1, d_inexact + 1, s_);
+    int h[2];
+    GWB_CUDA(cudaMemcpyAsync(h, d_inexact, sizeof(h), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    const bool bf16_exact = (h[0] & 2) == 0 && (h[1] & 2) == 0;
+    const int req = cfg_.precision;
+    if (bf16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_BF16X3)) aux_mode_ = 3;
+    else if (bf16_exact && req == GWB_PREC_BF16X2) aux_mode_ = 4;
+    else aux_mode_ = 2;
+    if (aux_mode_ >= 3) {
+      Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16));
+      Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
+      launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, s_);
+      launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+    } else {
+      launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_lo_, 2, s_);
+      launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
+    }
+  }
+
   void build_plans() {
+    if (aux_mode_ >= 3) {
+      const int planes = aux_mode_ == 3 ? 3 : 2;
+      auto plane_k = [](float* base, int64_t plane_elems, int k) {
+        return static_cast<void*>(reinterpret_cast<uint16_t*>(base) + k * plane_elems);
+      };
+      auto b1 = [&](int q, const int* skip) {
+        GemmDesc d;
+        d.M = m_; d.N = n_; d.K = m_;
+        d.bf16_planes = planes;
+        d.a_bf16 = Dy_bf_; d.lda = ldm_;
+        for (int k = 0; k < planes; ++k) d.b_bf16[k] = plane_k(Pa_[q], n_ * ldm_, k);
+        d.ldb = ldm_;
+        d.c_planes = planes;
+        for (int k = 0; k < planes; ++k) d.c_bf16[k] = plane_k(Vta_, m_ * ldn_, k);
+        d.ldc = ldn_;
+        d.skip = skip;
+        GemmPlan* p = gemm_plan_create(d);
+        plans_.push_back(p);
+        return p;
+      };
+      auto b2 = [&](const int* skip) {
+        GemmDesc d;
+        d.M = n_; d.N = m_; d.K = n_;
+        d.bf16_planes = planes;
+        d.a_bf16 = Dx_bf_; d.lda = ldn_;
+        for (int k = 0; k < planes; ++k) d.b_bf16[k] = plane_k(Vta_, m_ * ldn_, k);
+        d.ldb = ldn_;
+        d.c = G_; d.ldc = ldm_;
+        d.skip = skip;
+        GemmPlan* p = gemm_plan_create(d);
+        plans_.push_back(p);
+        return p;
+      };
+      for (int q = 0; q < 2; ++q) {
+        g1_[q] = b1(q, &st_->done);
+        g1t_[q] = b1(q, &st_->flags);
+      }
+      g2_ = b2(&st_->done);
+      g2t_ = b2(&st_->flags);
+      return;
+    }
     auto g1 = [&](int q, const int* skip) {
       GemmDesc d;
       d.M = m_; d.N = n_; d.K = m_;
@@ -837,6 +906,9 @@ class BregmanEngine {
   std::vector<void*> bufs_;
   std::vector<GemmPlan*> plans_;
   float *Dx_, *Dy_, *Dx_lo_, *Dy_lo_, *P_[2], *Pa_[2], *Vt_, *Vta_, *G_, *rowmax_;
+  float* Dx_bf_ = nullptr;
+  float* Dy_bf_ = nullptr;
+  int aux_mode_ = 2;
   double *mu_, *nu_, *f_, *fn_, *g_, *row_err_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
       *row_sum_, *obj_part_, *wpart_;
   float* col_pe_;
