@@ -38,7 +38,9 @@ def run(batch=4096, iters=500, n=128, trace=False):
     reps = gw.bapg_solve_batched(*args, cfg, with_trace=trace)
     wall = time.perf_counter() - t0
     ms, cnt = C.c_double(), C.c_int64()
-    abi.load().gwb_batched_last_kernel_ms(C.byref(ms), C.byref(cnt))
+    fn = abi.load().gwb_batched_last_kernel_ms
+    fn.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    fn(C.byref(ms), C.byref(cnt))
     flops = 2.0 * 2.0 * n * n * (n + n) * batch  # 4 GEMMs of n³ MACs per iteration, all problems
     # Executed tensor work: 128-padded tiles, 3 bf16 planes per GEMM.
     exec_flops = 4 * 3 * 2.0 * 128 ** 3 * batch
@@ -57,5 +59,4 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=500)
     ap.add_argument("--size", type=int, default=128)
     a = ap.parse_args()
-    abi.load().gwb_batched_last_kernel_ms.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     print(json.dumps(run(a.batch, a.iters, a.size)), flush=True)
