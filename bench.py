@@ -410,6 +410,52 @@ def dense_rows_dev(torch, n, edges, r0, rows):
     return d
 
 
+class HostRows:
+    """Lazy host rows of a 0/1 adjacency: `rows[r0:r1]` builds those rows
+    (fp32) from the edge list, so each rank materialises only its slice."""
+
+    def __init__(self, n, edges):
+        e = np.concatenate([edges, edges[:, ::-1]])
+        self.n, self.e = n, e[np.argsort(e[:, 0], kind="stable")]
+
+    def __getitem__(self, sl):
+        r0, r1 = sl.start, min(sl.stop, self.n)
+        out = np.zeros((max(r1 - r0, 0), self.n), dtype=np.float32)
+        lo, hi = np.searchsorted(self.e[:, 0], [r0, r1])
+        sel = self.e[lo:hi]
+        out[sel[:, 0] - r0, sel[:, 1]] = 1.0
+        return out
+
+
+def run_sharded_e2e(args, world, rank, local, dist, edges, tgt, prec):
+    """e2e at N GPUs through the public multi-GPU entry dist.solve_sharded:
+    host rows of D_X (this rank's), host D_Y and marginals uploaded, the
+    e2e_iters-iteration solve, this rank's rows of π and w read back — all in
+    the timed region; value = iterations / max over ranks of the wall time."""
+    import torch
+    from paper_2205_08115_b200 import abi
+    from paper_2205_08115_b200 import dist as D
+    n = args.n
+    dx = HostRows(n, edges)
+    dy = HostRows(n, tgt)[0:n]
+    u = np.full(n, 1.0 / n)
+    cfg = abi.default_config(rho=0.1, max_iters=args.e2e_iters, rel_tol=1e-30, precision=prec)
+    dist.barrier()
+    t0 = time.perf_counter()
+    r = D.solve_sharded(cfg, dx, dy, u, u, dist, rank, world, local)
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    rv = r["pi_rows"].shape[0]
+    return {"value": r["iterations_used"] / dt, "unit": "it/s", "iterations": r["iterations_used"],
+            "seconds": dt,
+            "h2d_bytes_per_step": int(rv * n * 4 + dy.nbytes + 2 * n * 4),
+            "d2h_bytes_per_step": int(2 * r["pi_rows"].nbytes),
+            "note": "per rank: one dist.solve_sharded call (host fp32 rows in, fp64 π/w rows "
+                    "out); bytes are rank 0's; time is the max over ranks"}
+
+
 def run_sharded_bench(args, world, rank, local, dist):
     """N > 1: c4 rows of π, w, D_X sharded over the ranks (strong scaling of
     the fixed n=m=20000 problem); Vᵀ all-gathers, column-statistics
@@ -436,6 +482,7 @@ def run_sharded_bench(args, world, rank, local, dist):
     D.iterate_sharded([shard], comm, args.warmup, poll_every=0)
     torch.cuda.synchronize()
     dist.barrier()
+    launches0 = shard.launches()
     clocks = ClockSampler(local)
     with clocks:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -445,6 +492,7 @@ def run_sharded_bench(args, world, rank, local, dist):
         ev1.record(shard.stream)
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
+    launches = shard.launches() - launches0
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -471,9 +519,24 @@ def run_sharded_bench(args, world, rank, local, dist):
             "tflops": {"algorithmic_per_iteration": flops_it,
                        "achieved_whole_step": flops_it * value / 1e12},
             "roofline": None, "cpu_baseline": None, "e2e": None,
-            "gpu_launches": None, "clocks": clocks.summary(),
+            "gpu_launches": launches, "clocks": clocks.summary(),
         }
     shard.close()
+    del shard
+    torch.cuda.empty_cache()
+    if rank == 0:
+        tf32 = measure_tf32_peak(torch)
+        per_gpu = flops_it / world * value / 1e12
+        line["roofline"] = {
+            "bound": "tensor", "scope": "whole sharded step per GPU (GEMM chain + projections "
+            "+ collectives), algorithmic FLOPs / world / step time",
+            "achieved": per_gpu, "unit": "TFLOP/s", "peak": tf32["sustained"],
+            "peak_source": f"cuBLAS TF32 sustained, measured in this run ({tf32['how']})",
+            "frac": per_gpu / tf32["sustained"], "traffic": None}
+    if not args.no_e2e:
+        e2e = run_sharded_e2e(args, world, rank, local, dist, edges, tgt, prec)
+        if rank == 0:
+            line["e2e"] = e2e
     if not args.no_variants:
         c5 = c5_variant(world, rank, local, dist)
         if rank == 0:

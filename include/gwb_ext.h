@@ -62,6 +62,8 @@ GWB_API int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows,
                                       const float* nu, gwb_status* st);
 GWB_API int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st);
 GWB_API int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st);
+/* Kernels launched so far by phases 0-5 of this shard (measurement hook). */
+GWB_API int32_t gwb_shard_launches(gwb_shard* s, int64_t* launches);
 GWB_API int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st);
 GWB_API int32_t gwb_shard_status(gwb_shard* s, int32_t* done, int32_t* iter,
                                  int32_t* flags, int32_t* converged,

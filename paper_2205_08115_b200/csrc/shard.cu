@@ -342,6 +342,8 @@ class ShardEngine {
   }
 
   // Phases between collectives (see file comment).
+  int64_t launches() const { return launches_; }
+
   void phase(int ph) {
     GWB_CUDA(cudaSetDevice(dev_));
     const int q = parity_;
@@ -349,29 +351,35 @@ class ShardEngine {
     switch (ph) {
       case 0:  // A1: Vᵀ slot ← D_Y · W_rᵀ
         GWB_CUDA(gemm_launch(g1_[q], s_));
+        launches_ += 1;
         break;
       case 1:  // A2: G_r, row projection
         GWB_CUDA(gemm_launch(g2_, s_));
         launch_row_update(d, true, s_);
+        launches_ += 3;
         break;
       case 2:  // B1
         GWB_CUDA(gemm_launch(g1p_, s_));
+        launches_ += 1;
         break;
       case 3:  // B2: G_r, local column partials → stats slot
         GWB_CUDA(gemm_launch(g2_, s_));
         launch_col_partial(d, s_);
         shard_col_local_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
             d, stats_ + static_cast<int64_t>(rank_) * 3 * m_, m_);
+        launches_ += 3;
         break;
       case 4:  // B3: global column merge, write pass, local diagnostics
         shard_col_global_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
             d, stats_, world_);
         launch_col_write(d, s_);
         shard_diag_kernel<<<1, 512, 0, s_>>>(d, diag_, err_, rank_, row_begin_, 0);
+        launches_ += d.n >= 1 ? 5 : 4;
         break;
       case 5:  // F: global finalize; w' becomes w
         shard_finalize_kernel<<<1, 1, 0, s_>>>(d, diag_, err_, cfg_.rel_tol, 0);
         parity_ ^= 1;
+        launches_ += 1;
         break;
       case 6:  // tail A1 (chain on the final w; runs after convergence)
         GWB_CUDA(gemm_launch(g1t_[q], s_));
@@ -555,6 +563,7 @@ class ShardEngine {
   bool bf16_;
   int64_t nr_, row_begin_, rows_valid_, ldk_, ldm_;
   int parity_ = 0;
+  int64_t launches_ = 0;  // kernels launched by phases 0-5 (bench gpu_launches)
   std::vector<void*> bufs_;
   std::vector<GemmPlan*> plans_;
   float *Dx_, *Dy_, *Dx_aux_, *Dy_aux_, *P_, *P_aux_, *W_[2], *W_aux_[2], *G_;
@@ -649,6 +658,12 @@ int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st) {
 
 int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st) {
   return shard_guard(st, [&] { s->eng->phase(phase); });
+}
+
+int32_t gwb_shard_launches(gwb_shard* s, int64_t* launches) {
+  if (!s || !launches) return GWB_ERR_INVALID;
+  *launches = s->eng->launches();
+  return GWB_OK;
 }
 
 int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st) {

@@ -61,6 +61,7 @@ _SIGS = {
     "gwb_shard_reset": (C.c_int32, [_P, _ST]),
     "gwb_shard_phase": (C.c_int32, [_P, C.c_int32, _ST]),
     "gwb_shard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
+    "gwb_shard_launches": (C.c_int32, [_P, _I64P]),
     "gwb_shard_status": (C.c_int32, [_P, _I32P, _I32P, _I32P, _I32P, _I32P, _I32P, _ST]),
     "gwb_shard_finish": (C.c_int32, [_P, _ST]),
     "gwb_shard_records": (C.c_int32, [_P, C.c_int32, C.POINTER(abi.Record), _ST]),
@@ -146,6 +147,11 @@ class GpuShard:
         _check(st)
         keys = ("done", "iter", "flags", "converged", "err_iter", "zero_index")
         return {k: x.value for k, x in zip(keys, v)}
+
+    def launches(self) -> int:
+        v = C.c_int64()
+        self.lib.gwb_shard_launches(self.h, C.byref(v))
+        return v.value
 
     def finish(self):
         st = abi.Status()
@@ -308,6 +314,46 @@ def run_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> dict:
     """Full sharded solve: iterations, then the tail record."""
     iterate_sharded(shards, comm, iters, poll_every)
     return finish_sharded(shards, comm)
+
+
+def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
+                  device: int = 0, poll_every: int = 16) -> dict:
+    """Row-sharded BAPG from HOST inputs — the public multi-GPU entry, called
+    by every rank of a torch.distributed (NCCL) job with the same arguments.
+
+    `dx` is anything that slices to host rows (`dx[r0:r1]`, e.g. an n×n numpy
+    array, a memmap, or a lazy row builder), so a rank only materialises its
+    own rows of D_X; `dy`, `mu`, `nu` are full host arrays.  The rank uploads
+    its rows, runs the solve (bapg_solve semantics, solvers.cpp:138-217) and
+    returns its rows of π and w (fp64), the agreed trace, convergence flag
+    and iteration count.  Errors raise the reference exception on every rank.
+    """
+    import numpy as np
+    import torch
+    n, m = len(mu), len(nu)
+    shard = GpuShard(cfg, n, m, rank, world, device)
+    try:
+        rb, rv = shard.row_begin, shard.rows_valid
+        dev = torch.device("cuda", device)
+        rows = np.ascontiguousarray(dx[rb:rb + rv], dtype=np.float32).reshape(rv, n)
+        if rv == 0:
+            rows = np.zeros((1, n), dtype=np.float32)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+        dx_d, dy_d = t(rows), t(dy)
+        mu_d = t(np.asarray(mu)[rb:rb + max(rv, 1)] if rv else np.zeros(1))
+        shard.load(dx_d, dy_d, mu_d, t(nu))
+        del dx_d, dy_d
+        shard.reset()
+        st = run_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters, poll_every)
+        raise_shard_flags(st)
+        used = st["iter"] - 1
+        recs = shard.records(used)
+        pi, w = shard.rows()
+        return {"pi_rows": pi, "w_rows": w, "row_begin": rb, "trace": recs,
+                "converged": bool(st["converged"]), "iterations_used": used,
+                "launches": shard.launches()}
+    finally:
+        shard.close()
 
 
 def raise_shard_flags(st: dict):

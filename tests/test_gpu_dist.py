@@ -65,3 +65,32 @@ def test_sharded_stop_rule_and_errors(gpu, port):
     inst2.solver["rho"] = 1e-7
     with pytest.raises(abi.NumericalInstabilityError, match="exp overflow; increase rho"):
         _run(inst2, 2, "bf16x3", 5)
+
+
+def test_solve_sharded_public_entry_nccl_world1(gpu, port):
+    # dist.solve_sharded from host inputs over a real one-rank NCCL group
+    # (the multi-GPU public entry; the box has one GPU).
+    import os
+    import socket
+    import torch
+    import torch.distributed as tdist
+    inst = I.config1(seed=4, n=300)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port_no = sk.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    tdist.init_process_group("nccl", rank=0, world_size=1,
+                             device_id=torch.device("cuda", 0))
+    try:
+        cfg = abi.default_config(rho=0.1, max_iters=40, rel_tol=1e-30)
+        r = dist.solve_sharded(cfg, inst.dx, inst.dy, inst.mu, inst.nu, tdist, 0, 1, 0)
+    finally:
+        tdist.destroy_process_group()
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert r["iterations_used"] == o.iterations_used == 40
+    assert np.abs(r["pi_rows"] - o.pi).max() / np.abs(o.pi).max() < 1e-4
+    assert np.abs(r["w_rows"] - o.w).max() / np.abs(o.w).max() < 1e-4
+    obj, ref = r["trace"][-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - ref) <= 1e-5 * abs(ref)
+    assert r["launches"] > 0
