@@ -152,6 +152,27 @@ GWB_API int32_t gwb_bpg_solve GWB_SOLVE_SIGNATURE;
 GWB_API int32_t gwb_ebpg_solve GWB_SOLVE_SIGNATURE;
 GWB_API int32_t gwb_hbpg_solve GWB_SOLVE_SIGNATURE;
 
+/* gw::solve(adjacency_distance(Graph(n, edges_x)), adjacency_distance(Graph(m,
+ * edges_y)), mu, nu, cfg) — tasks.cpp:167-174 + types.cpp:155-174 + solvers.cpp
+ * :499-515 in one call.  Edge lists are int32 pairs (a, b); they are
+ * validated as the reference Graph constructor does (GWB_ERR_INVALID:
+ * "graph must have at least one node", "self-loop at node a",
+ * "edge (a,b) out of range for N nodes"; duplicates are harmless) and the
+ * dense 0/1 structure matrices are built on the device from 8 B per edge
+ * instead of uploading n² + m² fp64 entries.  Outputs and errors as
+ * gwb_solve. */
+GWB_API int32_t gwb_solve_graphs(const gwb_config* cfg, int64_t n,
+                                 const int32_t* edges_x, int64_t count_x,
+                                 int64_t m, const int32_t* edges_y,
+                                 int64_t count_y, const double* mu,
+                                 const double* nu, const double* initial,
+                                 gwb_observer observer, void* user,
+                                 double* out_final, double* out_pi,
+                                 double* out_w, gwb_record* trace,
+                                 int32_t trace_cap, int32_t* n_records,
+                                 int32_t* converged, int32_t* iterations_used,
+                                 gwb_status* st);
+
 /* gw::gw_objective (solvers.hpp:12-13, solvers.cpp:64-69): -Σ (D_X π D_Y)⊙π.
  * pi is pi_rows×pi_cols (shape-checked against n, m). */
 GWB_API int32_t gwb_gw_objective(const double* dx, int64_t n, const double* dy,

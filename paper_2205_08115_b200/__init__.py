@@ -6,7 +6,7 @@ Python mirror of the reference ``gw::`` interface used by tests and bench.
 """
 from .api import (  # noqa: F401
     COLS, ROWS, ConfigError, Coupling, DimensionMismatchError, DistanceMatrix, DomainError,
-    IterationRecord, NumericalInstabilityError, ProbabilityVector, SinkhornResult,
+    Graph, IterationRecord, NumericalInstabilityError, adjacency_distance, ProbabilityVector, SinkhornResult,
     SolveOptions, SolveReport, SolverConfig, UnsupportedError, ZeroSumLineError, bapg_solve,
     bapg_solve_batched,
     bpg_solve, ebpg_solve, gw_objective, hard_assignment, hbpg_solve, kl_scale, lipschitz_bound,

@@ -184,6 +184,10 @@ SIGNATURES = {
                                                C.c_int64, _D, C.c_int64, _D, _ST]),
     "gwb_split_gap": (C.c_int32, [_D, _D, C.c_int64, C.c_int64, _D, _ST]),
     "gwb_hard_assignment": (C.c_int32, [_D, C.c_int64, C.c_int64, _I32, _ST]),
+    "gwb_solve_graphs": (C.c_int32, [C.POINTER(Config), C.c_int64, C.POINTER(C.c_int32),
+                                     C.c_int64, C.c_int64, C.POINTER(C.c_int32), C.c_int64,
+                                     _D, _D, _D, OBSERVER, C.c_void_p, _D, _D, _D,
+                                     C.POINTER(Record), C.c_int32, _I32, _I32, _I32, _ST]),
     "gwb_bapg_solve_batched": (C.c_int32, [C.POINTER(Config), C.c_int64, _D,
                                            C.c_int64, _D, C.c_int64, _D, _D, _D,
                                            _D, _D, C.POINTER(Record), C.c_int32,

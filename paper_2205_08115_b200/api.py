@@ -60,10 +60,57 @@ class DistanceMatrix:
         return obj
 
     def size(self) -> int:
-        return self._e.shape[0]
+        g = getattr(self, "_graph", None)
+        return g.num_nodes() if g is not None else self._e.shape[0]
 
     def entries(self) -> np.ndarray:
+        if getattr(self, "_e", None) is None:  # graph-backed: materialise on demand
+            g = self._graph
+            a = np.zeros((g.num_nodes(), g.num_nodes()), order="F")
+            e = g.edges()
+            a[e[:, 0], e[:, 1]] = 1.0
+            a[e[:, 1], e[:, 0]] = 1.0
+            self._e = a
         return self._e
+
+    def graph(self) -> Optional["Graph"]:
+        """The Graph this matrix is the adjacency of (adjacency_distance), or None."""
+        return getattr(self, "_graph", None)
+
+
+class Graph:
+    """gw::Graph (types.hpp:120-130, types.cpp:155-174): edges stored as
+    canonical (min, max) pairs, sorted, duplicates removed."""
+
+    def __init__(self, num_nodes: int, edges):
+        if num_nodes <= 0:
+            raise ValueError("graph must have at least one node")
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        for a, b in e:
+            if a == b:
+                raise ValueError(f"self-loop at node {a}")
+            if a < 0 or b < 0 or a >= num_nodes or b >= num_nodes:
+                raise ValueError(f"edge ({a},{b}) out of range for {num_nodes} nodes")
+        canon = np.stack([e.min(axis=1), e.max(axis=1)], axis=1) if len(e) else e
+        self._n = int(num_nodes)
+        self._edges = np.unique(canon, axis=0).astype(np.int32) if len(e) else \
+            np.zeros((0, 2), dtype=np.int32)
+
+    def num_nodes(self) -> int:
+        return self._n
+
+    def edges(self) -> np.ndarray:
+        return self._edges
+
+
+def adjacency_distance(g: Graph) -> DistanceMatrix:
+    """gw::adjacency_distance (tasks.cpp:167-174): the 0/1 adjacency.  The
+    matrix keeps its graph, so `solve` builds it on the device from the edge
+    list (gwb_solve_graphs) instead of uploading n² fp64 entries."""
+    dm = DistanceMatrix.__new__(DistanceMatrix)
+    dm._e = None
+    dm._graph = g
+    return dm
 
 
 class ProbabilityVector:
@@ -245,10 +292,21 @@ def _solve(entry, d_x, d_y, mu, nu, config, opts):
             opts.observer(int(it), pi, w)
             return 0
         cb = abi.OBSERVER(_obs)
-    fn = getattr(lib, _ENTRY[entry])
-    fn(C.byref(cfg), _ptr(d_x.entries()), n, _ptr(d_y.entries()), m, _ptr(mu.weights()),
-       _ptr(nu.weights()), _ptr(init), cb, None, _ptr(out_final), _ptr(out_pi), _ptr(out_w),
-       trace, cap, C.byref(n_rec), C.byref(conv), C.byref(used), C.byref(st))
+    gx, gy = d_x.graph(), d_y.graph()
+    if gx is not None and gy is not None:
+        # Both are adjacency_distance(graph): D is built on the device.
+        ex, ey = np.ascontiguousarray(gx.edges()), np.ascontiguousarray(gy.edges())
+        i32 = C.POINTER(C.c_int32)
+        lib.gwb_solve_graphs(C.byref(cfg), n, ex.ctypes.data_as(i32), len(ex), m,
+                             ey.ctypes.data_as(i32), len(ey), _ptr(mu.weights()),
+                             _ptr(nu.weights()), _ptr(init), cb, None, _ptr(out_final),
+                             _ptr(out_pi), _ptr(out_w), trace, cap, C.byref(n_rec),
+                             C.byref(conv), C.byref(used), C.byref(st))
+    else:
+        fn = getattr(lib, _ENTRY[entry])
+        fn(C.byref(cfg), _ptr(d_x.entries()), n, _ptr(d_y.entries()), m, _ptr(mu.weights()),
+           _ptr(nu.weights()), _ptr(init), cb, None, _ptr(out_final), _ptr(out_pi),
+           _ptr(out_w), trace, cap, C.byref(n_rec), C.byref(conv), C.byref(used), C.byref(st))
     abi.raise_for(st)
     recs = [IterationRecord(iter=r.iter, objective=r.objective,
                             marginal_infeasibility=r.marginal_infeasibility,

@@ -612,15 +612,19 @@ class BregmanEngine {
   }
 
   void load(const double* dx, const double* dy, const double* mu, const double* nu,
-            const double* initial) {
-    const int64_t big = std::max(std::max(n_ * n_, m_ * m_), n_ * m_);
+            const double* initial, const GraphInput* graphs) {
+    const int64_t big = graphs ? n_ * m_ : std::max(std::max(n_ * n_, m_ * m_), n_ * m_);
     std::unique_ptr<void, DevFree> stage(dalloc<double>(static_cast<size_t>(big)));
     double* sp = static_cast<double*>(stage.get());
-    GWB_CUDA(cudaMemcpyAsync(sp, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, s_));
-    launch_colmajor64_to_rowmajor32(sp, n_, n_, Dx_, ldn_, s_);
-
-    GWB_CUDA(cudaMemcpyAsync(sp, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, s_));
-    launch_colmajor64_to_rowmajor32(sp, m_, m_, Dy_, ldm_, s_);
+    if (graphs) {
+      build_adjacency(graphs->ex, graphs->cx, n_, Dx_, ldn_, s_);
+      build_adjacency(graphs->ey, graphs->cy, m_, Dy_, ldm_, s_);
+    } else {
+      GWB_CUDA(cudaMemcpyAsync(sp, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, s_));
+      launch_colmajor64_to_rowmajor32(sp, n_, n_, Dx_, ldn_, s_);
+      GWB_CUDA(cudaMemcpyAsync(sp, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, s_));
+      launch_colmajor64_to_rowmajor32(sp, m_, m_, Dy_, ldm_, s_);
+    }
     choose_precision();
     GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
@@ -951,7 +955,7 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
                    const double* dy, int64_t m, const double* mu, const double* nu,
                    const double* initial, gwb_observer observer, void* user, double* out_final,
                    gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                   int32_t* iterations_used) {
+                   int32_t* iterations_used, const GraphInput* graphs) {
   if (cfg->record_residual)
     api_fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
   if (trace && trace_cap < cfg->max_iters) api_fail(GWB_ERR_CAPACITY, "trace capacity < max_iters");
@@ -966,14 +970,15 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
   const bool bpg_may_run =
       algo == GWB_BPG || (algo == GWB_HBPG && cfg->max_iters >= 1);
   BregmanEngine eng(device, n, m, *cfg, algo);
-  eng.load(dx, dy, mu, nu, initial);
+  eng.load(dx, dy, mu, nu, initial, graphs);
   std::vector<double> host_pi;
   eng.run(observer, user, &host_pi);
   const BState s = eng.status();
   if (s.flags) raise_breg(s, cfg->log_domain != 0);
   const int used = s.iter - 1;
   if (bpg_may_run && (algo == GWB_BPG || s.used1 < used || s.phase == 2) && !cfg->quiet) {
-    const double lip = device_lipschitz_bound(dx, n, dy, m);
+    const double lip = graphs ? device_lipschitz_bound_graphs(*graphs, n, m)
+                              : device_lipschitz_bound(dx, n, dy, m);
     if (lip > 0.0 && cfg->step > 1.0 / lip)
       std::fprintf(stderr,
                    "bpg: step %g exceeds sigma/L_f = %g; descent is not guaranteed at this step "

@@ -193,7 +193,7 @@ void raise_device_flags(const gwb::DevStatus& s, const char* solver) {
 // bapg_solve (solvers.cpp:138-217) on the device engine.
 void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, int64_t m,
           const double* mu, const double* nu, const double* initial, gwb_observer observer,
-          void* user, const SolveOut& o) {
+          void* user, const SolveOut& o, const gwb::GraphInput* graphs) {
   if (cfg->geometry != GWB_ENTROPY)
     fail(GWB_ERR_UNSUPPORTED, "quadratic-geometry BAPG is outside the B200 path (DESIGN.md)");
   if (cfg->record_residual)
@@ -226,7 +226,10 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
     fail(GWB_ERR_CAPACITY, fmt("trace capacity %d < max_iters %d", o.trace_cap, cfg->max_iters));
   const int device = primary_device();
   BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
-  eng.load_host(dx, dy, mu, nu);
+  if (graphs)
+    eng.load_graphs(*graphs, mu, nu);
+  else
+    eng.load_host(dx, dy, mu, nu);
   eng.reset(initial ? w0.data() : nullptr);
   gwb::DevStatus s;
   if (!observer) {
@@ -273,7 +276,7 @@ int32_t solve_impl(int32_t expected, const gwb_config* cfg, const double* dx, in
                    const double* initial, gwb_observer observer, void* user, double* out_final,
                    double* out_pi, double* out_w, gwb_record* trace, int32_t trace_cap,
                    int32_t* n_records, int32_t* converged, int32_t* iterations_used,
-                   gwb_status* st) {
+                   gwb_status* st, const gwb::GraphInput* graphs = nullptr) {
   return guarded(st, [&] {
     if (!cfg) fail(GWB_ERR_CONFIG, "null config");
     const int32_t algo = expected >= 0 ? expected : cfg->algorithm;
@@ -283,18 +286,19 @@ int32_t solve_impl(int32_t expected, const gwb_config* cfg, const double* dx, in
     }
     validate_config(cfg);
     if (n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "distance matrix must be nonempty");
-    if (!dx || !dy || !mu || !nu || !out_final) fail(GWB_ERR_INVALID, "null input/output buffer");
+    if ((!graphs && (!dx || !dy)) || !mu || !nu || !out_final)
+      fail(GWB_ERR_INVALID, "null input/output buffer");
     if (n_records) *n_records = 0;
     const SolveOut o{out_final, out_pi, out_w, trace, trace_cap, n_records, converged, iterations_used};
     switch (algo) {
       case GWB_BAPG:
-        bapg(cfg, dx, n, dy, m, mu, nu, initial, observer, user, o);
+        bapg(cfg, dx, n, dy, m, mu, nu, initial, observer, user, o, graphs);
         return;
       case GWB_EBPG:
       case GWB_BPG:
       case GWB_HBPG:
         gwb::bregman_solve(cfg, algo, dx, n, dy, m, mu, nu, initial, observer, user, out_final,
-                           trace, trace_cap, n_records, converged, iterations_used);
+                           trace, trace_cap, n_records, converged, iterations_used, graphs);
         return;
       case GWB_FW:
         fail(GWB_ERR_UNSUPPORTED,
@@ -357,6 +361,39 @@ int32_t gwb_bapg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_BAPG, GWB_SOL
 int32_t gwb_bpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_BPG, GWB_SOLVE_ARGS); }
 int32_t gwb_ebpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_EBPG, GWB_SOLVE_ARGS); }
 int32_t gwb_hbpg_solve GWB_SOLVE_SIGNATURE { return solve_impl(GWB_HBPG, GWB_SOLVE_ARGS); }
+
+namespace {
+// Graph::Graph validation (types.cpp:155-174).
+void validate_graph(int64_t nodes, const int32_t* edges, int64_t count) {
+  if (nodes <= 0) fail(GWB_ERR_INVALID, "graph must have at least one node");
+  if (count < 0 || (count > 0 && !edges)) fail(GWB_ERR_INVALID, "null edge list");
+  for (int64_t k = 0; k < count; ++k) {
+    const int32_t a = edges[2 * k], b = edges[2 * k + 1];
+    if (a == b) fail(GWB_ERR_INVALID, fmt("self-loop at node %d", a));
+    if (a < 0 || b < 0 || a >= nodes || b >= nodes)
+      fail(GWB_ERR_INVALID, fmt("edge (%d,%d) out of range for %lld nodes", a, b,
+                                static_cast<long long>(nodes)));
+  }
+}
+}  // namespace
+
+int32_t gwb_solve_graphs(const gwb_config* cfg, int64_t n, const int32_t* edges_x,
+                         int64_t count_x, int64_t m, const int32_t* edges_y, int64_t count_y,
+                         const double* mu, const double* nu, const double* initial,
+                         gwb_observer observer, void* user, double* out_final, double* out_pi,
+                         double* out_w, gwb_record* trace, int32_t trace_cap,
+                         int32_t* n_records, int32_t* converged, int32_t* iterations_used,
+                         gwb_status* st) {
+  const int32_t rc = guarded(st, [&] {
+    validate_graph(n, edges_x, count_x);
+    validate_graph(m, edges_y, count_y);
+  });
+  if (rc != GWB_OK) return rc;
+  const gwb::GraphInput g{edges_x, count_x, edges_y, count_y};
+  return solve_impl(-1, cfg, nullptr, n, nullptr, m, mu, nu, initial, observer, user, out_final,
+                    out_pi, out_w, trace, trace_cap, n_records, converged, iterations_used, st,
+                    &g);
+}
 
 int32_t gwb_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
                          const double* pi, int64_t pi_rows, int64_t pi_cols, double* out,

@@ -4,12 +4,18 @@
 // float4 accesses never leave the allocation.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
 
 #include "devutil.cuh"
 #include "kernels.cuh"
+
+namespace gwb {
+void check_cuda(cudaError_t e, const char* what);  // solver.cu: throws CudaError
+}
+#define GWB_CUDA_K(x) ::gwb::check_cuda((x), #x)
 
 namespace gwb {
 
@@ -508,6 +514,30 @@ void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, floa
 void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,
                              float* P, cudaStream_t s) {
   product_coupling_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(mu, nu, n, m, ld, P);
+}
+
+namespace {
+__global__ void adjacency_kernel(const int2* __restrict__ e, int64_t count, float* D, int64_t ld) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int2 p = e[k];
+    D[static_cast<int64_t>(p.x) * ld + p.y] = 1.0f;
+    D[static_cast<int64_t>(p.y) * ld + p.x] = 1.0f;
+  }
+}
+}  // namespace
+
+void build_adjacency(const int32_t* edges_host, int64_t count, int64_t rows, float* D, int64_t ld,
+                     cudaStream_t s) {
+  GWB_CUDA_K(cudaMemsetAsync(D, 0, sizeof(float) * static_cast<size_t>(rows) * ld, s));
+  if (count <= 0) return;
+  int2* e = nullptr;
+  GWB_CUDA_K(cudaMallocAsync(reinterpret_cast<void**>(&e), sizeof(int2) * count, s));
+  GWB_CUDA_K(cudaMemcpyAsync(e, edges_host, sizeof(int2) * count, cudaMemcpyHostToDevice, s));
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  adjacency_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(e, count, D, ld);
+  GWB_CUDA_K(cudaGetLastError());
+  GWB_CUDA_K(cudaFreeAsync(e, s));
 }
 
 }  // namespace gwb

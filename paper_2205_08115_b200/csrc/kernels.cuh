@@ -140,6 +140,18 @@ void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
                     int* out_inexact, cudaStream_t s);
 // P = μ νᵀ (product coupling, types.cpp:204-207) in row-major fp32.
+// Graph inputs: host int32 edge lists (pairs a, b; validated by the caller)
+// standing for D = adjacency_distance(g) (tasks.cpp:167-174).
+struct GraphInput {
+  const int32_t* ex;
+  int64_t cx;
+  const int32_t* ey;
+  int64_t cy;
+};
+// D (rows × rows fp32 row-major, leading dim ld) ← 0/1 adjacency of the host
+// edge list: zero fill, one H2D of 8 B per edge, scatter D[a][b] = D[b][a] = 1.
+void build_adjacency(const int32_t* edges_host, int64_t count, int64_t rows, float* D, int64_t ld,
+                     cudaStream_t s);
 void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,
                              float* P, cudaStream_t s);
 

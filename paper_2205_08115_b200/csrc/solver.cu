@@ -353,6 +353,17 @@ void BapgEngine::load_host(const double* dx, const double* dy, const double* mu,
   launch_colmajor64_to_rowmajor32(stage, m_, m_, Dy_, ldm_, stream_);
   GWB_CUDA(cudaStreamSynchronize(stream_));
   GWB_CUDA(cudaFree(stage));
+  load_marginals(mu, nu);
+}
+
+void BapgEngine::load_graphs(const GraphInput& g, const double* mu, const double* nu) {
+  GWB_CUDA(cudaSetDevice(device_));
+  build_adjacency(g.ex, g.cx, n_, Dx_, ldn_, stream_);
+  build_adjacency(g.ey, g.cy, m_, Dy_, ldm_, stream_);
+  load_marginals(mu, nu);
+}
+
+void BapgEngine::load_marginals(const double* mu, const double* nu) {
   std::vector<float> mu32(n_), nu32(m_);
   for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
   for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);

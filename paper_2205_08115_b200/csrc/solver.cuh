@@ -49,6 +49,8 @@ class BapgEngine {
   // Inputs from host fp64 column-major (symmetric D: layout-free) or from
   // device fp32 row-major.
   void load_host(const double* dx, const double* dy, const double* mu, const double* nu);
+  // D_X, D_Y = adjacency_distance of host edge lists, built on the device.
+  void load_graphs(const GraphInput& g, const double* mu, const double* nu);
   void load_device(const float* dx, int64_t ldx, const float* dy, int64_t ldy, const float* mu,
                    const float* nu);
   // π0 = μνᵀ or `initial` (host fp64 col-major); w0 = kl_scale(π0, ν, Cols)
@@ -80,6 +82,7 @@ class BapgEngine {
   void alloc();
   void build_plans();
   void prepare_d();
+  void load_marginals(const double* mu, const double* nu);  // + prepare_d()
   int64_t enqueue_iteration(int parity, double rel_tol);
   int64_t enqueue_half(int parity, bool half_b, double rel_tol);
   void destroy_graphs();

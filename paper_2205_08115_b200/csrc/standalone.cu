@@ -318,16 +318,15 @@ void device_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out
 }
 
 // spectral_norm (solvers.cpp:113-129): power iteration on D² in fp64.
-static double spectral_norm_dev(const double* d_host, int64_t n) {
-  DBuf<double> d(static_cast<size_t>(n) * n), x(n), t(n), y(n);
-  d.up(d_host);
-  if (sum_sq_diff(d.p, nullptr, n * n) == 0.0) return 0.0;
+static double spectral_norm_on_device(const double* d, int64_t n) {
+  DBuf<double> x(n), t(n), y(n);
+  if (sum_sq_diff(d, nullptr, n * n) == 0.0) return 0.0;
   std::vector<double> hx(n, 1.0 / std::sqrt(static_cast<double>(n)));
   x.up(hx.data());
   double lambda = 0.0;
   for (int it = 0; it < 10000; ++it) {
-    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d.p, n, x.p, t.p);
-    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d.p, n, t.p, y.p);
+    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d, n, x.p, t.p);
+    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d, n, t.p, y.p);
     const double est = std::sqrt(sum_sq_diff(y.p, nullptr, n));
     if (est == 0.0) return 0.0;
     div_kernel<<<blocks(n, 256), 256>>>(y.p, n, est);
@@ -339,9 +338,43 @@ static double spectral_norm_dev(const double* d_host, int64_t n) {
   return std::sqrt(lambda);
 }
 
+static double spectral_norm_dev(const double* d_host, int64_t n) {
+  DBuf<double> d(static_cast<size_t>(n) * n);
+  d.up(d_host);
+  return spectral_norm_on_device(d.p, n);
+}
+
+__global__ void adjacency64_kernel(const int2* e, int64_t count, int64_t n, double* D) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int2 p = e[k];
+    D[static_cast<int64_t>(p.x) * n + p.y] = 1.0;
+    D[static_cast<int64_t>(p.y) * n + p.x] = 1.0;
+  }
+}
+
+// ‖A‖₂ of adjacency_distance(g) (tasks.cpp:167-174) built on the device.
+static double spectral_norm_graph(const int32_t* edges, int64_t count, int64_t n) {
+  DBuf<double> d(static_cast<size_t>(n) * n);
+  GWB_CUDA(cudaMemset(d.p, 0, sizeof(double) * static_cast<size_t>(n) * n));
+  if (count > 0) {
+    DBuf<int2> e(static_cast<size_t>(count));
+    GWB_CUDA(cudaMemcpy(e.p, edges, sizeof(int2) * count, cudaMemcpyHostToDevice));
+    adjacency64_kernel<<<static_cast<unsigned>(std::min<int64_t>(blocks(count, 256), 1184)), 256>>>(
+        e.p, count, n, d.p);
+    GWB_CUDA(cudaGetLastError());
+  }
+  return spectral_norm_on_device(d.p, n);
+}
+
 double device_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m) {
   GWB_CUDA(cudaSetDevice(api_device()));
   return spectral_norm_dev(dx, n) * spectral_norm_dev(dy, m);
+}
+
+double device_lipschitz_bound_graphs(const GraphInput& g, int64_t n, int64_t m) {
+  GWB_CUDA(cudaSetDevice(api_device()));
+  return spectral_norm_graph(g.ex, g.cx, n) * spectral_norm_graph(g.ey, g.cy, m);
 }
 
 void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* mu,

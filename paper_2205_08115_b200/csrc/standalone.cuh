@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/gwb.h"
+#include "kernels.cuh"
 
 namespace gwb {
 
@@ -21,6 +22,7 @@ double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_
 void device_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
                              double* out);
 double device_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m);
+double device_lipschitz_bound_graphs(const GraphInput& g, int64_t n, int64_t m);
 void device_kl_scale(const double* pi, int64_t n, int64_t m, const double* target, int32_t axis,
                      double* out);
 void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* mu,
@@ -37,7 +39,7 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
                    const double* dy, int64_t m, const double* mu, const double* nu,
                    const double* initial, gwb_observer observer, void* user, double* out_final,
                    gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                   int32_t* iterations_used);
+                   int32_t* iterations_used, const GraphInput* graphs = nullptr);
 
 // Batched BAPG over independent small problems (config 5).
 void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
