@@ -237,10 +237,10 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
-PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4}
-PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2"}
+PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5}
+PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse"}
 # tensor passes per chain GEMM for 0/1 structure matrices, and the MMA kind
-PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16")}
+PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16"), 5: (0, "none")}
 
 
 def time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks=None):
@@ -319,7 +319,7 @@ def run_ours(args, world, rank, local, dist):
     main = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks)
     variants = {}
     if not args.no_variants:
-        for name in ("3xtf32", "bf16x2"):
+        for name in ("3xtf32", "bf16x2", "sparse"):
             if PREC_NAMES[name] == main["precision"]:
                 continue
             v = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, PREC_NAMES[name],
@@ -327,6 +327,13 @@ def run_ours(args, world, rank, local, dist):
             variants[name] = {"value": world * args.steps / (v["ms"] * 1e-3), "unit": "it/s",
                               "chain_tflops_alg": (v["flops_it"] / 2) / (v["chain_ms"] * 1e-3) / 1e12
                               if v["chain_ms"] > 0 else None}
+            if name == "sparse":
+                # HBM/L2-bound: report the chain time and the projection passes.
+                variants[name].update({
+                    "chain_ms_per_half_step": v["chain_ms"],
+                    "projection_ms_per_half_step": v["scal_ms"],
+                    "note": "CSR row-gather chain (fp32 exact-order sums): a separate metric, "
+                            "SURVEY 8(f) row 2; FLOPs are the sparse ones"})
     ms = main["ms"]
     value_rank = args.steps / (ms * 1e-3)
     value = value_rank * world  # replicas: every rank runs the full problem

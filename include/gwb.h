@@ -50,7 +50,8 @@ enum gwb_precision {
   GWB_PREC_TF32 = 1,    /* 1 kind::tf32 pass, rna-rounded operands */
   GWB_PREC_3XTF32 = 2,  /* hi/lo TF32 split passes (2 when D is 0/1) */
   GWB_PREC_BF16X3 = 3,  /* exact-bf16 D × 3 bf16 planes of the iterate (24-bit) */
-  GWB_PREC_BF16X2 = 4   /* exact-bf16 D × 2 bf16 planes (16-bit) */
+  GWB_PREC_BF16X2 = 4,  /* exact-bf16 D × 2 bf16 planes (16-bit) */
+  GWB_PREC_SPARSE = 5   /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
 };
 
 /* Error codes; each maps to one reference exception class. */

@@ -160,6 +160,8 @@ void validate_config(const gwb_config* c) {
   if (c->perturbation < 0.0 || c->perturbation >= 1.0)
     fail(GWB_ERR_CONFIG, "perturbation must lie in [0, 1)");
   if (c->switch_iters < 0) fail(GWB_ERR_CONFIG, "switch-iters must be >= 0");
+  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_SPARSE)
+    fail(GWB_ERR_CONFIG, "unknown precision");
 }
 
 void require_algorithm(const gwb_config* c, int32_t expected, const char* who) {

@@ -91,6 +91,8 @@ BapgEngine::~BapgEngine() {
   }
   gemm_plan_destroy(g2_);
   gemm_plan_destroy(g2_tail_);
+  csr_free(cx_);
+  csr_free(cy_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], Vt_,
@@ -155,10 +157,11 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.mu64 = mu64_;
   d.nu64 = nu64_;
   d.P = P_;
-  d.P_aux = P_aux_;
+  // The sparse chain reads the fp32 iterates directly: no operand copies.
+  d.P_aux = sparse() ? nullptr : P_aux_;
   d.W = W_[q];
   d.W_new = W_[1 - q];
-  d.W_aux = W_aux_[1 - q];
+  d.W_aux = sparse() ? nullptr : W_aux_[1 - q];
   d.aux_mode = aux_mode();
   d.plane = n_ * ldm_;
   d.row_part = row_part_;
@@ -191,6 +194,14 @@ void BapgEngine::prepare_d() {
   dfree(d_inexact);
   dx_exact_ = (h_inexact[0] & 1) == 0;
   dy_exact_ = (h_inexact[1] & 1) == 0;
+  if (precision_ == GWB_PREC_SPARSE) {
+    destroy_graphs();
+    csr_free(cx_);
+    csr_free(cy_);
+    cx_ = csr_from_dense(Dx_, n_, ldn_, stream_);
+    cy_ = csr_from_dense(Dy_, m_, ldm_, stream_);
+    return;
+  }
   const bool bf16_exact = (h_inexact[0] & 2) == 0 && (h_inexact[1] & 2) == 0;
   if (precision_ == GWB_PREC_AUTO)
     precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, h_max[0], h_max[1], rho_);
@@ -431,8 +442,14 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
     e2 = ev_get();
     GWB_CUDA(cudaEventRecord(e0, stream_));
   }
-  GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
-  GWB_CUDA(gemm_launch(g2_, stream_));
+  if (sparse()) {
+    // Uᵀ = (D_X·X)ᵀ, then G = (D_Y·Uᵀ)ᵀ: two CSR row-gathers (sparse.cu).
+    launch_rowgather(cx_, half_b ? P_ : W_[q], ldm_, m_, Vt_, ldn_, true, &st_->done, stream_);
+    launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->done, stream_);
+  } else {
+    GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
+    GWB_CUDA(gemm_launch(g2_, stream_));
+  }
   launches += 2;
   if (timing_) GWB_CUDA(cudaEventRecord(e1, stream_));
   if (!half_b) {
@@ -524,8 +541,13 @@ void BapgEngine::run(int max_iters, double rel_tol) {
 void BapgEngine::tail() {
   GWB_CUDA(cudaSetDevice(device_));
   const BapgDev d = dev_view(parity_);
-  GWB_CUDA(gemm_launch(g1_tail_[parity_], stream_));
-  GWB_CUDA(gemm_launch(g2_tail_, stream_));
+  if (sparse()) {
+    launch_rowgather(cx_, W_[parity_], ldm_, m_, Vt_, ldn_, true, &st_->flags, stream_);
+    launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->flags, stream_);
+  } else {
+    GWB_CUDA(gemm_launch(g1_tail_[parity_], stream_));
+    GWB_CUDA(gemm_launch(g2_tail_, stream_));
+  }
   launch_row_update(d, false, stream_);
   launch_finalize(d, 0.0, true, stream_);
   GWB_CUDA(cudaGetLastError());
@@ -618,6 +640,8 @@ void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
 }
 
 double BapgEngine::gemm_flops_per_iter() const {
+  if (sparse())  // two half-steps × two row-gathers, 2 flops per stored entry touched
+    return 2.0 * 2.0 * (static_cast<double>(cx_.nnz) * m_ + static_cast<double>(cy_.nnz) * n_);
   // Two half-steps × (m·n·m + n·m·n) MACs × 2.
   return 2.0 * 2.0 * static_cast<double>(n_) * m_ * static_cast<double>(n_ + m_);
 }

@@ -14,6 +14,7 @@
 #include "../../include/gwb.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "sparse.cuh"
 
 namespace gwb {
 
@@ -100,7 +101,9 @@ class BapgEngine {
   // device buffers
   float *Dx_ = nullptr, *Dx_aux_ = nullptr, *Dy_ = nullptr, *Dy_aux_ = nullptr;
   float *Dx_bf_ = nullptr, *Dy_bf_ = nullptr;  // bf16 copies (bf16 split modes)
+  Csr cx_, cy_;                                // sparse chain (GWB_PREC_SPARSE)
   bool bf16() const { return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2; }
+  bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
   int aux_mode() const {
     return precision_ == GWB_PREC_TF32 ? 1
            : precision_ == GWB_PREC_BF16X3 ? 3

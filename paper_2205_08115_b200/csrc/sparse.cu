@@ -1,0 +1,164 @@
+// sparse.cu — CSR construction and the column-blocked row-gather SpMM used
+// by the sparse chain (see sparse.cuh).
+//
+// G = D_X · X · D_Yᵀ is evaluated as
+//   Uᵀ = (D_X · X)ᵀ     row-gather over the rows of X, tile-transposed store
+//   G  = (D_Y · Uᵀ)ᵀ    row-gather over the rows of Uᵀ, tile-transposed store
+// so both products gather whole rows (coalesced float4) and both results land
+// in the layouts the projection kernels already read (G row-major).
+#include "sparse.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+#include <vector>
+
+namespace gwb {
+
+void check_cuda(cudaError_t e, const char* what);  // solver.cu
+
+#define GWB_CUDA_S(x) ::gwb::check_cuda((x), #x)
+
+namespace {
+
+constexpr int kTileRows = 32;   // output rows per CTA
+constexpr int kTileCols = 128;  // output columns per CTA (a float4 per lane)
+constexpr int kThreads = 256;   // 8 warps × 4 rows
+
+__global__ void csr_count_kernel(const float* __restrict__ D, int64_t rows, int64_t ld,
+                                 int32_t* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  if (i >= rows) return;
+  const int lane = threadIdx.x & 31;
+  int c = 0;
+  for (int64_t j = lane; j < rows; j += 32) c += D[i * ld + j] != 0.0f;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[i] = c;
+}
+
+__global__ void csr_fill_kernel(const float* __restrict__ D, int64_t rows, int64_t ld,
+                                const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                float* __restrict__ val) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  if (i >= rows) return;
+  const int lane = threadIdx.x & 31;
+  int32_t off = row_ptr[i];
+  for (int64_t j0 = 0; j0 < rows; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const float v = j < rows ? D[i * ld + j] : 0.0f;
+    const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0f);
+    if (v != 0.0f) {
+      const int32_t p = off + __popc(mask & ((1u << lane) - 1u));
+      col[p] = static_cast<int32_t>(j);
+      val[p] = v;
+    }
+    off += __popc(mask);
+  }
+}
+
+// One CTA: kTileRows output rows × kTileCols columns.  Warp w owns rows
+// r0 + 4w … r0 + 4w + 3; lane l owns columns c0 + 4l … c0 + 4l + 3.
+template <bool kTranspose>
+__global__ void __launch_bounds__(kThreads) rowgather_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+    const float* __restrict__ val, int64_t rows_out, const float* __restrict__ in,
+    int64_t ld_in, int64_t cols, float* __restrict__ out, int64_t ld_out, const int* skip) {
+  if (skip && *skip) return;
+  __shared__ float tile[kTranspose ? kTileCols : 1][kTileRows + 1];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTileRows;
+  const int64_t c = static_cast<int64_t>(blockIdx.y) * kTileCols + lane * 4;
+  const bool col_ok = c < cols;  // ld_in, ld_out are multiples of 32: c..c+3 stay inside
+#pragma unroll
+  for (int rr = 0; rr < kTileRows / 8; ++rr) {
+    const int lr = warp * (kTileRows / 8) + rr;
+    const int64_t i = r0 + lr;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < rows_out && col_ok) {
+      const int32_t p1 = row_ptr[i + 1];
+      for (int32_t p = row_ptr[i]; p < p1; ++p) {
+        const float a = val[p];
+        const float4 x = __ldg(reinterpret_cast<const float4*>(in + static_cast<int64_t>(col[p]) * ld_in + c));
+        acc.x = fmaf(a, x.x, acc.x);
+        acc.y = fmaf(a, x.y, acc.y);
+        acc.z = fmaf(a, x.z, acc.z);
+        acc.w = fmaf(a, x.w, acc.w);
+      }
+    }
+    if (!kTranspose) {
+      if (i < rows_out && col_ok) *reinterpret_cast<float4*>(out + i * ld_out + c) = acc;
+    } else {
+      tile[lane * 4 + 0][lr] = acc.x;
+      tile[lane * 4 + 1][lr] = acc.y;
+      tile[lane * 4 + 2][lr] = acc.z;
+      tile[lane * 4 + 3][lr] = acc.w;
+    }
+  }
+  if (kTranspose) {
+    __syncthreads();
+    // outᵀ rows = columns of the tile; each warp writes 16 rows of 32 floats.
+    for (int cc = warp; cc < kTileCols; cc += kThreads / 32) {
+      const int64_t j = static_cast<int64_t>(blockIdx.y) * kTileCols + cc;
+      const int64_t i = r0 + lane;
+      if (j < cols && i < rows_out) out[j * ld_out + i] = tile[cc][lane];
+    }
+  }
+}
+
+}  // namespace
+
+Csr csr_from_dense(const float* D, int64_t rows, int64_t ld, cudaStream_t s) {
+  Csr c;
+  c.rows = rows;
+  int32_t* cnt = nullptr;
+  GWB_CUDA_S(cudaMalloc(&cnt, sizeof(int32_t) * (rows + 1)));
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  csr_count_kernel<<<grid, 256, 0, s>>>(D, rows, ld, cnt);
+  GWB_CUDA_S(cudaGetLastError());
+  std::vector<int32_t> h(static_cast<size_t>(rows) + 1, 0);
+  GWB_CUDA_S(cudaMemcpyAsync(h.data() + 1, cnt, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, s));
+  GWB_CUDA_S(cudaStreamSynchronize(s));
+  int64_t total = 0;
+  for (int64_t i = 1; i <= rows; ++i) {
+    total += h[i];
+    h[i] = static_cast<int32_t>(total);
+  }
+  if (total > 0x7fffffffLL) {
+    cudaFree(cnt);
+    throw std::invalid_argument("structure matrix too dense for the sparse chain (nnz > 2^31)");
+  }
+  c.nnz = total;
+  c.row_ptr = cnt;  // reused as row_ptr (rows + 1 entries)
+  GWB_CUDA_S(cudaMemcpyAsync(c.row_ptr, h.data(), sizeof(int32_t) * (rows + 1), cudaMemcpyHostToDevice, s));
+  GWB_CUDA_S(cudaMalloc(&c.col, sizeof(int32_t) * std::max<int64_t>(total, 1)));
+  GWB_CUDA_S(cudaMalloc(&c.val, sizeof(float) * std::max<int64_t>(total, 1)));
+  csr_fill_kernel<<<grid, 256, 0, s>>>(D, rows, ld, c.row_ptr, c.col, c.val);
+  GWB_CUDA_S(cudaGetLastError());
+  GWB_CUDA_S(cudaStreamSynchronize(s));  // h goes out of scope
+  return c;
+}
+
+void csr_free(Csr& c) {
+  if (c.row_ptr) cudaFree(c.row_ptr);
+  if (c.col) cudaFree(c.col);
+  if (c.val) cudaFree(c.val);
+  c = Csr{};
+}
+
+void launch_rowgather(const Csr& A, const float* in, int64_t ld_in, int64_t cols, float* out,
+                      int64_t ld_out, bool transpose_out, const int* skip, cudaStream_t s) {
+  // blockIdx.x (fastest) walks row tiles, so one column slab of `in`
+  // (rows × 512 B) is shared by all CTAs in flight and stays in L2.
+  const dim3 grid(static_cast<unsigned>((A.rows + kTileRows - 1) / kTileRows),
+                  static_cast<unsigned>((cols + kTileCols - 1) / kTileCols));
+  if (transpose_out)
+    rowgather_kernel<true><<<grid, kThreads, 0, s>>>(A.row_ptr, A.col, A.val, A.rows, in, ld_in,
+                                                     cols, out, ld_out, skip);
+  else
+    rowgather_kernel<false><<<grid, kThreads, 0, s>>>(A.row_ptr, A.col, A.val, A.rows, in, ld_in,
+                                                      cols, out, ld_out, skip);
+  GWB_CUDA_S(cudaGetLastError());
+}
+
+}  // namespace gwb
