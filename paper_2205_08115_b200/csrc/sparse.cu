@@ -58,41 +58,65 @@ __global__ void csr_fill_kernel(const float* __restrict__ D, int64_t rows, int64
 }
 
 // One CTA: kTileRows output rows × kTileCols columns.  Warp w owns rows
-// r0 + 4w … r0 + 4w + 3; lane l owns columns c0 + 4l … c0 + 4l + 3.
+// r0 + 4w … r0 + 4w + 3; lane l owns columns c0 + 4l … c0 + 4l + 3.  Each
+// row's (col, val) pairs are fetched 32 at a time with one coalesced load and
+// broadcast by shuffles; the gathers are issued four at a time.
 template <bool kTranspose>
 __global__ void __launch_bounds__(kThreads) rowgather_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
     const float* __restrict__ val, int64_t rows_out, const float* __restrict__ in,
     int64_t ld_in, int64_t cols, float* __restrict__ out, int64_t ld_out, const int* skip) {
   if (skip && *skip) return;
-  __shared__ float tile[kTranspose ? kTileCols : 1][kTileRows + 1];
+  // [column mod 4][column / 4][row]: conflict-free on both the scatter (lanes
+  // vary column / 4) and the transposed read (lanes vary row).
+  __shared__ float tile[kTranspose ? 4 : 1][kTranspose ? 32 : 1][kTileRows + 1];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTileRows;
   const int64_t c = static_cast<int64_t>(blockIdx.y) * kTileCols + lane * 4;
   const bool col_ok = c < cols;  // ld_in, ld_out are multiples of 32: c..c+3 stay inside
-#pragma unroll
+  const float* in_c = in + (col_ok ? c : 0);
+#pragma unroll 1
   for (int rr = 0; rr < kTileRows / 8; ++rr) {
     const int lr = warp * (kTileRows / 8) + rr;
     const int64_t i = r0 + lr;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < rows_out && col_ok) {
-      const int32_t p1 = row_ptr[i + 1];
-      for (int32_t p = row_ptr[i]; p < p1; ++p) {
-        const float a = val[p];
-        const float4 x = __ldg(reinterpret_cast<const float4*>(in + static_cast<int64_t>(col[p]) * ld_in + c));
-        acc.x = fmaf(a, x.x, acc.x);
-        acc.y = fmaf(a, x.y, acc.y);
-        acc.z = fmaf(a, x.z, acc.z);
-        acc.w = fmaf(a, x.w, acc.w);
+    if (i < rows_out) {
+      const int32_t beg = row_ptr[i], end = row_ptr[i + 1];
+      for (int32_t base = beg; base < end; base += 32) {
+        const int cnt = min(32, end - base);
+        const int32_t my_k = lane < cnt ? col[base + lane] : 0;
+        const float my_a = lane < cnt ? val[base + lane] : 0.f;
+        for (int t = 0; t < cnt; t += 4) {
+          int32_t k[4];
+          float a[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            k[u] = __shfl_sync(0xffffffffu, my_k, (t + u) & 31);
+            a[u] = __shfl_sync(0xffffffffu, my_a, (t + u) & 31);
+            if (t + u >= cnt) a[u] = 0.f;  // k[u] is a valid row (lane ≥ cnt loads row 0)
+          }
+          float4 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            x[u] = col_ok ? __ldg(reinterpret_cast<const float4*>(in_c + static_cast<int64_t>(k[u]) * ld_in))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc.x = fmaf(a[u], x[u].x, acc.x);
+            acc.y = fmaf(a[u], x[u].y, acc.y);
+            acc.z = fmaf(a[u], x[u].z, acc.z);
+            acc.w = fmaf(a[u], x[u].w, acc.w);
+          }
+        }
       }
     }
     if (!kTranspose) {
       if (i < rows_out && col_ok) *reinterpret_cast<float4*>(out + i * ld_out + c) = acc;
     } else {
-      tile[lane * 4 + 0][lr] = acc.x;
-      tile[lane * 4 + 1][lr] = acc.y;
-      tile[lane * 4 + 2][lr] = acc.z;
-      tile[lane * 4 + 3][lr] = acc.w;
+      tile[0][lane][lr] = acc.x;
+      tile[1][lane][lr] = acc.y;
+      tile[2][lane][lr] = acc.z;
+      tile[3][lane][lr] = acc.w;
     }
   }
   if (kTranspose) {
@@ -101,7 +125,7 @@ __global__ void __launch_bounds__(kThreads) rowgather_kernel(
     for (int cc = warp; cc < kTileCols; cc += kThreads / 32) {
       const int64_t j = static_cast<int64_t>(blockIdx.y) * kTileCols + cc;
       const int64_t i = r0 + lane;
-      if (j < cols && i < rows_out) out[j * ld_out + i] = tile[cc][lane];
+      if (j < cols && i < rows_out) out[j * ld_out + i] = tile[cc & 3][cc >> 2][lane];
     }
   }
 }
