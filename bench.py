@@ -237,10 +237,11 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
-PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5}
-PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse"}
+PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6}
+PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32"}
 # tensor passes per chain GEMM for 0/1 structure matrices, and the MMA kind
-PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16"), 5: (0, "none")}
+PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16"), 5: (0, "none"),
+               6: (0, "fp32 FMA")}
 
 
 def time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks=None):

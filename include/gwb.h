@@ -51,7 +51,8 @@ enum gwb_precision {
   GWB_PREC_3XTF32 = 2,  /* hi/lo TF32 split passes (2 when D is 0/1) */
   GWB_PREC_BF16X3 = 3,  /* exact-bf16 D × 3 bf16 planes of the iterate (24-bit) */
   GWB_PREC_BF16X2 = 4,  /* exact-bf16 D × 2 bf16 planes (16-bit) */
-  GWB_PREC_SPARSE = 5   /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
+  GWB_PREC_SPARSE = 5,  /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
+  GWB_PREC_FP32 = 6     /* FP32-pipe chain for skinny problems (m ≤ 32); AUTO picks it */
 };
 
 /* Error codes; each maps to one reference exception class. */

@@ -160,7 +160,7 @@ void validate_config(const gwb_config* c) {
   if (c->perturbation < 0.0 || c->perturbation >= 1.0)
     fail(GWB_ERR_CONFIG, "perturbation must lie in [0, 1)");
   if (c->switch_iters < 0) fail(GWB_ERR_CONFIG, "switch-iters must be >= 0");
-  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_SPARSE)
+  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_FP32)
     fail(GWB_ERR_CONFIG, "unknown precision");
 }
 

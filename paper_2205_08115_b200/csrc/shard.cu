@@ -619,8 +619,8 @@ int32_t gwb_shard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t ra
   return shard_guard(st, [&] {
     if (!cfg || n < 1 || m < 1 || world < 1 || rank < 0 || rank >= world)
       throw std::invalid_argument("gwb_shard_create: bad arguments");
-    if (cfg->precision == GWB_PREC_SPARSE)
-      throw std::invalid_argument("gwb_shard_create: the sparse chain is single-GPU only");
+    if (cfg->precision == GWB_PREC_SPARSE || cfg->precision == GWB_PREC_FP32)
+      throw std::invalid_argument("gwb_shard_create: the sparse and fp32 chains are single-GPU only");
     auto* s = new gwb_shard();
     s->n = n;
     s->m = m;

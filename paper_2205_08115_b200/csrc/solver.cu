@@ -93,6 +93,8 @@ BapgEngine::~BapgEngine() {
   gemm_plan_destroy(g2_tail_);
   csr_free(cx_);
   csr_free(cy_);
+  dfree(Vs_);
+  dfree(DyT_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], Vt_,
@@ -158,10 +160,10 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.nu64 = nu64_;
   d.P = P_;
   // The sparse chain reads the fp32 iterates directly: no operand copies.
-  d.P_aux = sparse() ? nullptr : P_aux_;
+  d.P_aux = no_planes() ? nullptr : P_aux_;
   d.W = W_[q];
   d.W_new = W_[1 - q];
-  d.W_aux = sparse() ? nullptr : W_aux_[1 - q];
+  d.W_aux = no_planes() ? nullptr : W_aux_[1 - q];
   d.aux_mode = aux_mode();
   d.plane = n_ * ldm_;
   d.row_part = row_part_;
@@ -194,6 +196,18 @@ void BapgEngine::prepare_d() {
   dfree(d_inexact);
   dx_exact_ = (h_inexact[0] & 1) == 0;
   dy_exact_ = (h_inexact[1] & 1) == 0;
+  // Skinny problems (m ≤ 32, config 3): the FP32-pipe chain (skinny.cu).
+  // An explicit GWB_PREC_FP32 with larger m resolves like AUTO.
+  if (precision_ == GWB_PREC_FP32 && m_ > kSkinnyMaxN) precision_ = GWB_PREC_AUTO;
+  if (precision_ == GWB_PREC_AUTO && m_ <= kSkinnyMaxN) precision_ = GWB_PREC_FP32;
+  if (precision_ == GWB_PREC_FP32) {
+    destroy_graphs();
+    if (!Vs_) Vs_ = dalloc<float>(static_cast<size_t>(n_) * ldm_);
+    if (!DyT_) DyT_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
+    launch_transpose(Dy_, m_, m_, ldm_, DyT_, ldm_, stream_);
+    GWB_CUDA(cudaStreamSynchronize(stream_));
+    return;
+  }
   if (precision_ == GWB_PREC_SPARSE) {
     destroy_graphs();
     csr_free(cx_);
@@ -446,6 +460,12 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
     // Uᵀ = (D_X·X)ᵀ, then G = (D_Y·Uᵀ)ᵀ: two CSR row-gathers (sparse.cu).
     launch_rowgather(cx_, half_b ? P_ : W_[q], ldm_, m_, Vt_, ldn_, true, &st_->done, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->done, stream_);
+  } else if (fp32()) {
+    // V = X·D_Yᵀ, then G = D_X·V on the FP32 pipes (skinny.cu).
+    launch_skinny(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vs_, ldm_, n_, static_cast<int>(m_), m_,
+                  &st_->done, stream_);
+    launch_skinny(Dx_, ldn_, Vs_, ldm_, G_, ldm_, n_, static_cast<int>(m_), n_, &st_->done,
+                  stream_);
   } else {
     GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
     GWB_CUDA(gemm_launch(g2_, stream_));
@@ -544,6 +564,11 @@ void BapgEngine::tail() {
   if (sparse()) {
     launch_rowgather(cx_, W_[parity_], ldm_, m_, Vt_, ldn_, true, &st_->flags, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->flags, stream_);
+  } else if (fp32()) {
+    launch_skinny(W_[parity_], ldm_, DyT_, ldm_, Vs_, ldm_, n_, static_cast<int>(m_), m_,
+                  &st_->flags, stream_);
+    launch_skinny(Dx_, ldn_, Vs_, ldm_, G_, ldm_, n_, static_cast<int>(m_), n_, &st_->flags,
+                  stream_);
   } else {
     GWB_CUDA(gemm_launch(g1_tail_[parity_], stream_));
     GWB_CUDA(gemm_launch(g2_tail_, stream_));

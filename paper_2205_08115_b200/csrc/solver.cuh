@@ -14,6 +14,7 @@
 #include "../../include/gwb.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "skinny.cuh"
 #include "sparse.cuh"
 
 namespace gwb {
@@ -102,8 +103,11 @@ class BapgEngine {
   float *Dx_ = nullptr, *Dx_aux_ = nullptr, *Dy_ = nullptr, *Dy_aux_ = nullptr;
   float *Dx_bf_ = nullptr, *Dy_bf_ = nullptr;  // bf16 copies (bf16 split modes)
   Csr cx_, cy_;                                // sparse chain (GWB_PREC_SPARSE)
+  float *Vs_ = nullptr, *DyT_ = nullptr;       // skinny chain (GWB_PREC_FP32): V, D_Yᵀ
   bool bf16() const { return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2; }
   bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
+  bool fp32() const { return precision_ == GWB_PREC_FP32; }
+  bool no_planes() const { return sparse() || fp32(); }  // chains read the fp32 iterates
   int aux_mode() const {
     return precision_ == GWB_PREC_TF32 ? 1
            : precision_ == GWB_PREC_BF16X3 ? 3

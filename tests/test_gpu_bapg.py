@@ -83,3 +83,26 @@ def test_bapg_marginal_invariants(gpu):
     assert np.abs(pi.sum(axis=1) - inst.mu).max() <= 1e-10
     assert np.abs(w.sum(axis=0) - inst.nu).max() <= 1e-10
     assert abs(rep.final_coupling.entries().sum() - 1.0) <= 1e-9
+
+
+@pytest.mark.parametrize("precision", ["auto", "fp32"])
+def test_bapg_skinny_partition(gpu, port, precision):
+    # c3 shape class (m ≤ 32): AUTO runs the FP32-pipe chain (csrc/skinny.cu).
+    inst = I.config3(seed=2, n=700, k=20)
+    rep, o = run_both(port, inst, precision, max_iters=50)
+    assert rep.iterations_used == o.iterations_used
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+    check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
+
+
+def test_bapg_skinny_ragged_k(gpu, port):
+    # every N class of the skinny kernel's dispatch (m = 1, 5, 13, 32)
+    for k in (1, 5, 13, 32):
+        inst = I.config3(seed=k, n=300, k=k)
+        rep, o = run_both(port, inst, "auto", max_iters=20)
+        assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL, k
+        obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+        assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref), k
