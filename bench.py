@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-peak", action="store_true",
+                    help="skip the cuBLAS TF32 roofline measurement (profiling runs)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded NCCL path even at one rank (testing)")
     ap.add_argument("--cpu-size", dest="cpu_n", type=int, default=2500)
@@ -340,7 +342,7 @@ def run_ours(args, world, rank, local, dist):
     value = value_rank * world  # replicas: every rank runs the full problem
 
     peaks, peak_src = measured_peaks()
-    tf32 = measure_tf32_peak(torch) if rank == 0 else None
+    tf32 = measure_tf32_peak(torch) if (rank == 0 and not args.no_peak) else None
     # The chain runs inside 150 ms steps back to back: the sustained figure is its roofline.
     tf32_peak = tf32["sustained"] if tf32 else None
     flops_it = main["flops_it"]
