@@ -219,6 +219,19 @@ GWB_API int32_t gwb_split_gap(const double* pi, const double* w, int64_t n, int6
 GWB_API int32_t gwb_hard_assignment(const double* pi, int64_t n, int64_t m,
                             int32_t* out, gwb_status* st);
 
+/* gw::coupling_entropy (diagnostics.hpp:37-38, diagnostics.cpp:44-53):
+ * -Σ π log π over positive entries, nats (fp64 device reduction). */
+GWB_API int32_t gwb_coupling_entropy(const double* pi, int64_t n, int64_t m,
+                                     double* out, gwb_status* st);
+
+/* gw::alignment_accuracy (tasks.hpp:64, tasks.cpp:202-214): percentage of
+ * gt entries matched by pred.  GWB_ERR_DIMENSION if n_pred < n_gt
+ * ("alignment_accuracy: prediction does not cover all ground-truth nodes"),
+ * GWB_ERR_INVALID if n_gt == 0 ("empty ground truth"). */
+GWB_API int32_t gwb_alignment_accuracy(const int32_t* pred, int64_t n_pred,
+                                       const int32_t* gt, int64_t n_gt,
+                                       double* out, gwb_status* st);
+
 /* Batched BAPG over `batch` independent problems sharing n and m (config 5).
  * The reference has no batched API; its equivalent is `batch` calls of
  * gw::solve from the experiment worker pool (experiment.cpp:273-304).
@@ -272,6 +285,24 @@ GWB_API int32_t gwb_session_pi(gwb_session* s, float** pi, int64_t* ld, gwb_stat
 GWB_API int32_t gwb_session_kernel_ms(gwb_session* s, int32_t kind, double* avg_ms,
                               int64_t* count, gwb_status* st);
 GWB_API int32_t gwb_session_destroy(gwb_session* s);
+
+/* run_cell's post-solve readout (experiment.cpp:169-195) of the session's
+ * final coupling ½(π + w), computed on the device: gw_objective,
+ * marginal_infeasibility, coupling_entropy, split_gap(π, w), and the
+ * hard_assignment (written to `assignment`, n entries, if non-null) with its
+ * alignment_accuracy against `ground_truth` (n_gt entries, if non-null;
+ * same errors as gwb_alignment_accuracy).  Nothing n×m crosses PCIe. */
+typedef struct gwb_readout {
+  double objective;
+  double marginal_infeasibility;
+  double entropy;
+  double split_gap;
+  double accuracy;      /* valid iff has_accuracy */
+  int32_t has_accuracy;
+} gwb_readout;
+GWB_API int32_t gwb_session_readout(gwb_session* s, const int32_t* ground_truth,
+                                    int64_t n_gt, int32_t* assignment,
+                                    gwb_readout* out, gwb_status* st);
 
 /* Library identity: build string including the compiled GPU arch. */
 GWB_API const char* gwb_version(void);

@@ -88,6 +88,8 @@ class Oracle:
             L.gwref_marginal_infeasibility.argtypes = [_D, C.c_int64, C.c_int64, _D, _D, _D, _ST]
             L.gwref_split_gap.argtypes = [_D, _D, C.c_int64, C.c_int64, _D, _ST]
             L.gwref_hard_assignment.argtypes = [_D, C.c_int64, C.c_int64, _I, _ST]
+            L.gwref_coupling_entropy.argtypes = [_D, C.c_int64, C.c_int64, _D, _ST]
+            L.gwref_alignment_accuracy.argtypes = [_I, C.c_int64, _I, C.c_int64, _D, _ST]
         else:
             L.gwo_lipschitz_bound.argtypes = [_D, C.c_int64, _D, C.c_int64]
             L.gwo_lipschitz_bound.restype = C.c_double
@@ -96,6 +98,9 @@ class Oracle:
             L.gwo_split_gap.argtypes = [_D, _D, C.c_int64, C.c_int64]
             L.gwo_split_gap.restype = C.c_double
             L.gwo_hard_assignment.argtypes = [_D, C.c_int64, C.c_int64, _I]
+            L.gwo_coupling_entropy.argtypes = [_D, C.c_int64, C.c_int64]
+            L.gwo_coupling_entropy.restype = C.c_double
+            L.gwo_alignment_accuracy.argtypes = [_I, C.c_int64, _I, C.c_int64, _D, _ST]
 
     # -- solver -------------------------------------------------------------
     def solve(self, cfg: abi.Config, dx, dy, mu, nu, initial=None) -> OracleResult:
@@ -193,6 +198,25 @@ class Oracle:
         else:
             self.lib.gwo_hard_assignment(_p(pi), pi.shape[0], pi.shape[1], out.ctypes.data_as(_I))
         return out
+
+
+    def coupling_entropy(self, pi):
+        pi = _f(pi)
+        if self.kind == "reference":
+            out, st = C.c_double(0), abi.Status()
+            self.lib.gwref_coupling_entropy(_p(pi), pi.shape[0], pi.shape[1], C.byref(out), C.byref(st))
+            return out.value
+        return self.lib.gwo_coupling_entropy(_p(pi), pi.shape[0], pi.shape[1])
+
+    def alignment_accuracy(self, pred, gt):
+        """Returns (code, accuracy %, message)."""
+        pred = np.ascontiguousarray(pred, dtype=np.int32)
+        gt = np.ascontiguousarray(gt, dtype=np.int32)
+        out, st = C.c_double(0), abi.Status()
+        rc = getattr(self.lib, self.pre + "alignment_accuracy")(
+            pred.ctypes.data_as(_I), pred.size, gt.ctypes.data_as(_I), gt.size, C.byref(out),
+            C.byref(st))
+        return rc, out.value, st.message.decode(errors="replace")
 
 
 def reference_generators():

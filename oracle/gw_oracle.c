@@ -339,6 +339,30 @@ void gwo_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out) {
   }
 }
 
+/* coupling_entropy: diagnostics.cpp:44-53, column-major walk, 0 log 0 := 0. */
+double gwo_coupling_entropy(const double* pi, int64_t n, int64_t m) {
+  double h = 0.0;
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      const double p = pi[IDX(i, j, n)];
+      if (p > 0.0) h -= p * log(p);
+    }
+  return h;
+}
+
+/* alignment_accuracy: tasks.cpp:202-214. */
+int32_t gwo_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
+                               int64_t n_gt, double* out, gwb_status* st) {
+  if (n_pred < n_gt)
+    return set_status(st, GWB_ERR_DIMENSION, NULL, 0,
+                      "alignment_accuracy: prediction does not cover all ground-truth nodes");
+  if (n_gt == 0) return set_status(st, GWB_ERR_INVALID, NULL, 0, "empty ground truth");
+  int64_t hits = 0;
+  for (int64_t i = 0; i < n_gt; ++i) hits += pred[i] == gt[i];
+  *out = 100.0 * (double)hits / (double)n_gt;
+  return set_status(st, GWB_OK, NULL, 0, "");
+}
+
 /* validate(SolverConfig): types.cpp:176-188. */
 int32_t gwo_validate_config(const gwb_config* c, gwb_status* st) {
   if (c->rho <= 0.0) return set_status(st, GWB_ERR_CONFIG, NULL, 0, "rho must be positive");

@@ -53,6 +53,11 @@ double gwo_split_gap(const double* pi, const double* w, int64_t n, int64_t m);
 double gwo_lipschitz_bound(const double* dx, int64_t n, const double* dy,
                            int64_t m);
 void gwo_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out);
+/* coupling_entropy, diagnostics.cpp:44-53. */
+double gwo_coupling_entropy(const double* pi, int64_t n, int64_t m);
+/* alignment_accuracy, tasks.cpp:202-214 (returns a gwb_code; *out in %). */
+int32_t gwo_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
+                               int64_t n_gt, double* out, gwb_status* st);
 int32_t gwo_validate_config(const gwb_config* cfg, gwb_status* st);
 int32_t gwo_solve(const gwb_config* cfg, const double* dx, int64_t n,
                   const double* dy, int64_t m, const double* mu,

@@ -244,6 +244,19 @@ int32_t gwref_hard_assignment(const double* pi, int64_t n, int64_t m,
   });
 }
 
+int32_t gwref_coupling_entropy(const double* pi, int64_t n, int64_t m, double* out,
+                               gwb_status* st) {
+  return guarded(st, [&] { *out = gw::coupling_entropy(from_col_major(pi, n, m)); });
+}
+
+int32_t gwref_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
+                                 int64_t n_gt, double* out, gwb_status* st) {
+  return guarded(st, [&] {
+    *out = gw::alignment_accuracy(std::vector<int>(pred, pred + n_pred),
+                                  std::vector<int>(gt, gt + n_gt));
+  });
+}
+
 // Generators (tasks.cpp) — used to pin the product's instance builders.
 int32_t gwref_gen_barabasi_albert(int32_t n, int32_t m_attach, uint64_t seed,
                                   int32_t* edges, int64_t cap, int64_t* count,

@@ -48,6 +48,19 @@ class Config(C.Structure):
     ]
 
 
+class Readout(C.Structure):
+    """gwb_readout: run_cell's post-solve readout (experiment.cpp:169-195)."""
+
+    _fields_ = [
+        ("objective", C.c_double),
+        ("marginal_infeasibility", C.c_double),
+        ("entropy", C.c_double),
+        ("split_gap", C.c_double),
+        ("accuracy", C.c_double),
+        ("has_accuracy", C.c_int32),
+    ]
+
+
 def default_config(**kw) -> Config:
     """SolverConfig defaults (types.hpp:132-147; test_core.cpp:145-159)."""
     c = Config(
@@ -184,6 +197,10 @@ SIGNATURES = {
                                                C.c_int64, _D, C.c_int64, _D, _ST]),
     "gwb_split_gap": (C.c_int32, [_D, _D, C.c_int64, C.c_int64, _D, _ST]),
     "gwb_hard_assignment": (C.c_int32, [_D, C.c_int64, C.c_int64, _I32, _ST]),
+    "gwb_coupling_entropy": (C.c_int32, [_D, C.c_int64, C.c_int64, _D, _ST]),
+    "gwb_session_readout": (C.c_int32, [C.c_void_p, _I32, C.c_int64, _I32, C.POINTER(Readout),
+                                        _ST]),
+    "gwb_alignment_accuracy": (C.c_int32, [_I32, C.c_int64, _I32, C.c_int64, _D, _ST]),
     "gwb_solve_graphs": (C.c_int32, [C.POINTER(Config), C.c_int64, C.POINTER(C.c_int32),
                                      C.c_int64, C.c_int64, C.POINTER(C.c_int32), C.c_int64,
                                      _D, _D, _D, OBSERVER, C.c_void_p, _D, _D, _D,

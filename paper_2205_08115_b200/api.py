@@ -515,5 +515,26 @@ def hard_assignment(pi) -> np.ndarray:
     return out
 
 
+def coupling_entropy(pi) -> float:
+    """gw::coupling_entropy (diagnostics.cpp:44-53): −Σ π log π, nats."""
+    p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
+    out, st = C.c_double(0), abi.Status()
+    abi.load().gwb_coupling_entropy(_ptr(p), p.shape[0], p.shape[1], C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def alignment_accuracy(pred, ground_truth) -> float:
+    """gw::alignment_accuracy (tasks.cpp:202-214), percent."""
+    a = np.ascontiguousarray(pred, dtype=np.int32)
+    g = np.ascontiguousarray(ground_truth, dtype=np.int32)
+    out, st = C.c_double(0), abi.Status()
+    i32 = C.POINTER(C.c_int32)
+    abi.load().gwb_alignment_accuracy(a.ctypes.data_as(i32), a.size, g.ctypes.data_as(i32), g.size,
+                                      C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
 def version() -> str:
     return abi.load().gwb_version().decode()

@@ -458,6 +458,27 @@ int32_t gwb_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out
   return guarded(st, [&] { gwb::device_hard_assignment(pi, n, m, out); });
 }
 
+int32_t gwb_coupling_entropy(const double* pi, int64_t n, int64_t m, double* out,
+                             gwb_status* st) {
+  return guarded(st, [&] {
+    if (!pi || !out) fail(GWB_ERR_INVALID, "null buffer");
+    *out = n * m > 0 ? gwb::device_coupling_entropy(pi, n, m) : 0.0;
+  });
+}
+
+int32_t gwb_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
+                               int64_t n_gt, double* out, gwb_status* st) {
+  return guarded(st, [&] {
+    // O(n) integer work: host side, as the reference.
+    if (n_pred < n_gt)
+      fail(GWB_ERR_DIMENSION, "alignment_accuracy: prediction does not cover all ground-truth nodes");
+    if (n_gt == 0) fail(GWB_ERR_INVALID, "empty ground truth");
+    int64_t hits = 0;
+    for (int64_t i = 0; i < n_gt; ++i) hits += pred[i] == gt[i];
+    *out = 100.0 * static_cast<double>(hits) / static_cast<double>(n_gt);
+  });
+}
+
 int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
                                const double* dy, int64_t m, const double* mu, const double* nu,
                                double* out_final, double* out_pi, double* out_w,
@@ -557,6 +578,28 @@ int32_t gwb_session_pi(gwb_session* s, float** pi, int64_t* ld, gwb_status* st) 
 int32_t gwb_session_kernel_ms(gwb_session* s, int32_t kind, double* avg_ms, int64_t* count,
                               gwb_status* st) {
   return guarded(st, [&] { s->eng->kernel_ms(kind, avg_ms, count); });
+}
+
+int32_t gwb_session_readout(gwb_session* s, const int32_t* ground_truth, int64_t n_gt,
+                            int32_t* assignment, gwb_readout* out, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!s || !out) fail(GWB_ERR_INVALID, "null session or output");
+    if (ground_truth) {
+      if (n_gt == 0) fail(GWB_ERR_INVALID, "empty ground truth");
+      if (s->eng->n() < n_gt)
+        fail(GWB_ERR_DIMENSION,
+             "alignment_accuracy: prediction does not cover all ground-truth nodes");
+    }
+    gwb::Readout r;
+    s->eng->readout(ground_truth, n_gt, assignment, &r);
+    std::memset(out, 0, sizeof(*out));
+    out->objective = r.objective;
+    out->marginal_infeasibility = r.marginal_infeasibility;
+    out->entropy = r.entropy;
+    out->split_gap = r.split_gap;
+    out->accuracy = r.accuracy;
+    out->has_accuracy = ground_truth != nullptr;
+  });
 }
 
 int32_t gwb_session_destroy(gwb_session* s) {

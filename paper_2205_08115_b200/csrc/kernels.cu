@@ -546,4 +546,123 @@ void build_adjacency(const int32_t* edges_host, int64_t count, int64_t rows, flo
   GWB_CUDA_K(cudaFreeAsync(e, s));
 }
 
+// ---------------------------------------------------------------------------
+// Post-solve readout (column-major fp64 couplings).
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void rowsums_cm64_kernel(const double* pi, int64_t n, int64_t m, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t j = 0; j < m; ++j) s += pi[j * n + i];  // coalesced across threads
+  out[i] = s;
+}
+
+__global__ void colsums_cm64_kernel(const double* pi, int64_t n, int64_t m, double* out) {
+  const int64_t j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += pi[j * n + i];
+  s = warp_sum(s);
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += sh[w];
+    out[j] = t;
+  }
+}
+
+__global__ void argmax_rows_cm64_kernel(const double* pi, int64_t n, int64_t m, int32_t* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t best = 0;
+  double bv = pi[i];
+  for (int64_t j = 1; j < m; ++j) {
+    const double v = pi[j * n + i];
+    if (v > bv) {
+      bv = v;
+      best = j;
+    }
+  }
+  out[i] = static_cast<int32_t>(best);
+}
+
+__global__ void sqdiff_kernel(const double* a, const double* b, int64_t len, double* part) {
+  double t = 0.0;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double d = b ? a[k] - b[k] : a[k];
+    t += d * d;
+  }
+  t = warp_sum(t);
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) u += sh[w];
+    part[blockIdx.x] = u;
+  }
+}
+
+__global__ void count_equal_kernel(const int32_t* a, const int32_t* b, int64_t len,
+                                   unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += a[k] == b[k];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);  // integer: order-free
+}
+
+template <class T>
+T* dev_alloc(size_t count) {
+  void* p = nullptr;
+  GWB_CUDA_K(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+  return static_cast<T*>(p);
+}
+}  // namespace
+
+void launch_rowsums_cm64(const double* pi, int64_t n, int64_t m, double* out, cudaStream_t s) {
+  rowsums_cm64_kernel<<<grid1d(n, 256), 256, 0, s>>>(pi, n, m, out);
+  GWB_CUDA_K(cudaGetLastError());
+}
+
+void launch_colsums_cm64(const double* pi, int64_t n, int64_t m, double* out, cudaStream_t s) {
+  colsums_cm64_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(pi, n, m, out);
+  GWB_CUDA_K(cudaGetLastError());
+}
+
+void launch_argmax_rows_cm64(const double* pi, int64_t n, int64_t m, int32_t* out, cudaStream_t s) {
+  argmax_rows_cm64_kernel<<<grid1d(n, 256), 256, 0, s>>>(pi, n, m, out);
+  GWB_CUDA_K(cudaGetLastError());
+}
+
+double sum_sq_diff_dev(const double* a, const double* b, int64_t len, cudaStream_t s) {
+  constexpr int kBlocks = 592;
+  double* part = dev_alloc<double>(kBlocks);
+  sqdiff_kernel<<<kBlocks, 256, 0, s>>>(a, b, len, part);
+  GWB_CUDA_K(cudaGetLastError());
+  double h[kBlocks];
+  GWB_CUDA_K(cudaMemcpyAsync(h, part, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GWB_CUDA_K(cudaStreamSynchronize(s));
+  cudaFree(part);
+  double t = 0.0;
+  for (double v : h) t += v;
+  return t;
+}
+
+int64_t count_equal_dev(const int32_t* a, const int32_t* b, int64_t len, cudaStream_t s) {
+  auto* c = dev_alloc<unsigned long long>(1);
+  GWB_CUDA_K(cudaMemsetAsync(c, 0, sizeof(unsigned long long), s));
+  count_equal_kernel<<<std::min<unsigned>(grid1d(len, 256), 592u), 256, 0, s>>>(a, b, len, c);
+  GWB_CUDA_K(cudaGetLastError());
+  unsigned long long h = 0;
+  GWB_CUDA_K(cudaMemcpyAsync(&h, c, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GWB_CUDA_K(cudaStreamSynchronize(s));
+  cudaFree(c);
+  return static_cast<int64_t>(h);
+}
+
 }  // namespace gwb

@@ -140,6 +140,17 @@ void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
                     int* out_inexact, cudaStream_t s);
 // P = μ νᵀ (product coupling, types.cpp:204-207) in row-major fp32.
+// Post-solve readout on a device fp64 column-major coupling (n × m):
+// row/column sums, per-row argmax (hard_assignment, tasks.cpp:190-200:
+// strict '>', lowest column wins ties), ‖a − b‖² and agreement counts.
+void launch_rowsums_cm64(const double* pi, int64_t n, int64_t m, double* out, cudaStream_t s);
+void launch_colsums_cm64(const double* pi, int64_t n, int64_t m, double* out, cudaStream_t s);
+void launch_argmax_rows_cm64(const double* pi, int64_t n, int64_t m, int32_t* out, cudaStream_t s);
+// Σ (a_k − b_k)² (b nullable ⇒ Σ a_k²), fp64, deterministic; host result.
+double sum_sq_diff_dev(const double* a, const double* b, int64_t len, cudaStream_t s);
+// #{i : a_i == b_i} over len entries; host result.
+int64_t count_equal_dev(const int32_t* a, const int32_t* b, int64_t len, cudaStream_t s);
+
 // Graph inputs: host int32 edge lists (pairs a, b; validated by the caller)
 // standing for D = adjacency_distance(g) (tasks.cpp:167-174).
 struct GraphInput {

@@ -9,6 +9,8 @@
 // synchronisation; the host polls `done` two chunks behind.
 #include "solver.cuh"
 
+#include "standalone.cuh"
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -662,6 +664,49 @@ void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
   // One mark per half-step of each kind; GEMM marks cover two launches.
   *avg_ms = cnt ? total / static_cast<double>(cnt) : 0.0;
   *count = cnt;
+}
+
+void BapgEngine::readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_host,
+                         Readout* r) {
+  GWB_CUDA(cudaSetDevice(device_));
+  const DevStatus s = status();
+  const int par = s.iter >= 1 ? (s.iter - 1) & 1 : parity_;  // buffer holding the current w
+  const size_t len = static_cast<size_t>(n_) * m_;
+  double* pi64 = dalloc<double>(len);
+  double* w64 = dalloc<double>(len);
+  double* fin64 = dalloc<double>(len);
+  double* work = dalloc<double>(static_cast<size_t>(std::max(n_, m_)));
+  double* rs = dalloc<double>(n_);
+  double* cs = dalloc<double>(m_);
+  float* fin32 = dalloc<float>(static_cast<size_t>(n_) * ldm_);
+  int32_t* assign = dalloc<int32_t>(n_);
+  // K8 fix-up, then the final coupling ½(π + w) (solvers.cpp:214-216).
+  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+  launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  launch_average64(pi64, w64, fin64, static_cast<int64_t>(len), stream_);
+  r->split_gap = std::sqrt(sum_sq_diff_dev(pi64, w64, static_cast<int64_t>(len), stream_));
+  // marginal_infeasibility (diagnostics.cpp:9-19): ‖πᵀ1 − ν‖/m + ‖π1 − μ‖/n.
+  launch_rowsums_cm64(fin64, n_, m_, rs, stream_);
+  launch_colsums_cm64(fin64, n_, m_, cs, stream_);
+  r->marginal_infeasibility = std::sqrt(sum_sq_diff_dev(cs, nu64_, m_, stream_)) / m_ +
+                              std::sqrt(sum_sq_diff_dev(rs, mu64_, n_, stream_)) / n_;
+  r->entropy = coupling_entropy_dev(fin64, static_cast<int64_t>(len), stream_);
+  // gw_objective of the final coupling (3xTF32 chain on its fp32 copy).
+  launch_colmajor64_to_rowmajor32(fin64, n_, m_, fin32, ldm_, stream_);
+  r->objective = gw_objective_dev(Dx_, ldn_, Dy_, ldm_, fin32, n_, m_, stream_);
+  // hard_assignment (tasks.cpp:190-200) and alignment_accuracy (:202-214).
+  launch_argmax_rows_cm64(fin64, n_, m_, assign, stream_);
+  if (assign_host)
+    GWB_CUDA(cudaMemcpyAsync(assign_host, assign, sizeof(int32_t) * n_, cudaMemcpyDeviceToHost, stream_));
+  if (gt_host) {
+    int32_t* gt = dalloc<int32_t>(static_cast<size_t>(n_gt));
+    GWB_CUDA(cudaMemcpyAsync(gt, gt_host, sizeof(int32_t) * n_gt, cudaMemcpyHostToDevice, stream_));
+    const int64_t hits = count_equal_dev(assign, gt, n_gt, stream_);
+    r->accuracy = 100.0 * static_cast<double>(hits) / static_cast<double>(n_gt);
+    dfree(gt);
+  }
+  GWB_CUDA(cudaStreamSynchronize(stream_));
+  for (void* p : std::initializer_list<void*>{pi64, w64, fin64, work, rs, cs, fin32, assign}) dfree(p);
 }
 
 double BapgEngine::gemm_flops_per_iter() const {

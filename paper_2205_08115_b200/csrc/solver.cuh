@@ -35,6 +35,11 @@ struct HostRecord {
   double objective, marginal_infeasibility, split_gap, rel_change, elapsed;
 };
 
+// run_cell's readout of the final coupling (experiment.cpp:169-195).
+struct Readout {
+  double objective = 0, marginal_infeasibility = 0, entropy = 0, split_gap = 0, accuracy = 0;
+};
+
 class BapgEngine {
  public:
   // n×n D_X, m×m D_Y; `precision` resolved to PREC_TF32 or PREC_3XTF32.
@@ -69,6 +74,11 @@ class BapgEngine {
   std::vector<HostRecord> records(int count);
   // Outputs as host fp64 column-major (nullable pointers are skipped).
   void outputs(double* out_final, double* out_pi, double* out_w);
+  // Post-solve readout on the device: objective, marginal infeasibility,
+  // entropy of the final coupling, split gap, hard assignment (copied to
+  // `assign_host` if non-null) and its accuracy against `gt_host` (n_gt
+  // entries; skipped if null).  Only the scalars / assignment leave the GPU.
+  void readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_host, Readout* r);
   // Device pointers (session API).
   float* pi_dev() const { return P_; }
   int64_t ld() const { return ldm_; }

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <vector>
 
+#include "devutil.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "solver.cuh"
@@ -432,35 +433,26 @@ void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* m
   c.down(out);
 }
 
-double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
-                           const double* pi) {
-  // −⟨D_X π D_Y, π⟩ (solvers.cpp:64-69) with the tcgen05 chain in 3xTF32.
-  GWB_CUDA(cudaSetDevice(api_device()));
-  const int64_t ldn = round_up(n, 32), ldm = round_up(m, 32);
-  const int64_t big = std::max(n * n, std::max(m * m, n * m));
-  DBuf<double> stage(static_cast<size_t>(big));
-  DBuf<float> Dx(n * ldn), Dx_lo(n * ldn), Dy(m * ldm), Dy_lo(m * ldm), P(n * ldm),
-      P_lo(n * ldm), Vt(m * ldn), Vt_lo(m * ldn), G(n * ldm);
-  cudaStream_t s = nullptr;
-  GWB_CUDA(cudaMemcpy(stage.p, dx, sizeof(double) * n * n, cudaMemcpyHostToDevice));
-  launch_colmajor64_to_rowmajor32(stage.p, n, n, Dx.p, ldn, s);
-  launch_tf32_aux(Dx.p, n, n, ldn, Dx_lo.p, 2, s);
-  GWB_CUDA(cudaMemcpy(stage.p, dy, sizeof(double) * m * m, cudaMemcpyHostToDevice));
-  launch_colmajor64_to_rowmajor32(stage.p, m, m, Dy.p, ldm, s);
-  launch_tf32_aux(Dy.p, m, m, ldm, Dy_lo.p, 2, s);
-  GWB_CUDA(cudaMemcpy(stage.p, pi, sizeof(double) * n * m, cudaMemcpyHostToDevice));
-  launch_colmajor64_to_rowmajor32(stage.p, n, m, P.p, ldm, s);
-  launch_tf32_aux(P.p, n, m, ldm, P_lo.p, 2, s);
+// −⟨D_X π D_Y, π⟩ (solvers.cpp:64-69) on device fp32 row-major operands with
+// the tcgen05 chain in 3xTF32 (splits computed here).
+double gw_objective_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int64_t ldm,
+                        const float* P_in, int64_t n, int64_t m, cudaStream_t s) {
+  DBuf<float> Dx_lo(n * ldn), Dy_lo(m * ldm), P_lo(n * ldm), Vt(m * round_up(n, 32)),
+      Vt_lo(m * round_up(n, 32)), G(n * ldm);
+  launch_tf32_aux(Dx_in, n, n, ldn, Dx_lo.p, 2, s);
+  launch_tf32_aux(Dy_in, m, m, ldm, Dy_lo.p, 2, s);
+  launch_tf32_aux(P_in, n, m, ldm, P_lo.p, 2, s);
+  const int64_t ldv = round_up(n, 32);
   GemmDesc g1;
   g1.M = m; g1.N = n; g1.K = m;
-  g1.a = Dy.p; g1.a_lo = Dy_lo.p; g1.lda = ldm;
-  g1.b = P.p; g1.b_lo = P_lo.p; g1.ldb = ldm;
-  g1.c = Vt.p; g1.c_aux = Vt_lo.p; g1.ldc = ldn; g1.aux_mode = 2;
+  g1.a = Dy_in; g1.a_lo = Dy_lo.p; g1.lda = ldm;
+  g1.b = P_in; g1.b_lo = P_lo.p; g1.ldb = ldm;
+  g1.c = Vt.p; g1.c_aux = Vt_lo.p; g1.ldc = ldv; g1.aux_mode = 2;
   g1.three_pass = true;
   GemmDesc g2;
   g2.M = n; g2.N = m; g2.K = n;
-  g2.a = Dx.p; g2.a_lo = Dx_lo.p; g2.lda = ldn;
-  g2.b = Vt.p; g2.b_lo = Vt_lo.p; g2.ldb = ldn;
+  g2.a = Dx_in; g2.a_lo = Dx_lo.p; g2.lda = ldn;
+  g2.b = Vt.p; g2.b_lo = Vt_lo.p; g2.ldb = ldv;
   g2.c = G.p; g2.ldc = ldm;
   g2.three_pass = true;
   GemmPlan* p1 = gemm_plan_create(g1);
@@ -468,13 +460,65 @@ double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_
   GWB_CUDA(gemm_launch(p1, s));
   GWB_CUDA(gemm_launch(p2, s));
   DBuf<double> part(n);
-  dot_rows_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(G.p, P.p, n, m, ldm, part.p);
+  dot_rows_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(G.p, P_in, n, m, ldm, part.p);
   GWB_CUDA(cudaGetLastError());
+  GWB_CUDA(cudaStreamSynchronize(s));
   const double v = reduce_host(part);
   gemm_plan_destroy(p1);
   gemm_plan_destroy(p2);
   return -v;
 }
 
+double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
+                           const double* pi) {
+  GWB_CUDA(cudaSetDevice(api_device()));
+  const int64_t ldn = round_up(n, 32), ldm = round_up(m, 32);
+  const int64_t big = std::max(n * n, std::max(m * m, n * m));
+  DBuf<double> stage(static_cast<size_t>(big));
+  DBuf<float> Dx(n * ldn), Dy(m * ldm), P(n * ldm);
+  cudaStream_t s = nullptr;
+  GWB_CUDA(cudaMemcpy(stage.p, dx, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  launch_colmajor64_to_rowmajor32(stage.p, n, n, Dx.p, ldn, s);
+  GWB_CUDA(cudaMemcpy(stage.p, dy, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+  launch_colmajor64_to_rowmajor32(stage.p, m, m, Dy.p, ldm, s);
+  GWB_CUDA(cudaMemcpy(stage.p, pi, sizeof(double) * n * m, cudaMemcpyHostToDevice));
+  launch_colmajor64_to_rowmajor32(stage.p, n, m, P.p, ldm, s);
+  return gw_objective_dev(Dx.p, ldn, Dy.p, ldm, P.p, n, m, s);
+}
+
+// coupling_entropy (diagnostics.cpp:44-53): −Σ π log π over positive entries.
+__global__ void entropy_kernel(const double* __restrict__ pi, int64_t len, double* part) {
+  double h = 0.0;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double p = pi[k];
+    if (p > 0.0) h -= p * log(p);
+  }
+  h = dev::warp_sum(h);
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += sh[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+double coupling_entropy_dev(const double* pi_dev, int64_t len, cudaStream_t s) {
+  constexpr int kBlocks = 592;
+  DBuf<double> part(kBlocks);
+  entropy_kernel<<<kBlocks, 256, 0, s>>>(pi_dev, len, part.p);
+  GWB_CUDA(cudaGetLastError());
+  GWB_CUDA(cudaStreamSynchronize(s));
+  return reduce_host(part);
+}
+
+double device_coupling_entropy(const double* pi, int64_t n, int64_t m) {
+  GWB_CUDA(cudaSetDevice(api_device()));
+  DBuf<double> d(static_cast<size_t>(n) * m);
+  d.up(pi);
+  return coupling_entropy_dev(d.p, n * m, nullptr);
+}
 
 }  // namespace gwb

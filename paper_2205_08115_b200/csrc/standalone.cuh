@@ -19,6 +19,11 @@ int api_device();
 
 double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
                            const double* pi);
+// Device-resident forms used by the session readout.
+double gw_objective_dev(const float* Dx, int64_t ldn, const float* Dy, int64_t ldm,
+                        const float* P, int64_t n, int64_t m, cudaStream_t s);
+double coupling_entropy_dev(const double* pi_dev, int64_t len, cudaStream_t s);
+double device_coupling_entropy(const double* pi, int64_t n, int64_t m);
 void device_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
                              double* out);
 double device_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m);
