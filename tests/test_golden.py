@@ -37,15 +37,22 @@ def test_port_reproduces_golden(port, path):
 def test_gpu_matches_golden(gpu, path):
     import paper_2205_08115_b200 as gw
     z, cfg = load(path)
-    if cfg.algorithm != abi.BAPG:
-        pytest.skip("eBPG/BPG/hBPG device path checked in test_gpu_bregman")
-    sc = gw.SolverConfig(algorithm="bapg", rho=cfg.rho, max_iters=cfg.max_iters,
-                         rel_tol=cfg.rel_tol, quiet=True)
+    names = {v: k for k, v in abi.ALGORITHMS.items()}
+    sc = gw.SolverConfig(algorithm=names[cfg.algorithm], rho=cfg.rho, step=cfg.step,
+                         epsilon_reg=cfg.epsilon_reg, inner_iters=cfg.inner_iters,
+                         inner_tol=cfg.inner_tol, rel_tol=cfg.rel_tol, max_iters=cfg.max_iters,
+                         perturbation=cfg.perturbation, switch_iters=cfg.switch_iters,
+                         seed=cfg.seed, log_domain=bool(cfg.log_domain), quiet=True)
     rep = gw.solve(gw.DistanceMatrix.trusted(z["dx"]), gw.DistanceMatrix.trusted(z["dy"]),
                    gw.ProbabilityVector(z["mu"]), gw.ProbabilityVector(z["nu"]), sc)
     final = rep.final_coupling.entries()
     assert np.abs(final - z["final"]).max() <= 1e-4 * np.abs(z["final"]).max()
     obj = rep.trace[-1].objective
     assert abs(obj - z["trace"][-1, 1]) <= 1e-5 * abs(z["trace"][-1, 1])
-    if cfg.rel_tol > 1e-20:  # stop-rule parity: same iteration within ±1
+    if cfg.rel_tol > 1e-20 and cfg.algorithm == abi.BAPG:
+        # stop-rule parity: same iteration within ±1
         assert abs(rep.iterations_used - int(z["iterations"])) <= 1
+    elif cfg.rel_tol > 1e-20:
+        # Bregman goldens may stop on an exact fp64 fixed point the fp32
+        # iterate cannot see: never earlier than the reference.
+        assert rep.iterations_used >= int(z["iterations"])
