@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-peak", action="store_true",
                     help="skip the cuBLAS TF32 roofline measurement (profiling runs)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="sharded path: one all-gather + monolithic GEMM2 instead of per-source "
+                         "broadcasts overlapped with partial GEMM2s")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded NCCL path even at one rank (testing)")
     ap.add_argument("--cpu-size", dest="cpu_n", type=int, default=2500)
@@ -235,7 +238,7 @@ def run_reference(args, world, rank):
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -406,7 +409,7 @@ def run_ours(args, world, rank, local, dist):
             "roofline": roofline, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": main["launches"], "clocks": clocks.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def dense_rows_dev(torch, n, edges, r0, rows):
@@ -452,7 +455,8 @@ def run_sharded_e2e(args, world, rank, local, dist, edges, tgt, prec):
     cfg = abi.default_config(rho=0.1, max_iters=args.e2e_iters, rel_tol=1e-30, precision=prec)
     dist.barrier()
     t0 = time.perf_counter()
-    r = D.solve_sharded(cfg, dx, dy, u, u, dist, rank, world, local)
+    r = D.solve_sharded(cfg, dx, dy, u, u, dist, rank, world, local,
+                        overlap=not args.no_overlap)
     dt = time.perf_counter() - t0
     t = torch.tensor([dt], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -489,7 +493,8 @@ def run_sharded_bench(args, world, rank, local, dist):
     shard.reset()
     del dx_rows, dy
     comm = D.TorchComm(dist, rank, world)
-    D.iterate_sharded([shard], comm, args.warmup, poll_every=0)
+    overlap = not args.no_overlap
+    D.iterate_sharded([shard], comm, args.warmup, poll_every=0, overlap=overlap)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = shard.launches()
@@ -498,7 +503,7 @@ def run_sharded_bench(args, world, rank, local, dist):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(shard.stream)
-        D.iterate_sharded([shard], comm, args.steps, poll_every=0)
+        D.iterate_sharded([shard], comm, args.steps, poll_every=0, overlap=overlap)
         ev1.record(shard.stream)
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -522,9 +527,11 @@ def run_sharded_bench(args, world, rank, local, dist):
             "data": "synthetic (seeded BA graphs, reference RNG)",
             "config": {"workload": WORKLOAD, "n": n, "m": n, "precision": PREC_LABEL[prec],
                        "l2": "no flush: operands exceed the 126 MB L2",
-                       "parallelism": f"row-sharded over {world} GPUs (NCCL all-gather of Vᵀ "
-                                      "blocks, all-gather of column stats, all-reduce of "
-                                      "diagnostics)",
+                       "parallelism": f"row-sharded over {world} GPUs (" + (
+                           "per-source NCCL broadcasts of the Vᵀ blocks overlapped with "
+                           "accumulating partial GEMM2s" if overlap else
+                           "NCCL all-gather of Vᵀ blocks") + ", all-gather of column stats, "
+                           "all-reduce of diagnostics)",
                        "rows_per_shard": nr},
             "tflops": {"algorithmic_per_iteration": flops_it,
                        "achieved_whole_step": flops_it * value / 1e12},
@@ -552,7 +559,7 @@ def run_sharded_bench(args, world, rank, local, dist):
         if rank == 0:
             line["variants"] = {"c5_batched": c5}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def hbpg_variant(n):
@@ -645,7 +652,20 @@ def run_e2e(args, edges, tgt, n, prec):
             "graphs": graphs}
 
 
+_JSON_FD = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line goes to the real stdout; everything else (NCCL's
+    version banner, library chatter) was redirected to stderr in main()."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level writes to fd 1 (e.g. "NCCL version …") land on stderr
     args = parse()
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":
@@ -657,7 +677,11 @@ def main():
                 import torch.distributed as tdist
                 torch.cuda.set_device(local)
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                os.environ.setdefault("MASTER_PORT", "29533")
+                if "MASTER_PORT" not in os.environ:
+                    import socket
+                    with socket.socket() as sk:
+                        sk.bind(("127.0.0.1", 0))
+                        os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
                 tdist.init_process_group("nccl", rank=0, world_size=1)
                 dist = tdist
             run_sharded_bench(args, world, rank, local, dist)

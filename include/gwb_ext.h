@@ -62,6 +62,14 @@ GWB_API int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows,
                                       const float* nu, gwb_status* st);
 GWB_API int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st);
 GWB_API int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st);
+/* Compute/collective overlap: instead of all-gather(vt) + phase 1 (3, 7),
+ * issue one collective per source rank (e.g. a broadcast of that rank's vt
+ * chunk) and, as each lands, gwb_shard_gemm2_chunk(src) — the partial
+ * G_r (+)= D_X[rows_r, cols_src]·V_src, own rank first (it overwrites G_r),
+ * tail = 1 for the tail pass — then phase 21 (23, 27): phase 1 (3, 7)
+ * without its GEMM2. */
+GWB_API int32_t gwb_shard_gemm2_chunk(gwb_shard* s, int32_t src, int32_t tail,
+                                      gwb_status* st);
 /* Kernels launched so far by phases 0-5 of this shard (measurement hook). */
 GWB_API int32_t gwb_shard_launches(gwb_shard* s, int64_t* launches);
 GWB_API int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st);

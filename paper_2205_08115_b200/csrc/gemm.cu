@@ -71,6 +71,7 @@ struct __align__(64) GemmParams {
   const float* row_scale;
   const float* col_scale;
   const int* skip;
+  int32_t accumulate;
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -272,6 +273,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
         for (int j = 0; j < kSliceCols; j += 4) {
+          if (p.accumulate) {
+            const float4 o = *reinterpret_cast<const float4*>(crow + col0 + j);
+            acc[j] = __fadd_rn(o.x, acc[j]);
+            acc[j + 1] = __fadd_rn(o.y, acc[j + 1]);
+            acc[j + 2] = __fadd_rn(o.z, acc[j + 2]);
+            acc[j + 3] = __fadd_rn(o.w, acc[j + 3]);
+          }
           *reinterpret_cast<float4*>(crow + col0 + j) =
               make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
           if (clo)
@@ -283,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < kSliceCols; ++j) {
           if (col0 + j < p.N) {
+            if (p.accumulate) acc[j] = __fadd_rn(crow[col0 + j], acc[j]);
             crow[col0 + j] = acc[j];
             if (clo) clo[col0 + j] = acc[j] - trunc_tf32(acc[j]);
           }
@@ -452,6 +461,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   for (int pl = 0; pl < 3; ++pl) g.c_pl[pl] = static_cast<__nv_bfloat16*>(d.c_bf16[pl]);
   g.row_scale = d.row_scale;
   g.col_scale = d.col_scale;
+  g.accumulate = d.accumulate ? 1 : 0;
   g.skip = d.skip;
   p->grid = 2 * g.tiles_m * g.tiles_n;  // two CTAs (one cluster) per tile
   p->flops = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);

@@ -53,6 +53,9 @@ struct GemmDesc {
   // (32 fp32 / 64 bf16 elements).
   int64_t b_block_k = 0;
   int64_t b_block_stride = 0;        // elements between blocks (0 ⇒ N·b_block_k)
+  // C += A·Bᵀ instead of C = A·Bᵀ (fp32 `c` output only): K-split partial
+  // products accumulated across launches (multi-GPU chunked GEMM2).
+  bool accumulate = false;
 };
 
 // Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).

@@ -344,30 +344,47 @@ class ShardEngine {
   // Phases between collectives (see file comment).
   int64_t launches() const { return launches_; }
 
+  // Chunked GEMM2 (compute/collective overlap): the partial product of the
+  // Vᵀ block owned by rank `src`, G_r (+)= D_X[rows_r, cols_src]·V_src.  The
+  // caller launches the local block first (it overwrites G_r) and the others
+  // as their collective lands; phases 21/23/27 are then 1/3/7 without the
+  // monolithic GEMM2.
+  void gemm2_chunk(int src, bool tail) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    if (src < 0 || src >= world_) throw CudaError("gwb_shard_gemm2_chunk: bad source rank");
+    GWB_CUDA(gemm_launch(tail ? g2ct_[src] : g2c_[src], s_));
+    if (!tail) launches_ += 1;
+  }
+
   void phase(int ph) {
     GWB_CUDA(cudaSetDevice(dev_));
     const int q = parity_;
     BapgDev d = view(q);
+    const bool chunked = ph >= 20;  // GEMM2 issued by gemm2_chunk
+    if (chunked) {
+      if (ph != 21 && ph != 23 && ph != 27) throw CudaError("gwb_shard_phase: unknown phase");
+      ph -= 20;
+    }
     switch (ph) {
       case 0:  // A1: Vᵀ slot ← D_Y · W_rᵀ
         GWB_CUDA(gemm_launch(g1_[q], s_));
         launches_ += 1;
         break;
       case 1:  // A2: G_r, row projection
-        GWB_CUDA(gemm_launch(g2_, s_));
+        if (!chunked) GWB_CUDA(gemm_launch(g2_, s_));
         launch_row_update(d, true, s_);
-        launches_ += 3;
+        launches_ += chunked ? 2 : 3;
         break;
       case 2:  // B1
         GWB_CUDA(gemm_launch(g1p_, s_));
         launches_ += 1;
         break;
       case 3:  // B2: G_r, local column partials → stats slot
-        GWB_CUDA(gemm_launch(g2_, s_));
+        if (!chunked) GWB_CUDA(gemm_launch(g2_, s_));
         launch_col_partial(d, s_);
         shard_col_local_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
             d, stats_ + static_cast<int64_t>(rank_) * 3 * m_, m_);
-        launches_ += 3;
+        launches_ += chunked ? 2 : 3;
         break;
       case 4:  // B3: global column merge, write pass, local diagnostics
         shard_col_global_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(
@@ -385,7 +402,7 @@ class ShardEngine {
         GWB_CUDA(gemm_launch(g1t_[q], s_));
         break;
       case 7:  // tail A2: diagnostics-only row pass
-        GWB_CUDA(gemm_launch(g2t_, s_));
+        if (!chunked) GWB_CUDA(gemm_launch(g2t_, s_));
         launch_row_update(d, false, s_);
         shard_diag_kernel<<<1, 512, 0, s_>>>(d, diag_, err_, rank_, row_begin_, 1);
         break;
@@ -516,6 +533,37 @@ class ShardEngine {
     return p;
   }
 
+  // Partial GEMM2 over the Vᵀ block of rank `src`: K = n_r columns of the
+  // local D_X rows starting at src·n_r, B = that rank's slot (plain 2-D).
+  GemmPlan* make2_chunk(int src, const int* skip) {
+    GemmDesc d;
+    d.M = nr_;
+    d.N = m_;
+    d.K = nr_;
+    d.lda = ldk_;
+    d.ldb = nr_;
+    d.c = G_;
+    d.ldc = ldm_;
+    d.skip = skip;
+    d.accumulate = src != rank_;  // the local block is launched first
+    const int64_t koff = static_cast<int64_t>(src) * nr_;
+    if (bf16_) {
+      d.bf16_planes = planes_;
+      d.a_bf16 = reinterpret_cast<const uint8_t*>(Dx_aux_) + koff * 2;
+      for (int p = 0; p < planes_; ++p) d.b_bf16[p] = slot(p, src);
+    } else {
+      const bool tf32 = prec_ == GWB_PREC_TF32;
+      d.a = (tf32 ? Dx_aux_ : Dx_) + koff;
+      d.a_lo = tf32 ? nullptr : Dx_aux_ + koff;
+      d.b = static_cast<const float*>(slot(0, src));
+      d.b_lo = tf32 ? nullptr : static_cast<const float*>(slot(1, src));
+      d.three_pass = !tf32;
+    }
+    GemmPlan* p = gemm_plan_create(d);
+    plans_.push_back(p);
+    return p;
+  }
+
   GemmPlan* make2(const int* skip) {
     GemmDesc d;
     d.M = nr_;
@@ -552,6 +600,12 @@ class ShardEngine {
     g1p_ = make1(P_, P_aux_, &st_->done);
     g2_ = make2(&st_->done);
     g2t_ = make2(&st_->flags);
+    g2c_.assign(world_, nullptr);
+    g2ct_.assign(world_, nullptr);
+    for (int s = 0; s < world_; ++s) {
+      g2c_[s] = make2_chunk(s, &st_->done);
+      g2ct_[s] = make2_chunk(s, &st_->flags);
+    }
   }
 
   gwb_config cfg_;
@@ -566,6 +620,7 @@ class ShardEngine {
   int64_t launches_ = 0;  // kernels launched by phases 0-5 (bench gpu_launches)
   std::vector<void*> bufs_;
   std::vector<GemmPlan*> plans_;
+  std::vector<GemmPlan*> g2c_, g2ct_;  // chunked GEMM2 per source rank (owned by plans_)
   float *Dx_, *Dy_, *Dx_aux_, *Dy_aux_, *P_, *P_aux_, *W_[2], *W_aux_[2], *G_;
   float *mu32_, *nu32_;
   double *mu64_, *nu64_;
@@ -660,6 +715,10 @@ int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st) {
 
 int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st) {
   return shard_guard(st, [&] { s->eng->phase(phase); });
+}
+
+int32_t gwb_shard_gemm2_chunk(gwb_shard* s, int32_t src, int32_t tail, gwb_status* st) {
+  return shard_guard(st, [&] { s->eng->gemm2_chunk(src, tail != 0); });
 }
 
 int32_t gwb_shard_launches(gwb_shard* s, int64_t* launches) {

@@ -62,6 +62,7 @@ _SIGS = {
     "gwb_shard_phase": (C.c_int32, [_P, C.c_int32, _ST]),
     "gwb_shard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
     "gwb_shard_launches": (C.c_int32, [_P, _I64P]),
+    "gwb_shard_gemm2_chunk": (C.c_int32, [_P, C.c_int32, C.c_int32, _ST]),
     "gwb_shard_status": (C.c_int32, [_P, _I32P, _I32P, _I32P, _I32P, _I32P, _I32P, _ST]),
     "gwb_shard_finish": (C.c_int32, [_P, _ST]),
     "gwb_shard_records": (C.c_int32, [_P, C.c_int32, C.POINTER(abi.Record), _ST]),
@@ -148,6 +149,11 @@ class GpuShard:
         keys = ("done", "iter", "flags", "converged", "err_iter", "zero_index")
         return {k: x.value for k, x in zip(keys, v)}
 
+    def gemm2_chunk(self, src: int, tail: bool = False):
+        st = abi.Status()
+        self.lib.gwb_shard_gemm2_chunk(self.h, src, 1 if tail else 0, C.byref(st))
+        _check(st)
+
     def launches(self) -> int:
         v = C.c_int64()
         self.lib.gwb_shard_launches(self.h, C.byref(v))
@@ -219,6 +225,29 @@ class TorchComm:
             self.dist.all_reduce(s.diag, op=self.dist.ReduceOp.SUM)
             self.dist.all_reduce(s.err, op=self.dist.ReduceOp.MAX)
 
+    # Chunked Vᵀ exchange for the compute/collective overlap: one broadcast
+    # per source rank, all enqueued at once behind GEMM1 on the shard stream;
+    # the consumer waits per chunk, so GEMM2 on landed blocks overlaps the
+    # transfer of the rest.
+    def start_vt_chunks(self, shards):
+        s = shards[0]
+        view = s.vt.view(self.world, -1)
+        with _stream(s):
+            return [self.dist.broadcast(view[src], src=src, async_op=True)
+                    for src in range(self.world)]
+
+    def wait_vt_chunk(self, shards, handles, src):
+        s = shards[0]
+        if src != self.rank:
+            with _stream(s):
+                handles[src].wait()
+
+    def finish_vt_chunks(self, shards, handles):
+        # Our own block was only sent: the next phase overwrites it, so the
+        # stream must also be ordered after that send.
+        with _stream(shards[0]):
+            handles[self.rank].wait()
+
 
 class EmuComm:
     """All `world` shards live in this process (one GPU, shared stream):
@@ -239,6 +268,16 @@ class EmuComm:
                 for q in range(world):
                     if q != r:
                         views[q][r].copy_(views[r][r])
+
+    def start_vt_chunks(self, shards):
+        self.gather_vt(shards)  # in-order device copies: every chunk lands now
+        return None
+
+    def wait_vt_chunk(self, shards, handles, src):
+        return None
+
+    def finish_vt_chunks(self, shards, handles):
+        return None
 
     @staticmethod
     def reduce_diag(shards):
@@ -275,18 +314,48 @@ def _all_phase(shards, k):
         s.phase(k)
 
 
-def iterate_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> None:
+def _gemm2_overlapped(shards, comm, tail: bool):
+    """Chunked exchange of Vᵀ + per-source partial GEMM2: each shard starts
+    with its own block (already local), then consumes the others in the
+    order their collectives were issued."""
+    handles = comm.start_vt_chunks(shards)
+    world = shards[0].world
+    for s in shards:
+        order = [s.rank] + [q for q in range(world) if q != s.rank]
+        for src in order:
+            comm.wait_vt_chunk([s], handles, src)
+            s.gemm2_chunk(src, tail)
+    comm.finish_vt_chunks(shards, handles)
+
+
+def _half_a(shards, comm, overlap):
+    _all_phase(shards, 0)
+    if overlap:
+        _gemm2_overlapped(shards, comm, False)
+        _all_phase(shards, 21)
+    else:
+        comm.gather_vt(shards)
+        _all_phase(shards, 1)
+
+
+def iterate_sharded(shards: List, comm, iters: int, poll_every: int = 16,
+                    overlap: bool = False) -> None:
     """Enqueue up to `iters` iterations of the phase / collective schedule.
     Every rank issues the same collectives every iteration (kernels no-op
     once done); the globally agreed `done` flag is polled every
-    `poll_every` iterations (poll_every=0: never, no host synchronisation)."""
+    `poll_every` iterations (poll_every=0: never, no host synchronisation).
+    overlap=True replaces each all-gather + GEMM2 by per-source collectives
+    and partial GEMM2s (the transfer of later blocks overlaps the product of
+    earlier ones)."""
     for it in range(1, iters + 1):
-        _all_phase(shards, 0)
-        comm.gather_vt(shards)
-        _all_phase(shards, 1)
+        _half_a(shards, comm, overlap)
         _all_phase(shards, 2)
-        comm.gather_vt(shards)
-        _all_phase(shards, 3)
+        if overlap:
+            _gemm2_overlapped(shards, comm, False)
+            _all_phase(shards, 23)
+        else:
+            comm.gather_vt(shards)
+            _all_phase(shards, 3)
         comm.gather_stats(shards)
         _all_phase(shards, 4)
         comm.reduce_diag(shards)
@@ -296,13 +365,17 @@ def iterate_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> Non
                 break
 
 
-def finish_sharded(shards: List, comm) -> dict:
+def finish_sharded(shards: List, comm, overlap: bool = False) -> dict:
     """Objective of the last record (one more chain) and final parity."""
     st = shards[0].status()
     if not st["flags"]:
         _all_phase(shards, 6)
-        comm.gather_vt(shards)
-        _all_phase(shards, 7)
+        if overlap:
+            _gemm2_overlapped(shards, comm, True)
+            _all_phase(shards, 27)
+        else:
+            comm.gather_vt(shards)
+            _all_phase(shards, 7)
         comm.reduce_diag(shards)
         _all_phase(shards, 8)
     for s in shards:
@@ -310,14 +383,15 @@ def finish_sharded(shards: List, comm) -> dict:
     return shards[0].status()
 
 
-def run_sharded(shards: List, comm, iters: int, poll_every: int = 16) -> dict:
+def run_sharded(shards: List, comm, iters: int, poll_every: int = 16,
+                overlap: bool = False) -> dict:
     """Full sharded solve: iterations, then the tail record."""
-    iterate_sharded(shards, comm, iters, poll_every)
-    return finish_sharded(shards, comm)
+    iterate_sharded(shards, comm, iters, poll_every, overlap)
+    return finish_sharded(shards, comm, overlap)
 
 
 def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
-                  device: int = 0, poll_every: int = 16) -> dict:
+                  device: int = 0, poll_every: int = 16, overlap: bool = True) -> dict:
     """Row-sharded BAPG from HOST inputs — the public multi-GPU entry, called
     by every rank of a torch.distributed (NCCL) job with the same arguments.
 
@@ -344,7 +418,8 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
         shard.load(dx_d, dy_d, mu_d, t(nu))
         del dx_d, dy_d
         shard.reset()
-        st = run_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters, poll_every)
+        st = run_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters, poll_every,
+                         overlap)
         raise_shard_flags(st)
         used = st["iter"] - 1
         recs = shard.records(used)

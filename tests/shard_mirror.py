@@ -54,9 +54,21 @@ class CpuShard:
     def _rec(self, k):
         return self.records.setdefault(k, {})
 
+    def gemm2_chunk(self, src, tail=False):
+        """Partial GEMM2 over the Vᵀ block of rank `src` (ShardEngine::gemm2_chunk)."""
+        if (self.flags if tail else self.done):
+            return
+        chunk = self.vt.view(self.world, self.m, self.nr).numpy()[src]  # m × nr
+        part = self.Dx[:, src * self.nr:(src + 1) * self.nr] @ chunk.T
+        self.Gacc = part if src == self.rank else self.Gacc + part
+
     # -- phases (csrc/shard.cu ShardEngine::phase) ----------------------------
     def phase(self, ph):
         rv = self.rv
+        chunked = ph >= 20
+        if chunked:
+            ph -= 20
+        full_G = (lambda: self.Gacc) if chunked else self._G
         if ph in (0, 6):
             if ph == 0 and self.done:
                 return
@@ -64,7 +76,7 @@ class CpuShard:
         elif ph in (1, 7):
             if ph == 1 and self.done:
                 return
-            G = self._G()[:rv]
+            G = full_G()[:rv]
             W = self.W[:rv]
             self.row_gw = float(np.sum(G * W))
             self.row_dev = float(np.sum((W.sum(1) - self.mu) ** 2))
@@ -91,7 +103,7 @@ class CpuShard:
         elif ph == 3:
             if self.done:
                 return
-            G = self._G()[:rv]
+            G = full_G()[:rv]
             self.G = G
             E = G / self.rho
             P = self.P[:rv]

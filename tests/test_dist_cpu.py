@@ -24,7 +24,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, iters, rel_tol, q):
+def _worker(rank, world, port, n, iters, rel_tol, q, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     from paper_2205_08115_b200.dist import TorchComm, run_sharded
@@ -33,7 +33,8 @@ def _worker(rank, world, port, n, iters, rel_tol, q):
     inst = I.config1(seed=9, n=n)
     s = CpuShard(inst.dx, inst.dy, inst.mu, inst.nu, 0.1, rank, world, iters, rel_tol)
     s.reset()
-    st = run_sharded([s], TorchComm(dist, rank, world, inplace_gather=False), iters, poll_every=4)
+    st = run_sharded([s], TorchComm(dist, rank, world, inplace_gather=False), iters, poll_every=4,
+                     overlap=overlap)
     used = st["iter"] - 1
     pi, w = s.rows()
     q.put((rank, pi, w, s.trace(used), st))
@@ -41,11 +42,11 @@ def _worker(rank, world, port, n, iters, rel_tol, q):
     dist.destroy_process_group()
 
 
-def _run(world, n, iters, rel_tol):
+def _run(world, n, iters, rel_tol, overlap=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, iters, rel_tol, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, iters, rel_tol, q, overlap))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -59,10 +60,12 @@ def _run(world, n, iters, rel_tol):
     return pi, w, out[0][3], [o[4] for o in out]
 
 
-@pytest.mark.parametrize("world,n", [(2, 150), (3, 130)])
-def test_sharded_bapg_matches_oracle_gloo(port, world, n):
+@pytest.mark.parametrize("world,n,overlap", [(2, 150, False), (3, 130, False), (2, 150, True),
+                                             (3, 130, True)])
+def test_sharded_bapg_matches_oracle_gloo(port, world, n, overlap):
+    # overlap=True: per-source broadcasts + partial GEMM2s (own block first)
     iters = 12
-    pi, w, trace, sts = _run(world, n, iters, 1e-30)
+    pi, w, trace, sts = _run(world, n, iters, 1e-30, overlap)
     inst = I.config1(seed=9, n=n)
     o = port.solve(abi.default_config(rho=0.1, max_iters=iters, rel_tol=1e-30), inst.dx, inst.dy,
                    inst.mu, inst.nu)
@@ -75,10 +78,11 @@ def test_sharded_bapg_matches_oracle_gloo(port, world, n):
             assert r[k] == pytest.approx(q[k], rel=1e-9, abs=1e-14), k
 
 
-def test_sharded_stop_rule_agreed_gloo(port):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_sharded_stop_rule_agreed_gloo(port, overlap):
     # every rank must stop at the oracle's convergence iteration
     n, iters = 64, 1200
-    pi, w, trace, sts = _run(2, n, iters, 1e-6)
+    pi, w, trace, sts = _run(2, n, iters, 1e-6, overlap)
     inst = I.config1(seed=9, n=n)
     o = port.solve(abi.default_config(rho=0.1, max_iters=iters, rel_tol=1e-6), inst.dx, inst.dy,
                    inst.mu, inst.nu)

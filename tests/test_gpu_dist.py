@@ -14,7 +14,7 @@ PREC = {"bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2, "3xtf32": abi.PREC
         "tf32": abi.PREC_TF32}
 
 
-def _run(inst, world, prec, iters, rel_tol=1e-30):
+def _run(inst, world, prec, iters, rel_tol=1e-30, overlap=False):
     import torch
     cfg = abi.default_config(rho=inst.solver["rho"], max_iters=iters, rel_tol=rel_tol,
                              precision=PREC[prec])
@@ -24,7 +24,7 @@ def _run(inst, world, prec, iters, rel_tol=1e-30):
     shards = dist.shards_from_dense(cfg, dx, dy, mu, nu, world, stream=stream)
     for s in shards:
         s.reset()
-    st = dist.run_sharded(shards, dist.EmuComm(), iters, poll_every=8)
+    st = dist.run_sharded(shards, dist.EmuComm(), iters, poll_every=8, overlap=overlap)
     dist.raise_shard_flags(st)
     rows = [s.rows() for s in shards]
     pi = np.vstack([r[0] for r in rows])
@@ -39,10 +39,12 @@ def _run(inst, world, prec, iters, rel_tol=1e-30):
 @pytest.mark.parametrize("world,prec,case", [
     (2, "bf16x3", "er"), (3, "bf16x3", "er"), (4, "bf16x2", "er"), (2, "3xtf32", "gmm"),
     (3, "tf32", "er")])
-def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case, overlap):
+    # overlap=True: per-source chunks + accumulating partial GEMM2s
     inst = I.config1(seed=4, n=300) if case == "er" else I.config2(seed=2, n=260, m=200)
     iters = 30
-    pi, w, recs, st, cfg = _run(inst, world, prec, iters)
+    pi, w, recs, st, cfg = _run(inst, world, prec, iters, overlap=overlap)
     o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
     assert o.code == 0 and st["iter"] - 1 == iters
     assert np.abs(pi - o.pi).max() <= 1e-4 * np.abs(o.pi).max()
@@ -54,17 +56,21 @@ def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case):
         assert abs(r.rel_change - q["rel_change"]) <= 2e-3 * q["rel_change"] + 1e-7
 
 
-def test_sharded_stop_rule_and_errors(gpu, port):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_sharded_stop_rule_and_errors(gpu, port, overlap):
     inst = I.config1(seed=9, n=64)
-    pi, w, recs, st, cfg = _run(inst, 2, "bf16x3", 1200, rel_tol=1e-6)
+    pi, w, recs, st, cfg = _run(inst, 2, "bf16x3", 1200, rel_tol=1e-6, overlap=overlap)
     o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
     assert o.converged and st["converged"]
-    assert abs((st["iter"] - 1) - o.iterations_used) <= 1
+    # rel_change decays slowly near rel_tol (ratio ≈ 0.99/iteration here), so
+    # fp32 summation order (the chunked GEMM2 accumulates per source block)
+    # can move the crossing by a few iterations: allow 0.5%.
+    assert abs((st["iter"] - 1) - o.iterations_used) <= max(1, 0.005 * o.iterations_used)
     # overflow → NumericalInstabilityError agreed by every rank
     inst2 = I.config1(seed=2, n=96)
     inst2.solver["rho"] = 1e-7
     with pytest.raises(abi.NumericalInstabilityError, match="exp overflow; increase rho"):
-        _run(inst2, 2, "bf16x3", 5)
+        _run(inst2, 2, "bf16x3", 5, overlap=overlap)
 
 
 def test_solve_sharded_public_entry_nccl_world1(gpu, port):
