@@ -106,3 +106,35 @@ def test_bapg_skinny_ragged_k(gpu, port):
         assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL, k
         obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
         assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref), k
+
+
+def test_concurrent_solves_are_reentrant_and_deterministic(gpu):
+    # SURVEY §8(b) threading contract: concurrent solve() calls on distinct
+    # inputs (the experiment worker pool) are safe and deterministic — each
+    # call owns its stream and workspace.
+    import threading
+    insts = [I.config1(seed=s, n=200 + 40 * s) for s in range(4)]
+
+    def one(inst):
+        cfg = gw.SolverConfig(rho=0.1, max_iters=30, rel_tol=1e-30, quiet=True)
+        return gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                        gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu), cfg)
+
+    sequential = [one(x).final_coupling.entries() for x in insts]
+    out = [None] * len(insts)
+    errs = []
+
+    def worker(k):
+        try:
+            out[k] = one(insts[k]).final_coupling.entries()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(insts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(out, sequential):
+        assert np.array_equal(a, b)
