@@ -427,15 +427,50 @@ static void initial_coupling(const double* mu, int64_t n, const double* nu,
   }
 }
 
+/* simplex_project: projections.cpp:36-53 — Euclidean projection of v onto
+ * {x ≥ 0, Σx = s} by a descending sort and the running threshold. */
+static int cmp_desc(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x < y) - (x > y);
+}
+
+static void simplex_project(const double* v, int64_t n, int64_t stride, double s, double* u,
+                            double* out) {
+  for (int64_t j = 0; j < n; ++j) u[j] = v[j * stride];
+  qsort(u, (size_t)n, sizeof(double), cmp_desc);
+  double cumsum = 0.0, theta = u[0] - s;
+  for (int64_t j = 0; j < n; ++j) {
+    cumsum += u[j];
+    const double cand = (cumsum - s) / (double)(j + 1);
+    if (u[j] - cand > 0.0) theta = cand;
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    const double x = v[j * stride] - theta;
+    out[j * stride] = x > 0.0 ? x : 0.0;
+  }
+}
+
+/* euclid_project: projections.cpp:55-77, column-major pi. */
+static void euclid_project(const double* pi, int64_t n, int64_t m, const double* target,
+                           int axis, double* out) {
+  const int64_t len = axis == GWB_ROWS ? m : n;
+  double* u = (double*)malloc(sizeof(double) * (size_t)(len > 0 ? len : 1));
+  if (axis == GWB_ROWS) {
+    for (int64_t i = 0; i < n; ++i) simplex_project(pi + i, m, n, target[i], u, out + i);
+  } else {
+    for (int64_t j = 0; j < m; ++j)
+      simplex_project(pi + j * n, n, 1, target[j], u, out + j * n);
+  }
+  free(u);
+}
+
 /* bapg_solve, entropy geometry: solvers.cpp:138-217. */
 static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
                     const double* dy, int64_t m, const double* mu,
                     const double* nu, const double* initial, double* out_final,
                     double* out_pi, double* out_w, trace_buf* tb,
                     int32_t* converged, int32_t* iters_used, gwb_status* st) {
-  if (cfg->geometry != GWB_ENTROPY)
-    return set_status(st, GWB_ERR_UNSUPPORTED, NULL, 0,
-                      "quadratic-geometry BAPG is outside the B200 path");
+  const int entropy = cfg->geometry == GWB_ENTROPY;
   const size_t len = (size_t)n * (size_t)m;
   double* pi = (double*)malloc(sizeof(double) * len);
   double* w = (double*)malloc(sizeof(double) * len);
@@ -444,7 +479,7 @@ static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
   double* avg = (double*)malloc(sizeof(double) * len);
   int32_t rc = GWB_OK;
   initial_coupling(mu, n, nu, m, initial, pi);
-  for (size_t k = 0; k < len; ++k) {
+  for (size_t k = 0; entropy && k < len; ++k) {
     if (!(pi[k] > 0.0)) {
       rc = set_status(st, GWB_ERR_CONFIG, NULL, 0,
                       "bapg entropy geometry requires a strictly positive "
@@ -452,14 +487,27 @@ static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
       goto done;
     }
   }
-  rc = gwo_kl_scale(pi, n, m, nu, m, GWB_COLS, w, st); /* :152-153 */
-  if (rc) goto done;
+  if (entropy) {
+    rc = gwo_kl_scale(pi, n, m, nu, m, GWB_COLS, w, st); /* :152-153 */
+    if (rc) goto done;
+  } else {
+    euclid_project(pi, n, m, nu, GWB_COLS, w);
+  }
   {
     const double t0 = now_seconds();
     int32_t iter = 0;
     *converged = 0;
     while (iter < cfg->max_iters) {
       ++iter;
+      if (!entropy) { /* quadratic geometry, :179-182 */
+        gwo_structure_product(dx, n, dy, m, w, e);
+        for (size_t k = 0; k < len; ++k) e[k] = w[k] + e[k] / cfg->rho;
+        euclid_project(e, n, m, mu, GWB_ROWS, pi);
+        gwo_structure_product(dx, n, dy, m, pi, e);
+        for (size_t k = 0; k < len; ++k) e[k] = pi[k] + e[k] / cfg->rho;
+        euclid_project(e, n, m, nu, GWB_COLS, w_next);
+        goto checked;
+      }
       /* half-step a, :164-170 */
       gwo_structure_product(dx, n, dy, m, w, e);
       double emax = -INFINITY;
@@ -498,6 +546,7 @@ static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
         rc = numerical(st, "bapg", iter, what);
       }
       if (rc) goto done;
+    checked:
       if (!all_finite(pi, len) || !all_finite(w_next, len)) { /* :187-189 */
         rc = numerical(st, "bapg", iter, "non-finite iterate");
         goto done;

@@ -748,6 +748,7 @@ Failure batched_generic(const gwb_config* cfg, int device, int64_t batch, const 
                         int64_t n, const double* dy, int64_t m, const double* mu,
                         const double* nu, const BatchedOut& o, int64_t base) {
   BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
+  eng.set_geometry(cfg->geometry);
   const size_t len = static_cast<size_t>(n) * m;
   Failure first;
   for (int64_t b = 0; b < batch; ++b) {
@@ -789,7 +790,9 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   const bool onchip_prec = cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_BF16X3;
   g_last_ms = 0.0;
   g_last_problems = 0;
-  if (n > kT || m > kT || !onchip_prec) {
+  // The on-chip kernel implements the entropy geometry; the quadratic one
+  // runs problem by problem on the generic engine.
+  if (n > kT || m > kT || !onchip_prec || cfg->geometry != GWB_ENTROPY) {
     const Failure f = batched_generic(cfg, device, batch, dx, n, dy, m, mu, nu, o, 0);
     if (f.problem >= 0) raise_failure(f);
     return;

@@ -196,13 +196,12 @@ void raise_device_flags(const gwb::DevStatus& s, const char* solver) {
 void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, int64_t m,
           const double* mu, const double* nu, const double* initial, gwb_observer observer,
           void* user, const SolveOut& o, const gwb::GraphInput* graphs) {
-  if (cfg->geometry != GWB_ENTROPY)
-    fail(GWB_ERR_UNSUPPORTED, "quadratic-geometry BAPG is outside the B200 path (DESIGN.md)");
+  const bool entropy = cfg->geometry == GWB_ENTROPY;
   if (cfg->record_residual)
     fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
   const size_t len = static_cast<size_t>(n) * static_cast<size_t>(m);
   std::vector<double> w0;
-  if (initial) {
+  if (initial && entropy) {
     // initial_coupling + positivity (solvers.cpp:146-151), w0 = kl_scale(π0, ν, Cols)
     // (solvers.cpp:152; projections.cpp:23-31) — an O(nm) host pass, once.
     for (size_t k = 0; k < len; ++k)
@@ -228,11 +227,13 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
     fail(GWB_ERR_CAPACITY, fmt("trace capacity %d < max_iters %d", o.trace_cap, cfg->max_iters));
   const int device = primary_device();
   BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
+  eng.set_geometry(cfg->geometry);
   if (graphs)
     eng.load_graphs(*graphs, mu, nu);
   else
     eng.load_host(dx, dy, mu, nu);
-  eng.reset(initial ? w0.data() : nullptr);
+  // Quadratic: π⁰ itself goes to the device, which projects it (reset()).
+  eng.reset(initial ? (entropy ? w0.data() : initial) : nullptr);
   gwb::DevStatus s;
   if (!observer) {
     eng.run(cfg->max_iters, cfg->rel_tol);
@@ -488,7 +489,6 @@ int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch, const doubl
     if (!cfg) fail(GWB_ERR_CONFIG, "null config");
     require_algorithm(cfg, GWB_BAPG, "bapg_solve");
     validate_config(cfg);
-    if (cfg->geometry != GWB_ENTROPY) fail(GWB_ERR_UNSUPPORTED, "quadratic geometry unsupported");
     if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual unsupported");
     if (batch < 1 || n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "empty batch or problem");
     gwb::device_bapg_batched(cfg, batch, dx, n, dy, m, mu, nu, out_final, out_pi, out_w, trace,
@@ -525,6 +525,7 @@ int32_t gwb_session_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t 
     auto* s = new gwb_session();
     s->cfg = *cfg;
     s->eng.reset(new BapgEngine(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr));
+    s->eng->set_geometry(cfg->geometry);
     *out = s;
   });
 }

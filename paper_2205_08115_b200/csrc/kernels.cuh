@@ -151,6 +151,14 @@ double sum_sq_diff_dev(const double* a, const double* b, int64_t len, cudaStream
 // #{i : a_i == b_i} over len entries; host result.
 int64_t count_equal_dev(const int32_t* a, const int32_t* b, int64_t len, cudaStream_t s);
 
+// Quadratic (Euclidean) geometry, quadratic.cu: half-step a (row simplex
+// projections of w + G/ρ, + flag check), half-step b (column projections of
+// π + G/ρ into W_new, record partials, flag check), and w⁰ = column
+// projection of π⁰ (reset).
+void launch_row_quad(const BapgDev& d, cudaStream_t s);
+void launch_col_quad(const BapgDev& d, cudaStream_t s);
+void launch_quad_reset(const BapgDev& d, const float* pi0, float* w0, cudaStream_t s);
+
 // Graph inputs: host int32 edge lists (pairs a, b; validated by the caller)
 // standing for D = adjacency_distance(g) (tasks.cpp:167-174).
 struct GraphInput {

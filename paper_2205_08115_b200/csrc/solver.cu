@@ -422,16 +422,21 @@ void BapgEngine::load_device(const float* dx, int64_t ldx, const float* dy, int6
 void BapgEngine::reset(const double* w0_host) {
   GWB_CUDA(cudaSetDevice(device_));
   launch_status_reset(st_, stream_);
+  // Entropy: w0_host is w⁰ (the caller applied kl_scale).  Quadratic: it is
+  // π⁰ (or null for μνᵀ) and w⁰ = euclid_project(π⁰, ν, Cols) on the device
+  // (solvers.cpp:152-153), staged through P (overwritten by half-step a).
+  float* dst = quadratic() ? P_ : W_[0];
   if (w0_host) {
     double* stage = nullptr;
     GWB_CUDA(cudaMalloc(&stage, sizeof(double) * n_ * m_));
     GWB_CUDA(cudaMemcpyAsync(stage, w0_host, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, stream_));
-    launch_colmajor64_to_rowmajor32(stage, n_, m_, W_[0], ldm_, stream_);
+    launch_colmajor64_to_rowmajor32(stage, n_, m_, dst, ldm_, stream_);
     GWB_CUDA(cudaStreamSynchronize(stream_));
     GWB_CUDA(cudaFree(stage));
   } else {
-    launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, W_[0], stream_);
+    launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, dst, stream_);
   }
+  if (quadratic()) launch_quad_reset(dev_view(0), P_, W_[0], stream_);
   launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], aux_mode(), stream_);
   parity_ = 0;
   GWB_CUDA(cudaGetLastError());
@@ -475,12 +480,18 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
   launches += 2;
   if (timing_) GWB_CUDA(cudaEventRecord(e1, stream_));
   if (!half_b) {
-    launch_row_update(d, true, stream_);
+    if (quadratic())
+      launch_row_quad(d, stream_);
+    else
+      launch_row_update(d, true, stream_);
     launches += 2;
   } else {
-    launch_col_update(d, stream_);
+    if (quadratic())
+      launch_col_quad(d, stream_);
+    else
+      launch_col_update(d, stream_);
     launch_finalize(d, rel_tol, false, stream_);
-    launches += 6;
+    launches += quadratic() ? 4 : 6;
   }
   if (timing_) {
     GWB_CUDA(cudaEventRecord(e2, stream_));
@@ -523,7 +534,7 @@ int64_t BapgEngine::iterate(int iters, double rel_tol, bool use_graph) {
         graph_iters_ = kChunkIters;
       }
       GWB_CUDA(cudaGraphLaunch(ge, stream_));
-      launches += kChunkIters * 12;
+      launches += kChunkIters * (quadratic() ? 10 : 12);
       done += kChunkIters;  // even ⇒ parity unchanged
     }
   }

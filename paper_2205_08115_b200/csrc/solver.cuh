@@ -83,6 +83,10 @@ class BapgEngine {
   float* pi_dev() const { return P_; }
   int64_t ld() const { return ldm_; }
   int precision() const { return precision_; }
+  // gwb_geometry: GWB_ENTROPY (KL projections) or GWB_QUADRATIC (Euclidean
+  // simplex projections, quadratic.cu).  Set before reset().
+  void set_geometry(int g) { geometry_ = g; }
+  bool quadratic() const { return geometry_ == GWB_QUADRATIC; }
   // CUDA-event timing of kernel classes inside iterate() (enabled on demand).
   void set_timing(bool on) { timing_ = on; }
   void kernel_ms(int kind, double* avg_ms, int64_t* count);
@@ -148,6 +152,7 @@ class BapgEngine {
   cudaGraphExec_t graph_[2] = {nullptr, nullptr};  // chunk graph per start parity
   int graph_iters_ = 0;
 
+  int geometry_ = GWB_ENTROPY;
   bool timing_ = false;
   double last_ms_[2] = {0.0, 0.0};
   int64_t last_cnt_[2] = {0, 0};

@@ -18,6 +18,10 @@ CASES = [
     ("bpg", lambda: I.config1(seed=7, n=64), dict(algorithm=abi.BPG, step=5.0, max_iters=12, inner_iters=10)),
     ("hbpg", lambda: I.config1(seed=8, n=64), dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10, switch_iters=6, max_iters=14)),
     ("bpg-perturb", lambda: I.config1(seed=9, n=48), dict(algorithm=abi.BPG, perturbation=0.01, max_iters=8, inner_iters=20)),
+    # quadratic geometry (euclid_project, projections.cpp:36-77; solvers.cpp:179-182)
+    ("bapg-quad-er", lambda: I.config1(seed=10, n=72), dict(algorithm=abi.BAPG, geometry=abi.QUADRATIC, rho=0.1, max_iters=30)),
+    ("bapg-quad-gmm", lambda: I.config2(seed=11, n=60, m=44), dict(algorithm=abi.BAPG, geometry=abi.QUADRATIC, rho=2.0, max_iters=40)),
+    ("bapg-quad-stop", lambda: I.config1(seed=12, n=50), dict(algorithm=abi.BAPG, geometry=abi.QUADRATIC, rho=1.0, max_iters=400, rel_tol=1e-8)),
 ]
 
 
