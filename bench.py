@@ -220,10 +220,32 @@ def cpu_reference_sample(n_target, cpu_n, budget_s=20.0):
     assert r.code == 0, r.message
     its = iters / dt
     scale = (cpu_n / n_target) ** 3
-    return {"value": its * scale, "unit": "it/s", "cores": cores, "kind": "reference",
-            "sample": f"reference bapg_solve (oracle/_ref, OpenBLAS fp64, {cores} threads) on "
-                      f"BA n=m={cpu_n}: {iters} iterations in {dt:.2f}s = {its:.3f} it/s, "
-                      f"scaled by (n/{n_target})^3 to n={n_target}"}
+    out = {"value": its * scale, "unit": "it/s", "cores": cores, "kind": "reference",
+           "sample": f"reference bapg_solve (oracle/_ref, OpenBLAS fp64, {cores} threads) on "
+                     f"BA n=m={cpu_n}: {iters} iterations in {dt:.2f}s = {its:.3f} it/s, "
+                     f"scaled by (n/{n_target})^3 to n={n_target}"}
+    # SURVEY §8(d) setting (i): one thread, faithful to the reference's
+    # single-threaded Eigen GEMM (same BLAS, thread count set at run time).
+    try:
+        from oracle.bindings import openblas_path
+        blas = C.CDLL(openblas_path())
+        setn = blas.scipy_openblas_set_num_threads64_
+        setn.argtypes = [C.c_int]
+        setn(1)
+        cfg.max_iters = max(1, min(iters, int(budget_s / 2 / max(dt / iters * cores, 1e-3))))
+        t0 = time.perf_counter()
+        r1 = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+        d1 = time.perf_counter() - t0
+        setn(cores)
+        if r1.code == 0:
+            i1 = cfg.max_iters / d1
+            out["value_1thread"] = i1 * scale
+            out["sample_1thread"] = (f"same, 1 thread: {cfg.max_iters} iterations in {d1:.2f}s = "
+                                     f"{i1:.3f} it/s, scaled to n={n_target}")
+    except Exception as ex:  # reported, not fatal
+        out["value_1thread"] = None
+        out["sample_1thread"] = f"unavailable: {ex}"
+    return out
 
 
 def run_reference(args, world, rank):
