@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -72,6 +73,10 @@ struct __align__(64) GemmParams {
   const float* col_scale;
   const int* skip;
   int32_t accumulate;
+  int32_t splits;      // > 1: split-K; partials to ws[split][M][ldw]
+  int32_t kb_per_split;
+  float* ws;
+  int64_t ldw;
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -109,8 +114,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
 
-  // Grouped rasterisation over pair tiles.
-  const int pid = blockIdx.x >> 1;
+  // Grouped rasterisation over pair tiles (split-K: one tile sweep per split).
+  const int pid_all = blockIdx.x >> 1;
+  const int tiles_all = p.tiles_m * p.tiles_n;
+  const int split = pid_all / tiles_all;
+  const int pid = pid_all - split * tiles_all;
   const int per_group = kGroupM * p.tiles_n;
   const int group = pid / per_group;
   const int first_m = group * kGroupM;
@@ -139,7 +147,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   const int kblk = p.kind ? kBK16 : kBK;  // elements per 128-B k-block
-  const int kblocks = (p.K + kblk - 1) / kblk;
+  const int kblocks_all = (p.K + kblk - 1) / kblk;
+  const int kb_begin = p.splits > 1 ? split * p.kb_per_split : 0;
+  const int kblocks = p.splits > 1 ? max(0, min(kblocks_all - kb_begin, p.kb_per_split)) : kblocks_all;
   const int total = p.passes * kblocks;
   const int chunk = p.chunk;
   const int nchunks = (total + chunk - 1) / chunk;
@@ -153,7 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t ph = (it / kStages) & 1;
         ptx::mbar_wait(&empty[s], ph ^ 1);
         const int pass = it / kblocks;
-        const int kb = it - pass * kblocks;
+        const int kb = kb_begin + it - pass * kblocks;
         const uint32_t fbar = ptx::mapa(&full[s], 0);
         if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
         ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk, a_row);
@@ -227,7 +237,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
     }
     const int row = a_row + static_cast<int>(lane_base + lane);
-    if (row < p.M) {
+    if (p.splits > 1 && row < p.M) {
+      // Split-K partial: raw sums, the reduce kernel applies the epilogue.
+      float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
+      const int col0 = tn * kBN + static_cast<int>(col_base);
+#pragma unroll
+      for (int j = 0; j < kSliceCols; j += 4)
+        if (col0 + j < p.ldw)
+          *reinterpret_cast<float4*>(wrow + col0 + j) =
+              make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else if (row < p.M) {
       const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
       float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
       float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
@@ -305,6 +324,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<kTmemCols>(tmem);
+  }
+}
+
+// Split-K reduction + epilogue: one CTA per output row, fixed summation order
+// over the splits, then the same output modes as the GEMM epilogue.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ GemmParams p) {
+  if (p.skip != nullptr && *p.skip != 0) return;
+  const int row = blockIdx.x;
+  const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
+  for (int c0 = threadIdx.x * 8; c0 < p.N; c0 += blockDim.x * 8) {
+    float x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = 0.0f;
+    for (int s = 0; s < p.splits; ++s) {
+      const float* w = p.ws + static_cast<int64_t>(s) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw + c0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < p.ldw) x[q] = __fadd_rn(x[q], w[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float v = x[q] * rs;
+      if (p.col_scale != nullptr) v *= (c0 + q < p.N) ? p.col_scale[c0 + q] : 0.0f;
+      x[q] = p.aux_mode == 1 ? rna_tf32(v) : v;
+    }
+    const int64_t off = static_cast<int64_t>(row) * p.ldc + c0;
+    if (p.c_planes > 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (c0 + q >= p.N) continue;
+        float r = x[q];
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(r);
+        r -= __bfloat162float(h0);
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(r);
+        r -= __bfloat162float(h1);
+        const __nv_bfloat16 h2 = __float2bfloat16_rn(r);
+        p.c_pl[0][off + q] = h0;
+        p.c_pl[1][off + q] = p.c_planes == 2 ? __float2bfloat16_rn(x[q] - __bfloat162float(h0)) : h1;
+        if (p.c_planes == 3) p.c_pl[2][off + q] = h2;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (c0 + q >= p.N) continue;
+        float v = x[q];
+        if (p.accumulate) v = __fadd_rn(p.c[off + q], v);
+        p.c[off + q] = v;
+        if (p.aux_mode == 2) p.c_aux[off + q] = v - trunc_tf32(v);
+      }
+    }
   }
 }
 
@@ -389,6 +458,10 @@ struct GemmPlan {
   GemmParams params;
   int grid = 0;
   double flops = 0.0;
+  float* ws = nullptr;  // split-K workspace (owned)
+  ~GemmPlan() {
+    if (ws) cudaFree(ws);
+  }
 };
 
 GemmPlan* gemm_plan_create(const GemmDesc& d) {
@@ -463,7 +536,27 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.col_scale = d.col_scale;
   g.accumulate = d.accumulate ? 1 : 0;
   g.skip = d.skip;
-  p->grid = 2 * g.tiles_m * g.tiles_n;  // two CTAs (one cluster) per tile
+  // Split-K when one sweep of pair tiles leaves most of the 74 SM pairs idle
+  // (n ≲ 2000): each split keeps ≥ 4 k-blocks, the grid stays one wave.
+  const int tiles = g.tiles_m * g.tiles_n;
+  const int kblocks = (g.K + (g.kind ? kBK16 : kBK) - 1) / (g.kind ? kBK16 : kBK);
+  int splits = 1;
+  if (d.split_k >= 2) {
+    splits = d.split_k;
+  } else if (d.split_k == 0 && tiles < 74) {
+    splits = std::max(1, std::min(74 / tiles, kblocks / 4));
+  }
+  splits = std::max(1, std::min(splits, kblocks));
+  g.splits = splits;
+  if (splits > 1) {
+    g.kb_per_split = (kblocks + splits - 1) / splits;
+    g.splits = (kblocks + g.kb_per_split - 1) / g.kb_per_split;  // no empty splits
+    g.ldw = (d.N + 7) / 8 * 8;
+    if (cudaMalloc(&p->ws, sizeof(float) * static_cast<size_t>(g.splits) * d.M * g.ldw) != cudaSuccess)
+      throw std::runtime_error("gemm: split-K workspace allocation failed");
+    g.ws = p->ws;
+  }
+  p->grid = 2 * g.tiles_m * g.tiles_n * g.splits;  // two CTAs (one cluster) per tile
   p->flops = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
   return p;
 }
@@ -472,8 +565,12 @@ void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
   gemm_tf32_kernel<<<p->grid, kThreads, kSmemBytes, s>>>(p->params);
+  if (p->params.splits > 1)
+    splitk_reduce_kernel<<<p->params.M, 256, 0, s>>>(p->params);
   return cudaGetLastError();
 }
+
+int gemm_launches(const GemmPlan* p) { return p->params.splits > 1 ? 2 : 1; }
 
 double gemm_flops(const GemmPlan* p) { return p->flops; }
 int gemm_passes(const GemmPlan* p) { return p->params.passes; }

@@ -56,6 +56,11 @@ struct GemmDesc {
   // C += A·Bᵀ instead of C = A·Bᵀ (fp32 `c` output only): K-split partial
   // products accumulated across launches (multi-GPU chunked GEMM2).
   bool accumulate = false;
+  // Split-K for grids smaller than one wave of CTA pairs (small problems):
+  // 0 = automatic, 1 = never, S ≥ 2 = force S splits.  Partial products go
+  // to a plan-owned fp32 workspace and a second kernel sums them in a fixed
+  // order and applies the epilogue (scales, operand copies, planes).
+  int split_k = 0;
 };
 
 // Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).
@@ -67,5 +72,7 @@ cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s);
 // Algorithmic FLOPs of one launch (2·M·N·K, independent of the pass count).
 double gemm_flops(const GemmPlan* p);
 int gemm_passes(const GemmPlan* p);
+// Kernel launches per gemm_launch (2 with split-K).
+int gemm_launches(const GemmPlan* p);
 
 }  // namespace gwb

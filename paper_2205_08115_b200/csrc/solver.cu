@@ -476,6 +476,7 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
   } else {
     GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
     GWB_CUDA(gemm_launch(g2_, stream_));
+    launches += gemm_launches(g1_[q][half_b ? 1 : 0]) + gemm_launches(g2_) - 2;
   }
   launches += 2;
   if (timing_) GWB_CUDA(cudaEventRecord(e1, stream_));
@@ -524,8 +525,9 @@ int64_t BapgEngine::iterate(int iters, double rel_tol, bool use_graph) {
         cudaGraph_t g;
         GWB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         int q = parity_;
+        graph_launches_ = 0;
         for (int k = 0; k < kChunkIters; ++k) {
-          enqueue_iteration(q, rel_tol);
+          graph_launches_ += enqueue_iteration(q, rel_tol);
           q ^= 1;
         }
         GWB_CUDA(cudaStreamEndCapture(stream_, &g));
@@ -534,7 +536,7 @@ int64_t BapgEngine::iterate(int iters, double rel_tol, bool use_graph) {
         graph_iters_ = kChunkIters;
       }
       GWB_CUDA(cudaGraphLaunch(ge, stream_));
-      launches += kChunkIters * (quadratic() ? 10 : 12);
+      launches += graph_launches_;
       done += kChunkIters;  // even ⇒ parity unchanged
     }
   }

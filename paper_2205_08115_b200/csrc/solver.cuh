@@ -151,6 +151,7 @@ class BapgEngine {
 
   cudaGraphExec_t graph_[2] = {nullptr, nullptr};  // chunk graph per start parity
   int graph_iters_ = 0;
+  int64_t graph_launches_ = 0;  // kernels in one captured chunk
 
   int geometry_ = GWB_ENTROPY;
   bool timing_ = false;
