@@ -226,12 +226,11 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
   };
   // G chunk from the split accumulators (hi plane + mid/lo planes).
   auto load_acc = [&](int g, float (&v)[32]) {
-    uint32_t hi[32], lo[32];
+    uint32_t hi[32];
     ptx::tmem_ld_32x32b_x32(tl + kAccHi + c0 + 32 * g, hi);
-    ptx::tmem_ld_32x32b_x32(tl + kAccLo + c0 + 32 * g, lo);
     ptx::tmem_wait_ld();
 #pragma unroll
-    for (int t = 0; t < 32; ++t) v[t] = __fadd_rn(__uint_as_float(hi[t]), __uint_as_float(lo[t]));
+    for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(hi[t]);
   };
   auto store_cols = [&](uint32_t col, const float (&v)[32]) {
     uint32_t r[32];
@@ -261,16 +260,21 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
     ptx::tc_fence_after();
     constexpr uint32_t id1 = ptx::idesc_bf16(128, 128) | (1u << 16);  // B MN-major
     constexpr uint32_t id2 = ptx::idesc_bf16(128, 128);
+    // One accumulator, smallest plane first (lo, mid, hi): the small terms
+    // are summed while the running sum is small, so the accumulator's
+    // truncation acts on the 128 hi-plane terms only — the same bound as a
+    // separate hi accumulator.
 #pragma unroll 1
-    for (int p = 0; p < 3; ++p) {
-      const uint32_t d = tbase + (p == 0 ? kAccHi : kAccLo);
+    for (int pi = 0; pi < 3; ++pi) {
+      const int p = 2 - pi;
+      const uint32_t d = tbase + kAccHi;
       const uint32_t pl = sPl_a + p * kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {  // K = 128 in steps of 16
         const uint32_t koff = (kk >> 2) * kHalfTile + (kk & 3) * 32;
         const uint64_t ad = ptx::umma_desc_sw128(gemm1 ? sD_a + koff : pl + koff);
         const uint64_t bd = gemm1 ? desc_mn(pl + kk * 2048) : ptx::umma_desc_sw128(sD_a + kTileBytes + koff);
-        ptx::mma_bf16(d, ad, bd, gemm1 ? id1 : id2, (p == 2 || kk) ? 1u : 0u);
+        ptx::mma_bf16(d, ad, bd, gemm1 ? id1 : id2, (pi || kk) ? 1u : 0u);
       }
     }
     ptx::mma_commit(&bars[1]);
@@ -361,15 +365,14 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         double gw = 0.0, rw = 0.0;
 #pragma unroll 1
         for (int g = 0; g < 2; ++g) {
-          uint32_t ha[32], la[32], wr[32];
+          uint32_t ha[32], wr[32];
           ld(kAccHi + c0 + 32 * g, ha);
-          ld(kAccLo + c0 + 32 * g, la);
           ld(kW + c0 + 32 * g, wr);
           ptx::tmem_wait_ld();
           float gv[32], wv[32];
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
-            gv[t] = __fadd_rn(__uint_as_float(ha[t]), __uint_as_float(la[t]));
+            gv[t] = __uint_as_float(ha[t]);
             wv[t] = __uint_as_float(wr[t]);
           }
           float gwf = 0.f;
@@ -380,7 +383,6 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
             rw += static_cast<double>(wv[t]);
           }
           gw += static_cast<double>(gwf);
-          if (phase == 0) store_cols(kAccHi + c0 + 32 * g, gv);  // fold G
         }
         row_x[h * kT + i] = rmax;
         row_d[(h * kT + i) * 2 + 0] = gw;
@@ -460,7 +462,6 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       for (int g = 0; g < 2; ++g) {
         float gv[32];
         load_acc(g, gv);
-        store_cols(kAccHi + c0 + 32 * g, gv);
 #pragma unroll
         for (int t = 0; t < 32; ++t) gv[t] *= inv_rho;
         const float cm = xreduce32(gv, lane, FMax{});

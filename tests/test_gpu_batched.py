@@ -85,7 +85,11 @@ def test_batched_ragged_nonuniform(gpu, port):
         mu = rng.uniform(0.5, 1.5, n)
         nu = rng.uniform(0.5, 1.5, m)
         probs.append((dx, dy, mu / mu.sum(), nu / nu.sum()))
-    cfg = gw.SolverConfig(algorithm="bapg", rho=0.05, max_iters=80, rel_tol=1e-30, quiet=True)
+    # ρ = 0.1 as config 5: at ρ = 0.05 this instance sits at the fp32-iterate
+    # limit for every engine here (the single-problem dense engine also
+    # lands at 0.8–1.0e-4 of the 1e-4 bound), so it would test rounding
+    # order rather than the padding this test is about.
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=80, rel_tol=1e-30, quiet=True)
     check_against_oracle(port, solve_batch(probs, cfg), probs, cfg)
 
 
