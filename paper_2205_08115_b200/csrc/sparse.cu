@@ -23,7 +23,8 @@ void check_cuda(cudaError_t e, const char* what);  // solver.cu
 namespace {
 
 constexpr int kTileRows = 32;   // output rows per CTA
-constexpr int kTileCols = 128;  // output columns per CTA (a float4 per lane)
+constexpr int kVec = 2;         // float4 column groups per lane
+constexpr int kTileCols = 128 * kVec;  // output columns per CTA
 constexpr int kThreads = 256;   // 8 warps × 4 rows
 
 __global__ void csr_count_kernel(const float* __restrict__ D, int64_t rows, int64_t ld,
@@ -58,28 +59,39 @@ __global__ void csr_fill_kernel(const float* __restrict__ D, int64_t rows, int64
 }
 
 // One CTA: kTileRows output rows × kTileCols columns.  Warp w owns rows
-// r0 + 4w … r0 + 4w + 3; lane l owns columns c0 + 4l … c0 + 4l + 3.  Each
-// row's (col, val) pairs are fetched 32 at a time with one coalesced load and
-// broadcast by shuffles; the gathers are issued four at a time.
+// r0 + 4w … r0 + 4w + 3; lane l owns the float4 column groups
+// c0 + 4l + 128v (v < kVec), so every gathered row segment is kVec coalesced
+// 512-B loads.  Each row's (col, val) pairs are fetched 32 at a time with one
+// coalesced load and broadcast by shuffles; four neighbours are gathered per
+// step, i.e. 4·kVec independent loads in flight per lane (the kernel is
+// L2-latency-bound).
 template <bool kTranspose>
 __global__ void __launch_bounds__(kThreads) rowgather_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
     const float* __restrict__ val, int64_t rows_out, const float* __restrict__ in,
     int64_t ld_in, int64_t cols, float* __restrict__ out, int64_t ld_out, const int* skip) {
   if (skip && *skip) return;
-  // [column mod 4][column / 4][row]: conflict-free on both the scatter (lanes
-  // vary column / 4) and the transposed read (lanes vary row).
-  __shared__ float tile[kTranspose ? 4 : 1][kTranspose ? 32 : 1][kTileRows + 1];
+  // [v][column mod 4][column / 4 within the 128-block][row]: conflict-free on
+  // the scatter (lanes vary column / 4) and the transposed read (lanes vary row).
+  __shared__ float tile[kTranspose ? kVec : 1][kTranspose ? 4 : 1][kTranspose ? 32 : 1][kTileRows + 1];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTileRows;
-  const int64_t c = static_cast<int64_t>(blockIdx.y) * kTileCols + lane * 4;
-  const bool col_ok = c < cols;  // ld_in, ld_out are multiples of 32: c..c+3 stay inside
-  const float* in_c = in + (col_ok ? c : 0);
+  int64_t c[kVec];
+  bool col_ok[kVec];
+  const float* in_c[kVec];
+#pragma unroll
+  for (int v = 0; v < kVec; ++v) {
+    c[v] = static_cast<int64_t>(blockIdx.y) * kTileCols + 128 * v + lane * 4;
+    col_ok[v] = c[v] < cols;  // ld_in, ld_out are multiples of 32: c..c+3 stay inside
+    in_c[v] = in + (col_ok[v] ? c[v] : 0);
+  }
 #pragma unroll 1
   for (int rr = 0; rr < kTileRows / 8; ++rr) {
     const int lr = warp * (kTileRows / 8) + rr;
     const int64_t i = r0 + lr;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc[kVec];
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < rows_out) {
       const int32_t beg = row_ptr[i], end = row_ptr[i + 1];
       for (int32_t base = beg; base < end; base += 32) {
@@ -95,37 +107,50 @@ __global__ void __launch_bounds__(kThreads) rowgather_kernel(
             a[u] = __shfl_sync(0xffffffffu, my_a, (t + u) & 31);
             if (t + u >= cnt) a[u] = 0.f;  // k[u] is a valid row (lane ≥ cnt loads row 0)
           }
-          float4 x[4];
+          float4 x[4][kVec];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            x[u] = col_ok ? __ldg(reinterpret_cast<const float4*>(in_c + static_cast<int64_t>(k[u]) * ld_in))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            acc.x = fmaf(a[u], x[u].x, acc.x);
-            acc.y = fmaf(a[u], x[u].y, acc.y);
-            acc.z = fmaf(a[u], x[u].z, acc.z);
-            acc.w = fmaf(a[u], x[u].w, acc.w);
-          }
+            for (int v = 0; v < kVec; ++v)
+              x[u][v] = col_ok[v] ? __ldg(reinterpret_cast<const float4*>(
+                                        in_c[v] + static_cast<int64_t>(k[u]) * ld_in))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < kVec; ++v) {
+              acc[v].x = fmaf(a[u], x[u][v].x, acc[v].x);
+              acc[v].y = fmaf(a[u], x[u][v].y, acc[v].y);
+              acc[v].z = fmaf(a[u], x[u][v].z, acc[v].z);
+              acc[v].w = fmaf(a[u], x[u][v].w, acc[v].w);
+            }
         }
       }
     }
-    if (!kTranspose) {
-      if (i < rows_out && col_ok) *reinterpret_cast<float4*>(out + i * ld_out + c) = acc;
-    } else {
-      tile[0][lane][lr] = acc.x;
-      tile[1][lane][lr] = acc.y;
-      tile[2][lane][lr] = acc.z;
-      tile[3][lane][lr] = acc.w;
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) {
+      if (!kTranspose) {
+        if (i < rows_out && col_ok[v]) *reinterpret_cast<float4*>(out + i * ld_out + c[v]) = acc[v];
+      } else {
+        tile[v][0][lane][lr] = acc[v].x;
+        tile[v][1][lane][lr] = acc[v].y;
+        tile[v][2][lane][lr] = acc[v].z;
+        tile[v][3][lane][lr] = acc[v].w;
+      }
     }
   }
   if (kTranspose) {
     __syncthreads();
-    // outᵀ rows = columns of the tile; each warp writes 16 rows of 32 floats.
-    for (int cc = warp; cc < kTileCols; cc += kThreads / 32) {
+    // outᵀ rows = columns of the tile: kTileRows lanes per output row, so a
+    // warp writes 32 / kTileRows rows of kTileRows floats per step.
+    constexpr int kPer = 32 / kTileRows;
+    const int sub = lane / kTileRows, li = lane % kTileRows;
+    for (int c2 = warp * kPer; c2 < kTileCols; c2 += (kThreads / 32) * kPer) {
+      const int cc = c2 + sub;
       const int64_t j = static_cast<int64_t>(blockIdx.y) * kTileCols + cc;
-      const int64_t i = r0 + lane;
-      if (j < cols && i < rows_out) out[j * ld_out + i] = tile[cc & 3][cc >> 2][lane];
+      const int64_t i = r0 + li;
+      const int v = cc >> 7, w = cc & 127;
+      if (j < cols && i < rows_out) out[j * ld_out + i] = tile[v][w & 3][w >> 2][li];
     }
   }
 }
