@@ -623,8 +623,9 @@ def c5_variant(world, rank, local, dist, iters=500, total=4096):
             "kernel_ms": ms, "tflops_alg": flops / (ms * 1e-3) / 1e12,
             "tflops_exec_bf16": 3 * flops / (ms * 1e-3) / 1e12,
             "e2e": {"value": iters / wall, "unit": "batched it/s", "seconds": wall,
-                    "h2d_bytes_per_step": total * 2 * (128 * 128 * 8 + 128 * 8),
-                    "d2h_bytes_per_step": total * 3 * 128 * 128 * 8}}
+                    "h2d_bytes_per_step": r["h2d_bytes"], "d2h_bytes_per_step": r["d2h_bytes"],
+                    "note": "one gwb_bapg_solve_batched call from pinned fp64 host buffers "
+                            "(H2D of all inputs, D2H of every final coupling)"}}
 
 
 def run_e2e(args, edges, tgt, n, prec):

@@ -667,12 +667,15 @@ __global__ void batched_fixup_kernel(const float* __restrict__ P, const float* _
 
 template <class T>
 struct DevBuf {
+  // Stream-ordered allocation: the default pool keeps the memory, so repeated
+  // batched calls do not pay cudaMalloc/cudaFree of gigabytes each time.
   T* p = nullptr;
-  explicit DevBuf(size_t count) {
-    if (count) GWB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  cudaStream_t s = nullptr;
+  DevBuf(size_t count, cudaStream_t stream) : s(stream) {
+    if (count) GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
   }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -798,6 +801,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
     if (f.problem >= 0) raise_failure(f);
     return;
   }
+  pool_keep(device);
   cudaStream_t s;
   GWB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard {
@@ -809,14 +813,16 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   // Bound the device working set: problems are processed in chunks.
   const int64_t chunk = std::min<int64_t>(batch, 16384);
   const size_t len = static_cast<size_t>(n) * m;
-  DevBuf<double> d_dx(chunk * n * n), d_dy(chunk * m * m), d_mu(chunk * n), d_nu(chunk * m);
-  DevBuf<uint8_t> d_pack(chunk * 2 * kTileBytes);
-  DevBuf<double> d_mup(chunk * kT), d_nup(chunk * kT);
-  DevBuf<float> d_P(chunk * kT * kT), d_W(chunk * kT * kT);
-  DevBuf<DevRecord> d_rec(trace ? chunk * (cfg->max_iters + 2) : 0);
-  DevBuf<BatchStatus> d_st(chunk);
-  DevBuf<double> d_pi(out_pi ? chunk * len : 0), d_w(out_w ? chunk * len : 0), d_fin(chunk * len);
-  DevBuf<int> d_inexact(1);
+  DevBuf<double> d_dx(chunk * n * n, s), d_dy(chunk * m * m, s), d_mu(chunk * n, s),
+      d_nu(chunk * m, s);
+  DevBuf<uint8_t> d_pack(chunk * 2 * kTileBytes, s);
+  DevBuf<double> d_mup(chunk * kT, s), d_nup(chunk * kT, s);
+  DevBuf<float> d_P(chunk * kT * kT, s), d_W(chunk * kT * kT, s);
+  DevBuf<DevRecord> d_rec(trace ? chunk * (cfg->max_iters + 2) : 0, s);
+  DevBuf<BatchStatus> d_st(chunk, s);
+  DevBuf<double> d_pi(out_pi ? chunk * len : 0, s), d_w(out_w ? chunk * len : 0, s),
+      d_fin(chunk * len, s);
+  DevBuf<int> d_inexact(1, s);
   GWB_CUDA(cudaFuncSetAttribute(bapg_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmem)));
   cudaEvent_t ev0, ev1;

@@ -128,11 +128,17 @@ int primary_device() {
     fail(GWB_ERR_RUNTIME, "no CUDA device available: the GW solver path runs only on sm_100 GPUs");
   }
   if (g_devices[0] >= count) fail(GWB_ERR_RUNTIME, fmt("device %d not present", g_devices[0]));
-  cudaDeviceProp prop;
-  cudaGetDeviceProperties(&prop, g_devices[0]);
-  if (prop.major != 10)
-    fail(GWB_ERR_RUNTIME, fmt("device %d is sm_%d%d; this build targets sm_100a", g_devices[0],
-                              prop.major, prop.minor));
+  // Compute capability, once per device (cudaGetDeviceProperties is slow).
+  static std::vector<int> checked;
+  if (std::find(checked.begin(), checked.end(), g_devices[0]) == checked.end()) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, g_devices[0]);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, g_devices[0]);
+    if (major != 10)
+      fail(GWB_ERR_RUNTIME, fmt("device %d is sm_%d%d; this build targets sm_100a", g_devices[0],
+                                major, minor));
+    checked.push_back(g_devices[0]);
+  }
   return g_devices[0];
 }
 

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 namespace gwb {
 
@@ -33,19 +34,41 @@ namespace {
 constexpr int kChunkIters = 16;  // iterations per captured graph (even)
 
 template <class T>
-T* dalloc(size_t count) {
+T* dalloc(cudaStream_t s, size_t count) {
+  // Stream-ordered allocation + zero fill on the engine's own stream: ordered
+  // with every later kernel, and served from the device's memory pool on
+  // repeated solves (pool_keep) instead of fresh cudaMalloc/cudaFree.
   void* p = nullptr;
-  GWB_CUDA(cudaMalloc(&p, count * sizeof(T) + 256));
-  // The engines run on non-blocking streams, which do not order against the
-  // legacy stream cudaMemset uses: wait for the zero-fill before returning.
-  GWB_CUDA(cudaMemset(p, 0, count * sizeof(T) + 256));
-  GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+  GWB_CUDA(cudaMallocAsync(&p, count * sizeof(T) + 256, s));
+  GWB_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T) + 256, s));
   return static_cast<T*>(p);
 }
 
-void dfree(void* p) {
-  if (p) cudaFree(p);
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
 }
+
+}  // namespace
+
+// Keep freed stream-ordered memory cached in the device's default pool (the
+// default release threshold of 0 would return it to the driver at every
+// synchronisation), so repeated solves — the experiment worker pool — reuse
+// their workspace.  Once per device.
+void pool_keep(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done.push_back(device);
+}
+
+namespace {
 
 }  // namespace
 
@@ -79,6 +102,7 @@ BapgEngine::BapgEngine(int device, int64_t n, int64_t m, double rho, int precisi
     GWB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     own_stream_ = true;
   }
+  pool_keep(device_);
   alloc();
 }
 
@@ -95,14 +119,14 @@ BapgEngine::~BapgEngine() {
   gemm_plan_destroy(g2_tail_);
   csr_free(cx_);
   csr_free(cy_);
-  dfree(Vs_);
-  dfree(DyT_);
+  dfree(Vs_, stream_);
+  dfree(DyT_, stream_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], Vt_,
            Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
            col_max_, col_scale_, col_psump_, col_dev_, st_, rec_})
-    dfree(p);
+    dfree(p, stream_);
   if (h_done_) cudaFreeHost(h_done_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto& mk : ev_marks_) {
@@ -114,37 +138,37 @@ BapgEngine::~BapgEngine() {
 
 void BapgEngine::alloc() {
   const size_t nm = static_cast<size_t>(n_) * ldm_;
-  Dx_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
-  Dy_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
-  P_ = dalloc<float>(nm);
+  Dx_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_);
+  Dy_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
+  P_ = dalloc<float>(stream_, nm);
   // Operand copies hold one fp32 plane (TF32 modes) or up to three bf16
   // planes (bf16x3): size them for 6 B/element.
-  P_aux_ = dalloc<float>(nm * 3 / 2);
+  P_aux_ = dalloc<float>(stream_, nm * 3 / 2);
   for (int q = 0; q < 2; ++q) {
-    W_[q] = dalloc<float>(nm);
-    W_aux_[q] = dalloc<float>(nm * 3 / 2);
+    W_[q] = dalloc<float>(stream_, nm);
+    W_aux_[q] = dalloc<float>(stream_, nm * 3 / 2);
   }
-  Vt_ = dalloc<float>(static_cast<size_t>(m_) * ldn_);
+  Vt_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_);
   if (precision_ != GWB_PREC_TF32)
-    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2);
-  G_ = dalloc<float>(nm);
-  mu32_ = dalloc<float>(ldn_);
-  nu32_ = dalloc<float>(ldm_);
-  mu64_ = dalloc<double>(ldn_);
-  nu64_ = dalloc<double>(ldm_);
-  row_part_ = dalloc<RowPart>(n_);
-  cw_part_ = dalloc<ColWritePart>(n_);
+    Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
+  G_ = dalloc<float>(stream_, nm);
+  mu32_ = dalloc<float>(stream_, ldn_);
+  nu32_ = dalloc<float>(stream_, ldm_);
+  mu64_ = dalloc<double>(stream_, ldn_);
+  nu64_ = dalloc<double>(stream_, ldm_);
+  row_part_ = dalloc<RowPart>(stream_, n_);
+  cw_part_ = dalloc<ColWritePart>(stream_, n_);
   // Column-pass chunking: enough CTAs to fill the chip (≥ 2 waves of 148).
   const int64_t col_blocks = (m_ + 127) / 128;
   chunks_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n_ + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks)));
-  col_pmax_ = dalloc<float>(static_cast<size_t>(chunks_) * m_);
-  col_psum_ = dalloc<float>(static_cast<size_t>(chunks_) * m_);
-  col_psump_ = dalloc<double>(static_cast<size_t>(chunks_) * m_);
-  col_max_ = dalloc<float>(ldm_);
-  col_scale_ = dalloc<float>(ldm_);
-  col_dev_ = dalloc<double>(ldm_);
-  st_ = dalloc<DevStatus>(1);
-  rec_ = dalloc<DevRecord>(static_cast<size_t>(max_iters_) + 2);
+  col_pmax_ = dalloc<float>(stream_, static_cast<size_t>(chunks_) * m_);
+  col_psum_ = dalloc<float>(stream_, static_cast<size_t>(chunks_) * m_);
+  col_psump_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
+  col_max_ = dalloc<float>(stream_, ldm_);
+  col_scale_ = dalloc<float>(stream_, ldm_);
+  col_dev_ = dalloc<double>(stream_, ldm_);
+  st_ = dalloc<DevStatus>(stream_, 1);
+  rec_ = dalloc<DevRecord>(stream_, static_cast<size_t>(max_iters_) + 2);
   GWB_CUDA(cudaMallocHost(&h_done_, 4 * sizeof(int)));
 }
 
@@ -185,8 +209,8 @@ BapgDev BapgEngine::dev_view(int q) const {
 
 void BapgEngine::prepare_d() {
   // Exactness / max of each structure matrix decides the operand copies.
-  float* d_max = dalloc<float>(2);
-  int* d_inexact = dalloc<int>(2);
+  float* d_max = dalloc<float>(stream_, 2);
+  int* d_inexact = dalloc<int>(stream_, 2);
   launch_analyze(Dx_, n_, n_, ldn_, d_max, d_inexact, stream_);
   launch_analyze(Dy_, m_, m_, ldm_, d_max + 1, d_inexact + 1, stream_);
   float h_max[2];
@@ -194,8 +218,8 @@ void BapgEngine::prepare_d() {
   GWB_CUDA(cudaMemcpyAsync(h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, stream_));
   GWB_CUDA(cudaMemcpyAsync(h_inexact, d_inexact, sizeof(h_inexact), cudaMemcpyDeviceToHost, stream_));
   GWB_CUDA(cudaStreamSynchronize(stream_));
-  dfree(d_max);
-  dfree(d_inexact);
+  dfree(d_max, stream_);
+  dfree(d_inexact, stream_);
   dx_exact_ = (h_inexact[0] & 1) == 0;
   dy_exact_ = (h_inexact[1] & 1) == 0;
   // Skinny problems (m ≤ 32, config 3): the FP32-pipe chain (skinny.cu).
@@ -204,8 +228,8 @@ void BapgEngine::prepare_d() {
   if (precision_ == GWB_PREC_AUTO && m_ <= kSkinnyMaxN) precision_ = GWB_PREC_FP32;
   if (precision_ == GWB_PREC_FP32) {
     destroy_graphs();
-    if (!Vs_) Vs_ = dalloc<float>(static_cast<size_t>(n_) * ldm_);
-    if (!DyT_) DyT_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
+    if (!Vs_) Vs_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldm_);
+    if (!DyT_) DyT_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
     launch_transpose(Dy_, m_, m_, ldm_, DyT_, ldm_, stream_);
     GWB_CUDA(cudaStreamSynchronize(stream_));
     return;
@@ -226,10 +250,10 @@ void BapgEngine::prepare_d() {
   if ((precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2) && !bf16_exact)
     precision_ = GWB_PREC_3XTF32;
   if (precision_ != GWB_PREC_TF32 && !Vt_aux_)
-    Vt_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2);
+    Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
   if (bf16()) {
-    if (!Dx_bf_) Dx_bf_ = dalloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16);
-    if (!Dy_bf_) Dy_bf_ = dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16);
+    if (!Dx_bf_) Dx_bf_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_ / 2 + 16);
+    if (!Dy_bf_) Dy_bf_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_ / 2 + 16);
     launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
     launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
     build_plans();
@@ -237,11 +261,11 @@ void BapgEngine::prepare_d() {
   }
   const int mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
   if (!dx_exact_) {
-    if (!Dx_aux_) Dx_aux_ = dalloc<float>(static_cast<size_t>(n_) * ldn_);
+    if (!Dx_aux_) Dx_aux_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_);
     launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_aux_, mode, stream_);
   }
   if (!dy_exact_) {
-    if (!Dy_aux_) Dy_aux_ = dalloc<float>(static_cast<size_t>(m_) * ldm_);
+    if (!Dy_aux_) Dy_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
     launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_aux_, mode, stream_);
   }
   build_plans();
@@ -373,13 +397,13 @@ void BapgEngine::load_host(const double* dx, const double* dy, const double* mu,
   GWB_CUDA(cudaSetDevice(device_));
   const int64_t big = std::max(n_ * n_, m_ * m_);
   double* stage = nullptr;
-  GWB_CUDA(cudaMalloc(&stage, static_cast<size_t>(big) * sizeof(double)));
+  GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stage), static_cast<size_t>(big) * sizeof(double), stream_));
   GWB_CUDA(cudaMemcpyAsync(stage, dx, sizeof(double) * n_ * n_, cudaMemcpyHostToDevice, stream_));
   launch_colmajor64_to_rowmajor32(stage, n_, n_, Dx_, ldn_, stream_);
   GWB_CUDA(cudaMemcpyAsync(stage, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, stream_));
   launch_colmajor64_to_rowmajor32(stage, m_, m_, Dy_, ldm_, stream_);
   GWB_CUDA(cudaStreamSynchronize(stream_));
-  GWB_CUDA(cudaFree(stage));
+  GWB_CUDA(cudaFreeAsync(stage, stream_));
   load_marginals(mu, nu);
 }
 
@@ -428,11 +452,11 @@ void BapgEngine::reset(const double* w0_host) {
   float* dst = quadratic() ? P_ : W_[0];
   if (w0_host) {
     double* stage = nullptr;
-    GWB_CUDA(cudaMalloc(&stage, sizeof(double) * n_ * m_));
+    GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stage), sizeof(double) * n_ * m_, stream_));
     GWB_CUDA(cudaMemcpyAsync(stage, w0_host, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, stream_));
     launch_colmajor64_to_rowmajor32(stage, n_, m_, dst, ldm_, stream_);
     GWB_CUDA(cudaStreamSynchronize(stream_));
-    GWB_CUDA(cudaFree(stage));
+    GWB_CUDA(cudaFreeAsync(stage, stream_));
   } else {
     launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, dst, stream_);
   }
@@ -625,9 +649,9 @@ void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
   double* pi64 = nullptr;
   double* w64 = nullptr;
   double* work = nullptr;
-  GWB_CUDA(cudaMalloc(&pi64, len * sizeof(double)));
-  GWB_CUDA(cudaMalloc(&w64, len * sizeof(double)));
-  GWB_CUDA(cudaMalloc(&work, sizeof(double) * std::max(n_, m_)));
+  GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pi64), len * sizeof(double), stream_));
+  GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w64), len * sizeof(double), stream_));
+  GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), sizeof(double) * std::max(n_, m_), stream_));
   // K8 fix-up: exact fp64 row (π) / column (w) re-projection.
   launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
   launch_rowmajor32_to_colmajor64(W_[parity_], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
@@ -638,9 +662,9 @@ void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
     GWB_CUDA(cudaMemcpyAsync(out_final, pi64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   }
   GWB_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(pi64);
-  cudaFree(w64);
-  cudaFree(work);
+  cudaFreeAsync(pi64, stream_);
+  cudaFreeAsync(w64, stream_);
+  cudaFreeAsync(work, stream_);
 }
 
 void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
@@ -685,14 +709,14 @@ void BapgEngine::readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_h
   const DevStatus s = status();
   const int par = s.iter >= 1 ? (s.iter - 1) & 1 : parity_;  // buffer holding the current w
   const size_t len = static_cast<size_t>(n_) * m_;
-  double* pi64 = dalloc<double>(len);
-  double* w64 = dalloc<double>(len);
-  double* fin64 = dalloc<double>(len);
-  double* work = dalloc<double>(static_cast<size_t>(std::max(n_, m_)));
-  double* rs = dalloc<double>(n_);
-  double* cs = dalloc<double>(m_);
-  float* fin32 = dalloc<float>(static_cast<size_t>(n_) * ldm_);
-  int32_t* assign = dalloc<int32_t>(n_);
+  double* pi64 = dalloc<double>(stream_, len);
+  double* w64 = dalloc<double>(stream_, len);
+  double* fin64 = dalloc<double>(stream_, len);
+  double* work = dalloc<double>(stream_, static_cast<size_t>(std::max(n_, m_)));
+  double* rs = dalloc<double>(stream_, n_);
+  double* cs = dalloc<double>(stream_, m_);
+  float* fin32 = dalloc<float>(stream_, static_cast<size_t>(n_) * ldm_);
+  int32_t* assign = dalloc<int32_t>(stream_, n_);
   // K8 fix-up, then the final coupling ½(π + w) (solvers.cpp:214-216).
   launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
   launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
@@ -712,14 +736,14 @@ void BapgEngine::readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_h
   if (assign_host)
     GWB_CUDA(cudaMemcpyAsync(assign_host, assign, sizeof(int32_t) * n_, cudaMemcpyDeviceToHost, stream_));
   if (gt_host) {
-    int32_t* gt = dalloc<int32_t>(static_cast<size_t>(n_gt));
+    int32_t* gt = dalloc<int32_t>(stream_, static_cast<size_t>(n_gt));
     GWB_CUDA(cudaMemcpyAsync(gt, gt_host, sizeof(int32_t) * n_gt, cudaMemcpyHostToDevice, stream_));
     const int64_t hits = count_equal_dev(assign, gt, n_gt, stream_);
     r->accuracy = 100.0 * static_cast<double>(hits) / static_cast<double>(n_gt);
-    dfree(gt);
+    dfree(gt, stream_);
   }
   GWB_CUDA(cudaStreamSynchronize(stream_));
-  for (void* p : std::initializer_list<void*>{pi64, w64, fin64, work, rs, cs, fin32, assign}) dfree(p);
+  for (void* p : std::initializer_list<void*>{pi64, w64, fin64, work, rs, cs, fin32, assign}) dfree(p, stream_);
 }
 
 double BapgEngine::gemm_flops_per_iter() const {

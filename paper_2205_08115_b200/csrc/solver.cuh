@@ -26,6 +26,8 @@ struct CudaError : std::exception {
 };
 
 void check_cuda(cudaError_t e, const char* what);
+// Keep stream-ordered allocations cached in the device's default pool.
+void pool_keep(int device);
 #define GWB_CUDA(x) ::gwb::check_cuda((x), #x)
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }

