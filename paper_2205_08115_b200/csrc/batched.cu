@@ -731,7 +731,7 @@ struct Failure {
 
 // Same precedence as the single-problem path (capi.cu raise_device_flags,
 // solvers.cpp:164-189); the detail names the problem.
-[[noreturn]] void raise_failure(const Failure& f) {
+[[noreturn]] void raise_failure(const Failure& f, bool name_problem = true) {
   std::string detail;
   if (f.flags & kFlagOverflowA)
     detail = "exp overflow; increase rho";
@@ -743,6 +743,7 @@ struct Failure {
     detail = fmtmsg("column %lld has nonpositive sum; cannot rescale", f.zero_index, "");
   else
     detail = "non-finite iterate";
+  if (!name_problem) api_numerical("bapg", f.iter, detail);
   api_numerical("bapg", f.iter, fmtmsg("problem %lld: %s", f.problem, detail.c_str()));
 }
 
@@ -785,7 +786,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
                          const double* dy, int64_t m, const double* mu, const double* nu,
                          double* out_final, double* out_pi, double* out_w, gwb_record* trace,
                          int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                         int32_t* iterations_used) {
+                         int32_t* iterations_used, bool name_problem) {
   if (!dx || !dy || !mu || !nu || !out_final) api_fail(GWB_ERR_INVALID, "null input/output buffer");
   if (trace && trace_cap < cfg->max_iters) api_fail(GWB_ERR_CAPACITY, "trace capacity < max_iters");
   const int device = api_device();
@@ -798,7 +799,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   // runs problem by problem on the generic engine.
   if (n > kT || m > kT || !onchip_prec || cfg->geometry != GWB_ENTROPY) {
     const Failure f = batched_generic(cfg, device, batch, dx, n, dy, m, mu, nu, o, 0);
-    if (f.problem >= 0) raise_failure(f);
+    if (f.problem >= 0) raise_failure(f, name_problem);
     return;
   }
   pool_keep(device);
@@ -918,7 +919,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
       if (iterations_used) iterations_used[b] = st.used;
     }
   }
-  if (first.problem >= 0) raise_failure(first);
+  if (first.problem >= 0) raise_failure(first, name_problem);
 }
 
 }  // namespace gwb
