@@ -466,11 +466,10 @@ struct GemmPlan {
 };
 
 GemmPlan* gemm_plan_create(const GemmDesc& d) {
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kSmemBytes));
-  });
+  // Per current device (attributes are per device context); cheap, and plans
+  // are created once per solve.
+  cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kSmemBytes));
   auto* p = new GemmPlan();
   GemmParams& g = p->params;
   std::memset(&g, 0, sizeof(g));
