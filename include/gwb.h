@@ -64,7 +64,7 @@ enum gwb_code {
   GWB_ERR_ZERO_SUM = 4,      /* gw::ZeroSumLineError       types.hpp:36-45 */
   GWB_ERR_INVALID = 5,       /* std::invalid_argument (value-type checks) */
   GWB_ERR_DOMAIN = 6,        /* std::domain_error */
-  GWB_ERR_UNSUPPORTED = 7,   /* outside the B200 path (FW, quadratic, residual) */
+  GWB_ERR_UNSUPPORTED = 7,   /* outside the B200 path (FW) */
   GWB_ERR_RUNTIME = 8,       /* CUDA / NCCL / no device: std::runtime_error */
   GWB_ERR_CAPACITY = 9       /* caller-provided trace buffer too small */
 };
@@ -232,6 +232,24 @@ GWB_API int32_t gwb_alignment_accuracy(const int32_t* pred, int64_t n_pred,
                                        const int32_t* gt, int64_t n_gt,
                                        double* out, gwb_status* st);
 
+/* gw::dykstra_project (projections.hpp:46-51, projections.cpp:165-187):
+ * Euclidean projection of pi onto Π(μ, ν) by Dykstra's alternating
+ * projections; stops once the inf-norm marginal error ≤ tol.
+ * GWB_ERR_RUNTIME "dykstra_project did not converge in <max_iters> sweeps;
+ * final constraint violation <err>" otherwise (fp64 on the device). */
+GWB_API int32_t gwb_dykstra_project(const double* pi, int64_t n, int64_t m,
+                                    const double* mu, const double* nu, double tol,
+                                    int32_t max_iters, double* out, gwb_status* st);
+
+/* gw::luo_tseng_residual (diagnostics.hpp:27-29, diagnostics.cpp:33-42):
+ * ‖π − dykstra_project(π + D_X π D_Y, μ, ν, dykstra_tol)‖_F (10000 sweeps;
+ * the reference default dykstra_tol is 1e-8).  Also filled into every
+ * gwb_record when gwb_config.record_residual is set. */
+GWB_API int32_t gwb_luo_tseng_residual(const double* dx, int64_t n, const double* dy,
+                                       int64_t m, const double* pi, const double* mu,
+                                       const double* nu, double dykstra_tol, double* out,
+                                       gwb_status* st);
+
 /* Batched BAPG over `batch` independent problems sharing n and m (config 5).
  * The reference has no batched API; its equivalent is `batch` calls of
  * gw::solve from the experiment worker pool (experiment.cpp:273-304).
@@ -289,6 +307,8 @@ GWB_API int32_t gwb_session_destroy(gwb_session* s);
 /* run_cell's post-solve readout (experiment.cpp:169-195) of the session's
  * final coupling ½(π + w), computed on the device: gw_objective,
  * marginal_infeasibility, coupling_entropy, split_gap(π, w), and the
+ * luo_tseng_residual (NaN when its Dykstra projection does not converge, as
+ * run_cell's catch, experiment.cpp:177-182), the
  * hard_assignment (written to `assignment`, n entries, if non-null) with its
  * alignment_accuracy against `ground_truth` (n_gt entries, if non-null;
  * same errors as gwb_alignment_accuracy).  Nothing n×m crosses PCIe. */
@@ -297,6 +317,7 @@ typedef struct gwb_readout {
   double marginal_infeasibility;
   double entropy;
   double split_gap;
+  double residual;      /* luo_tseng_residual; NaN if Dykstra did not converge */
   double accuracy;      /* valid iff has_accuracy */
   int32_t has_accuracy;
 } gwb_readout;

@@ -27,6 +27,12 @@ GWB_API int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b,
  * batched call took the generic engine.  Measurement hook for bench.py. */
 GWB_API int32_t gwb_batched_last_kernel_ms(double* ms, int64_t* problems);
 
+/* Sweeps used and device time (CUDA events around the sweep loop on its
+ * stream) of the last Dykstra projection run in this process (the
+ * gwb_dykstra_project leaf, a Luo-Tseng residual or a readout).
+ * Measurement hook for tools/bench_residual.py. */
+GWB_API int32_t gwb_dykstra_last_stats(int32_t* sweeps, double* ms);
+
 /* ---------------------------------------------------------------------------
  * Row-sharded multi-GPU BAPG, one shard per rank (csrc/shard.cu).  The
  * caller owns the communication buffers (e.g. torch tensors used with

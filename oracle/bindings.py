@@ -83,6 +83,10 @@ class Oracle:
         getattr(L, pre + "kl_scale").argtypes = [_D, C.c_int64, C.c_int64, _D, C.c_int64, C.c_int32, _D, _ST]
         getattr(L, pre + "sinkhorn_project").argtypes = [_D, C.c_int64, C.c_int64, _D, _D, C.c_double,
                                                 C.c_int32, C.c_int32, _D, _I, _D, _I, _ST]
+        getattr(L, pre + "dykstra_project").argtypes = [_D, C.c_int64, C.c_int64, _D, _D, C.c_double,
+                                                        C.c_int32, _D, _I, _ST]
+        getattr(L, pre + "luo_tseng_residual").argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _D, _D,
+                                                           C.c_double, _D, _ST]
         if kind == "reference":
             L.gwref_lipschitz_bound.argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _ST]
             L.gwref_marginal_infeasibility.argtypes = [_D, C.c_int64, C.c_int64, _D, _D, _D, _ST]
@@ -126,7 +130,8 @@ class Oracle:
             res.trace = [dict(iter=r.iter, objective=r.objective,
                               marginal_infeasibility=r.marginal_infeasibility,
                               split_gap=r.split_gap, rel_change=r.rel_change,
-                              elapsed_seconds=r.elapsed_seconds, phase=r.phase)
+                              elapsed_seconds=r.elapsed_seconds, phase=r.phase,
+                              residual=r.residual if r.has_residual else None)
                          for r in trace[: nr.value]]
         return res
 
@@ -161,6 +166,26 @@ class Oracle:
                                                      C.byref(it), C.byref(err), C.byref(cv), C.byref(st))
         return rc, dict(coupling=out, iterations=it.value, marginal_error=err.value,
                         converged=bool(cv.value)), st
+
+    def dykstra_project(self, pi, mu, nu, tol=1e-8, max_iters=10000):
+        """Returns (code, projected coupling, message)."""
+        pi = _f(pi)
+        mu, nu = np.ascontiguousarray(mu, float), np.ascontiguousarray(nu, float)
+        out, st, sw = np.empty_like(pi, order="F"), abi.Status(), C.c_int32(0)
+        rc = getattr(self.lib, self.pre + "dykstra_project")(_p(pi), pi.shape[0], pi.shape[1], _p(mu),
+                                                            _p(nu), tol, max_iters, _p(out),
+                                                            C.byref(sw), C.byref(st))
+        return rc, out, st.message.decode(errors="replace")
+
+    def luo_tseng_residual(self, dx, dy, pi, mu, nu, tol=1e-8):
+        """Returns (code, residual, message)."""
+        dx, dy, pi = _f(dx), _f(dy), _f(pi)
+        mu, nu = np.ascontiguousarray(mu, float), np.ascontiguousarray(nu, float)
+        out, st = C.c_double(0), abi.Status()
+        rc = getattr(self.lib, self.pre + "luo_tseng_residual")(_p(dx), dx.shape[0], _p(dy), dy.shape[0],
+                                                               _p(pi), _p(mu), _p(nu), tol,
+                                                               C.byref(out), C.byref(st))
+        return rc, out.value, st.message.decode(errors="replace")
 
     def lipschitz_bound(self, dx, dy):
         dx, dy = _f(dx), _f(dy)

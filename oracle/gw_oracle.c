@@ -464,6 +464,75 @@ static void euclid_project(const double* pi, int64_t n, int64_t m, const double*
   free(u);
 }
 
+/* dykstra_project: projections.cpp:165-187 — Dykstra's alternating Euclidean
+ * projections onto C1 (rows) and C2 (columns) with correction terms p, q;
+ * stops once marginal_error_inf(x) ≤ tol, else runtime_error. */
+int32_t gwo_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
+                            const double* nu, double tol, int32_t max_iters, double* out,
+                            int32_t* sweeps, gwb_status* st) {
+  const size_t len = (size_t)n * (size_t)m;
+  double* p = (double*)calloc(len, sizeof(double));
+  double* q = (double*)calloc(len, sizeof(double));
+  double* v = (double*)malloc(sizeof(double) * len);
+  double* y = (double*)malloc(sizeof(double) * len);
+  memcpy(out, pi, sizeof(double) * len);
+  double err = 0.0;
+  int32_t rc = GWB_ERR_RUNTIME;
+  *sweeps = 0;
+  for (int32_t sweep = 1; sweep <= max_iters; ++sweep) {
+    for (size_t k = 0; k < len; ++k) v[k] = out[k] + p[k];
+    euclid_project(v, n, m, mu, GWB_ROWS, y);
+    for (size_t k = 0; k < len; ++k) p[k] = v[k] - y[k];
+    for (size_t k = 0; k < len; ++k) v[k] = y[k] + q[k];
+    euclid_project(v, n, m, nu, GWB_COLS, out);
+    for (size_t k = 0; k < len; ++k) q[k] = v[k] - out[k];
+    *sweeps = sweep;
+    err = marginal_error_inf(out, n, m, mu, nu);
+    if (err <= tol) {
+      rc = GWB_OK;
+      break;
+    }
+  }
+  free(p);
+  free(q);
+  free(v);
+  free(y);
+  if (rc != GWB_OK)
+    return set_status(st, GWB_ERR_RUNTIME, NULL, 0,
+                      "dykstra_project did not converge in %d sweeps; final constraint "
+                      "violation %g", max_iters, err);
+  return set_status(st, GWB_OK, NULL, 0, "");
+}
+
+/* luo_tseng_residual: diagnostics.cpp:33-42 — ‖π − Proj_Π(μ,ν)(π + D_X π D_Y)‖_F
+ * with the Dykstra projection at dykstra_tol (default 1e-8, 10000 sweeps). */
+int32_t gwo_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
+                               const double* pi, const double* mu, const double* nu,
+                               double dykstra_tol, double* out, gwb_status* st) {
+  const size_t len = (size_t)n * (size_t)m;
+  double* shifted = (double*)malloc(sizeof(double) * len);
+  double* proj = (double*)malloc(sizeof(double) * len);
+  gwo_structure_product(dx, n, dy, m, pi, shifted);
+  for (size_t k = 0; k < len; ++k) shifted[k] = pi[k] + shifted[k];
+  int32_t sweeps = 0;
+  const int32_t rc = gwo_dykstra_project(shifted, n, m, mu, nu, dykstra_tol, 10000, proj,
+                                         &sweeps, st);
+  if (rc == GWB_OK) *out = fro_diff(pi, proj, len);
+  free(shifted);
+  free(proj);
+  return rc;
+}
+
+/* The optional per-record residual (solvers.cpp:202-204, 278-280, 348-350). */
+static int32_t record_residual(const gwb_config* cfg, const double* dx, int64_t n,
+                               const double* dy, int64_t m, const double* pi,
+                               const double* mu, const double* nu, gwb_record* rec,
+                               gwb_status* st) {
+  if (!cfg->record_residual) return GWB_OK;
+  rec->has_residual = 1;
+  return gwo_luo_tseng_residual(dx, n, dy, m, pi, mu, nu, 1e-8, &rec->residual, st);
+}
+
 /* bapg_solve, entropy geometry: solvers.cpp:138-217. */
 static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
                     const double* dy, int64_t m, const double* mu,
@@ -564,6 +633,8 @@ static int32_t bapg(const gwb_config* cfg, const double* dx, int64_t n,
       rec.split_gap = gwo_split_gap(pi, w, n, m);
       rec.rel_change = rel_change;
       rec.elapsed_seconds = now_seconds() - t0;
+      rc = record_residual(cfg, dx, n, dy, m, avg, mu, nu, &rec, st);
+      if (rc) goto done;
       rc = push_record(tb, &rec, st);
       if (rc) goto done;
       if (rel_change <= cfg->rel_tol) {
@@ -661,6 +732,8 @@ static int32_t ebpg(const gwb_config* cfg, const double* dx, int64_t n,
     rec.marginal_infeasibility = gwo_marginal_infeasibility(pi, n, m, mu, nu);
     rec.rel_change = rel_change;
     rec.elapsed_seconds = now_seconds() - t0;
+    rc = record_residual(cfg, dx, n, dy, m, pi, mu, nu, &rec, st);
+    if (rc) goto done;
     rc = push_record(tb, &rec, st);
     if (rc) goto done;
     if (rel_change <= cfg->rel_tol) {
@@ -744,6 +817,8 @@ static int32_t bpg(const gwb_config* cfg, const double* dx, int64_t n,
     rec.marginal_infeasibility = gwo_marginal_infeasibility(pi, n, m, mu, nu);
     rec.rel_change = rel_change;
     rec.elapsed_seconds = now_seconds() - t0;
+    rc = record_residual(cfg, dx, n, dy, m, pi, mu, nu, &rec, st);
+    if (rc) goto done;
     rc = push_record(tb, &rec, st);
     if (rc) goto done;
     if (rel_change <= cfg->rel_tol) {

@@ -58,6 +58,14 @@ double gwo_coupling_entropy(const double* pi, int64_t n, int64_t m);
 /* alignment_accuracy, tasks.cpp:202-214 (returns a gwb_code; *out in %). */
 int32_t gwo_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
                                int64_t n_gt, double* out, gwb_status* st);
+/* dykstra_project, projections.cpp:165-187; luo_tseng_residual,
+ * diagnostics.cpp:33-42 (gwb codes; GWB_ERR_RUNTIME on non-convergence). */
+int32_t gwo_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
+                            const double* nu, double tol, int32_t max_iters, double* out,
+                            int32_t* sweeps, gwb_status* st);
+int32_t gwo_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
+                               const double* pi, const double* mu, const double* nu,
+                               double dykstra_tol, double* out, gwb_status* st);
 int32_t gwo_validate_config(const gwb_config* cfg, gwb_status* st);
 int32_t gwo_solve(const gwb_config* cfg, const double* dx, int64_t n,
                   const double* dy, int64_t m, const double* mu,

@@ -257,6 +257,28 @@ int32_t gwref_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int3
   });
 }
 
+int32_t gwref_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
+                              const double* nu, double tol, int32_t max_iters, double* out,
+                              int32_t* sweeps, gwb_status* st) {
+  *sweeps = 0;  // the reference does not report the sweep count
+  return guarded(st, [&] {
+    to_col_major(gw::dykstra_project(from_col_major(pi, n, m), gw::ProbabilityVector(vec(mu, n)),
+                                     gw::ProbabilityVector(vec(nu, m)), tol, max_iters),
+                 out);
+  });
+}
+
+int32_t gwref_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
+                                 const double* pi, const double* mu, const double* nu,
+                                 double dykstra_tol, double* out, gwb_status* st) {
+  return guarded(st, [&] {
+    *out = gw::luo_tseng_residual(gw::DistanceMatrix(from_col_major(dx, n, n)),
+                                  gw::DistanceMatrix(from_col_major(dy, m, m)),
+                                  from_col_major(pi, n, m), gw::ProbabilityVector(vec(mu, n)),
+                                  gw::ProbabilityVector(vec(nu, m)), dykstra_tol);
+  });
+}
+
 // Generators (tasks.cpp) — used to pin the product's instance builders.
 int32_t gwref_gen_barabasi_albert(int32_t n, int32_t m_attach, uint64_t seed,
                                   int32_t* edges, int64_t cap, int64_t* count,

@@ -56,6 +56,7 @@ class Readout(C.Structure):
         ("marginal_infeasibility", C.c_double),
         ("entropy", C.c_double),
         ("split_gap", C.c_double),
+        ("residual", C.c_double),
         ("accuracy", C.c_double),
         ("has_accuracy", C.c_int32),
     ]
@@ -198,6 +199,11 @@ SIGNATURES = {
     "gwb_split_gap": (C.c_int32, [_D, _D, C.c_int64, C.c_int64, _D, _ST]),
     "gwb_hard_assignment": (C.c_int32, [_D, C.c_int64, C.c_int64, _I32, _ST]),
     "gwb_coupling_entropy": (C.c_int32, [_D, C.c_int64, C.c_int64, _D, _ST]),
+    "gwb_dykstra_last_stats": (C.c_int32, [C.POINTER(C.c_int32), _D]),
+    "gwb_dykstra_project": (C.c_int32, [_D, C.c_int64, C.c_int64, _D, _D, C.c_double, C.c_int32,
+                                        _D, _ST]),
+    "gwb_luo_tseng_residual": (C.c_int32, [_D, C.c_int64, _D, C.c_int64, _D, _D, _D, C.c_double,
+                                           _D, _ST]),
     "gwb_session_readout": (C.c_int32, [C.c_void_p, _I32, C.c_int64, _I32, C.POINTER(Readout),
                                         _ST]),
     "gwb_alignment_accuracy": (C.c_int32, [_I32, C.c_int64, _I32, C.c_int64, _D, _ST]),

@@ -380,7 +380,8 @@ def bapg_solve_batched(d_xs, d_ys, mus, nus, config: SolverConfig,
             recs = [IterationRecord(iter=r.iter, objective=r.objective,
                                     marginal_infeasibility=r.marginal_infeasibility,
                                     split_gap=r.split_gap, rel_change=r.rel_change,
-                                    elapsed_seconds=r.elapsed_seconds, phase=r.phase)
+                                    elapsed_seconds=r.elapsed_seconds, phase=r.phase,
+                                    residual=r.residual if r.has_residual else None)
                     for r in trace[b * cap: b * cap + int(n_rec[b])]]
         shape = lambda a: Coupling(a[sl].reshape((n, m), order="F"))
         out.append(SolveReport(final_coupling=shape(out_final), pi_half=shape(out_pi),
@@ -520,6 +521,35 @@ def coupling_entropy(pi) -> float:
     p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
     out, st = C.c_double(0), abi.Status()
     abi.load().gwb_coupling_entropy(_ptr(p), p.shape[0], p.shape[1], C.byref(out), C.byref(st))
+    abi.raise_for(st)
+    return out.value
+
+
+def dykstra_project(pi, mu: ProbabilityVector, nu: ProbabilityVector, tol: float = 1e-8,
+                    max_iters: int = 10000) -> np.ndarray:
+    """gw::dykstra_project (projections.cpp:165-187): Euclidean projection onto
+    Π(μ, ν); RuntimeError if the marginals do not reach `tol` in `max_iters`."""
+    p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
+    if p.shape != (mu.size(), nu.size()):
+        raise DimensionMismatchError("dykstra_project: shape mismatch")
+    out, st = np.empty_like(p, order="F"), abi.Status()
+    abi.load().gwb_dykstra_project(_ptr(p), p.shape[0], p.shape[1], _ptr(mu.weights()),
+                                   _ptr(nu.weights()), tol, max_iters, _ptr(out), C.byref(st))
+    abi.raise_for(st)
+    return out
+
+
+def luo_tseng_residual(d_x: DistanceMatrix, d_y: DistanceMatrix, pi, mu: ProbabilityVector,
+                       nu: ProbabilityVector, dykstra_tol: float = 1e-8) -> float:
+    """gw::luo_tseng_residual (diagnostics.cpp:33-42):
+    ‖π − dykstra_project(π + D_X π D_Y)‖_F."""
+    p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
+    if p.shape != (d_x.size(), d_y.size()):
+        raise DimensionMismatchError("luo_tseng_residual: shape mismatch")
+    out, st = C.c_double(0), abi.Status()
+    abi.load().gwb_luo_tseng_residual(_ptr(d_x.entries()), d_x.size(), _ptr(d_y.entries()),
+                                      d_y.size(), _ptr(p), _ptr(mu.weights()), _ptr(nu.weights()),
+                                      dykstra_tol, C.byref(out), C.byref(st))
     abi.raise_for(st)
     return out.value
 

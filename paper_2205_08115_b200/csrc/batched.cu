@@ -759,8 +759,16 @@ Failure batched_generic(const gwb_config* cfg, int device, int64_t batch, const 
   for (int64_t b = 0; b < batch; ++b) {
     eng.load_host(dx + b * n * n, dy + b * m * m, mu + b * n, nu + b * m);
     eng.reset(nullptr);
-    eng.run(cfg->max_iters, cfg->rel_tol);
-    const DevStatus s = eng.status();
+    std::vector<double> residuals;
+    DevStatus s;
+    if (cfg->record_residual) {  // per-record Luo-Tseng residual (solvers.cpp:202-204)
+      s = eng.run_stepped(cfg->max_iters, cfg->rel_tol, [&](int, const DevStatus&) {
+        residuals.push_back(eng.residual_of_average(1e-8));
+      });
+    } else {
+      eng.run(cfg->max_iters, cfg->rel_tol);
+      s = eng.status();
+    }
     if (s.flags) {
       if (first.problem < 0) first = Failure{base + b, s.flags, s.err_iter, s.zero_index};
       continue;
@@ -769,7 +777,12 @@ Failure batched_generic(const gwb_config* cfg, int device, int64_t batch, const 
     eng.tail();
     if (o.trace) {
       const std::vector<HostRecord> recs = eng.records(used);
-      fill_trace(o.trace + b * o.trace_cap, recs.data(), used);
+      gwb_record* t = o.trace + b * o.trace_cap;
+      fill_trace(t, recs.data(), used);
+      for (size_t k = 0; k < residuals.size() && k < static_cast<size_t>(used); ++k) {
+        t[k].residual = residuals[k];
+        t[k].has_residual = 1;
+      }
     }
     if (o.n_records) o.n_records[b] = o.trace ? used : 0;
     if (o.converged) o.converged[b] = s.converged;
@@ -797,7 +810,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   g_last_problems = 0;
   // The on-chip kernel implements the entropy geometry; the quadratic one
   // runs problem by problem on the generic engine.
-  if (n > kT || m > kT || !onchip_prec || cfg->geometry != GWB_ENTROPY) {
+  if (n > kT || m > kT || !onchip_prec || cfg->geometry != GWB_ENTROPY || cfg->record_residual) {
     const Failure f = batched_generic(cfg, device, batch, dx, n, dy, m, mu, nu, o, 0);
     if (f.problem >= 0) raise_failure(f, name_problem);
     return;

@@ -690,6 +690,8 @@ class BregmanEngine {
       GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
       GWB_CUDA(cudaStreamSynchronize(s_));
       if (h.flags) break;
+      // record_residual (solvers.cpp:278-280, 348-350), before the observer.
+      if (cfg_.record_residual && h.iter - 1 == k) residuals_.push_back(residual_of(P_[k & 1]));
       if (observer && h.iter - 1 == k) {
         to_host(P_[k & 1], 1, host_pi);
         if (observer(user, k, host_pi->data(), nullptr, n_, m_) != 0)
@@ -698,6 +700,8 @@ class BregmanEngine {
       if (h.done) break;
     }
   }
+
+  const std::vector<double>& residuals() const { return residuals_; }
 
   BState status() {
     BState h;
@@ -742,6 +746,14 @@ class BregmanEngine {
   T* keep(T* p) {
     bufs_.push_back(p);
     return p;
+  }
+
+  // luo_tseng_residual (diagnostics.cpp:33-42) of the fp32 iterate P.
+  double residual_of(const float* P) {
+    std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_));
+    double* pi64 = static_cast<double*>(o.get());
+    launch_rowmajor32_to_colmajor64(P, n_, m_, ldm_, pi64, -1, nullptr, nullptr, s_);
+    return luo_tseng_residual_dev(Dx_, ldn_, Dy_, ldm_, pi64, n_, m_, mu_, nu_, 1e-8, s_);
   }
 
   void to_host(float* P, int, std::vector<double>* out) {
@@ -920,6 +932,7 @@ class BregmanEngine {
   BState* st_;
   BRecord* rec_;
   BDev base_;
+  std::vector<double> residuals_;
   GemmPlan *g1_[2], *g1t_[2], *g2_, *g2t_;
 };
 
@@ -956,8 +969,6 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
                    const double* initial, gwb_observer observer, void* user, double* out_final,
                    gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
                    int32_t* iterations_used, const GraphInput* graphs) {
-  if (cfg->record_residual)
-    api_fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
   if (trace && trace_cap < cfg->max_iters) api_fail(GWB_ERR_CAPACITY, "trace capacity < max_iters");
   if (initial) {
     const size_t len = static_cast<size_t>(n) * m;
@@ -997,6 +1008,10 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
       o.rel_change = r[k].rel;
       o.elapsed_seconds = r[k].elapsed;
       o.phase = algo == GWB_HBPG ? r[k].phase : 0;
+      if (k <= static_cast<int>(eng.residuals().size())) {
+        o.residual = eng.residuals()[k - 1];
+        o.has_residual = 1;
+      }
     }
   }
   if (n_records) *n_records = trace ? used : 0;

@@ -203,8 +203,6 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
           const double* mu, const double* nu, const double* initial, gwb_observer observer,
           void* user, const SolveOut& o, const gwb::GraphInput* graphs) {
   const bool entropy = cfg->geometry == GWB_ENTROPY;
-  if (cfg->record_residual)
-    fail(GWB_ERR_UNSUPPORTED, "record_residual (Luo-Tseng, Dykstra) is outside the B200 path");
   const size_t len = static_cast<size_t>(n) * static_cast<size_t>(m);
   std::vector<double> w0;
   if (initial && entropy) {
@@ -234,7 +232,7 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
   // Small problems (n, m ≤ 128, product-coupling start, no observer): the
   // whole solve runs on one SM in the on-chip batched kernel (batched.cu),
   // which falls back to this engine itself for non-bf16-exact D.
-  if (!observer && !initial && !graphs && entropy && n <= 128 && m <= 128 &&
+  if (!observer && !cfg->record_residual && !initial && !graphs && entropy && n <= 128 && m <= 128 &&
       (cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_BF16X3)) {
     gwb::device_bapg_batched(cfg, 1, dx, n, dy, m, mu, nu, o.out_final, o.out_pi, o.out_w,
                              o.trace, o.trace_cap, o.n_records, o.converged, o.iterations_used,
@@ -251,22 +249,24 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
   // Quadratic: π⁰ itself goes to the device, which projects it (reset()).
   eng.reset(initial ? (entropy ? w0.data() : initial) : nullptr);
   gwb::DevStatus s;
-  if (!observer) {
+  std::vector<double> residuals;
+  if (!observer && !cfg->record_residual) {
     eng.run(cfg->max_iters, cfg->rel_tol);
     s = eng.status();
     raise_device_flags(s, "bapg");
   } else {
-    // Slow path: host-synchronous iterations so the observer sees π, w.
-    std::vector<double> hp(len), hw(len);
-    for (int k = 0; k < cfg->max_iters; ++k) {
-      eng.iterate(1, cfg->rel_tol, false);
-      s = eng.status();
-      raise_device_flags(s, "bapg");
-      eng.outputs(nullptr, hp.data(), hw.data());
-      if (observer(user, s.iter - 1, hp.data(), hw.data(), n, m) != 0)
-        fail(GWB_ERR_RUNTIME, "observer requested abort");
-      if (s.converged) break;
-    }
+    // Slow path: host-synchronous iterations so the record's Luo-Tseng
+    // residual (solvers.cpp:202-204) and then the observer (:206) see π, w.
+    std::vector<double> hp(observer ? len : 0), hw(observer ? len : 0);
+    s = eng.run_stepped(cfg->max_iters, cfg->rel_tol, [&](int k, const gwb::DevStatus&) {
+      if (cfg->record_residual) residuals.push_back(eng.residual_of_average(1e-8));
+      if (observer) {
+        eng.outputs(nullptr, hp.data(), hw.data());
+        if (observer(user, k, hp.data(), hw.data(), n, m) != 0)
+          fail(GWB_ERR_RUNTIME, "observer requested abort");
+      }
+    });
+    raise_device_flags(s, "bapg");
   }
   const int used = s.iter - 1;
   eng.tail();
@@ -282,6 +282,10 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
       r.rel_change = recs[k].rel_change;
       r.elapsed_seconds = recs[k].elapsed;
       r.phase = 0;
+      if (k < static_cast<int>(residuals.size())) {
+        r.residual = residuals[k];
+        r.has_residual = 1;
+      }
     }
   }
   if (o.n_records) *o.n_records = o.trace ? used : 0;
@@ -483,6 +487,26 @@ int32_t gwb_coupling_entropy(const double* pi, int64_t n, int64_t m, double* out
   });
 }
 
+int32_t gwb_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
+                            const double* nu, double tol, int32_t max_iters, double* out,
+                            gwb_status* st) {
+  return guarded(st, [&] {
+    if (!pi || !mu || !nu || !out) fail(GWB_ERR_INVALID, "null buffer");
+    if (n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "dykstra_project: shape mismatch");
+    gwb::device_dykstra_project(pi, n, m, mu, nu, tol, max_iters, out);
+  });
+}
+
+int32_t gwb_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
+                               const double* pi, const double* mu, const double* nu,
+                               double dykstra_tol, double* out, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!dx || !dy || !pi || !mu || !nu || !out) fail(GWB_ERR_INVALID, "null buffer");
+    if (n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "luo_tseng_residual: shape mismatch");
+    *out = gwb::device_luo_tseng_residual(dx, n, dy, m, pi, mu, nu, dykstra_tol);
+  });
+}
+
 int32_t gwb_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_t* gt,
                                int64_t n_gt, double* out, gwb_status* st) {
   return guarded(st, [&] {
@@ -505,7 +529,6 @@ int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch, const doubl
     if (!cfg) fail(GWB_ERR_CONFIG, "null config");
     require_algorithm(cfg, GWB_BAPG, "bapg_solve");
     validate_config(cfg);
-    if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual unsupported");
     if (batch < 1 || n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "empty batch or problem");
     gwb::device_bapg_batched(cfg, batch, dx, n, dy, m, mu, nu, out_final, out_pi, out_w, trace,
                              trace_cap, n_records, converged, iterations_used);
@@ -614,6 +637,7 @@ int32_t gwb_session_readout(gwb_session* s, const int32_t* ground_truth, int64_t
     out->marginal_infeasibility = r.marginal_infeasibility;
     out->entropy = r.entropy;
     out->split_gap = r.split_gap;
+    out->residual = r.residual;
     out->accuracy = r.accuracy;
     out->has_accuracy = ground_truth != nullptr;
   });

@@ -678,6 +678,8 @@ int32_t gwb_shard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t ra
       throw std::invalid_argument("gwb_shard_create: the sparse and fp32 chains are single-GPU only");
     if (cfg->geometry != GWB_ENTROPY)
       throw std::invalid_argument("gwb_shard_create: the quadratic geometry is single-GPU only");
+    if (cfg->record_residual)  // Dykstra on a row shard would need per-sweep column exchanges
+      throw std::invalid_argument("gwb_shard_create: record_residual is single-GPU only");
     auto* s = new gwb_shard();
     s->n = n;
     s->m = m;

@@ -597,6 +597,44 @@ void BapgEngine::run(int max_iters, double rel_tol) {
   parity_ = (s.iter - 1) & 1;
 }
 
+DevStatus BapgEngine::run_stepped(int max_iters, double rel_tol,
+                                  const std::function<void(int, const DevStatus&)>& after) {
+  DevStatus s = status();
+  for (int k = 0; k < max_iters; ++k) {
+    iterate(1, rel_tol, false);
+    s = status();
+    if (s.flags) return s;
+    after(s.iter - 1, s);
+    if (s.converged) break;
+  }
+  return s;
+}
+
+double BapgEngine::residual_of_average(double dykstra_tol) {
+  GWB_CUDA(cudaSetDevice(device_));
+  const size_t len = static_cast<size_t>(n_) * m_;
+  double* pi64 = dalloc<double>(stream_, len);
+  double* w64 = dalloc<double>(stream_, len);
+  double* work = dalloc<double>(stream_, static_cast<size_t>(std::max(n_, m_)));
+  // The reference's fp64 halves: K8 fix-up, then ½(π + w) (solvers.cpp:193).
+  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+  launch_rowmajor32_to_colmajor64(W_[parity_], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  launch_average64(pi64, w64, pi64, static_cast<int64_t>(len), stream_);
+  auto release = [&] {
+    for (void* p : std::initializer_list<void*>{pi64, w64, work}) dfree(p, stream_);
+  };
+  double r = 0.0;
+  try {
+    r = luo_tseng_residual_dev(Dx_, ldn_, Dy_, ldm_, pi64, n_, m_, mu64_, nu64_, dykstra_tol,
+                               stream_);
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+  return r;
+}
+
 void BapgEngine::tail() {
   GWB_CUDA(cudaSetDevice(device_));
   const BapgDev d = dev_view(parity_);
@@ -728,6 +766,16 @@ void BapgEngine::readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_h
   r->marginal_infeasibility = std::sqrt(sum_sq_diff_dev(cs, nu64_, m_, stream_)) / m_ +
                               std::sqrt(sum_sq_diff_dev(rs, mu64_, n_, stream_)) / n_;
   r->entropy = coupling_entropy_dev(fin64, static_cast<int64_t>(len), stream_);
+  // luo_tseng_residual of the final coupling; run_cell records NaN when the
+  // Dykstra projection throws (experiment.cpp:177-182).
+  try {
+    r->residual = luo_tseng_residual_dev(Dx_, ldn_, Dy_, ldm_, fin64, n_, m_, mu64_, nu64_, 1e-8,
+                                         stream_);
+  } catch (const CudaError&) {
+    throw;
+  } catch (...) {
+    r->residual = std::nan("");
+  }
   // gw_objective of the final coupling (3xTF32 chain on its fp32 copy).
   launch_colmajor64_to_rowmajor32(fin64, n_, m_, fin32, ldm_, stream_);
   r->objective = gw_objective_dev(Dx_, ldn_, Dy_, ldm_, fin32, n_, m_, stream_);

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/gwb.h"
@@ -40,6 +41,7 @@ struct HostRecord {
 // run_cell's readout of the final coupling (experiment.cpp:169-195).
 struct Readout {
   double objective = 0, marginal_infeasibility = 0, entropy = 0, split_gap = 0, accuracy = 0;
+  double residual = 0;  // NaN when Dykstra does not converge (experiment.cpp:177-182)
 };
 
 class BapgEngine {
@@ -70,6 +72,14 @@ class BapgEngine {
   int64_t iterate(int iters, double rel_tol, bool use_graph);
   // Polls convergence between chunks; returns when done or all enqueued.
   void run(int max_iters, double rel_tol);
+  // Host-stepped solve (observer / record_residual slow path): one
+  // iteration per step, after(k, status) once iteration k has executed;
+  // stops at convergence, max_iters or a device flag (returned status).
+  DevStatus run_stepped(int max_iters, double rel_tol,
+                        const std::function<void(int, const DevStatus&)>& after);
+  // luo_tseng_residual (diagnostics.cpp:33-42) of the current average
+  // ½(π + w) (solvers.cpp:202-204); raises if Dykstra does not converge.
+  double residual_of_average(double dykstra_tol);
   // Objective / row-infeasibility of the last iteration (one more chain).
   void tail();
   DevStatus status();

@@ -26,6 +26,9 @@ struct DBuf {
   explicit DBuf(size_t count) : n(count) {
     GWB_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 256));
     GWB_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 256));
+    // The memset runs on the legacy stream, which does not order with the
+    // engines' non-blocking streams: finish it before the buffer is used.
+    GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   }
   ~DBuf() {
     if (p) cudaFree(p);
@@ -433,12 +436,13 @@ void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* m
   c.down(out);
 }
 
-// −⟨D_X π D_Y, π⟩ (solvers.cpp:64-69) on device fp32 row-major operands with
-// the tcgen05 chain in 3xTF32 (splits computed here).
-double gw_objective_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int64_t ldm,
-                        const float* P_in, int64_t n, int64_t m, cudaStream_t s) {
+// G = D_X π D_Y (solvers.cpp:16-19) on device fp32 row-major operands with
+// the tcgen05 chain in 3xTF32 (splits computed here); G row-major, ld = ldm.
+void structure_product_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int64_t ldm,
+                           const float* P_in, int64_t n, int64_t m, float* G_out,
+                           cudaStream_t s) {
   DBuf<float> Dx_lo(n * ldn), Dy_lo(m * ldm), P_lo(n * ldm), Vt(m * round_up(n, 32)),
-      Vt_lo(m * round_up(n, 32)), G(n * ldm);
+      Vt_lo(m * round_up(n, 32));
   launch_tf32_aux(Dx_in, n, n, ldn, Dx_lo.p, 2, s);
   launch_tf32_aux(Dy_in, m, m, ldm, Dy_lo.p, 2, s);
   launch_tf32_aux(P_in, n, m, ldm, P_lo.p, 2, s);
@@ -453,20 +457,27 @@ double gw_objective_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int
   g2.M = n; g2.N = m; g2.K = n;
   g2.a = Dx_in; g2.a_lo = Dx_lo.p; g2.lda = ldn;
   g2.b = Vt.p; g2.b_lo = Vt_lo.p; g2.ldb = ldv;
-  g2.c = G.p; g2.ldc = ldm;
+  g2.c = G_out; g2.ldc = ldm;
   g2.three_pass = true;
   GemmPlan* p1 = gemm_plan_create(g1);
   GemmPlan* p2 = gemm_plan_create(g2);
   GWB_CUDA(gemm_launch(p1, s));
   GWB_CUDA(gemm_launch(p2, s));
+  GWB_CUDA(cudaStreamSynchronize(s));  // the DBuf temporaries are freed on return
+  gemm_plan_destroy(p1);
+  gemm_plan_destroy(p2);
+}
+
+// −⟨D_X π D_Y, π⟩ (solvers.cpp:64-69) on device fp32 row-major operands.
+double gw_objective_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int64_t ldm,
+                        const float* P_in, int64_t n, int64_t m, cudaStream_t s) {
+  DBuf<float> G(n * ldm);
+  structure_product_dev(Dx_in, ldn, Dy_in, ldm, P_in, n, m, G.p, s);
   DBuf<double> part(n);
   dot_rows_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(G.p, P_in, n, m, ldm, part.p);
   GWB_CUDA(cudaGetLastError());
   GWB_CUDA(cudaStreamSynchronize(s));
-  const double v = reduce_host(part);
-  gemm_plan_destroy(p1);
-  gemm_plan_destroy(p2);
-  return -v;
+  return -reduce_host(part);
 }
 
 double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,

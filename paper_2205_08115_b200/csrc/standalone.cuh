@@ -23,6 +23,32 @@ double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_
 double gw_objective_dev(const float* Dx, int64_t ldn, const float* Dy, int64_t ldm,
                         const float* P, int64_t n, int64_t m, cudaStream_t s);
 double coupling_entropy_dev(const double* pi_dev, int64_t len, cudaStream_t s);
+// G (row-major fp32, ld = ldm) = D_X·P·D_Y, 3xTF32 tcgen05 chain; synchronous.
+void structure_product_dev(const float* Dx, int64_t ldn, const float* Dy, int64_t ldm,
+                           const float* P, int64_t n, int64_t m, float* G, cudaStream_t s);
+
+// Dykstra projection onto Π(μ, ν) (projections.cpp:165-187) and the
+// Luo-Tseng residual (diagnostics.cpp:33-42), residual.cu.  x: column-major
+// fp64 n×m on the device, projected in place.
+struct DykstraOutcome {
+  bool converged = false;
+  int sweeps = 0;
+  double err = 0.0;
+};
+DykstraOutcome dykstra_dev(double* x, int64_t n, int64_t m, const double* mu64,
+                           const double* nu64, double tol, int max_iters, cudaStream_t s);
+// runtime_error "dykstra_project did not converge in <k> sweeps; …"
+[[noreturn]] void dykstra_fail(int max_iters, double err);
+// ‖π − Proj(π + D_X π D_Y)‖_F for a device column-major fp64 π; D_X, D_Y
+// row-major fp32.  Raises via dykstra_fail on non-convergence (10000 sweeps).
+double luo_tseng_residual_dev(const float* Dx, int64_t ldn, const float* Dy, int64_t ldm,
+                              const double* pi, int64_t n, int64_t m, const double* mu64,
+                              const double* nu64, double tol, cudaStream_t s);
+void device_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
+                            const double* nu, double tol, int32_t max_iters, double* out);
+double device_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
+                                 const double* pi, const double* mu, const double* nu,
+                                 double tol);
 double device_coupling_entropy(const double* pi, int64_t n, int64_t m);
 void device_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
                              double* out);

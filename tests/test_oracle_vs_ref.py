@@ -72,3 +72,46 @@ def test_initial_coupling_and_positivity(port, ref):
     a = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
     b = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
     assert a.code == b.code == abi.ERR_CONFIG and a.message == b.message
+
+
+# ---- Luo-Tseng residual / Dykstra (diagnostics.cpp:33-42, projections.cpp:165-187)
+
+def _residual_instance(seed=3, n=40, m=30):
+    rng = np.random.default_rng(seed)
+    dx = I.adjacency(n, I.erdos_renyi(n, 0.2, seed))
+    dy = I.adjacency(m, I.erdos_renyi(m, 0.2, seed + 1))
+    mu = rng.uniform(0.5, 1.5, n)
+    nu = rng.uniform(0.5, 1.5, m)
+    mu, nu = mu / mu.sum(), nu / nu.sum()
+    pi = np.asfortranarray(np.outer(mu, nu) * rng.uniform(0.5, 1.5, (n, m)))
+    return dx, dy, mu, nu, pi
+
+
+def test_dykstra_and_residual_match_reference(port, ref):
+    dx, dy, mu, nu, pi = _residual_instance()
+    a, b = port.dykstra_project(3.0 * pi, mu, nu), ref.dykstra_project(3.0 * pi, mu, nu)
+    assert a[0] == b[0] == 0
+    assert np.abs(a[1] - b[1]).max() <= 1e-15
+    ra, rb = port.luo_tseng_residual(dx, dy, pi, mu, nu), ref.luo_tseng_residual(dx, dy, pi, mu, nu)
+    assert ra[0] == rb[0] == 0 and ra[1] == pytest.approx(rb[1], rel=1e-12)
+    # non-convergence: runtime_error with the reference's message
+    a, b = port.dykstra_project(3.0 * pi, mu, nu, max_iters=2), ref.dykstra_project(3.0 * pi, mu, nu, max_iters=2)
+    assert a[0] == b[0] == abi.ERR_RUNTIME and a[2] == b[2]
+    assert a[2].startswith("dykstra_project did not converge in 2 sweeps; final constraint violation")
+
+
+@pytest.mark.parametrize("over", [
+    dict(algorithm=abi.BAPG, rho=0.5),
+    dict(algorithm=abi.BAPG, geometry=abi.QUADRATIC, rho=1.0),
+    dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10, switch_iters=3),
+], ids=["bapg", "bapg-quad", "hbpg"])
+def test_record_residual_matches_reference(port, ref, over):
+    dx, dy, mu, nu, _ = _residual_instance(seed=5, n=36, m=28)
+    cfg = abi.default_config(rel_tol=1e-30, max_iters=6, quiet=1, record_residual=1, **over)
+    a = port.solve(cfg, dx, dy, mu, nu)
+    b = ref.solve(cfg, dx, dy, mu, nu)
+    assert a.code == b.code == 0, (a.message, b.message)
+    assert len(a.trace) == len(b.trace) == 6
+    for x, y in zip(a.trace, b.trace):
+        assert y["residual"] is not None
+        assert x["residual"] == pytest.approx(y["residual"], rel=1e-10)

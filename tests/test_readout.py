@@ -101,3 +101,5 @@ def test_session_readout_matches_run_cell(gpu, port):
     assert out.has_accuracy == 1
     rc, acc, _ = port.alignment_accuracy(assign, gt)
     assert rc == 0 and out.accuracy == acc
+    rc, res, _ = port.luo_tseng_residual(inst.dx, inst.dy, plan, inst.mu, inst.nu)
+    assert rc == 0 and abs(out.residual - res) <= 1e-4 * res
