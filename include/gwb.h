@@ -232,6 +232,19 @@ GWB_API int32_t gwb_alignment_accuracy(const int32_t* pred, int64_t n_pred,
                                        const int32_t* gt, int64_t n_gt,
                                        double* out, gwb_status* st);
 
+/* gw::write_coupling_csv / write_coupling_csv_file (io.hpp:36-37,
+ * io.cpp:183-199): "rows,cols\n" then each row's entries as "%.17g" joined
+ * by ',' and ended by '\n' — formatted on the device (exact decimal
+ * conversion, round-half-even as glibc), only text crosses PCIe.
+ * gwb_format_coupling_csv writes into `out` (cap bytes) and sets *len to the
+ * bytes needed; out == NULL queries the size, a short buffer gives
+ * GWB_ERR_CAPACITY.  The file form fails with GWB_ERR_RUNTIME
+ * "cannot write '<path>'" as the reference. */
+GWB_API int32_t gwb_format_coupling_csv(const double* pi, int64_t n, int64_t m, char* out,
+                                        int64_t cap, int64_t* len, gwb_status* st);
+GWB_API int32_t gwb_write_coupling_csv_file(const char* path, const double* pi, int64_t n,
+                                            int64_t m, gwb_status* st);
+
 /* gw::dykstra_project (projections.hpp:46-51, projections.cpp:165-187):
  * Euclidean projection of pi onto Π(μ, ν) by Dykstra's alternating
  * projections; stops once the inf-norm marginal error ≤ tol.
@@ -324,6 +337,12 @@ typedef struct gwb_readout {
 GWB_API int32_t gwb_session_readout(gwb_session* s, const int32_t* ground_truth,
                                     int64_t n_gt, int32_t* assignment,
                                     gwb_readout* out, gwb_status* st);
+
+/* write_coupling_csv_file of the session's final coupling ½(π + w)
+ * (run_cell's `--coupling-out`, experiment.cpp; io.cpp:195-199), formatted
+ * on the device. */
+GWB_API int32_t gwb_session_write_coupling_csv(gwb_session* s, const char* path,
+                                               gwb_status* st);
 
 /* Library identity: build string including the compiled GPU arch. */
 GWB_API const char* gwb_version(void);

@@ -87,6 +87,8 @@ class Oracle:
                                                         C.c_int32, _D, _I, _ST]
         getattr(L, pre + "luo_tseng_residual").argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _D, _D,
                                                            C.c_double, _D, _ST]
+        getattr(L, pre + "format_coupling_csv").argtypes = [_D, C.c_int64, C.c_int64, C.c_char_p,
+                                                            C.c_int64, C.POINTER(C.c_int64), _ST]
         if kind == "reference":
             L.gwref_lipschitz_bound.argtypes = [_D, C.c_int64, _D, C.c_int64, _D, _ST]
             L.gwref_marginal_infeasibility.argtypes = [_D, C.c_int64, C.c_int64, _D, _D, _D, _ST]
@@ -186,6 +188,17 @@ class Oracle:
                                                                _p(pi), _p(mu), _p(nu), tol,
                                                                C.byref(out), C.byref(st))
         return rc, out.value, st.message.decode(errors="replace")
+
+    def format_coupling_csv(self, pi) -> bytes:
+        """write_coupling_csv (io.cpp:183-193) as bytes."""
+        pi = _f(pi)
+        n, m = pi.shape
+        ln, st = C.c_int64(0), abi.Status()
+        fn = getattr(self.lib, self.pre + "format_coupling_csv")
+        fn(_p(pi), n, m, None, 0, C.byref(ln), C.byref(st))
+        buf = C.create_string_buffer(max(1, ln.value))
+        fn(_p(pi), n, m, buf, ln.value, C.byref(ln), C.byref(st))
+        return buf.raw[: ln.value]
 
     def lipschitz_bound(self, dx, dy):
         dx, dy = _f(dx), _f(dy)

@@ -363,6 +363,34 @@ int32_t gwo_alignment_accuracy(const int32_t* pred, int64_t n_pred, const int32_
   return set_status(st, GWB_OK, NULL, 0, "");
 }
 
+/* write_coupling_csv: io.cpp:183-193 — "rows,cols\n", then every row as
+ * "%.17g" values joined by ',' and ended by '\n'.  *len = bytes needed; the
+ * text is written only if it fits in cap. */
+int32_t gwo_format_coupling_csv(const double* pi, int64_t n, int64_t m, char* out, int64_t cap,
+                                int64_t* len, gwb_status* st) {
+  char buf[32];
+  int64_t pos = 0;
+  const int h = snprintf(buf, sizeof(buf), "%lld,%lld\n", (long long)n, (long long)m);
+  if (out && pos + h <= cap) memcpy(out + pos, buf, (size_t)h);
+  pos += h;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      int k = 0;
+      if (j) buf[k++] = ',';
+      k += snprintf(buf + k, sizeof(buf) - (size_t)k, "%.17g", pi[IDX(i, j, n)]);
+      if (j == m - 1) buf[k++] = '\n';
+      if (out && pos + k <= cap) memcpy(out + pos, buf, (size_t)k);
+      pos += k;
+    }
+  if (m == 0)
+    for (int64_t i = 0; i < n; ++i) {
+      if (out && pos + 1 <= cap) out[pos] = '\n';
+      ++pos;
+    }
+  *len = pos;
+  return set_status(st, GWB_OK, NULL, 0, "");
+}
+
 /* validate(SolverConfig): types.cpp:176-188. */
 int32_t gwo_validate_config(const gwb_config* c, gwb_status* st) {
   if (c->rho <= 0.0) return set_status(st, GWB_ERR_CONFIG, NULL, 0, "rho must be positive");

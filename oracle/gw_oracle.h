@@ -66,6 +66,9 @@ int32_t gwo_dykstra_project(const double* pi, int64_t n, int64_t m, const double
 int32_t gwo_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,
                                const double* pi, const double* mu, const double* nu,
                                double dykstra_tol, double* out, gwb_status* st);
+/* write_coupling_csv, io.cpp:183-193 (%.17g). */
+int32_t gwo_format_coupling_csv(const double* pi, int64_t n, int64_t m, char* out, int64_t cap,
+                                int64_t* len, gwb_status* st);
 int32_t gwo_validate_config(const gwb_config* cfg, gwb_status* st);
 int32_t gwo_solve(const gwb_config* cfg, const double* dx, int64_t n,
                   const double* dy, int64_t m, const double* mu,

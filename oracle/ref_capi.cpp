@@ -9,11 +9,13 @@
 // Nothing here is shipped in the product library.
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
 #include "../include/gwb.h"
 #include "gw/diagnostics.hpp"
+#include "gw/io.hpp"
 #include "gw/projections.hpp"
 #include "gw/solvers.hpp"
 #include "gw/tasks.hpp"
@@ -276,6 +278,19 @@ int32_t gwref_luo_tseng_residual(const double* dx, int64_t n, const double* dy, 
                                   gw::DistanceMatrix(from_col_major(dy, m, m)),
                                   from_col_major(pi, n, m), gw::ProbabilityVector(vec(mu, n)),
                                   gw::ProbabilityVector(vec(nu, m)), dykstra_tol);
+  });
+}
+
+// write_coupling_csv (io.cpp:183-193) into a caller buffer; *len = bytes
+// needed (the text is written only if it fits in cap).
+int32_t gwref_format_coupling_csv(const double* pi, int64_t n, int64_t m, char* out, int64_t cap,
+                                  int64_t* len, gwb_status* st) {
+  return guarded(st, [&] {
+    std::ostringstream os;
+    gw::write_coupling_csv(os, from_col_major(pi, n, m));
+    const std::string s = os.str();
+    *len = static_cast<int64_t>(s.size());
+    if (out && cap >= *len) std::memcpy(out, s.data(), s.size());
   });
 }
 

@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     Graph, IterationRecord, NumericalInstabilityError, adjacency_distance, ProbabilityVector, SinkhornResult,
     SolveOptions, SolveReport, SolverConfig, UnsupportedError, ZeroSumLineError, bapg_solve,
     alignment_accuracy, bapg_solve_batched, coupling_entropy, dykstra_project, luo_tseng_residual,
+    format_coupling_csv, write_coupling_csv_file,
     bpg_solve, ebpg_solve, gw_objective, hard_assignment, hbpg_solve, kl_scale, lipschitz_bound,
     marginal_infeasibility, product_coupling, sinkhorn_project, sinkhorn_project_log, solve,
     split_gap, validate, validate_inputs, version)

@@ -199,6 +199,10 @@ SIGNATURES = {
     "gwb_split_gap": (C.c_int32, [_D, _D, C.c_int64, C.c_int64, _D, _ST]),
     "gwb_hard_assignment": (C.c_int32, [_D, C.c_int64, C.c_int64, _I32, _ST]),
     "gwb_coupling_entropy": (C.c_int32, [_D, C.c_int64, C.c_int64, _D, _ST]),
+    "gwb_format_coupling_csv": (C.c_int32, [_D, C.c_int64, C.c_int64, C.c_char_p, C.c_int64,
+                                            C.POINTER(C.c_int64), _ST]),
+    "gwb_write_coupling_csv_file": (C.c_int32, [C.c_char_p, _D, C.c_int64, C.c_int64, _ST]),
+    "gwb_session_write_coupling_csv": (C.c_int32, [C.c_void_p, C.c_char_p, _ST]),
     "gwb_dykstra_last_stats": (C.c_int32, [C.POINTER(C.c_int32), _D]),
     "gwb_dykstra_project": (C.c_int32, [_D, C.c_int64, C.c_int64, _D, _D, C.c_double, C.c_int32,
                                         _D, _ST]),

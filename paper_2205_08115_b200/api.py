@@ -554,6 +554,29 @@ def luo_tseng_residual(d_x: DistanceMatrix, d_y: DistanceMatrix, pi, mu: Probabi
     return out.value
 
 
+def format_coupling_csv(pi) -> bytes:
+    """gw::write_coupling_csv (io.cpp:183-193) as bytes, formatted on the device."""
+    p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
+    n, m = p.shape
+    ln, st = C.c_int64(0), abi.Status()
+    lib = abi.load()
+    lib.gwb_format_coupling_csv(_ptr(p), n, m, None, 0, C.byref(ln), C.byref(st))
+    abi.raise_for(st)
+    buf = C.create_string_buffer(max(1, ln.value))
+    lib.gwb_format_coupling_csv(_ptr(p), n, m, buf, ln.value, C.byref(ln), C.byref(st))
+    abi.raise_for(st)
+    return buf.raw[: ln.value]
+
+
+def write_coupling_csv_file(path: str, pi) -> None:
+    """gw::write_coupling_csv_file (io.cpp:195-199)."""
+    p = _f64(pi.entries() if isinstance(pi, Coupling) else pi)
+    st = abi.Status()
+    abi.load().gwb_write_coupling_csv_file(str(path).encode(), _ptr(p), p.shape[0], p.shape[1],
+                                           C.byref(st))
+    abi.raise_for(st)
+
+
 def alignment_accuracy(pred, ground_truth) -> float:
     """gw::alignment_accuracy (tasks.cpp:202-214), percent."""
     a = np.ascontiguousarray(pred, dtype=np.int32)

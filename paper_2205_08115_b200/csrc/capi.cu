@@ -487,6 +487,44 @@ int32_t gwb_coupling_entropy(const double* pi, int64_t n, int64_t m, double* out
   });
 }
 
+int32_t gwb_format_coupling_csv(const double* pi, int64_t n, int64_t m, char* out, int64_t cap,
+                                int64_t* len, gwb_status* st) {
+  return guarded(st, [&] {
+    if ((!pi && n * m > 0) || !len) fail(GWB_ERR_INVALID, "null buffer");
+    if (n < 0 || m < 0) fail(GWB_ERR_DIMENSION, "negative shape");
+    int64_t pos = 0;
+    gwb::device_coupling_csv(pi, n, m, [&](const char* b, int64_t k) {
+      if (out && pos + k <= cap) std::memcpy(out + pos, b, static_cast<size_t>(k));
+      pos += k;
+    }, len);
+    if (out && cap < *len)
+      fail(GWB_ERR_CAPACITY, fmt("buffer of %lld bytes < %lld needed", static_cast<long long>(cap),
+                                 static_cast<long long>(*len)));
+  });
+}
+
+int32_t gwb_write_coupling_csv_file(const char* path, const double* pi, int64_t n, int64_t m,
+                                    gwb_status* st) {
+  return guarded(st, [&] {
+    if (!path || (!pi && n * m > 0)) fail(GWB_ERR_INVALID, "null buffer");
+    if (n < 0 || m < 0) fail(GWB_ERR_DIMENSION, "negative shape");
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) fail(GWB_ERR_RUNTIME, std::string("cannot write '") + path + "'");  // io.cpp:197
+    int64_t total = 0;
+    bool ok = true;
+    try {
+      gwb::device_coupling_csv(pi, n, m, [&](const char* b, int64_t k) {
+        ok = ok && std::fwrite(b, 1, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+      }, &total);
+    } catch (...) {
+      std::fclose(f);
+      throw;
+    }
+    ok = std::fclose(f) == 0 && ok;
+    if (!ok) fail(GWB_ERR_RUNTIME, std::string("cannot write '") + path + "'");
+  });
+}
+
 int32_t gwb_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
                             const double* nu, double tol, int32_t max_iters, double* out,
                             gwb_status* st) {
@@ -640,6 +678,25 @@ int32_t gwb_session_readout(gwb_session* s, const int32_t* ground_truth, int64_t
     out->residual = r.residual;
     out->accuracy = r.accuracy;
     out->has_accuracy = ground_truth != nullptr;
+  });
+}
+
+int32_t gwb_session_write_coupling_csv(gwb_session* s, const char* path, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!s || !path) fail(GWB_ERR_INVALID, "null session or path");
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) fail(GWB_ERR_RUNTIME, std::string("cannot write '") + path + "'");
+    bool ok = true;
+    try {
+      s->eng->final_csv([&](const char* b, int64_t k) {
+        ok = ok && std::fwrite(b, 1, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+      });
+    } catch (...) {
+      std::fclose(f);
+      throw;
+    }
+    ok = std::fclose(f) == 0 && ok;
+    if (!ok) fail(GWB_ERR_RUNTIME, std::string("cannot write '") + path + "'");
   });
 }
 

@@ -635,6 +635,28 @@ double BapgEngine::residual_of_average(double dykstra_tol) {
   return r;
 }
 
+int64_t BapgEngine::final_csv(const std::function<void(const char*, int64_t)>& sink) {
+  GWB_CUDA(cudaSetDevice(device_));
+  const DevStatus s = status();
+  const int par = s.iter >= 1 ? (s.iter - 1) & 1 : parity_;  // buffer holding the current w
+  const size_t len = static_cast<size_t>(n_) * m_;
+  double* pi64 = dalloc<double>(stream_, len);
+  double* w64 = dalloc<double>(stream_, len);
+  double* work = dalloc<double>(stream_, static_cast<size_t>(std::max(n_, m_)));
+  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+  launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  launch_average64(pi64, w64, pi64, static_cast<int64_t>(len), stream_);
+  int64_t total = 0;
+  try {
+    total = coupling_csv_dev(pi64, n_, m_, stream_, sink);
+  } catch (...) {
+    for (void* p : std::initializer_list<void*>{pi64, w64, work}) dfree(p, stream_);
+    throw;
+  }
+  for (void* p : std::initializer_list<void*>{pi64, w64, work}) dfree(p, stream_);
+  return total;
+}
+
 void BapgEngine::tail() {
   GWB_CUDA(cudaSetDevice(device_));
   const BapgDev d = dev_view(parity_);

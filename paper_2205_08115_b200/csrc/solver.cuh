@@ -80,6 +80,9 @@ class BapgEngine {
   // luo_tseng_residual (diagnostics.cpp:33-42) of the current average
   // ½(π + w) (solvers.cpp:202-204); raises if Dykstra does not converge.
   double residual_of_average(double dykstra_tol);
+  // write_coupling_csv of the final coupling ½(π + w) (K8 fix-up first),
+  // formatted on the device and streamed to `sink`; returns the byte count.
+  int64_t final_csv(const std::function<void(const char*, int64_t)>& sink);
   // Objective / row-infeasibility of the last iteration (one more chain).
   void tail();
   DevStatus status();

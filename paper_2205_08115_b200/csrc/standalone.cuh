@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/gwb.h"
@@ -44,6 +45,14 @@ DykstraOutcome dykstra_dev(double* x, int64_t n, int64_t m, const double* mu64,
 double luo_tseng_residual_dev(const float* Dx, int64_t ldn, const float* Dy, int64_t ldm,
                               const double* pi, int64_t n, int64_t m, const double* mu64,
                               const double* nu64, double tol, cudaStream_t s);
+// write_coupling_csv (io.cpp:183-193) of a device column-major fp64 n×m
+// coupling, formatted on the device ("%.17g") and streamed to `sink` in
+// row blocks; returns the total byte count (csv.cu).
+int64_t coupling_csv_dev(const double* pi, int64_t n, int64_t m, cudaStream_t s,
+                         const std::function<void(const char*, int64_t)>& sink);
+void device_coupling_csv(const double* pi, int64_t n, int64_t m,
+                         const std::function<void(const char*, int64_t)>& sink,
+                         int64_t* total);
 void device_dykstra_project(const double* pi, int64_t n, int64_t m, const double* mu,
                             const double* nu, double tol, int32_t max_iters, double* out);
 double device_luo_tseng_residual(const double* dx, int64_t n, const double* dy, int64_t m,

@@ -115,3 +115,23 @@ def test_record_residual_matches_reference(port, ref, over):
     for x, y in zip(a.trace, b.trace):
         assert y["residual"] is not None
         assert x["residual"] == pytest.approx(y["residual"], rel=1e-10)
+
+
+# ---- write_coupling_csv (io.cpp:183-193)
+
+def csv_cases():
+    rng = np.random.default_rng(17)
+    big = rng.standard_normal((9, 7)) * 10.0 ** rng.integers(-320, 300, (9, 7))
+    big.flat[:12] = [0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 2.2250738585072014e-308,
+                     1.7976931348623157e308, 0.0001, 0.00001, 1e16, 1e17]
+    # exact ties at the 17th digit: odd k · 2^-2 with 16 integer digits
+    k = rng.integers(4 * 10**15, 9 * 10**15, 20) | 1
+    ties = (k.astype(np.float64) / 4.0).reshape(4, 5)
+    unit = rng.random((6, 11))
+    return [big, ties, unit, np.ones((1, 1)), np.zeros((3, 0)), np.full((2, 3), 0.1)]
+
+
+def test_coupling_csv_matches_reference(port, ref):
+    for a in csv_cases():
+        a = np.asfortranarray(a)
+        assert port.format_coupling_csv(a) == ref.format_coupling_csv(a)
