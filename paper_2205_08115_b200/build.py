@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 SOURCES = ["gemm.cu", "kernels.cu", "solver.cu", "standalone.cu", "bregman.cu", "shard.cu",
-           "batched.cu", "sparse.cu", "skinny.cu", "quadratic.cu", "residual.cu", "csv.cu", "capi.cu", "instances.cpp"]
+           "batched.cu", "sparse.cu", "skinny.cu", "skinny_tc.cu", "quadratic.cu", "residual.cu", "csv.cu", "capi.cu", "instances.cpp"]
 
 
 def _nvcc() -> str:

@@ -455,6 +455,11 @@ CUtensorMap make_map_blocked(const void* ptr, int64_t rows, int64_t block_k, int
 
 }  // namespace
 
+CUtensorMap gemm_tensor_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                            int esize) {
+  return make_map(ptr, rows, cols, ld, box_rows, esize);
+}
+
 struct GemmPlan {
   GemmParams params;
   int grid = 0;

@@ -63,6 +63,12 @@ struct GemmDesc {
   int split_k = 0;
 };
 
+// 2-D TMA descriptor of a row-major rows×cols matrix (leading dim ld
+// elements; esize 4 = fp32, 2 = bf16), box = box_rows × 128 B, 128-B swizzle,
+// zero fill out of bounds.
+CUtensorMap gemm_tensor_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                            int esize);
+
 // Opaque, pre-encoded launch (TMA descriptors built once, reusable in graphs).
 struct GemmPlan;
 

@@ -12,6 +12,7 @@
 // Sums are fp32 in a fixed order (deterministic, no operand splitting).
 #include "skinny.cuh"
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace gwb {
@@ -26,10 +27,15 @@ constexpr int kWarps = 8;
 constexpr int kRows = kRowsPerWarp * kWarps;  // rows of C per CTA
 constexpr int kChunk = 256;                  // K rows of B staged per step
 
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
 template <int NQ>
 __global__ void __launch_bounds__(kWarps * 32) skinny_kernel(
     const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
-    float* __restrict__ C, int64_t ldc, int64_t M, int N, int64_t K, const int* skip) {
+    float* __restrict__ C, int64_t ldc, int64_t M, int N, int64_t K, const int* skip,
+    uint16_t* __restrict__ planes, int nplanes, int64_t ldp, int64_t pstride) {
   if (skip && *skip) return;
   constexpr int NP = NQ * 4;
   __shared__ __align__(16) float bs[kChunk][NP];
@@ -102,7 +108,18 @@ __global__ void __launch_bounds__(kWarps * 32) skinny_kernel(
         v[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
       }
     }
-    if (rok[r] && lane < N) C[(row0 + r) * ldc + lane] = v[0];
+    if (rok[r] && lane < N) {
+      if (planes) {  // transposed bf16 split planes of the result
+        float x = v[0];
+        for (int q = 0; q < nplanes; ++q) {
+          const float h = __bfloat162float(__float2bfloat16_rn(x));
+          planes[q * pstride + lane * ldp + row0 + r] = bf16_bits(h);
+          x -= h;
+        }
+      } else {
+        C[(row0 + r) * ldc + lane] = v[0];
+      }
+    }
   }
 }
 
@@ -125,13 +142,16 @@ void launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds,
   check_cuda(cudaGetLastError(), "transpose_kernel");
 }
 
-void launch_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
-                   int64_t M, int N, int64_t K, const int* skip, cudaStream_t s) {
+namespace {
+void skinny_dispatch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                     int64_t ldc, int64_t M, int N, int64_t K, const int* skip, uint16_t* planes,
+                     int nplanes, int64_t ldp, int64_t pstride, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((M + kRows - 1) / kRows);
   const int nq = (N + 3) / 4;
 #define GWB_SKINNY(Q) \
   case Q:             \
-    skinny_kernel<Q><<<grid, kWarps * 32, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K, skip); \
+    skinny_kernel<Q><<<grid, kWarps * 32, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K, skip, planes, \
+                                                  nplanes, ldp, pstride);                     \
     break;
   switch (nq) {
     GWB_SKINNY(1)
@@ -147,6 +167,19 @@ void launch_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, flo
   }
 #undef GWB_SKINNY
   check_cuda(cudaGetLastError(), "skinny_kernel");
+}
+}  // namespace
+
+void launch_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                   int64_t M, int N, int64_t K, const int* skip, cudaStream_t s) {
+  skinny_dispatch(A, lda, B, ldb, C, ldc, M, N, K, skip, nullptr, 0, 0, 0, s);
+}
+
+void launch_skinny_planes(const float* A, int64_t lda, const float* B, int64_t ldb, void* planes,
+                          int nplanes, int64_t ldp, int64_t pstride, int64_t M, int N, int64_t K,
+                          const int* skip, cudaStream_t s) {
+  skinny_dispatch(A, lda, B, ldb, nullptr, 0, M, N, K, skip, static_cast<uint16_t*>(planes),
+                  nplanes, ldp, pstride, s);
 }
 
 }  // namespace gwb

@@ -119,6 +119,8 @@ BapgEngine::~BapgEngine() {
   gemm_plan_destroy(g2_tail_);
   csr_free(cx_);
   csr_free(cy_);
+  skinny_tc_plan_destroy(stc_, stream_);
+  skinny_tc_plan_destroy(stc_tail_, stream_);
   dfree(Vs_, stream_);
   dfree(DyT_, stream_);
   for (void* p : std::initializer_list<void*>{
@@ -222,9 +224,35 @@ void BapgEngine::prepare_d() {
   dfree(d_inexact, stream_);
   dx_exact_ = (h_inexact[0] & 1) == 0;
   dy_exact_ = (h_inexact[1] & 1) == 0;
-  // Skinny problems (m ≤ 32, config 3): the FP32-pipe chain (skinny.cu).
-  // An explicit GWB_PREC_FP32 with larger m resolves like AUTO.
+  // Skinny problems (m ≤ 32, config 3).  With an exact-bf16 D_X (0/1
+  // graphs) AUTO / BF16X3 run the bf16x3 chain as FP32-pipe GEMM1 (K = m)
+  // writing Vᵀ planes + tensor-core GEMM2 streaming D_X (skinny_tc.cu);
+  // otherwise AUTO takes the FP32-pipe chain (skinny.cu).  An explicit
+  // GWB_PREC_FP32 with larger m resolves like AUTO.
   if (precision_ == GWB_PREC_FP32 && m_ > kSkinnyMaxN) precision_ = GWB_PREC_AUTO;
+  skinny_tc_plan_destroy(stc_, stream_);
+  skinny_tc_plan_destroy(stc_tail_, stream_);
+  stc_ = stc_tail_ = nullptr;
+  skinny_tc_ = false;
+  if (m_ <= kSkinnyMaxN && (h_inexact[0] & 2) == 0 &&
+      (precision_ == GWB_PREC_AUTO || precision_ == GWB_PREC_BF16X3)) {
+    destroy_graphs();
+    precision_ = GWB_PREC_BF16X3;
+    skinny_tc_ = true;
+    if (!DyT_) DyT_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
+    launch_transpose(Dy_, m_, m_, ldm_, DyT_, ldm_, stream_);
+    if (!Dx_bf_) Dx_bf_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_ / 2 + 16);
+    launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
+    if (!Vt_aux_) Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
+    const void* vt[3];
+    for (int k = 0; k < 3; ++k) vt[k] = reinterpret_cast<uint16_t*>(Vt_aux_) + k * m_ * ldn_;
+    stc_ = skinny_tc_plan_create(Dx_bf_, ldn_, vt, 3, ldn_, G_, ldm_, n_, static_cast<int>(m_), n_,
+                                 &st_->done, stream_);
+    stc_tail_ = skinny_tc_plan_create(Dx_bf_, ldn_, vt, 3, ldn_, G_, ldm_, n_,
+                                      static_cast<int>(m_), n_, &st_->flags, stream_);
+    GWB_CUDA(cudaStreamSynchronize(stream_));
+    return;
+  }
   if (precision_ == GWB_PREC_AUTO && m_ <= kSkinnyMaxN) precision_ = GWB_PREC_FP32;
   if (precision_ == GWB_PREC_FP32) {
     destroy_graphs();
@@ -491,6 +519,11 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
     // Uᵀ = (D_X·X)ᵀ, then G = (D_Y·Uᵀ)ᵀ: two CSR row-gathers (sparse.cu).
     launch_rowgather(cx_, half_b ? P_ : W_[q], ldm_, m_, Vt_, ldn_, true, &st_->done, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->done, stream_);
+  } else if (skinny_tc_) {
+    // Vᵀ planes = (X·D_Yᵀ)ᵀ on the FP32 pipes, then G = D_X·V on the tensor cores.
+    launch_skinny_planes(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vt_aux_, 3, ldn_, m_ * ldn_, n_,
+                         static_cast<int>(m_), m_, &st_->done, stream_);
+    skinny_tc_launch(stc_, stream_);
   } else if (fp32()) {
     // V = X·D_Yᵀ, then G = D_X·V on the FP32 pipes (skinny.cu).
     launch_skinny(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vs_, ldm_, n_, static_cast<int>(m_), m_,
@@ -663,6 +696,10 @@ void BapgEngine::tail() {
   if (sparse()) {
     launch_rowgather(cx_, W_[parity_], ldm_, m_, Vt_, ldn_, true, &st_->flags, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->flags, stream_);
+  } else if (skinny_tc_) {
+    launch_skinny_planes(W_[parity_], ldm_, DyT_, ldm_, Vt_aux_, 3, ldn_, m_ * ldn_, n_,
+                         static_cast<int>(m_), m_, &st_->flags, stream_);
+    skinny_tc_launch(stc_tail_, stream_);
   } else if (fp32()) {
     launch_skinny(W_[parity_], ldm_, DyT_, ldm_, Vs_, ldm_, n_, static_cast<int>(m_), m_,
                   &st_->flags, stream_);

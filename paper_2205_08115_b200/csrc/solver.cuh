@@ -136,7 +136,12 @@ class BapgEngine {
   bool bf16() const { return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2; }
   bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
   bool fp32() const { return precision_ == GWB_PREC_FP32; }
-  bool no_planes() const { return sparse() || fp32(); }  // chains read the fp32 iterates
+  // Skinny bf16x3 chain (m ≤ 32, exact-bf16 D_X): FP32-pipe GEMM1 writing
+  // Vᵀ planes, tensor-core GEMM2 (skinny_tc.cu).
+  bool skinny_tc_ = false;
+  SkinnyTcPlan* stc_ = nullptr;       // skip on done
+  SkinnyTcPlan* stc_tail_ = nullptr;  // skip on flags
+  bool no_planes() const { return sparse() || fp32() || skinny_tc_; }  // chains read the fp32 iterates
   int aux_mode() const {
     return precision_ == GWB_PREC_TF32 ? 1
            : precision_ == GWB_PREC_BF16X3 ? 3

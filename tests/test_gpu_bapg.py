@@ -87,7 +87,9 @@ def test_bapg_marginal_invariants(gpu):
 
 @pytest.mark.parametrize("precision", ["auto", "fp32"])
 def test_bapg_skinny_partition(gpu, port, precision):
-    # c3 shape class (m ≤ 32): AUTO runs the FP32-pipe chain (csrc/skinny.cu).
+    # c3 shape class (m ≤ 32): AUTO runs the skinny bf16x3 chain (FP32-pipe
+    # GEMM1 → tensor-core GEMM2 with split-K, csrc/skinny_tc.cu) for a 0/1
+    # D_X; "fp32" forces the FP32-pipe chain (csrc/skinny.cu).
     inst = I.config3(seed=2, n=700, k=20)
     rep, o = run_both(port, inst, precision, max_iters=50)
     assert rep.iterations_used == o.iterations_used
@@ -98,14 +100,35 @@ def test_bapg_skinny_partition(gpu, port, precision):
     check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
 
 
-def test_bapg_skinny_ragged_k(gpu, port):
-    # every N class of the skinny kernel's dispatch (m = 1, 5, 13, 32)
-    for k in (1, 5, 13, 32):
-        inst = I.config3(seed=k, n=300, k=k)
-        rep, o = run_both(port, inst, "auto", max_iters=20)
+@pytest.mark.parametrize("precision", ["auto", "fp32"])
+def test_bapg_skinny_ragged_k(gpu, port, precision):
+    # every N class of the skinny kernels' dispatch (m = 1, 5, 13, 32),
+    # ragged n (row tiles and k-blocks with tails)
+    for k, n in ((1, 300), (5, 333), (13, 129), (32, 517)):
+        inst = I.config3(seed=k, n=n, k=k)
+        rep, o = run_both(port, inst, precision, max_iters=20)
         assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL, k
         obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
         assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref), k
+
+
+def test_bapg_skinny_full_c3(gpu, port):
+    # BASELINE c3 at full size (n = 4000, K = 20): 32 row tiles × 4 K splits.
+    inst = I.config3()
+    rep, o = run_both(port, inst, "auto", max_iters=30)
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+    check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
+
+
+def test_bapg_skinny_weighted_d_takes_fp32_pipes(gpu, port):
+    # m ≤ 32 with a non-bf16-exact D_X (Euclidean): AUTO keeps the FP32 chain.
+    g = I.config2(seed=5, n=300, m=24)
+    rep, o = run_both(port, g, "auto", max_iters=20)
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
 
 
 def test_concurrent_solves_are_reentrant_and_deterministic(gpu):
