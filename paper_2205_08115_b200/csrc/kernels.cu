@@ -84,6 +84,69 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   }
 }
 
+// Narrow rows (m ≤ 128, e.g. config 3): one warp per row, 8 rows per CTA.
+// Lane l covers columns [4l, 4l+4) exactly as thread l does in the CTA-per-row
+// kernel, where only warp 0 holds data at this width — the shuffles and
+// merges are the same, so the results are bitwise identical.
+constexpr int kNarrowM = 128;
+constexpr int kWarpRows = kRowThreads / 32;
+
+__global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d, int write, int tail) {
+  if (tail ? d.st->flags != 0 : d.st->done != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
+  if (i >= d.n) return;
+  const float* g = d.G + i * d.ld;
+  const float* w = d.W + i * d.ld;
+  const int64_t m = d.m;
+  const float inv_rho = d.inv_rho;
+  const int64_t j = lane * 4;
+  MaxSum ms{-INFINITY, 0.f};
+  double sums[2] = {0.0, 0.0};
+  float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), w4 = g4;
+  if (j < m) {
+    g4 = *reinterpret_cast<const float4*>(g + j);
+    w4 = *reinterpret_cast<const float4*>(w + j);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < m) {
+        ms_add(ms, gv[q] * inv_rho, wv[q]);
+        sums[0] += static_cast<double>(gv[q]) * wv[q];
+        sums[1] += wv[q];
+      }
+    }
+  }
+  ms = warp_merge(ms);
+  sums[0] = warp_sum(sums[0]);
+  sums[1] = warp_sum(sums[1]);
+  if (lane == 0) {
+    d.row_part[i].gw = sums[0];
+    const double dev = sums[1] - d.mu64[i];
+    d.row_part[i].rowdev = dev * dev;
+  }
+  if (!write) return;
+  const float S = ms.s;
+  const float r = ms.mx;
+  if (lane == 0) {
+    if (r > 700.0f) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (!(S > 0.0f) || !isfinite(S) || isnan(r)) {
+      atomicOr(&d.st->flags, kFlagZeroA);
+      atomicMin(&d.st->zero_index, static_cast<int>(i));
+    }
+  }
+  if (j >= m) return;
+  const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
+  float4 o;
+  o.x = (j + 0 < m) ? scale * w4.x * __expf(g4.x * inv_rho - r) : 0.f;
+  o.y = (j + 1 < m) ? scale * w4.y * __expf(g4.y * inv_rho - r) : 0.f;
+  o.z = (j + 2 < m) ? scale * w4.z * __expf(g4.z * inv_rho - r) : 0.f;
+  o.w = (j + 3 < m) ? scale * w4.w * __expf(g4.w * inv_rho - r) : 0.f;
+  *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
+  if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
+}
+
 // ---------------------------------------------------------------------------
 // Half-step b, pass 1: per (row chunk, 128-column block) partials.
 // ---------------------------------------------------------------------------
@@ -220,6 +283,62 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
     atomicOr(&d.st->flags, kFlagNonFinite);
   if (threadIdx.x == 0) {
+    ColWritePart& c = d.cw_part[i];
+    c.gw = sums[0];
+    c.split = sums[1];
+    c.diff = sums[2];
+    c.wold = sums[3];
+    c.gp = sums[4];
+  }
+}
+
+// col_write for narrow rows (m ≤ 128): one warp per row, as row_update_warps.
+__global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d) {
+  if (d.st->done) return;
+  if (d.st->flags != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
+  if (i >= d.n) return;
+  const int64_t m = d.m;
+  const int64_t j = lane * 4;
+  const float inv_rho = d.inv_rho;
+  double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
+  bool finite = true;
+  if (j < m) {
+    const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + j);
+    const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + j);
+    const float4 w4 = *reinterpret_cast<const float4*>(d.W + i * d.ld + j);
+    const float4 cm = *reinterpret_cast<const float4*>(d.col_max + j);
+    const float4 cs = *reinterpret_cast<const float4*>(d.col_scale + j);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+    const float mv[4] = {cm.x, cm.y, cm.z, cm.w};
+    const float sv[4] = {cs.x, cs.y, cs.z, cs.w};
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < m) {
+        o[q] = sv[q] * pv[q] * __expf(gv[q] * inv_rho - mv[q]);
+        finite = finite && isfinite(o[q]);
+        sums[0] += static_cast<double>(gv[q]) * o[q];
+        const double sp = static_cast<double>(pv[q]) - o[q];
+        sums[1] += sp * sp;
+        const double df = static_cast<double>(o[q]) - wv[q];
+        sums[2] += df * df;
+        sums[3] += static_cast<double>(wv[q]) * wv[q];
+        sums[4] += static_cast<double>(gv[q]) * pv[q];
+      } else {
+        o[q] = 0.f;
+      }
+    }
+    *reinterpret_cast<float4*>(d.W_new + i * d.ld + j) = make_float4(o[0], o[1], o[2], o[3]);
+    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3]);
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) sums[q] = warp_sum(sums[q]);
+  if (!__all_sync(0xffffffffu, finite ? 1 : 0) && lane == 0) atomicOr(&d.st->flags, kFlagNonFinite);
+  if (lane == 0) {
     ColWritePart& c = d.cw_part[i];
     c.gw = sums[0];
     c.split = sums[1];
@@ -443,8 +562,21 @@ inline unsigned grid1d(int64_t work, int threads) {
 
 }  // namespace
 
+namespace {
+void launch_col_write_pass(const BapgDev& d, cudaStream_t s) {
+  if (d.m <= kNarrowM)
+    col_write_warps_kernel<<<static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows), kRowThreads,
+                             0, s>>>(d);
+  else
+    col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+}
+}  // namespace
+
 void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
-  if (d.n >= 1)
+  if (d.n >= 1 && d.m <= kNarrowM)
+    row_update_warps_kernel<<<static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows), kRowThreads,
+                              0, s>>>(d, write ? 1 : 0, write ? 0 : 1);
+  else if (d.n >= 1)
     row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
                                                                          write ? 0 : 1);
   if (write) flag_check_kernel<<<1, 1, 0, s>>>(d.st);
@@ -457,7 +589,7 @@ void launch_col_update(const BapgDev& d, cudaStream_t s) {
   col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
   col_combine_kernel<<<grid1d(d.m * 32, 256), 256, 0, s>>>(d);
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
-  col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+  launch_col_write_pass(d, s);
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 
@@ -471,7 +603,7 @@ void launch_col_partial(const BapgDev& d, cudaStream_t s) {
 
 void launch_col_write(const BapgDev& d, cudaStream_t s) {
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
-  if (d.n >= 1) col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+  if (d.n >= 1) launch_col_write_pass(d, s);
   flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 

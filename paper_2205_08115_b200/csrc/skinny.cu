@@ -131,6 +131,62 @@ __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, in
   dst[c * ldd + r] = src[r * lds + c];
 }
 
+// Small-K product with transposed bf16-plane output (GEMM1 of the skinny
+// bf16x3 chain, K = N = m ≤ 32): one CTA per 32 rows of C, lane = row, the 8
+// warps splitting the N output columns (the per-column FMA chains are the
+// latency; a single warp per row block ran 4k dependent instructions).  The
+// 32×K block of A is read coalesced (lane = k) into a padded shared tile, B
+// (K×N ≤ 4 KB) is staged alongside; each lane sums over k in order and
+// writes the split planes of Cᵀ — at a fixed column, 32 consecutive rows.
+constexpr int kSmallKWarps = 8;
+__global__ void __launch_bounds__(32 * kSmallKWarps) small_k_planes_kernel(
+    const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t M,
+    int N, int K, const int* skip, uint16_t* __restrict__ planes, int nplanes, int64_t ldp,
+    int64_t pstride) {
+  if (skip && *skip) return;
+  __shared__ float bs[32][32];
+  __shared__ float at[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+  // Warp w stages rows / k-rows w, w+8, w+16, w+24: 8 loads in flight per lane.
+  float bv[4], av[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int k = warp + kSmallKWarps * t;
+    bv[t] = (k < K && lane < N) ? B[static_cast<int64_t>(k) * ldb + lane] : 0.f;
+    av[t] = (r0 + k < M && lane < K) ? A[(r0 + k) * lda + lane] : 0.f;
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    bs[warp + kSmallKWarps * t][lane] = bv[t];
+    at[warp + kSmallKWarps * t][lane] = av[t];
+  }
+  __syncthreads();
+  const int64_t row = r0 + lane;
+  float a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = at[lane][k];
+  for (int c = warp; c < N; c += kSmallKWarps) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < K) acc = fmaf(a[k], bs[k][c], acc);
+    if (row < M) {
+      // ldp == 0: the skinny GEMM2's packed operand — per 64-row k-block, a
+      // 32 × 128-B tile in the 128-B swizzle layout (skinny_tc.cu).
+      const int64_t off = ldp ? static_cast<int64_t>(c) * ldp + row
+                              : (row >> 6) * 2048 + c * 64 +
+                                    ((((row >> 3) & 7) ^ (c & 7)) << 3) + (row & 7);
+      float x = acc;
+      for (int q = 0; q < nplanes; ++q) {
+        const float h = __bfloat162float(__float2bfloat16_rn(x));
+        planes[q * pstride + off] = bf16_bits(h);
+        x -= h;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 void launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst,
@@ -178,6 +234,14 @@ void launch_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, flo
 void launch_skinny_planes(const float* A, int64_t lda, const float* B, int64_t ldb, void* planes,
                           int nplanes, int64_t ldp, int64_t pstride, int64_t M, int N, int64_t K,
                           const int* skip, cudaStream_t s) {
+  if (ldp == 0 && (K > 32 || N > 32))
+    check_cuda(cudaErrorInvalidValue, "launch_skinny_planes: packed output needs K, N <= 32");
+  if (K <= 32 && N <= 32) {
+    small_k_planes_kernel<<<static_cast<unsigned>((M + 31) / 32), 32 * kSmallKWarps, 0, s>>>(A, lda, B, ldb, M, N, static_cast<int>(K), skip,
+                                    static_cast<uint16_t*>(planes), nplanes, ldp, pstride);
+    check_cuda(cudaGetLastError(), "small_k_planes_kernel");
+    return;
+  }
   skinny_dispatch(A, lda, B, ldb, nullptr, 0, M, N, K, skip, static_cast<uint16_t*>(planes),
                   nplanes, ldp, pstride, s);
 }

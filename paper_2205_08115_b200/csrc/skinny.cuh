@@ -15,20 +15,26 @@ void launch_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, flo
                    int64_t M, int N, int64_t K, const int* skip, cudaStream_t s);
 // As launch_skinny, but C is written transposed as `planes` (2 or 3) bf16
 // split planes (hi = rn(c), mid = rn(c − hi), …): plane p holds Cᵀ (N × M,
-// leading dim ldp) at element offset p·pstride — the B operand of the
-// tensor-core skinny GEMM2 (skinny_tc.cu).
+// leading dim ldp) at element offset p·pstride.  ldp == 0 writes the packed
+// B operand of the tensor-core skinny GEMM2 instead (skinny_tc.cu; needs
+// K, N ≤ 32; pstride = skinny_tc_packed_b_elems(M) per plane).
 void launch_skinny_planes(const float* A, int64_t lda, const float* B, int64_t ldb, void* planes,
                           int nplanes, int64_t ldp, int64_t pstride, int64_t M, int N, int64_t K,
                           const int* skip, cudaStream_t s);
 
-// G[M×N] (fp32 row-major, ldc) = D · Σ_p V_pᵀ on the tensor cores, D an
-// exact-bf16 M×K matrix (leading dim ldd) and V_p the bf16 planes (N × K,
-// leading dim ldv), N ≤ 32 (skinny_tc.cu).  Plans own their split-K
-// workspace; a launch is one kernel.
+// G[M×N] (fp32 row-major, ldc) = D · Σ_p V_pᵀ on the tensor cores, N ≤ 32
+// (skinny_tc.cu).  D (M×K, exact in bf16) is packed once into the kernel's
+// shared-memory tile order (128 rows × 64 k per 16-KB tile, 128-B swizzle)
+// so every load is one contiguous bulk copy; the V planes arrive packed
+// the same way (32 × 64 per 4-KB tile) from launch_skinny_planes(ldp = 0).
+// Plans own their split-K workspace; a launch is one kernel.
+int64_t skinny_tc_packed_a_bytes(int64_t M, int64_t K);
+int64_t skinny_tc_packed_b_elems(int64_t K);  // bf16 elements per plane
+void skinny_tc_pack_a(const float* D, int64_t ld, int64_t M, int64_t K, void* out, cudaStream_t s);
 struct SkinnyTcPlan;
-SkinnyTcPlan* skinny_tc_plan_create(const void* d_bf16, int64_t ldd, const void* const* vt_planes,
-                                    int planes, int64_t ldv, float* c, int64_t ldc, int64_t M,
-                                    int N, int64_t K, const int* skip, cudaStream_t s);
+SkinnyTcPlan* skinny_tc_plan_create(const void* a_packed, const void* b_packed, int planes,
+                                    float* c, int64_t ldc, int64_t M, int N, int64_t K,
+                                    const int* skip, cudaStream_t s);
 void skinny_tc_plan_destroy(SkinnyTcPlan* plan, cudaStream_t s);
 void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s);
 

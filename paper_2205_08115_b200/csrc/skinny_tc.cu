@@ -1,20 +1,27 @@
 // skinny_tc.cu — GEMM2 of the skinny chain (m ≤ 32, config 3) on the tensor
 // cores: G[M×N] = D · Σ_p V_pᵀ with D an exact-bf16 n×n structure matrix
 // (0/1 graph) and V_p the three bf16 planes of Vᵀ (N×K, N ≤ 32), i.e. the
-// bf16x3 chain with N padded to 32.  The product is a pure stream of D
-// (K-major, TMA, 128-B swizzle): 16 KB of D per 64-wide k-block against
-// 3 × 4 KB of V planes, 12 tcgen05.mma (M=128, N=32, K=16) per k-block.
+// bf16x3 chain with N padded to 32.  The product is a pure stream of D:
+// 16 KB of D per 64-wide k-block against 3 × 4 KB of V planes, 12
+// tcgen05.mma (M=128, N=32, K=16) per k-block.  D is constant across the
+// solve, so it is packed once into the exact shared-memory tile order
+// (K-major, 128-B swizzle) and each k-block is one contiguous 16-KB bulk
+// copy: with 2-D TMA boxes (128 rows × 128 B scattered at the row pitch) the
+// same stream reached only 1.4 TB/s.
 //
 // One CTA per (128-row tile, K split); the split count fills the SMs with
 // one CTA each.  Warp 0: TMA producer over a 6-stage ring; warp 1: MMA
 // issuer; warps 2–5: epilogue, one TMEM lane quadrant each.  As in gemm.cu,
 // the tensor core's truncating fp32 accumulation is bounded by restarting it
 // every 2 k-blocks in one of two TMEM buffers and promoting each chunk into
-// fp32 registers with round-to-nearest adds.  K-split partials go to a
-// workspace; in the last CTA of a row tile to finish (arrival counter) each
-// epilogue thread sums its row's partials in split order and writes it —
-// deterministic, no second launch.
+// fp32 registers with round-to-nearest adds.  The K splits of a row tile run
+// as one thread-block cluster: partials stay in shared memory and are summed
+// in split order through distributed shared memory (deterministic; no
+// workspace, fences or second launch — a global-memory arrival-counter
+// version spent 2–7 µs of a ~20 µs launch in that tail).
+#include <cooperative_groups.h>
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +33,8 @@
 #include "skinny.cuh"
 
 namespace gwb {
+
+namespace cg = cooperative_groups;
 
 void check_cuda(cudaError_t e, const char* what);  // solver.cu
 
@@ -41,13 +50,11 @@ constexpr int kThreads = 192;
 constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes;
 
 struct SkinnyTcParams {
-  CUtensorMap a_map;
-  CUtensorMap b_map[3];
+  const uint8_t* a;     // packed D: [tile][k-block] 16-KB swizzled tiles
+  const uint8_t* b;     // packed planes: [plane][k-block] 4-KB swizzled tiles
   int planes;
   float* c;
   int64_t ldc;
-  float* ws;            // [splits][M][kBN] partial sums (splits > 1)
-  unsigned* counters;   // per row tile (splits > 1), left at 0 after each launch
   int64_t M;
   int N;
   int kblocks, splits, kb_per;
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_slot;
-  __shared__ int last_cta;
+  __shared__ __align__(16) float part[kBM][kBN + 4];  // split-K partial (padded rows)
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
   const int kb0 = split * p.kb_per;
@@ -70,7 +77,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nchunks = (nkb + kPromote - 1) / kPromote;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&p.a_map);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -95,10 +101,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
         uint8_t* st = smem + static_cast<size_t>(s) * kStageBytes;
         ptx::mbar_arrive_expect_tx(&full[s], bytes);
-        const int kc = (kb0 + it) * kBK;
-        ptx::tma_load_2d(st, &p.a_map, &full[s], kc, tile * kBM);
+        const int64_t kb = kb0 + it;
+        ptx::bulk_g2s(st, p.a + (static_cast<int64_t>(tile) * p.kblocks + kb) * kATile, kATile,
+                      &full[s]);
         for (int q = 0; q < p.planes; ++q)
-          ptx::tma_load_2d(st + kATile + q * kBTile, &p.b_map[q], &full[s], kc, 0);
+          ptx::bulk_g2s(st + kATile + q * kBTile,
+                        p.b + (static_cast<int64_t>(q) * p.kblocks + kb) * kBTile, kBTile, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -146,60 +154,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ptx::mbar_arrive(&acc_empty[b]);
     }
     const int64_t row = static_cast<int64_t>(tile) * kBM + quad * 32 + lane;
-    const bool rok = row < p.M;
-    if (p.splits > 1 && rok) {
-      float4* w = reinterpret_cast<float4*>(p.ws + (static_cast<int64_t>(split) * p.M + row) * kBN);
+    if (p.splits == 1) {
+      if (row < p.M)
+        for (int j = 0; j < p.N; ++j) p.c[row * p.ldc + j] = acc[j];
+    } else {
+      float* pr = &part[quad * 32 + lane][0];
 #pragma unroll
       for (int j = 0; j < kBN / 4; ++j)
-        w[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        reinterpret_cast<float4*>(pr)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
     }
-    bool write = p.splits == 1;
-    if (p.splits > 1) {
-      // The last CTA of the row tile to arrive sums the partials in split
-      // order (its own from registers: the same bits it stored).
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-      if (warp == 2 && lane == 0)
-        last_cta = atomicAdd(&p.counters[tile], 1u) == static_cast<unsigned>(p.splits - 1);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      write = last_cta != 0;
-      if (write) {
-        __threadfence();
-        float tot[kBN];
-#pragma unroll
-        for (int j = 0; j < kBN; ++j) tot[j] = 0.f;
-        for (int s2 = 0; s2 < p.splits; ++s2) {
-          float part[kBN];
-          if (s2 == split) {
-#pragma unroll
-            for (int j = 0; j < kBN; ++j) part[j] = acc[j];
-          } else if (rok) {
-            const float4* w = reinterpret_cast<const float4*>(
-                p.ws + (static_cast<int64_t>(s2) * p.M + row) * kBN);
-#pragma unroll
-            for (int j = 0; j < kBN / 4; ++j) {
-              const float4 v4 = __ldcg(w + j);
-              part[4 * j] = v4.x;
-              part[4 * j + 1] = v4.y;
-              part[4 * j + 2] = v4.z;
-              part[4 * j + 3] = v4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < kBN; ++j) part[j] = 0.f;
-          }
-#pragma unroll
-          for (int j = 0; j < kBN; ++j) tot[j] += part[j];
-        }
-#pragma unroll
-        for (int j = 0; j < kBN; ++j) acc[j] = tot[j];
-        if (warp == 2 && lane == 0) p.counters[tile] = 0u;  // ready for the next launch
-      }
-    }
-    if (write && rok)
-      for (int j = 0; j < p.N; ++j) p.c[row * p.ldc + j] = acc[j];
   }
-
+  if (p.splits > 1) {
+    // The splits of a row tile form a cluster: rank k sums rows
+    // [k·128/S, (k+1)·128/S) of the S partials through distributed shared
+    // memory, in split order (deterministic), and writes them coalesced.
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    const int S = p.splits;
+    const int rows_per = (kBM + S - 1) / S;
+    const int rbeg = split * rows_per, rend = min(kBM, rbeg + rows_per);
+    for (int e = threadIdx.x; e < (rend - rbeg) * kBN; e += kThreads) {
+      const int r = rbeg + e / kBN, j = e % kBN;
+      const int64_t row = static_cast<int64_t>(tile) * kBM + r;
+      if (row >= p.M || j >= p.N) continue;
+      float sum = 0.f;
+      for (int q = 0; q < S; ++q) sum += *cluster.map_shared_rank(&part[r][j], q);
+      p.c[row * p.ldc + j] = sum;
+    }
+    cluster.sync();  // peers may still read this CTA's partials
+  }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -208,22 +191,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// D (fp32 row-major, exact in bf16) → packed tiles; zero beyond M × K.
+__global__ void pack_a_kernel(const float* __restrict__ D, int64_t ld, int64_t M, int64_t K,
+                              int kblocks, uint16_t* __restrict__ out) {
+  const int64_t t = blockIdx.x;  // tile · kblocks + k-block
+  const int64_t mt = t / kblocks, kb = t % kblocks;
+  uint16_t* dst = out + t * (kATile / 2);
+  for (int idx = threadIdx.x; idx < kBM * kBK; idx += blockDim.x) {
+    const int r = idx / kBK, k = idx % kBK;  // k fastest: coalesced reads
+    const int64_t gr = mt * kBM + r, gk = kb * kBK + k;
+    const float v = (gr < M && gk < K) ? D[gr * ld + gk] : 0.f;
+    const int off = r * 64 + ((((k >> 3) & 7) ^ (r & 7)) << 3) + (k & 7);
+    dst[off] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  }
+}
+
 }  // namespace
+
+int64_t skinny_tc_packed_a_bytes(int64_t M, int64_t K) {
+  return ((M + kBM - 1) / kBM) * ((K + kBK - 1) / kBK) * static_cast<int64_t>(kATile);
+}
+
+int64_t skinny_tc_packed_b_elems(int64_t K) { return ((K + kBK - 1) / kBK) * (kBTile / 2); }
+
+void skinny_tc_pack_a(const float* D, int64_t ld, int64_t M, int64_t K, void* out, cudaStream_t s) {
+  const int kblocks = static_cast<int>((K + kBK - 1) / kBK);
+  const int64_t tiles = (M + kBM - 1) / kBM;
+  pack_a_kernel<<<static_cast<unsigned>(tiles * kblocks), 256, 0, s>>>(D, ld, M, K, kblocks,
+                                                                       static_cast<uint16_t*>(out));
+  check_cuda(cudaGetLastError(), "pack_a_kernel");
+}
 
 struct SkinnyTcPlan {
   SkinnyTcParams params;
   int grid = 0;
 };
 
-SkinnyTcPlan* skinny_tc_plan_create(const void* d_bf16, int64_t ldd, const void* const* vt_planes,
-                                    int planes, int64_t ldv, float* c, int64_t ldc, int64_t M,
-                                    int N, int64_t K, const int* skip, cudaStream_t s) {
+SkinnyTcPlan* skinny_tc_plan_create(const void* a_packed, const void* b_packed, int planes,
+                                    float* c, int64_t ldc, int64_t M, int N, int64_t K,
+                                    const int* skip, cudaStream_t s) {
   if (N < 1 || N > kBN) throw std::invalid_argument("skinny_tc: N must be in [1, 32]");
   if (planes < 1 || planes > 3) throw std::invalid_argument("skinny_tc: 1..3 planes");
   auto* plan = new SkinnyTcPlan();
   SkinnyTcParams& p = plan->params;
-  p.a_map = gemm_tensor_map(d_bf16, M, K, ldd, kBM, 2);
-  for (int q = 0; q < planes; ++q) p.b_map[q] = gemm_tensor_map(vt_planes[q], N, K, ldv, kBN, 2);
+  p.a = static_cast<const uint8_t*>(a_packed);
+  p.b = static_cast<const uint8_t*>(b_packed);
   p.planes = planes;
   p.c = c;
   p.ldc = ldc;
@@ -235,21 +247,12 @@ SkinnyTcPlan* skinny_tc_plan_create(const void* d_bf16, int64_t ldd, const void*
   check_cuda(cudaGetDevice(&dev), "skinny_tc: device");
   check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "skinny_tc: SMs");
   const int tiles = static_cast<int>((M + kBM - 1) / kBM);
-  // One CTA per SM: split K so that tiles × splits ≤ #SMs, ≥ 2 k-blocks each.
-  int splits = std::max(1, std::min(sms / std::max(tiles, 1), p.kblocks / 2));
+  // One CTA per SM: split K so that tiles × splits ≤ #SMs, ≥ 2 k-blocks
+  // each; the splits of a tile form one cluster (≤ 8, portable).
+  int splits = std::max(1, std::min(std::min(sms / std::max(tiles, 1), p.kblocks / 2), 8));
   p.kb_per = (p.kblocks + splits - 1) / splits;
   splits = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
   p.splits = splits;
-  p.ws = nullptr;
-  p.counters = nullptr;
-  if (splits > 1) {
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&p.ws),
-                               static_cast<size_t>(splits) * M * kBN * sizeof(float), s),
-               "skinny_tc: workspace");
-    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&p.counters), tiles * sizeof(unsigned), s),
-               "skinny_tc: counters");
-    check_cuda(cudaMemsetAsync(p.counters, 0, tiles * sizeof(unsigned), s), "skinny_tc: counters");
-  }
   plan->grid = tiles * splits;
   static thread_local int attr_device = -1;
   if (attr_device != dev) {
@@ -262,15 +265,24 @@ SkinnyTcPlan* skinny_tc_plan_create(const void* d_bf16, int64_t ldd, const void*
 }
 
 void skinny_tc_plan_destroy(SkinnyTcPlan* plan, cudaStream_t s) {
-  if (!plan) return;
-  if (plan->params.ws) cudaFreeAsync(plan->params.ws, s);
-  if (plan->params.counters) cudaFreeAsync(plan->params.counters, s);
+  (void)s;
   delete plan;
 }
 
 void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s) {
-  skinny_tc_kernel<<<plan->grid, kThreads, kSmem, s>>>(plan->params);
-  check_cuda(cudaGetLastError(), "skinny_tc_kernel");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(plan->grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(plan->params.splits);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  check_cuda(cudaLaunchKernelEx(&cfg, skinny_tc_kernel, plan->params), "skinny_tc_kernel");
 }
 
 }  // namespace gwb

@@ -123,6 +123,8 @@ BapgEngine::~BapgEngine() {
   skinny_tc_plan_destroy(stc_tail_, stream_);
   dfree(Vs_, stream_);
   dfree(DyT_, stream_);
+  dfree(Dxp_, stream_);
+  dfree(Vtp_, stream_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], Vt_,
@@ -241,15 +243,14 @@ void BapgEngine::prepare_d() {
     skinny_tc_ = true;
     if (!DyT_) DyT_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
     launch_transpose(Dy_, m_, m_, ldm_, DyT_, ldm_, stream_);
-    if (!Dx_bf_) Dx_bf_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_ / 2 + 16);
-    launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
-    if (!Vt_aux_) Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
-    const void* vt[3];
-    for (int k = 0; k < 3; ++k) vt[k] = reinterpret_cast<uint16_t*>(Vt_aux_) + k * m_ * ldn_;
-    stc_ = skinny_tc_plan_create(Dx_bf_, ldn_, vt, 3, ldn_, G_, ldm_, n_, static_cast<int>(m_), n_,
-                                 &st_->done, stream_);
-    stc_tail_ = skinny_tc_plan_create(Dx_bf_, ldn_, vt, 3, ldn_, G_, ldm_, n_,
-                                      static_cast<int>(m_), n_, &st_->flags, stream_);
+    if (!Dxp_) Dxp_ = dalloc<uint8_t>(stream_, static_cast<size_t>(skinny_tc_packed_a_bytes(n_, n_)));
+    skinny_tc_pack_a(Dx_, ldn_, n_, n_, Dxp_, stream_);
+    vtp_plane_ = skinny_tc_packed_b_elems(n_);
+    if (!Vtp_) Vtp_ = dalloc<uint16_t>(stream_, static_cast<size_t>(3 * vtp_plane_));  // zero tails
+    stc_ = skinny_tc_plan_create(Dxp_, Vtp_, 3, G_, ldm_, n_, static_cast<int>(m_), n_, &st_->done,
+                                 stream_);
+    stc_tail_ = skinny_tc_plan_create(Dxp_, Vtp_, 3, G_, ldm_, n_, static_cast<int>(m_), n_,
+                                      &st_->flags, stream_);
     GWB_CUDA(cudaStreamSynchronize(stream_));
     return;
   }
@@ -521,7 +522,7 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->done, stream_);
   } else if (skinny_tc_) {
     // Vᵀ planes = (X·D_Yᵀ)ᵀ on the FP32 pipes, then G = D_X·V on the tensor cores.
-    launch_skinny_planes(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vt_aux_, 3, ldn_, m_ * ldn_, n_,
+    launch_skinny_planes(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vtp_, 3, 0, vtp_plane_, n_,
                          static_cast<int>(m_), m_, &st_->done, stream_);
     skinny_tc_launch(stc_, stream_);
   } else if (fp32()) {
@@ -697,7 +698,7 @@ void BapgEngine::tail() {
     launch_rowgather(cx_, W_[parity_], ldm_, m_, Vt_, ldn_, true, &st_->flags, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->flags, stream_);
   } else if (skinny_tc_) {
-    launch_skinny_planes(W_[parity_], ldm_, DyT_, ldm_, Vt_aux_, 3, ldn_, m_ * ldn_, n_,
+    launch_skinny_planes(W_[parity_], ldm_, DyT_, ldm_, Vtp_, 3, 0, vtp_plane_, n_,
                          static_cast<int>(m_), m_, &st_->flags, stream_);
     skinny_tc_launch(stc_tail_, stream_);
   } else if (fp32()) {

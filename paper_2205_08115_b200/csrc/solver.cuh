@@ -141,6 +141,9 @@ class BapgEngine {
   bool skinny_tc_ = false;
   SkinnyTcPlan* stc_ = nullptr;       // skip on done
   SkinnyTcPlan* stc_tail_ = nullptr;  // skip on flags
+  void* Dxp_ = nullptr;               // D_X packed in GEMM2 tile order
+  void* Vtp_ = nullptr;               // Vᵀ bf16 planes packed in tile order
+  int64_t vtp_plane_ = 0;             // bf16 elements per packed plane
   bool no_planes() const { return sparse() || fp32() || skinny_tc_; }  // chains read the fp32 iterates
   int aux_mode() const {
     return precision_ == GWB_PREC_TF32 ? 1
