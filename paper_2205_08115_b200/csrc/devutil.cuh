@@ -82,7 +82,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// (max, Σ v·e^{x−max}) online accumulator.
+// (max, Σ v·e^{x−max}) online accumulator.  The FMAs are explicit so every
+// kernel that inlines these computes bit-identical sums (no context-dependent
+// contraction).
 struct MaxSum {
   float mx;
   float s;
@@ -90,10 +92,10 @@ struct MaxSum {
 
 __device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) {
   if (e > a.mx) {
-    a.s = a.s * __expf(a.mx - e) + v;
+    a.s = __fmaf_rn(a.s, __expf(a.mx - e), v);
     a.mx = e;
   } else {
-    a.s += v * __expf(e - a.mx);
+    a.s = __fmaf_rn(v, __expf(e - a.mx), a.s);
   }
 }
 
@@ -103,7 +105,7 @@ __device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) {
   const float M = fmaxf(a.mx, b.mx);
   MaxSum r;
   r.mx = M;
-  r.s = a.s * __expf(a.mx - M) + b.s * __expf(b.mx - M);
+  r.s = __fmaf_rn(a.s, __expf(a.mx - M), __fmul_rn(b.s, __expf(b.mx - M)));
   // NaN propagation: any NaN max poisons the sum.
   if (isnan(a.mx) || isnan(b.mx)) {
     r.mx = NAN;

@@ -25,6 +25,11 @@ using namespace dev;
 constexpr int kRowThreads = 256;
 
 // ---------------------------------------------------------------------------
+// The exponent argument is formed explicitly as rn(rn(g·(1/ρ)) − max): the
+// same rounded products feed the online (max, Σ) pass and the write pass, so
+// numerators and normaliser agree and no kernel variant can contract the
+// expression differently (FMA vs. multiply-then-subtract).
+
 // Half-step a: one CTA per row.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int write, int tail) {
@@ -45,8 +50,8 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        ms_add(ms, gv[q] * inv_rho, wv[q]);
-        sums[0] += static_cast<double>(gv[q]) * wv[q];
+        ms_add(ms, __fmul_rn(gv[q], inv_rho), wv[q]);
+        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(wv[q]), sums[0]);
         sums[1] += wv[q];
       }
     }
@@ -75,10 +80,10 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
     const float4 w4 = *reinterpret_cast<const float4*>(w + j);
     float4 o;
-    o.x = (j + 0 < m) ? scale * w4.x * __expf(g4.x * inv_rho - r) : 0.f;
-    o.y = (j + 1 < m) ? scale * w4.y * __expf(g4.y * inv_rho - r) : 0.f;
-    o.z = (j + 2 < m) ? scale * w4.z * __expf(g4.z * inv_rho - r) : 0.f;
-    o.w = (j + 3 < m) ? scale * w4.w * __expf(g4.w * inv_rho - r) : 0.f;
+    o.x = (j + 0 < m) ? scale * w4.x * __expf(__fsub_rn(__fmul_rn(g4.x, inv_rho), r)) : 0.f;
+    o.y = (j + 1 < m) ? scale * w4.y * __expf(__fsub_rn(__fmul_rn(g4.y, inv_rho), r)) : 0.f;
+    o.z = (j + 2 < m) ? scale * w4.z * __expf(__fsub_rn(__fmul_rn(g4.z, inv_rho), r)) : 0.f;
+    o.w = (j + 3 < m) ? scale * w4.w * __expf(__fsub_rn(__fmul_rn(g4.w, inv_rho), r)) : 0.f;
     *reinterpret_cast<float4*>(p + j) = o;
     if (d.P_aux) aux_store4(d.P_aux, am, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
   }
@@ -112,13 +117,17 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        ms_add(ms, gv[q] * inv_rho, wv[q]);
-        sums[0] += static_cast<double>(gv[q]) * wv[q];
+        ms_add(ms, __fmul_rn(gv[q], inv_rho), wv[q]);
+        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(wv[q]), sums[0]);
         sums[1] += wv[q];
       }
     }
   }
   ms = warp_merge(ms);
+  // The xor butterfly leaves lane-dependent roundings; every lane takes lane
+  // 0's (max, Σ), as the CTA-per-row kernel broadcasts warp 0 lane 0's.
+  ms.mx = __shfl_sync(0xffffffffu, ms.mx, 0);
+  ms.s = __shfl_sync(0xffffffffu, ms.s, 0);
   sums[0] = warp_sum(sums[0]);
   sums[1] = warp_sum(sums[1]);
   if (lane == 0) {
@@ -139,10 +148,10 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
   if (j >= m) return;
   const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
   float4 o;
-  o.x = (j + 0 < m) ? scale * w4.x * __expf(g4.x * inv_rho - r) : 0.f;
-  o.y = (j + 1 < m) ? scale * w4.y * __expf(g4.y * inv_rho - r) : 0.f;
-  o.z = (j + 2 < m) ? scale * w4.z * __expf(g4.z * inv_rho - r) : 0.f;
-  o.w = (j + 3 < m) ? scale * w4.w * __expf(g4.w * inv_rho - r) : 0.f;
+  o.x = (j + 0 < m) ? scale * w4.x * __expf(__fsub_rn(__fmul_rn(g4.x, inv_rho), r)) : 0.f;
+  o.y = (j + 1 < m) ? scale * w4.y * __expf(__fsub_rn(__fmul_rn(g4.y, inv_rho), r)) : 0.f;
+  o.z = (j + 2 < m) ? scale * w4.z * __expf(__fsub_rn(__fmul_rn(g4.z, inv_rho), r)) : 0.f;
+  o.w = (j + 3 < m) ? scale * w4.w * __expf(__fsub_rn(__fmul_rn(g4.w, inv_rho), r)) : 0.f;
   *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
   if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
 }
@@ -166,10 +175,10 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
     for (int64_t i = r0 + warp; i < r1; i += kColThreads / 32) {
       const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
       const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + c0);
-      ms_add(ms[0], g4.x * inv_rho, p4.x);
-      ms_add(ms[1], g4.y * inv_rho, p4.y);
-      ms_add(ms[2], g4.z * inv_rho, p4.z);
-      ms_add(ms[3], g4.w * inv_rho, p4.w);
+      ms_add(ms[0], __fmul_rn(g4.x, inv_rho), p4.x);
+      ms_add(ms[1], __fmul_rn(g4.y, inv_rho), p4.y);
+      ms_add(ms[2], __fmul_rn(g4.z, inv_rho), p4.z);
+      ms_add(ms[3], __fmul_rn(g4.w, inv_rho), p4.w);
       ps[0] += p4.x;
       ps[1] += p4.y;
       ps[2] += p4.z;
@@ -262,15 +271,15 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        o[q] = sv[q] * pv[q] * __expf(gv[q] * inv_rho - mv[q]);
+        o[q] = sv[q] * pv[q] * __expf(__fsub_rn(__fmul_rn(gv[q], inv_rho), mv[q]));
         finite = finite && isfinite(o[q]);
-        sums[0] += static_cast<double>(gv[q]) * o[q];
+        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(o[q]), sums[0]);
         const double sp = static_cast<double>(pv[q]) - o[q];
-        sums[1] += sp * sp;
+        sums[1] = __fma_rn(sp, sp, sums[1]);
         const double df = static_cast<double>(o[q]) - wv[q];
-        sums[2] += df * df;
-        sums[3] += static_cast<double>(wv[q]) * wv[q];
-        sums[4] += static_cast<double>(gv[q]) * pv[q];
+        sums[2] = __fma_rn(df, df, sums[2]);
+        sums[3] = __fma_rn(static_cast<double>(wv[q]), static_cast<double>(wv[q]), sums[3]);
+        sums[4] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(pv[q]), sums[4]);
       } else {
         o[q] = 0.f;
       }
@@ -319,15 +328,15 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        o[q] = sv[q] * pv[q] * __expf(gv[q] * inv_rho - mv[q]);
+        o[q] = sv[q] * pv[q] * __expf(__fsub_rn(__fmul_rn(gv[q], inv_rho), mv[q]));
         finite = finite && isfinite(o[q]);
-        sums[0] += static_cast<double>(gv[q]) * o[q];
+        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(o[q]), sums[0]);
         const double sp = static_cast<double>(pv[q]) - o[q];
-        sums[1] += sp * sp;
+        sums[1] = __fma_rn(sp, sp, sums[1]);
         const double df = static_cast<double>(o[q]) - wv[q];
-        sums[2] += df * df;
-        sums[3] += static_cast<double>(wv[q]) * wv[q];
-        sums[4] += static_cast<double>(gv[q]) * pv[q];
+        sums[2] = __fma_rn(df, df, sums[2]);
+        sums[3] = __fma_rn(static_cast<double>(wv[q]), static_cast<double>(wv[q]), sums[3]);
+        sums[4] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(pv[q]), sums[4]);
       } else {
         o[q] = 0.f;
       }
