@@ -144,28 +144,11 @@ __device__ float block_max(float v) {
   return t;
 }
 
-// (max, Σ e^{x−max}) in fp64 state with fp32 exponentials of small arguments.
-struct LseAcc {
-  double mx;
-  double s;
-};
-__device__ __forceinline__ void lse_add(LseAcc& a, double x) {
-  if (x > a.mx) {
-    a.s = a.s * static_cast<double>(__expf(static_cast<float>(a.mx - x))) + 1.0;
-    a.mx = x;
-  } else if (x > -INFINITY) {
-    a.s += static_cast<double>(__expf(static_cast<float>(x - a.mx)));
-  } else if (isnan(x)) {
-    a.mx = NAN;
-  }
-}
-__device__ __forceinline__ LseAcc lse_merge(LseAcc a, LseAcc b) {
-  if (isnan(a.mx) || isnan(b.mx)) return LseAcc{NAN, NAN};
-  if (b.mx == -INFINITY) return a;
-  if (a.mx == -INFINITY) return b;
-  const double M = fmax(a.mx, b.mx);
-  return LseAcc{M, a.s * exp(a.mx - M) + b.s * exp(b.mx - M)};
-}
+// (max, Σ e^{x−max}) in fp64 state with fp32 exponentials of small
+// arguments: the online LSE accumulator of the BAPG projections
+// (devutil.cuh), instantiated for fp64 with unit weights.
+using LseAcc = OnlineLse<double>;
+__device__ __forceinline__ void lse_add(LseAcc& a, double x) { dev::lse_add(a, x, 1.0); }
 
 // ---------------------------------------------------------------------------
 // form: one CTA per row.
@@ -240,10 +223,7 @@ __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   }
   // block merge (fixed order)
   __shared__ double smx[kThreads / 32], ss[kThreads / 32];
-  for (int o = 16; o > 0; o >>= 1) {
-    LseAcc b{__shfl_xor_sync(0xffffffffu, a.mx, o), __shfl_xor_sync(0xffffffffu, a.s, o)};
-    a = lse_merge(a, b);
-  }
+  a = lse_warp_merge(a);
   const int w = threadIdx.x / 32, l = threadIdx.x & 31;
   if (l == 0) {
     smx[w] = a.mx;

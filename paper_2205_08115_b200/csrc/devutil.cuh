@@ -82,48 +82,71 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// (max, Σ v·e^{x−max}) online accumulator.  The FMAs are explicit so every
-// kernel that inlines these computes bit-identical sums (no context-dependent
-// contraction).
-struct MaxSum {
-  float mx;
-  float s;
+// Online log-sum-exp accumulator (max, Σ w·e^{x−max}) shared by the BAPG
+// projections (kernels.cu: fp32 state, iterate weights) and the eBPG / BPG
+// Sinkhorn scaling (bregman.cu: fp64 potentials, unit weights): the same
+// add, merge and warp butterfly, in a fixed order.  Per-element
+// exponentials are fp32 MUFU in both (arguments ≤ 0); the merge exp is fp32
+// for the fp32 state and libdevice exp for the fp64 one.  FMAs are explicit
+// so every kernel that inlines these computes bit-identical sums (no
+// context-dependent contraction).
+template <class T>
+struct OnlineLse {
+  T mx;
+  T s;
 };
+__device__ __forceinline__ float lse_ex(float x) { return __expf(x); }
+__device__ __forceinline__ double lse_ex(double x) {
+  return static_cast<double>(__expf(static_cast<float>(x)));
+}
+__device__ __forceinline__ float lse_ex_merge(float x) { return __expf(x); }
+__device__ __forceinline__ double lse_ex_merge(double x) { return exp(x); }
+__device__ __forceinline__ float lse_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double lse_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float lse_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double lse_mul(double a, double b) { return __dmul_rn(a, b); }
 
-__device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) {
-  if (e > a.mx) {
-    a.s = __fmaf_rn(a.s, __expf(a.mx - e), v);
-    a.mx = e;
-  } else {
-    a.s = __fmaf_rn(v, __expf(e - a.mx), a.s);
+// a ⊕= (x, w): -inf contributes nothing, NaN poisons the max.
+template <class T>
+__device__ __forceinline__ void lse_add(OnlineLse<T>& a, T x, T w) {
+  if (x > a.mx) {
+    a.s = lse_fma(a.s, lse_ex(a.mx - x), w);
+    a.mx = x;
+  } else if (x > -INFINITY) {
+    a.s = lse_fma(w, lse_ex(x - a.mx), a.s);
+  } else if (isnan(x)) {
+    a.mx = NAN;
   }
 }
 
-__device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) {
+template <class T>
+__device__ __forceinline__ OnlineLse<T> lse_merge(OnlineLse<T> a, OnlineLse<T> b) {
+  if (isnan(a.mx) || isnan(b.mx)) return OnlineLse<T>{static_cast<T>(NAN), static_cast<T>(NAN)};
   if (b.mx == -INFINITY) return a;
   if (a.mx == -INFINITY) return b;
-  const float M = fmaxf(a.mx, b.mx);
-  MaxSum r;
-  r.mx = M;
-  r.s = __fmaf_rn(a.s, __expf(a.mx - M), __fmul_rn(b.s, __expf(b.mx - M)));
-  // NaN propagation: any NaN max poisons the sum.
-  if (isnan(a.mx) || isnan(b.mx)) {
-    r.mx = NAN;
-    r.s = NAN;
-  }
-  return r;
+  const T M = a.mx > b.mx ? a.mx : b.mx;
+  return OnlineLse<T>{M, lse_fma(a.s, lse_ex_merge(a.mx - M), lse_mul(b.s, lse_ex_merge(b.mx - M)))};
 }
 
-__device__ __forceinline__ MaxSum warp_merge(MaxSum a) {
+// xor butterfly over the warp; lanes may differ by an ulp afterwards, so
+// callers that need one value per warp take lane 0's.
+template <class T>
+__device__ __forceinline__ OnlineLse<T> lse_warp_merge(OnlineLse<T> a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    MaxSum b;
+    OnlineLse<T> b;
     b.mx = __shfl_xor_sync(0xffffffffu, a.mx, o);
     b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
-    a = ms_merge(a, b);
+    a = lse_merge(a, b);
   }
   return a;
 }
+
+// The BAPG names (fp32 state, iterate-weighted terms).
+using MaxSum = OnlineLse<float>;
+__device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) { lse_add(a, e, v); }
+__device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) { return lse_merge(a, b); }
+__device__ __forceinline__ MaxSum warp_merge(MaxSum a) { return lse_warp_merge(a); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
