@@ -334,15 +334,32 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
   if (p.skip != nullptr && *p.skip != 0) return;
   const int row = blockIdx.x;
   const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
+  // ldw (a multiple of 8) and ldc (of 32) and 256-B aligned buffers make
+  // every 8-column group 16-B aligned (fp32 float4 pairs, bf16 uint4).
   for (int c0 = threadIdx.x * 8; c0 < p.N; c0 += blockDim.x * 8) {
     float x[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) x[q] = 0.0f;
-    for (int s = 0; s < p.splits; ++s) {
-      const float* w = p.ws + static_cast<int64_t>(s) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw + c0;
+    // Splits in order; 4 at a time with all their loads in flight.
+    for (int s0 = 0; s0 < p.splits; s0 += 4) {
+      float4 v[4][2];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + q < p.ldw) x[q] = __fadd_rn(x[q], w[q]);
+      for (int t = 0; t < 4; ++t) {
+        if (s0 + t < p.splits) {
+          const float4* w = reinterpret_cast<const float4*>(
+              p.ws + static_cast<int64_t>(s0 + t) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw + c0);
+          v[t][0] = __ldcs(w);
+          v[t][1] = __ldcs(w + 1);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (s0 + t >= p.splits) break;
+        const float f[8] = {v[t][0].x, v[t][0].y, v[t][0].z, v[t][0].w,
+                            v[t][1].x, v[t][1].y, v[t][1].z, v[t][1].w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = __fadd_rn(x[q], f[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -351,19 +368,25 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
       x[q] = p.aux_mode == 1 ? rna_tf32(v) : v;
     }
     const int64_t off = static_cast<int64_t>(row) * p.ldc + c0;
+    const bool full = c0 + 8 <= p.N;
     if (p.c_planes > 0) {
+      alignas(16) __nv_bfloat16 h[3][8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        if (c0 + q >= p.N) continue;
         float r = x[q];
-        const __nv_bfloat16 h0 = __float2bfloat16_rn(r);
-        r -= __bfloat162float(h0);
-        const __nv_bfloat16 h1 = __float2bfloat16_rn(r);
-        r -= __bfloat162float(h1);
-        const __nv_bfloat16 h2 = __float2bfloat16_rn(r);
-        p.c_pl[0][off + q] = h0;
-        p.c_pl[1][off + q] = p.c_planes == 2 ? __float2bfloat16_rn(x[q] - __bfloat162float(h0)) : h1;
-        if (p.c_planes == 3) p.c_pl[2][off + q] = h2;
+        h[0][q] = __float2bfloat16_rn(r);
+        r -= __bfloat162float(h[0][q]);
+        h[1][q] = __float2bfloat16_rn(r);
+        r -= __bfloat162float(h[1][q]);
+        h[2][q] = __float2bfloat16_rn(r);
+        if (p.c_planes == 2) h[1][q] = __float2bfloat16_rn(x[q] - __bfloat162float(h[0][q]));
+      }
+      for (int pl = 0; pl < p.c_planes; ++pl) {
+        if (full) {
+          *reinterpret_cast<uint4*>(p.c_pl[pl] + off) = *reinterpret_cast<const uint4*>(h[pl]);
+        } else {
+          for (int q = 0; q < 8 && c0 + q < p.N; ++q) p.c_pl[pl][off + q] = h[pl][q];
+        }
       }
     } else {
 #pragma unroll
