@@ -23,7 +23,45 @@ CASES = {
     "bpg_er48": (lambda: I.config1(seed=16, n=48), dict(algorithm=abi.BPG, step=5.0, max_iters=10, inner_iters=10)),
     "hbpg_er48": (lambda: I.config1(seed=17, n=48), dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0,
                                                          inner_iters=10, switch_iters=5, max_iters=12)),
+    # quadratic geometry (euclid_project) and the per-record Luo-Tseng residual
+    "bapg_quad_gmm40x32": (lambda: I.config2(seed=18, n=40, m=32),
+                           dict(algorithm=abi.BAPG, geometry=abi.QUADRATIC, rho=2.0, max_iters=25)),
+    "bapg_er40_residual": (lambda: I.config1(seed=19, n=40),
+                           dict(algorithm=abi.BAPG, rho=0.5, max_iters=6, record_residual=1)),
+    "hbpg_er36_residual": (lambda: I.config1(seed=20, n=36),
+                           dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10,
+                                switch_iters=3, max_iters=6, record_residual=1)),
 }
+
+
+def leaf_fixtures(ref, out):
+    """Leaves off the solver path: luo_tseng_residual / dykstra_project
+    (diagnostics.cpp:33-42, projections.cpp:165-187) and write_coupling_csv
+    (io.cpp:183-193), computed by the reference build."""
+    rng = np.random.default_rng(21)
+    n, m = 40, 30
+    dx = I.adjacency(n, I.erdos_renyi(n, 0.2, 21))
+    dy = I.adjacency(m, I.erdos_renyi(m, 0.2, 22))
+    mu = rng.uniform(0.5, 1.5, n)
+    nu = rng.uniform(0.5, 1.5, m)
+    mu, nu = mu / mu.sum(), nu / nu.sum()
+    pi = np.asfortranarray(np.outer(mu, nu) * rng.uniform(0.5, 1.5, (n, m)))
+    rc, res, msg = ref.luo_tseng_residual(dx, dy, pi, mu, nu)
+    assert rc == 0, msg
+    rc, proj, msg = ref.dykstra_project(3.0 * pi, mu, nu)
+    assert rc == 0, msg
+    np.savez_compressed(os.path.join(out, "leaf_residual_er40x30.npz"), dx=dx, dy=dy, mu=mu, nu=nu,
+                        pi=pi, residual=res, dykstra_in=3.0 * pi, dykstra_out=proj)
+    print("leaf_residual_er40x30", res)
+    a = rng.standard_normal((12, 9)) * 10.0 ** rng.integers(-320, 300, (12, 9))
+    a.flat[:10] = [0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1e16, 1e17, 1e-4, 1e-5]
+    k = rng.integers(4 * 10**15, 9 * 10**15, 8) | 1
+    a.flat[10:18] = k.astype(np.float64) / 4.0  # exact 17th-digit ties
+    a = np.asfortranarray(a)
+    text = ref.format_coupling_csv(a)
+    np.savez_compressed(os.path.join(out, "leaf_csv_mixed12x9.npz"), a=a,
+                        text=np.frombuffer(text, dtype=np.uint8))
+    print("leaf_csv_mixed12x9", len(text), "bytes")
 
 
 def main():
@@ -38,12 +76,14 @@ def main():
         r = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
         assert r.code == 0, r.message
         tr = np.array([[t["iter"], t["objective"], t["marginal_infeasibility"], t["split_gap"],
-                        t["rel_change"], t["phase"]] for t in r.trace])
+                        t["rel_change"], t["phase"],
+                        np.nan if t.get("residual") is None else t["residual"]] for t in r.trace])
         cfg_vec = np.array([getattr(cfg, f) for f, _ in abi.Config._fields_], dtype=np.float64)
         np.savez_compressed(os.path.join(out, name + ".npz"), dx=inst.dx, dy=inst.dy, mu=inst.mu,
                             nu=inst.nu, final=r.final, trace=tr, config=cfg_vec,
                             converged=r.converged, iterations=r.iterations_used)
         print(name, r.iterations_used, r.converged, r.trace[-1]["objective"])
+    leaf_fixtures(ref, out)
 
 
 if __name__ == "__main__":
