@@ -227,8 +227,12 @@ class ShardEngine {
       GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
       own_stream_ = true;
     }
+    // AUTO depends on the exactness of every rank's rows of D_X, which this
+    // rank cannot see: the orchestrator resolves it (dist.resolve_precision).
+    if (cfg.precision == GWB_PREC_AUTO)
+      throw std::invalid_argument(
+          "gwb_shard_create: resolve AUTO precision across ranks first (bf16x3 or 3xtf32)");
     prec_ = cfg.precision;
-    if (prec_ == GWB_PREC_AUTO) prec_ = GWB_PREC_BF16X3;
     bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2;
     planes_ = prec_ == GWB_PREC_BF16X3 ? 3 : (prec_ == GWB_PREC_TF32 ? 1 : 2);
     esize_ = bf16_ ? 2 : 4;

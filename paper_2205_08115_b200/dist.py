@@ -405,6 +405,16 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
     import numpy as np
     import torch
     n, m = len(mu), len(nu)
+    if cfg.precision == abi.PREC_AUTO:
+        # Every rank checks its own rows of D_X (and D_Y); the verdict is the
+        # all-reduced minimum, so all ranks pick the same chain.
+        plan = ShardPlan(n, world)
+        rb0, rv0 = plan.row_begin(rank), plan.rows_valid(rank)
+        ok = (rv0 == 0 or bf16_exact(np.asarray(dx[rb0:rb0 + rv0], dtype=np.float32))) and \
+            bf16_exact(np.asarray(dy, dtype=np.float32))
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        cfg = resolve_precision(cfg, bool(flag.item()))
     shard = GpuShard(cfg, n, m, rank, world, device)
     try:
         rb, rv = shard.row_begin, shard.rows_valid
@@ -452,11 +462,34 @@ def raise_shard_flags(st: dict):
     num("non-finite iterate")
 
 
+def bf16_exact(t) -> bool:
+    """True if every entry of the (torch or numpy) array is exact in bf16."""
+    import numpy as np
+    import torch
+    x = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
+    x = x.float()
+    return bool(torch.equal(x.to(torch.bfloat16).float(), x))
+
+
+def resolve_precision(cfg: abi.Config, exact: bool) -> abi.Config:
+    """AUTO resolved as the single-GPU engine does: bf16x3 when
+    both structure matrices are exact in bf16, else 3xTF32.  With sharded
+    D_X the exactness must be agreed by every rank first (each rank only
+    sees its rows): `exact` is that global verdict."""
+    if cfg.precision != abi.PREC_AUTO:
+        return cfg
+    out = abi.Config()
+    C.pointer(out)[0] = cfg
+    out.precision = abi.PREC_BF16X3 if exact else abi.PREC_3XTF32
+    return out
+
+
 def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, device=0,
                       stream=None) -> List[GpuShard]:
     """Build shard engines from full device tensors (tests / emulation)."""
     import torch
     n, m = dx.shape[0], dy.shape[0]
+    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy))
     shards = []
     for r in (range(world) if ranks is None else ranks):
         s = GpuShard(cfg, n, m, r, world, device, stream)

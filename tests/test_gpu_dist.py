@@ -10,7 +10,7 @@ from paper_2205_08115_b200 import instances as I
 
 pytestmark = pytest.mark.gpu
 
-PREC = {"bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2, "3xtf32": abi.PREC_3XTF32,
+PREC = {"auto": abi.PREC_AUTO, "bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2, "3xtf32": abi.PREC_3XTF32,
         "tf32": abi.PREC_TF32}
 
 
@@ -57,6 +57,16 @@ def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case, overlap):
 
 
 @pytest.mark.parametrize("overlap", [False, True])
+def test_sharded_auto_precision_with_weighted_d(gpu, port):
+    # AUTO under sharding is resolved from every rank's rows (dist.resolve_
+    # precision): Euclidean D is not bf16-exact, so the shards run 3xTF32.
+    inst = I.config2(seed=3, n=200, m=150)
+    pi, w, recs, st, cfg = _run(inst, 2, "auto", 20)
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert np.abs(pi - o.pi).max() / np.abs(o.pi).max() < 1e-4
+    assert abs(recs[-1].objective - o.trace[-1]["objective"]) <= 1e-5 * abs(o.trace[-1]["objective"])
+
+
 def test_sharded_stop_rule_and_errors(gpu, port, overlap):
     inst = I.config1(seed=9, n=64)
     pi, w, recs, st, cfg = _run(inst, 2, "bf16x3", 1200, rel_tol=1e-6, overlap=overlap)
