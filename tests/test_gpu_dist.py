@@ -56,7 +56,6 @@ def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case, overlap):
         assert abs(r.rel_change - q["rel_change"]) <= 2e-3 * q["rel_change"] + 1e-7
 
 
-@pytest.mark.parametrize("overlap", [False, True])
 def test_sharded_auto_precision_with_weighted_d(gpu, port):
     # AUTO under sharding is resolved from every rank's rows (dist.resolve_
     # precision): Euclidean D is not bf16-exact, so the shards run 3xTF32.
@@ -67,6 +66,7 @@ def test_sharded_auto_precision_with_weighted_d(gpu, port):
     assert abs(recs[-1].objective - o.trace[-1]["objective"]) <= 1e-5 * abs(o.trace[-1]["objective"])
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 def test_sharded_stop_rule_and_errors(gpu, port, overlap):
     inst = I.config1(seed=9, n=64)
     pi, w, recs, st, cfg = _run(inst, 2, "bf16x3", 1200, rel_tol=1e-6, overlap=overlap)
