@@ -113,6 +113,48 @@ GWB_API void gwb_gen_gmm3d(int32_t n, int32_t k, double sigma, uint64_t seed,
 GWB_API void gwb_distance_maxnorm_f32(int32_t n, const double* xyz,
                                       float* out);
 
+/* ---------------------------------------------------------------------------
+ * Row-sharded eBPG / BPG / hBPG (csrc/bregman.cu, orchestrated by dist.py).
+ * Rank r owns rows [r·n_r, r·n_r + n_r) of D_X (n_r = ⌈n/world⌉ rounded up
+ * to 64, padded_rows = world·n_r) and computes those rows of the chain;
+ * π, the Sinkhorn potentials and the records are replicated.  The caller
+ * owns two buffers and issues the collectives on the shard's stream:
+ *   vt: vt_bytes, [world][planes][m][n_r] (rank r's slot = its Vᵀ block),
+ *   g:  padded_rows × ld fp32 (G; rank r's rows are one contiguous block).
+ * Per outer iteration k = 1, 2, …:  phase(k, 0) · all-gather(vt) ·
+ * phase(k, 1) · all-gather(g) · phase(k, 2) [form, Sinkhorn sweeps, write,
+ * record; identical on every rank] · status.  After the loop, unless flags
+ * are set: phase(used, 3) · all-gather(vt) · phase(used, 4) · all-gather(g)
+ * · phase(used, 5) (the last record's objective), then finish.
+ * cfg->precision must be resolved (GWB_PREC_BF16X3 / BF16X2 / 3XTF32);
+ * the observer and record_residual are single-GPU only.
+ * ------------------------------------------------------------------------- */
+typedef struct gwb_bshard gwb_bshard;
+
+GWB_API int32_t gwb_bshard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t rank,
+                                  int32_t world, int32_t device, void* stream,
+                                  gwb_bshard** out, gwb_status* st);
+GWB_API int32_t gwb_bshard_layout(gwb_bshard* s, int64_t* rows_per_shard, int64_t* row_begin,
+                                  int64_t* rows_valid, int64_t* padded_rows, int64_t* ld,
+                                  int32_t* planes, int32_t* elem_bytes, int64_t* vt_bytes,
+                                  gwb_status* st);
+GWB_API int32_t gwb_bshard_set_comm(gwb_bshard* s, void* vt, float* g, gwb_status* st);
+/* dx_rows: rows_valid × n fp32 on the device (leading dim ldx), dy: m × m
+ * fp32 device (ldy); mu (n) and nu (m) host fp64. */
+GWB_API int32_t gwb_bshard_load_device(gwb_bshard* s, const float* dx_rows, int64_t ldx,
+                                       const float* dy, int64_t ldy, const double* mu,
+                                       const double* nu, gwb_status* st);
+GWB_API int32_t gwb_bshard_phase(gwb_bshard* s, int32_t k, int32_t op, gwb_status* st);
+GWB_API int32_t gwb_bshard_status(gwb_bshard* s, int32_t* done, int32_t* iter, int32_t* flags,
+                                  int32_t* converged, gwb_status* st);
+GWB_API int32_t gwb_bshard_stream(gwb_bshard* s, void** stream, gwb_status* st);
+/* The reference error (if flags are set), the trace, convergence and the
+ * final coupling (host fp64 column-major n × m, nullable). */
+GWB_API int32_t gwb_bshard_finish(gwb_bshard* s, double* out_final, gwb_record* trace,
+                                  int32_t trace_cap, int32_t* n_records, int32_t* converged,
+                                  int32_t* iterations_used, gwb_status* st);
+GWB_API int32_t gwb_bshard_destroy(gwb_bshard* s);
+
 #ifdef __cplusplus
 }
 #endif

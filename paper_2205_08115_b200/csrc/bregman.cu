@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <stdexcept>
 #include <vector>
 
 #include "devutil.cuh"
@@ -545,23 +546,56 @@ struct DevFree {
 // ---------------------------------------------------------------------------
 class BregmanEngine {
  public:
-  BregmanEngine(int device, int64_t n, int64_t m, const gwb_config& cfg, int algo)
+  // world > 0: row-sharded chain (rank of world).  Rank r owns
+  // rows [r·n_r, r·n_r + n_r) of D_X (n_r = ⌈n/world⌉ rounded up to 64) and
+  // computes those rows of G; Vᵀ and G are completed by caller-issued
+  // all-gathers between the phases (sphase), and π, the Sinkhorn state and
+  // the records stay replicated — every rank runs the same deterministic
+  // kernels on the same data, so stop and phase decisions agree.
+  BregmanEngine(int device, int64_t n, int64_t m, const gwb_config& cfg, int algo,
+                int world = 0, int rank = 0, cudaStream_t stream = nullptr)
       : dev_(device), n_(n), m_(m), ldn_(round_up(n, 32)), ldm_(round_up(m, 32)), cfg_(cfg),
         algo_(algo) {
     GWB_CUDA(cudaSetDevice(dev_));
-    GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
-    const size_t nm = static_cast<size_t>(n_) * ldm_;
-    Dx_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_));
+    if (stream) {
+      s_ = stream;
+    } else {
+      GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+      own_stream_ = true;
+    }
+    sharded_ = world > 0;
+    rows_alloc_ = n_;
+    if (sharded_) {
+      world_ = world;
+      rank_ = rank;
+      nr_ = round_up((n_ + world_ - 1) / world_, 64);
+      npad_ = nr_ * world_;
+      row0_ = static_cast<int64_t>(rank_) * nr_;
+      rows_valid_ = std::max<int64_t>(0, std::min<int64_t>(nr_, n_ - row0_));
+      ldk_ = round_up(npad_, 64);
+      rows_alloc_ = npad_;
+      // The chain precision is fixed up front (resolved by the orchestrator):
+      // it sets the exchange-buffer layout the caller allocates.
+      const int req = cfg_.precision;
+      aux_mode_ = req == GWB_PREC_BF16X3 ? 3 : req == GWB_PREC_BF16X2 ? 4 : 2;
+      planes_ = aux_mode_ == 3 ? 3 : 2;
+      esize_ = aux_mode_ >= 3 ? 2 : 4;
+    }
+    pstride_ = rows_alloc_ * ldm_;
+    const size_t nm = static_cast<size_t>(rows_alloc_) * ldm_;
+    const size_t dx_elems =
+        sharded_ ? static_cast<size_t>(nr_) * ldk_ : static_cast<size_t>(n_) * ldn_;
+    Dx_ = keep(dalloc<float>(dx_elems));
     Dy_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
-    Dx_lo_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_));
+    Dx_lo_ = keep(dalloc<float>(dx_elems));
     Dy_lo_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
     for (int q = 0; q < 2; ++q) {
       P_[q] = keep(dalloc<float>(nm));
       Pa_[q] = keep(dalloc<float>(nm * 3 / 2));  // fp32 residual or up to 3 bf16 planes
     }
-    Vt_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
-    Vta_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
-    G_ = keep(dalloc<float>(nm));
+    Vt_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
+    Vta_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
+    G_ = sharded_ ? nullptr : keep(dalloc<float>(nm));  // sharded: caller-owned (set_comm)
     mu_ = keep(dalloc<double>(n_));
     nu_ = keep(dalloc<double>(m_));
     f_ = keep(dalloc<double>(n_));
@@ -588,7 +622,77 @@ class BregmanEngine {
     cudaStreamSynchronize(s_);
     for (auto* p : plans_) gemm_plan_destroy(p);
     for (void* p : bufs_) cudaFree(p);
-    cudaStreamDestroy(s_);
+    if (own_stream_) cudaStreamDestroy(s_);
+  }
+
+  // ---- sharded mode --------------------------------------------------------
+  int64_t rows_per_shard() const { return nr_; }
+  int64_t row_begin() const { return row0_; }
+  int64_t rows_valid() const { return rows_valid_; }
+  int64_t padded_rows() const { return npad_; }
+  int64_t ld() const { return ldm_; }
+  int planes() const { return planes_; }
+  int esize() const { return esize_; }
+  int64_t vt_bytes() const { return static_cast<int64_t>(planes_) * world_ * m_ * nr_ * esize_; }
+  cudaStream_t stream() const { return s_; }
+  // vt: [world][planes][m][n_r] gather buffer; g: npad × ld fp32 (G, all rows).
+  void set_comm(void* vt, float* g) {
+    vt_ = static_cast<uint8_t*>(vt);
+    G_ = g;
+  }
+
+  // Sharded inputs: device fp32 rows of D_X (rows_valid × n, leading dim
+  // ldx) and D_Y (m × m, ldy); host fp64 μ (n) and ν (m).  The precision
+  // must be resolved (the ranks' exactness verdict, dist.resolve_precision).
+  void load_sharded(const float* dx_rows, int64_t ldx, const float* dy, int64_t ldy,
+                    const double* mu, const double* nu) {
+    if (!vt_ || !G_) api_fail(GWB_ERR_INVALID, "bregman shard: set_comm before load");
+    if (rows_valid_ > 0)
+      GWB_CUDA(cudaMemcpy2DAsync(Dx_, ldk_ * 4, dx_rows, ldx * 4, n_ * 4, rows_valid_,
+                                 cudaMemcpyDeviceToDevice, s_));
+    GWB_CUDA(cudaMemcpy2DAsync(Dy_, ldm_ * 4, dy, ldy * 4, m_ * 4, m_, cudaMemcpyDeviceToDevice, s_));
+    if (aux_mode_ >= 3) {
+      Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_ / 2 + 16));
+      Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
+      launch_to_bf16(Dx_, nr_, ldk_, ldk_, Dx_bf_, s_);
+      launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+    } else {
+      launch_tf32_aux(Dx_, nr_, ldk_, ldk_, Dx_lo_, 2, s_);
+      launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
+    }
+    GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
+    std::vector<float> mu32(n_), nu32(m_);
+    for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
+    for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
+    std::unique_ptr<void, DevFree> a(dalloc<float>(n_)), b(dalloc<float>(m_));
+    GWB_CUDA(cudaMemcpyAsync(a.get(), mu32.data(), 4 * n_, cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(b.get(), nu32.data(), 4 * m_, cudaMemcpyHostToDevice, s_));
+    launch_product_coupling(static_cast<float*>(a.get()), static_cast<float*>(b.get()), n_, m_, ldm_,
+                            P_[0], s_);
+    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_);
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    build_shard_plans();
+    begin();
+  }
+
+  // One step of the sharded schedule for outer iteration k (ops 0–2) or the
+  // tail record after `k` = iterations used (ops 3–5):
+  //   0 / 3: local GEMM1 → this rank's Vᵀ slot     [caller: all-gather vt]
+  //   1 / 4: local GEMM2 → this rank's rows of G   [caller: all-gather G]
+  //   2: form, Sinkhorn sweeps, write, finalize (replicated); 5: tail record.
+  void sphase(int k, int op) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    switch (op) {
+      case 0: GWB_CUDA(gemm_launch(s1_[(k - 1) & 1], s_)); break;
+      case 1: GWB_CUDA(gemm_launch(s2_, s_)); break;
+      case 2: iterate_rest(k); break;
+      case 3: GWB_CUDA(gemm_launch(s1t_[k & 1], s_)); break;
+      case 4: GWB_CUDA(gemm_launch(s2t_, s_)); break;
+      case 5: tail_rest(k); break;
+      default: api_fail(GWB_ERR_INVALID, "bregman shard: unknown phase");
+    }
+    GWB_CUDA(cudaGetLastError());
   }
 
   void load(const double* dx, const double* dy, const double* mu, const double* nu,
@@ -622,13 +726,13 @@ class BregmanEngine {
                               ldm_, P_[0], s_);
       GWB_CUDA(cudaStreamSynchronize(s_));
     }
-    launch_tf32_aux(P_[0], n_, m_, ldm_, Pa_[0], aux_mode_, s_);
+    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_);
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_plans();
   }
 
-  // Runs the whole solve; returns iterations used.
-  void run(gwb_observer observer, void* user, std::vector<double>* host_pi) {
+  // Device status reset and the hBPG phase budget (solvers.cpp:365-426).
+  void begin() {
     const int budget1 = algo_ == GWB_EBPG ? cfg_.max_iters
                         : algo_ == GWB_BPG ? 0
                                            : std::min(cfg_.switch_iters, cfg_.max_iters);
@@ -638,13 +742,17 @@ class BregmanEngine {
     d.budget1 = budget1;
     d.has_phase2 = algo_ != GWB_EBPG;
     base_ = d;
+  }
+
+  // Everything of outer iteration k after the chain: the form pass, ≤
+  // inner_iters Sinkhorn sweeps, the write pass and the record; returns the
+  // device status after the iteration.
+  BState iterate_rest(int k) {
+    const int q = (k - 1) & 1;
+    BDev v = base_;
+    rebind(v, q);
     const int rows_per_chunk = static_cast<int>((n_ + chunks_ - 1) / chunks_);
-    for (int k = 1; k <= cfg_.max_iters; ++k) {
-      const int q = (k - 1) & 1;
-      BDev v = base_;
-      rebind(v, q);
-      GWB_CUDA(gemm_launch(g1_[q], s_));
-      GWB_CUDA(gemm_launch(g2_, s_));
+    {
       form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 0);
       form_check_kernel<<<1, 1024, 0, s_>>>(v);
       for (int sw = 1; sw <= cfg_.inner_iters; ++sw) {
@@ -666,9 +774,21 @@ class BregmanEngine {
       write_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk);
       breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 0);
       GWB_CUDA(cudaGetLastError());
-      BState h;
-      GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
-      GWB_CUDA(cudaStreamSynchronize(s_));
+    }
+    BState h;
+    GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
+    return h;
+  }
+
+  // Runs the whole solve (single GPU).
+  void run(gwb_observer observer, void* user, std::vector<double>* host_pi) {
+    begin();
+    for (int k = 1; k <= cfg_.max_iters; ++k) {
+      const int q = (k - 1) & 1;
+      GWB_CUDA(gemm_launch(g1_[q], s_));
+      GWB_CUDA(gemm_launch(g2_, s_));
+      const BState h = iterate_rest(k);
       if (h.flags) break;
       // record_residual (solvers.cpp:278-280, 348-350), before the observer.
       if (cfg_.record_residual && h.iter - 1 == k) residuals_.push_back(residual_of(P_[k & 1]));
@@ -693,10 +813,13 @@ class BregmanEngine {
   // Objective of the last record: one more chain on the final π.
   void tail(int used) {
     const int q = used & 1;
-    BDev v = base_;
-    rebind(v, q);
     GWB_CUDA(gemm_launch(g1t_[q], s_));
     GWB_CUDA(gemm_launch(g2t_, s_));
+    tail_rest(used);
+  }
+  void tail_rest(int used) {
+    BDev v = base_;
+    rebind(v, used & 1);
     form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 1);
     breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 1);
     GWB_CUDA(cudaGetLastError());
@@ -753,7 +876,7 @@ class BregmanEngine {
     d.ld = ldm_;
     d.G = G_;
     d.aux_mode = aux_mode_;
-    d.plane = n_ * ldm_;
+    d.plane = pstride_;
     d.mu64 = mu_;
     d.nu64 = nu_;
     d.f = f_;
@@ -831,7 +954,7 @@ class BregmanEngine {
         d.M = m_; d.N = n_; d.K = m_;
         d.bf16_planes = planes;
         d.a_bf16 = Dy_bf_; d.lda = ldm_;
-        for (int k = 0; k < planes; ++k) d.b_bf16[k] = plane_k(Pa_[q], n_ * ldm_, k);
+        for (int k = 0; k < planes; ++k) d.b_bf16[k] = plane_k(Pa_[q], pstride_, k);
         d.ldb = ldm_;
         d.c_planes = planes;
         for (int k = 0; k < planes; ++k) d.c_bf16[k] = plane_k(Vta_, m_ * ldn_, k);
@@ -894,10 +1017,80 @@ class BregmanEngine {
     g2t_ = g2(&st_->flags);
   }
 
+  void* slot(int p, int r) const {
+    return vt_ + ((static_cast<int64_t>(r) * planes_ + p) * m_ * nr_) * esize_;
+  }
+
+  // Local chain plans (as ShardEngine, csrc/shard.cu): GEMM1 on this rank's
+  // rows of π into its Vᵀ slot, GEMM2 of its D_X rows against the gathered
+  // blocked-K Vᵀ into its rows of G.
+  void build_shard_plans() {
+    const bool bf = aux_mode_ >= 3;
+    auto make1 = [&](int q, const int* skip) {
+      GemmDesc d;
+      d.M = m_; d.N = nr_; d.K = m_;
+      d.lda = ldm_; d.ldb = ldm_; d.ldc = nr_;
+      d.skip = skip;
+      if (bf) {
+        d.bf16_planes = planes_;
+        d.a_bf16 = Dy_bf_;
+        for (int p = 0; p < planes_; ++p)
+          d.b_bf16[p] = reinterpret_cast<uint16_t*>(Pa_[q]) + p * pstride_ + row0_ * ldm_;
+        d.c_planes = planes_;
+        for (int p = 0; p < planes_; ++p) d.c_bf16[p] = slot(p, rank_);
+      } else {
+        d.a = Dy_; d.a_lo = Dy_lo_;
+        d.b = P_[q] + row0_ * ldm_; d.b_lo = Pa_[q] + row0_ * ldm_;
+        d.c = static_cast<float*>(slot(0, rank_));
+        d.c_aux = static_cast<float*>(slot(1, rank_));
+        d.aux_mode = 2;
+        d.three_pass = true;
+      }
+      GemmPlan* p = gemm_plan_create(d);
+      plans_.push_back(p);
+      return p;
+    };
+    auto make2 = [&](const int* skip) {
+      GemmDesc d;
+      d.M = nr_; d.N = m_; d.K = npad_;
+      d.lda = ldk_;
+      d.b_block_k = nr_;
+      d.b_block_stride = static_cast<int64_t>(planes_) * m_ * nr_;
+      d.c = G_ + row0_ * ldm_; d.ldc = ldm_;
+      d.skip = skip;
+      if (bf) {
+        d.bf16_planes = planes_;
+        d.a_bf16 = Dx_bf_;
+        for (int p = 0; p < planes_; ++p) d.b_bf16[p] = slot(p, 0);
+      } else {
+        d.a = Dx_; d.a_lo = Dx_lo_;
+        d.b = static_cast<const float*>(slot(0, 0));
+        d.b_lo = static_cast<const float*>(slot(1, 0));
+        d.three_pass = true;
+      }
+      GemmPlan* p = gemm_plan_create(d);
+      plans_.push_back(p);
+      return p;
+    };
+    for (int q = 0; q < 2; ++q) {
+      s1_[q] = make1(q, &st_->done);
+      s1t_[q] = make1(q, &st_->flags);
+    }
+    s2_ = make2(&st_->done);
+    s2t_ = make2(&st_->flags);
+  }
+
   int dev_;
   int64_t n_, m_, ldn_, ldm_;
   gwb_config cfg_;
   int algo_;
+  bool own_stream_ = false;
+  bool sharded_ = false;
+  int world_ = 1, rank_ = 0, planes_ = 3, esize_ = 2;
+  int64_t nr_ = 0, npad_ = 0, row0_ = 0, rows_valid_ = 0, ldk_ = 0, rows_alloc_ = 0, pstride_ = 0;
+  uint8_t* vt_ = nullptr;
+  GemmPlan *s1_[2] = {nullptr, nullptr}, *s1t_[2] = {nullptr, nullptr}, *s2_ = nullptr,
+           *s2t_ = nullptr;
   cudaStream_t s_ = nullptr;
   std::vector<void*> bufs_;
   std::vector<GemmPlan*> plans_;
@@ -1004,6 +1197,87 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
   std::vector<double> target(m);
   for (int64_t j = 0; j < m; ++j) target[j] = (1.0 - p) * nu[j] + p / static_cast<double>(m);
   eng.output(used, out_final, target);
+}
+
+// ---- row-sharded eBPG / BPG / hBPG (C-ABI in capi.cu) ---------
+struct BregShard {
+  std::unique_ptr<BregmanEngine> eng;
+  gwb_config cfg;
+  int algo;
+  std::vector<double> nu;
+};
+
+BregShard* bshard_create(const gwb_config& cfg, int algo, int64_t n, int64_t m, int world, int rank,
+                         int device, cudaStream_t s) {
+  auto* b = new BregShard();
+  b->cfg = cfg;
+  b->algo = algo;
+  b->eng.reset(new BregmanEngine(device, n, m, cfg, algo, world, rank, s));
+  return b;
+}
+void bshard_destroy(BregShard* b) { delete b; }
+void bshard_layout(BregShard* b, int64_t* rows_per_shard, int64_t* row_begin, int64_t* rows_valid,
+                   int64_t* padded_rows, int64_t* ld) {
+  *rows_per_shard = b->eng->rows_per_shard();
+  *row_begin = b->eng->row_begin();
+  *rows_valid = b->eng->rows_valid();
+  *padded_rows = b->eng->padded_rows();
+  *ld = b->eng->ld();
+}
+void bshard_comm_layout(BregShard* b, int32_t* planes, int32_t* esize, int64_t* vt_bytes) {
+  *planes = b->eng->planes();
+  *esize = b->eng->esize();
+  *vt_bytes = b->eng->vt_bytes();
+}
+void bshard_set_comm(BregShard* b, void* vt, float* g) { b->eng->set_comm(vt, g); }
+void bshard_load(BregShard* b, const float* dx_rows, int64_t ldx, const float* dy, int64_t ldy,
+                 const double* mu, const double* nu, int64_t m) {
+  b->nu.assign(nu, nu + m);
+  b->eng->load_sharded(dx_rows, ldx, dy, ldy, mu, nu);
+}
+void bshard_phase(BregShard* b, int k, int op) { b->eng->sphase(k, op); }
+void bshard_status(BregShard* b, int32_t* done, int32_t* iter, int32_t* flags, int32_t* converged) {
+  const BState h = b->eng->status();
+  *done = h.done;
+  *iter = h.iter;
+  *flags = h.flags;
+  *converged = h.converged;
+}
+void* bshard_stream(BregShard* b) { return b->eng->stream(); }
+
+// After the schedule (and, without flags, the tail ops 3–5): the reference
+// errors, records, convergence and the final coupling, as bregman_solve.
+void bshard_finish(BregShard* b, double* out_final, gwb_record* trace, int32_t trace_cap,
+                   int32_t* n_records, int32_t* converged, int32_t* iterations_used) {
+  BregmanEngine& eng = *b->eng;
+  const BState s = eng.status();
+  if (s.flags) raise_breg(s, b->cfg.log_domain != 0);
+  const int used = s.iter - 1;
+  if (trace && trace_cap < used) api_fail(GWB_ERR_CAPACITY, "trace capacity < iterations used");
+  const std::vector<BRecord> r = eng.records(used);
+  if (trace) {
+    for (int k = 1; k <= used; ++k) {
+      gwb_record& o = trace[k - 1];
+      std::memset(&o, 0, sizeof(o));
+      o.iter = k;
+      o.objective = -r[k].obj;
+      o.marginal_infeasibility = r[k].infeas;
+      o.rel_change = r[k].rel;
+      o.elapsed_seconds = r[k].elapsed;
+      o.phase = b->algo == GWB_HBPG ? r[k].phase : 0;
+    }
+  }
+  if (n_records) *n_records = trace ? used : 0;
+  if (converged) *converged = s.converged;
+  if (iterations_used) *iterations_used = used;
+  if (out_final) {
+    const int64_t m = static_cast<int64_t>(b->nu.size());
+    const bool last_bpg = used >= 1 && r[used].phase == 2;
+    const double p = last_bpg ? b->cfg.perturbation : 0.0;
+    std::vector<double> target(m);
+    for (int64_t j = 0; j < m; ++j) target[j] = (1.0 - p) * b->nu[j] + p / static_cast<double>(m);
+    eng.output(used, out_final, target);
+  }
 }
 
 }  // namespace gwb

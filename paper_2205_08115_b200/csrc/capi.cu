@@ -700,6 +700,88 @@ int32_t gwb_session_write_coupling_csv(gwb_session* s, const char* path, gwb_sta
   });
 }
 
+// ---- row-sharded eBPG / BPG / hBPG (bregman.cu) ----------------------------
+struct gwb_bshard {
+  gwb::BregShard* b = nullptr;
+  int64_t n = 0, m = 0;
+  ~gwb_bshard() { gwb::bshard_destroy(b); }
+};
+
+int32_t gwb_bshard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t rank, int32_t world,
+                          int32_t device, void* stream, gwb_bshard** out, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!cfg || !out) fail(GWB_ERR_INVALID, "null argument");
+    validate_config(cfg);
+    if (cfg->algorithm != GWB_EBPG && cfg->algorithm != GWB_BPG && cfg->algorithm != GWB_HBPG)
+      fail(GWB_ERR_CONFIG, "gwb_bshard_create: algorithm must be ebpg, bpg or hbpg");
+    if (n < 1 || m < 1 || world < 1 || rank < 0 || rank >= world)
+      fail(GWB_ERR_DIMENSION, "gwb_bshard_create: bad shape or rank");
+    if (cfg->precision != GWB_PREC_BF16X3 && cfg->precision != GWB_PREC_BF16X2 &&
+        cfg->precision != GWB_PREC_3XTF32)
+      fail(GWB_ERR_CONFIG,
+           "gwb_bshard_create: resolve the precision across ranks first (bf16x3, bf16x2 or 3xtf32)");
+    if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual is single-GPU only");
+    auto* s = new gwb_bshard();
+    s->n = n;
+    s->m = m;
+    try {
+      s->b = gwb::bshard_create(*cfg, cfg->algorithm, n, m, world, rank, device,
+                                static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int32_t gwb_bshard_layout(gwb_bshard* s, int64_t* rows_per_shard, int64_t* row_begin,
+                          int64_t* rows_valid, int64_t* padded_rows, int64_t* ld, int32_t* planes,
+                          int32_t* elem_bytes, int64_t* vt_bytes, gwb_status* st) {
+  return guarded(st, [&] {
+    gwb::bshard_layout(s->b, rows_per_shard, row_begin, rows_valid, padded_rows, ld);
+    gwb::bshard_comm_layout(s->b, planes, elem_bytes, vt_bytes);
+  });
+}
+
+int32_t gwb_bshard_set_comm(gwb_bshard* s, void* vt, float* g, gwb_status* st) {
+  return guarded(st, [&] { gwb::bshard_set_comm(s->b, vt, g); });
+}
+
+int32_t gwb_bshard_load_device(gwb_bshard* s, const float* dx_rows, int64_t ldx, const float* dy,
+                               int64_t ldy, const double* mu, const double* nu, gwb_status* st) {
+  return guarded(st, [&] {
+    if (!dy || !mu || !nu) fail(GWB_ERR_INVALID, "null input");
+    gwb::bshard_load(s->b, dx_rows, ldx, dy, ldy, mu, nu, s->m);
+  });
+}
+
+int32_t gwb_bshard_phase(gwb_bshard* s, int32_t k, int32_t op, gwb_status* st) {
+  return guarded(st, [&] { gwb::bshard_phase(s->b, k, op); });
+}
+
+int32_t gwb_bshard_status(gwb_bshard* s, int32_t* done, int32_t* iter, int32_t* flags,
+                          int32_t* converged, gwb_status* st) {
+  return guarded(st, [&] { gwb::bshard_status(s->b, done, iter, flags, converged); });
+}
+
+int32_t gwb_bshard_stream(gwb_bshard* s, void** stream, gwb_status* st) {
+  return guarded(st, [&] { *stream = gwb::bshard_stream(s->b); });
+}
+
+int32_t gwb_bshard_finish(gwb_bshard* s, double* out_final, gwb_record* trace, int32_t trace_cap,
+                          int32_t* n_records, int32_t* converged, int32_t* iterations_used,
+                          gwb_status* st) {
+  return guarded(st, [&] {
+    gwb::bshard_finish(s->b, out_final, trace, trace_cap, n_records, converged, iterations_used);
+  });
+}
+
+int32_t gwb_bshard_destroy(gwb_bshard* s) {
+  delete s;
+  return GWB_OK;
+}
+
 int32_t gwb_session_destroy(gwb_session* s) {
   delete s;
   return GWB_OK;

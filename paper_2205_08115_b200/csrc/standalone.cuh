@@ -81,6 +81,25 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
                    gwb_record* trace, int32_t trace_cap, int32_t* n_records, int32_t* converged,
                    int32_t* iterations_used, const GraphInput* graphs = nullptr);
 
+// Row-sharded eBPG / BPG / hBPG (bregman.cu): the chain runs on this rank's
+// rows of D_X with caller-issued all-gathers of Vᵀ and G between phases;
+// the Sinkhorn state and π are replicated (dist.py orchestrates).
+struct BregShard;
+BregShard* bshard_create(const gwb_config& cfg, int algo, int64_t n, int64_t m, int world, int rank,
+                         int device, cudaStream_t s);
+void bshard_destroy(BregShard* b);
+void bshard_layout(BregShard* b, int64_t* rows_per_shard, int64_t* row_begin, int64_t* rows_valid,
+                   int64_t* padded_rows, int64_t* ld);
+void bshard_comm_layout(BregShard* b, int32_t* planes, int32_t* esize, int64_t* vt_bytes);
+void bshard_set_comm(BregShard* b, void* vt, float* g);
+void bshard_load(BregShard* b, const float* dx_rows, int64_t ldx, const float* dy, int64_t ldy,
+                 const double* mu, const double* nu, int64_t m);
+void bshard_phase(BregShard* b, int k, int op);
+void bshard_status(BregShard* b, int32_t* done, int32_t* iter, int32_t* flags, int32_t* converged);
+void* bshard_stream(BregShard* b);
+void bshard_finish(BregShard* b, double* out_final, gwb_record* trace, int32_t trace_cap,
+                   int32_t* n_records, int32_t* converged, int32_t* iterations_used);
+
 // Batched BAPG over independent small problems (config 5).
 void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx, int64_t n,
                          const double* dy, int64_t m, const double* mu, const double* nu,

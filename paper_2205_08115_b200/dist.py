@@ -68,6 +68,18 @@ _SIGS = {
     "gwb_shard_records": (C.c_int32, [_P, C.c_int32, C.POINTER(abi.Record), _ST]),
     "gwb_shard_rows": (C.c_int32, [_P, _P, _P, _ST]),
     "gwb_shard_destroy": (C.c_int32, [_P]),
+    "gwb_bshard_create": (C.c_int32, [C.POINTER(abi.Config), C.c_int64, C.c_int64, C.c_int32,
+                                      C.c_int32, C.c_int32, _P, C.POINTER(_P), _ST]),
+    "gwb_bshard_layout": (C.c_int32, [_P, _I64P, _I64P, _I64P, _I64P, _I64P, _I32P, _I32P, _I64P,
+                                      _ST]),
+    "gwb_bshard_set_comm": (C.c_int32, [_P, _P, _P, _ST]),
+    "gwb_bshard_load_device": (C.c_int32, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, _ST]),
+    "gwb_bshard_phase": (C.c_int32, [_P, C.c_int32, C.c_int32, _ST]),
+    "gwb_bshard_status": (C.c_int32, [_P, _I32P, _I32P, _I32P, _I32P, _ST]),
+    "gwb_bshard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
+    "gwb_bshard_finish": (C.c_int32, [_P, _P, C.POINTER(abi.Record), C.c_int32, _I32P, _I32P,
+                                      _I32P, _ST]),
+    "gwb_bshard_destroy": (C.c_int32, [_P]),
 }
 
 
@@ -192,6 +204,170 @@ class GpuShard:
             pass
 
 
+class BregShard:
+    """One rank's row-sharded eBPG / BPG / hBPG engine (csrc/bregman.cu) with
+    its torch-owned exchange buffers: `vt` (the Vᵀ gather buffer, as
+    GpuShard) and `g` (G, padded_rows × ld fp32; rank r's rows are block r)."""
+
+    def __init__(self, cfg: abi.Config, n: int, m: int, rank: int, world: int,
+                 device: int = 0, stream=None):
+        import torch
+        self.torch = torch
+        self.lib = _lib()
+        self.n, self.m, self.rank, self.world = n, m, rank, world
+        self.max_iters = cfg.max_iters
+        st = abi.Status()
+        self.h = _P()
+        sp = None if stream is None else stream.cuda_stream
+        self.lib.gwb_bshard_create(C.byref(cfg), n, m, rank, world, device, sp, C.byref(self.h),
+                                   C.byref(st))
+        _check(st)
+        v = [C.c_int64() for _ in range(5)]
+        pl, es, vb = C.c_int32(), C.c_int32(), C.c_int64()
+        self.lib.gwb_bshard_layout(self.h, *[C.byref(x) for x in v], C.byref(pl), C.byref(es),
+                                   C.byref(vb), C.byref(st))
+        _check(st)
+        self.rows_per_shard, self.row_begin, self.rows_valid, self.padded_rows, self.ld = \
+            (x.value for x in v)
+        self.planes, self.elem_bytes = pl.value, es.value
+        dev = torch.device("cuda", device)
+        self.vt = torch.zeros(vb.value, dtype=torch.uint8, device=dev)
+        self.g = torch.zeros(self.padded_rows * self.ld, dtype=torch.float32, device=dev)
+        self.lib.gwb_bshard_set_comm(self.h, self.vt.data_ptr(), self.g.data_ptr(), C.byref(st))
+        _check(st)
+        spp = _P()
+        self.lib.gwb_bshard_stream(self.h, C.byref(spp), C.byref(st))
+        self.stream = torch.cuda.ExternalStream(spp.value, device=dev)
+
+    def load(self, dx_rows, dy, mu, nu):
+        """dx_rows / dy: device fp32 tensors (rows_valid × n, m × m); mu, nu:
+        host fp64 arrays (full length)."""
+        import numpy as np
+        st = abi.Status()
+        self.torch.cuda.synchronize()
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        nu = np.ascontiguousarray(nu, dtype=np.float64)
+        self.lib.gwb_bshard_load_device(self.h, dx_rows.data_ptr(), dx_rows.stride(0),
+                                        dy.data_ptr(), dy.stride(0), mu.ctypes.data,
+                                        nu.ctypes.data, C.byref(st))
+        _check(st)
+
+    def phase(self, k: int, op: int):
+        st = abi.Status()
+        self.lib.gwb_bshard_phase(self.h, k, op, C.byref(st))
+        _check(st)
+
+    def status(self) -> dict:
+        st = abi.Status()
+        v = [C.c_int32() for _ in range(4)]
+        self.lib.gwb_bshard_status(self.h, *[C.byref(x) for x in v], C.byref(st))
+        _check(st)
+        return dict(zip(("done", "iter", "flags", "converged"), (x.value for x in v)))
+
+    def finish(self, want_final: bool = True) -> dict:
+        import numpy as np
+        st = abi.Status()
+        cap = max(1, self.max_iters)
+        trace = (abi.Record * cap)()
+        nr, cv, used = C.c_int32(), C.c_int32(), C.c_int32()
+        final = np.zeros((self.n, self.m), order="F") if want_final else None
+        self.lib.gwb_bshard_finish(self.h, None if final is None else final.ctypes.data, trace, cap,
+                                   C.byref(nr), C.byref(cv), C.byref(used), C.byref(st))
+        _check(st)
+        return {"final": final, "trace": list(trace[: nr.value]), "converged": bool(cv.value),
+                "iterations_used": used.value}
+
+    def close(self):
+        if self.h:
+            self.lib.gwb_bshard_destroy(self.h)
+            self.h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_bregman_sharded(shards: List, comm, max_iters: int) -> List[dict]:
+    """Sharded eBPG / BPG / hBPG schedule (gwb_ext.h): per outer iteration
+    GEMM1 · all-gather(Vᵀ) · GEMM2 · all-gather(G) · replicated Sinkhorn and
+    record; then the tail record; returns each shard's finish() result."""
+    k = 0
+    for k in range(1, max_iters + 1):
+        for op in (0, 1, 2):
+            _all_bphase(shards, k, op)
+            if op == 0:
+                comm.gather_vt(shards)
+            elif op == 1:
+                comm.gather_g(shards)
+        st = shards[0].status()
+        if st["flags"] or st["done"]:
+            break
+    st = shards[0].status()
+    if not st["flags"]:
+        used = st["iter"] - 1
+        _all_bphase(shards, used, 3)
+        comm.gather_vt(shards)
+        _all_bphase(shards, used, 4)
+        comm.gather_g(shards)
+        _all_bphase(shards, used, 5)
+    return [s.finish() for s in shards]
+
+
+def _all_bphase(shards, k, op):
+    for s in shards:
+        s.phase(k, op)
+
+
+def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
+                          device: int = 0) -> dict:
+    """Row-sharded eBPG / BPG / hBPG from HOST inputs (ebpg_solve /
+    bpg_solve / hbpg_solve semantics, solvers.cpp:219-426) — called by every
+    rank with the same arguments; `dx` only has to slice to host rows.
+    The chain is sharded by rows of D_X (Vᵀ and G all-gathered over NCCL);
+    the Sinkhorn scaling and the iterate are replicated, so every rank
+    returns the same final coupling and trace."""
+    import numpy as np
+    import torch
+    n, m = len(mu), len(nu)
+    plan = ShardPlan(n, world)
+    rb, rv = plan.row_begin(rank), plan.rows_valid(rank)
+    rows = np.ascontiguousarray(dx[rb:rb + rv], dtype=np.float32).reshape(rv, n)
+    if cfg.precision == abi.PREC_AUTO:
+        ok = (rv == 0 or bf16_exact(rows)) and bf16_exact(np.asarray(dy, dtype=np.float32))
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        cfg = resolve_precision(cfg, bool(flag.item()))
+    shard = BregShard(cfg, n, m, rank, world, device)
+    try:
+        dev = torch.device("cuda", device)
+        if rv == 0:
+            rows = np.zeros((1, n), dtype=np.float32)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+        shard.load(t(rows), t(dy), mu, nu)
+        return run_bregman_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters)[0]
+    finally:
+        shard.close()
+
+
+def bregman_shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, device=0,
+                              stream=None) -> List[BregShard]:
+    """Sharded Bregman engines from full device tensors (tests / emulation);
+    mu, nu host fp64."""
+    import torch
+    n, m = dx.shape[0], dy.shape[0]
+    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy))
+    shards = []
+    for r in range(world):
+        s = BregShard(cfg, n, m, r, world, device, stream)
+        rows = dx[s.row_begin:s.row_begin + max(s.rows_valid, 1)].contiguous()
+        s.load(rows, dy.contiguous(), mu, nu)
+        shards.append(s)
+    torch.cuda.synchronize()
+    return shards
+
+
 # ---------------------------------------------------------------------------
 class TorchComm:
     """Collectives for one local shard per process via torch.distributed
@@ -218,6 +394,11 @@ class TorchComm:
         s = shards[0]
         with _stream(s):
             self._gather(s.stats)
+
+    def gather_g(self, shards):
+        s = shards[0]
+        with _stream(s):
+            self._gather(s.g)
 
     def reduce_diag(self, shards):
         s = shards[0]
@@ -258,6 +439,9 @@ class EmuComm:
 
     def gather_stats(self, shards):
         self._gather(shards, "stats")
+
+    def gather_g(self, shards):
+        self._gather(shards, "g")
 
     @staticmethod
     def _gather(shards, attr):

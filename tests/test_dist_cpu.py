@@ -97,3 +97,47 @@ def test_shard_plan():
     assert sum(p.rows_valid(r) for r in range(8)) == 20000
     p = ShardPlan(100, 3)
     assert [p.rows_valid(r) for r in range(3)] == [64, 36, 0]
+
+
+# ---- row-sharded eBPG / BPG / hBPG orchestration (dist.run_bregman_sharded)
+
+def _bworker(rank, world, port, over, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2205_08115_b200.dist import TorchComm, run_bregman_sharded
+    from tests.bshard_mirror import CpuBregShard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = I.config1(seed=6, n=90)
+    cfg = abi.default_config(rel_tol=1e-30, quiet=1, **over)
+    s = CpuBregShard(cfg, inst.dx, inst.dy, inst.mu, inst.nu, rank, world)
+    out = run_bregman_sharded([s], TorchComm(dist, rank, world, inplace_gather=False),
+                              cfg.max_iters)[0]
+    q.put((rank, out["final"], [t["objective"] for t in out["trace"]],
+           [t["phase"] for t in out["trace"]], out["iterations_used"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("over", [
+    dict(algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10, switch_iters=3, max_iters=7),
+    dict(algorithm=abi.BPG, step=5.0, inner_iters=10, max_iters=5, perturbation=0.01),
+], ids=["hbpg", "bpg"])
+def test_sharded_bregman_matches_oracle_gloo(port, world, over):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pno = _free_port()
+    procs = [ctx.Process(target=_bworker, args=(r, world, pno, over, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    inst = I.config1(seed=6, n=90)
+    cfg = abi.default_config(rel_tol=1e-30, quiet=1, **over)
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    assert o.code == 0, o.message
+    for _, final, objs, phases, used in res:
+        assert used == o.iterations_used
+        assert np.abs(final - o.final).max() <= 1e-10 * np.abs(o.final).max()
+        np.testing.assert_allclose(objs, [t["objective"] for t in o.trace], rtol=1e-9)
+        assert phases == [t["phase"] for t in o.trace]
