@@ -339,6 +339,16 @@ def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, worl
         flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         cfg = resolve_precision(cfg, bool(flag.item()))
+    if (not cfg.quiet and rank == 0 and cfg.algorithm in (abi.BPG, abi.HBPG)
+            and cfg.max_iters >= 1 and isinstance(dx, np.ndarray)):
+        # The BPG step-size warning (solvers.cpp:226-234) from the full
+        # host matrices: the fp64 device power iteration of lipschitz_bound.
+        from . import api
+        lip = api.lipschitz_bound(api.DistanceMatrix.trusted(dx), api.DistanceMatrix.trusted(dy))
+        if lip > 0.0 and cfg.step > 1.0 / lip:
+            import sys
+            print(f"bpg: step {cfg.step:g} exceeds sigma/L_f = {1.0 / lip:g}; descent is not "
+                  "guaranteed at this step size", file=sys.stderr)
     shard = BregShard(cfg, n, m, rank, world, device)
     try:
         dev = torch.device("cuda", device)
