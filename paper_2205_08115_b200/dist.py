@@ -339,16 +339,6 @@ def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, worl
         flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         cfg = resolve_precision(cfg, bool(flag.item()))
-    if (not cfg.quiet and rank == 0 and cfg.algorithm in (abi.BPG, abi.HBPG)
-            and cfg.max_iters >= 1 and isinstance(dx, np.ndarray)):
-        # The BPG step-size warning (solvers.cpp:226-234) from the full
-        # host matrices: the fp64 device power iteration of lipschitz_bound.
-        from . import api
-        lip = api.lipschitz_bound(api.DistanceMatrix.trusted(dx), api.DistanceMatrix.trusted(dy))
-        if lip > 0.0 and cfg.step > 1.0 / lip:
-            import sys
-            print(f"bpg: step {cfg.step:g} exceeds sigma/L_f = {1.0 / lip:g}; descent is not "
-                  "guaranteed at this step size", file=sys.stderr)
     shard = BregShard(cfg, n, m, rank, world, device)
     try:
         dev = torch.device("cuda", device)
@@ -356,9 +346,21 @@ def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, worl
             rows = np.zeros((1, n), dtype=np.float32)
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
         shard.load(t(rows), t(dy), mu, nu)
-        return run_bregman_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters)[0]
+        out = run_bregman_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters)[0]
     finally:
         shard.close()
+    ran_bpg = cfg.algorithm == abi.BPG or any(r.phase == 2 for r in out["trace"])
+    if not cfg.quiet and rank == 0 and ran_bpg and isinstance(dx, np.ndarray):
+        # The BPG step-size warning (solvers.cpp:226-234), printed when a BPG
+        # phase ran, as bregman_solve does; fp64 device power iteration on
+        # the full host matrices.
+        from . import api
+        lip = api.lipschitz_bound(api.DistanceMatrix.trusted(dx), api.DistanceMatrix.trusted(dy))
+        if lip > 0.0 and cfg.step > 1.0 / lip:
+            import sys
+            print(f"bpg: step {cfg.step:g} exceeds sigma/L_f = {1.0 / lip:g}; descent is not "
+                  "guaranteed at this step size", file=sys.stderr)
+    return out
 
 
 def bregman_shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, device=0,
