@@ -119,6 +119,33 @@ __device__ __forceinline__ void lse_add(OnlineLse<T>& a, T x, T w) {
   }
 }
 
+// a ⊕= K unit-weight terms at once: one max / rescale per block, the K
+// exponentials in fp32, summed, then added in the accumulator's type — the
+// bandwidth-bound form of K lse_add(a, x, 1) calls (equal up to rounding).
+template <int K, class T>
+__device__ __forceinline__ void lse_add_block(OnlineLse<T>& a, const T (&x)[K]) {
+  T mb = -INFINITY;
+  bool nan = false;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    nan = nan || isnan(x[q]);
+    mb = x[q] > mb ? x[q] : mb;
+  }
+  if (nan) {
+    a.mx = NAN;
+    return;
+  }
+  if (mb == -INFINITY) return;
+  if (mb > a.mx) {
+    a.s = lse_mul(a.s, lse_ex(a.mx - mb));
+    a.mx = mb;
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int q = 0; q < K; ++q) sum += __expf(static_cast<float>(x[q] - a.mx));
+  a.s += static_cast<T>(sum);
+}
+
 template <class T>
 __device__ __forceinline__ OnlineLse<T> lse_merge(OnlineLse<T> a, OnlineLse<T> b) {
   if (isnan(a.mx) || isnan(b.mx)) return OnlineLse<T>{static_cast<T>(NAN), static_cast<T>(NAN)};
