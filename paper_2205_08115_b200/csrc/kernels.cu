@@ -89,11 +89,15 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   }
 }
 
-// Narrow rows (m ≤ 128, e.g. config 3): one warp per row, 8 rows per CTA.
-// Lane l covers columns [4l, 4l+4) exactly as thread l does in the CTA-per-row
-// kernel, where only warp 0 holds data at this width — the shuffles and
-// merges are the same, so the results are bitwise identical.
+// Narrow rows (m ≤ kNarrowM, config 3): one warp per row, 8 rows per CTA,
+// lane l covering the float4 groups at columns 4l + 128v — the row sits in
+// registers between the (max, Σ) pass and the write, no block barriers.
+// For m ≤ 128 the lane assignment is that of the CTA-per-row kernel (where
+// only warp 0 holds data at that width), so the results are bitwise
+// identical.  Widening to m ≤ 1024 (config 1) measured slower on the same
+// box (7906–7961 vs 8048 it/s: 125 CTAs for n = 1000 rows), so it stays 128.
 constexpr int kNarrowM = 128;
+constexpr int kNarrowV = kNarrowM / 128;  // float4 groups per lane
 constexpr int kWarpRows = kRowThreads / 32;
 
 __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d, int write, int tail) {
@@ -105,15 +109,24 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
   const float* w = d.W + i * d.ld;
   const int64_t m = d.m;
   const float inv_rho = d.inv_rho;
-  const int64_t j = lane * 4;
   MaxSum ms{-INFINITY, 0.f};
   double sums[2] = {0.0, 0.0};
-  float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), w4 = g4;
-  if (j < m) {
-    g4 = *reinterpret_cast<const float4*>(g + j);
-    w4 = *reinterpret_cast<const float4*>(w + j);
-    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+  float4 g4[kNarrowV], w4[kNarrowV];
+#pragma unroll
+  for (int v = 0; v < kNarrowV; ++v) {
+    const int64_t j = lane * 4 + 128 * v;
+    g4[v] = w4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < m) {
+      g4[v] = *reinterpret_cast<const float4*>(g + j);
+      w4[v] = *reinterpret_cast<const float4*>(w + j);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < kNarrowV; ++v) {
+    const int64_t j = lane * 4 + 128 * v;
+    if (j >= m) break;
+    const float gv[4] = {g4[v].x, g4[v].y, g4[v].z, g4[v].w};
+    const float wv[4] = {w4[v].x, w4[v].y, w4[v].z, w4[v].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
@@ -145,15 +158,19 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
       atomicMin(&d.st->zero_index, static_cast<int>(i));
     }
   }
-  if (j >= m) return;
   const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
-  float4 o;
-  o.x = (j + 0 < m) ? scale * w4.x * __expf(__fsub_rn(__fmul_rn(g4.x, inv_rho), r)) : 0.f;
-  o.y = (j + 1 < m) ? scale * w4.y * __expf(__fsub_rn(__fmul_rn(g4.y, inv_rho), r)) : 0.f;
-  o.z = (j + 2 < m) ? scale * w4.z * __expf(__fsub_rn(__fmul_rn(g4.z, inv_rho), r)) : 0.f;
-  o.w = (j + 3 < m) ? scale * w4.w * __expf(__fsub_rn(__fmul_rn(g4.w, inv_rho), r)) : 0.f;
-  *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
-  if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
+#pragma unroll
+  for (int v = 0; v < kNarrowV; ++v) {
+    const int64_t j = lane * 4 + 128 * v;
+    if (j >= m) break;
+    float4 o;
+    o.x = (j + 0 < m) ? scale * w4[v].x * __expf(__fsub_rn(__fmul_rn(g4[v].x, inv_rho), r)) : 0.f;
+    o.y = (j + 1 < m) ? scale * w4[v].y * __expf(__fsub_rn(__fmul_rn(g4[v].y, inv_rho), r)) : 0.f;
+    o.z = (j + 2 < m) ? scale * w4[v].z * __expf(__fsub_rn(__fmul_rn(g4[v].z, inv_rho), r)) : 0.f;
+    o.w = (j + 3 < m) ? scale * w4[v].w * __expf(__fsub_rn(__fmul_rn(g4[v].w, inv_rho), r)) : 0.f;
+    *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
+    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   }
 }
 
-// col_write for narrow rows (m ≤ 128): one warp per row, as row_update_warps.
+// col_write for narrow rows (m ≤ 1024): one warp per row, as row_update_warps.
 __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d) {
   if (d.st->done) return;
   if (d.st->flags != 0) return;
@@ -309,11 +326,13 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
   if (i >= d.n) return;
   const int64_t m = d.m;
-  const int64_t j = lane * 4;
   const float inv_rho = d.inv_rho;
   double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
   bool finite = true;
-  if (j < m) {
+#pragma unroll 2
+  for (int v = 0; v < kNarrowV; ++v) {
+    const int64_t j = lane * 4 + 128 * v;
+    if (j >= m) break;
     const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + j);
     const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + j);
     const float4 w4 = *reinterpret_cast<const float4*>(d.W + i * d.ld + j);
