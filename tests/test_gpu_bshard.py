@@ -55,6 +55,15 @@ def test_sharded_bregman_matches_oracle(gpu, port, world, algo, over):
     _check(outs, o)
 
 
+def test_sharded_hbpg_empty_ranks(gpu, port):
+    # n = 100 over 4 ranks: 64-row shards, so ranks 2 and 3 own no rows.
+    inst = I.config1(seed=9, n=100)
+    outs, cfg = _run(inst, 4, algorithm=abi.HBPG, epsilon_reg=0.1, step=5.0, inner_iters=10,
+                     switch_iters=2, max_iters=5)
+    o = port.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+    _check(outs, o)
+
+
 def test_sharded_hbpg_weighted_d_3xtf32(gpu, port):
     # Euclidean D: AUTO resolves to 3xTF32 (dist.resolve_precision).
     g = I.config2(seed=4, n=150, m=120)
