@@ -390,10 +390,14 @@ class TorchComm:
         self.inplace = inplace_gather
 
     def _gather(self, buf):
-        view = buf.view(self.world, -1)
         if self.inplace:
-            self.dist.all_gather_into_tensor(view, view[self.rank])
+            # 1-D concatenation form (NCCL and gloo both accept it): rank r's
+            # block of the flat buffer is its input, in place.
+            flat = buf.view(-1)
+            c = flat.numel() // self.world
+            self.dist.all_gather_into_tensor(flat, flat[self.rank * c:(self.rank + 1) * c])
         else:
+            view = buf.view(self.world, -1)
             parts = list(view.unbind(0))
             self.dist.all_gather(parts, view[self.rank].clone())
 

@@ -33,7 +33,7 @@ def _worker(rank, world, port, n, iters, rel_tol, q, overlap=False):
     inst = I.config1(seed=9, n=n)
     s = CpuShard(inst.dx, inst.dy, inst.mu, inst.nu, 0.1, rank, world, iters, rel_tol)
     s.reset()
-    st = run_sharded([s], TorchComm(dist, rank, world, inplace_gather=False), iters, poll_every=4,
+    st = run_sharded([s], TorchComm(dist, rank, world), iters, poll_every=4,
                      overlap=overlap)
     used = st["iter"] - 1
     pi, w = s.rows()
@@ -110,7 +110,7 @@ def _bworker(rank, world, port, over, q):
     inst = I.config1(seed=6, n=90)
     cfg = abi.default_config(rel_tol=1e-30, quiet=1, **over)
     s = CpuBregShard(cfg, inst.dx, inst.dy, inst.mu, inst.nu, rank, world)
-    out = run_bregman_sharded([s], TorchComm(dist, rank, world, inplace_gather=False),
+    out = run_bregman_sharded([s], TorchComm(dist, rank, world),
                               cfg.max_iters)[0]
     q.put((rank, out["final"], [t["objective"] for t in out["trace"]],
            [t["phase"] for t in out["trace"]], out["iterations_used"]))
