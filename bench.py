@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", dest="n", type=int, default=20000)
-    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2", "f16x2"])
     ap.add_argument("--e2e-iters", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -264,11 +264,12 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------------------
-PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6}
-PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32"}
+PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6,
+              "f16x2": 7}
+PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2"}
 # tensor passes per chain GEMM for 0/1 structure matrices, and the MMA kind
 PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16"), 5: (0, "none"),
-               6: (0, "fp32 FMA")}
+               6: (0, "fp32 FMA"), 7: (2, "f16")}
 
 
 def time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks=None):
@@ -347,7 +348,7 @@ def run_ours(args, world, rank, local, dist):
     main = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks)
     variants = {}
     if not args.no_variants:
-        for name in ("3xtf32", "bf16x2", "sparse"):
+        for name in ("bf16x3", "3xtf32", "bf16x2", "sparse"):
             if PREC_NAMES[name] == main["precision"]:
                 continue
             v = time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, PREC_NAMES[name],
@@ -375,23 +376,33 @@ def run_ours(args, world, rank, local, dist):
     achieved = chain_flops / (main["chain_ms"] * 1e-3) / 1e12 if main["chain_ms"] > 0 else None
     passes, kind = PREC_PASSES[main["precision"]]
     label = PREC_LABEL[main["precision"]]
-    exec_peak = peaks.get("bf16_tflops_sustained") if kind == "bf16" else tf32_peak
+    f16_pipe = kind in ("bf16", "f16")
+    exec_peak = peaks.get("bf16_tflops_sustained") if f16_pipe else tf32_peak
+    # Roofline of the chain as executed: split-operand passes share the
+    # kind::f16 (bf16 / fp16, same dense rate) or kind::tf32 tensor peak, so
+    # the algorithmic FLOP/s it can reach is that peak ÷ passes.  The
+    # north-star TF32 roofline (cuBLAS TF32 sustained, measured in this run)
+    # is reported beside it.
+    peak = (exec_peak / passes) if (exec_peak and passes) else tf32_peak
     roofline = {
         "bound": "tensor",
         "kernel": "gemm_tf32_kernel, CTA-pair tcgen05 (D_Y·πᵀ then D_X·V per half-step)",
         "achieved": achieved, "unit": "TFLOP/s",
-        "peak": tf32_peak,
-        "peak_source": "FP32-accumulate TF32 roofline: cuBLAS TF32 sustained, measured in this "
-                       f"run ({tf32['how'] if tf32 else ''}; MEASURED_PEAKS.json carries bf16 "
-                       f"only; {peak_src})",
-        "peak_burst": tf32["burst"] if tf32 else None,
-        "frac_of_burst": (achieved / tf32["burst"]) if (achieved and tf32) else None,
-        "frac": (achieved / tf32_peak) if (achieved and tf32_peak) else None,
+        "peak": peak,
+        "peak_source": (f"measured {'bf16/fp16' if f16_pipe else 'TF32'} dense sustained peak "
+                        f"({'MEASURED_PEAKS.json bf16_tflops_sustained' if f16_pipe else 'cuBLAS TF32, this run'}) "
+                        f"/ {passes} split passes ({label}, fp32 accumulate)"),
+        "frac": (achieved / peak) if (achieved and peak) else None,
+        "tf32_roofline": tf32_peak,
+        "tf32_roofline_source": "FP32-accumulate TF32 roofline (north star): cuBLAS TF32 sustained, "
+                                f"measured in this run ({tf32['how'] if tf32 else ''}; {peak_src})",
+        "tf32_roofline_burst": tf32["burst"] if tf32 else None,
+        "frac_vs_tf32_roofline": (achieved / tf32_peak) if (achieved and tf32_peak) else None,
         "precision": label, "passes": passes, "mma_kind": kind,
         "executed_tflops": achieved * passes if achieved else None,
         "executed_peak": exec_peak,
-        "executed_peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained" if kind == "bf16"
-                                 else "cuBLAS TF32 measured in this run"),
+        "executed_peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (fp16 and bf16 share "
+                                 "the kind::f16 rate)" if f16_pipe else "cuBLAS TF32 measured in this run"),
         "executed_frac": (achieved * passes / exec_peak) if (achieved and exec_peak) else None,
         "algorithmic_flops_per_launch_pair": chain_flops,
         "traffic": gemm_traffic(n),

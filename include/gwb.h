@@ -52,7 +52,10 @@ enum gwb_precision {
   GWB_PREC_BF16X3 = 3,  /* exact-bf16 D × 3 bf16 planes of the iterate (24-bit) */
   GWB_PREC_BF16X2 = 4,  /* exact-bf16 D × 2 bf16 planes (16-bit) */
   GWB_PREC_SPARSE = 5,  /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
-  GWB_PREC_FP32 = 6     /* FP32-pipe chain for skinny problems (m ≤ 32); AUTO picks it */
+  GWB_PREC_FP32 = 6,    /* FP32-pipe chain for skinny problems (m ≤ 32); AUTO picks it */
+  GWB_PREC_F16X2 = 7    /* exact-fp16 D × 2 fp16 planes of the power-of-two-scaled
+                           iterate (22-bit operands); AUTO picks it for 0/1 graphs
+                           (single-GPU BAPG; other solvers run it as bf16x3) */
 };
 
 /* Error codes; each maps to one reference exception class. */

@@ -587,8 +587,9 @@ class BregmanEngine {
       rows_alloc_ = npad_;
       // The chain precision is fixed up front (resolved by the orchestrator):
       // it sets the exchange-buffer layout the caller allocates.
+      // f16x2 is a single-GPU BAPG chain; here it runs as bf16x3.
       const int req = cfg_.precision;
-      aux_mode_ = req == GWB_PREC_BF16X3 ? 3 : req == GWB_PREC_BF16X2 ? 4 : 2;
+      aux_mode_ = (req == GWB_PREC_BF16X3 || req == GWB_PREC_F16X2) ? 3 : req == GWB_PREC_BF16X2 ? 4 : 2;
       planes_ = aux_mode_ == 3 ? 3 : 2;
       esize_ = aux_mode_ >= 3 ? 2 : 4;
     }
@@ -943,7 +944,9 @@ class BregmanEngine {
     GWB_CUDA(cudaStreamSynchronize(s_));
     const bool bf16_exact = (h[0] & 2) == 0 && (h[1] & 2) == 0;
     const int req = cfg_.precision;
-    if (bf16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_BF16X3)) aux_mode_ = 3;
+    // f16x2 is a single-GPU BAPG chain; the Bregman solvers run it as bf16x3.
+    if (bf16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_BF16X3 || req == GWB_PREC_F16X2))
+      aux_mode_ = 3;
     else if (bf16_exact && req == GWB_PREC_BF16X2) aux_mode_ = 4;
     else aux_mode_ = 2;
     if (aux_mode_ >= 3) {

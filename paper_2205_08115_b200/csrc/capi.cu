@@ -166,7 +166,7 @@ void validate_config(const gwb_config* c) {
   if (c->perturbation < 0.0 || c->perturbation >= 1.0)
     fail(GWB_ERR_CONFIG, "perturbation must lie in [0, 1)");
   if (c->switch_iters < 0) fail(GWB_ERR_CONFIG, "switch-iters must be >= 0");
-  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_FP32)
+  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_F16X2)
     fail(GWB_ERR_CONFIG, "unknown precision");
 }
 
@@ -717,7 +717,7 @@ int32_t gwb_bshard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t r
     if (n < 1 || m < 1 || world < 1 || rank < 0 || rank >= world)
       fail(GWB_ERR_DIMENSION, "gwb_bshard_create: bad shape or rank");
     if (cfg->precision != GWB_PREC_BF16X3 && cfg->precision != GWB_PREC_BF16X2 &&
-        cfg->precision != GWB_PREC_3XTF32)
+        cfg->precision != GWB_PREC_3XTF32 && cfg->precision != GWB_PREC_F16X2)
       fail(GWB_ERR_CONFIG,
            "gwb_bshard_create: resolve the precision across ranks first (bf16x3, bf16x2 or 3xtf32)");
     if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual is single-GPU only");

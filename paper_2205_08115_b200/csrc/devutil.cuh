@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -53,12 +54,31 @@ __device__ __forceinline__ float aux_of(float x, int mode) {
 // GEMM operand copy of 4 consecutive values at element offset `off`:
 //   mode 1/2: one fp32 plane (rna_tf32(x) or x − trunc_tf32(x));
 //   mode 3/4: 3 or 2 bf16 planes, `plane` elements apart, whose sum is x
-//             (round-to-nearest splits hi = rn(x), mid = rn(x − hi), …).
+//             (round-to-nearest splits hi = rn(x), mid = rn(x − hi), …);
+//   mode 5:   2 fp16 planes of x·scale (scale a power of two chosen by the
+//             caller so that x·scale stays inside fp16 range; f16x2).
 __device__ __forceinline__ void aux_store4(float* aux, int mode, int64_t plane, int64_t off,
-                                           float a, float b, float c, float d) {
+                                           float a, float b, float c, float d,
+                                           float scale = 1.0f) {
   if (mode <= 2) {
     *reinterpret_cast<float4*>(aux + off) =
         make_float4(aux_of(a, mode), aux_of(b, mode), aux_of(c, mode), aux_of(d, mode));
+    return;
+  }
+  if (mode == 5) {
+    __half* base = reinterpret_cast<__half*>(aux);
+    float v[4] = {a * scale, b * scale, c * scale, d * scale};
+    for (int pl = 0; pl < 2; ++pl) {
+      __half h[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        h[q] = __float2half_rn(v[q]);
+        v[q] -= __half2float(h[q]);
+      }
+      *reinterpret_cast<uint2*>(base + pl * plane + off) =
+          make_uint2(__half_as_ushort(h[0]) | (static_cast<uint32_t>(__half_as_ushort(h[1])) << 16),
+                     __half_as_ushort(h[2]) | (static_cast<uint32_t>(__half_as_ushort(h[3])) << 16));
+    }
     return;
   }
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(aux);

@@ -28,6 +28,7 @@
 #include <stdexcept>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "gemm.cuh"
 #include "ptx.cuh"
@@ -53,6 +54,29 @@ constexpr uint32_t kStageBytes = kABytes + kBBytes;  // per CTA
 constexpr uint32_t kTmemCols = 2 * kBN;    // double-buffered accumulator
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
+// Round-to-nearest split of 8 fp32 values into three planes whose sum is x
+// (hi = rn(x), mid = rn(x − hi), lo = rn(x − hi − mid); each difference is
+// exact in fp32), as raw bf16 or fp16 bits.  A 2-plane consumer reads hi and
+// mid, i.e. rn(x − hi).
+__device__ __forceinline__ void split_planes8(const float* x, bool f16, uint16_t (&h)[3][8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float r = x[q];
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl) {
+      if (f16) {
+        const __half v = __float2half_rn(r);
+        h[pl][q] = __half_as_ushort(v);
+        r -= __half2float(v);
+      } else {
+        const __nv_bfloat16 v = __float2bfloat16_rn(r);
+        h[pl][q] = __bfloat16_as_ushort(v);
+        r -= __bfloat162float(v);
+      }
+    }
+  }
+}
+
 struct __align__(64) GemmParams {
   CUtensorMap a_map[2];
   CUtensorMap b_map[3];
@@ -62,10 +86,12 @@ struct __align__(64) GemmParams {
   int32_t b_sel[3];
   int32_t tiles_m, tiles_n;  // tiles_m counts 256-row pair tiles
   int32_t chunk;  // k-blocks accumulated in TMEM before promotion to registers
-  int32_t kind;   // 0: kind::tf32 (fp32 operands), 1: kind::f16 (bf16 operands)
+  int32_t kind;   // 0: kind::tf32 (fp32 operands), 1: kind::f16 with bf16
+                  // operands, 2: kind::f16 with fp16 operands
   int32_t b_block_k;  // > 0: B maps are 3-D [K/b_block_k][N][b_block_k]
   int32_t c_planes;
-  __nv_bfloat16* c_pl[3];
+  int32_t c_f16;  // output planes are fp16 (else bf16)
+  uint16_t* c_pl[3];
   float* c;
   float* c_aux;
   int64_t ldc;
@@ -180,7 +206,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && ptx::elect_one()) {
-      const uint32_t idesc = p.kind ? ptx::idesc_bf16(kPairM, kBN) : ptx::idesc_tf32(kPairM, kBN);
+      const uint32_t idesc = p.kind == 2   ? ptx::idesc_f16(kPairM, kBN)
+                             : p.kind == 1 ? ptx::idesc_bf16(kPairM, kBN)
+                                           : ptx::idesc_tf32(kPairM, kBN);
       for (int c = 0; c < nchunks; ++c) {
         const int b = c & 1;
         ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
@@ -260,28 +288,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc[j] = round_out ? rna_tf32(x) : x;
       }
       if (p.c_planes > 0) {
-        // bf16 split planes (RN): x ≈ hi + mid (+ lo), for a bf16-split GEMM.
+        // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
+        // split-operand GEMM.
         const int64_t off = static_cast<int64_t>(row) * p.ldc + col0;
         const bool vec = col0 + kSliceCols <= p.N && (p.ldc & 7) == 0;
 #pragma unroll
         for (int j0 = 0; j0 < kSliceCols; j0 += 8) {
-          __align__(16) __nv_bfloat16 h[3][8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float r = acc[j0 + q];
-            h[0][q] = __float2bfloat16_rn(r);
-            r -= __bfloat162float(h[0][q]);
-            h[1][q] = __float2bfloat16_rn(r);
-            r -= __bfloat162float(h[1][q]);
-            h[2][q] = __float2bfloat16_rn(r);
-          }
+          __align__(16) uint16_t h[3][8];
+          split_planes8(acc + j0, p.c_f16 != 0, h);
           for (int pl = 0; pl < p.c_planes; ++pl) {
-            if (pl == 1 && p.c_planes == 2) {  // x2: lo = rn(x − hi)
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                h[1][q] = __float2bfloat16_rn(acc[j0 + q] - __bfloat162float(h[0][q]));
-            }
-            __nv_bfloat16* dst = p.c_pl[pl] + off + j0;
+            uint16_t* dst = p.c_pl[pl] + off + j0;
             if (vec) {
               *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h[pl]);
             } else {
@@ -370,17 +386,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     const int64_t off = static_cast<int64_t>(row) * p.ldc + c0;
     const bool full = c0 + 8 <= p.N;
     if (p.c_planes > 0) {
-      alignas(16) __nv_bfloat16 h[3][8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float r = x[q];
-        h[0][q] = __float2bfloat16_rn(r);
-        r -= __bfloat162float(h[0][q]);
-        h[1][q] = __float2bfloat16_rn(r);
-        r -= __bfloat162float(h[1][q]);
-        h[2][q] = __float2bfloat16_rn(r);
-        if (p.c_planes == 2) h[1][q] = __float2bfloat16_rn(x[q] - __bfloat162float(h[0][q]));
-      }
+      alignas(16) uint16_t h[3][8];
+      split_planes8(x, p.c_f16 != 0, h);
       for (int pl = 0; pl < p.c_planes; ++pl) {
         if (full) {
           *reinterpret_cast<uint4*>(p.c_pl[pl] + off) = *reinterpret_cast<const uint4*>(h[pl]);
@@ -508,8 +515,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.a_sel[0] = 0;
   g.b_sel[0] = 0;
   if (d.bf16_planes > 0) {
-    // Σ_p A·B_p over bf16 planes (A exact in bf16).
-    g.kind = 1;
+    // Σ_p A·B_p over bf16 (or fp16) planes (A exact in that format).
+    g.kind = d.f16 ? 2 : 1;
     g.a_map[0] = make_map(d.a_bf16, d.M, d.K, d.lda, kBM, 2);
     g.a_map[1] = g.a_map[0];
     for (int pl = 0; pl < d.bf16_planes; ++pl) {
@@ -559,7 +566,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.ldc = d.ldc;
   g.aux_mode = d.aux_mode;
   g.c_planes = d.c_planes;
-  for (int pl = 0; pl < 3; ++pl) g.c_pl[pl] = static_cast<__nv_bfloat16*>(d.c_bf16[pl]);
+  g.c_f16 = d.f16 ? 1 : 0;
+  for (int pl = 0; pl < 3; ++pl) g.c_pl[pl] = static_cast<uint16_t*>(d.c_bf16[pl]);
   g.row_scale = d.row_scale;
   g.col_scale = d.col_scale;
   g.accumulate = d.accumulate ? 1 : 0;

@@ -47,6 +47,11 @@ struct GemmDesc {
   // of fp32 `c`: c_planes ∈ {0, 2, 3}; planes are M×N with leading dim ldc.
   int c_planes = 0;
   void* c_bf16[3] = {nullptr, nullptr, nullptr};
+  // fp16 instead of bf16 for A, the B planes and the output planes
+  // (kind::f16 with fp16 operands): 11-bit planes, so two planes carry a
+  // 22-bit operand.  The caller keeps every plane inside fp16 range with
+  // power-of-two scales folded into row_scale / col_scale.
+  bool f16 = false;
   // Blocked-K B operand (multi-GPU all-gather layout): when b_block_k > 0,
   // every B plane is stored as [K / b_block_k][N][b_block_k] (leading dim of
   // a block row = b_block_k); b_block_k must be a multiple of the k-block

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
     o.z = (j + 2 < m) ? scale * w4.z * __expf(__fsub_rn(__fmul_rn(g4.z, inv_rho), r)) : 0.f;
     o.w = (j + 3 < m) ? scale * w4.w * __expf(__fsub_rn(__fmul_rn(g4.w, inv_rho), r)) : 0.f;
     *reinterpret_cast<float4*>(p + j) = o;
-    if (d.P_aux) aux_store4(d.P_aux, am, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
+    if (d.P_aux) aux_store4(d.P_aux, am, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w, d.aux_scale);
   }
 }
 
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
     o.z = (j + 2 < m) ? scale * w4[v].z * __expf(__fsub_rn(__fmul_rn(g4[v].z, inv_rho), r)) : 0.f;
     o.w = (j + 3 < m) ? scale * w4[v].w * __expf(__fsub_rn(__fmul_rn(g4[v].w, inv_rho), r)) : 0.f;
     *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
-    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w);
+    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w, d.aux_scale);
   }
 }
 
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
       }
     }
     *reinterpret_cast<float4*>(wn + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (d.W_aux) aux_store4(d.W_aux, am, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3]);
+    if (d.W_aux) aux_store4(d.W_aux, am, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3], d.aux_scale);
   }
   MaxSum dummy{-INFINITY, 0.f};
   block_reduce<kRowThreads, 5>(dummy, sums);
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
       }
     }
     *reinterpret_cast<float4*>(d.W_new + i * d.ld + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3]);
+    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3], d.aux_scale);
   }
 #pragma unroll
   for (int q = 0; q < 5; ++q) sums[q] = warp_sum(sums[q]);
@@ -535,12 +535,12 @@ __global__ void average64_kernel(const double* a, const double* b, double* dst, 
 }
 
 __global__ void tf32_aux_kernel(const float* x, int64_t rows, int64_t cols, int64_t ld,
-                                float* out, int mode, int64_t plane) {
+                                float* out, int mode, int64_t plane, float scale) {
   const int64_t i = blockIdx.x;
   // ld is a multiple of 32, so whole float4 groups stay inside the row pitch.
   for (int64_t j = threadIdx.x * 4; j < cols; j += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(x + i * ld + j);
-    aux_store4(out, mode, plane, i * ld + j, v.x, v.y, v.z, v.w);
+    aux_store4(out, mode, plane, i * ld + j, v.x, v.y, v.z, v.w, scale);
   }
 }
 
@@ -549,6 +549,39 @@ __global__ void to_bf16_kernel(const float* x, int64_t rows, int64_t cols, int64
   const int64_t i = blockIdx.x;
   for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
     out[i * ld + j] = __float2bfloat16_rn(x[i * ld + j]);
+}
+
+__global__ void to_f16_kernel(const float* x, int64_t rows, int64_t cols, int64_t ld, __half* out) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+    out[i * ld + j] = __float2half_rn(x[i * ld + j]);
+}
+
+// f16x2 row scales of the GEMM1 output Vᵀ = D_Y·Xᵀ (f16x2).
+// Row i of Vᵀ is bounded a priori by x_max · Σ_l |D_Y[i][l]| (x_max bounds
+// every iterate entry: π_kl ≤ μ_k, w_kl ≤ ν_l), so σ_i = 14 − ⌈log2 bound⌉
+// keeps Vᵀ[i,:]·2^σ_i ≤ 2^14 inside fp16 range.  GEMM1 accumulates
+// 2^s1·Vᵀ (its B planes carry 2^s1), so its row scale is 2^(σ_i − s1);
+// GEMM2's column scale 2^−σ_j undoes σ.  All scales are powers of two.
+__global__ void f16_scales_kernel(const float* D, int64_t m, int64_t ld, float x_max, int s1,
+                                  float* g1_row_scale, float* g2_col_scale) {
+  const int64_t i = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t l = threadIdx.x; l < m; l += blockDim.x) acc += fabs(static_cast<double>(D[i * ld + l]));
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) sum += part[w];
+    const double bound = static_cast<double>(x_max) * sum;
+    int sigma = 0;
+    if (bound > 0.0) sigma = 14 - static_cast<int>(ceil(log2(bound)));
+    sigma = max(-100, min(100, sigma));
+    g1_row_scale[i] = ldexpf(1.0f, sigma - s1);
+    g2_col_scale[i] = ldexpf(1.0f, -sigma);
+  }
 }
 
 __global__ void product_coupling_kernel(const float* mu, const float* nu, int64_t n, int64_t m,
@@ -573,6 +606,7 @@ __global__ void analyze_kernel(const float* D, int64_t rows, int64_t cols, int64
     mx = fmaxf(mx, v);
     inexact |= (v != trunc_tf32(v)) ? 1 : 0;
     inexact |= (v != bf16_round(v)) ? 2 : 0;
+    inexact |= (fabsf(v) > 65504.0f || v != __half2float(__float2half_rn(v))) ? 4 : 0;
   }
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -661,9 +695,21 @@ void launch_average64(const double* a, const double* b, double* dst, int64_t len
 }
 
 void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
-                     cudaStream_t s) {
+                     cudaStream_t s, float scale) {
   tf32_aux_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld, out, mode,
-                                                               rows * ld);
+                                                               rows * ld, scale);
+}
+
+void launch_to_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
+                   cudaStream_t s) {
+  to_f16_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, rows, cols, ld,
+                                                            static_cast<__half*>(out));
+}
+
+void launch_f16_scales(const float* D, int64_t m, int64_t ld, float x_max, int s1,
+                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s) {
+  f16_scales_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(D, m, ld, x_max, s1, g1_row_scale,
+                                                             g2_col_scale);
 }
 
 void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,

@@ -82,6 +82,8 @@ struct BapgDev {
   int aux_mode;             // 1: aux = rna_tf32(x) (1xTF32 operand)
                             // 2: aux = x − trunc_tf32(x) (3xTF32 residual)
                             // 3/4: 3 / 2 bf16 split planes (bf16x3 / bf16x2)
+                            // 5: 2 fp16 split planes of x·aux_scale (f16x2)
+  float aux_scale;          // power of two (mode 5), else 1
   int64_t plane;            // elements per bf16 plane (n·ld)
   RowPart* row_part;        // n
   ColWritePart* cw_part;    // n
@@ -129,14 +131,24 @@ void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t col
 // dst = 0.5 (a + b), column-major fp64 of len elements.
 void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s);
 // GEMM operand copy of x (ld multiple of 4): mode 1: rna_tf32(x);
-// 2: x − trunc_tf32(x); 3/4: 3 or 2 bf16 split planes (plane = rows·ld).
+// 2: x − trunc_tf32(x); 3/4: 3 or 2 bf16 split planes (plane = rows·ld);
+// 5: 2 fp16 split planes of x·scale.
 void launch_tf32_aux(const float* x, int64_t rows, int64_t cols, int64_t ld, float* out, int mode,
-                     cudaStream_t s);
+                     cudaStream_t s, float scale = 1.0f);
+// out (fp16, same ld) = fp16_rn(x).
+void launch_to_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
+                   cudaStream_t s);
+// f16x2 power-of-two scales (kernels.cu: f16_scales_kernel): per row i of
+// the m×m structure matrix D, σ_i = 14 − ⌈log2(x_max · Σ_l |D[i][l]|)⌉;
+// g1_row_scale[i] = 2^(σ_i − s1), g2_col_scale[i] = 2^−σ_i.
+void launch_f16_scales(const float* D, int64_t m, int64_t ld, float x_max, int s1,
+                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s);
 // out (bf16, same ld) = bf16_rn(x).
 void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
                     cudaStream_t s);
-// Scans a structure matrix: *out_max = max entry, *out_inexact = 1 if any
-// entry is not exactly representable in TF32 (0/1 adjacency is exact).
+// Scans a structure matrix: *out_max = max entry, *out_inexact bit 1 if any
+// entry is not exactly representable in TF32, bit 2 in bf16, bit 4 in fp16
+// (0/1 adjacency is exact in all three).
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
                     int* out_inexact, cudaStream_t s);
 // P = μ νᵀ (product coupling, types.cpp:204-207) in row-major fp32.

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) row_quad_kernel(BapgDev d) {
       }
     }
     *reinterpret_cast<float4*>(p + j0) = make_float4(o[0], o[1], o[2], o[3]);
-    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j0, o[0], o[1], o[2], o[3]);
+    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j0, o[0], o[1], o[2], o[3], d.aux_scale);
   }
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0) atomicOr(&d.st->flags, kFlagNonFinite);
 }
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) quad_col_diag_kernel(BapgDev d) {
         sums[4] += gv * pv;
       }
     }
-    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j0, n4.x, n4.y, n4.z, n4.w);
+    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j0, n4.x, n4.y, n4.z, n4.w, d.aux_scale);
   }
   MaxSum dummy{-INFINITY, 0.f};
   block_reduce<kThreads, 5>(dummy, sums);

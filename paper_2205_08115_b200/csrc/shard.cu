@@ -232,7 +232,8 @@ class ShardEngine {
     if (cfg.precision == GWB_PREC_AUTO)
       throw std::invalid_argument(
           "gwb_shard_create: resolve AUTO precision across ranks first (bf16x3 or 3xtf32)");
-    prec_ = cfg.precision;
+    // f16x2 is the single-GPU BAPG chain; the row-sharded chain runs bf16x3.
+    prec_ = cfg.precision == GWB_PREC_F16X2 ? GWB_PREC_BF16X3 : cfg.precision;
     bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2;
     planes_ = prec_ == GWB_PREC_BF16X3 ? 3 : (prec_ == GWB_PREC_TF32 ? 1 : 2);
     esize_ = bf16_ ? 2 : 4;

@@ -72,18 +72,17 @@ namespace {
 
 }  // namespace
 
-int resolve_precision(int requested, bool d_exact, double dmax_x, double dmax_y, double rho) {
-  if (requested == GWB_PREC_TF32 || requested == GWB_PREC_3XTF32) return requested;
-  // AUTO (measured on B200): a 3-term split with fp32
-  // accumulate.  When both structure matrices are exact in bf16 (0/1
-  // graphs) the split runs as bf16x3 — D × (hi + mid + lo) bf16 planes,
-  // 24-bit operands, 1.5 TF32-pass equivalents — otherwise as 3xTF32.
-  // 1xTF32 misses the 1e-5 objective bound and bf16x2 is reduced precision;
-  // both stay explicit opt-ins.
-  (void)dmax_x;
-  (void)dmax_y;
-  (void)rho;
-  return d_exact ? GWB_PREC_BF16X3 : GWB_PREC_3XTF32;
+int resolve_precision(int requested, bool bf16_exact, bool f16_exact) {
+  if (requested != GWB_PREC_AUTO) return requested;
+  // AUTO (measured on B200): a split-operand chain with fp32
+  // accumulate, at least as precise as 3xTF32.  When both structure
+  // matrices are exact in fp16 (0/1 graphs) it runs as f16x2 — D × (hi +
+  // lo) fp16 planes of the power-of-two-scaled iterate, 22-bit operands in
+  // 2 kind::f16 passes; exact in bf16 only: bf16x3 (24-bit, 3 passes);
+  // otherwise 3xTF32.  1xTF32 misses the 1e-5 objective bound and bf16x2
+  // (16-bit operands) is reduced precision; both stay explicit opt-ins.
+  if (f16_exact) return GWB_PREC_F16X2;
+  return bf16_exact ? GWB_PREC_BF16X3 : GWB_PREC_3XTF32;
 }
 
 BapgEngine::BapgEngine(int device, int64_t n, int64_t m, double rho, int precision,
@@ -129,7 +128,7 @@ BapgEngine::~BapgEngine() {
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], Vt_,
            Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
-           col_max_, col_scale_, col_psump_, col_dev_, st_, rec_})
+           col_max_, col_scale_, col_psump_, col_dev_, st_, rec_, f16_g1_rs_, f16_g2_cs_})
     dfree(p, stream_);
   if (h_done_) cudaFreeHost(h_done_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
@@ -195,6 +194,7 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.W_new = W_[1 - q];
   d.W_aux = no_planes() ? nullptr : W_aux_[1 - q];
   d.aux_mode = aux_mode();
+  d.aux_scale = aux_scale();
   d.plane = n_ * ldm_;
   d.row_part = row_part_;
   d.cw_part = cw_part_;
@@ -272,10 +272,13 @@ void BapgEngine::prepare_d() {
     return;
   }
   const bool bf16_exact = (h_inexact[0] & 2) == 0 && (h_inexact[1] & 2) == 0;
+  const bool f16_exact = (h_inexact[0] & 4) == 0 && (h_inexact[1] & 4) == 0;
   if (precision_ == GWB_PREC_AUTO)
-    precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, h_max[0], h_max[1], rho_);
-  // bf16 splits need exactly representable structure matrices (0/1 graphs);
-  // otherwise fall back to 3xTF32, which splits both operands.
+    precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, f16_exact);
+  // Split-plane chains need exactly representable structure matrices (0/1
+  // graphs); otherwise fall back to bf16x3 (f16x2 only) or 3xTF32, which
+  // splits both operands.
+  if (precision_ == GWB_PREC_F16X2 && !f16_exact) precision_ = GWB_PREC_BF16X3;
   if ((precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2) && !bf16_exact)
     precision_ = GWB_PREC_3XTF32;
   if (precision_ != GWB_PREC_TF32 && !Vt_aux_)
@@ -283,8 +286,18 @@ void BapgEngine::prepare_d() {
   if (bf16()) {
     if (!Dx_bf_) Dx_bf_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_ / 2 + 16);
     if (!Dy_bf_) Dy_bf_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_ / 2 + 16);
-    launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
-    launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
+    if (f16()) {
+      launch_to_f16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
+      launch_to_f16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
+      f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(std::max(x_max_, 1e-30))));
+      if (!f16_g1_rs_) f16_g1_rs_ = dalloc<float>(stream_, ldm_);
+      if (!f16_g2_cs_) f16_g2_cs_ = dalloc<float>(stream_, ldm_);
+      launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_, f16_g2_cs_,
+                        stream_);
+    } else {
+      launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
+      launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
+    }
     build_plans();
     return;
   }
@@ -314,8 +327,12 @@ void BapgEngine::build_plans() {
   const int* done = &st_->done;
   const int* flags = &st_->flags;
   if (bf16()) {
-    // bf16 split chain: A = D (exact bf16), B = planes of W / P / V.
+    // Split-plane chain: A = D (exact bf16 / fp16), B = planes of W / P / V.
+    // f16x2 carries power-of-two scales: GEMM1's B planes hold X·2^s1, its
+    // row scale maps row i of the accumulator to Vᵀ·2^σ_i, GEMM2's column
+    // scale 2^−σ_j returns G unscaled.
     const int planes = precision_ == GWB_PREC_BF16X3 ? 3 : 2;
+    const bool f16 = this->f16();
     auto planes_of = [](float* base, int64_t plane_elems, int k) {
       return static_cast<void*>(reinterpret_cast<uint16_t*>(base) + k * plane_elems);
     };
@@ -333,6 +350,8 @@ void BapgEngine::build_plans() {
       for (int k = 0; k < planes; ++k) d.c_bf16[k] = planes_of(Vt_aux_, m_ * ldn_, k);
       d.ldc = ldn_;
       d.skip = skip;
+      d.f16 = f16;
+      if (f16) d.row_scale = f16_g1_rs_;
       return gemm_plan_create(d);
     };
     auto gemm2 = [&](const int* skip) {
@@ -348,6 +367,8 @@ void BapgEngine::build_plans() {
       d.c = G_;
       d.ldc = ldm_;
       d.skip = skip;
+      d.f16 = f16;
+      if (f16) d.col_scale = f16_g2_cs_;
       return gemm_plan_create(d);
     };
     for (int q = 0; q < 2; ++q) {
@@ -447,6 +468,9 @@ void BapgEngine::load_marginals(const double* mu, const double* nu) {
   std::vector<float> mu32(n_), nu32(m_);
   for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
   for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
+  x_max_ = 0.0;
+  for (int64_t i = 0; i < n_; ++i) x_max_ = std::max(x_max_, std::fabs(mu[i]));
+  for (int64_t j = 0; j < m_; ++j) x_max_ = std::max(x_max_, std::fabs(nu[j]));
   GWB_CUDA(cudaMemcpyAsync(mu64_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
   GWB_CUDA(cudaMemcpyAsync(nu64_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, stream_));
   GWB_CUDA(cudaMemcpyAsync(mu32_, mu32.data(), sizeof(float) * n_, cudaMemcpyHostToDevice, stream_));
@@ -466,6 +490,9 @@ void BapgEngine::load_device(const float* dx, int64_t ldx, const float* dy, int6
   GWB_CUDA(cudaMemcpyAsync(nu32.data(), nu, sizeof(float) * m_, cudaMemcpyDeviceToHost, stream_));
   GWB_CUDA(cudaStreamSynchronize(stream_));
   std::vector<double> mu64(mu32.begin(), mu32.end()), nu64(nu32.begin(), nu32.end());
+  x_max_ = 0.0;
+  for (double v : mu64) x_max_ = std::max(x_max_, std::fabs(v));
+  for (double v : nu64) x_max_ = std::max(x_max_, std::fabs(v));
   GWB_CUDA(cudaMemcpyAsync(mu64_, mu64.data(), sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
   GWB_CUDA(cudaMemcpyAsync(nu64_, nu64.data(), sizeof(double) * m_, cudaMemcpyHostToDevice, stream_));
   GWB_CUDA(cudaStreamSynchronize(stream_));
@@ -490,7 +517,7 @@ void BapgEngine::reset(const double* w0_host) {
     launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, dst, stream_);
   }
   if (quadratic()) launch_quad_reset(dev_view(0), P_, W_[0], stream_);
-  launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], aux_mode(), stream_);
+  launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], aux_mode(), stream_, aux_scale());
   parity_ = 0;
   GWB_CUDA(cudaGetLastError());
 }

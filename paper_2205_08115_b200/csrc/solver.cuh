@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <functional>
@@ -133,7 +134,12 @@ class BapgEngine {
   float *Dx_bf_ = nullptr, *Dy_bf_ = nullptr;  // bf16 copies (bf16 split modes)
   Csr cx_, cy_;                                // sparse chain (GWB_PREC_SPARSE)
   float *Vs_ = nullptr, *DyT_ = nullptr;       // skinny chain (GWB_PREC_FP32): V, D_Yᵀ
-  bool bf16() const { return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2; }
+  // Split-plane chains on kind::f16 (bf16 planes, or fp16 planes for f16x2).
+  bool bf16() const {
+    return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2 ||
+           precision_ == GWB_PREC_F16X2;
+  }
+  bool f16() const { return precision_ == GWB_PREC_F16X2; }
   bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
   bool fp32() const { return precision_ == GWB_PREC_FP32; }
   // Skinny bf16x3 chain (m ≤ 32, exact-bf16 D_X): FP32-pipe GEMM1 writing
@@ -149,8 +155,19 @@ class BapgEngine {
     return precision_ == GWB_PREC_TF32 ? 1
            : precision_ == GWB_PREC_BF16X3 ? 3
            : precision_ == GWB_PREC_BF16X2 ? 4
+           : precision_ == GWB_PREC_F16X2  ? 5
                                            : 2;
   }
+  // f16x2 scaling: every iterate entry is ≤ x_max_ =
+  // max(max μ, max ν) (π_kl ≤ μ_k after the row projection, w_kl ≤ ν_l after
+  // the column one), so the B planes of GEMM1 carry x·2^f16_s1_ with
+  // f16_s1_ = 14 − ⌈log2 x_max_⌉; per-row scales for Vᵀ (f16_g1_rs_ on
+  // GEMM1's output, f16_g2_cs_ undoing them on GEMM2's).
+  double x_max_ = 1.0;
+  int f16_s1_ = 0;
+  float* f16_g1_rs_ = nullptr;
+  float* f16_g2_cs_ = nullptr;
+  float aux_scale() const { return f16() ? std::ldexp(1.0f, f16_s1_) : 1.0f; }
   float *P_ = nullptr, *P_aux_ = nullptr, *W_[2] = {nullptr, nullptr},
         *W_aux_[2] = {nullptr, nullptr};
   float *Vt_ = nullptr, *Vt_aux_ = nullptr, *G_ = nullptr;
@@ -188,6 +205,6 @@ class BapgEngine {
 };
 
 // Resolves GWB_PREC_AUTO (see gwb.h).
-int resolve_precision(int requested, bool d_exact, double dmax_x, double dmax_y, double rho);
+int resolve_precision(int requested, bool bf16_exact, bool f16_exact);
 
 }  // namespace gwb

@@ -43,7 +43,7 @@ def check_argmax(pi, pi_ref, tol):
     return decided.mean()
 
 
-@pytest.mark.parametrize("precision", ["auto", "tf32", "3xtf32", "bf16x3", "bf16x2"])
+@pytest.mark.parametrize("precision", ["auto", "tf32", "3xtf32", "bf16x3", "bf16x2", "f16x2"])
 def test_bapg_er_small(gpu, port, precision):
     inst = I.config1(seed=3, n=256)
     rep, o = run_both(port, inst, precision, max_iters=60)
@@ -63,9 +63,10 @@ def test_bapg_er_small(gpu, port, precision):
         assert abs(r.split_gap - q["split_gap"]) <= 1e-3 * q["split_gap"] + 1e-9
 
 
-@pytest.mark.parametrize("precision", ["3xtf32", "bf16x3"])
+@pytest.mark.parametrize("precision", ["3xtf32", "bf16x3", "f16x2"])
 def test_bapg_gmm_small(gpu, port, precision):
-    # Euclidean distances are not exact in bf16: bf16x3 must fall back to 3xTF32.
+    # Euclidean distances are not exact in bf16 / fp16: bf16x3 and f16x2 must
+    # fall back to 3xTF32.
     inst = I.config2(seed=1, n=320, m=256)
     rep, o = run_both(port, inst, precision, max_iters=40)
     assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
@@ -161,3 +162,100 @@ def test_concurrent_solves_are_reentrant_and_deterministic(gpu):
     assert not errs, errs
     for a, b in zip(out, sequential):
         assert np.array_equal(a, b)
+
+
+# f16x2 (AUTO for fp16-exact structure matrices on the single-GPU engine):
+# D in fp16 × two fp16 planes of the power-of-two-scaled iterate.  The cases
+# below stress the scaling: hub-heavy BA degrees, non-uniform
+# and ragged marginals, integer weights > 1, and a coupling driven far from
+# uniform (small ρ, many iterations) so its entries span many binades.
+def _f16_case(port, inst, **over):
+    rep, o = run_both(port, inst, "auto", **over)
+    assert rep.iterations_used == o.iterations_used
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL
+    assert rel_scale(rep.w_half.entries(), o.w) < PI_TOL
+    for r, q in zip(rep.trace, o.trace):
+        assert abs(r.objective - q["objective"]) <= OBJ_TOL * abs(q["objective"])
+    check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
+    return rep, o
+
+
+def _session_precision(inst, precision):
+    import ctypes as C
+    import torch
+    lib = abi.load()
+    cfg = gw.SolverConfig(precision=precision, quiet=True, max_iters=4).to_abi()
+    st = abi.Status()
+    sess = C.c_void_p()
+    n, m = inst.dx.shape[0], inst.dy.shape[0]
+    lib.gwb_session_create(C.byref(cfg), n, m, 0, C.byref(sess), C.byref(st))
+    abi.raise_for(st)
+    dev = dict(device="cuda", dtype=torch.float32)
+    dx, dy = torch.tensor(inst.dx, **dev), torch.tensor(inst.dy, **dev)
+    mu, nu = torch.tensor(inst.mu, **dev), torch.tensor(inst.nu, **dev)
+    lib.gwb_session_load_device(sess, dx.data_ptr(), n, dy.data_ptr(), m, mu.data_ptr(),
+                                nu.data_ptr(), None, C.byref(st))
+    abi.raise_for(st)
+    rprec, flops = C.c_int32(0), C.c_double(0)
+    lib.gwb_session_info(sess, C.byref(rprec), C.byref(flops), C.byref(st))
+    lib.gwb_session_destroy(sess)
+    return rprec.value
+
+
+def test_f16x2_is_auto_for_graphs(gpu):
+    # 0/1 graphs resolve AUTO to f16x2; Euclidean D (not fp16-exact) to 3xTF32;
+    # an explicit f16x2 request on such D falls back to 3xTF32 as well.
+    assert _session_precision(I.config1(seed=3, n=256), "auto") == abi.PREC_F16X2
+    gmm = I.config2(seed=1, n=320, m=256)
+    assert _session_precision(gmm, "auto") == abi.PREC_3XTF32
+    assert _session_precision(gmm, "f16x2") == abi.PREC_3XTF32
+
+
+def test_f16x2_ba_hubs(gpu, port):
+    inst = I.config4(n=1024)
+    _f16_case(port, inst, max_iters=200)
+
+
+def test_f16x2_nonuniform_ragged(gpu, port):
+    rng = np.random.default_rng(11)
+    base = I.config1(seed=4, n=300)
+    n, m = 300, 260
+    dx = base.dx
+    dy = base.dy[:m, :m].copy()
+    mu = rng.uniform(0.05, 3.0, n)
+    mu /= mu.sum()
+    nu = rng.uniform(0.05, 3.0, m) ** 3
+    nu /= nu.sum()
+    inst = I.Instance(name="ragged", dx=dx, dy=dy, mu=mu, nu=nu, solver=dict(base.solver))
+    _f16_case(port, inst, max_iters=120)
+
+
+def test_f16x2_integer_weights(gpu, port):
+    # Hop-count-like integer weights up to 40: exact in fp16, Vᵀ row bounds
+    # scale with the weighted degrees.
+    rng = np.random.default_rng(5)
+    base = I.config1(seed=6, n=288)
+    w = rng.integers(1, 41, size=base.dx.shape)
+    w = np.triu(w, 1) + np.triu(w, 1).T
+    dx = base.dx * w
+    dy = base.dy * w
+    inst = I.Instance(name="weighted", dx=dx, dy=dy, mu=base.mu, nu=base.nu,
+                      solver=dict(base.solver, rho=5.0))
+    _f16_case(port, inst, max_iters=80)
+
+
+@pytest.mark.parametrize("precision", ["auto", "bf16x3"])
+def test_concentrated_coupling(gpu, port, precision):
+    # ρ = 0.05, 300 iterations: the coupling has found the permutation (max
+    # entry 1/n) and its entries span > 100 binades (some below fp32's
+    # normal range), far outside the scale the f16x2 bounds are tight for.
+    inst = I.config1(seed=8, n=256)
+    rep, o = run_both(port, inst, precision, max_iters=300, rho=0.05)
+    fin = o.final[o.final > 1e-300]
+    assert np.log2(fin.max() / fin.min()) > 100
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL
+    for r, q in zip(rep.trace, o.trace):
+        assert abs(r.objective - q["objective"]) <= OBJ_TOL * abs(q["objective"])
+    check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)

@@ -14,7 +14,7 @@ import torch
 from paper_2205_08115_b200 import abi
 from paper_2205_08115_b200 import instances as I
 
-PREC = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6}
+PREC = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6, "f16x2": 7}
 
 
 def session_rate(inst, iters, prec="auto", warm=3):
@@ -54,7 +54,7 @@ def session_rate(inst, iters, prec="auto", warm=3):
     ms = e0.elapsed_time(e1)
     lib.gwb_session_destroy(s)
     return {"it_per_s": iters / (ms * 1e-3), "ms_per_it": ms / iters,
-            "precision": {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32"}[rp.value],
+            "precision": {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2"}[rp.value],
             "tflops_alg": fl.value * iters / (ms * 1e-3) / 1e12, "launches": L.value}
 
 

@@ -12,7 +12,7 @@ cases = [("c1-256", I.config1(seed=3, n=256), 60), ("c1-1000", I.config1(seed=0)
 for name, inst, iters in cases:
     o = port.solve(gw.SolverConfig(quiet=True, **{**inst.solver, "max_iters": iters}).to_abi(),
                    inst.dx, inst.dy, inst.mu, inst.nu)
-    for prec in ("tf32", "3xtf32", "bf16x3", "bf16x2"):
+    for prec in sys.argv[1].split(",") if len(sys.argv) > 1 else ("tf32", "3xtf32", "bf16x3", "bf16x2", "f16x2"):
         cfg = gw.SolverConfig(precision=prec, quiet=True, **{**inst.solver, "max_iters": iters})
         t = time.time()
         rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),

@@ -11,7 +11,7 @@ from paper_2205_08115_b200 import abi
 from paper_2205_08115_b200 import instances as I
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
-prec = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5}[
+prec = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "f16x2": 7}[
     sys.argv[2] if len(sys.argv) > 2 else "auto"]
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 e = I.barabasi_albert(n, 5, I.mix_seed(0, 41))
