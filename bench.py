@@ -657,7 +657,7 @@ def hbpg_variant(n):
     return {"value": (len(rates) / sum(1.0 / x for x in rates)) if rates else None,
             "unit": "it/s", "ebpg_it_per_s": r["ebpg_it_per_s"], "bpg_it_per_s": r["bpg_it_per_s"],
             "iterations": r["iters"], "e2e_seconds": r["wall_s"],
-            "note": "harmonic mean of the eBPG and BPG phase rates; chain bf16x3 (0/1 graphs)"}
+            "note": "harmonic mean of the eBPG and BPG phase rates; chain f16x2 (0/1 graphs, AUTO)"}
 
 
 def c5_variant(world, rank, local, dist, iters=500, total=4096):

@@ -77,7 +77,9 @@ struct BDev {
   const float* P;       // π_k
   float* P_new;
   float* P_aux_new;
-  int aux_mode;         // GEMM operand copy of P_new: 2 = 3xTF32 residual, 3/4 = bf16 planes
+  int aux_mode;         // GEMM operand copy of P_new: 2 = 3xTF32 residual, 3/4 = bf16
+                        // planes, 5 = fp16 planes of P_new·aux_scale (f16x2)
+  float aux_scale;
   int64_t plane;        // elements per bf16 plane (n·ld)
   const double* mu64;
   const double* nu64;
@@ -434,7 +436,8 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
       }
       *reinterpret_cast<float4*>(d.P_new + i * d.ld + c0) = make_float4(o[0], o[1], o[2], o[3]);
       if (d.P_aux_new)
-        aux_store4(d.P_aux_new, d.aux_mode, d.plane, i * d.ld + c0, o[0], o[1], o[2], o[3]);
+        aux_store4(d.P_aux_new, d.aux_mode, d.plane, i * d.ld + c0, o[0], o[1], o[2], o[3],
+                   d.aux_scale);
     }
     rs = warp_sum(rs);
     if (lane == 0) d.row_sum[static_cast<int64_t>(blockIdx.x) * d.n + i] = rs;
@@ -724,6 +727,14 @@ class BregmanEngine {
       GWB_CUDA(cudaMemcpyAsync(sp, dy, sizeof(double) * m_ * m_, cudaMemcpyHostToDevice, s_));
       launch_colmajor64_to_rowmajor32(sp, m_, m_, Dy_, ldm_, s_);
     }
+    // f16x2 bound on every iterate entry: the written coupling has column
+    // sums ν (the Sinkhorn scaling ends on a column update; BPG's
+    // perturbation adds ≤ 1/(nm)), π₀ = μνᵀ or the caller's initial coupling.
+    x_max_ = 0.0;
+    for (int64_t i = 0; i < n_; ++i) x_max_ = std::max(x_max_, std::fabs(mu[i]));
+    for (int64_t j = 0; j < m_; ++j) x_max_ = std::max(x_max_, std::fabs(nu[j]));
+    if (initial)
+      for (int64_t k = 0; k < n_ * m_; ++k) x_max_ = std::max(x_max_, std::fabs(initial[k]));
     choose_precision();
     GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
@@ -741,7 +752,7 @@ class BregmanEngine {
                               ldm_, P_[0], s_);
       GWB_CUDA(cudaStreamSynchronize(s_));
     }
-    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_);
+    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_, aux_scale());
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_plans();
   }
@@ -891,6 +902,7 @@ class BregmanEngine {
     d.ld = ldm_;
     d.G = G_;
     d.aux_mode = aux_mode_;
+    d.aux_scale = aux_scale();
     d.plane = pstride_;
     d.mu64 = mu_;
     d.nu64 = nu_;
@@ -930,9 +942,10 @@ class BregmanEngine {
     d.P_aux_new = Pa_[1 - q];
   }
 
-  // Chain precision, as for BAPG: bf16 planes of the
-  // iterate against exact bf16 structure matrices when both are 0/1-like,
-  // otherwise 3xTF32 (both operands split).
+  // Chain precision, as for BAPG: fp16 planes of the scaled
+  // iterate against exact fp16 structure matrices (f16x2) when both are
+  // 0/1-like, bf16x3 when exact in bf16 only, otherwise 3xTF32 (both
+  // operands split).
   void choose_precision() {
     std::unique_ptr<void, DevFree> mx(dalloc<float>(2)), ix(dalloc<int>(2));
     float* d_max = static_cast<float*>(mx.get());
@@ -943,22 +956,36 @@ class BregmanEngine {
     GWB_CUDA(cudaMemcpyAsync(h, d_inexact, sizeof(h), cudaMemcpyDeviceToHost, s_));
     GWB_CUDA(cudaStreamSynchronize(s_));
     const bool bf16_exact = (h[0] & 2) == 0 && (h[1] & 2) == 0;
+    const bool f16_exact = (h[0] & 4) == 0 && (h[1] & 4) == 0;
     const int req = cfg_.precision;
-    // f16x2 is a single-GPU BAPG chain; the Bregman solvers run it as bf16x3.
-    if (bf16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_BF16X3 || req == GWB_PREC_F16X2))
+    if (f16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_F16X2))
+      aux_mode_ = 5;
+    else if (bf16_exact && (req == GWB_PREC_AUTO || req == GWB_PREC_BF16X3 || req == GWB_PREC_F16X2))
       aux_mode_ = 3;
     else if (bf16_exact && req == GWB_PREC_BF16X2) aux_mode_ = 4;
     else aux_mode_ = 2;
     if (aux_mode_ >= 3) {
       Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16));
       Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
-      launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, s_);
-      launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+      if (aux_mode_ == 5) {
+        // f16x2 scales as in the BAPG engine.
+        launch_to_f16(Dx_, n_, n_, ldn_, Dx_bf_, s_);
+        launch_to_f16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+        f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(std::max(x_max_, 1e-30))));
+        f16_g1_rs_ = keep(dalloc<float>(ldm_));
+        f16_g2_cs_ = keep(dalloc<float>(ldm_));
+        launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_,
+                          f16_g2_cs_, s_);
+      } else {
+        launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, s_);
+        launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+      }
     } else {
       launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_lo_, 2, s_);
       launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
     }
   }
+  float aux_scale() const { return aux_mode_ == 5 ? std::ldexp(1.0f, f16_s1_) : 1.0f; }
 
   void build_plans() {
     if (aux_mode_ >= 3) {
@@ -977,6 +1004,8 @@ class BregmanEngine {
         for (int k = 0; k < planes; ++k) d.c_bf16[k] = plane_k(Vta_, m_ * ldn_, k);
         d.ldc = ldn_;
         d.skip = skip;
+        d.f16 = aux_mode_ == 5;
+        if (d.f16) d.row_scale = f16_g1_rs_;
         GemmPlan* p = gemm_plan_create(d);
         plans_.push_back(p);
         return p;
@@ -990,6 +1019,8 @@ class BregmanEngine {
         d.ldb = ldn_;
         d.c = G_; d.ldc = ldm_;
         d.skip = skip;
+        d.f16 = aux_mode_ == 5;
+        if (d.f16) d.col_scale = f16_g2_cs_;
         GemmPlan* p = gemm_plan_create(d);
         plans_.push_back(p);
         return p;
@@ -1115,6 +1146,10 @@ class BregmanEngine {
   float* Dx_bf_ = nullptr;
   float* Dy_bf_ = nullptr;
   int aux_mode_ = 2;
+  double x_max_ = 1.0;  // f16x2: bound on every iterate entry
+  int f16_s1_ = 0;
+  float* f16_g1_rs_ = nullptr;
+  float* f16_g2_cs_ = nullptr;
   double *mu_, *nu_, *f_, *fn_, *g_, *row_err_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
       *row_sum_, *obj_part_, *wpart_;
   float* col_pe_;

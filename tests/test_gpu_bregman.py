@@ -82,3 +82,29 @@ def test_bregman_golden(gpu, path):
         assert rep.iterations_used == int(z["iterations"])
     assert np.abs(rep.final_coupling.entries() - z["final"]).max() <= 1e-4 * np.abs(z["final"]).max()
     assert abs(rep.trace[-1].objective - z["trace"][-1, 1]) <= 1e-5 * abs(z["trace"][-1, 1])
+
+
+@pytest.mark.parametrize("precision", ["auto", "bf16x3"])
+def test_hbpg_initial_coupling_and_precisions(gpu, port, precision):
+    # AUTO runs the Bregman chain as f16x2 for 0/1 graphs; an initial
+    # coupling concentrated on a permutation (entries 0.9/n ≫ μ_i ν_j) sets
+    # the f16x2 iterate bound.
+    inst = I.config1(seed=12, n=200)
+    n = inst.dx.shape[0]
+    rng = np.random.default_rng(3)
+    init = np.full((n, n), 0.1 / (n * n))
+    init[np.arange(n), rng.permutation(n)] += 0.9 / n
+    init = np.asfortranarray(init / init.sum())
+    cfg = gw.SolverConfig(algorithm="hbpg", epsilon_reg=0.1, step=5.0, inner_iters=10,
+                          switch_iters=5, max_iters=10, rel_tol=1e-30, quiet=True,
+                          precision=precision)
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu), cfg,
+                   gw.SolveOptions(initial=init))
+    o = port.solve(cfg.to_abi(), inst.dx, inst.dy, inst.mu, inst.nu, init)
+    assert o.code == 0, o.message
+    assert rep.iterations_used == o.iterations_used
+    f, fr = rep.final_coupling.entries(), o.final
+    assert np.abs(f - fr).max() <= 1e-4 * np.abs(fr).max()
+    for r, q in zip(rep.trace, o.trace):
+        assert abs(r.objective - q["objective"]) <= 1e-5 * abs(q["objective"])
