@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -91,6 +92,7 @@ struct __align__(64) GemmParams {
   int32_t b_block_k;  // > 0: B maps are 3-D [K/b_block_k][N][b_block_k]
   int32_t c_planes;
   int32_t c_f16;  // output planes are fp16 (else bf16)
+  int32_t fused;  // split planes share one stage: {A, B_0 … B_{passes−1}}
   uint16_t* c_pl[3];
   float* c;
   float* c_aux;
@@ -177,14 +179,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kblocks_all = (p.K + kblk - 1) / kblk;
   const int kb_begin = p.splits > 1 ? split * p.kb_per_split : 0;
   const int kblocks = p.splits > 1 ? max(0, min(kblocks_all - kb_begin, p.kb_per_split)) : kblocks_all;
-  const int total = p.passes * kblocks;
+  // Fused planes: the work item is a k-block carrying every plane pass.
+  const int total = p.fused ? kblocks : p.passes * kblocks;
   const int chunk = p.chunk;
+  const uint32_t f_stage_bytes = kABytes + static_cast<uint32_t>(p.passes) * kBBytes;
+  const int f_stages = static_cast<int>((kStages * kStageBytes) / f_stage_bytes);
   const int nchunks = (total + chunk - 1) / chunk;
   const int a_row = tm * kPairM + static_cast<int>(rank) * kBM;
   const int b_row = tn * kBN + static_cast<int>(rank) * kHalfN;
 
   if (warp == 0) {
     if (ptx::elect_one()) {
+      if (p.fused) {
+        // One stage per k-block: A once, then every B plane (A is shared by
+        // the plane passes, so it crosses L2 → SMEM once instead of per pass).
+        for (int it = 0; it < total; ++it) {
+          const int s = it % f_stages;
+          const uint32_t ph = (it / f_stages) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          const int kb = kb_begin + it;
+          const uint32_t fbar = ptx::mapa(&full[s], 0);
+          uint8_t* st = smem + s * f_stage_bytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
+          ptx::tma_load_2d_2sm(st, &p.a_map[0], fbar, kb * kblk, a_row);
+          for (int pl = 0; pl < p.passes; ++pl) {
+            void* dst = st + kABytes + pl * kBBytes;
+            if (p.b_block_k > 0) {
+              const int kk = kb * kblk;
+              ptx::tma_load_3d_2sm(dst, &p.b_map[pl], fbar, kk % p.b_block_k, b_row,
+                                   kk / p.b_block_k);
+            } else {
+              ptx::tma_load_2d_2sm(dst, &p.b_map[pl], fbar, kb * kblk, b_row);
+            }
+          }
+        }
+      } else {
       for (int it = 0; it < total; ++it) {
         const int s = it % kStages;
         const uint32_t ph = (it / kStages) & 1;
@@ -203,6 +232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                b_row);
         }
       }
+      }
     }
   } else if (warp == 1) {
     if (leader && ptx::elect_one()) {
@@ -216,6 +246,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
         const int it0 = c * chunk;
         const int it1 = min(total, it0 + chunk);
+        if (p.fused) {
+          for (int it = it0; it < it1; ++it) {
+            const int s = it % f_stages;
+            const uint32_t ph = (it / f_stages) & 1;
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t a_base = ptx::smem_u32(smem + s * f_stage_bytes);
+            // Smallest plane first: the tensor core's truncating accumulation
+            // then acts on the hi-plane terms only (as in batched.cu).
+            for (int pl = p.passes - 1; pl >= 0; --pl) {
+              const uint32_t b_base = a_base + kABytes + pl * kBBytes;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
+                const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32);
+                const uint32_t accum = (it != it0 || pl != p.passes - 1 || k != 0) ? 1u : 0u;
+                ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
+              }
+            }
+            ptx::mma_commit_2sm(&empty[s], 0x3);
+          }
+          ptx::mma_commit_2sm(&tfull[b], 0x3);
+          continue;
+        }
         for (int it = it0; it < it1; ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
@@ -557,6 +611,16 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
   g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
+  // Split planes share one pipeline stage (A loaded once per k-block).  The
+  // promotion chunk stays at the same MMA count: promote_every (pass,
+  // k-block) items = promote_every·4 MMAs → ⌈promote_every / passes⌉
+  // k-blocks of all planes (2 planes: 1 k-block = 8 MMAs, as before).
+  static const bool unfused_env = std::getenv("GWB_GEMM_UNFUSED") != nullptr;
+  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env) {
+    g.fused = 1;
+    if (d.promote_every > 0)
+      g.chunk = std::max(1, (d.promote_every + d.bf16_planes - 1) / d.bf16_planes);
+  }
   g.b_block_k = static_cast<int32_t>(d.b_block_k);
   if (d.b_block_k > 0 &&
       (d.K % d.b_block_k != 0 || d.b_block_k % (d.bf16_planes > 0 ? kBK16 : kBK) != 0))

@@ -52,6 +52,10 @@ struct GemmDesc {
   // 22-bit operand.  The caller keeps every plane inside fp16 range with
   // power-of-two scales folded into row_scale / col_scale.
   bool f16 = false;
+  // Split planes in one pipeline stage {A, B_0, …} per k-block, A loaded
+  // once for every plane pass (default); false: one stage per (pass,
+  // k-block), A re-loaded per pass (A/B testing; env GWB_GEMM_UNFUSED=1).
+  bool fuse_planes = true;
   // Blocked-K B operand (multi-GPU all-gather layout): when b_block_k > 0,
   // every B plane is stored as [K / b_block_k][N][b_block_k] (leading dim of
   // a block row = b_block_k); b_block_k must be a multiple of the k-block
