@@ -518,11 +518,11 @@ def run_sharded_bench(args, world, rank, local, dist):
     dx_rows = dense_rows_dev(torch, n, edges, rb, rv)
     dy = dense_dev(torch, n, tgt)
     mu = torch.full((n,), 1.0 / n, device="cuda", dtype=torch.float32)
-    prec = PREC_NAMES[args.precision] or abi.PREC_BF16X3  # 0/1 graphs: AUTO = bf16x3
+    prec = PREC_NAMES[args.precision] or abi.PREC_F16X2  # 0/1 graphs: AUTO = f16x2
     cfg = abi.default_config(rho=0.1, max_iters=args.steps + args.warmup + 4, rel_tol=1e-30,
                              precision=prec)
     shard = D.GpuShard(cfg, n, n, rank, world, local)
-    shard.load(dx_rows, dy, mu[rb:rb + max(rv, 1)].contiguous(), mu)
+    shard.load(dx_rows, dy, mu[rb:rb + max(rv, 1)].contiguous(), mu, x_max=1.0 / n)
     shard.reset()
     del dx_rows, dy
     comm = D.TorchComm(dist, rank, world)
@@ -612,7 +612,7 @@ def hbpg_sharded_variant(args, world, rank, local, dist, edges, tgt, iters=12, s
     u = np.full(n, 1.0 / n)
     cfg = abi.default_config(algorithm=abi.HBPG, rho=0.1, epsilon_reg=0.1, step=5.0, inner_iters=10,
                              inner_tol=1e-9, switch_iters=switch, max_iters=iters, rel_tol=1e-30,
-                             quiet=1, precision=abi.PREC_BF16X3)  # 0/1 graphs
+                             quiet=1, precision=abi.PREC_F16X2)  # 0/1 graphs: AUTO = f16x2
     sh = D.BregShard(cfg, n, n, rank, world, local)
     sh.load(dx_rows, dy, u, u)
     del dx_rows, dy
@@ -642,7 +642,7 @@ def hbpg_sharded_variant(args, world, rank, local, dist, edges, tgt, iters=12, s
     return {"value": timed / (ms * 1e-3), "unit": "it/s", "iterations_timed": timed,
             "phases_seen": "eBPG then BPG (switch_iters %d)" % switch, "ms": ms,
             "flags": st["flags"],
-            "note": "outer iterations %d-%d of %d; chain bf16x3 sharded by rows (NCCL all-gather "
+            "note": "outer iterations %d-%d of %d; chain f16x2 sharded by rows (NCCL all-gather "
                     "of Vt and G), Sinkhorn sweeps replicated on every rank" % (warm + 1, iters, iters)}
 
 

@@ -66,6 +66,12 @@ GWB_API int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows,
                                       int64_t ldx, const float* dy,
                                       int64_t ldy, const float* mu_rows,
                                       const float* nu, gwb_status* st);
+/* f16x2 chains (GWB_PREC_F16X2) only, before load: the bound on every
+ * iterate entry, max(max μ, max ν) over ALL ranks (the row projection
+ * keeps π_kl ≤ μ_k, the column projection w_kl ≤ ν_l).  Every rank must
+ * pass the same value: it sets the power-of-two plane scales of the
+ * gathered Vᵀ blocks. */
+GWB_API int32_t gwb_shard_set_iterate_bound(gwb_shard* s, double x_max, gwb_status* st);
 GWB_API int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st);
 GWB_API int32_t gwb_shard_phase(gwb_shard* s, int32_t phase, gwb_status* st);
 /* Compute/collective overlap: instead of all-gather(vt) + phase 1 (3, 7),

@@ -590,9 +590,8 @@ class BregmanEngine {
       rows_alloc_ = npad_;
       // The chain precision is fixed up front (resolved by the orchestrator):
       // it sets the exchange-buffer layout the caller allocates.
-      // f16x2 is a single-GPU BAPG chain; here it runs as bf16x3.
       const int req = cfg_.precision;
-      aux_mode_ = (req == GWB_PREC_BF16X3 || req == GWB_PREC_F16X2) ? 3 : req == GWB_PREC_BF16X2 ? 4 : 2;
+      aux_mode_ = req == GWB_PREC_BF16X3 ? 3 : req == GWB_PREC_BF16X2 ? 4 : req == GWB_PREC_F16X2 ? 5 : 2;
       planes_ = aux_mode_ == 3 ? 3 : 2;
       esize_ = aux_mode_ >= 3 ? 2 : 4;
     }
@@ -672,8 +671,23 @@ class BregmanEngine {
     if (aux_mode_ >= 3) {
       Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_ / 2 + 16));
       Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
-      launch_to_bf16(Dx_, nr_, ldk_, ldk_, Dx_bf_, s_);
-      launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+      if (aux_mode_ == 5) {
+        // f16x2: every rank holds the full μ, ν (host) and D_Y, so the
+        // bound and the Vᵀ row scales agree across ranks.
+        x_max_ = 0.0;
+        for (int64_t i = 0; i < n_; ++i) x_max_ = std::max(x_max_, std::fabs(mu[i]));
+        for (int64_t j = 0; j < m_; ++j) x_max_ = std::max(x_max_, std::fabs(nu[j]));
+        launch_to_f16(Dx_, nr_, ldk_, ldk_, Dx_bf_, s_);
+        launch_to_f16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+        f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(std::max(x_max_, 1e-30))));
+        f16_g1_rs_ = keep(dalloc<float>(ldm_));
+        f16_g2_cs_ = keep(dalloc<float>(ldm_));
+        launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_,
+                          f16_g2_cs_, s_);
+      } else {
+        launch_to_bf16(Dx_, nr_, ldk_, ldk_, Dx_bf_, s_);
+        launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
+      }
     } else {
       launch_tf32_aux(Dx_, nr_, ldk_, ldk_, Dx_lo_, 2, s_);
       launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_lo_, 2, s_);
@@ -688,7 +702,7 @@ class BregmanEngine {
     GWB_CUDA(cudaMemcpyAsync(b.get(), nu32.data(), 4 * m_, cudaMemcpyHostToDevice, s_));
     launch_product_coupling(static_cast<float*>(a.get()), static_cast<float*>(b.get()), n_, m_, ldm_,
                             P_[0], s_);
-    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_);
+    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_, aux_scale());
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_shard_plans();
     begin();
@@ -1086,6 +1100,8 @@ class BregmanEngine {
           d.b_bf16[p] = reinterpret_cast<uint16_t*>(Pa_[q]) + p * pstride_ + row0_ * ldm_;
         d.c_planes = planes_;
         for (int p = 0; p < planes_; ++p) d.c_bf16[p] = slot(p, rank_);
+        d.f16 = aux_mode_ == 5;
+        if (d.f16) d.row_scale = f16_g1_rs_;
       } else {
         d.a = Dy_; d.a_lo = Dy_lo_;
         d.b = P_[q] + row0_ * ldm_; d.b_lo = Pa_[q] + row0_ * ldm_;
@@ -1110,6 +1126,8 @@ class BregmanEngine {
         d.bf16_planes = planes_;
         d.a_bf16 = Dx_bf_;
         for (int p = 0; p < planes_; ++p) d.b_bf16[p] = slot(p, 0);
+        d.f16 = aux_mode_ == 5;
+        if (d.f16) d.col_scale = f16_g2_cs_;
       } else {
         d.a = Dx_; d.a_lo = Dx_lo_;
         d.b = static_cast<const float*>(slot(0, 0));

@@ -232,13 +232,13 @@ class ShardEngine {
     if (cfg.precision == GWB_PREC_AUTO)
       throw std::invalid_argument(
           "gwb_shard_create: resolve AUTO precision across ranks first (bf16x3 or 3xtf32)");
-    // f16x2 is the single-GPU BAPG chain; the row-sharded chain runs bf16x3.
-    prec_ = cfg.precision == GWB_PREC_F16X2 ? GWB_PREC_BF16X3 : cfg.precision;
-    bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2;
+    prec_ = cfg.precision;
+    f16_ = prec_ == GWB_PREC_F16X2;
+    bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2 || f16_;  // split planes
     planes_ = prec_ == GWB_PREC_BF16X3 ? 3 : (prec_ == GWB_PREC_TF32 ? 1 : 2);
     esize_ = bf16_ ? 2 : 4;
     aux_mode_ = prec_ == GWB_PREC_TF32 ? 1 : prec_ == GWB_PREC_3XTF32 ? 2
-                : prec_ == GWB_PREC_BF16X3 ? 3 : 4;
+                : prec_ == GWB_PREC_BF16X3 ? 3 : f16_ ? 5 : 4;
     nr_ = round_up((n_ + world_ - 1) / world_, 64);
     row_begin_ = static_cast<int64_t>(rank_) * nr_;
     rows_valid_ = std::max<int64_t>(0, std::min<int64_t>(nr_, n_ - row_begin_));
@@ -324,7 +324,22 @@ class ShardEngine {
                              cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu64_, d_nu.data(), 8 * m_, cudaMemcpyHostToDevice, s_));
     // Operand copies of the structure matrices.
-    if (bf16_) {
+    if (f16_) {
+      // f16x2: the scales derive from the global iterate
+      // bound and the replicated D_Y, so every rank writes its Vᵀ block with
+      // the same per-row scales and GEMM2 undoes them with one column scale.
+      if (!(x_max_ > 0.0))
+        throw std::invalid_argument(
+            "gwb_shard: f16x2 needs gwb_shard_set_iterate_bound (max of mu and nu over all "
+            "ranks) before load");
+      launch_to_f16(Dx_, nr_, ldk_, ldk_, Dx_aux_, s_);
+      launch_to_f16(Dy_, m_, ldm_, ldm_, Dy_aux_, s_);
+      f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(x_max_)));
+      if (!f16_g1_rs_) f16_g1_rs_ = keep(dalloc<float>(ldm_));
+      if (!f16_g2_cs_) f16_g2_cs_ = keep(dalloc<float>(ldm_));
+      launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_,
+                        f16_g2_cs_, s_);
+    } else if (bf16_) {
       launch_to_bf16(Dx_, nr_, ldk_, ldk_, Dx_aux_, s_);
       launch_to_bf16(Dy_, m_, ldm_, ldm_, Dy_aux_, s_);
     } else {
@@ -340,7 +355,7 @@ class ShardEngine {
     launch_status_reset(st_, s_);
     if (rows_valid_ > 0) {
       launch_product_coupling(mu32_, nu32_, rows_valid_, m_, ldm_, W_[0], s_);
-      launch_tf32_aux(W_[0], nr_, m_, ldm_, W_aux_[0], aux_mode_, s_);
+      launch_tf32_aux(W_[0], nr_, m_, ldm_, W_aux_[0], aux_mode_, s_, aux_scale());
     }
     parity_ = 0;
     GWB_CUDA(cudaGetLastError());
@@ -479,6 +494,7 @@ class ShardEngine {
     d.W_new = W_[1 - q];
     d.W_aux = W_aux_[1 - q];
     d.aux_mode = aux_mode_;
+    d.aux_scale = aux_scale();
     d.plane = nr_ * ldm_;
     d.row_part = row_part_;
     d.cw_part = cw_part_;
@@ -522,6 +538,8 @@ class ShardEngine {
       for (int p = 0; p < planes_; ++p) d.b_bf16[p] = aux_plane(X_aux, p);
       d.c_planes = planes_;
       for (int p = 0; p < planes_; ++p) d.c_bf16[p] = slot(p, rank_);
+      d.f16 = f16_;
+      if (f16_) d.row_scale = f16_g1_rs_;
     } else {
       const bool tf32 = prec_ == GWB_PREC_TF32;
       d.a = tf32 ? Dy_aux_ : Dy_;
@@ -556,6 +574,8 @@ class ShardEngine {
       d.bf16_planes = planes_;
       d.a_bf16 = reinterpret_cast<const uint8_t*>(Dx_aux_) + koff * 2;
       for (int p = 0; p < planes_; ++p) d.b_bf16[p] = slot(p, src);
+      d.f16 = f16_;
+      if (f16_) d.col_scale = f16_g2_cs_;
     } else {
       const bool tf32 = prec_ == GWB_PREC_TF32;
       d.a = (tf32 ? Dx_aux_ : Dx_) + koff;
@@ -584,6 +604,8 @@ class ShardEngine {
       d.bf16_planes = planes_;
       d.a_bf16 = Dx_aux_;
       for (int p = 0; p < planes_; ++p) d.b_bf16[p] = plane_base(p);
+      d.f16 = f16_;
+      if (f16_) d.col_scale = f16_g2_cs_;
     } else {
       const bool tf32 = prec_ == GWB_PREC_TF32;
       d.a = tf32 ? Dx_aux_ : Dx_;
@@ -619,7 +641,19 @@ class ShardEngine {
   cudaStream_t s_;
   bool own_stream_ = false;
   int prec_, planes_, esize_, aux_mode_;
-  bool bf16_;
+  bool bf16_, f16_ = false;
+  // f16x2: global bound on every iterate entry (max μ, max ν over all
+  // ranks, set by the orchestrator) and the scales derived from it.
+  double x_max_ = 0.0;
+  int f16_s1_ = 0;
+  float* f16_g1_rs_ = nullptr;
+  float* f16_g2_cs_ = nullptr;
+
+ public:
+  void set_iterate_bound(double x_max) { x_max_ = x_max; }
+  float aux_scale() const { return f16_ ? std::ldexp(1.0f, f16_s1_) : 1.0f; }
+
+ private:
   int64_t nr_, row_begin_, rows_valid_, ldk_, ldm_;
   int parity_ = 0;
   int64_t launches_ = 0;  // kernels launched by phases 0-5 (bench gpu_launches)
@@ -716,6 +750,14 @@ int32_t gwb_shard_set_comm(gwb_shard* s, void* vt_gather, void* col_stats, doubl
 int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows, int64_t ldx, const float* dy,
                               int64_t ldy, const float* mu_rows, const float* nu, gwb_status* st) {
   return shard_guard(st, [&] { s->eng->load(dx_rows, ldx, dy, ldy, mu_rows, nu); });
+}
+
+int32_t gwb_shard_set_iterate_bound(gwb_shard* s, double x_max, gwb_status* st) {
+  return shard_guard(st, [&] {
+    if (!(x_max > 0.0) || !std::isfinite(x_max))
+      throw std::invalid_argument("gwb_shard_set_iterate_bound: bound must be positive and finite");
+    s->eng->set_iterate_bound(x_max);
+  });
 }
 
 int32_t gwb_shard_reset(gwb_shard* s, gwb_status* st) {

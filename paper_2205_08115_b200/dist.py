@@ -58,6 +58,7 @@ _SIGS = {
     "gwb_shard_layout": (C.c_int32, [_P, _I64P, _I64P, _I64P, _I32P, _I32P, _I64P, _I64P, _ST]),
     "gwb_shard_set_comm": (C.c_int32, [_P, _P, _P, _P, _P, _ST]),
     "gwb_shard_load_device": (C.c_int32, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, _ST]),
+    "gwb_shard_set_iterate_bound": (C.c_int32, [_P, C.c_double, _ST]),
     "gwb_shard_reset": (C.c_int32, [_P, _ST]),
     "gwb_shard_phase": (C.c_int32, [_P, C.c_int32, _ST]),
     "gwb_shard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
@@ -132,11 +133,19 @@ class GpuShard:
         self.lib.gwb_shard_stream(self.h, C.byref(sp), C.byref(st))
         self.stream = torch.cuda.ExternalStream(sp.value, device=dev)
         self.max_iters = cfg.max_iters
+        self.precision = cfg.precision
 
-    def load(self, dx_rows, dy, mu_rows, nu):
+    def load(self, dx_rows, dy, mu_rows, nu, x_max=None):
         """Device fp32 tensors: dx_rows (rows_valid × n, any leading dim),
-        dy (m × m), mu_rows (rows_valid), nu (m)."""
+        dy (m × m), mu_rows (rows_valid), nu (m).  f16x2 chains also need
+        x_max = max(max μ, max ν) over ALL ranks (the iterate bound every
+        rank must agree on, gwb_shard_set_iterate_bound)."""
         st = abi.Status()
+        if self.precision == abi.PREC_F16X2:
+            if x_max is None:
+                raise ValueError("f16x2 shard: pass x_max = max(max mu, max nu) over all ranks")
+            self.lib.gwb_shard_set_iterate_bound(self.h, float(x_max), C.byref(st))
+            _check(st)
         self.torch.cuda.synchronize()
         self.lib.gwb_shard_load_device(self.h, dx_rows.data_ptr(), dx_rows.stride(0),
                                        dy.data_ptr(), dy.stride(0), mu_rows.data_ptr(),
@@ -335,10 +344,7 @@ def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, worl
     rb, rv = plan.row_begin(rank), plan.rows_valid(rank)
     rows = np.ascontiguousarray(dx[rb:rb + rv], dtype=np.float32).reshape(rv, n)
     if cfg.precision == abi.PREC_AUTO:
-        ok = (rv == 0 or bf16_exact(rows)) and bf16_exact(np.asarray(dy, dtype=np.float32))
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        cfg = resolve_precision(cfg, bool(flag.item()))
+        cfg = _agree_precision(cfg, rows if rv else None, dy, dist, device)
     shard = BregShard(cfg, n, m, rank, world, device)
     try:
         dev = torch.device("cuda", device)
@@ -369,7 +375,7 @@ def bregman_shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, devic
     mu, nu host fp64."""
     import torch
     n, m = dx.shape[0], dy.shape[0]
-    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy))
+    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy), f16_exact(dx) and f16_exact(dy))
     shards = []
     for r in range(world):
         s = BregShard(cfg, n, m, r, world, device, stream)
@@ -606,15 +612,12 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
     import torch
     n, m = len(mu), len(nu)
     if cfg.precision == abi.PREC_AUTO:
-        # Every rank checks its own rows of D_X (and D_Y); the verdict is the
-        # all-reduced minimum, so all ranks pick the same chain.
+        # Every rank checks its own rows of D_X (and D_Y); the verdicts are
+        # all-reduced (minimum), so all ranks pick the same chain.
         plan = ShardPlan(n, world)
         rb0, rv0 = plan.row_begin(rank), plan.rows_valid(rank)
-        ok = (rv0 == 0 or bf16_exact(np.asarray(dx[rb0:rb0 + rv0], dtype=np.float32))) and \
-            bf16_exact(np.asarray(dy, dtype=np.float32))
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", device))
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        cfg = resolve_precision(cfg, bool(flag.item()))
+        cfg = _agree_precision(cfg, np.asarray(dx[rb0:rb0 + rv0], dtype=np.float32) if rv0 else None,
+                               dy, dist, device)
     shard = GpuShard(cfg, n, m, rank, world, device)
     try:
         rb, rv = shard.row_begin, shard.rows_valid
@@ -625,7 +628,8 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
         dx_d, dy_d = t(rows), t(dy)
         mu_d = t(np.asarray(mu)[rb:rb + max(rv, 1)] if rv else np.zeros(1))
-        shard.load(dx_d, dy_d, mu_d, t(nu))
+        shard.load(dx_d, dy_d, mu_d, t(nu),
+                   x_max=float(max(np.abs(np.asarray(mu)).max(), np.abs(np.asarray(nu)).max())))
         del dx_d, dy_d
         shard.reset()
         st = run_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters, poll_every,
@@ -662,6 +666,20 @@ def raise_shard_flags(st: dict):
     num("non-finite iterate")
 
 
+def f16_exact(t) -> bool:
+    """True if every entry of the (torch or numpy) array is exact in fp16."""
+    import numpy as np
+    import torch
+    x = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
+    x = x.float()
+    return bool(torch.equal(x.to(torch.float16).float(), x))
+
+
+def exact_flags(t) -> int:
+    """Bit 1: exact in bf16; bit 2: exact in fp16 (the AUTO verdict ranks agree on)."""
+    return (1 if bf16_exact(t) else 0) | (2 if f16_exact(t) else 0)
+
+
 def bf16_exact(t) -> bool:
     """True if every entry of the (torch or numpy) array is exact in bf16."""
     import numpy as np
@@ -671,16 +689,32 @@ def bf16_exact(t) -> bool:
     return bool(torch.equal(x.to(torch.bfloat16).float(), x))
 
 
-def resolve_precision(cfg: abi.Config, exact: bool) -> abi.Config:
-    """AUTO resolved as the single-GPU engine does: bf16x3 when
-    both structure matrices are exact in bf16, else 3xTF32.  With sharded
-    D_X the exactness must be agreed by every rank first (each rank only
-    sees its rows): `exact` is that global verdict."""
+def _agree_precision(cfg: abi.Config, rows, dy, dist, device: int) -> abi.Config:
+    """AUTO across ranks: each rank tests its own rows of D_X (None: owns no
+    rows) and D_Y for bf16 / fp16 exactness; a MIN all-reduce of the two
+    verdicts makes every rank resolve the same chain."""
+    import numpy as np
+    import torch
+    dyf = np.asarray(dy, dtype=np.float32)
+    ok_bf = (rows is None or bf16_exact(rows)) and bf16_exact(dyf)
+    ok_f16 = (rows is None or f16_exact(rows)) and f16_exact(dyf)
+    dev = torch.device("cuda", device) if torch.cuda.is_available() else torch.device("cpu")
+    flag = torch.tensor([int(ok_bf), int(ok_f16)], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return resolve_precision(cfg, bool(flag[0].item()), bool(flag[1].item()))
+
+
+def resolve_precision(cfg: abi.Config, exact: bool, f16: bool = False) -> abi.Config:
+    """AUTO resolved as the single-GPU engine does: f16x2 when
+    both structure matrices are exact in fp16, bf16x3 when exact in bf16,
+    else 3xTF32.  With sharded D_X the exactness must be agreed by every
+    rank first (each rank only sees its rows): `exact` / `f16` are those
+    global verdicts."""
     if cfg.precision != abi.PREC_AUTO:
         return cfg
     out = abi.Config()
     C.pointer(out)[0] = cfg
-    out.precision = abi.PREC_BF16X3 if exact else abi.PREC_3XTF32
+    out.precision = abi.PREC_F16X2 if f16 else abi.PREC_BF16X3 if exact else abi.PREC_3XTF32
     return out
 
 
@@ -689,14 +723,15 @@ def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, d
     """Build shard engines from full device tensors (tests / emulation)."""
     import torch
     n, m = dx.shape[0], dy.shape[0]
-    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy))
+    cfg = resolve_precision(cfg, bf16_exact(dx) and bf16_exact(dy), f16_exact(dx) and f16_exact(dy))
+    x_max = float(max(mu.abs().max().item(), nu.abs().max().item()))
     shards = []
     for r in (range(world) if ranks is None else ranks):
         s = GpuShard(cfg, n, m, r, world, device, stream)
         rb, rv = s.row_begin, s.rows_valid
         rows = dx[rb:rb + max(rv, 1)].contiguous()
         murows = mu[rb:rb + max(rv, 1)].contiguous()
-        s.load(rows, dy.contiguous(), murows, nu.contiguous())
+        s.load(rows, dy.contiguous(), murows, nu.contiguous(), x_max=x_max)
         shards.append(s)
     torch.cuda.synchronize()
     return shards

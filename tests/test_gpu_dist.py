@@ -11,7 +11,7 @@ from paper_2205_08115_b200 import instances as I
 pytestmark = pytest.mark.gpu
 
 PREC = {"auto": abi.PREC_AUTO, "bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2, "3xtf32": abi.PREC_3XTF32,
-        "tf32": abi.PREC_TF32}
+        "tf32": abi.PREC_TF32, "f16x2": abi.PREC_F16X2}
 
 
 def _run(inst, world, prec, iters, rel_tol=1e-30, overlap=False):
@@ -38,7 +38,7 @@ def _run(inst, world, prec, iters, rel_tol=1e-30, overlap=False):
 
 @pytest.mark.parametrize("world,prec,case", [
     (2, "bf16x3", "er"), (3, "bf16x3", "er"), (4, "bf16x2", "er"), (2, "3xtf32", "gmm"),
-    (3, "tf32", "er")])
+    (3, "tf32", "er"), (2, "f16x2", "er"), (3, "auto", "er")])
 @pytest.mark.parametrize("overlap", [False, True])
 def test_sharded_emulated_matches_oracle(gpu, port, world, prec, case, overlap):
     # overlap=True: per-source chunks + accumulating partial GEMM2s
