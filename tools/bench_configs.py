@@ -64,3 +64,6 @@ if __name__ == "__main__":
                               ("c3", I.config3(), 500), ("c4@8192", I.config4(n=8192), 20)]:
         out[name] = session_rate(inst, iters)
         print(name, json.dumps(out[name]), flush=True)
+        if name in ("c1", "c4@8192") and "--compare" in sys.argv:
+            r = session_rate(inst, iters, "bf16x3")
+            print(name, "bf16x3", json.dumps(r), flush=True)
