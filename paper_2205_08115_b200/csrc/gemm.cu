@@ -93,6 +93,7 @@ struct __align__(64) GemmParams {
   int32_t c_planes;
   int32_t c_f16;  // output planes are fp16 (else bf16)
   int32_t fused;  // split planes share one stage: {A, B_0 … B_{passes−1}}
+  int32_t group_m;  // row tiles per rasterisation group (kGroupM; env GWB_GEMM_GROUP_M)
   uint16_t* c_pl[3];
   float* c;
   float* c_aux;
@@ -148,10 +149,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int tiles_all = p.tiles_m * p.tiles_n;
   const int split = pid_all / tiles_all;
   const int pid = pid_all - split * tiles_all;
-  const int per_group = kGroupM * p.tiles_n;
+  const int per_group = p.group_m * p.tiles_n;
   const int group = pid / per_group;
-  const int first_m = group * kGroupM;
-  const int gsize = min(p.tiles_m - first_m, kGroupM);
+  const int first_m = group * p.group_m;
+  const int gsize = min(p.tiles_m - first_m, p.group_m);
   const int in_group = pid % per_group;
   const int tm = first_m + in_group % gsize;
   const int tn = in_group / gsize;
@@ -611,6 +612,11 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
   g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
+  static const int group_env = [] {
+    const char* e = std::getenv("GWB_GEMM_GROUP_M");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  g.group_m = group_env > 0 ? group_env : kGroupM;
   // Split planes share one pipeline stage (A loaded once per k-block).  The
   // promotion chunk stays at the same MMA count: promote_every (pass,
   // k-block) items = promote_every·4 MMAs → ⌈promote_every / passes⌉
