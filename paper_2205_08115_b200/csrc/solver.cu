@@ -72,8 +72,15 @@ namespace {
 
 }  // namespace
 
-int resolve_precision(int requested, bool bf16_exact, bool f16_exact) {
+int resolve_precision(int requested, bool bf16_exact, bool f16_exact, bool quadratic) {
   if (requested != GWB_PREC_AUTO) return requested;
+  // Quadratic geometry: the simplex projection changes its support
+  // discontinuously, so the BAPG map amplifies fp32-level differences near
+  // convergence (measured: ×2.4 per iteration on uniform-marginal 0/1
+  // graphs, where projection inputs tie exactly).  It keeps the 24-bit
+  // bf16x3 chain with separate plane passes (tests/test_gpu_quadratic.py,
+  // tools/quad_probe.py).
+  if (quadratic) return bf16_exact ? GWB_PREC_BF16X3 : GWB_PREC_3XTF32;
   // AUTO (measured on B200): a split-operand chain with fp32
   // accumulate, at least as precise as 3xTF32.  When both structure
   // matrices are exact in fp16 (0/1 graphs) it runs as f16x2 — D × (hi +
@@ -274,7 +281,7 @@ void BapgEngine::prepare_d() {
   const bool bf16_exact = (h_inexact[0] & 2) == 0 && (h_inexact[1] & 2) == 0;
   const bool f16_exact = (h_inexact[0] & 4) == 0 && (h_inexact[1] & 4) == 0;
   if (precision_ == GWB_PREC_AUTO)
-    precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, f16_exact);
+    precision_ = resolve_precision(GWB_PREC_AUTO, bf16_exact, f16_exact, quadratic());
   // Split-plane chains need exactly representable structure matrices (0/1
   // graphs); otherwise fall back to bf16x3 (f16x2 only) or 3xTF32, which
   // splits both operands.
@@ -352,6 +359,7 @@ void BapgEngine::build_plans() {
       d.skip = skip;
       d.f16 = f16;
       if (f16) d.row_scale = f16_g1_rs_;
+      d.fuse_planes = !quadratic();  // separate plane passes keep exact ties (see resolve_precision)
       return gemm_plan_create(d);
     };
     auto gemm2 = [&](const int* skip) {
@@ -369,6 +377,7 @@ void BapgEngine::build_plans() {
       d.skip = skip;
       d.f16 = f16;
       if (f16) d.col_scale = f16_g2_cs_;
+      d.fuse_planes = !quadratic();
       return gemm_plan_create(d);
     };
     for (int q = 0; q < 2; ++q) {

@@ -205,6 +205,6 @@ class BapgEngine {
 };
 
 // Resolves GWB_PREC_AUTO (see gwb.h).
-int resolve_precision(int requested, bool bf16_exact, bool f16_exact);
+int resolve_precision(int requested, bool bf16_exact, bool f16_exact, bool quadratic);
 
 }  // namespace gwb
