@@ -141,3 +141,40 @@ def test_sharded_bregman_matches_oracle_gloo(port, world, over):
         assert np.abs(final - o.final).max() <= 1e-10 * np.abs(o.final).max()
         np.testing.assert_allclose(objs, [t["objective"] for t in o.trace], rtol=1e-9)
         assert phases == [t["phase"] for t in o.trace]
+
+
+def _agree_worker(rank, world, port, values, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2205_08115_b200 import dist as D
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows = np.zeros((4, 8), dtype=np.float32)
+    rows[0, 1] = values[rank]  # this rank's rows of D_X
+    dy = np.eye(8, dtype=np.float32)
+    cfg = D.resolve_precision(abi.default_config(), True)  # pass-through check below
+    out = D._agree_precision(abi.default_config(), rows, dy, dist, 0)
+    q.put((rank, out.precision, cfg.precision))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("values,expect", [
+    ((1.0, 1.0), abi.PREC_F16X2),               # 0/1 rows everywhere
+    ((1.0, 2.0 ** 20), abi.PREC_BF16X3),        # rank 1: exact in bf16, beyond fp16 range
+    ((1.0, 1.0 / 3.0), abi.PREC_3XTF32),        # rank 1: exact in neither
+])
+def test_auto_precision_agreed_across_ranks(values, expect):
+    # dist._agree_precision: every rank tests its own rows; the MIN
+    # all-reduce of the bf16 / fp16 verdicts makes all ranks pick one chain.
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, values, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(o[1] == expect for o in out), out
+    assert all(o[2] == abi.PREC_BF16X3 for o in out)  # explicit exact flag, no fp16 verdict
