@@ -377,7 +377,9 @@ def run_ours(args, world, rank, local, dist):
     passes, kind = PREC_PASSES[main["precision"]]
     label = PREC_LABEL[main["precision"]]
     f16_pipe = kind in ("bf16", "f16")
-    exec_peak = peaks.get("bf16_tflops_sustained") if f16_pipe else tf32_peak
+    # The chain GEMM runs faster than cuBLAS's own sustained bf16 figure, so
+    # the burst (best-of-10) peak is the ceiling it is measured against.
+    exec_peak = peaks.get("bf16_tflops") if f16_pipe else (tf32["burst"] if tf32 else None)
     # Roofline of the chain as executed: split-operand passes share the
     # kind::f16 (bf16 / fp16, same dense rate) or kind::tf32 tensor peak, so
     # the algorithmic FLOP/s it can reach is that peak ÷ passes.  The
@@ -389,8 +391,8 @@ def run_ours(args, world, rank, local, dist):
         "kernel": "gemm_tf32_kernel, CTA-pair tcgen05 (D_Y·πᵀ then D_X·V per half-step)",
         "achieved": achieved, "unit": "TFLOP/s",
         "peak": peak,
-        "peak_source": (f"measured {'bf16/fp16' if f16_pipe else 'TF32'} dense sustained peak "
-                        f"({'MEASURED_PEAKS.json bf16_tflops_sustained' if f16_pipe else 'cuBLAS TF32, this run'}) "
+        "peak_source": (f"measured {'bf16/fp16' if f16_pipe else 'TF32'} dense burst peak "
+                        f"({'MEASURED_PEAKS.json bf16_tflops (burst)' if f16_pipe else 'cuBLAS TF32 burst, this run'}) "
                         f"/ {passes} split passes ({label}, fp32 accumulate)"),
         "frac": (achieved / peak) if (achieved and peak) else None,
         "tf32_roofline": tf32_peak,
@@ -401,7 +403,10 @@ def run_ours(args, world, rank, local, dist):
         "precision": label, "passes": passes, "mma_kind": kind,
         "executed_tflops": achieved * passes if achieved else None,
         "executed_peak": exec_peak,
-        "executed_peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (fp16 and bf16 share "
+        "executed_frac_vs_sustained": (achieved * passes / peaks["bf16_tflops_sustained"])
+                                      if (achieved and f16_pipe and peaks.get("bf16_tflops_sustained")) else None,
+        "frac_vs_tf32_roofline_burst": (achieved / tf32["burst"]) if (achieved and tf32) else None,
+        "executed_peak_source": ("MEASURED_PEAKS.json bf16_tflops, burst (fp16 and bf16 share "
                                  "the kind::f16 rate)" if f16_pipe else "cuBLAS TF32 measured in this run"),
         "executed_frac": (achieved * passes / exec_peak) if (achieved and exec_peak) else None,
         "algorithmic_flops_per_launch_pair": chain_flops,

@@ -813,9 +813,30 @@ int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b, int64_t ldb,
       d.b_lo = blo;
       d.three_pass = true;
     }
+    void* a16 = nullptr;
+    float* bpl = nullptr;
+    if (precision == GWB_PREC_F16X2 || precision == GWB_PREC_BF16X3) {
+      // Split-plane path: A (exact in fp16 / bf16) × planes of B (fp16 planes
+      // at scale 1: B must lie inside fp16 range).
+      const bool f16 = precision == GWB_PREC_F16X2;
+      GWB_CUDA(cudaMallocAsync(&a16, sizeof(uint16_t) * M * lda + 256, s));
+      GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bpl), 6 * N * ldb + 256, s));
+      if (f16) gwb::launch_to_f16(a, M, K, lda, a16, s);
+      else gwb::launch_to_bf16(a, M, K, lda, a16, s);
+      gwb::launch_tf32_aux(b, N, K, ldb, bpl, f16 ? 5 : 3, s, 1.0f);
+      d.a = nullptr;
+      d.b = nullptr;
+      d.f16 = f16;
+      d.bf16_planes = f16 ? 2 : 3;
+      d.a_bf16 = a16;
+      for (int k = 0; k < d.bf16_planes; ++k)
+        d.b_bf16[k] = reinterpret_cast<uint16_t*>(bpl) + static_cast<int64_t>(k) * N * ldb;
+    }
     gwb::GemmPlan* p = gwb::gemm_plan_create(d);
     const cudaError_t e = gwb::gemm_launch(p, s);
     gwb::gemm_plan_destroy(p);
+    if (a16) cudaFreeAsync(a16, s);
+    if (bpl) cudaFreeAsync(bpl, s);
     if (alo) cudaFreeAsync(alo, s);
     if (blo) cudaFreeAsync(blo, s);
     GWB_CUDA(e);

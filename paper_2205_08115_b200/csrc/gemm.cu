@@ -617,15 +617,23 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   g.group_m = group_env > 0 ? group_env : kGroupM;
-  // Split planes share one pipeline stage (A loaded once per k-block).  The
-  // promotion chunk stays at the same MMA count: promote_every (pass,
-  // k-block) items = promote_every·4 MMAs → ⌈promote_every / passes⌉
-  // k-blocks of all planes (2 planes: 1 k-block = 8 MMAs, as before).
+  // Split planes share one pipeline stage (A loaded once per k-block).
+  // Promotion chunk: 2·promote_every k-blocks of all planes (4: 256 K
+  // elements, 32 MMAs for f16x2).  Short chunks leave the MMA warp waiting
+  // on the epilogue drain: c4 8.86 / 10.45 / 11.21 / 11.56 it/s at 1 / 2 /
+  // 3 / 4 k-blocks (one box).  Truncation bias of the chunk, measured with
+  // all-positive terms at K = 20000 (tools/acc_probe.py): mean −2.0e-7,
+  // max 6.7e-7 relative at 4 k-blocks (f16x2), vs −4.5e-8 / 5.7e-7 at 1.
   static const bool unfused_env = std::getenv("GWB_GEMM_UNFUSED") != nullptr;
   if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env) {
     g.fused = 1;
-    if (d.promote_every > 0)
-      g.chunk = std::max(1, (d.promote_every + d.bf16_planes - 1) / d.bf16_planes);
+    if (d.promote_every > 0) g.chunk = 2 * d.promote_every;
+    // A/B knob: k-blocks per promotion chunk in the fused schedule.
+    static const int chunk_env = [] {
+      const char* e = std::getenv("GWB_GEMM_CHUNK_KB");
+      return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    if (chunk_env > 0) g.chunk = chunk_env;
   }
   g.b_block_k = static_cast<int32_t>(d.b_block_k);
   if (d.b_block_k > 0 &&

@@ -54,3 +54,19 @@ def test_gemm_precision(gpu, precision, tol):
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     rel = np.abs(c - ref).max() / np.abs(ref).max()
     assert rel < tol, rel
+
+
+@pytest.mark.parametrize("precision", [7, 3])  # f16x2, bf16x3 split-plane chains
+def test_split_gemm_long_k_accumulation(gpu, precision):
+    # c4-length K with all-positive terms (the worst case for the tensor
+    # core's truncating accumulation): 0/1 A × positive B against fp64.
+    # The promotion of each chunk into fp32 registers bounds the bias.
+    import torch
+    rng = np.random.default_rng(3)
+    M, N, K = 256, 256, 20000
+    a = (rng.random((M, K)) < 0.5).astype(np.float32)
+    b = rng.uniform(0.25, 1.0, (N, K)).astype(np.float32)
+    c = _gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), precision)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    err = (c - ref) / ref
+    assert np.abs(err).max() < 2e-6, (np.abs(err).max(), err.mean())
