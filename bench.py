@@ -181,7 +181,7 @@ def measure_tf32_peak(torch, sustain_s=3.0):
 
 # ---------------------------------------------------------------------------
 def build_instance(n, seed=0):
-    from paper_2205_08115_b200 import instances as I
+    from harness import instances as I
     e = I.barabasi_albert(n, 5, I.mix_seed(seed, 41))
     noisy = I.edge_noise(n, e, 0.02, 0.02, I.mix_seed(I.mix_seed(seed, 41), 1))
     tgt, perm = I.permute_graph(n, noisy, I.mix_seed(I.mix_seed(seed, 41), 2))
@@ -202,7 +202,7 @@ def cpu_reference_sample(n_target, cpu_n, budget_s=20.0):
     FLOP ratio of the GEMM-dominated iteration (6·n·m·(n+m), n=m ⇒ ∝ n³)."""
     from oracle.bindings import Oracle
     from paper_2205_08115_b200 import abi
-    from paper_2205_08115_b200 import instances as I
+    from harness import instances as I
     cores = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     ref = Oracle("reference")
@@ -700,7 +700,8 @@ def run_e2e(args, edges, tgt, n, prec):
     H2D of D_X, D_Y, μ, ν and D2H of the final coupling + trace inside the
     timed region.  Iterations/s = e2e_iters / wall time of the call."""
     import torch
-    from paper_2205_08115_b200 import abi, instances as I
+    from paper_2205_08115_b200 import abi
+    from harness import instances as I
 
     def pinned(shape):
         # Page-locked host buffers (the contract's "pinned host memory"):
@@ -766,7 +767,22 @@ def main():
     _JSON_FD = os.dup(1)
     os.dup2(2, 1)  # C-level writes to fd 1 (e.g. "NCCL version …") land on stderr
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: one rank per GPU under
+        # torch.distributed.run (the driver's own launch form).
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.dup2(_JSON_FD, 1)
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                  f"--master-port={port}", os.path.abspath(__file__),
+                                  *sys.argv[1:]])
     world, rank, local, dist = dist_setup(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks "
+                         "(WORLD_SIZE); they must agree")
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -17,7 +17,7 @@
 #include <utility>
 #include <vector>
 
-#include "../../include/gwb_ext.h"
+#include "gwbinst.h"
 
 namespace {
 
@@ -25,6 +25,7 @@ class Rng {  // same draw sequence as gw::Rng (rng.hpp:13-53)
  public:
   explicit Rng(uint64_t seed) : eng_(seed) {}
   double uniform01() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
+  double uniform(double a, double b) { return a + (b - a) * uniform01(); }
   uint64_t below(uint64_t n) {
     const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
     uint64_t r;
@@ -90,7 +91,7 @@ uint64_t key(int32_t a, int32_t b) {
 extern "C" {
 
 // Barabási–Albert graph, algorithm of gen_barabasi_albert (tasks.cpp:22-65).
-GWB_API int64_t gwb_gen_barabasi_albert(int32_t n, int32_t m_attach, uint64_t seed,
+GWBINST_API int64_t gwbinst_gen_barabasi_albert(int32_t n, int32_t m_attach, uint64_t seed,
                                 int32_t* out, int64_t cap) {
   if (m_attach < 1 || m_attach >= n) return -1;
   Rng rng(seed);
@@ -130,7 +131,7 @@ GWB_API int64_t gwb_gen_barabasi_albert(int32_t n, int32_t m_attach, uint64_t se
 // Erdős–Rényi G(n, p): gen_gaussian_partition(n, 1, p, 0, seed)
 // (tasks.cpp:67-112) with a single cluster, which draws the cluster size
 // from one Box-Muller normal and then one uniform per pair i<j.
-GWB_API int64_t gwb_gen_erdos_renyi(int32_t n, double p, uint64_t seed, int32_t* out,
+GWBINST_API int64_t gwbinst_gen_erdos_renyi(int32_t n, double p, uint64_t seed, int32_t* out,
                             int64_t cap) {
   Rng rng(seed);
   (void)rng.normal();  // the k=1 cluster-size draw; size is then forced to n
@@ -143,7 +144,7 @@ GWB_API int64_t gwb_gen_erdos_renyi(int32_t n, double p, uint64_t seed, int32_t*
 
 // Stochastic block model with k equal blocks (label = i·k/n): new generator
 // (the reference's planted partition uses Gaussian block sizes).
-GWB_API int64_t gwb_gen_sbm_equal(int32_t n, int32_t k, double p_in, double p_out,
+GWBINST_API int64_t gwbinst_gen_sbm_equal(int32_t n, int32_t k, double p_in, double p_out,
                           uint64_t seed, int32_t* out, int64_t cap,
                           int32_t* labels) {
   Rng rng(seed);
@@ -161,7 +162,7 @@ GWB_API int64_t gwb_gen_sbm_equal(int32_t n, int32_t k, double p_in, double p_ou
 // add_noise samples, tasks.cpp:131-137) and add floor(q_add·|E|) pairs absent
 // from the input graph by rejection sampling (the reference enumerates all
 // absent pairs, O(n²) memory, impractical at n = 20000).  New generator.
-GWB_API int64_t gwb_edge_noise(int32_t n, const int32_t* edges, int64_t count,
+GWBINST_API int64_t gwbinst_edge_noise(int32_t n, const int32_t* edges, int64_t count,
                        double q_remove, double q_add, uint64_t seed,
                        int32_t* out, int64_t cap) {
   Rng rng(seed);
@@ -194,7 +195,7 @@ GWB_API int64_t gwb_edge_noise(int32_t n, const int32_t* edges, int64_t count,
 
 // Uniform relabeling, algorithm of permute_graph (tasks.cpp:141-154);
 // perm maps old index -> new.
-GWB_API int64_t gwb_permute_graph(int32_t n, const int32_t* edges, int64_t count,
+GWBINST_API int64_t gwbinst_permute_graph(int32_t n, const int32_t* edges, int64_t count,
                           uint64_t seed, int32_t* out, int32_t* perm) {
   Rng rng(seed);
   std::vector<int32_t> p(static_cast<size_t>(n));
@@ -212,7 +213,7 @@ GWB_API int64_t gwb_permute_graph(int32_t n, const int32_t* edges, int64_t count
 // 3-D isotropic Gaussian mixture (new generator for config 2): k means
 // uniform in [0,1]^3, each point picks a component with `below(k)` and adds
 // sigma·N(0, I).  Points are row-major n×3.
-GWB_API void gwb_gen_gmm3d(int32_t n, int32_t k, double sigma, uint64_t seed,
+GWBINST_API void gwbinst_gen_gmm3d(int32_t n, int32_t k, double sigma, uint64_t seed,
                    double* xyz) {
   Rng rng(seed);
   std::vector<double> means(static_cast<size_t>(3 * k));
@@ -225,7 +226,7 @@ GWB_API void gwb_gen_gmm3d(int32_t n, int32_t k, double sigma, uint64_t seed,
 
 // Euclidean distance matrix (fp64 math), divided by its max and rounded to
 // fp32 so that fp32 and fp64 consumers see identical values.  out: n×n fp32.
-GWB_API void gwb_distance_maxnorm_f32(int32_t n, const double* xyz, float* out) {
+GWBINST_API void gwbinst_distance_maxnorm_f32(int32_t n, const double* xyz, float* out) {
   std::vector<double> d(static_cast<size_t>(n) * n);
   double mx = 0.0;
   for (int i = 0; i < n; ++i) {
@@ -239,6 +240,23 @@ GWB_API void gwb_distance_maxnorm_f32(int32_t n, const double* xyz, float* out) 
     }
   }
   for (size_t k = 0; k < d.size(); ++k) out[k] = static_cast<float>(mx > 0 ? d[k] / mx : 0.0);
+}
+
+// jittered_product (experiment.cpp:41-58): the reference's seeded start for
+// the experiment harness.  Entries are drawn column by column; the sum is a
+// plain running sum in the same order.
+GWBINST_API void gwbinst_jittered_product(const double* mu, int64_t n, const double* nu, int64_t m,
+                                          double jitter, uint64_t seed, double* out) {
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t i = 0; i < n; ++i) out[j * n + i] = mu[i] * nu[j];
+  if (jitter > 0.0) {
+    Rng rng(seed);
+    for (int64_t j = 0; j < m; ++j)
+      for (int64_t i = 0; i < n; ++i) out[j * n + i] *= 1.0 + jitter * rng.uniform(-1.0, 1.0);
+    double total = 0.0;
+    for (int64_t k = 0; k < n * m; ++k) total += out[k];
+    for (int64_t k = 0; k < n * m; ++k) out[k] /= total;
+  }
 }
 
 }  // extern "C"

@@ -1,8 +1,10 @@
 """Seeded synthetic workloads of BASELINE.json.
 
-Edge lists come from the C++ generators in ``libgwb.so`` (reference RNG and,
-where the reference has one, the reference algorithm); dense matrices are
-built here.  The same arrays feed the GPU path and the CPU oracle.
+Bench / test harness, not product code.  Edge lists come from the C++
+generators in ``harness/libgwbinst.so`` (reference RNG and, where the
+reference has one, the reference algorithm; built by ``build.py`` with g++,
+no CUDA); dense matrices are built here.  The same arrays feed the GPU path
+and the CPU oracle.  The product library ``libgwb.so`` holds no generator.
 """
 from __future__ import annotations
 
@@ -12,34 +14,43 @@ from typing import Optional
 
 import numpy as np
 
-from . import abi
+import os
 
 _I32P = C.POINTER(C.c_int32)
 _DP = C.POINTER(C.c_double)
 _FP = C.POINTER(C.c_float)
 
 _SIGS = {
-    "gwb_gen_barabasi_albert": (C.c_int64, [C.c_int32, C.c_int32, C.c_uint64, _I32P, C.c_int64]),
-    "gwb_gen_erdos_renyi": (C.c_int64, [C.c_int32, C.c_double, C.c_uint64, _I32P, C.c_int64]),
-    "gwb_gen_sbm_equal": (C.c_int64, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64,
+    "gwbinst_gen_barabasi_albert": (C.c_int64, [C.c_int32, C.c_int32, C.c_uint64, _I32P, C.c_int64]),
+    "gwbinst_gen_erdos_renyi": (C.c_int64, [C.c_int32, C.c_double, C.c_uint64, _I32P, C.c_int64]),
+    "gwbinst_gen_sbm_equal": (C.c_int64, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64,
                                       _I32P, C.c_int64, _I32P]),
-    "gwb_edge_noise": (C.c_int64, [C.c_int32, _I32P, C.c_int64, C.c_double, C.c_double, C.c_uint64,
+    "gwbinst_edge_noise": (C.c_int64, [C.c_int32, _I32P, C.c_int64, C.c_double, C.c_double, C.c_uint64,
                                    _I32P, C.c_int64]),
-    "gwb_permute_graph": (C.c_int64, [C.c_int32, _I32P, C.c_int64, C.c_uint64, _I32P, _I32P]),
-    "gwb_gen_gmm3d": (None, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, _DP]),
-    "gwb_distance_maxnorm_f32": (None, [C.c_int32, _DP, _FP]),
+    "gwbinst_permute_graph": (C.c_int64, [C.c_int32, _I32P, C.c_int64, C.c_uint64, _I32P, _I32P]),
+    "gwbinst_gen_gmm3d": (None, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, _DP]),
+    "gwbinst_distance_maxnorm_f32": (None, [C.c_int32, _DP, _FP]),
+    "gwbinst_jittered_product": (None, [_DP, C.c_int64, _DP, C.c_int64, C.c_double, C.c_uint64,
+                                        _DP]),
 }
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgwbinst.so")
+_LIB = None
 
 
 def _lib():
-    lib = abi.load()
-    if not getattr(lib, "_gen_ready", False):
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            from paper_2205_08115_b200 import build
+            build.build_harness()
+        lib = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        lib._gen_ready = True
-    return lib
+        _LIB = lib
+    return _LIB
 
 
 def _ip(a: np.ndarray):
@@ -60,12 +71,12 @@ def _call_edges(fn, cap_hint: int, *args):
 
 def barabasi_albert(n: int, m_attach: int, seed: int) -> np.ndarray:
     """gen_barabasi_albert (tasks.cpp:22-65)."""
-    return _call_edges(_lib().gwb_gen_barabasi_albert, n * m_attach + 64, n, m_attach, seed)
+    return _call_edges(_lib().gwbinst_gen_barabasi_albert, n * m_attach + 64, n, m_attach, seed)
 
 
 def erdos_renyi(n: int, p: float, seed: int) -> np.ndarray:
     """G(n, p) = gen_gaussian_partition(n, 1, p, 0, seed) (tasks.cpp:67-112)."""
-    return _call_edges(_lib().gwb_gen_erdos_renyi, int(p * n * n / 2 * 1.2) + 64, n, p, seed)
+    return _call_edges(_lib().gwbinst_gen_erdos_renyi, int(p * n * n / 2 * 1.2) + 64, n, p, seed)
 
 
 def sbm_equal(n: int, k: int, p_in: float, p_out: float, seed: int):
@@ -75,7 +86,7 @@ def sbm_equal(n: int, k: int, p_in: float, p_out: float, seed: int):
     cap = est
     while True:
         buf = np.empty(2 * cap, dtype=np.int32)
-        cnt = lib.gwb_gen_sbm_equal(n, k, p_in, p_out, seed, _ip(buf), cap, _ip(labels))
+        cnt = lib.gwbinst_gen_sbm_equal(n, k, p_in, p_out, seed, _ip(buf), cap, _ip(labels))
         if cnt <= cap:
             return buf[: 2 * cnt].reshape(-1, 2), labels
         cap = int(cnt)
@@ -84,7 +95,7 @@ def sbm_equal(n: int, k: int, p_in: float, p_out: float, seed: int):
 def edge_noise(n: int, edges: np.ndarray, q_remove: float, q_add: float, seed: int) -> np.ndarray:
     e = np.ascontiguousarray(edges, dtype=np.int32)
     cnt = e.shape[0]
-    return _call_edges(_lib().gwb_edge_noise, cnt + int(q_add * cnt) + 16, n, _ip(e), cnt,
+    return _call_edges(_lib().gwbinst_edge_noise, cnt + int(q_add * cnt) + 16, n, _ip(e), cnt,
                        q_remove, q_add, seed)
 
 
@@ -93,7 +104,7 @@ def permute_graph(n: int, edges: np.ndarray, seed: int):
     e = np.ascontiguousarray(edges, dtype=np.int32)
     out = np.empty_like(e)
     perm = np.empty(n, dtype=np.int32)
-    cnt = _lib().gwb_permute_graph(n, _ip(e), e.shape[0], seed, _ip(out), _ip(perm))
+    cnt = _lib().gwbinst_permute_graph(n, _ip(e), e.shape[0], seed, _ip(out), _ip(perm))
     return out[:cnt], perm
 
 
@@ -108,7 +119,7 @@ def adjacency(n: int, edges: np.ndarray, dtype=np.float64) -> np.ndarray:
 
 def gmm_points(n: int, k: int, sigma: float, seed: int) -> np.ndarray:
     xyz = np.empty((n, 3), dtype=np.float64)
-    _lib().gwb_gen_gmm3d(n, k, sigma, seed, xyz.ctypes.data_as(_DP))
+    _lib().gwbinst_gen_gmm3d(n, k, sigma, seed, xyz.ctypes.data_as(_DP))
     return xyz
 
 
@@ -116,8 +127,19 @@ def distance_maxnorm(xyz: np.ndarray) -> np.ndarray:
     n = xyz.shape[0]
     out = np.empty((n, n), dtype=np.float32)
     x = np.ascontiguousarray(xyz, dtype=np.float64)
-    _lib().gwb_distance_maxnorm_f32(n, x.ctypes.data_as(_DP), out.ctypes.data_as(_FP))
+    _lib().gwbinst_distance_maxnorm_f32(n, x.ctypes.data_as(_DP), out.ctypes.data_as(_FP))
     return np.asfortranarray(out.astype(np.float64))
+
+
+def jittered_product(mu: np.ndarray, nu: np.ndarray, jitter: float, seed: int) -> np.ndarray:
+    """jittered_product (experiment.cpp:41-58): the reference harness's start,
+    μνᵀ with a seeded multiplicative jitter, renormalised.  n×m, Fortran order."""
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    nu = np.ascontiguousarray(nu, dtype=np.float64)
+    out = np.empty((mu.size, nu.size), dtype=np.float64, order="F")
+    _lib().gwbinst_jittered_product(mu.ctypes.data_as(_DP), mu.size, nu.ctypes.data_as(_DP),
+                                    nu.size, float(jitter), seed, out.ctypes.data_as(_DP))
+    return out
 
 
 def mix_seed(seed: int, k: int) -> int:

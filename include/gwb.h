@@ -40,11 +40,16 @@ enum gwb_geometry { GWB_ENTROPY = 0, GWB_QUADRATIC = 1 };
 enum gwb_axis { GWB_ROWS = 0, GWB_COLS = 1 };
 
 /* Tensor-core precision of the D_X·π·D_Y chain (B200 extension, not in
- * SolverConfig).  3xTF32 splits the non-exact operands into hi + lo TF32
- * parts (a 0/1 structure matrix is exact, so its lo pass is dropped) and
- * meets the π (1e-4) and objective (1e-5) parity bounds; 1xTF32 uses
- * rna-rounded operands and is faster but misses the objective bound.
- * AUTO currently resolves to 3xTF32. */
+ * SolverConfig).  All modes keep fp32 iterates and fp32 accumulation.
+ * AUTO picks, by the exactness of the structure matrices:
+ *   - both exact in fp16 (0/1 graphs, small integer weights): F16X2 — in the
+ *     BAPG, eBPG / BPG / hBPG and row-sharded engines;
+ *   - exact in bf16 only: BF16X3 (also the skinny m ≤ 32 chain and the
+ *     batched n, m ≤ 128 kernel for 0/1 graphs);
+ *   - otherwise: 3XTF32 (hi/lo splits of both operands).
+ * An explicit split-plane request (F16X2 / BF16X3 / BF16X2) on a D that is
+ * not exact in that format falls back F16X2 -> BF16X3 -> 3XTF32, as AUTO
+ * would; TF32 (1 pass) and BF16X2 are faster, reduced-precision opt-ins. */
 enum gwb_precision {
   GWB_PREC_AUTO = 0,
   GWB_PREC_TF32 = 1,    /* 1 kind::tf32 pass, rna-rounded operands */
@@ -54,8 +59,7 @@ enum gwb_precision {
   GWB_PREC_SPARSE = 5,  /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
   GWB_PREC_FP32 = 6,    /* FP32-pipe chain for skinny problems (m ≤ 32); AUTO picks it */
   GWB_PREC_F16X2 = 7    /* exact-fp16 D × 2 fp16 planes of the power-of-two-scaled
-                           iterate (22-bit operands); AUTO picks it for 0/1 graphs
-                           (single-GPU BAPG; other solvers run it as bf16x3) */
+                           iterate (22-bit operands); AUTO picks it for 0/1 graphs */
 };
 
 /* Error codes; each maps to one reference exception class. */

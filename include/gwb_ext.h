@@ -97,28 +97,6 @@ GWB_API int32_t gwb_shard_rows(gwb_shard* s, double* pi_rows, double* w_rows,
                                gwb_status* st);
 GWB_API int32_t gwb_shard_destroy(gwb_shard* s);
 
-/* Instance generators (paper_2205_08115_b200/csrc/instances.cpp).  Edge
- * lists are int32 pairs (a < b), canonical order; return the edge count
- * (the buffer holds min(count, cap) edges) or -1 on invalid arguments. */
-GWB_API int64_t gwb_gen_barabasi_albert(int32_t n, int32_t m_attach,
-                                        uint64_t seed, int32_t* out,
-                                        int64_t cap);
-GWB_API int64_t gwb_gen_erdos_renyi(int32_t n, double p, uint64_t seed,
-                                    int32_t* out, int64_t cap);
-GWB_API int64_t gwb_gen_sbm_equal(int32_t n, int32_t k, double p_in,
-                                  double p_out, uint64_t seed, int32_t* out,
-                                  int64_t cap, int32_t* labels);
-GWB_API int64_t gwb_edge_noise(int32_t n, const int32_t* edges, int64_t count,
-                               double q_remove, double q_add, uint64_t seed,
-                               int32_t* out, int64_t cap);
-GWB_API int64_t gwb_permute_graph(int32_t n, const int32_t* edges,
-                                  int64_t count, uint64_t seed, int32_t* out,
-                                  int32_t* perm);
-GWB_API void gwb_gen_gmm3d(int32_t n, int32_t k, double sigma, uint64_t seed,
-                           double* xyz);
-GWB_API void gwb_distance_maxnorm_f32(int32_t n, const double* xyz,
-                                      float* out);
-
 /* ---------------------------------------------------------------------------
  * Row-sharded eBPG / BPG / hBPG (csrc/bregman.cu, orchestrated by dist.py).
  * Rank r owns rows [r·n_r, r·n_r + n_r) of D_X (n_r = ⌈n/world⌉ rounded up

@@ -285,14 +285,21 @@ def _solve(entry, d_x, d_y, mu, nu, config, opts):
     st = abi.Status()
 
     cb = abi.OBSERVER()
+    raised = []
     if opts.observer is not None:
         def _obs(_user, it, pi_p, w_p, nn, mm):
-            pi = np.ctypeslib.as_array(pi_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
-            w = None
-            if w_p:
-                w = np.ctypeslib.as_array(w_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
-            opts.observer(int(it), pi, w)
-            return 0
+            # An exception in the observer aborts the solve and reaches the
+            # caller unchanged, as a C++ observer's would (solvers.cpp:206).
+            try:
+                pi = np.ctypeslib.as_array(pi_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
+                w = None
+                if w_p:
+                    w = np.ctypeslib.as_array(w_p, shape=(nn * mm,)).reshape((nn, mm), order="F").copy()
+                opts.observer(int(it), pi, w)
+                return 0
+            except BaseException as ex:  # noqa: BLE001 — rethrown after the call
+                raised.append(ex)
+                return 1
         cb = abi.OBSERVER(_obs)
     gx, gy = d_x.graph(), d_y.graph()
     if gx is not None and gy is not None:
@@ -309,6 +316,8 @@ def _solve(entry, d_x, d_y, mu, nu, config, opts):
         fn(C.byref(cfg), _ptr(d_x.entries()), n, _ptr(d_y.entries()), m, _ptr(mu.weights()),
            _ptr(nu.weights()), _ptr(init), cb, None, _ptr(out_final), _ptr(out_pi),
            _ptr(out_w), trace, cap, C.byref(n_rec), C.byref(conv), C.byref(used), C.byref(st))
+    if raised:
+        raise raised[0]
     abi.raise_for(st)
     recs = [IterationRecord(iter=r.iter, objective=r.objective,
                             marginal_infeasibility=r.marginal_infeasibility,

@@ -23,7 +23,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 SOURCES = ["gemm.cu", "kernels.cu", "solver.cu", "standalone.cu", "bregman.cu", "shard.cu",
-           "batched.cu", "sparse.cu", "skinny.cu", "skinny_tc.cu", "quadratic.cu", "residual.cu", "csv.cu", "capi.cu", "instances.cpp"]
+           "batched.cu", "sparse.cu", "skinny.cu", "skinny_tc.cu", "quadratic.cu", "residual.cu", "csv.cu", "capi.cu"]
+HARNESS = os.path.join(ROOT, "harness")
+HARNESS_LIB = os.path.join(HARNESS, "libgwbinst.so")
 
 
 def _nvcc() -> str:
@@ -94,9 +96,44 @@ def build_oracle(verbose: bool = False) -> None:
         print(r.stdout)
 
 
+def build_harness(verbose: bool = False) -> str:
+    """Bench / test instance generators (harness/libgwbinst.so): host C++,
+    deliberately outside the product library."""
+    src = os.path.join(HARNESS, "instances.cpp")
+    hdr = os.path.join(HARNESS, "gwbinst.h")
+    if (os.path.exists(HARNESS_LIB)
+            and os.path.getmtime(HARNESS_LIB) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+        return HARNESS_LIB
+    cmd = ["g++", "-O3", "-std=c++20", "-fPIC", "-shared", "-fvisibility=hidden", src,
+           "-o", HARNESS_LIB + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"harness build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    os.replace(HARNESS_LIB + ".tmp", HARNESS_LIB)
+    if verbose:
+        print(f"built {HARNESS_LIB}")
+    return HARNESS_LIB
+
+
+def build_dropin(verbose: bool = False) -> None:
+    """dropin/_build/libgw_dropin.so: the reference-signature drop-in
+    (dropin/gw_b200.cpp) compiled against the reference headers where they
+    lie, linked to libgwb.so — built only where /root/reference exists (this
+    container); the GPU box uses the prebuilt file."""
+    if not os.path.isdir("/root/reference/proj/include"):
+        return
+    r = subprocess.run(["make", "-C", os.path.join(ROOT, "dropin")], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"drop-in build failed\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(r.stdout)
+
+
 def build_all(verbose: bool = False) -> None:
     build_lib(verbose)
+    build_harness(verbose)
     build_oracle(verbose)
+    build_dropin(verbose)
 
 
 if __name__ == "__main__":

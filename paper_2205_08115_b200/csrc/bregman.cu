@@ -669,6 +669,15 @@ class BregmanEngine {
                                  cudaMemcpyDeviceToDevice, s_));
     GWB_CUDA(cudaMemcpy2DAsync(Dy_, ldm_ * 4, dy, ldy * 4, m_ * 4, m_, cudaMemcpyDeviceToDevice, s_));
     if (aux_mode_ >= 3) {
+      // Split planes round D to fp16 / bf16: refuse an inexact D (the
+      // orchestrator downgrades across ranks first, dist.resolve_precision).
+      const int bits = analyze_inexact(Dx_, rows_valid_, n_, ldk_, s_) |
+                       analyze_inexact(Dy_, m_, m_, ldm_, s_);
+      if (!split_exact(cfg_.precision, bits))
+        api_fail(GWB_ERR_CONFIG,
+                 "bregman shard: the requested split-plane precision needs structure matrices "
+                 "exact in fp16 (f16x2) / bf16 (bf16x3, bf16x2); resolve it across ranks first "
+                 "(dist.resolve_precision)");
       Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_ / 2 + 16));
       Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
       if (aux_mode_ == 5) {

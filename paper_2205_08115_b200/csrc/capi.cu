@@ -719,7 +719,7 @@ int32_t gwb_bshard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t r
     if (cfg->precision != GWB_PREC_BF16X3 && cfg->precision != GWB_PREC_BF16X2 &&
         cfg->precision != GWB_PREC_3XTF32 && cfg->precision != GWB_PREC_F16X2)
       fail(GWB_ERR_CONFIG,
-           "gwb_bshard_create: resolve the precision across ranks first (bf16x3, bf16x2 or 3xtf32)");
+           "gwb_bshard_create: resolve the precision across ranks first (f16x2, bf16x3, bf16x2 or 3xtf32; dist.resolve_precision)");
     if (cfg->record_residual) fail(GWB_ERR_UNSUPPORTED, "record_residual is single-GPU only");
     auto* s = new gwb_bshard();
     s->n = n;

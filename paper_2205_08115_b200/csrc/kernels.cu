@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "../../include/gwb.h"
 #include "devutil.cuh"
 #include "kernels.cuh"
 
@@ -721,6 +722,27 @@ void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
                     int* out_inexact, cudaStream_t s) {
   analyze_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(D, rows, cols, ld, out_max, out_inexact);
+}
+
+int analyze_inexact(const float* D, int64_t rows, int64_t cols, int64_t ld, cudaStream_t s) {
+  if (rows < 1 || cols < 1) return 0;
+  void* buf = nullptr;
+  GWB_CUDA_K(cudaMallocAsync(&buf, 16, s));
+  GWB_CUDA_K(cudaMemsetAsync(buf, 0, 16, s));
+  float* d_max = static_cast<float*>(buf);
+  int* d_inexact = reinterpret_cast<int*>(static_cast<char*>(buf) + 8);
+  launch_analyze(D, rows, cols, ld, d_max, d_inexact, s);
+  int h = 0;
+  GWB_CUDA_K(cudaMemcpyAsync(&h, d_inexact, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GWB_CUDA_K(cudaFreeAsync(buf, s));
+  GWB_CUDA_K(cudaStreamSynchronize(s));
+  return h;
+}
+
+bool split_exact(int precision, int inexact_bits) {
+  if (precision == GWB_PREC_F16X2) return (inexact_bits & 4) == 0;
+  if (precision == GWB_PREC_BF16X3 || precision == GWB_PREC_BF16X2) return (inexact_bits & 2) == 0;
+  return true;
 }
 
 void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,

@@ -151,6 +151,13 @@ void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void
 // (0/1 adjacency is exact in all three).
 void launch_analyze(const float* D, int64_t rows, int64_t cols, int64_t ld, float* out_max,
                     int* out_inexact, cudaStream_t s);
+// launch_analyze + readback: the inexact bits of a structure matrix (0 for
+// an empty one).  Synchronises the stream.
+int analyze_inexact(const float* D, int64_t rows, int64_t cols, int64_t ld, cudaStream_t s);
+// True if a structure matrix with these inexact bits is represented exactly
+// by the operand copy of a split-plane chain (f16x2: fp16; bf16x3 / bf16x2:
+// bf16).  The TF32 chains split both operands and need no exact D.
+bool split_exact(int precision, int inexact_bits);
 // P = μ νᵀ (product coupling, types.cpp:204-207) in row-major fp32.
 // Post-solve readout on a device fp64 column-major coupling (n × m):
 // row/column sums, per-row argmax (hard_assignment, tasks.cpp:190-200:

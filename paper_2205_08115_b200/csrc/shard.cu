@@ -206,6 +206,11 @@ __global__ void shard_finalize_kernel(BapgDev d, const double* diag, const doubl
   }
 }
 
+// A configuration the engine refuses (maps to GWB_ERR_CONFIG).
+struct ShardConfigError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
@@ -231,7 +236,7 @@ class ShardEngine {
     // rank cannot see: the orchestrator resolves it (dist.resolve_precision).
     if (cfg.precision == GWB_PREC_AUTO)
       throw std::invalid_argument(
-          "gwb_shard_create: resolve AUTO precision across ranks first (bf16x3 or 3xtf32)");
+          "gwb_shard_create: resolve AUTO precision across ranks first (f16x2, bf16x3 or 3xtf32; dist.resolve_precision)");
     prec_ = cfg.precision;
     f16_ = prec_ == GWB_PREC_F16X2;
     bf16_ = prec_ == GWB_PREC_BF16X3 || prec_ == GWB_PREC_BF16X2 || f16_;  // split planes
@@ -323,6 +328,19 @@ class ShardEngine {
     GWB_CUDA(cudaMemcpyAsync(mu64_, d_mu.data(), 8 * std::max<int64_t>(rows_valid_, 1),
                              cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu64_, d_nu.data(), 8 * m_, cudaMemcpyHostToDevice, s_));
+    // A split-plane chain rounds D_X / D_Y to fp16 or bf16: refuse a D that
+    // is not exact there (the orchestrator agrees the precision across ranks
+    // and downgrades first, dist.resolve_precision, as the single-GPU engine
+    // does; reaching this is a caller error, never a silent rounding).
+    if (bf16_) {
+      const int bits = analyze_inexact(Dx_, rows_valid_, n_, ldk_, s_) |
+                       analyze_inexact(Dy_, m_, m_, ldm_, s_);
+      if (!split_exact(prec_, bits))
+        throw ShardConfigError(
+            "gwb_shard: the requested split-plane precision needs structure matrices exact in "
+            "fp16 (f16x2) / bf16 (bf16x3, bf16x2); resolve it across ranks first "
+            "(dist.resolve_precision)");
+    }
     // Operand copies of the structure matrices.
     if (f16_) {
       // f16x2: the scales derive from the global iterate
@@ -695,6 +713,13 @@ int32_t shard_guard(gwb_status* st, F&& f) {
     f();
     if (st) std::memset(st, 0, sizeof(*st));
     return GWB_OK;
+  } catch (const gwb::ShardConfigError& e) {
+    if (st) {
+      std::memset(st, 0, sizeof(*st));
+      st->code = GWB_ERR_CONFIG;
+      std::snprintf(st->message, sizeof(st->message), "%s", e.what());
+    }
+    return GWB_ERR_CONFIG;
   } catch (const std::exception& e) {
     if (st) {
       std::memset(st, 0, sizeof(*st));

@@ -343,7 +343,7 @@ def solve_bregman_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, worl
     plan = ShardPlan(n, world)
     rb, rv = plan.row_begin(rank), plan.rows_valid(rank)
     rows = np.ascontiguousarray(dx[rb:rb + rv], dtype=np.float32).reshape(rv, n)
-    if cfg.precision == abi.PREC_AUTO:
+    if needs_agreement(cfg):
         cfg = _agree_precision(cfg, rows if rv else None, dy, dist, device)
     shard = BregShard(cfg, n, m, rank, world, device)
     try:
@@ -611,7 +611,7 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
     import numpy as np
     import torch
     n, m = len(mu), len(nu)
-    if cfg.precision == abi.PREC_AUTO:
+    if needs_agreement(cfg):
         # Every rank checks its own rows of D_X (and D_Y); the verdicts are
         # all-reduced (minimum), so all ranks pick the same chain.
         plan = ShardPlan(n, world)
@@ -710,12 +710,28 @@ def resolve_precision(cfg: abi.Config, exact: bool, f16: bool = False) -> abi.Co
     else 3xTF32.  With sharded D_X the exactness must be agreed by every
     rank first (each rank only sees its rows): `exact` / `f16` are those
     global verdicts."""
-    if cfg.precision != abi.PREC_AUTO:
+    p = cfg.precision
+    if p == abi.PREC_AUTO:
+        p = abi.PREC_F16X2 if f16 else abi.PREC_BF16X3 if exact else abi.PREC_3XTF32
+    # An explicit split-plane request on a D that is not exact in its format
+    # falls back as the single-GPU engine does (solver.cu prepare_d):
+    # f16x2 -> bf16x3 -> 3xTF32.
+    if p == abi.PREC_F16X2 and not f16:
+        p = abi.PREC_BF16X3
+    if p in (abi.PREC_BF16X3, abi.PREC_BF16X2) and not exact:
+        p = abi.PREC_3XTF32
+    if p == cfg.precision:
         return cfg
     out = abi.Config()
     C.pointer(out)[0] = cfg
-    out.precision = abi.PREC_F16X2 if f16 else abi.PREC_BF16X3 if exact else abi.PREC_3XTF32
+    out.precision = p
     return out
+
+
+def needs_agreement(cfg: abi.Config) -> bool:
+    """AUTO and the split-plane chains depend on D's exactness, which each
+    rank only sees for its own rows."""
+    return cfg.precision in (abi.PREC_AUTO, abi.PREC_F16X2, abi.PREC_BF16X3, abi.PREC_BF16X2)
 
 
 def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, device=0,

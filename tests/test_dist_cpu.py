@@ -14,7 +14,7 @@ import pytest
 import torch.multiprocessing as mp
 
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 from paper_2205_08115_b200.dist import ShardPlan
 
 
@@ -143,7 +143,7 @@ def test_sharded_bregman_matches_oracle_gloo(port, world, over):
         assert phases == [t["phase"] for t in o.trace]
 
 
-def _agree_worker(rank, world, port, values, q):
+def _agree_worker(rank, world, port, values, q, request=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     from paper_2205_08115_b200 import dist as D
@@ -152,7 +152,9 @@ def _agree_worker(rank, world, port, values, q):
     rows[0, 1] = values[rank]  # this rank's rows of D_X
     dy = np.eye(8, dtype=np.float32)
     cfg = D.resolve_precision(abi.default_config(), True)  # pass-through check below
-    out = D._agree_precision(abi.default_config(), rows, dy, dist, 0)
+    req = abi.default_config() if request is None else abi.default_config(precision=request)
+    assert D.needs_agreement(req)
+    out = D._agree_precision(req, rows, dy, dist, 0)
     q.put((rank, out.precision, cfg.precision))
     dist.barrier()
     dist.destroy_process_group()
@@ -178,3 +180,36 @@ def test_auto_precision_agreed_across_ranks(values, expect):
         assert p.exitcode == 0
     assert all(o[1] == expect for o in out), out
     assert all(o[2] == abi.PREC_BF16X3 for o in out)  # explicit exact flag, no fp16 verdict
+
+
+@pytest.mark.parametrize("request_prec,values,expect", [
+    (abi.PREC_F16X2, (1.0, 1.0), abi.PREC_F16X2),
+    (abi.PREC_F16X2, (1.0, 2.0 ** 20), abi.PREC_BF16X3),   # weighted beyond fp16 on rank 1
+    (abi.PREC_F16X2, (0.7, 1.0), abi.PREC_3XTF32),         # rank 0: exact in neither
+    (abi.PREC_BF16X3, (1.0, 1.0 / 3.0), abi.PREC_3XTF32),
+    (abi.PREC_BF16X2, (1.0, 2.0 ** 20), abi.PREC_BF16X2),  # bf16-exact: kept
+])
+def test_explicit_split_precision_downgraded_across_ranks(request_prec, values, expect):
+    # An explicit f16x2 / bf16x3 / bf16x2 request on a weighted D must not
+    # round D silently: every rank agrees on the exactness and
+    # falls back as the single-GPU engine does (f16x2 -> bf16x3 -> 3xTF32).
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, values, q, request_prec))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(o[1] == expect for o in out), out
+
+
+def test_resolve_precision_passthrough_for_tf32_chains():
+    from paper_2205_08115_b200 import dist as D
+    for p in (abi.PREC_3XTF32, abi.PREC_TF32):
+        cfg = abi.default_config(precision=p)
+        assert not D.needs_agreement(cfg)
+        assert D.resolve_precision(cfg, False, False).precision == p

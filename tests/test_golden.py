@@ -11,7 +11,7 @@ from paper_2205_08115_b200 import abi
 
 HERE = os.path.join(os.path.dirname(__file__), "golden")
 GOLD = sorted(g for g in glob.glob(os.path.join(HERE, "*.npz"))
-              if not os.path.basename(g).startswith("leaf_"))
+              if not os.path.basename(g).startswith(("leaf_", "fp_")))
 IDS = [os.path.basename(g)[:-4] for g in GOLD]
 
 

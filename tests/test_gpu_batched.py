@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2205_08115_b200 as gw
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 PI_TOL = 1e-4
 OBJ_TOL = 1e-5

@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import paper_2205_08115_b200 as gw
-from paper_2205_08115_b200 import abi, instances as I
+from paper_2205_08115_b200 import abi
+from harness import instances as I
 
 pytestmark = pytest.mark.gpu
 

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2205_08115_b200 import abi, dist
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 pytestmark = pytest.mark.gpu
 

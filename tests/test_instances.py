@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 from tests.conftest import have_ref
 
 needs_ref = pytest.mark.skipif(not have_ref(), reason="reference build absent")

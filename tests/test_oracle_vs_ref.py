@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 CASES = [
     ("bapg-er", lambda: I.config1(seed=1, n=96), dict(algorithm=abi.BAPG, rho=0.1, max_iters=40)),

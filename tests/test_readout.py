@@ -9,7 +9,7 @@ import pytest
 
 import paper_2205_08115_b200 as gw
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 
 def _coupling(n=37, m=23, seed=0):

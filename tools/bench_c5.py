@@ -17,7 +17,7 @@ import numpy as np
 
 import paper_2205_08115_b200 as gw
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 
 def problems(batch, seed=0, n=128):

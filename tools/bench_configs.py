@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 PREC = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6, "f16x2": 7}
 

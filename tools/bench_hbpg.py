@@ -13,7 +13,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2205_08115_b200 as gw
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 
 def run(n, iters, switch):

@@ -12,7 +12,8 @@ import numpy as np
 
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import paper_2205_08115_b200 as gw  # noqa: E402
-from paper_2205_08115_b200 import abi, instances as I  # noqa: E402
+from paper_2205_08115_b200 import abi
+from harness import instances as I  # noqa: E402
 
 
 def stats():

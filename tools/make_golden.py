@@ -11,7 +11,7 @@ import numpy as np
 
 from oracle.bindings import Oracle
 from paper_2205_08115_b200 import abi
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 
 CASES = {
     "bapg_er64": (lambda: I.config1(seed=11, n=64), dict(algorithm=abi.BAPG, rho=0.1, max_iters=60)),

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
 import paper_2205_08115_b200 as gw
-from paper_2205_08115_b200 import instances as I
+from harness import instances as I
 from oracle.bindings import Oracle
 
 port = Oracle("port")
