@@ -115,7 +115,12 @@ def c5_case(ref, name, count=256, full_count=32):
             qs.append(q)
             scales.append(s)
     path = os.path.join(OUT, f"fp_{name}.npz")
-    np.savez_compressed(path, objective=np.array(objs), top_idx=np.array(tops_i),
+    # Problems may stop early (rel_change exactly 0 <= rel_tol): pad with NaN.
+    width = max(len(o) for o in objs)
+    obj = np.full((count, width), np.nan)
+    for k, o in enumerate(objs):
+        obj[k, : len(o)] = o
+    np.savez_compressed(path, objective=obj, top_idx=np.array(tops_i),
                         top_val=np.array(tops_v), rowsum=np.array(rows), colsum=np.array(cols),
                         q=np.array(qs), scale=np.array(scales), input_sha=np.array(shas),
                         iterations=np.array(its), config=cfg_vector(cfg), count=count,
