@@ -248,17 +248,85 @@ def cpu_reference_sample(n_target, cpu_n, budget_s=20.0):
     return out
 
 
+def reference_c4_instance(n, seed=0):
+    """The c4 inputs built with the REFERENCE's own generators (oracle/_ref:
+    gen_barabasi_albert tasks.cpp:22-65, permute_graph :141-154) plus the
+    harness's edge noise (no reference equivalent) — the same edges
+    build_instance() makes for our arm (tests/test_instances.py pins the
+    generators edge for edge).  Nothing from libgwb.so is loaded."""
+    import ctypes as C
+    from harness import instances as I
+    from oracle.bindings import reference_generators
+    from paper_2205_08115_b200 import abi
+    lib = reference_generators()
+    st = abi.Status()
+    cap = n * 5 + 64
+    buf = np.empty(2 * cap, dtype=np.int32)
+    cnt = C.c_int64(0)
+    I32 = C.POINTER(C.c_int32)
+    lib.gwref_gen_barabasi_albert(n, 5, I.mix_seed(seed, 41), buf.ctypes.data_as(I32), cap,
+                                  C.byref(cnt), C.byref(st))
+    abi.raise_for(st)
+    e = buf[: 2 * cnt.value].reshape(-1, 2).copy()
+    noisy = I.edge_noise(n, e, 0.02, 0.02, I.mix_seed(I.mix_seed(seed, 41), 1))
+    noisy = np.ascontiguousarray(noisy, dtype=np.int32)
+    tgt = np.empty_like(noisy)
+    perm = np.empty(n, dtype=np.int32)
+    lib.gwref_permute_graph(n, noisy.ctypes.data_as(I32), len(noisy),
+                            I.mix_seed(I.mix_seed(seed, 41), 2), tgt.ctypes.data_as(I32),
+                            perm.ctypes.data_as(I32), C.byref(st))
+    abi.raise_for(st)
+    return e, tgt
+
+
 def run_reference(args, world, rank):
+    """`--impl reference`: the reference's own CPU solver (oracle/_ref: the
+    reference TUs compiled unmodified against eigen_lite, fp64 GEMM in
+    OpenBLAS, all host threads) on OUR arm's workload — c4, BA n=m=20000.
+
+    One real reference iteration at n = 20000 is ~1e14 fp64 FLOP (three
+    D_X·π·D_Y chains: two half-steps and the per-iteration trace objective,
+    solvers.cpp:164-197), i.e. minutes on the box's host cores.  The step is
+    therefore one real iteration: gw::solve with max_iters = 1 (init +
+    iteration 1 + its trace record), timed once; K×W such steps would not
+    fit the driver's time limit, so `steps` = 1 and `warmup` = 0 are what
+    was run (the requested K / W are echoed)."""
     if rank != 0:
         return
-    cb = cpu_reference_sample(args.n, args.cpu_n)
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "it/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / cb["value"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BA graphs)",
-            "config": {"workload": WORKLOAD, "parallelism": "cpu threads"},
-            "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
+    from harness import instances as I
+    from oracle.bindings import Oracle
+    from paper_2205_08115_b200 import abi
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    n = args.n
+    t0 = time.perf_counter()
+    e, tgt = reference_c4_instance(n)
+    dx = I.adjacency(n, e)
+    dy = I.adjacency(n, tgt)
+    u = np.full(n, 1.0 / n)
+    gen_s = time.perf_counter() - t0
+    ref = Oracle("reference")
+    cfg = abi.default_config(rho=0.1, max_iters=1, rel_tol=1e-30, quiet=1)
+    t0 = time.perf_counter()
+    r = ref.solve(cfg, dx, dy, u, u)
+    dt = time.perf_counter() - t0
+    assert r.code == 0, r.message
+    value = 1.0 / dt
+    sample = (f"reference gw::solve (oracle/_ref: reference TUs + eigen_lite + OpenBLAS fp64, "
+              f"{cores} threads) on the c4 instance itself (BA n=m={n}): max_iters=1, one real "
+              f"iteration incl. its trace objective in {dt:.1f}s (instance built in {gen_s:.1f}s, "
+              f"untimed)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BA graphs, reference "
+            "generators)", "same_config": True,
+            "config": {"workload": WORKLOAD, "n": n, "m": n, "parallelism": f"cpu, {cores} threads"},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "objective_iter1": r.trace[0]["objective"],
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -419,13 +487,9 @@ def run_ours(args, world, rank, local, dist):
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = run_e2e(args, edges, tgt, n, prec)
+    configs = None
     if not args.no_variants and rank == 0:
-        for name, fn in (("c4_hbpg", lambda: hbpg_variant(n)),
-                         ("c5_batched", lambda: c5_variant(world, rank, local, None))):
-            try:
-                variants[name] = fn()
-            except Exception as ex:  # reported, not fatal
-                variants[name] = {"value": None, "error": str(ex)}
+        configs = config_rows(args, lib, abi, torch, local, peaks, tf32)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         try:
@@ -444,7 +508,8 @@ def run_ours(args, world, rank, local, dist):
                        "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
             "tflops": {"algorithmic_per_iteration": flops_it,
                        "achieved_whole_step": flops_it * value_rank / 1e12},
-            "roofline": roofline, "variants": variants, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "variants": variants, "configs": configs,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": main["launches"], "clocks": clocks.summary(),
         }
         emit(line)
@@ -651,20 +716,6 @@ def hbpg_sharded_variant(args, world, rank, local, dist, edges, tgt, iters=12, s
                     "of Vt and G), Sinkhorn sweeps replicated on every rank" % (warm + 1, iters, iters)}
 
 
-def hbpg_variant(n):
-    """c4 "plus hBPG" (rho 0.1, eps 0.1, 10 inner Sinkhorn sweeps): 12 outer
-    iterations (6 eBPG then 6 BPG) through gw.solve; rates from the device
-    trace clock, the call's wall time (host fp64 in/out) as e2e."""
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
-    import bench_hbpg
-    r = bench_hbpg.run(n, 12, 6)
-    rates = [x for x in (r["ebpg_it_per_s"], r["bpg_it_per_s"]) if x]
-    return {"value": (len(rates) / sum(1.0 / x for x in rates)) if rates else None,
-            "unit": "it/s", "ebpg_it_per_s": r["ebpg_it_per_s"], "bpg_it_per_s": r["bpg_it_per_s"],
-            "iterations": r["iters"], "e2e_seconds": r["wall_s"],
-            "note": "harmonic mean of the eBPG and BPG phase rates; chain f16x2 (0/1 graphs, AUTO)"}
-
-
 def c5_variant(world, rank, local, dist, iters=500, total=4096):
     """Config 5: 4096 ER(128, 0.1) problems x 500 BAPG iterations on the
     batched on-chip kernel, partitioned across ranks with no communication.
@@ -693,6 +744,252 @@ def c5_variant(world, rank, local, dist, iters=500, total=4096):
                     "h2d_bytes_per_step": r["h2d_bytes"], "d2h_bytes_per_step": r["d2h_bytes"],
                     "note": "one gwb_bapg_solve_batched call from pinned fp64 host buffers "
                             "(H2D of all inputs, D2H of every final coupling)"}}
+
+
+# ---------------------------------------------------------------------------
+# The other BASELINE.json configs (c1, c2, c3, c4 hBPG, c5) at their stated
+# sizes and iteration counts, each with the SURVEY §8(d) roofline and a
+# same-config reference CPU figure.
+
+def session_run(lib, abi, torch, inst, iters, device, warm=3):
+    """Device-resident BAPG on `inst` (inputs uploaded before the timed
+    region), `iters` iterations replayed as CUDA graphs on the session stream,
+    timed with CUDA events on that stream."""
+    ldn = (inst.n + 31) // 32 * 32
+    ldm = (inst.m + 31) // 32 * 32
+    up = lambda a, ld: torch.nn.functional.pad(
+        torch.tensor(np.ascontiguousarray(a), dtype=torch.float32), (0, ld - a.shape[1])).cuda()
+    dx, dy = up(inst.dx, ldn), up(inst.dy, ldm)
+    mu = torch.tensor(inst.mu, dtype=torch.float32).cuda()
+    nu = torch.tensor(inst.nu, dtype=torch.float32).cuda()
+    cfg = abi.default_config(rho=inst.solver["rho"], max_iters=iters + warm + 4, rel_tol=1e-30)
+    st = abi.Status()
+    sess = C.c_void_p()
+    lib.gwb_session_create(C.byref(cfg), inst.n, inst.m, device, C.byref(sess), C.byref(st))
+    abi.raise_for(st)
+    try:
+        lib.gwb_session_load_device(sess, dx.data_ptr(), ldn, dy.data_ptr(), ldm, mu.data_ptr(),
+                                    nu.data_ptr(), None, C.byref(st))
+        abi.raise_for(st)
+        lib.gwb_session_reset(sess, None, C.byref(st))
+        abi.raise_for(st)
+        sp = C.c_void_p()
+        lib.gwb_session_stream(sess, C.byref(sp), C.byref(st))
+        stream = torch.cuda.ExternalStream(sp.value)
+        rp, fl = C.c_int32(), C.c_double()
+        lib.gwb_session_info(sess, C.byref(rp), C.byref(fl), C.byref(st))
+        launches = C.c_int64(0)
+        lib.gwb_session_iterate(sess, warm, None, C.byref(launches), C.byref(st))
+        abi.raise_for(st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = C.c_int64(0)
+        lib.gwb_session_iterate(sess, iters, None, C.byref(launches), C.byref(st))
+        e1.record(stream)
+        e1.synchronize()
+        abi.raise_for(st)
+        return {"ms": e0.elapsed_time(e1), "launches": int(launches.value),
+                "precision": rp.value, "flops_it": fl.value}
+    finally:
+        lib.gwb_session_destroy(sess)
+
+
+def roofline_its(flops, nbytes, tflops, gbs):
+    """SURVEY §8(d) additive model: T = F / P + B / BW (the half-steps are
+    serial)."""
+    return 1.0 / (flops / (tflops * 1e12) + nbytes / (gbs * 1e9))
+
+
+def exec_peak(prec, peaks, tf32):
+    """Algorithmic FLOP/s ceiling of the chain as executed: the measured peak
+    of its MMA kind divided by its passes (f16x2 / bf16x2: 2 kind::f16,
+    bf16x3: 3, 3xTF32: 2 kind::tf32 for a 0/1 D (else 3), TF32: 1)."""
+    passes, kind = PREC_PASSES[prec]
+    if kind in ("bf16", "f16"):
+        return peaks["bf16_tflops"] / passes, f"bf16/fp16 burst {peaks['bf16_tflops']} / {passes}"
+    if kind == "tf32" and tf32:
+        return tf32["burst"] / passes, f"cuBLAS TF32 burst {tf32['burst']:.1f} / {passes}"
+    return None, "n/a"
+
+
+def cpu_ref_rate(inst, budget_s=4.0, initial=None, max_iters=None):
+    """The reference build (oracle/_ref, all host threads) on the config's own
+    instance: a probe iteration, then as many iterations as fit `budget_s`
+    (at most the config's count).  Returns it/s and the sample text."""
+    from oracle.bindings import Oracle
+    from paper_2205_08115_b200 import abi
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    ref = Oracle("reference")
+    kw = dict(inst.solver)
+    kw.update(rel_tol=1e-30, quiet=1, max_iters=1)
+    cfg = abi.default_config(**kw)
+    t0 = time.perf_counter()
+    r = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=initial)
+    t1 = time.perf_counter() - t0
+    assert r.code == 0, r.message
+    k = max(2, min(max_iters or inst.solver["max_iters"], int(budget_s / max(t1, 1e-4))))
+    cfg.max_iters = k
+    t0 = time.perf_counter()
+    r = ref.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu, initial=initial)
+    dt = time.perf_counter() - t0
+    assert r.code == 0, r.message
+    return {"value": k / dt, "unit": "it/s", "cores": cores, "kind": "reference",
+            "sample": f"reference gw::solve (oracle/_ref, OpenBLAS fp64, {cores} threads) on this "
+                      f"config's instance: {k} of its {inst.solver['max_iters']} iterations in "
+                      f"{dt:.2f}s"}
+
+
+def _c5_ref_worker(k):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from harness import instances as I
+    from oracle.bindings import Oracle
+    from paper_2205_08115_b200 import abi
+    inst = I.config5_problem(k)
+    kw = dict(inst.solver)
+    kw.update(quiet=1)
+    t0 = time.perf_counter()
+    r = Oracle("reference").solve(abi.default_config(**kw), inst.dx, inst.dy, inst.mu, inst.nu)
+    assert r.code == 0, r.message
+    return time.perf_counter() - t0
+
+
+def cpu_c5_rate(total=4096, iters=500):
+    """The reference's worker pool (experiment.cpp:273-304): `cores` parallel
+    single-threaded gw::solve calls.  A sample of 2 problems per core is
+    solved in full; batched it/s = iters ÷ (the whole batch's extrapolated
+    wall time)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    sample = 2 * cores
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_c5_ref_worker, range(sample))
+    wall = time.perf_counter() - t0
+    est = wall * total / sample
+    return {"value": iters / est, "unit": "batched it/s", "cores": cores, "kind": "reference",
+            "sample": f"reference gw::solve per problem (oracle/_ref, 1 BLAS thread each) in a "
+                      f"{cores}-process pool: {sample} of the {total} c5 problems x {iters} "
+                      f"iterations in {wall:.2f}s (pool start-up included), scaled to {total}"}
+
+
+def cpu_hbpg_rate(n_target=20000, cpu_n=2000, iters=4, switch=2):
+    """c4 hBPG on the reference build: one outer iteration at n = 20000 is
+    minutes of fp64 BLAS, so BA n=cpu_n (same generator) is timed over
+    `iters` outer iterations (eBPG then BPG) and scaled by the n^3 FLOP ratio
+    of the chain-dominated iteration."""
+    from harness import instances as I
+    inst = I.config4(n=cpu_n, algorithm="hbpg")
+    inst.solver.update(max_iters=iters, switch_iters=switch)
+    r = cpu_ref_rate(inst, budget_s=1e9, max_iters=iters)
+    scale = (cpu_n / n_target) ** 3
+    r["sample"] += f"; BA n={cpu_n} hBPG, scaled by (n/{n_target})^3 to n={n_target}"
+    r["value_at_sample_n"] = r["value"]
+    r["value"] *= scale
+    return r
+
+
+def config_rows(args, lib, abi, torch, device, peaks, tf32):
+    """c1, c2, c3 (device-resident sessions, full iteration counts), c4 hBPG
+    (full 200 iterations through gw.solve) and c5 (4096 distinct problems x
+    500 iterations through gwb_bapg_solve_batched), each with the §8(d)
+    roofline fraction and a same-config reference CPU figure."""
+    from harness import instances as I
+    bw = peaks["hbm_gbs"]
+    rows = {}
+    for name, make, iters in (("c1", I.config1, 2000), ("c2", I.config2, 1000),
+                              ("c3", I.config3, 500)):
+        inst = make()
+        r = session_run(lib, abi, torch, inst, iters, device)
+        its = iters / (r["ms"] * 1e-3)
+        n, m = inst.n, inst.m
+        flops = 4.0 * n * m * (n + m)
+        if name == "c3":  # §8(d): D_X read twice in fp32 per iteration + 24nK
+            nbytes, bound = 2.0 * n * n * 4 + 24.0 * n * m, "hbm"
+        else:
+            nbytes, bound = 24.0 * n * m, "tensor"
+        P, psrc = exec_peak(r["precision"], peaks, tf32)
+        row = {"value": its, "unit": "it/s", "iterations": iters, "ms_per_it": r["ms"] / iters,
+               "precision": PREC_LABEL[r["precision"]], "gpu_launches": r["launches"],
+               "n": n, "m": m, "bound": bound,
+               "algorithmic": {"flops_per_it": flops, "bytes_per_it": nbytes}}
+        if P:
+            rl = roofline_its(flops, nbytes, P, bw)
+            row["roofline"] = {"its": rl, "frac": its / rl, "peak_tflops": P, "peak_source": psrc,
+                               "hbm_gbs": bw, "model": "T = F_alg / P_exec + B_alg / BW_HBM"}
+        if tf32:
+            rl = roofline_its(flops, nbytes, tf32["sustained"], bw)
+            row["roofline_tf32"] = {"its": rl, "frac": its / rl,
+                                    "peak_tflops": tf32["sustained"]}
+        if not args.no_cpu:
+            try:
+                row["cpu_baseline"] = cpu_ref_rate(inst)
+            except Exception as ex:  # reported, not fatal
+                row["cpu_baseline"] = {"value": None, "error": str(ex)}
+        rows[name] = row
+        del inst
+    try:
+        rows["c4_hbpg"] = hbpg_full(args.n, peaks, tf32)
+        if not args.no_cpu:
+            rows["c4_hbpg"]["cpu_baseline"] = cpu_hbpg_rate(args.n)
+    except Exception as ex:  # reported, not fatal
+        rows["c4_hbpg"] = {"value": None, "error": str(ex)}
+    try:
+        rows["c5"] = c5_variant(1, 0, device, None)
+        f = 4096 * 4.0 * 128 * 128 * 256
+        P = peaks["bf16_tflops"] / 3
+        rows["c5"]["roofline"] = {"its": P * 1e12 / f, "frac": rows["c5"]["value"] / (P * 1e12 / f),
+                                  "peak_tflops": P, "peak_source":
+                                  f"bf16 burst {peaks['bf16_tflops']} / 3 planes (bf16x3)",
+                                  "flops_per_batched_it": f, "model": "T = F_alg / P_exec "
+                                  "(operands on-chip: no HBM term)"}
+        if not args.no_cpu:
+            rows["c5"]["cpu_baseline"] = cpu_c5_rate()
+    except Exception as ex:  # reported, not fatal
+        rows["c5"] = {"value": None, "error": str(ex)}
+    return rows
+
+
+def hbpg_full(n, peaks, tf32, iters=200, switch=100):
+    """c4 "plus hBPG" at the full config (eps 0.1, step 5, 10 inner Sinkhorn
+    sweeps, inner_tol 1e-9, switch_iters 100, 200 outer iterations) through
+    gw.solve from host fp64 buffers.  value = iterations ÷ the device trace
+    clock (reset → last record); e2e = iterations ÷ the call's wall time
+    (6.4 GB H2D of D_X, D_Y and the coupling D2H included)."""
+    import paper_2205_08115_b200 as gw
+    from harness import instances as I
+    inst = I.config4(n=n, algorithm="hbpg")
+    s = dict(inst.solver)
+    s.update(max_iters=iters, switch_iters=switch)
+    cfg = gw.SolverConfig(quiet=True, **s)
+    a = (gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+         gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu))
+    t0 = time.perf_counter()
+    rep = gw.solve(*a, cfg)
+    wall = time.perf_counter() - t0
+    tr = rep.trace
+    dev_s = tr[-1].elapsed_seconds
+    its = rep.iterations_used / dev_s
+    flops = 2.0 * n * n * (n + n)            # one chain per outer iteration
+    nbytes = 96.0 * n * n                    # §8(d): formation + 10 sweeps + write
+    bw = peaks["hbm_gbs"]
+    P = peaks["bf16_tflops"] / 2             # f16x2 chain (AUTO for 0/1 graphs)
+    rl = roofline_its(flops, nbytes, P, bw)
+    out = {"value": its, "unit": "it/s", "iterations": rep.iterations_used,
+           "phases": {"ebpg": sum(r.phase == 1 for r in tr), "bpg": sum(r.phase == 2 for r in tr)},
+           "device_s": dev_s, "objective": tr[-1].objective,
+           "roofline": {"its": rl, "frac": its / rl, "peak_tflops": P, "hbm_gbs": bw,
+                        "model": "T = F_alg / P_exec + B_alg / BW_HBM (F = one chain, B = 96nm)"},
+           "e2e": {"value": rep.iterations_used / wall, "unit": "it/s", "seconds": wall,
+                   "h2d_bytes_per_step": int(2 * 8 * n * n + 16 * n),
+                   "d2h_bytes_per_step": int(8 * n * n)},
+           "note": "full c4 hBPG config; the Sinkhorn sweeps exit early at inner_tol"}
+    if tf32:
+        rl = roofline_its(flops, nbytes, tf32["sustained"], bw)
+        out["roofline_tf32"] = {"its": rl, "frac": its / rl, "peak_tflops": tf32["sustained"]}
+    return out
 
 
 def run_e2e(args, edges, tgt, n, prec):
@@ -779,29 +1076,33 @@ def main():
                                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
                                   f"--master-port={port}", os.path.abspath(__file__),
                                   *sys.argv[1:]])
+    if args.impl == "reference":
+        # The reference is a CPU solver: rank 0 alone runs and prints it.
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        run_reference(args, world, int(os.environ.get("RANK", "0")))
+        return
     world, rank, local, dist = dist_setup(args)
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks "
                          "(WORLD_SIZE); they must agree")
-    if args.impl == "reference":
-        run_reference(args, world, rank)
+    if world > 1 or args.sharded:
+        if dist is None:  # one-rank process group so the NCCL calls are real
+            import torch
+            import torch.distributed as tdist
+            torch.cuda.set_device(local)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                import socket
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            tdist.init_process_group("nccl", rank=0, world_size=1)
+            dist = tdist
+        run_sharded_bench(args, world, rank, local, dist)
     else:
-        if world > 1 or args.sharded:
-            if dist is None:  # one-rank process group so the NCCL calls are real
-                import torch
-                import torch.distributed as tdist
-                torch.cuda.set_device(local)
-                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                if "MASTER_PORT" not in os.environ:
-                    import socket
-                    with socket.socket() as sk:
-                        sk.bind(("127.0.0.1", 0))
-                        os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
-                tdist.init_process_group("nccl", rank=0, world_size=1)
-                dist = tdist
-            run_sharded_bench(args, world, rank, local, dist)
-        else:
-            run_ours(args, world, rank, local, dist)
+        run_ours(args, world, rank, local, dist)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -84,6 +84,11 @@ GWB_API int32_t gwb_shard_gemm2_chunk(gwb_shard* s, int32_t src, int32_t tail,
                                       gwb_status* st);
 /* Kernels launched so far by phases 0-5 of this shard (measurement hook). */
 GWB_API int32_t gwb_shard_launches(gwb_shard* s, int64_t* launches);
+/* Exact fp64 marginals for this shard (host: its rows_valid entries of μ,
+ * all m of ν), after gwb_shard_load_device and before reset: the iterates
+ * are fp64 and the projections scale to these (projections.cpp:12-34). */
+GWB_API int32_t gwb_shard_set_marginals64(gwb_shard* s, const double* mu_rows, const double* nu,
+                                          gwb_status* st);
 GWB_API int32_t gwb_shard_stream(gwb_shard* s, void** stream, gwb_status* st);
 GWB_API int32_t gwb_shard_status(gwb_shard* s, int32_t* done, int32_t* iter,
                                  int32_t* flags, int32_t* converged,

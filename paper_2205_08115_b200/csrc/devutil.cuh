@@ -46,9 +46,12 @@ __device__ __forceinline__ float rna_tf32(float x) {
 }
 
 // Operand copy for the next GEMM: 1 → TF32 round-to-nearest-away (unbiased
-// 1xTF32 input), 2 → residual x − trunc_tf32(x) (3xTF32 low part).
+// 1xTF32 input), 2 → residual x − trunc_tf32(x) (3xTF32 low part), itself
+// rounded to nearest at TF32 precision: kind::tf32 truncates its fp32
+// operands, and a truncated residual biases every product low (measured:
+// 1e-6 relative on c2's weighted chain); a pre-rounded one is read exactly.
 __device__ __forceinline__ float aux_of(float x, int mode) {
-  return mode == 1 ? rna_tf32(x) : x - trunc_tf32(x);
+  return mode == 1 ? rna_tf32(x) : rna_tf32(x - trunc_tf32(x));
 }
 
 // GEMM operand copy of 4 consecutive values at element offset `off`:
@@ -90,6 +93,67 @@ __device__ __forceinline__ void aux_store4(float* aux, int mode, int64_t plane, 
     for (int q = 0; q < 4; ++q) {
       h[q] = bf16_round(v[q]);
       v[q] -= h[q];
+    }
+    *reinterpret_cast<uint2*>(base + pl * plane + off) =
+        make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+  }
+}
+
+// GEMM operand copies of 4 consecutive fp64 iterate values (entropy BAPG
+// keeps π, w in fp64).  `copy32` (nullable) receives the fp32
+// value — the hi operand of the TF32 chains and the input of the raw-iterate
+// chains (sparse, skinny).  Planes are split from the fp64 value, so the
+// split keeps the bits below fp32:
+//   mode 1: aux = rna_tf32(fp32(x));
+//   mode 2: aux = rna_tf32(x − trunc_tf32(fp32(x)))  (hi is read from copy32);
+//   mode 3/4: 3 / 2 bf16 planes, hi = rn(x), mid = rn(x − hi), …;
+//   mode 5: 2 fp16 planes of x·scale.
+__device__ __forceinline__ void aux_store4_64(float* aux, float* copy32, int mode, int64_t plane,
+                                              int64_t off, const double (&x)[4], float scale) {
+  if (copy32) {
+    *reinterpret_cast<float4*>(copy32 + off) =
+        make_float4(static_cast<float>(x[0]), static_cast<float>(x[1]), static_cast<float>(x[2]),
+                    static_cast<float>(x[3]));
+  }
+  if (!aux) return;
+  if (mode <= 2) {
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float f = static_cast<float>(x[q]);
+      o[q] = mode == 1 ? rna_tf32(f)
+                       : rna_tf32(static_cast<float>(x[q] - static_cast<double>(trunc_tf32(f))));
+    }
+    *reinterpret_cast<float4*>(aux + off) = make_float4(o[0], o[1], o[2], o[3]);
+    return;
+  }
+  if (mode == 5) {
+    __half* base = reinterpret_cast<__half*>(aux);
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = x[q] * static_cast<double>(scale);
+    for (int pl = 0; pl < 2; ++pl) {
+      __half h[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        h[q] = __double2half(v[q]);
+        v[q] -= static_cast<double>(__half2float(h[q]));
+      }
+      *reinterpret_cast<uint2*>(base + pl * plane + off) =
+          make_uint2(__half_as_ushort(h[0]) | (static_cast<uint32_t>(__half_as_ushort(h[1])) << 16),
+                     __half_as_ushort(h[2]) | (static_cast<uint32_t>(__half_as_ushort(h[3])) << 16));
+    }
+    return;
+  }
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(aux);
+  double v[4] = {x[0], x[1], x[2], x[3]};
+  const int planes = mode == 3 ? 3 : 2;
+  for (int pl = 0; pl < planes; ++pl) {
+    float h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = __bfloat162float(__double2bfloat16(v[q]));
+      v[q] -= static_cast<double>(h[q]);
     }
     *reinterpret_cast<uint2*>(base + pl * plane + off) =
         make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
@@ -195,6 +259,43 @@ __device__ __forceinline__ void ms_add(MaxSum& a, float e, float v) { lse_add(a,
 __device__ __forceinline__ MaxSum ms_merge(MaxSum a, MaxSum b) { return lse_merge(a, b); }
 __device__ __forceinline__ MaxSum warp_merge(MaxSum a) { return lse_warp_merge(a); }
 
+// fp64 online (max, Σ w·e^{x−max}) with correctly rounded-class fp64
+// exponentials: the accumulator of the entropy BAPG projections, whose
+// iterates are fp64 like the reference's (the fp32 MUFU form above injects
+// ~1e-7 relative noise per element and half-step, which BAPG's saddle
+// escapes amplify past the 1e-5 objective bound on c1).
+struct Lse64 {
+  double mx;
+  double s;
+};
+__device__ __forceinline__ void lse64_add(Lse64& a, double x, double w) {
+  if (x > a.mx) {
+    a.s = __fma_rn(a.s, exp(a.mx - x), w);
+    a.mx = x;
+  } else if (x > -INFINITY) {
+    a.s = __fma_rn(w, exp(x - a.mx), a.s);
+  } else if (isnan(x)) {
+    a.mx = NAN;
+  }
+}
+__device__ __forceinline__ Lse64 lse64_merge(Lse64 a, Lse64 b) {
+  if (isnan(a.mx) || isnan(b.mx)) return Lse64{NAN, NAN};
+  if (b.mx == -INFINITY) return a;
+  if (a.mx == -INFINITY) return b;
+  const double M = a.mx > b.mx ? a.mx : b.mx;
+  return Lse64{M, __fma_rn(a.s, exp(a.mx - M), __dmul_rn(b.s, exp(b.mx - M)))};
+}
+__device__ __forceinline__ Lse64 lse64_warp_merge(Lse64 a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Lse64 b;
+    b.mx = __shfl_xor_sync(0xffffffffu, a.mx, o);
+    b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
+    a = lse64_merge(a, b);
+  }
+  return a;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -224,6 +325,39 @@ __device__ void block_reduce(MaxSum& ms, double (&sums)[kSums]) {
   for (int k = 0; k < kSums; ++k) t[k] = 0.0;
   for (int q = 0; q < kWarps; ++q) {  // fixed order ⇒ deterministic
     r = ms_merge(r, MaxSum{s_mx[q], s_s[q]});
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) t[k] += s_d[k][q];
+  }
+  ms = r;
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = t[k];
+  __syncthreads();
+}
+
+// block_reduce for the fp64 accumulator; lane 0 of each warp feeds a
+// fixed-order merge, the result is broadcast to all threads.
+template <int kThreads, int kSums>
+__device__ void block_reduce64(Lse64& ms, double (&sums)[kSums]) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ double s_mx[kWarps], s_s[kWarps];
+  __shared__ double s_d[kSums > 0 ? kSums : 1][kWarps];
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  ms = lse64_warp_merge(ms);
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) sums[k] = warp_sum(sums[k]);
+  if (l == 0) {
+    s_mx[w] = ms.mx;
+    s_s[w] = ms.s;
+#pragma unroll
+    for (int k = 0; k < kSums; ++k) s_d[k][w] = sums[k];
+  }
+  __syncthreads();
+  Lse64 r{-INFINITY, 0.0};
+  double t[kSums > 0 ? kSums : 1];
+#pragma unroll
+  for (int k = 0; k < kSums; ++k) t[k] = 0.0;
+  for (int q = 0; q < kWarps; ++q) {
+    r = lse64_merge(r, Lse64{s_mx[q], s_s[q]});
 #pragma unroll
     for (int k = 0; k < kSums; ++k) t[k] += s_d[k][q];
   }

@@ -26,10 +26,29 @@ using namespace dev;
 constexpr int kRowThreads = 256;
 
 // ---------------------------------------------------------------------------
-// The exponent argument is formed explicitly as rn(rn(g·(1/ρ)) − max): the
-// same rounded products feed the online (max, Σ) pass and the write pass, so
-// numerators and normaliser agree and no kernel variant can contract the
-// expression differently (FMA vs. multiply-then-subtract).
+// Entropy BAPG projections on fp64 iterates.  G arrives in
+// fp32 from the chain; the exponent x = g·(1/ρ), the online (max, Σ), the
+// exponentials and the iterates are fp64, as the reference computes them
+// (solvers.cpp:164-177, projections.cpp:12-34).  The same helper forms x
+// in the (max, Σ) pass and the write pass, so numerators and normaliser
+// agree bitwise.
+__device__ __forceinline__ double expo(float g, double inv_rho) {
+  return __dmul_rn(static_cast<double>(g), inv_rho);
+}
+
+__device__ __forceinline__ void load_d4(const double* p, double (&v)[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
+}
+
+__device__ __forceinline__ void store_d4(double* p, const double (&v)[4]) {
+  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+}
 
 // Half-step a: one CTA per row.
 // ---------------------------------------------------------------------------
@@ -37,27 +56,27 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   if (tail ? d.st->flags != 0 : d.st->done != 0) return;
   const int64_t i = blockIdx.x;
   const float* g = d.G + i * d.ld;
-  const float* w = d.W + i * d.ld;
+  const double* w = d.W64 + i * d.ld;
   const int64_t m = d.m;
-  const float inv_rho = d.inv_rho;
+  const double inv_rho = d.inv_rho64;
 
-  MaxSum ms{-INFINITY, 0.f};
+  Lse64 ms{-INFINITY, 0.0};
   double sums[2] = {0.0, 0.0};  // ⟨G,W⟩, ΣW
   for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
-    const float4 w4 = *reinterpret_cast<const float4*>(w + j);
+    double wv[4];
+    load_d4(w + j, wv);
     const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        ms_add(ms, __fmul_rn(gv[q], inv_rho), wv[q]);
-        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(wv[q]), sums[0]);
+        lse64_add(ms, expo(gv[q], inv_rho), wv[q]);
+        sums[0] = __fma_rn(static_cast<double>(gv[q]), wv[q], sums[0]);
         sums[1] += wv[q];
       }
     }
   }
-  block_reduce<kRowThreads, 2>(ms, sums);
+  block_reduce64<kRowThreads, 2>(ms, sums);
 
   if (threadIdx.x == 0) {
     d.row_part[i].gw = sums[0];
@@ -65,40 +84,35 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
     d.row_part[i].rowdev = dev * dev;
   }
   if (!write) return;
-  const float S = ms.s;
-  const float r = ms.mx;
+  const double S = ms.s;
+  const double r = ms.mx;
   if (threadIdx.x == 0) {
-    if (r > 700.0f) atomicOr(&d.st->flags, kFlagOverflowA);
-    if (!(S > 0.0f) || !isfinite(S) || isnan(r)) {
+    if (r > 700.0) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
       atomicOr(&d.st->flags, kFlagZeroA);
       atomicMin(&d.st->zero_index, static_cast<int>(i));
     }
   }
-  const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
-  float* p = d.P + i * d.ld;
-  const int am = d.aux_mode;
+  const double scale = d.mu64[i] / S;
+  double* p = d.P64 + i * d.ld;
   for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
-    const float4 w4 = *reinterpret_cast<const float4*>(w + j);
-    float4 o;
-    o.x = (j + 0 < m) ? scale * w4.x * __expf(__fsub_rn(__fmul_rn(g4.x, inv_rho), r)) : 0.f;
-    o.y = (j + 1 < m) ? scale * w4.y * __expf(__fsub_rn(__fmul_rn(g4.y, inv_rho), r)) : 0.f;
-    o.z = (j + 2 < m) ? scale * w4.z * __expf(__fsub_rn(__fmul_rn(g4.z, inv_rho), r)) : 0.f;
-    o.w = (j + 3 < m) ? scale * w4.w * __expf(__fsub_rn(__fmul_rn(g4.w, inv_rho), r)) : 0.f;
-    *reinterpret_cast<float4*>(p + j) = o;
-    if (d.P_aux) aux_store4(d.P_aux, am, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w, d.aux_scale);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    double wv[4], o[4];
+    load_d4(w + j, wv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = (j + q < m) ? scale * wv[q] * exp(expo(gv[q], inv_rho) - r) : 0.0;
+    store_d4(p + j, o);
+    aux_store4_64(d.P_aux, d.P, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
 }
 
 // Narrow rows (m ≤ kNarrowM, config 3): one warp per row, 8 rows per CTA,
-// lane l covering the float4 groups at columns 4l + 128v — the row sits in
+// lane l covering the 4-column groups at 4l + 128v — the row sits in
 // registers between the (max, Σ) pass and the write, no block barriers.
-// For m ≤ 128 the lane assignment is that of the CTA-per-row kernel (where
-// only warp 0 holds data at that width), so the results are bitwise
-// identical.  Widening to m ≤ 1024 (config 1) measured slower on the same
-// box (7906–7961 vs 8048 it/s: 125 CTAs for n = 1000 rows), so it stays 128.
 constexpr int kNarrowM = 128;
-constexpr int kNarrowV = kNarrowM / 128;  // float4 groups per lane
+constexpr int kNarrowV = kNarrowM / 128;  // 4-column groups per lane
 constexpr int kWarpRows = kRowThreads / 32;
 
 __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d, int write, int tail) {
@@ -107,39 +121,45 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
   if (i >= d.n) return;
   const float* g = d.G + i * d.ld;
-  const float* w = d.W + i * d.ld;
+  const double* w = d.W64 + i * d.ld;
   const int64_t m = d.m;
-  const float inv_rho = d.inv_rho;
-  MaxSum ms{-INFINITY, 0.f};
+  const double inv_rho = d.inv_rho64;
+  Lse64 ms{-INFINITY, 0.0};
   double sums[2] = {0.0, 0.0};
-  float4 g4[kNarrowV], w4[kNarrowV];
+  float gv[kNarrowV][4];
+  double wv[kNarrowV][4];
 #pragma unroll
   for (int v = 0; v < kNarrowV; ++v) {
     const int64_t j = lane * 4 + 128 * v;
-    g4[v] = w4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      gv[v][q] = 0.f;
+      wv[v][q] = 0.0;
+    }
     if (j < m) {
-      g4[v] = *reinterpret_cast<const float4*>(g + j);
-      w4[v] = *reinterpret_cast<const float4*>(w + j);
+      const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+      gv[v][0] = g4.x;
+      gv[v][1] = g4.y;
+      gv[v][2] = g4.z;
+      gv[v][3] = g4.w;
+      load_d4(w + j, wv[v]);
     }
   }
 #pragma unroll
   for (int v = 0; v < kNarrowV; ++v) {
     const int64_t j = lane * 4 + 128 * v;
     if (j >= m) break;
-    const float gv[4] = {g4[v].x, g4[v].y, g4[v].z, g4[v].w};
-    const float wv[4] = {w4[v].x, w4[v].y, w4[v].z, w4[v].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j + q < m) {
-        ms_add(ms, __fmul_rn(gv[q], inv_rho), wv[q]);
-        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(wv[q]), sums[0]);
-        sums[1] += wv[q];
+        lse64_add(ms, expo(gv[v][q], inv_rho), wv[v][q]);
+        sums[0] = __fma_rn(static_cast<double>(gv[v][q]), wv[v][q], sums[0]);
+        sums[1] += wv[v][q];
       }
     }
   }
-  ms = warp_merge(ms);
-  // The xor butterfly leaves lane-dependent roundings; every lane takes lane
-  // 0's (max, Σ), as the CTA-per-row kernel broadcasts warp 0 lane 0's.
+  ms = lse64_warp_merge(ms);
+  // The xor butterfly leaves lane-dependent roundings; every lane takes lane 0's.
   ms.mx = __shfl_sync(0xffffffffu, ms.mx, 0);
   ms.s = __shfl_sync(0xffffffffu, ms.s, 0);
   sums[0] = warp_sum(sums[0]);
@@ -150,27 +170,26 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
     d.row_part[i].rowdev = dev * dev;
   }
   if (!write) return;
-  const float S = ms.s;
-  const float r = ms.mx;
+  const double S = ms.s;
+  const double r = ms.mx;
   if (lane == 0) {
-    if (r > 700.0f) atomicOr(&d.st->flags, kFlagOverflowA);
-    if (!(S > 0.0f) || !isfinite(S) || isnan(r)) {
+    if (r > 700.0) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
       atomicOr(&d.st->flags, kFlagZeroA);
       atomicMin(&d.st->zero_index, static_cast<int>(i));
     }
   }
-  const float scale = static_cast<float>(d.mu64[i] / static_cast<double>(S));
+  const double scale = d.mu64[i] / S;
 #pragma unroll
   for (int v = 0; v < kNarrowV; ++v) {
     const int64_t j = lane * 4 + 128 * v;
     if (j >= m) break;
-    float4 o;
-    o.x = (j + 0 < m) ? scale * w4[v].x * __expf(__fsub_rn(__fmul_rn(g4[v].x, inv_rho), r)) : 0.f;
-    o.y = (j + 1 < m) ? scale * w4[v].y * __expf(__fsub_rn(__fmul_rn(g4[v].y, inv_rho), r)) : 0.f;
-    o.z = (j + 2 < m) ? scale * w4[v].z * __expf(__fsub_rn(__fmul_rn(g4[v].z, inv_rho), r)) : 0.f;
-    o.w = (j + 3 < m) ? scale * w4[v].w * __expf(__fsub_rn(__fmul_rn(g4[v].w, inv_rho), r)) : 0.f;
-    *reinterpret_cast<float4*>(d.P + i * d.ld + j) = o;
-    if (d.P_aux) aux_store4(d.P_aux, d.aux_mode, d.plane, i * d.ld + j, o.x, o.y, o.z, o.w, d.aux_scale);
+    double o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[q] = (j + q < m) ? scale * wv[v][q] * exp(expo(gv[v][q], inv_rho) - r) : 0.0;
+    store_d4(d.P64 + i * d.ld + j, o);
+    aux_store4_64(d.P_aux, d.P, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
 }
 
@@ -178,7 +197,7 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
 // Half-step b, pass 1: per (row chunk, 128-column block) partials.
 // ---------------------------------------------------------------------------
 constexpr int kColThreads = 256;
-constexpr int kColWidth = 128;  // columns per CTA (32 lanes × float4)
+constexpr int kColWidth = 128;  // columns per CTA (32 lanes × 4)
 
 __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int rows_per_chunk) {
   if (d.st->done) return;
@@ -186,25 +205,24 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
   const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
-  const float inv_rho = d.inv_rho;
-  MaxSum ms[4] = {{-INFINITY, 0.f}, {-INFINITY, 0.f}, {-INFINITY, 0.f}, {-INFINITY, 0.f}};
+  const double inv_rho = d.inv_rho64;
+  Lse64 ms[4] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}};
   double ps[4] = {0.0, 0.0, 0.0, 0.0};
   if (c0 < d.m) {
     for (int64_t i = r0 + warp; i < r1; i += kColThreads / 32) {
       const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
-      const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + c0);
-      ms_add(ms[0], __fmul_rn(g4.x, inv_rho), p4.x);
-      ms_add(ms[1], __fmul_rn(g4.y, inv_rho), p4.y);
-      ms_add(ms[2], __fmul_rn(g4.z, inv_rho), p4.z);
-      ms_add(ms[3], __fmul_rn(g4.w, inv_rho), p4.w);
-      ps[0] += p4.x;
-      ps[1] += p4.y;
-      ps[2] += p4.z;
-      ps[3] += p4.w;
+      double pv[4];
+      load_d4(d.P64 + i * d.ld + c0, pv);
+      lse64_add(ms[0], expo(g4.x, inv_rho), pv[0]);
+      lse64_add(ms[1], expo(g4.y, inv_rho), pv[1]);
+      lse64_add(ms[2], expo(g4.z, inv_rho), pv[2]);
+      lse64_add(ms[3], expo(g4.w, inv_rho), pv[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps[q] += pv[q];
     }
   }
-  __shared__ float s_mx[kColThreads / 32][kColWidth];
-  __shared__ float s_s[kColThreads / 32][kColWidth];
+  __shared__ double s_mx[kColThreads / 32][kColWidth];
+  __shared__ double s_s[kColThreads / 32][kColWidth];
   __shared__ double s_p[kColThreads / 32][kColWidth];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -217,10 +235,10 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
     const int c = threadIdx.x;
     const int64_t col = static_cast<int64_t>(blockIdx.x) * kColWidth + c;
     if (col < d.m) {
-      MaxSum r{-INFINITY, 0.f};
+      Lse64 r{-INFINITY, 0.0};
       double p = 0.0;
       for (int q = 0; q < kColThreads / 32; ++q) {
-        r = ms_merge(r, MaxSum{s_mx[q][c], s_s[q][c]});
+        r = lse64_merge(r, Lse64{s_mx[q][c], s_s[q][c]});
         p += s_p[q][c];
       }
       const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + col;
@@ -232,32 +250,48 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
 }
 
 // Half-step b, pass 2: merge chunk partials per column, raise errors.  One
-// warp per column: lanes take the row chunks, then a fixed-order warp merge
-// (a serial loop over ~60 chunks was latency-bound: 44 µs at c3).
+// warp per column: lanes take the row chunks, then a fixed-order warp merge.
 __global__ void col_combine_kernel(BapgDev d) {
   if (d.st->done) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   if (j >= d.m) return;
   const int lane = threadIdx.x & 31;
-  MaxSum r{-INFINITY, 0.f};
+  Lse64 r{-INFINITY, 0.0};
   double p = 0.0;
   for (int c = lane; c < d.chunks; c += 32) {
     const int64_t o = static_cast<int64_t>(c) * d.m + j;
-    r = ms_merge(r, MaxSum{d.col_pmax[o], d.col_psum[o]});
+    r = lse64_merge(r, Lse64{d.col_pmax[o], d.col_psum[o]});
     p += d.col_psump[o];
   }
-  r = warp_merge(r);
+  r = lse64_warp_merge(r);
   p = warp_sum(p);
   if (lane != 0) return;
-  if (r.mx > 700.0f) atomicOr(&d.st->flags, kFlagOverflowB);
-  if (!(r.s > 0.0f) || !isfinite(r.s) || isnan(r.mx)) {
+  if (r.mx > 700.0) atomicOr(&d.st->flags, kFlagOverflowB);
+  if (!(r.s > 0.0) || !isfinite(r.s) || isnan(r.mx)) {
     atomicOr(&d.st->flags, kFlagZeroB);
     atomicMin(&d.st->zero_index, static_cast<int>(j));
   }
   d.col_max[j] = r.mx;
-  d.col_scale[j] = static_cast<float>(d.nu64[j] / static_cast<double>(r.s));
+  d.col_scale[j] = d.nu64[j] / r.s;
   const double dev = p - d.nu64[j];
   d.col_dev[j] = dev * dev;
+}
+
+// One element of the half-step-b write: w' = scale_j · π · e^{x − max_j},
+// with the fused record partials (gw, split, diff, wold, gp).
+__device__ __forceinline__ double col_write_elem(float g, double p, double w, double mx,
+                                                 double sc, double inv_rho, double (&sums)[5],
+                                                 bool& finite) {
+  const double o = sc * p * exp(expo(g, inv_rho) - mx);
+  finite = finite && isfinite(o);
+  sums[0] = __fma_rn(static_cast<double>(g), o, sums[0]);
+  const double sp = p - o;
+  sums[1] = __fma_rn(sp, sp, sums[1]);
+  const double df = o - w;
+  sums[2] = __fma_rn(df, df, sums[2]);
+  sums[3] = __fma_rn(w, w, sums[3]);
+  sums[4] = __fma_rn(static_cast<double>(g), p, sums[4]);
+  return o;
 }
 
 // Half-step b, pass 3: write W_new, fused diagnostics. One CTA per row.
@@ -266,47 +300,30 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   if (d.st->flags != 0) return;
   const int64_t i = blockIdx.x;
   const float* g = d.G + i * d.ld;
-  const float* p = d.P + i * d.ld;
-  const float* wo = d.W + i * d.ld;
-  float* wn = d.W_new + i * d.ld;
-  const int am = d.aux_mode;
-  const float inv_rho = d.inv_rho;
+  const double* p = d.P64 + i * d.ld;
+  const double* wo = d.W64 + i * d.ld;
+  double* wn = d.W64_new + i * d.ld;
+  const double inv_rho = d.inv_rho64;
   const int64_t m = d.m;
   double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
   bool finite = true;
   for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
-    const float4 p4 = *reinterpret_cast<const float4*>(p + j);
-    const float4 w4 = *reinterpret_cast<const float4*>(wo + j);
-    const float4 cm = *reinterpret_cast<const float4*>(d.col_max + j);
-    const float4 cs = *reinterpret_cast<const float4*>(d.col_scale + j);
     const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-    const float mv[4] = {cm.x, cm.y, cm.z, cm.w};
-    const float sv[4] = {cs.x, cs.y, cs.z, cs.w};
-    float o[4];
+    double pv[4], wv[4], mv[4], sv[4], o[4];
+    load_d4(p + j, pv);
+    load_d4(wo + j, wv);
+    load_d4(d.col_max + j, mv);
+    load_d4(d.col_scale + j, sv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (j + q < m) {
-        o[q] = sv[q] * pv[q] * __expf(__fsub_rn(__fmul_rn(gv[q], inv_rho), mv[q]));
-        finite = finite && isfinite(o[q]);
-        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(o[q]), sums[0]);
-        const double sp = static_cast<double>(pv[q]) - o[q];
-        sums[1] = __fma_rn(sp, sp, sums[1]);
-        const double df = static_cast<double>(o[q]) - wv[q];
-        sums[2] = __fma_rn(df, df, sums[2]);
-        sums[3] = __fma_rn(static_cast<double>(wv[q]), static_cast<double>(wv[q]), sums[3]);
-        sums[4] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(pv[q]), sums[4]);
-      } else {
-        o[q] = 0.f;
-      }
-    }
-    *reinterpret_cast<float4*>(wn + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (d.W_aux) aux_store4(d.W_aux, am, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3], d.aux_scale);
+    for (int q = 0; q < 4; ++q)
+      o[q] = (j + q < m) ? col_write_elem(gv[q], pv[q], wv[q], mv[q], sv[q], inv_rho, sums, finite)
+                         : 0.0;
+    store_d4(wn + j, o);
+    aux_store4_64(d.W_aux, d.W_new, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
-  MaxSum dummy{-INFINITY, 0.f};
-  block_reduce<kRowThreads, 5>(dummy, sums);
+  Lse64 dummy{-INFINITY, 0.0};
+  block_reduce64<kRowThreads, 5>(dummy, sums);
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
     atomicOr(&d.st->flags, kFlagNonFinite);
   if (threadIdx.x == 0) {
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   }
 }
 
-// col_write for narrow rows (m ≤ 1024): one warp per row, as row_update_warps.
+// col_write for narrow rows (m ≤ 128): one warp per row, as row_update_warps.
 __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d) {
   if (d.st->done) return;
   if (d.st->flags != 0) return;
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
   if (i >= d.n) return;
   const int64_t m = d.m;
-  const float inv_rho = d.inv_rho;
+  const double inv_rho = d.inv_rho64;
   double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
   bool finite = true;
 #pragma unroll 2
@@ -335,34 +352,18 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
     const int64_t j = lane * 4 + 128 * v;
     if (j >= m) break;
     const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + j);
-    const float4 p4 = *reinterpret_cast<const float4*>(d.P + i * d.ld + j);
-    const float4 w4 = *reinterpret_cast<const float4*>(d.W + i * d.ld + j);
-    const float4 cm = *reinterpret_cast<const float4*>(d.col_max + j);
-    const float4 cs = *reinterpret_cast<const float4*>(d.col_scale + j);
     const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-    const float mv[4] = {cm.x, cm.y, cm.z, cm.w};
-    const float sv[4] = {cs.x, cs.y, cs.z, cs.w};
-    float o[4];
+    double pv[4], wv[4], mv[4], sv[4], o[4];
+    load_d4(d.P64 + i * d.ld + j, pv);
+    load_d4(d.W64 + i * d.ld + j, wv);
+    load_d4(d.col_max + j, mv);
+    load_d4(d.col_scale + j, sv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (j + q < m) {
-        o[q] = sv[q] * pv[q] * __expf(__fsub_rn(__fmul_rn(gv[q], inv_rho), mv[q]));
-        finite = finite && isfinite(o[q]);
-        sums[0] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(o[q]), sums[0]);
-        const double sp = static_cast<double>(pv[q]) - o[q];
-        sums[1] = __fma_rn(sp, sp, sums[1]);
-        const double df = static_cast<double>(o[q]) - wv[q];
-        sums[2] = __fma_rn(df, df, sums[2]);
-        sums[3] = __fma_rn(static_cast<double>(wv[q]), static_cast<double>(wv[q]), sums[3]);
-        sums[4] = __fma_rn(static_cast<double>(gv[q]), static_cast<double>(pv[q]), sums[4]);
-      } else {
-        o[q] = 0.f;
-      }
-    }
-    *reinterpret_cast<float4*>(d.W_new + i * d.ld + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (d.W_aux) aux_store4(d.W_aux, d.aux_mode, d.plane, i * d.ld + j, o[0], o[1], o[2], o[3], d.aux_scale);
+    for (int q = 0; q < 4; ++q)
+      o[q] = (j + q < m) ? col_write_elem(gv[q], pv[q], wv[q], mv[q], sv[q], inv_rho, sums, finite)
+                         : 0.0;
+    store_d4(d.W64_new + i * d.ld + j, o);
+    aux_store4_64(d.W_aux, d.W_new, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
 #pragma unroll
   for (int q = 0; q < 5; ++q) sums[q] = warp_sum(sums[q]);
@@ -443,7 +444,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(BapgDev d, double
   r.elapsed = 1e-9 * static_cast<double>(globaltimer() - st->t0);
   const double rel = sqrt(t[4]) / sqrt(t[5]);
   st->iter = k + 1;
-  if (stop_rule(rel, rel_tol)) {
+  // fp64 iterates: the reference's rule as is (solvers.cpp:208), including
+  // exact fp64 fixed points (rel_change == 0) under a pinned rel_tol; fp32
+  // iterates (quadratic geometry): dev::stop_rule.
+  if (d.P64 ? rel <= rel_tol : stop_rule(rel, rel_tol)) {
     st->converged = 1;
     st->done = 1;
   }
@@ -465,14 +469,15 @@ __global__ void status_reset_kernel(DevStatus* st) {
 // ---------------------------------------------------------------------------
 // Conversions.
 // ---------------------------------------------------------------------------
+template <class T>
 __global__ void c64_to_r32_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
-                                  float* __restrict__ dst, int64_t ld) {
-  __shared__ float tile[32][33];
+                                  T* __restrict__ dst, int64_t ld) {
+  __shared__ T tile[32][33];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;  // row block
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * 32;  // col block
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int64_t i = i0 + threadIdx.x, j = j0 + y;
-    if (i < rows && j < cols) tile[y][threadIdx.x] = static_cast<float>(src[j * rows + i]);
+    if (i < rows && j < cols) tile[y][threadIdx.x] = static_cast<T>(src[j * rows + i]);
   }
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -481,7 +486,8 @@ __global__ void c64_to_r32_kernel(const double* __restrict__ src, int64_t rows, 
   }
 }
 
-__global__ void row_sums64_kernel(const float* src, int64_t rows, int64_t cols, int64_t ld,
+template <class T>
+__global__ void row_sums64_kernel(const T* src, int64_t rows, int64_t cols, int64_t ld,
                                   double* out) {
   const int64_t i = blockIdx.x;
   double s = 0.0;
@@ -497,7 +503,8 @@ __global__ void row_sums64_kernel(const float* src, int64_t rows, int64_t cols, 
   }
 }
 
-__global__ void col_sums64_kernel(const float* src, int64_t rows, int64_t cols, int64_t ld,
+template <class T>
+__global__ void col_sums64_kernel(const T* src, int64_t rows, int64_t cols, int64_t ld,
                                   double* out) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= cols) return;
@@ -506,7 +513,8 @@ __global__ void col_sums64_kernel(const float* src, int64_t rows, int64_t cols, 
   out[j] = s;
 }
 
-__global__ void r32_to_c64_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+template <class T>
+__global__ void r32_to_c64_kernel(const T* __restrict__ src, int64_t rows, int64_t cols,
                                   int64_t ld, double* __restrict__ dst, int axis,
                                   const double* __restrict__ target,
                                   const double* __restrict__ sums) {
@@ -585,11 +593,23 @@ __global__ void f16_scales_kernel(const float* D, int64_t m, int64_t ld, float x
   }
 }
 
-__global__ void product_coupling_kernel(const float* mu, const float* nu, int64_t n, int64_t m,
-                                        int64_t ld, float* P) {
+template <class T>
+__global__ void product_coupling_kernel(const T* mu, const T* nu, int64_t n, int64_t m,
+                                        int64_t ld, T* P) {
   const int64_t i = blockIdx.x;
-  const float a = mu[i];
+  const T a = mu[i];
   for (int64_t j = threadIdx.x; j < m; j += blockDim.x) P[i * ld + j] = a * nu[j];
+}
+
+// fp32 copy / GEMM operand planes of an fp64 iterate (ld multiple of 4).
+__global__ void iterate_copies_kernel(const double* x, int64_t cols, int64_t ld, float* copy32,
+                                      float* aux, int mode, int64_t plane, float scale) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x * 4; j < cols; j += blockDim.x * 4) {
+    double v[4];
+    load_d4(x + i * ld + j, v);
+    aux_store4_64(aux, copy32, mode, plane, i * ld + j, v, scale);
+  }
 }
 
 __device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
@@ -679,16 +699,46 @@ void launch_status_reset(DevStatus* st, cudaStream_t s) { status_reset_kernel<<<
 void launch_colmajor64_to_rowmajor32(const double* src, int64_t rows, int64_t cols, float* dst,
                                      int64_t ld, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
-  c64_to_r32_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, dst, ld);
+  c64_to_r32_kernel<float><<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, dst, ld);
+}
+
+void launch_colmajor64_to_rowmajor64(const double* src, int64_t rows, int64_t cols, double* dst,
+                                     int64_t ld, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  c64_to_r32_kernel<double><<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, dst, ld);
+}
+
+template <class T>
+static void to_colmajor64(const T* src, int64_t rows, int64_t cols, int64_t ld, double* dst,
+                          int axis, const double* target, double* work, cudaStream_t s) {
+  if (axis == 0) row_sums64_kernel<T><<<static_cast<unsigned>(rows), 256, 0, s>>>(src, rows, cols, ld, work);
+  if (axis == 1) col_sums64_kernel<T><<<grid1d(cols, 256), 256, 0, s>>>(src, rows, cols, ld, work);
+  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  r32_to_c64_kernel<T><<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld, dst, axis, target, work);
 }
 
 void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t cols, int64_t ld,
                                      double* dst, int axis, const double* target, double* work,
                                      cudaStream_t s) {
-  if (axis == 0) row_sums64_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(src, rows, cols, ld, work);
-  if (axis == 1) col_sums64_kernel<<<grid1d(cols, 256), 256, 0, s>>>(src, rows, cols, ld, work);
-  dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
-  r32_to_c64_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld, dst, axis, target, work);
+  to_colmajor64(src, rows, cols, ld, dst, axis, target, work, s);
+}
+
+void launch_rowmajor64_to_colmajor64(const double* src, int64_t rows, int64_t cols, int64_t ld,
+                                     double* dst, int axis, const double* target, double* work,
+                                     cudaStream_t s) {
+  to_colmajor64(src, rows, cols, ld, dst, axis, target, work, s);
+}
+
+void launch_iterate_copies(const double* x, int64_t rows, int64_t cols, int64_t ld, float* copy32,
+                           float* aux, int mode, float scale, cudaStream_t s) {
+  if (rows < 1 || (!copy32 && !aux)) return;
+  iterate_copies_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, cols, ld, copy32, aux, mode,
+                                                                    rows * ld, scale);
+}
+
+void launch_product_coupling64(const double* mu, const double* nu, int64_t n, int64_t m, int64_t ld,
+                               double* P, cudaStream_t s) {
+  product_coupling_kernel<double><<<static_cast<unsigned>(n), 256, 0, s>>>(mu, nu, n, m, ld, P);
 }
 
 void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s) {
@@ -747,7 +797,7 @@ bool split_exact(int precision, int inexact_bits) {
 
 void launch_product_coupling(const float* mu, const float* nu, int64_t n, int64_t m, int64_t ld,
                              float* P, cudaStream_t s) {
-  product_coupling_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(mu, nu, n, m, ld, P);
+  product_coupling_kernel<float><<<static_cast<unsigned>(n), 256, 0, s>>>(mu, nu, n, m, ld, P);
 }
 
 namespace {

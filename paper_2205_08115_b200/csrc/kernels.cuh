@@ -69,29 +69,38 @@ struct ColWritePart {  // per-row fp64 partials of the half-step-b write pass
 struct BapgDev {
   int64_t n, m, ld;         // P/W/G are n×m row-major, leading dim ld
   float inv_rho;
+  double inv_rho64;
   const float* G;
   const float* mu;          // fp32 marginals
   const float* nu;
   const double* mu64;
   const double* nu64;
+  // Entropy geometry: the iterates are fp64 (P64, W64 → W64_new), as the
+  // reference's; the fp32 arrays are optional copies written alongside
+  // (nullable): the hi operand of the TF32 chains and the input of the
+  // raw-iterate chains (sparse, skinny).  Quadratic geometry (quadratic.cu)
+  // keeps fp32 iterates in P / W / W_new.
+  double* P64;
+  double* W64;              // current w (read in both half-steps)
+  double* W64_new;          // next w (written by half-step b)
   float* P;
   float* P_aux;             // GEMM copy of P, see aux_mode (nullable)
-  float* W;                 // current w (read in both half-steps)
-  float* W_new;             // next w (written by half-step b)
+  float* W;                 // current w (quadratic)
+  float* W_new;             // next w (fp32 copy / quadratic iterate)
   float* W_aux;             // GEMM copy of W_new, see aux_mode (nullable)
   int aux_mode;             // 1: aux = rna_tf32(x) (1xTF32 operand)
-                            // 2: aux = x − trunc_tf32(x) (3xTF32 residual)
+                            // 2: aux = rn_tf32(x − trunc_tf32(x)) (3xTF32 residual)
                             // 3/4: 3 / 2 bf16 split planes (bf16x3 / bf16x2)
                             // 5: 2 fp16 split planes of x·aux_scale (f16x2)
   float aux_scale;          // power of two (mode 5), else 1
   int64_t plane;            // elements per bf16 plane (n·ld)
   RowPart* row_part;        // n
   ColWritePart* cw_part;    // n
-  float* col_pmax;          // chunks × m
-  float* col_psum;          // chunks × m
+  double* col_pmax;         // chunks × m
+  double* col_psum;         // chunks × m
   double* col_psump;        // chunks × m : Σ_i P_ij partials
-  float* col_max;           // m
-  float* col_scale;         // m
+  double* col_max;          // m
+  double* col_scale;        // m
   double* col_dev;          // m : (colsum(P)_j − ν_j)²
   int chunks;
   DevStatus* st;
@@ -128,6 +137,20 @@ void launch_colmajor64_to_rowmajor32(const double* src, int64_t rows, int64_t co
 void launch_rowmajor32_to_colmajor64(const float* src, int64_t rows, int64_t cols, int64_t ld,
                                      double* dst, int axis, const double* target, double* work,
                                      cudaStream_t s);
+// The same from a row-major fp64 iterate (entropy BAPG).
+void launch_rowmajor64_to_colmajor64(const double* src, int64_t rows, int64_t cols, int64_t ld,
+                                     double* dst, int axis, const double* target, double* work,
+                                     cudaStream_t s);
+// dst (row-major fp64, ld) = src (column-major fp64).
+void launch_colmajor64_to_rowmajor64(const double* src, int64_t rows, int64_t cols, double* dst,
+                                     int64_t ld, cudaStream_t s);
+// fp32 copy (nullable) and GEMM operand planes (nullable; aux_mode / scale
+// as BapgDev) of a row-major fp64 iterate.
+void launch_iterate_copies(const double* x, int64_t rows, int64_t cols, int64_t ld, float* copy32,
+                           float* aux, int mode, float scale, cudaStream_t s);
+// P = μ νᵀ in row-major fp64.
+void launch_product_coupling64(const double* mu, const double* nu, int64_t n, int64_t m, int64_t ld,
+                               double* P, cudaStream_t s);
 // dst = 0.5 (a + b), column-major fp64 of len elements.
 void launch_average64(const double* a, const double* b, double* dst, int64_t len, cudaStream_t s);
 // GEMM operand copy of x (ld multiple of 4): mode 1: rna_tf32(x);

@@ -97,8 +97,8 @@ __global__ void shard_col_global_kernel(BapgDev d, const double* stats, int P) {
     atomicOr(&d.st->flags, kFlagZeroB);
     atomicMin(&d.st->zero_index, static_cast<int>(j));
   }
-  d.col_max[j] = static_cast<float>(mx);
-  d.col_scale[j] = static_cast<float>(d.nu64[j] / s);
+  d.col_max[j] = mx;
+  d.col_scale[j] = d.nu64[j] / s;
   const double dev = p - d.nu64[j];
   d.col_dev[j] = dev * dev;
 }
@@ -255,6 +255,8 @@ class ShardEngine {
     Dx_aux_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_));
     Dy_aux_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
     P_ = keep(dalloc<float>(nm));
+    P64_ = keep(dalloc<double>(nm));
+    for (int q = 0; q < 2; ++q) W64_[q] = keep(dalloc<double>(nm));
     P_aux_ = keep(dalloc<float>(nm * 3 / 2));
     for (int q = 0; q < 2; ++q) {
       W_[q] = keep(dalloc<float>(nm));
@@ -271,11 +273,11 @@ class ShardEngine {
     chunks_ = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>((std::max<int64_t>(rows_valid_, 1) + 63) / 64,
                              (4 * 148 + col_blocks - 1) / col_blocks)));
-    col_pmax_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
-    col_psum_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
+    col_pmax_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_psum_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
     col_psump_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
-    col_max_ = keep(dalloc<float>(ldm_));
-    col_scale_ = keep(dalloc<float>(ldm_));
+    col_max_ = keep(dalloc<double>(ldm_));
+    col_scale_ = keep(dalloc<double>(ldm_));
     col_dev_ = keep(dalloc<double>(ldm_));
     st_ = keep(dalloc<DevStatus>(1));
     rec_ = keep(dalloc<DevRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
@@ -372,8 +374,9 @@ class ShardEngine {
     GWB_CUDA(cudaSetDevice(dev_));
     launch_status_reset(st_, s_);
     if (rows_valid_ > 0) {
-      launch_product_coupling(mu32_, nu32_, rows_valid_, m_, ldm_, W_[0], s_);
-      launch_tf32_aux(W_[0], nr_, m_, ldm_, W_aux_[0], aux_mode_, s_, aux_scale());
+      launch_product_coupling64(mu64_, nu64_, rows_valid_, m_, ldm_, W64_[0], s_);
+      launch_iterate_copies(W64_[0], nr_, m_, ldm_, needs_copy() ? W_[0] : nullptr, W_aux_[0],
+                            aux_mode_, aux_scale(), s_);
     }
     parity_ = 0;
     GWB_CUDA(cudaGetLastError());
@@ -475,16 +478,23 @@ class ShardEngine {
 
   // Local rows of π and w as row-major fp64 (rows_valid × m).
   void rows(double* pi, double* w) {
-    std::vector<float> buf(static_cast<size_t>(nr_) * ldm_);
-    auto get = [&](const float* src, double* dst) {
+    auto get = [&](const double* src, double* dst) {
       if (!dst || rows_valid_ == 0) return;
-      GWB_CUDA(cudaMemcpyAsync(buf.data(), src, 4 * nr_ * ldm_, cudaMemcpyDeviceToHost, s_));
+      GWB_CUDA(cudaMemcpy2DAsync(dst, 8 * m_, src, 8 * ldm_, 8 * m_, rows_valid_,
+                                 cudaMemcpyDeviceToHost, s_));
       GWB_CUDA(cudaStreamSynchronize(s_));
-      for (int64_t i = 0; i < rows_valid_; ++i)
-        for (int64_t j = 0; j < m_; ++j) dst[i * m_ + j] = buf[i * ldm_ + j];
     };
-    get(P_, pi);
-    get(W_[parity_], w);
+    get(P64_, pi);
+    get(W64_[parity_], w);
+  }
+
+  // Exact fp64 marginals (the load path carries fp32 device copies).
+  void set_marginals64(const double* mu_rows, const double* nu) {
+    GWB_CUDA(cudaSetDevice(dev_));
+    if (rows_valid_ > 0)
+      GWB_CUDA(cudaMemcpyAsync(mu64_, mu_rows, 8 * rows_valid_, cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaMemcpyAsync(nu64_, nu, 8 * m_, cudaMemcpyHostToDevice, s_));
+    GWB_CUDA(cudaStreamSynchronize(s_));
   }
 
  private:
@@ -501,15 +511,19 @@ class ShardEngine {
     d.m = m_;
     d.ld = ldm_;
     d.inv_rho = static_cast<float>(1.0 / cfg_.rho);
+    d.inv_rho64 = 1.0 / cfg_.rho;
     d.G = G_;
     d.mu = mu32_;
     d.nu = nu32_;
     d.mu64 = mu64_;
     d.nu64 = nu64_;
-    d.P = P_;
+    d.P64 = P64_;
+    d.W64 = W64_[q];
+    d.W64_new = W64_[1 - q];
+    d.P = needs_copy() ? P_ : nullptr;
     d.P_aux = P_aux_;
     d.W = W_[q];
-    d.W_new = W_[1 - q];
+    d.W_new = needs_copy() ? W_[1 - q] : nullptr;
     d.W_aux = W_aux_[1 - q];
     d.aux_mode = aux_mode_;
     d.aux_scale = aux_scale();
@@ -683,8 +697,12 @@ class ShardEngine {
   double *mu64_, *nu64_;
   RowPart* row_part_;
   ColWritePart* cw_part_;
-  float *col_pmax_, *col_psum_, *col_max_, *col_scale_;
+  double *col_pmax_, *col_psum_, *col_max_, *col_scale_;
   double *col_psump_, *col_dev_;
+  // fp64 iterates (as the single-GPU engine); P_ / W_ hold the
+  // fp32 hi operand copies of the 3xTF32 chain only.
+  double *P64_ = nullptr, *W64_[2] = {nullptr, nullptr};
+  bool needs_copy() const { return prec_ == GWB_PREC_3XTF32; }
   int chunks_ = 1;
   DevStatus* st_;
   DevRecord* rec_;
@@ -775,6 +793,14 @@ int32_t gwb_shard_set_comm(gwb_shard* s, void* vt_gather, void* col_stats, doubl
 int32_t gwb_shard_load_device(gwb_shard* s, const float* dx_rows, int64_t ldx, const float* dy,
                               int64_t ldy, const float* mu_rows, const float* nu, gwb_status* st) {
   return shard_guard(st, [&] { s->eng->load(dx_rows, ldx, dy, ldy, mu_rows, nu); });
+}
+
+int32_t gwb_shard_set_marginals64(gwb_shard* s, const double* mu_rows, const double* nu,
+                                  gwb_status* st) {
+  return shard_guard(st, [&] {
+    if (!s || !nu) throw std::invalid_argument("gwb_shard_set_marginals64: null argument");
+    s->eng->set_marginals64(mu_rows, nu);
+  });
 }
 
 int32_t gwb_shard_set_iterate_bound(gwb_shard* s, double x_max, gwb_status* st) {

@@ -133,7 +133,7 @@ BapgEngine::~BapgEngine() {
   dfree(Vtp_, stream_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
-           W_aux_[1], Vt_,
+           W_aux_[1], P64_, W64_[0], W64_[1], Vt_,
            Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
            col_max_, col_scale_, col_psump_, col_dev_, st_, rec_, f16_g1_rs_, f16_g2_cs_})
     dfree(p, stream_);
@@ -158,6 +158,8 @@ void BapgEngine::alloc() {
     W_[q] = dalloc<float>(stream_, nm);
     W_aux_[q] = dalloc<float>(stream_, nm * 3 / 2);
   }
+  P64_ = dalloc<double>(stream_, nm);
+  for (int q = 0; q < 2; ++q) W64_[q] = dalloc<double>(stream_, nm);
   Vt_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_);
   if (precision_ != GWB_PREC_TF32)
     Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
@@ -171,11 +173,11 @@ void BapgEngine::alloc() {
   // Column-pass chunking: enough CTAs to fill the chip (≥ 2 waves of 148).
   const int64_t col_blocks = (m_ + 127) / 128;
   chunks_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n_ + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks)));
-  col_pmax_ = dalloc<float>(stream_, static_cast<size_t>(chunks_) * m_);
-  col_psum_ = dalloc<float>(stream_, static_cast<size_t>(chunks_) * m_);
+  col_pmax_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
+  col_psum_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
   col_psump_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
-  col_max_ = dalloc<float>(stream_, ldm_);
-  col_scale_ = dalloc<float>(stream_, ldm_);
+  col_max_ = dalloc<double>(stream_, ldm_);
+  col_scale_ = dalloc<double>(stream_, ldm_);
   col_dev_ = dalloc<double>(stream_, ldm_);
   st_ = dalloc<DevStatus>(stream_, 1);
   rec_ = dalloc<DevRecord>(stream_, static_cast<size_t>(max_iters_) + 2);
@@ -189,16 +191,21 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.m = m_;
   d.ld = ldm_;
   d.inv_rho = static_cast<float>(1.0 / rho_);
+  d.inv_rho64 = 1.0 / rho_;
   d.G = G_;
   d.mu = mu32_;
   d.nu = nu32_;
   d.mu64 = mu64_;
   d.nu64 = nu64_;
-  d.P = P_;
-  // The sparse chain reads the fp32 iterates directly: no operand copies.
+  d.P64 = quadratic() ? nullptr : P64_;  // null selects fp32 semantics (quadratic.cu)
+  d.W64 = W64_[q];
+  d.W64_new = W64_[1 - q];
+  // fp32 copies only where a consumer reads them; the raw-iterate chains
+  // (sparse, skinny) take no operand planes.
+  d.P = needs_copy() ? P_ : nullptr;
   d.P_aux = no_planes() ? nullptr : P_aux_;
   d.W = W_[q];
-  d.W_new = W_[1 - q];
+  d.W_new = needs_copy() ? W_[1 - q] : nullptr;
   d.W_aux = no_planes() ? nullptr : W_aux_[1 - q];
   d.aux_mode = aux_mode();
   d.aux_scale = aux_scale();
@@ -514,7 +521,25 @@ void BapgEngine::reset(const double* w0_host) {
   // Entropy: w0_host is w⁰ (the caller applied kl_scale).  Quadratic: it is
   // π⁰ (or null for μνᵀ) and w⁰ = euclid_project(π⁰, ν, Cols) on the device
   // (solvers.cpp:152-153), staged through P (overwritten by half-step a).
-  float* dst = quadratic() ? P_ : W_[0];
+  if (!quadratic()) {
+    // fp64 w⁰ (the caller's kl_scale of π⁰, or μνᵀ), then its copies.
+    if (w0_host) {
+      double* stage = nullptr;
+      GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stage), sizeof(double) * n_ * m_, stream_));
+      GWB_CUDA(cudaMemcpyAsync(stage, w0_host, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, stream_));
+      launch_colmajor64_to_rowmajor64(stage, n_, m_, W64_[0], ldm_, stream_);
+      GWB_CUDA(cudaStreamSynchronize(stream_));
+      GWB_CUDA(cudaFreeAsync(stage, stream_));
+    } else {
+      launch_product_coupling64(mu64_, nu64_, n_, m_, ldm_, W64_[0], stream_);
+    }
+    launch_iterate_copies(W64_[0], n_, m_, ldm_, needs_copy() ? W_[0] : nullptr,
+                          no_planes() ? nullptr : W_aux_[0], aux_mode(), aux_scale(), stream_);
+    parity_ = 0;
+    GWB_CUDA(cudaGetLastError());
+    return;
+  }
+  float* dst = P_;
   if (w0_host) {
     double* stage = nullptr;
     GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&stage), sizeof(double) * n_ * m_, stream_));
@@ -525,7 +550,7 @@ void BapgEngine::reset(const double* w0_host) {
   } else {
     launch_product_coupling(mu32_, nu32_, n_, m_, ldm_, dst, stream_);
   }
-  if (quadratic()) launch_quad_reset(dev_view(0), P_, W_[0], stream_);
+  launch_quad_reset(dev_view(0), P_, W_[0], stream_);
   launch_tf32_aux(W_[0], n_, m_, ldm_, W_aux_[0], aux_mode(), stream_, aux_scale());
   parity_ = 0;
   GWB_CUDA(cudaGetLastError());
@@ -687,8 +712,7 @@ double BapgEngine::residual_of_average(double dykstra_tol) {
   double* w64 = dalloc<double>(stream_, len);
   double* work = dalloc<double>(stream_, static_cast<size_t>(std::max(n_, m_)));
   // The reference's fp64 halves: K8 fix-up, then ½(π + w) (solvers.cpp:193).
-  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
-  launch_rowmajor32_to_colmajor64(W_[parity_], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  iterates_to_colmajor64(parity_, pi64, w64, work);
   launch_average64(pi64, w64, pi64, static_cast<int64_t>(len), stream_);
   auto release = [&] {
     for (void* p : std::initializer_list<void*>{pi64, w64, work}) dfree(p, stream_);
@@ -713,8 +737,7 @@ int64_t BapgEngine::final_csv(const std::function<void(const char*, int64_t)>& s
   double* pi64 = dalloc<double>(stream_, len);
   double* w64 = dalloc<double>(stream_, len);
   double* work = dalloc<double>(stream_, static_cast<size_t>(std::max(n_, m_)));
-  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
-  launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  iterates_to_colmajor64(par, pi64, w64, work);
   launch_average64(pi64, w64, pi64, static_cast<int64_t>(len), stream_);
   int64_t total = 0;
   try {
@@ -787,8 +810,7 @@ void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
   GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w64), len * sizeof(double), stream_));
   GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), sizeof(double) * std::max(n_, m_), stream_));
   // K8 fix-up: exact fp64 row (π) / column (w) re-projection.
-  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
-  launch_rowmajor32_to_colmajor64(W_[parity_], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  iterates_to_colmajor64(parity_, pi64, w64, work);
   if (out_pi) GWB_CUDA(cudaMemcpyAsync(out_pi, pi64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   if (out_w) GWB_CUDA(cudaMemcpyAsync(out_w, w64, len * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   if (out_final) {
@@ -799,6 +821,26 @@ void BapgEngine::outputs(double* out_final, double* out_pi, double* out_w) {
   cudaFreeAsync(pi64, stream_);
   cudaFreeAsync(w64, stream_);
   cudaFreeAsync(work, stream_);
+}
+
+void BapgEngine::iterates_to_colmajor64(int par, double* pi64, double* w64, double* work) {
+  // K8 fix-up: exact fp64 row (π) / column (w) re-projection at the
+  // boundary (a no-op up to rounding for the fp64 entropy iterates).
+  if (quadratic()) {
+    launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+    launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  } else {
+    launch_rowmajor64_to_colmajor64(P64_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
+    launch_rowmajor64_to_colmajor64(W64_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  }
+}
+
+float* BapgEngine::pi_dev() {
+  if (!quadratic()) {
+    launch_iterate_copies(P64_, n_, m_, ldm_, P_, nullptr, aux_mode(), aux_scale(), stream_);
+    GWB_CUDA(cudaStreamSynchronize(stream_));
+  }
+  return P_;
 }
 
 void BapgEngine::kernel_ms(int kind, double* avg_ms, int64_t* count) {
@@ -852,8 +894,7 @@ void BapgEngine::readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_h
   float* fin32 = dalloc<float>(stream_, static_cast<size_t>(n_) * ldm_);
   int32_t* assign = dalloc<int32_t>(stream_, n_);
   // K8 fix-up, then the final coupling ½(π + w) (solvers.cpp:214-216).
-  launch_rowmajor32_to_colmajor64(P_, n_, m_, ldm_, pi64, 0, mu64_, work, stream_);
-  launch_rowmajor32_to_colmajor64(W_[par], n_, m_, ldm_, w64, 1, nu64_, work, stream_);
+  iterates_to_colmajor64(par, pi64, w64, work);
   launch_average64(pi64, w64, fin64, static_cast<int64_t>(len), stream_);
   r->split_gap = std::sqrt(sum_sq_diff_dev(pi64, w64, static_cast<int64_t>(len), stream_));
   // marginal_infeasibility (diagnostics.cpp:9-19): ‖πᵀ1 − ν‖/m + ‖π1 − μ‖/n.

@@ -95,8 +95,8 @@ class BapgEngine {
   // `assign_host` if non-null) and its accuracy against `gt_host` (n_gt
   // entries; skipped if null).  Only the scalars / assignment leave the GPU.
   void readout(const int32_t* gt_host, int64_t n_gt, int32_t* assign_host, Readout* r);
-  // Device pointers (session API).
-  float* pi_dev() const { return P_; }
+  // Device pointers (session API): an fp32 copy of π refreshed on request.
+  float* pi_dev();
   int64_t ld() const { return ldm_; }
   int precision() const { return precision_; }
   // gwb_geometry: GWB_ENTROPY (KL projections) or GWB_QUADRATIC (Euclidean
@@ -118,6 +118,8 @@ class BapgEngine {
   int64_t enqueue_iteration(int parity, double rel_tol);
   int64_t enqueue_half(int parity, bool half_b, double rel_tol);
   void destroy_graphs();
+  // π and the w in W[par] as column-major fp64 with the K8 fix-up.
+  void iterates_to_colmajor64(int par, double* pi64, double* w64, double* work);
 
   int device_;
   int64_t n_, m_, ldn_, ldm_;
@@ -168,14 +170,21 @@ class BapgEngine {
   float* f16_g1_rs_ = nullptr;
   float* f16_g2_cs_ = nullptr;
   float aux_scale() const { return f16() ? std::ldexp(1.0f, f16_s1_) : 1.0f; }
+  // Entropy geometry: π, w are fp64 (P64_, W64_) like the reference's; P_,
+  // W_ hold fp32 copies where a chain reads raw iterates (needs_copy()),
+  // and the quadratic geometry's fp32 iterates.
+  double *P64_ = nullptr, *W64_[2] = {nullptr, nullptr};
   float *P_ = nullptr, *P_aux_ = nullptr, *W_[2] = {nullptr, nullptr},
         *W_aux_[2] = {nullptr, nullptr};
+  bool needs_copy() const {
+    return quadratic() || no_planes() || precision_ == GWB_PREC_3XTF32;
+  }
   float *Vt_ = nullptr, *Vt_aux_ = nullptr, *G_ = nullptr;
   float *mu32_ = nullptr, *nu32_ = nullptr;
   double *mu64_ = nullptr, *nu64_ = nullptr;
   RowPart* row_part_ = nullptr;
   ColWritePart* cw_part_ = nullptr;
-  float *col_pmax_ = nullptr, *col_psum_ = nullptr, *col_max_ = nullptr, *col_scale_ = nullptr;
+  double *col_pmax_ = nullptr, *col_psum_ = nullptr, *col_max_ = nullptr, *col_scale_ = nullptr;
   double *col_psump_ = nullptr, *col_dev_ = nullptr;
   DevStatus* st_ = nullptr;
   DevRecord* rec_ = nullptr;

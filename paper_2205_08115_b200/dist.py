@@ -59,6 +59,7 @@ _SIGS = {
     "gwb_shard_set_comm": (C.c_int32, [_P, _P, _P, _P, _P, _ST]),
     "gwb_shard_load_device": (C.c_int32, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, _ST]),
     "gwb_shard_set_iterate_bound": (C.c_int32, [_P, C.c_double, _ST]),
+    "gwb_shard_set_marginals64": (C.c_int32, [_P, _P, _P, _ST]),
     "gwb_shard_reset": (C.c_int32, [_P, _ST]),
     "gwb_shard_phase": (C.c_int32, [_P, C.c_int32, _ST]),
     "gwb_shard_stream": (C.c_int32, [_P, C.POINTER(_P), _ST]),
@@ -135,11 +136,13 @@ class GpuShard:
         self.max_iters = cfg.max_iters
         self.precision = cfg.precision
 
-    def load(self, dx_rows, dy, mu_rows, nu, x_max=None):
+    def load(self, dx_rows, dy, mu_rows, nu, x_max=None, mu64=None, nu64=None):
         """Device fp32 tensors: dx_rows (rows_valid × n, any leading dim),
         dy (m × m), mu_rows (rows_valid), nu (m).  f16x2 chains also need
         x_max = max(max μ, max ν) over ALL ranks (the iterate bound every
-        rank must agree on, gwb_shard_set_iterate_bound)."""
+        rank must agree on, gwb_shard_set_iterate_bound).  `mu64` (this
+        rank's rows) / `nu64` (all m): the exact host fp64 marginals the fp64
+        iterates are projected onto (default: the fp32 device values)."""
         st = abi.Status()
         if self.precision == abi.PREC_F16X2:
             if x_max is None:
@@ -151,6 +154,13 @@ class GpuShard:
                                        dy.data_ptr(), dy.stride(0), mu_rows.data_ptr(),
                                        nu.data_ptr(), C.byref(st))
         _check(st)
+        if mu64 is not None and nu64 is not None:
+            import numpy as np
+            self._mu64 = np.ascontiguousarray(mu64, dtype=np.float64)
+            self._nu64 = np.ascontiguousarray(nu64, dtype=np.float64)
+            self.lib.gwb_shard_set_marginals64(self.h, self._mu64.ctypes.data, self._nu64.ctypes.data,
+                                               C.byref(st))
+            _check(st)
 
     def reset(self):
         st = abi.Status()
@@ -629,7 +639,9 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
         dx_d, dy_d = t(rows), t(dy)
         mu_d = t(np.asarray(mu)[rb:rb + max(rv, 1)] if rv else np.zeros(1))
         shard.load(dx_d, dy_d, mu_d, t(nu),
-                   x_max=float(max(np.abs(np.asarray(mu)).max(), np.abs(np.asarray(nu)).max())))
+                   x_max=float(max(np.abs(np.asarray(mu)).max(), np.abs(np.asarray(nu)).max())),
+                   mu64=np.asarray(mu, dtype=np.float64)[rb:rb + max(rv, 1)] if rv else np.zeros(1),
+                   nu64=np.asarray(nu, dtype=np.float64))
         del dx_d, dy_d
         shard.reset()
         st = run_sharded([shard], TorchComm(dist, rank, world), cfg.max_iters, poll_every,
@@ -735,7 +747,7 @@ def needs_agreement(cfg: abi.Config) -> bool:
 
 
 def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, device=0,
-                      stream=None) -> List[GpuShard]:
+                      stream=None, mu64=None, nu64=None) -> List[GpuShard]:
     """Build shard engines from full device tensors (tests / emulation)."""
     import torch
     n, m = dx.shape[0], dy.shape[0]
@@ -747,7 +759,8 @@ def shards_from_dense(cfg: abi.Config, dx, dy, mu, nu, world: int, ranks=None, d
         rb, rv = s.row_begin, s.rows_valid
         rows = dx[rb:rb + max(rv, 1)].contiguous()
         murows = mu[rb:rb + max(rv, 1)].contiguous()
-        s.load(rows, dy.contiguous(), murows, nu.contiguous(), x_max=x_max)
+        s.load(rows, dy.contiguous(), murows, nu.contiguous(), x_max=x_max,
+               mu64=None if mu64 is None else mu64[rb:rb + max(rv, 1)], nu64=nu64)
         shards.append(s)
     torch.cuda.synchronize()
     return shards

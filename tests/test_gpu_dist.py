@@ -21,7 +21,8 @@ def _run(inst, world, prec, iters, rel_tol=1e-30, overlap=False):
     t = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
     dx, dy, mu, nu = t(inst.dx), t(inst.dy), t(inst.mu), t(inst.nu)
     stream = torch.cuda.Stream()
-    shards = dist.shards_from_dense(cfg, dx, dy, mu, nu, world, stream=stream)
+    shards = dist.shards_from_dense(cfg, dx, dy, mu, nu, world, stream=stream,
+                                    mu64=np.asarray(inst.mu), nu64=np.asarray(inst.nu))
     for s in shards:
         s.reset()
     st = dist.run_sharded(shards, dist.EmuComm(), iters, poll_every=8, overlap=overlap)

@@ -78,7 +78,7 @@ def test_leaves_through_dropin(dl, port):
     pi /= pi.sum()
     err, v = DL.gw_objective(dl, dx, dy, pi)
     rc, want, _ = port.gw_objective(dx, dy, pi)
-    assert err is None and abs(v - want) <= 1e-7 * abs(want)
+    assert err is None and abs(v - want) <= 1e-5 * abs(want)  # 3xTF32 leaf, north-star bound
 
 
 def test_validation_order_double_fault(dl, port):
@@ -130,7 +130,7 @@ def test_observer_and_initial_through_dropin(dl, port, algorithm):
     assert list(r["observer_iters"]) == list(range(1, 8))
     mass = r["observer_mass"]
     want = 1.0 + (1e3 if algorithm == abi.BAPG else 0.0)  # Σπ (+ 1e3·Σw for BAPG)
-    np.testing.assert_allclose(mass, want, rtol=1e-9)
+    np.testing.assert_allclose(mass, want, rtol=1e-6)
     o = port.solve(c, inst.dx, inst.dy, inst.mu, inst.nu, initial=init)
     assert o.code == 0
     assert np.abs(r["final"] - o.final).max() <= 1e-4 * np.abs(o.final).max()

