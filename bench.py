@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", dest="n", type=int, default=20000)
-    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2", "f16x2"])
+    ap.add_argument("--precision", default="auto",
+                    choices=["auto", "tf32", "3xtf32", "bf16x3", "bf16x2", "f16x2", "f16x3"])
     ap.add_argument("--e2e-iters", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -333,11 +334,12 @@ def run_reference(args, world, rank):
 
 # ---------------------------------------------------------------------------
 PREC_NAMES = {"auto": 0, "tf32": 1, "3xtf32": 2, "bf16x3": 3, "bf16x2": 4, "sparse": 5, "fp32": 6,
-              "f16x2": 7}
-PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2"}
+              "f16x2": 7, "f16x3": 8}
+PREC_LABEL = {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2",
+              8: "f16x3"}
 # tensor passes per chain GEMM for 0/1 structure matrices, and the MMA kind
 PREC_PASSES = {1: (1, "tf32"), 2: (2, "tf32"), 3: (3, "bf16"), 4: (2, "bf16"), 5: (0, "none"),
-               6: (0, "fp32 FMA"), 7: (2, "f16")}
+               6: (0, "fp32 FMA"), 7: (2, "f16"), 8: (3, "f16")}
 
 
 def time_session(args, lib, abi, torch, dx, dy, mu, nu, n, local, prec, dist, clocks=None):

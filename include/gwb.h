@@ -46,7 +46,9 @@ enum gwb_axis { GWB_ROWS = 0, GWB_COLS = 1 };
  *     BAPG, eBPG / BPG / hBPG and row-sharded engines;
  *   - exact in bf16 only: BF16X3 (also the skinny m ≤ 32 chain and the
  *     batched n, m ≤ 128 kernel for 0/1 graphs);
- *   - otherwise: 3XTF32 (hi/lo splits of both operands).
+ *   - otherwise: F16X3 in the single-GPU BAPG engine (fp16 hi/lo planes of
+ *     both operands: kind::f16's accumulation carries far less truncation
+ *     bias than kind::tf32's), 3XTF32 in the other engines.
  * An explicit split-plane request (F16X2 / BF16X3 / BF16X2) on a D that is
  * not exact in that format falls back F16X2 -> BF16X3 -> 3XTF32, as AUTO
  * would; TF32 (1 pass) and BF16X2 are faster, reduced-precision opt-ins. */
@@ -58,8 +60,11 @@ enum gwb_precision {
   GWB_PREC_BF16X2 = 4,  /* exact-bf16 D × 2 bf16 planes (16-bit) */
   GWB_PREC_SPARSE = 5,  /* CSR row-gather chain, fp32 exact-order sums (sparse D) */
   GWB_PREC_FP32 = 6,    /* FP32-pipe chain for skinny problems (m ≤ 32); AUTO picks it */
-  GWB_PREC_F16X2 = 7    /* exact-fp16 D × 2 fp16 planes of the power-of-two-scaled
+  GWB_PREC_F16X2 = 7,   /* exact-fp16 D × 2 fp16 planes of the power-of-two-scaled
                            iterate (22-bit operands); AUTO picks it for 0/1 graphs */
+  GWB_PREC_F16X3 = 8    /* both operands as scaled fp16 hi + lo planes, 3 kind::f16
+                           passes (hi·hi + hi·lo + lo·hi, 22-bit operands); AUTO picks
+                           it for weighted D in the single-GPU BAPG engine */
 };
 
 /* Error codes; each maps to one reference exception class. */

@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "libgwb.so")
 BAPG, BPG, EBPG, HBPG, FW = 0, 1, 2, 3, 4
 ENTROPY, QUADRATIC = 0, 1
 ROWS, COLS = 0, 1
-PREC_AUTO, PREC_TF32, PREC_3XTF32, PREC_BF16X3, PREC_BF16X2, PREC_SPARSE, PREC_FP32, PREC_F16X2 = range(8)
+(PREC_AUTO, PREC_TF32, PREC_3XTF32, PREC_BF16X3, PREC_BF16X2, PREC_SPARSE, PREC_FP32, PREC_F16X2,
+ PREC_F16X3) = range(9)
 
 OK = 0
 ERR_CONFIG, ERR_DIMENSION, ERR_NUMERICAL, ERR_ZERO_SUM = 1, 2, 3, 4

@@ -186,14 +186,14 @@ class SolverConfig:
     log_domain: bool = False
     record_residual: bool = False
     # B200 extensions
-    precision: str = "auto"   # auto | tf32 | 3xtf32 | bf16x3 | bf16x2 | f16x2 | sparse | fp32
+    precision: str = "auto"   # auto | tf32 | 3xtf32 | bf16x3 | bf16x2 | f16x2 | f16x3 | sparse | fp32
     quiet: bool = False
 
     def to_abi(self) -> abi.Config:
         prec = {"auto": abi.PREC_AUTO, "tf32": abi.PREC_TF32, "3xtf32": abi.PREC_3XTF32,
                 "bf16x3": abi.PREC_BF16X3, "bf16x2": abi.PREC_BF16X2,
                 "sparse": abi.PREC_SPARSE, "fp32": abi.PREC_FP32,
-                "f16x2": abi.PREC_F16X2}
+                "f16x2": abi.PREC_F16X2, "f16x3": abi.PREC_F16X3}
         if self.algorithm not in abi.ALGORITHMS:
             raise ConfigError(f"unknown solver '{self.algorithm}' (expected bapg|bpg|ebpg|hbpg|fw)")
         if self.geometry not in ("entropy", "quadratic"):

@@ -166,7 +166,7 @@ void validate_config(const gwb_config* c) {
   if (c->perturbation < 0.0 || c->perturbation >= 1.0)
     fail(GWB_ERR_CONFIG, "perturbation must lie in [0, 1)");
   if (c->switch_iters < 0) fail(GWB_ERR_CONFIG, "switch-iters must be >= 0");
-  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_F16X2)
+  if (c->precision < GWB_PREC_AUTO || c->precision > GWB_PREC_F16X3)
     fail(GWB_ERR_CONFIG, "unknown precision");
 }
 
@@ -830,6 +830,22 @@ int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b, int64_t ldb,
       d.bf16_planes = f16 ? 2 : 3;
       d.a_bf16 = a16;
       for (int k = 0; k < d.bf16_planes; ++k)
+        d.b_bf16[k] = reinterpret_cast<uint16_t*>(bpl) + static_cast<int64_t>(k) * N * ldb;
+    }
+    if (precision == GWB_PREC_F16X3) {
+      // Both operands as scale-1 fp16 hi + lo planes (values inside fp16
+      // range), 3 passes.
+      GWB_CUDA(cudaMallocAsync(&a16, sizeof(uint16_t) * 2 * M * lda + 256, s));
+      GWB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bpl), 4 * N * ldb + 256, s));
+      gwb::launch_tf32_aux(a, M, K, lda, static_cast<float*>(a16), 5, s, 1.0f);
+      gwb::launch_tf32_aux(b, N, K, ldb, bpl, 5, s, 1.0f);
+      d.a = nullptr;
+      d.b = nullptr;
+      d.f16 = true;
+      d.bf16_planes = 2;
+      d.a_bf16 = a16;
+      d.a_bf16_lo = static_cast<uint16_t*>(a16) + M * lda;
+      for (int k = 0; k < 2; ++k)
         d.b_bf16[k] = reinterpret_cast<uint16_t*>(bpl) + static_cast<int64_t>(k) * N * ldb;
     }
     gwb::GemmPlan* p = gwb::gemm_plan_create(d);

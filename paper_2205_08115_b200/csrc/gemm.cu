@@ -119,6 +119,11 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(r);
 }
 
+// 3xTF32 low operand x − trunc_tf32(x), pre-rounded to TF32 so the MMA's
+// operand truncation reads it exactly (a truncated residual biases every
+// product low).
+__device__ __forceinline__ float tf32_lo(float x) { return rna_tf32(x - trunc_tf32(x)); }
+
 // The tensor core's fp32 accumulation truncates (measured: relative bias
 // ≈ −3.6e-8 per accumulated term, linear in K).  The MMA warp therefore
 // restarts accumulation every `chunk` k-blocks in one of two TMEM buffers
@@ -375,8 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
           if (clo)
             *reinterpret_cast<float4*>(clo + col0 + j) = make_float4(
-                acc[j] - trunc_tf32(acc[j]), acc[j + 1] - trunc_tf32(acc[j + 1]),
-                acc[j + 2] - trunc_tf32(acc[j + 2]), acc[j + 3] - trunc_tf32(acc[j + 3]));
+                tf32_lo(acc[j]), tf32_lo(acc[j + 1]), tf32_lo(acc[j + 2]), tf32_lo(acc[j + 3]));
         }
       } else {
 #pragma unroll
@@ -384,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (col0 + j < p.N) {
             if (p.accumulate) acc[j] = __fadd_rn(crow[col0 + j], acc[j]);
             crow[col0 + j] = acc[j];
-            if (clo) clo[col0 + j] = acc[j] - trunc_tf32(acc[j]);
+            if (clo) clo[col0 + j] = tf32_lo(acc[j]);
           }
         }
       }
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
         float v = x[q];
         if (p.accumulate) v = __fadd_rn(p.c[off + q], v);
         p.c[off + q] = v;
-        if (p.aux_mode == 2) p.c_aux[off + q] = v - trunc_tf32(v);
+        if (p.aux_mode == 2) p.c_aux[off + q] = tf32_lo(v);
       }
     }
   }
@@ -583,6 +587,18 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       g.b_sel[pl] = pl;
     }
     g.passes = d.bf16_planes;
+    if (d.a_bf16_lo) {
+      // f16x3: A and B both split in two planes; the lo·lo term is dropped.
+      if (d.bf16_planes != 2) throw std::runtime_error("gemm: split A needs two B planes");
+      g.a_map[1] = make_map(d.a_bf16_lo, d.M, d.K, d.lda, kBM, 2);
+      g.a_sel[0] = 1;  // lo·hi
+      g.b_sel[0] = 0;
+      g.a_sel[1] = 0;  // hi·lo
+      g.b_sel[1] = 1;
+      g.a_sel[2] = 0;  // hi·hi
+      g.b_sel[2] = 0;
+      g.passes = 3;
+    }
   } else {
   auto bmap = [&](const float* b) {
     return d.b_block_k > 0 ? make_map_blocked(b, d.N, d.b_block_k, d.K / d.b_block_k, kHalfN, 4,
@@ -625,7 +641,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // all-positive terms at K = 20000 (tools/acc_probe.py): mean −2.0e-7,
   // max 6.7e-7 relative at 4 k-blocks (f16x2), vs −4.5e-8 / 5.7e-7 at 1.
   static const bool unfused_env = std::getenv("GWB_GEMM_UNFUSED") != nullptr;
-  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env) {
+  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env && !d.a_bf16_lo) {
     g.fused = 1;
     if (d.promote_every > 0) g.chunk = 2 * d.promote_every;
     // A/B knob: k-blocks per promotion chunk in the fused schedule.

@@ -42,6 +42,8 @@ struct GemmDesc {
   // fp32 operand; C = Σ_p A·B_pᵀ.  Replaces a/b/*_lo when bf16_planes > 0.
   int bf16_planes = 0;               // 0 (TF32 path), 2 or 3
   const void* a_bf16 = nullptr;      // M×K bf16, leading dim lda
+  const void* a_bf16_lo = nullptr;   // optional second A plane (f16x3: A = hi + lo fp16
+                                     // planes; passes lo·hi + hi·lo + hi·hi, B has 2 planes)
   const void* b_bf16[3] = {nullptr, nullptr, nullptr};  // N×K planes, ldb
   // Output as bf16 split planes (for a following bf16-split GEMM) instead
   // of fp32 `c`: c_planes ∈ {0, 2, 3}; planes are M×N with leading dim ldc.

@@ -573,7 +573,7 @@ __global__ void to_f16_kernel(const float* x, int64_t rows, int64_t cols, int64_
 // 2^s1·Vᵀ (its B planes carry 2^s1), so its row scale is 2^(σ_i − s1);
 // GEMM2's column scale 2^−σ_j undoes σ.  All scales are powers of two.
 __global__ void f16_scales_kernel(const float* D, int64_t m, int64_t ld, float x_max, int s1,
-                                  float* g1_row_scale, float* g2_col_scale) {
+                                  int sa1, int sa2, float* g1_row_scale, float* g2_col_scale) {
   const int64_t i = blockIdx.x;
   double acc = 0.0;
   for (int64_t l = threadIdx.x; l < m; l += blockDim.x) acc += fabs(static_cast<double>(D[i * ld + l]));
@@ -588,8 +588,8 @@ __global__ void f16_scales_kernel(const float* D, int64_t m, int64_t ld, float x
     int sigma = 0;
     if (bound > 0.0) sigma = 14 - static_cast<int>(ceil(log2(bound)));
     sigma = max(-100, min(100, sigma));
-    g1_row_scale[i] = ldexpf(1.0f, sigma - s1);
-    g2_col_scale[i] = ldexpf(1.0f, -sigma);
+    g1_row_scale[i] = ldexpf(1.0f, sigma - s1 - sa1);
+    g2_col_scale[i] = ldexpf(1.0f, -sigma - sa2);
   }
 }
 
@@ -758,9 +758,10 @@ void launch_to_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, void*
 }
 
 void launch_f16_scales(const float* D, int64_t m, int64_t ld, float x_max, int s1,
-                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s) {
-  f16_scales_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(D, m, ld, x_max, s1, g1_row_scale,
-                                                             g2_col_scale);
+                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s, int sa1,
+                       int sa2) {
+  f16_scales_kernel<<<static_cast<unsigned>(m), 256, 0, s>>>(D, m, ld, x_max, s1, sa1, sa2,
+                                                             g1_row_scale, g2_col_scale);
 }
 
 void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,

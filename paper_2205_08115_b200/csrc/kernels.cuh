@@ -163,9 +163,12 @@ void launch_to_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, void*
                    cudaStream_t s);
 // f16x2 power-of-two scales (kernels.cu: f16_scales_kernel): per row i of
 // the m×m structure matrix D, σ_i = 14 − ⌈log2(x_max · Σ_l |D[i][l]|)⌉;
-// g1_row_scale[i] = 2^(σ_i − s1), g2_col_scale[i] = 2^−σ_i.
+// g1_row_scale[i] = 2^(σ_i − s1 − sa1), g2_col_scale[i] = 2^(−σ_i − sa2);
+// sa1 / sa2: power-of-two shifts of GEMM1's / GEMM2's A planes (f16x3: the
+// split structure matrices D_Y·2^sa1, D_X·2^sa2), 0 for exact D.
 void launch_f16_scales(const float* D, int64_t m, int64_t ld, float x_max, int s1,
-                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s);
+                       float* g1_row_scale, float* g2_col_scale, cudaStream_t s, int sa1 = 0,
+                       int sa2 = 0);
 // out (bf16, same ld) = bf16_rn(x).
 void launch_to_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, void* out,
                     cudaStream_t s);

@@ -756,8 +756,10 @@ int32_t gwb_shard_create(const gwb_config* cfg, int64_t n, int64_t m, int32_t ra
   return shard_guard(st, [&] {
     if (!cfg || n < 1 || m < 1 || world < 1 || rank < 0 || rank >= world)
       throw std::invalid_argument("gwb_shard_create: bad arguments");
-    if (cfg->precision == GWB_PREC_SPARSE || cfg->precision == GWB_PREC_FP32)
-      throw std::invalid_argument("gwb_shard_create: the sparse and fp32 chains are single-GPU only");
+    if (cfg->precision == GWB_PREC_SPARSE || cfg->precision == GWB_PREC_FP32 ||
+        cfg->precision == GWB_PREC_F16X3)
+      throw std::invalid_argument(
+          "gwb_shard_create: the sparse, fp32 and f16x3 chains are single-GPU only");
     if (cfg->geometry != GWB_ENTROPY)
       throw std::invalid_argument("gwb_shard_create: the quadratic geometry is single-GPU only");
     if (cfg->record_residual)  // Dykstra on a row shard would need per-sweep column exchanges

@@ -139,9 +139,14 @@ class BapgEngine {
   // Split-plane chains on kind::f16 (bf16 planes, or fp16 planes for f16x2).
   bool bf16() const {
     return precision_ == GWB_PREC_BF16X3 || precision_ == GWB_PREC_BF16X2 ||
-           precision_ == GWB_PREC_F16X2;
+           precision_ == GWB_PREC_F16X2 || precision_ == GWB_PREC_F16X3;
   }
-  bool f16() const { return precision_ == GWB_PREC_F16X2; }
+  // fp16 planes of the power-of-two-scaled iterate (f16x2, f16x3).
+  bool f16() const { return precision_ == GWB_PREC_F16X2 || precision_ == GWB_PREC_F16X3; }
+  // f16x3: the structure matrices are split too (hi + lo fp16 planes of
+  // D·2^sd_), for weighted D.
+  bool split_d() const { return precision_ == GWB_PREC_F16X3; }
+  int sdx_ = 0, sdy_ = 0;
   bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
   bool fp32() const { return precision_ == GWB_PREC_FP32; }
   // Skinny bf16x3 chain (m ≤ 32, exact-bf16 D_X): FP32-pipe GEMM1 writing
@@ -158,6 +163,7 @@ class BapgEngine {
            : precision_ == GWB_PREC_BF16X3 ? 3
            : precision_ == GWB_PREC_BF16X2 ? 4
            : precision_ == GWB_PREC_F16X2  ? 5
+           : precision_ == GWB_PREC_F16X3  ? 5
                                            : 2;
   }
   // f16x2 scaling: every iterate entry is ≤ x_max_ =

@@ -64,10 +64,10 @@ def test_bapg_er_small(gpu, port, precision):
         assert abs(r.split_gap - q["split_gap"]) <= 1e-3 * q["split_gap"] + 1e-9
 
 
-@pytest.mark.parametrize("precision", ["3xtf32", "bf16x3", "f16x2"])
+@pytest.mark.parametrize("precision", ["auto", "3xtf32", "bf16x3", "f16x2", "f16x3"])
 def test_bapg_gmm_small(gpu, port, precision):
     # Euclidean distances are not exact in bf16 / fp16: bf16x3 and f16x2 must
-    # fall back to 3xTF32.
+    # fall back to 3xTF32; AUTO and f16x3 split both operands.
     inst = I.config2(seed=1, n=320, m=256)
     rep, o = run_both(port, inst, precision, max_iters=40)
     assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
@@ -205,11 +205,12 @@ def _session_precision(inst, precision):
 
 
 def test_f16x2_is_auto_for_graphs(gpu):
-    # 0/1 graphs resolve AUTO to f16x2; Euclidean D (not fp16-exact) to 3xTF32;
-    # an explicit f16x2 request on such D falls back to 3xTF32 as well.
+    # 0/1 graphs resolve AUTO to f16x2; Euclidean D (not fp16-exact) to f16x3
+    # (both operands split); an explicit f16x2 request on such D falls back
+    # f16x2 -> bf16x3 -> 3xTF32.
     assert _session_precision(I.config1(seed=3, n=256), "auto") == abi.PREC_F16X2
     gmm = I.config2(seed=1, n=320, m=256)
-    assert _session_precision(gmm, "auto") == abi.PREC_3XTF32
+    assert _session_precision(gmm, "auto") == abi.PREC_F16X3
     assert _session_precision(gmm, "f16x2") == abi.PREC_3XTF32
 
 

@@ -43,7 +43,7 @@ def test_gemm_tf32_exact_operands(gpu, M, N, K):
     np.testing.assert_array_equal(c, a.astype(np.float64) @ b.astype(np.float64).T)
 
 
-@pytest.mark.parametrize("precision,tol", [(1, 2e-3), (2, 2e-6)])
+@pytest.mark.parametrize("precision,tol", [(1, 2e-3), (2, 2e-6), (8, 1e-6)])
 def test_gemm_precision(gpu, precision, tol):
     import torch
     rng = np.random.default_rng(1)
@@ -70,3 +70,23 @@ def test_split_gemm_long_k_accumulation(gpu, precision):
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     err = (c - ref) / ref
     assert np.abs(err).max() < 2e-6, (np.abs(err).max(), err.mean())
+
+
+@pytest.mark.parametrize("precision", [2, 8])  # 3xTF32, f16x3 (weighted operands)
+def test_weighted_gemm_bias(gpu, precision):
+    """Both operands weighted (c2's Euclidean distances): the mean relative
+    error measures the chain's accumulation bias, the max its noise.  kind::f16
+    (f16x3) must be at least 5x less biased than kind::tf32 (3xTF32)."""
+    import torch
+    rng = np.random.default_rng(9)
+    M, N, K = 512, 512, 2048
+    a = rng.uniform(0.0, 1.0, (M, K)).astype(np.float32)
+    b = rng.uniform(0.0, 1.0, (N, K)).astype(np.float32)
+    c = _gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), precision)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    err = (c - ref) / ref
+    print(f"precision {precision}: mean rel err {err.mean():.2e}, max {np.abs(err).max():.2e}")
+    if precision == 8:
+        assert abs(err.mean()) < 1e-7 and np.abs(err).max() < 1e-6
+    else:
+        assert np.abs(err).max() < 5e-6
