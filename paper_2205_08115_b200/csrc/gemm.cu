@@ -92,7 +92,8 @@ struct __align__(64) GemmParams {
   int32_t b_block_k;  // > 0: B maps are 3-D [K/b_block_k][N][b_block_k]
   int32_t c_planes;
   int32_t c_f16;  // output planes are fp16 (else bf16)
-  int32_t fused;  // split planes share one stage: {A, B_0 … B_{passes−1}}
+  int32_t fused;  // split planes share one stage: {A_0 … A_{a_planes−1}, B_0 … B_{b_planes−1}}
+  int32_t a_planes, b_planes;  // fused stage contents (pass p reads A_{a_sel[p]}, B_{b_sel[p]})
   int32_t group_m;  // row tiles per rasterisation group (kGroupM; env GWB_GEMM_GROUP_M)
   uint16_t* c_pl[3];
   float* c;
@@ -188,7 +189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // Fused planes: the work item is a k-block carrying every plane pass.
   const int total = p.fused ? kblocks : p.passes * kblocks;
   const int chunk = p.chunk;
-  const uint32_t f_stage_bytes = kABytes + static_cast<uint32_t>(p.passes) * kBBytes;
+  const uint32_t f_a_bytes = static_cast<uint32_t>(p.a_planes) * kABytes;
+  const uint32_t f_stage_bytes = f_a_bytes + static_cast<uint32_t>(p.b_planes) * kBBytes;
   const int f_stages = static_cast<int>((kStages * kStageBytes) / f_stage_bytes);
   const int nchunks = (total + chunk - 1) / chunk;
   const int a_row = tm * kPairM + static_cast<int>(rank) * kBM;
@@ -207,9 +209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fbar = ptx::mapa(&full[s], 0);
           uint8_t* st = smem + s * f_stage_bytes;
           if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
-          ptx::tma_load_2d_2sm(st, &p.a_map[0], fbar, kb * kblk, a_row);
-          for (int pl = 0; pl < p.passes; ++pl) {
-            void* dst = st + kABytes + pl * kBBytes;
+          for (int pa = 0; pa < p.a_planes; ++pa)
+            ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, a_row);
+          for (int pl = 0; pl < p.b_planes; ++pl) {
+            void* dst = st + f_a_bytes + pl * kBBytes;
             if (p.b_block_k > 0) {
               const int kk = kb * kblk;
               ptx::tma_load_3d_2sm(dst, &p.b_map[pl], fbar, kk % p.b_block_k, b_row,
@@ -258,11 +261,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t ph = (it / f_stages) & 1;
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
-            const uint32_t a_base = ptx::smem_u32(smem + s * f_stage_bytes);
-            // Smallest plane first: the tensor core's truncating accumulation
-            // then acts on the hi-plane terms only (as in batched.cu).
+            const uint32_t st_base = ptx::smem_u32(smem + s * f_stage_bytes);
+            // Smallest pass first (the last pass index is the smallest
+            // product): the tensor core's truncating accumulation then acts
+            // on the hi-plane terms only (as in batched.cu).
             for (int pl = p.passes - 1; pl >= 0; --pl) {
-              const uint32_t b_base = a_base + kABytes + pl * kBBytes;
+              const uint32_t a_base = st_base + p.a_sel[pl] * kABytes;
+              const uint32_t b_base = st_base + f_a_bytes + p.b_sel[pl] * kBBytes;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
@@ -591,11 +596,11 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       // f16x3: A and B both split in two planes; the lo·lo term is dropped.
       if (d.bf16_planes != 2) throw std::runtime_error("gemm: split A needs two B planes");
       g.a_map[1] = make_map(d.a_bf16_lo, d.M, d.K, d.lda, kBM, 2);
-      g.a_sel[0] = 1;  // lo·hi
+      g.a_sel[0] = 0;  // hi·hi
       g.b_sel[0] = 0;
       g.a_sel[1] = 0;  // hi·lo
       g.b_sel[1] = 1;
-      g.a_sel[2] = 0;  // hi·hi
+      g.a_sel[2] = 1;  // lo·hi (smallest: issued first in the fused schedule)
       g.b_sel[2] = 0;
       g.passes = 3;
     }
@@ -641,8 +646,10 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // all-positive terms at K = 20000 (tools/acc_probe.py): mean −2.0e-7,
   // max 6.7e-7 relative at 4 k-blocks (f16x2), vs −4.5e-8 / 5.7e-7 at 1.
   static const bool unfused_env = std::getenv("GWB_GEMM_UNFUSED") != nullptr;
-  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env && !d.a_bf16_lo) {
+  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env) {
     g.fused = 1;
+    g.a_planes = d.a_bf16_lo ? 2 : 1;
+    g.b_planes = d.bf16_planes;
     if (d.promote_every > 0) g.chunk = 2 * d.promote_every;
     // A/B knob: k-blocks per promotion chunk in the fused schedule.
     static const int chunk_env = [] {

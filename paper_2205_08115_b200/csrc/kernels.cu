@@ -108,6 +108,26 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   }
 }
 
+// Diagnostics-only row pass on fp32 iterates (quadratic geometry's tail
+// record): ⟨G_i, W_i⟩ and (Σ_j W_ij − μ_i)².
+__global__ void __launch_bounds__(kRowThreads) row_diag32_kernel(BapgDev d) {
+  if (d.st->flags != 0) return;
+  const int64_t i = blockIdx.x;
+  double sums[2] = {0.0, 0.0};
+  for (int64_t j = threadIdx.x; j < d.m; j += kRowThreads) {
+    const double g = d.G[i * d.ld + j], w = d.W[i * d.ld + j];
+    sums[0] = __fma_rn(g, w, sums[0]);
+    sums[1] += w;
+  }
+  Lse64 dummy{-INFINITY, 0.0};
+  block_reduce64<kRowThreads, 2>(dummy, sums);
+  if (threadIdx.x == 0) {
+    d.row_part[i].gw = sums[0];
+    const double dev = sums[1] - d.mu64[i];
+    d.row_part[i].rowdev = dev * dev;
+  }
+}
+
 // Narrow rows (m ≤ kNarrowM, config 3): one warp per row, 8 rows per CTA,
 // lane l covering the 4-column groups at 4l + 128v — the row sits in
 // registers between the (max, Σ) pass and the write, no block barriers.
@@ -656,6 +676,10 @@ void launch_col_write_pass(const BapgDev& d, cudaStream_t s) {
 }  // namespace
 
 void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
+  if (!d.P64) {  // fp32 iterates (quadratic geometry): diagnostics only
+    if (!write && d.n >= 1) row_diag32_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+    return;
+  }
   if (d.n >= 1 && d.m <= kNarrowM)
     row_update_warps_kernel<<<static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows), kRowThreads,
                               0, s>>>(d, write ? 1 : 0, write ? 0 : 1);

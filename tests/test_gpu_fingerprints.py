@@ -25,17 +25,17 @@ import pytest
 import paper_2205_08115_b200 as gw
 from harness import cases as C
 from harness import instances as I
-from tests.parity import (OBJ_TOL, PI_TOL, QUANT, argmax_check, decided_threshold,
-                          dequantise)
+from tests.parity import OBJ_TOL, PI_TOL, QUANT, argmax_check, dequantise
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.join(os.path.dirname(__file__), "golden")
 
-# Minimum decided fraction per case (measured margins of the reference
-# coupling; c3 from the product start is an exact symmetric fixed point:
-# every row is a 20-way exact tie, checked through the tied-set rule).
-MIN_DECIDED = {"c1": 0.9, "c1_jit": 0.9, "c3": 0.0, "c3_jit": 0.9, "c2": 0.5,
-               "c4_ba4000": 0.5, "c4_ba4000_jit": 0.5, "c4_hbpg_ba4000": 0.5,
+# Minimum decided fraction per case.  c3 from the product start is an exact
+# symmetric fixed point of the reference (every row a 20-way exact tie,
+# checked through the tied-set rule); after 3 iterations at n = 20000 the
+# coupling has barely left the product start.
+MIN_DECIDED = {"c1": 0.9, "c1_jit": 0.9, "c3": 0.0, "c3_jit": 0.9, "c2": 0.9,
+               "c4_ba4000": 0.9, "c4_ba4000_jit": 0.9, "c4_hbpg_ba4000": 0.8,
                "c4_n20000_it3": 0.0}
 
 
@@ -92,9 +92,8 @@ def test_fingerprint_full_coupling(gpu, name):
     np.testing.assert_allclose(pi.sum(axis=1), z["rowsum"], rtol=0, atol=PI_TOL * np.abs(z["rowsum"]).max())
     np.testing.assert_allclose(pi.sum(axis=0), z["colsum"], rtol=0, atol=PI_TOL * np.abs(z["colsum"]).max())
     pick = gw.hard_assignment(pi)
-    thr = decided_threshold(err + QUANT)
-    argmax_check(pick, lambda r, c: ref[r, c], z["top_idx"], z["top_val"], scale, thr,
-                 MIN_DECIDED[name], name)
+    argmax_check(pick, pi, z["top_idx"], z["top_val"], MIN_DECIDED[name], name,
+                 ref_value_at=lambda r, c: ref[r, c], slack=QUANT * scale)
 
 
 def test_fingerprint_c4_n20000_first_iterations(gpu):
@@ -125,13 +124,7 @@ def test_fingerprint_c4_n20000_first_iterations(gpu):
     # Argmax after 3 iterations: most rows are still near-uniform; the
     # tied/near-tie rules apply to all of them, decided rows must match.
     pick = gw.hard_assignment(pi)
-    top_idx, top_val = z["top_idx"], z["top_val"]
-
-    def value_at(r, c):
-        return pi[r, c]  # only used for picks outside the stored top-4: bounded by err
-
-    thr = decided_threshold(max(err_rows, err_block))
-    argmax_check(pick, value_at, top_idx, top_val, scale, thr, MIN_DECIDED[name], name)
+    argmax_check(pick, pi, z["top_idx"], z["top_val"], MIN_DECIDED[name], name)
 
 
 def test_fingerprint_c5_batched(gpu):
@@ -163,12 +156,12 @@ def test_fingerprint_c5_batched(gpu):
             err = np.abs(pi - ref).max() / scale
             worst_pi = max(worst_pi, err)
             assert err + QUANT <= PI_TOL, (k, err)
-            info = argmax_check(gw.hard_assignment(pi), lambda r, c: ref[r, c], z["top_idx"][k],
-                                z["top_val"][k], scale, decided_threshold(err + QUANT), 0.0,
-                                f"c5[{k}]")
+            info = argmax_check(gw.hard_assignment(pi), pi, z["top_idx"][k], z["top_val"][k], 0.0,
+                                f"c5[{k}]", ref_value_at=lambda r, c: ref[r, c],
+                                slack=QUANT * scale)
             decided += info["decided"]
             rows += info["rows"]
     print(f"c5: {count} problems, worst objective rel err {worst_obj:.2e}, worst coupling err "
           f"{worst_pi:.2e}, decided rows {decided}/{rows}")
     assert worst_obj <= OBJ_TOL
-    assert decided >= 0.5 * rows
+    assert decided >= 0.9 * rows
