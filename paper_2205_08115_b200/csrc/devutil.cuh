@@ -13,13 +13,14 @@
 namespace gwb {
 namespace dev {
 
-// Stop rule rel_change ≤ rel_tol (solvers.cpp:208, :284, :354) evaluated on
-// fp32 iterates.  Near a fixed point the fp32 iterate stops moving (rel_change
-// exactly 0, or only underflowed entries still change, rel ~1e-40) while the
-// fp64 reference keeps moving at its own noise floor (~1e-16).  A tolerance
-// below that floor (the pinned-benchmark idiom rel_tol = 1e-30) therefore
-// never triggers in the reference and never triggers here; any tolerance at
-// or above it is compared directly.
+// Stop rule rel_change ≤ rel_tol (solvers.cpp:208, :284, :354) for the engines
+// whose iterate still passes through fp32 (quadratic BAPG, eBPG / BPG /
+// hBPG): their iterate stops moving once changes fall below fp32 resolution
+// (rel_change exactly 0) where the reference's fp64 iterate still moves, so a
+// tolerance below the fp64 noise floor is not compared against it.  The fp64
+// entropy BAPG engines and the batched kernel (fp64 ‖Δw‖²) apply the
+// reference's rule as is — pinned c5 problems do cross rel_tol = 1e-30
+// (iteration 149-350) in the reference.
 constexpr double kFp64Floor = 1e-15;
 __host__ __device__ __forceinline__ bool stop_rule(double rel, double rel_tol) {
   return rel_tol >= kFp64Floor && rel <= rel_tol;

@@ -646,7 +646,10 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // all-positive terms at K = 20000 (tools/acc_probe.py): mean −2.0e-7,
   // max 6.7e-7 relative at 4 k-blocks (f16x2), vs −4.5e-8 / 5.7e-7 at 1.
   static const bool unfused_env = std::getenv("GWB_GEMM_UNFUSED") != nullptr;
-  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env) {
+  // Split A (f16x3) keeps separate pass stages: its fused 3-pass chunks
+  // accumulate 48 MMAs per promotion and measured a 3× larger truncation
+  // bias (−1.5e-6 vs −4.6e-7 relative at K = 2048, tests/test_gpu_gemm.py).
+  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env && !d.a_bf16_lo) {
     g.fused = 1;
     g.a_planes = d.a_bf16_lo ? 2 : 1;
     g.b_planes = d.bf16_planes;
