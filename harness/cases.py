@@ -62,5 +62,8 @@ CASES = {
     "c4_ba4000": (lambda: c4(4000), {}, True),
     "c4_ba4000_jit": (lambda: c4(4000, True), {}, True),
     "c4_hbpg_ba4000": (lambda: c4(4000, algorithm="hbpg"), {}, True),
+    # hBPG switched by budget before the reference's eBPG phase reaches its
+    # exact fp64 fixed point (iteration 9 at n = 4000).
+    "c4_hbpg_ba4000_sw8": (lambda: c4(4000, algorithm="hbpg"), {"switch_iters": 8}, True),
     "c4_n20000_it3": (lambda: c4(20000), {"max_iters": 3}, False),
 }

@@ -145,9 +145,12 @@ def test_fingerprint_c5_batched(gpu):
     obj_ref = z["objective"]
     worst_obj, worst_pi, decided, rows = 0.0, 0.0, 0, 0
     for k, rep in enumerate(reps):
-        assert rep.iterations_used == int(z["iterations"][k])
+        # The reference stops where rel_change crosses the pinned 1e-30
+        # (iterations 149-350 for most problems); so must the device.
+        assert rep.iterations_used == int(z["iterations"][k]), (k, rep.iterations_used)
         obj = np.array([r.objective for r in rep.trace])
-        worst_obj = max(worst_obj, np.abs(obj - obj_ref[k]).max() / np.abs(obj_ref[k]).max())
+        want = obj_ref[k][: len(obj)]
+        worst_obj = max(worst_obj, np.abs(obj - want).max() / np.abs(want).max())
         pi = rep.final_coupling.entries()
         np.testing.assert_allclose(pi.sum(axis=1), z["rowsum"][k], rtol=0, atol=1e-4 / 128)
         if k < z["q"].shape[0]:
