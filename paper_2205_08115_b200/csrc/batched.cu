@@ -807,19 +807,20 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
                          const double* dy, int64_t m, const double* mu, const double* nu,
                          double* out_final, double* out_pi, double* out_w, gwb_record* trace,
                          int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                         int32_t* iterations_used, bool name_problem) {
+                         int32_t* iterations_used, bool name_problem, int device,
+                         int64_t index_base, double* kernel_ms) {
   if (!dx || !dy || !mu || !nu || !out_final) api_fail(GWB_ERR_INVALID, "null input/output buffer");
   if (trace && trace_cap < cfg->max_iters) api_fail(GWB_ERR_CAPACITY, "trace capacity < max_iters");
-  const int device = api_device();
+  if (device < 0) device = api_device();
   GWB_CUDA(cudaSetDevice(device));
   const BatchedOut o{out_final, out_pi, out_w, trace, trace_cap, n_records, converged, iterations_used};
   const bool onchip_prec = cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_BF16X3;
-  g_last_ms = 0.0;
-  g_last_problems = 0;
+  double ms_total = 0.0;
+  if (kernel_ms) *kernel_ms = 0.0;
   // The on-chip kernel implements the entropy geometry; the quadratic one
   // runs problem by problem on the generic engine.
   if (n > kT || m > kT || !onchip_prec || cfg->geometry != GWB_ENTROPY || cfg->record_residual) {
-    const Failure f = batched_generic(cfg, device, batch, dx, n, dy, m, mu, nu, o, 0);
+    const Failure f = batched_generic(cfg, device, batch, dx, n, dy, m, mu, nu, o, index_base);
     if (f.problem >= 0) raise_failure(f, name_problem);
     return;
   }
@@ -921,8 +922,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
     GWB_CUDA(cudaStreamSynchronize(s));
     float kms = 0.f;
     GWB_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
-    g_last_ms += kms;
-    g_last_problems += cb;
+    ms_total += kms;
     for (int64_t k = 0; k < cb; ++k) {
       const BatchStatus& st = hst[k];
       const int64_t b = b0 + k;
@@ -940,7 +940,16 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
       if (iterations_used) iterations_used[b] = st.used;
     }
   }
-  if (first.problem >= 0) raise_failure(first, name_problem);
+  if (kernel_ms) *kernel_ms = ms_total;
+  if (first.problem >= 0) {
+    first.problem += index_base;
+    raise_failure(first, name_problem);
+  }
+}
+
+void set_batched_last(double ms, int64_t problems) {
+  g_last_ms = ms;
+  g_last_problems = problems;
 }
 
 }  // namespace gwb

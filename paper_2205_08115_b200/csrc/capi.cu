@@ -17,6 +17,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -142,6 +143,27 @@ int primary_device() {
   return g_devices[0];
 }
 
+// All selected devices (gwb_set_devices / GWB_DEVICES), validated: present and
+// sm_100.  A device listed twice runs two ranks / slices on it (the sharded
+// solve then emulates its collectives: a one-GPU test mode, shard.cu).
+std::vector<int> solve_devices() {
+  primary_device();
+  std::vector<int> devs;
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    devs = g_devices;
+  }
+  int count = 0;
+  cudaGetDeviceCount(&count);
+  for (size_t k = 0; k < devs.size(); ++k) {
+    if (devs[k] < 0 || devs[k] >= count) fail(GWB_ERR_RUNTIME, fmt("device %d not present", devs[k]));
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, devs[k]);
+    if (major != 10) fail(GWB_ERR_RUNTIME, fmt("device %d is not sm_100", devs[k]));
+  }
+  return devs;
+}
+
 const char* algo_name(int32_t a) {
   switch (a) {
     case GWB_BAPG: return "bapg";
@@ -198,6 +220,29 @@ void raise_device_flags(const gwb::DevStatus& s, const char* solver) {
   numerical(solver, it, "non-finite iterate");
 }
 
+// BAPG trace records (IterationRecord, phase 0) from the engine's records.
+void fill_trace(const SolveOut& o, const std::vector<gwb::HostRecord>& recs, int used,
+                const std::vector<double>& residuals) {
+  if (o.trace) {
+    for (int k = 0; k < used; ++k) {
+      gwb_record& r = o.trace[k];
+      std::memset(&r, 0, sizeof(r));
+      r.iter = k + 1;
+      r.objective = recs[k].objective;
+      r.marginal_infeasibility = recs[k].marginal_infeasibility;
+      r.split_gap = recs[k].split_gap;
+      r.rel_change = recs[k].rel_change;
+      r.elapsed_seconds = recs[k].elapsed;
+      r.phase = 0;
+      if (k < static_cast<int>(residuals.size())) {
+        r.residual = residuals[k];
+        r.has_residual = 1;
+      }
+    }
+  }
+  if (o.n_records) *o.n_records = o.trace ? used : 0;
+}
+
 // bapg_solve (solvers.cpp:138-217) on the device engine.
 void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, int64_t m,
           const double* mu, const double* nu, const double* initial, gwb_observer observer,
@@ -239,7 +284,24 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
                              /*name_problem=*/false);
     return;
   }
-  const int device = primary_device();
+  // Several devices selected (gwb_set_devices / GWB_DEVICES): one problem
+  // row-sharded across them in this process (shard.cu, NCCL over NVLink).
+  // The observer / residual slow path, a caller's initial coupling and graph
+  // inputs stay on the primary device.
+  const std::vector<int> devs = solve_devices();
+  if (devs.size() > 1 && !observer && !cfg->record_residual && !initial && !graphs && entropy) {
+    std::vector<gwb::HostRecord> recs;
+    int prec = 0;
+    const gwb::DevStatus s = gwb::bapg_multi_device(*cfg, devs, dx, n, dy, m, mu, nu, o.out_final,
+                                                    o.out_pi, o.out_w, &recs, &prec);
+    raise_device_flags(s, "bapg");
+    const int used = s.iter - 1;
+    fill_trace(o, recs, used, {});
+    if (o.converged) *o.converged = s.converged;
+    if (o.iterations_used) *o.iterations_used = used;
+    return;
+  }
+  const int device = devs[0];
   BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
   eng.set_geometry(cfg->geometry);
   if (graphs)
@@ -270,25 +332,7 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
   }
   const int used = s.iter - 1;
   eng.tail();
-  const std::vector<gwb::HostRecord> recs = eng.records(used);
-  if (o.trace) {
-    for (int k = 0; k < used; ++k) {
-      gwb_record& r = o.trace[k];
-      std::memset(&r, 0, sizeof(r));
-      r.iter = k + 1;
-      r.objective = recs[k].objective;
-      r.marginal_infeasibility = recs[k].marginal_infeasibility;
-      r.split_gap = recs[k].split_gap;
-      r.rel_change = recs[k].rel_change;
-      r.elapsed_seconds = recs[k].elapsed;
-      r.phase = 0;
-      if (k < static_cast<int>(residuals.size())) {
-        r.residual = residuals[k];
-        r.has_residual = 1;
-      }
-    }
-  }
-  if (o.n_records) *o.n_records = o.trace ? used : 0;
+  fill_trace(o, eng.records(used), used, residuals);
   if (o.converged) *o.converged = s.converged;
   if (o.iterations_used) *o.iterations_used = used;
   eng.outputs(o.out_final, o.out_pi, o.out_w);
@@ -568,8 +612,42 @@ int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch, const doubl
     require_algorithm(cfg, GWB_BAPG, "bapg_solve");
     validate_config(cfg);
     if (batch < 1 || n < 1 || m < 1) fail(GWB_ERR_DIMENSION, "empty batch or problem");
-    gwb::device_bapg_batched(cfg, batch, dx, n, dy, m, mu, nu, out_final, out_pi, out_w, trace,
-                             trace_cap, n_records, converged, iterations_used);
+    // Several devices: contiguous ranges of problems per GPU, no
+    // communication (one host thread per device); the lowest-index failing
+    // problem raises, as on one device.
+    const std::vector<int> devs = solve_devices();
+    const int P = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(devs.size()), batch));
+    std::vector<double> ms(P, 0.0);
+    std::vector<std::exception_ptr> errs(P);
+    auto slice = [&](int r) {
+      const int64_t b0 = batch * r / P, b1 = batch * (r + 1) / P;
+      const int64_t nn = n * n, mm = m * m, nm = n * m;
+      gwb::device_bapg_batched(cfg, b1 - b0, dx + b0 * nn, n, dy + b0 * mm, m, mu + b0 * n,
+                               nu + b0 * m, out_final + b0 * nm, out_pi ? out_pi + b0 * nm : nullptr,
+                               out_w ? out_w + b0 * nm : nullptr,
+                               trace ? trace + b0 * trace_cap : nullptr, trace_cap,
+                               n_records ? n_records + b0 : nullptr,
+                               converged ? converged + b0 : nullptr,
+                               iterations_used ? iterations_used + b0 : nullptr, true, devs[r], b0,
+                               &ms[r]);
+    };
+    if (P <= 1) {
+      slice(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int r = 0; r < P; ++r)
+        th.emplace_back([&, r] {
+          try {
+            slice(r);
+          } catch (...) {
+            errs[r] = std::current_exception();
+          }
+        });
+      for (auto& t : th) t.join();
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    }
+    gwb::set_batched_last(*std::max_element(ms.begin(), ms.end()), batch);
   });
 }
 

@@ -18,6 +18,8 @@
 // shard's stream; every kernel is a no-op once the solve is done, while the
 // collectives always run, so ranks never diverge in their collective calls.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -200,7 +202,8 @@ __global__ void shard_finalize_kernel(BapgDev d, const double* diag, const doubl
   // Local flags (if any) were all clean; keep the local done in sync.
   st->flags = 0;
   st->done = 0;
-  if (stop_rule(sqrt(diag[4]) / sqrt(diag[5]), rel_tol)) {
+  // fp64 iterates: the reference's rule as is (solvers.cpp:208).
+  if (sqrt(diag[4]) / sqrt(diag[5]) <= rel_tol) {
     st->converged = 1;
     st->done = st->gdone = 1;
   }
@@ -713,6 +716,308 @@ class ShardEngine {
   GemmPlan *g1_[2] = {nullptr, nullptr}, *g1t_[2] = {nullptr, nullptr}, *g1p_ = nullptr,
            *g2_ = nullptr, *g2t_ = nullptr;
 };
+
+
+// ---------------------------------------------------------------------------
+// In-library multi-device BAPG (one process, several GPUs): the row-sharded
+// engines above driven by the phase / collective schedule of
+// dist.iterate_sharded (all-gather form), with NCCL's single-process
+// communicator (ncclCommInitAll) over NVLink / NVSwitch.  NCCL is loaded at
+// run time (dlopen), so libgwb.so has no link dependency on it and a
+// single-device caller never touches it.
+namespace {
+
+struct NcclApi {
+  decltype(&ncclCommInitAll) comm_init_all = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+
+  static const NcclApi& get() {
+    static NcclApi api = [] {
+      NcclApi a;
+      void* h = nullptr;
+      for (const char* name : {"libnccl.so.2", "libnccl.so"})
+        if ((h = dlopen(name, RTLD_NOW | RTLD_LOCAL))) break;
+      if (!h) return a;
+      a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+      a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+      a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+      a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+      a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+      a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+      return a;
+    }();
+    if (!api.comm_init_all || !api.all_gather || !api.all_reduce || !api.group_start ||
+        !api.group_end || !api.comm_destroy)
+      throw CudaError("multi-device solve: libnccl.so.2 not found (GWB_DEVICES lists several GPUs)");
+    return api;
+  }
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess)
+      throw CudaError(std::string("NCCL ") + what + ": " + (error_string ? error_string(r) : "error"));
+  }
+};
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst,
+                                  int64_t count) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = static_cast<float>(src[k]);
+}
+
+// Device buffer freed on scope exit (current device set by the caller).
+struct DevBuf {
+  void* p = nullptr;
+  int dev = 0;
+  DevBuf() = default;
+  DevBuf(int device, size_t bytes) : dev(device) {
+    GWB_CUDA(cudaSetDevice(dev));
+    GWB_CUDA(cudaMalloc(&p, bytes + 256));
+    GWB_CUDA(cudaMemset(p, 0, bytes + 256));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), dev(o.dev) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      dev = o.dev;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) {
+      cudaSetDevice(dev);
+      cudaFree(p);
+      p = nullptr;
+    }
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+DevStatus bapg_multi_device(const gwb_config& cfg_in, const std::vector<int>& devices,
+                            const double* dx, int64_t n, const double* dy, int64_t m,
+                            const double* mu, const double* nu, double* out_final,
+                            double* out_pi, double* out_w, std::vector<HostRecord>* records,
+                            int* resolved_precision) {
+  const int P = static_cast<int>(devices.size());
+  gwb_config cfg = cfg_in;
+  const int64_t nr = round_up((n + P - 1) / P, 64);
+  // 1. Stage every rank's rows of D_X (a symmetric D's rows are its
+  //    contiguous columns in the column-major input), D_Y and the marginals
+  //    in fp32 on its device; agree on the chain precision from the
+  //    exactness of all ranks' rows (dist.resolve_precision's rules).
+  std::vector<DevBuf> rows(P), dys(P), mus(P), nus(P);
+  int bits = 0;
+  for (int r = 0; r < P; ++r) {
+    const int dev = devices[r];
+    const int64_t rb = static_cast<int64_t>(r) * nr;
+    const int64_t rv = std::max<int64_t>(0, std::min<int64_t>(nr, n - rb));
+    GWB_CUDA(cudaSetDevice(dev));
+    const int64_t big = std::max(std::max<int64_t>(rv, 1) * n, m * m);
+    DevBuf stage(dev, sizeof(double) * big);
+    rows[r] = DevBuf(dev, sizeof(float) * std::max<int64_t>(rv, 1) * n);
+    dys[r] = DevBuf(dev, sizeof(float) * m * m);
+    mus[r] = DevBuf(dev, sizeof(float) * std::max<int64_t>(rv, 1));
+    nus[r] = DevBuf(dev, sizeof(float) * m);
+    if (rv > 0) {
+      GWB_CUDA(cudaMemcpy(stage.p, dx + rb * n, sizeof(double) * rv * n, cudaMemcpyHostToDevice));
+      f64_to_f32_kernel<<<1184, 256>>>(stage.as<double>(), rows[r].as<float>(), rv * n);
+      GWB_CUDA(cudaMemcpy(stage.p, mu + rb, sizeof(double) * rv, cudaMemcpyHostToDevice));
+      f64_to_f32_kernel<<<1, 256>>>(stage.as<double>(), mus[r].as<float>(), rv);
+      bits |= analyze_inexact(rows[r].as<float>(), rv, n, n, nullptr);
+    }
+    GWB_CUDA(cudaMemcpy(stage.p, dy, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+    f64_to_f32_kernel<<<1184, 256>>>(stage.as<double>(), dys[r].as<float>(), m * m);
+    GWB_CUDA(cudaMemcpy(stage.p, nu, sizeof(double) * m, cudaMemcpyHostToDevice));
+    f64_to_f32_kernel<<<1, 256>>>(stage.as<double>(), nus[r].as<float>(), m);
+    if (r == 0) bits |= analyze_inexact(dys[r].as<float>(), m, m, m, nullptr);
+    GWB_CUDA(cudaDeviceSynchronize());
+  }
+  const bool f16 = (bits & 4) == 0, bf16 = (bits & 2) == 0;
+  int prec = cfg.precision;
+  if (prec == GWB_PREC_AUTO) prec = f16 ? GWB_PREC_F16X2 : bf16 ? GWB_PREC_BF16X3 : GWB_PREC_3XTF32;
+  if (prec == GWB_PREC_F16X2 && !f16) prec = GWB_PREC_BF16X3;
+  if ((prec == GWB_PREC_BF16X3 || prec == GWB_PREC_BF16X2) && !bf16) prec = GWB_PREC_3XTF32;
+  if (prec == GWB_PREC_F16X3) prec = GWB_PREC_3XTF32;  // the sharded engine's weighted-D chain
+  cfg.precision = prec;
+  if (resolved_precision) *resolved_precision = prec;
+  double x_max = 0.0;
+  for (int64_t i = 0; i < n; ++i) x_max = std::max(x_max, std::fabs(mu[i]));
+  for (int64_t j = 0; j < m; ++j) x_max = std::max(x_max, std::fabs(nu[j]));
+
+  // 2. Engines, exchange buffers, communicators.
+  std::vector<std::unique_ptr<ShardEngine>> eng;
+  std::vector<DevBuf> vt(P), stats(P), diag(P), err(P);
+  for (int r = 0; r < P; ++r) {
+    eng.emplace_back(new ShardEngine(cfg, n, m, r, P, devices[r], nullptr));
+    vt[r] = DevBuf(devices[r], static_cast<size_t>(eng[r]->vt_bytes()));
+    stats[r] = DevBuf(devices[r], static_cast<size_t>(eng[r]->stats_bytes()));
+    diag[r] = DevBuf(devices[r], sizeof(double) * kDiag);
+    err[r] = DevBuf(devices[r], sizeof(double) * kErr);
+    eng[r]->set_comm(vt[r].p, stats[r].p, diag[r].as<double>(), err[r].as<double>());
+    if (prec == GWB_PREC_F16X2) eng[r]->set_iterate_bound(x_max);
+    eng[r]->load(rows[r].as<float>(), n, dys[r].as<float>(), m, mus[r].as<float>(),
+                 nus[r].as<float>());
+    const int64_t rb = eng[r]->row_begin(), rv = eng[r]->rows_valid();
+    eng[r]->set_marginals64(rv > 0 ? mu + rb : mu, nu);
+    eng[r]->reset();
+  }
+  rows.clear();
+  dys.clear();
+  // A device listed twice (e.g. GWB_DEVICES=0,0 on a one-GPU box) runs the
+  // same schedule with emulated collectives: host-synchronised device copies
+  // in rank order and host reductions (dist.EmuComm's semantics) — a test
+  // mode for the orchestration; distinct devices use NCCL.
+  bool emulate = false;
+  for (int r = 0; r < P; ++r)
+    for (int q = 0; q < r; ++q) emulate = emulate || devices[q] == devices[r];
+  const NcclApi* nccl = emulate ? nullptr : &NcclApi::get();
+  std::vector<ncclComm_t> comms(emulate ? 0 : P);
+  if (!emulate) nccl->check(nccl->comm_init_all(comms.data(), P, devices.data()), "ncclCommInitAll");
+  struct CommGuard {
+    const NcclApi* api;
+    std::vector<ncclComm_t>& c;
+    ~CommGuard() {
+      for (auto x : c) api->comm_destroy(x);
+    }
+  } guard{nccl, comms};
+  auto sync_all = [&]() {
+    for (auto& e : eng) GWB_CUDA(cudaStreamSynchronize(e->stream()));
+  };
+
+  auto all_phase = [&](int ph) {
+    for (auto& e : eng) e->phase(ph);
+  };
+  auto gather = [&](std::vector<DevBuf>& buf, size_t chunk_bytes) {
+    if (emulate) {
+      sync_all();
+      for (int r = 0; r < P; ++r)
+        for (int q = 0; q < P; ++q)
+          if (q != r)
+            GWB_CUDA(cudaMemcpyPeer(buf[q].as<uint8_t>() + r * chunk_bytes, devices[q],
+                                    buf[r].as<uint8_t>() + r * chunk_bytes, devices[r], chunk_bytes));
+      return;
+    }
+    nccl->check(nccl->group_start(), "group start");
+    for (int r = 0; r < P; ++r) {
+      GWB_CUDA(cudaSetDevice(devices[r]));
+      uint8_t* base = buf[r].as<uint8_t>();
+      nccl->check(nccl->all_gather(base + r * chunk_bytes, base, chunk_bytes, ncclUint8, comms[r],
+                                 eng[r]->stream()),
+                 "all-gather");
+    }
+    nccl->check(nccl->group_end(), "group end");
+  };
+  auto reduce_diag = [&]() {
+    if (emulate) {
+      sync_all();
+      double dsum[kDiag] = {0}, emax[kErr];
+      for (int q = 0; q < kErr; ++q) emax[q] = -INFINITY;
+      for (int r = 0; r < P; ++r) {
+        double d[kDiag], e[kErr];
+        GWB_CUDA(cudaMemcpy(d, diag[r].p, sizeof(d), cudaMemcpyDeviceToHost));
+        GWB_CUDA(cudaMemcpy(e, err[r].p, sizeof(e), cudaMemcpyDeviceToHost));
+        for (int q = 0; q < kDiag; ++q) dsum[q] += d[q];
+        for (int q = 0; q < kErr; ++q) emax[q] = std::max(emax[q], e[q]);
+      }
+      for (int r = 0; r < P; ++r) {
+        GWB_CUDA(cudaMemcpy(diag[r].p, dsum, sizeof(dsum), cudaMemcpyHostToDevice));
+        GWB_CUDA(cudaMemcpy(err[r].p, emax, sizeof(emax), cudaMemcpyHostToDevice));
+      }
+      return;
+    }
+    nccl->check(nccl->group_start(), "group start");
+    for (int r = 0; r < P; ++r) {
+      GWB_CUDA(cudaSetDevice(devices[r]));
+      nccl->check(nccl->all_reduce(diag[r].p, diag[r].p, kDiag, ncclFloat64, ncclSum, comms[r],
+                                 eng[r]->stream()),
+                 "all-reduce");
+      nccl->check(nccl->all_reduce(err[r].p, err[r].p, kErr, ncclFloat64, ncclMax, comms[r],
+                                 eng[r]->stream()),
+                 "all-reduce");
+    }
+    nccl->check(nccl->group_end(), "group end");
+  };
+  const size_t vt_chunk = static_cast<size_t>(eng[0]->vt_bytes() / P);
+  const size_t stats_chunk = static_cast<size_t>(eng[0]->stats_bytes() / P);
+
+  // 3. Iterations (dist.iterate_sharded, all-gather schedule), the agreed
+  //    done flag polled every 16 iterations, then the tail record.
+  for (int it = 1; it <= cfg.max_iters; ++it) {
+    all_phase(0);
+    gather(vt, vt_chunk);
+    all_phase(1);
+    all_phase(2);
+    gather(vt, vt_chunk);
+    all_phase(3);
+    gather(stats, stats_chunk);
+    all_phase(4);
+    reduce_diag();
+    all_phase(5);
+    if (it % 16 == 0 || it == cfg.max_iters) {
+      if (eng[0]->status().done) break;
+    }
+  }
+  DevStatus st = eng[0]->status();
+  if (!st.flags) {
+    all_phase(6);
+    gather(vt, vt_chunk);
+    all_phase(7);
+    reduce_diag();
+    all_phase(8);
+  }
+  for (auto& e : eng) e->sync_parity();
+  st = eng[0]->status();
+  if (st.flags) return st;
+
+  // 4. Outputs: rows of π, w (fp64) into the column-major host layout.
+  const int used = st.iter - 1;
+  if (records) {
+    const std::vector<DevRecord> r = eng[0]->records(used);
+    records->assign(static_cast<size_t>(used), HostRecord{});
+    for (int k = 1; k <= used; ++k) {
+      const DevRecord& d = r[k];
+      HostRecord& h = (*records)[k - 1];
+      h.objective = -0.25 * (d.mpi_pi + 2.0 * d.mpi_w + d.mw_w);
+      h.marginal_infeasibility = 0.5 * std::sqrt(d.col_sq) / static_cast<double>(m) +
+                                 0.5 * std::sqrt(d.row_sq) / static_cast<double>(n);
+      h.split_gap = std::sqrt(d.split_sq);
+      h.rel_change = std::sqrt(d.diff_sq) / std::sqrt(d.wold_sq);
+      h.elapsed = d.elapsed;
+    }
+  }
+  std::vector<double> pr, wr;
+  for (int r = 0; r < P; ++r) {
+    const int64_t rb = eng[r]->row_begin(), rv = eng[r]->rows_valid();
+    if (rv <= 0) continue;
+    pr.assign(static_cast<size_t>(rv * m), 0.0);
+    wr.assign(static_cast<size_t>(rv * m), 0.0);
+    eng[r]->rows(pr.data(), wr.data());
+    for (int64_t i = 0; i < rv; ++i)
+      for (int64_t j = 0; j < m; ++j) {
+        const double p = pr[i * m + j], w = wr[i * m + j];
+        const int64_t o = j * n + rb + i;
+        if (out_pi) out_pi[o] = p;
+        if (out_w) out_w[o] = w;
+        if (out_final) out_final[o] = 0.5 * (p + w);
+      }
+  }
+  return st;
+}
 
 }  // namespace gwb
 

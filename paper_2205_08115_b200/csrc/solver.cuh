@@ -219,6 +219,16 @@ class BapgEngine {
   BapgDev dev_view(int parity) const;
 };
 
+// Row-sharded BAPG over several devices of this process (shard.cu: the
+// sharded engines + NCCL single-process communicator); host fp64 in / out as
+// gwb_solve.  Returns the agreed status (flags decoded by the caller);
+// `records` receives the trace.
+DevStatus bapg_multi_device(const gwb_config& cfg, const std::vector<int>& devices,
+                            const double* dx, int64_t n, const double* dy, int64_t m,
+                            const double* mu, const double* nu, double* out_final,
+                            double* out_pi, double* out_w, std::vector<HostRecord>* records,
+                            int* resolved_precision);
+
 // Resolves GWB_PREC_AUTO (see gwb.h).
 int resolve_precision(int requested, bool bf16_exact, bool f16_exact, bool quadratic);
 

@@ -105,6 +105,9 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
                          const double* dy, int64_t m, const double* mu, const double* nu,
                          double* out_final, double* out_pi, double* out_w, gwb_record* trace,
                          int32_t trace_cap, int32_t* n_records, int32_t* converged,
-                         int32_t* iterations_used, bool name_problem = true);
+                         int32_t* iterations_used, bool name_problem = true, int device = -1,
+                         int64_t index_base = 0, double* kernel_ms = nullptr);
+// gwb_batched_last_kernel_ms's record (device time of the last batched call).
+void set_batched_last(double ms, int64_t problems);
 
 }  // namespace gwb

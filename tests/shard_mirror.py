@@ -195,7 +195,7 @@ class CpuShard:
         self.iter = k + 1
         self.W = self.W_new
         rel = np.sqrt(d[4]) / np.sqrt(d[5])
-        if self.rel_tol >= 1e-15 and rel <= self.rel_tol:  # devutil.cuh stop_rule
+        if rel <= self.rel_tol:  # the reference rule (fp64 shard iterates, shard.cu)
             self.conv = True
             self.done = self.gdone = True
 
