@@ -289,7 +289,12 @@ GWB_API int32_t gwb_bapg_solve_batched(const gwb_config* cfg, int64_t batch,
                                int32_t* iterations_used, gwb_status* st);
 
 /* Device selection side channel (the reference API has no device knob).
- * Also read from env GWB_DEVICES="0,1,..." on first use. */
+ * Also read from env GWB_DEVICES="0,1,..." on first use.  The first id runs
+ * single-device work.  With several ids, BAPG solves without observer /
+ * residual / initial coupling / graph inputs are row-sharded over all of them
+ * in this process (NCCL single-process communicator, loaded at run time;
+ * a device listed twice emulates the collectives — a one-GPU test mode), and
+ * gwb_bapg_solve_batched splits its problems across them. */
 GWB_API int32_t gwb_set_devices(int32_t count, const int32_t* ids, gwb_status* st);
 
 /* ---------------------------------------------------------------------------
