@@ -923,7 +923,6 @@ int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b, int64_t ldb,
       d.bf16_planes = 2;
       d.a_bf16 = a16;
       d.a_bf16_lo = static_cast<uint16_t*>(a16) + M * lda;
-      d.promote_every = 1;
       for (int k = 0; k < 2; ++k)
         d.b_bf16[k] = reinterpret_cast<uint16_t*>(bpl) + static_cast<int64_t>(k) * N * ldb;
     }

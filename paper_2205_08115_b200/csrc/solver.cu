@@ -379,8 +379,10 @@ void BapgEngine::build_plans() {
       d.bf16_planes = planes;
       d.a_bf16 = Dy_bf_;
       if (split_d()) {
+        // Separate pass stages, promotion every 2 k-blocks (DESIGN.md §4a:
+        // the measured-best c2 schedule; every 1 k-block halves the bias but
+        // drains TMEM every 4 MMAs).
         d.a_bf16_lo = reinterpret_cast<uint16_t*>(Dy_bf_) + m_ * ldm_;
-        d.promote_every = 1;  // shortest chunks: least truncation bias (weighted D)
       }
       d.lda = ldm_;
       for (int k = 0; k < planes; ++k) d.b_bf16[k] = planes_of(X_aux, n_ * ldm_, k);
@@ -403,7 +405,6 @@ void BapgEngine::build_plans() {
       d.a_bf16 = Dx_bf_;
       if (split_d()) {
         d.a_bf16_lo = reinterpret_cast<uint16_t*>(Dx_bf_) + n_ * ldn_;
-        d.promote_every = 1;
       }
       d.lda = ldn_;
       for (int k = 0; k < planes; ++k) d.b_bf16[k] = planes_of(Vt_aux_, m_ * ldn_, k);
