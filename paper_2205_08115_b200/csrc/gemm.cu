@@ -684,9 +684,16 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   const int tiles = g.tiles_m * g.tiles_n;
   const int kblocks = (g.K + (g.kind ? kBK16 : kBK) - 1) / (g.kind ? kBK16 : kBK);
   int splits = 1;
-  if (d.split_k >= 2) {
-    splits = d.split_k;
-  } else if (d.split_k == 0 && tiles < 74) {
+  // A/B knob (recorded by bench.py): GWB_GEMM_SPLITK=1 disables split-K,
+  // ≥ 2 forces that many splits.
+  static const int splitk_env = [] {
+    const char* e = std::getenv("GWB_GEMM_SPLITK");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int split_req = splitk_env > 0 ? splitk_env : d.split_k;
+  if (split_req >= 2) {
+    splits = split_req;
+  } else if (split_req == 0 && tiles < 74) {
     splits = std::max(1, std::min(74 / tiles, kblocks / 4));
   }
   splits = std::max(1, std::min(splits, kblocks));
