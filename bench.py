@@ -507,7 +507,10 @@ def run_ours(args, world, rank, local, dist):
             "data": "synthetic (seeded BA graphs, reference RNG)",
             "config": {"workload": WORKLOAD, "n": n, "m": n, "precision": label,
                        "l2": "no flush: each operand (1.6 GB) exceeds the 126 MB L2",
-                       "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+                       "parallelism": "single GPU" if world == 1 else f"{world} replicas",
+                       # A/B environment knobs that change GEMM schedules
+                       # (and accumulation numerics): none in a driver run.
+                       "env_knobs": {k: v for k, v in os.environ.items() if k.startswith("GWB_")}},
             "tflops": {"algorithmic_per_iteration": flops_it,
                        "achieved_whole_step": flops_it * value_rank / 1e12},
             "roofline": roofline, "variants": variants, "configs": configs,
@@ -729,8 +732,10 @@ def c5_variant(world, rank, local, dist, iters=500, total=4096):
     lib = abi.load()
     st = abi.Status()
     lib.gwb_set_devices(1, (C.c_int32 * 1)(local), C.byref(st))
-    share = total // world + (1 if rank < total % world else 0)
-    r = bench_c5.run(share, iters)
+    from paper_2205_08115_b200 import dist as D
+    b0, b1 = D.batch_range(total, rank, world)
+    share = b1 - b0
+    r = bench_c5.run(share, iters, start=b0)
     ms, wall, used = r["kernel_ms"], r["e2e_s"], r["mean_iterations_used"]
     if dist is not None:
         t = torch.tensor([ms, wall, used * share], device="cuda", dtype=torch.float64)

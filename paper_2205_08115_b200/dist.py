@@ -657,6 +657,16 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
         shard.close()
 
 
+def batch_range(total: int, rank: int, world: int):
+    """Contiguous problem range [b0, b1) of `rank` when `total` independent
+    problems (config 5) are partitioned over `world` ranks with no
+    communication — the same split gwb_bapg_solve_batched makes across the
+    devices of one process."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    return total * rank // world, total * (rank + 1) // world
+
+
 def raise_shard_flags(st: dict):
     """Reference error semantics from the agreed flags (solvers.cpp:164-189)."""
     f, it = st["flags"], st["err_iter"]

@@ -213,3 +213,55 @@ def test_resolve_precision_passthrough_for_tf32_chains():
         cfg = abi.default_config(precision=p)
         assert not D.needs_agreement(cfg)
         assert D.resolve_precision(cfg, False, False).precision == p
+
+
+def _c5_worker(rank, world, port, total, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2205_08115_b200 import dist as D
+    from oracle.bindings import Oracle
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b0, b1 = D.batch_range(total, rank, world)
+    o = Oracle("port")
+    objs = []
+    for k in range(b0, b1):
+        inst = I.config5_problem(k, n=24)
+        cfg = abi.default_config(rho=0.1, max_iters=15, rel_tol=1e-30, quiet=1)
+        r = o.solve(cfg, inst.dx, inst.dy, inst.mu, inst.nu)
+        objs.append(r.trace[-1]["objective"])
+    sizes = [None] * world
+    dist.all_gather_object(sizes, (b0, b1, objs))
+    q.put((rank, sizes))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 7), (3, 8)])
+def test_c5_partition_across_ranks(world, total):
+    """Config 5 across ranks (bench.py c5, no communication): the ranges tile
+    the batch exactly once and the gathered per-problem results equal the
+    single-process ones, in problem order."""
+    from oracle.bindings import Oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c5_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = sorted(out[0], key=lambda t: t[0])
+    assert parts[0][0] == 0 and parts[-1][1] == total
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    gathered = [v for _, _, objs in parts for v in objs]
+    o = Oracle("port")
+    want = []
+    for k in range(total):
+        inst = I.config5_problem(k, n=24)
+        r = o.solve(abi.default_config(rho=0.1, max_iters=15, rel_tol=1e-30, quiet=1),
+                    inst.dx, inst.dy, inst.mu, inst.nu)
+        want.append(r.trace[-1]["objective"])
+    assert gathered == want

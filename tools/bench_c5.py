@@ -20,10 +20,10 @@ from paper_2205_08115_b200 import abi
 from harness import instances as I
 
 
-def problems(batch, seed=0, n=128):
-    """`batch` distinct c5 members (ER(n, 0.1) vs its noised permuted copy,
-    per-problem seeds), ~0.5 ms each to generate."""
-    return [I.config5_problem(k, seed=seed, n=n) for k in range(batch)]
+def problems(batch, seed=0, n=128, start=0):
+    """`batch` distinct c5 members start, start+1, … (ER(n, 0.1) vs its noised
+    permuted copy, per-problem seeds), ~0.5 ms each to generate."""
+    return [I.config5_problem(k, seed=seed, n=n) for k in range(start, start + batch)]
 
 
 def _pinned(count):
@@ -31,12 +31,12 @@ def _pinned(count):
     return torch.empty(count, dtype=torch.float64, pin_memory=True).numpy()
 
 
-def run(batch=4096, iters=500, n=128, trace=False):
+def run(batch=4096, iters=500, n=128, trace=False, start=0):
     """One gwb_bapg_solve_batched call over `batch` problems: inputs staged in
     pinned host memory beforehand (fp64 column-major, as the C-ABI takes
     them); the timed call includes their H2D copy, the solve and the D2H of
     every final coupling."""
-    probs = problems(batch, n=n)
+    probs = problems(batch, n=n, start=start)
     cfg = gw.SolverConfig(algorithm="bapg", rho=0.1, max_iters=iters, rel_tol=1e-30,
                           quiet=True).to_abi()
     nn = n * n
