@@ -73,9 +73,11 @@ struct BRecord {
 
 struct BDev {
   int64_t n, m, ld;
-  float* G;             // chain output, overwritten by LKs
-  const float* P;       // π_k
-  float* P_new;
+  const float* G;       // chain output (fp32)
+  double* LK;           // row-shifted log-kernel LKs (fp64, n × ld)
+  const double* P;      // π_k (fp64)
+  double* P_new;
+  float* P32_new;       // fp32 copy of π_{k+1}: the 3xTF32 hi operand (nullable)
   float* P_aux_new;
   int aux_mode;         // GEMM operand copy of P_new: 2 = 3xTF32 residual, 3/4 = bf16
                         // planes, 5 = fp16 planes of P_new·aux_scale (f16x2)
@@ -86,7 +88,7 @@ struct BDev {
   double* f;
   double* f_new;
   double* g;
-  float* rowmax;
+  double* rowmax;
   double* row_err;
   double* col_err;
   double* col_pm;       // chunks × m  (max, fp64)
@@ -97,8 +99,8 @@ struct BDev {
   double* obj_part;     // n
   double* wpart;        // (colblocks·chunks) × 2
   int chunks, colblocks;
-  float eb_scale;       // 2/ε
-  float bp_scale;       // 2t
+  double eb_scale;      // 2/ε
+  double bp_scale;      // 2t
   int log_domain;
   double perturb, uniform_mass;
   int budget1, max_iters, has_phase2;
@@ -147,44 +149,56 @@ __device__ float block_max(float v) {
   return t;
 }
 
+__device__ double block_max_d(double v) {
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = -INFINITY;
+  for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t = fmax(t, sh[q]);
+  return t;
+}
+
 // (max, Σ e^{x−max}) in fp64 state with fp32 exponentials of small
 // arguments: the online LSE accumulator of the BAPG projections
 // (devutil.cuh), instantiated for fp64 with unit weights.
-using LseAcc = OnlineLse<double>;
-__device__ __forceinline__ void lse_add(LseAcc& a, double x) { dev::lse_add(a, x, 1.0); }
 
 // ---------------------------------------------------------------------------
 // form: one CTA per row.
 __global__ void __launch_bounds__(kThreads) form_kernel(BDev d, int tail) {
   if (tail ? d.st->flags != 0 : skip(d)) return;
   const int64_t i = blockIdx.x;
-  float* g = d.G + i * d.ld;
-  const float* p = d.P + i * d.ld;
+  const float* g = d.G + i * d.ld;
+  const double* p = d.P + i * d.ld;
+  double* lkrow = d.LK + i * d.ld;
   const bool ebpg = d.st->phase == 1;
-  const float sc = ebpg ? d.eb_scale : d.bp_scale;
+  const double sc = ebpg ? d.eb_scale : d.bp_scale;
   double obj = 0.0;
-  float rmax = -INFINITY, emax = 0.0f;
+  double rmax = -INFINITY;
+  float emax = 0.0f;
   for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
-    const float gv = g[j], pv = p[j];
-    obj += static_cast<double>(gv) * pv;
-    const float e = sc * gv;
-    emax = fmaxf(emax, e);
-    const float lk = ebpg ? e : e + logf(pv);
-    rmax = fmaxf(rmax, lk);
+    const double gv = g[j], pv = p[j];
+    obj = __fma_rn(gv, pv, obj);
+    const double e = sc * gv;
+    emax = fmaxf(emax, static_cast<float>(e));
+    const double lk = ebpg ? e : e + log(pv);
+    rmax = fmax(rmax, lk);
   }
   obj = block_sum(obj);
   if (threadIdx.x == 0) d.obj_part[i] = obj;
   if (tail) return;
-  rmax = block_max(rmax);
+  rmax = block_max_d(rmax);
   emax = block_max(emax);
   if (threadIdx.x == 0) {
     d.rowmax[i] = rmax;
     atomicMax(&d.st->gmax_bits, __float_as_int(emax));
   }
   for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
-    const float e = sc * g[j];
-    const float lk = ebpg ? e : e + logf(p[j]);
-    g[j] = lk - rmax;
+    const double e = sc * static_cast<double>(g[j]);
+    const double lk = ebpg ? e : e + log(p[j]);
+    lkrow[j] = lk - rmax;
   }
 }
 
@@ -193,9 +207,9 @@ __global__ void form_check_kernel(BDev d) {
   BState* st = d.st;
   if (skip(d)) return;
   const float gmax = __int_as_float(st->gmax_bits);
-  float rmin = INFINITY;
-  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) rmin = fminf(rmin, d.rowmax[i]);
-  rmin = -block_max(-rmin);
+  double rmin = INFINITY;
+  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) rmin = fmin(rmin, d.rowmax[i]);
+  rmin = -block_max_d(-rmin);
   for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) d.g[j] = 0.0;
   if (threadIdx.x == 0) {
     st->sink_done = 0;
@@ -213,29 +227,23 @@ __global__ void form_check_kernel(BDev d) {
   }
 }
 
-// Sinkhorn row update for sweep s: f_new = log μ − LSE_j(max(LKs, floor) + g).
+// Sinkhorn row update for sweep s: f_new = log μ − LSE_j(max(LKs, floor) + g),
+// fp64 terms and exponentials (the reference's arithmetic, projections.cpp:92-163).
 __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   if (skip_sink(d)) return;
   const int64_t i = blockIdx.x;
-  const float* lk = d.G + i * d.ld;
+  const double* lk = d.LK + i * d.ld;
   const double floor_i = clamp_floor(d, i);
-  LseAcc a{-INFINITY, 0.0};
-  // float4 of the row, double2 pairs of g (ld and the allocations are padded).
-  for (int64_t j = threadIdx.x * 4; j < d.m; j += kThreads * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(lk + j);
+  Lse64 a{-INFINITY, 0.0};
+  for (int64_t j = threadIdx.x * 2; j < d.m; j += kThreads * 2) {
+    const double2 v = *reinterpret_cast<const double2*>(lk + j);
     const double2 g01 = *reinterpret_cast<const double2*>(d.g + j);
-    const double2 g23 = *reinterpret_cast<const double2*>(d.g + j + 2);
-    const float vv[4] = {v.x, v.y, v.z, v.w};
-    const double gg[4] = {g01.x, g01.y, g23.x, g23.y};
-    double x[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      x[q] = j + q < d.m ? fmax(static_cast<double>(vv[q]), floor_i) + gg[q] : -INFINITY;
-    lse_add_block<4>(a, x);
+    lse64_add(a, fmax(v.x, floor_i) + g01.x, 1.0);
+    if (j + 1 < d.m) lse64_add(a, fmax(v.y, floor_i) + g01.y, 1.0);
   }
   // block merge (fixed order)
   __shared__ double smx[kThreads / 32], ss[kThreads / 32];
-  a = lse_warp_merge(a);
+  a = lse64_warp_merge(a);
   const int w = threadIdx.x / 32, l = threadIdx.x & 31;
   if (l == 0) {
     smx[w] = a.mx;
@@ -243,8 +251,8 @@ __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  LseAcc r{-INFINITY, 0.0};
-  for (int q = 0; q < kThreads / 32; ++q) r = lse_merge(r, LseAcc{smx[q], ss[q]});
+  Lse64 r{-INFINITY, 0.0};
+  for (int q = 0; q < kThreads / 32; ++q) r = lse64_merge(r, Lse64{smx[q], ss[q]});
   const double lse = r.mx + log(r.s);
   const double fn = log(d.mu64[i]) - lse;
   d.f_new[i] = fn;
@@ -308,19 +316,19 @@ __global__ void __launch_bounds__(kThreads) col_lse_partial_kernel(BDev d, int r
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
   const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
   const bool want_emax = first_sweep && d.st->phase == 1 && !d.log_domain;
-  LseAcc a[4] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}};
+  Lse64 a[4] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}};
   float emax[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   if (c0 < d.m) {
-    // Per-element updates here: a 4-row block version (lse_add_block) ran
-    // 1.08 ms vs 0.82 ms at c4 (register pressure of the 16 staged doubles).
     for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
-      const float4 v = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
+      const double* lk = d.LK + i * d.ld + c0;
+      const double2 v01 = *reinterpret_cast<const double2*>(lk);
+      const double2 v23 = *reinterpret_cast<const double2*>(lk + 2);
       const double fl = clamp_floor(d, i), fi = d.f[i];
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        lse_add(a[q], fmax(static_cast<double>(vv[q]), fl) + fi);
-        if (want_emax) emax[q] = fmaxf(emax[q], vv[q] + d.rowmax[i]);
+        lse64_add(a[q], fmax(vv[q], fl) + fi, 1.0);
+        if (want_emax) emax[q] = fmaxf(emax[q], static_cast<float>(vv[q] + d.rowmax[i]));
       }
     }
   }
@@ -338,10 +346,10 @@ __global__ void __launch_bounds__(kThreads) col_lse_partial_kernel(BDev d, int r
     const int c = threadIdx.x;
     const int64_t col = static_cast<int64_t>(blockIdx.x) * kColWidth + c;
     if (col < d.m) {
-      LseAcc r{-INFINITY, 0.0};
+      Lse64 r{-INFINITY, 0.0};
       float e = -INFINITY;
       for (int q = 0; q < kThreads / 32; ++q) {
-        r = lse_merge(r, LseAcc{s_mx[q][c], s_s[q][c]});
+        r = lse64_merge(r, Lse64{s_mx[q][c], s_s[q][c]});
         e = fmaxf(e, s_e[q][c]);
       }
       const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + col;
@@ -356,11 +364,11 @@ __global__ void col_lse_combine_kernel(BDev d, int first_sweep) {
   if (skip_sink(d)) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= d.m) return;
-  LseAcc r{-INFINITY, 0.0};
+  Lse64 r{-INFINITY, 0.0};
   float e = -INFINITY;
   for (int c = 0; c < d.chunks; ++c) {
     const int64_t o = static_cast<int64_t>(c) * d.m + j;
-    r = lse_merge(r, LseAcc{d.col_pm[o], d.col_ps[o]});
+    r = lse64_merge(r, Lse64{d.col_pm[o], d.col_ps[o]});
     e = fmaxf(e, d.col_pemax[o]);
   }
   const double lse = r.mx + log(r.s);
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
   const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
   // Remark-1 perturbation applies to BPG iterations only (solvers.cpp:263-267).
   const bool perturb = d.perturb > 0.0 && d.st->phase == 2;
-  const float keep = static_cast<float>(1.0 - d.perturb);
-  const float add = static_cast<float>(d.perturb * d.uniform_mass);
+  const double keep = 1.0 - d.perturb;
+  const double add = d.perturb * d.uniform_mass;
   double cs[4] = {0.0, 0.0, 0.0, 0.0};
   double diff = 0.0, old = 0.0;
   const bool ok = c0 < d.m;
@@ -412,32 +420,30 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
   for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
     double rs = 0.0;
     if (ok) {
-      const float4 v = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
-      const float4 pv = *reinterpret_cast<const float4*>(d.P + i * d.ld + c0);
+      const double* lk = d.LK + i * d.ld + c0;
+      const double* pp = d.P + i * d.ld + c0;
       const double fl = clamp_floor(d, i), fi = d.f[i];
-      const float vv[4] = {v.x, v.y, v.z, v.w};
-      const float po[4] = {pv.x, pv.y, pv.z, pv.w};
-      float o[4];
+      double o[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (c0 + q < d.m) {
-          const double x = fmax(static_cast<double>(vv[q]), fl) + fi + gj[q];
-          float val = static_cast<float>(exp(x));
+          const double x = fmax(lk[q], fl) + fi + gj[q];
+          double val = exp(x);
           if (perturb) val = keep * val + add;
           o[q] = val;
           cs[q] += val;
           rs += val;
-          const double df = static_cast<double>(val) - po[q];
+          const double df = val - pp[q];
           diff += df * df;
-          old += static_cast<double>(po[q]) * po[q];
+          old += pp[q] * pp[q];
         } else {
-          o[q] = 0.0f;
+          o[q] = 0.0;
         }
       }
-      *reinterpret_cast<float4*>(d.P_new + i * d.ld + c0) = make_float4(o[0], o[1], o[2], o[3]);
-      if (d.P_aux_new)
-        aux_store4(d.P_aux_new, d.aux_mode, d.plane, i * d.ld + c0, o[0], o[1], o[2], o[3],
-                   d.aux_scale);
+      double* pn = d.P_new + i * d.ld + c0;
+      *reinterpret_cast<double2*>(pn) = make_double2(o[0], o[1]);
+      *reinterpret_cast<double2*>(pn + 2) = make_double2(o[2], o[3]);
+      aux_store4_64(d.P_aux_new, d.P32_new, d.aux_mode, d.plane, i * d.ld + c0, o, d.aux_scale);
     }
     rs = warp_sum(rs);
     if (lane == 0) d.row_sum[static_cast<int64_t>(blockIdx.x) * d.n + i] = rs;
@@ -604,9 +610,11 @@ class BregmanEngine {
     Dx_lo_ = keep(dalloc<float>(dx_elems));
     Dy_lo_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
     for (int q = 0; q < 2; ++q) {
-      P_[q] = keep(dalloc<float>(nm));
+      P_[q] = keep(dalloc<float>(nm));            // fp32 hi operand (3xTF32)
       Pa_[q] = keep(dalloc<float>(nm * 3 / 2));  // fp32 residual or up to 3 bf16 planes
+      P64_[q] = keep(dalloc<double>(nm));         // the iterate π (fp64)
     }
+    LK_ = keep(dalloc<double>(nm));               // row-shifted log-kernel (fp64)
     Vt_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
     Vta_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
     G_ = sharded_ ? nullptr : keep(dalloc<float>(nm));  // sharded: caller-owned (set_comm)
@@ -615,7 +623,7 @@ class BregmanEngine {
     f_ = keep(dalloc<double>(n_));
     fn_ = keep(dalloc<double>(n_));
     g_ = keep(dalloc<double>(m_));
-    rowmax_ = keep(dalloc<float>(n_));
+    rowmax_ = keep(dalloc<double>(n_));
     row_err_ = keep(dalloc<double>(n_));
     col_err_ = keep(dalloc<double>(m_));
     colblocks_ = static_cast<int>((m_ + kColWidth - 1) / kColWidth);
@@ -703,15 +711,8 @@ class BregmanEngine {
     }
     GWB_CUDA(cudaMemcpyAsync(mu_, mu, sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
     GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
-    std::vector<float> mu32(n_), nu32(m_);
-    for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
-    for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
-    std::unique_ptr<void, DevFree> a(dalloc<float>(n_)), b(dalloc<float>(m_));
-    GWB_CUDA(cudaMemcpyAsync(a.get(), mu32.data(), 4 * n_, cudaMemcpyHostToDevice, s_));
-    GWB_CUDA(cudaMemcpyAsync(b.get(), nu32.data(), 4 * m_, cudaMemcpyHostToDevice, s_));
-    launch_product_coupling(static_cast<float*>(a.get()), static_cast<float*>(b.get()), n_, m_, ldm_,
-                            P_[0], s_);
-    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_, aux_scale());
+    launch_product_coupling64(mu_, nu_, n_, m_, ldm_, P64_[0], s_);
+    init_copies();
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_shard_plans();
     begin();
@@ -763,19 +764,11 @@ class BregmanEngine {
     GWB_CUDA(cudaMemcpyAsync(nu_, nu, sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
     if (initial) {
       GWB_CUDA(cudaMemcpyAsync(sp, initial, sizeof(double) * n_ * m_, cudaMemcpyHostToDevice, s_));
-      launch_colmajor64_to_rowmajor32(sp, n_, m_, P_[0], ldm_, s_);
+      launch_colmajor64_to_rowmajor64(sp, n_, m_, P64_[0], ldm_, s_);
     } else {
-      std::vector<float> mu32(n_), nu32(m_);
-      for (int64_t i = 0; i < n_; ++i) mu32[i] = static_cast<float>(mu[i]);
-      for (int64_t j = 0; j < m_; ++j) nu32[j] = static_cast<float>(nu[j]);
-      std::unique_ptr<void, DevFree> a(dalloc<float>(n_)), b(dalloc<float>(m_));
-      GWB_CUDA(cudaMemcpyAsync(a.get(), mu32.data(), 4 * n_, cudaMemcpyHostToDevice, s_));
-      GWB_CUDA(cudaMemcpyAsync(b.get(), nu32.data(), 4 * m_, cudaMemcpyHostToDevice, s_));
-      launch_product_coupling(static_cast<float*>(a.get()), static_cast<float*>(b.get()), n_, m_,
-                              ldm_, P_[0], s_);
-      GWB_CUDA(cudaStreamSynchronize(s_));
+      launch_product_coupling64(mu_, nu_, n_, m_, ldm_, P64_[0], s_);
     }
-    launch_tf32_aux(P_[0], rows_alloc_, m_, ldm_, Pa_[0], aux_mode_, s_, aux_scale());
+    init_copies();
     GWB_CUDA(cudaStreamSynchronize(s_));
     build_plans();
   }
@@ -840,9 +833,9 @@ class BregmanEngine {
       const BState h = iterate_rest(k);
       if (h.flags) break;
       // record_residual (solvers.cpp:278-280, 348-350), before the observer.
-      if (cfg_.record_residual && h.iter - 1 == k) residuals_.push_back(residual_of(P_[k & 1]));
+      if (cfg_.record_residual && h.iter - 1 == k) residuals_.push_back(residual_of(P64_[k & 1]));
       if (observer && h.iter - 1 == k) {
-        to_host(P_[k & 1], 1, host_pi);
+        to_host(P64_[k & 1], 1, host_pi);
         if (observer(user, k, host_pi->data(), nullptr, n_, m_) != 0)
           api_fail(GWB_ERR_RUNTIME, "observer requested abort");
       }
@@ -887,7 +880,7 @@ class BregmanEngine {
     std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_)),
         w(dalloc<double>(std::max(n_, m_))), t(dalloc<double>(m_));
     GWB_CUDA(cudaMemcpyAsync(t.get(), col_target.data(), sizeof(double) * m_, cudaMemcpyHostToDevice, s_));
-    launch_rowmajor32_to_colmajor64(P_[used & 1], n_, m_, ldm_, static_cast<double*>(o.get()), 1,
+    launch_rowmajor64_to_colmajor64(P64_[used & 1], n_, m_, ldm_, static_cast<double*>(o.get()), 1,
                                     static_cast<double*>(t.get()), static_cast<double*>(w.get()), s_);
     GWB_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * n_ * m_, cudaMemcpyDeviceToHost, s_));
     GWB_CUDA(cudaStreamSynchronize(s_));
@@ -900,18 +893,24 @@ class BregmanEngine {
     return p;
   }
 
-  // luo_tseng_residual (diagnostics.cpp:33-42) of the fp32 iterate P.
-  double residual_of(const float* P) {
+  // fp32 hi operand (3xTF32 only) and GEMM planes of the initial iterate.
+  void init_copies() {
+    launch_iterate_copies(P64_[0], rows_alloc_, m_, ldm_, aux_mode_ == 2 ? P_[0] : nullptr, Pa_[0],
+                          aux_mode_, aux_scale(), s_);
+  }
+
+  // luo_tseng_residual (diagnostics.cpp:33-42) of the fp64 iterate P.
+  double residual_of(const double* P) {
     std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_));
     double* pi64 = static_cast<double*>(o.get());
-    launch_rowmajor32_to_colmajor64(P, n_, m_, ldm_, pi64, -1, nullptr, nullptr, s_);
+    launch_rowmajor64_to_colmajor64(P, n_, m_, ldm_, pi64, -1, nullptr, nullptr, s_);
     return luo_tseng_residual_dev(Dx_, ldn_, Dy_, ldm_, pi64, n_, m_, mu_, nu_, 1e-8, s_);
   }
 
-  void to_host(float* P, int, std::vector<double>* out) {
+  void to_host(const double* P, int, std::vector<double>* out) {
     out->resize(static_cast<size_t>(n_) * m_);
     std::unique_ptr<void, DevFree> o(dalloc<double>(static_cast<size_t>(n_) * m_));
-    launch_rowmajor32_to_colmajor64(P, n_, m_, ldm_, static_cast<double*>(o.get()), -1, nullptr,
+    launch_rowmajor64_to_colmajor64(P, n_, m_, ldm_, static_cast<double*>(o.get()), -1, nullptr,
                                     nullptr, s_);
     GWB_CUDA(cudaMemcpyAsync(out->data(), o.get(), sizeof(double) * n_ * m_, cudaMemcpyDeviceToHost, s_));
     GWB_CUDA(cudaStreamSynchronize(s_));
@@ -944,8 +943,8 @@ class BregmanEngine {
     d.wpart = wpart_;
     d.chunks = chunks_;
     d.colblocks = colblocks_;
-    d.eb_scale = static_cast<float>(2.0 / cfg_.epsilon_reg);
-    d.bp_scale = static_cast<float>(2.0 * cfg_.step);
+    d.eb_scale = 2.0 / cfg_.epsilon_reg;
+    d.bp_scale = 2.0 * cfg_.step;
     d.log_domain = cfg_.log_domain;
     d.perturb = cfg_.perturbation;
     d.uniform_mass = 1.0 / (static_cast<double>(n_) * static_cast<double>(m_));
@@ -960,9 +959,11 @@ class BregmanEngine {
   }
 
   void rebind(BDev& d, int q) {
-    d.P = P_[q];
-    d.P_new = P_[1 - q];
+    d.P = P64_[q];
+    d.P_new = P64_[1 - q];
+    d.P32_new = aux_mode_ == 2 ? P_[1 - q] : nullptr;
     d.P_aux_new = Pa_[1 - q];
+    d.LK = LK_;
   }
 
   // Chain precision, as for BAPG: fp16 planes of the scaled
@@ -1169,7 +1170,8 @@ class BregmanEngine {
   cudaStream_t s_ = nullptr;
   std::vector<void*> bufs_;
   std::vector<GemmPlan*> plans_;
-  float *Dx_, *Dy_, *Dx_lo_, *Dy_lo_, *P_[2], *Pa_[2], *Vt_, *Vta_, *G_, *rowmax_;
+  float *Dx_, *Dy_, *Dx_lo_, *Dy_lo_, *P_[2], *Pa_[2], *Vt_, *Vta_, *G_;
+  double *P64_[2] = {nullptr, nullptr}, *LK_ = nullptr, *rowmax_ = nullptr;
   float* Dx_bf_ = nullptr;
   float* Dy_bf_ = nullptr;
   int aux_mode_ = 2;
