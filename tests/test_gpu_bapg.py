@@ -261,3 +261,29 @@ def test_concentrated_coupling(gpu, port, precision):
     for r, q in zip(rep.trace, o.trace):
         assert abs(r.objective - q["objective"]) <= OBJ_TOL * abs(q["objective"])
     check_argmax(rep.final_coupling.entries(), o.final, PI_TOL)
+
+
+def test_f16x2_auto_large_nonuniform(gpu, port):
+    """The headline chain (f16x2, AUTO for 0/1 graphs) at c4-scale K with
+    non-uniform marginals: the power-of-two iterate scale (from max μ, ν),
+    the per-row Vᵀ scales and the fp16 Vᵀ planes all in play,
+    against the oracle (fp64) over the first iterations."""
+    n = 8192
+    inst = I.alignment_instance(I.barabasi_albert(n, 5, 77), n, 0.02, 77, "ba8192", {})
+    rng = np.random.default_rng(5)
+    mu = rng.uniform(0.2, 1.8, n)
+    nu = rng.uniform(0.2, 1.8, n)
+    mu, nu = mu / mu.sum(), nu / nu.sum()
+    cfg = gw.SolverConfig(rho=0.1, max_iters=3, rel_tol=1e-30, quiet=True)
+    assert _session_precision(inst, "auto") == abi.PREC_F16X2
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(mu), gw.ProbabilityVector(nu), cfg)
+    o = port.solve(cfg.to_abi(), inst.dx, inst.dy, mu, nu)
+    assert o.code == 0
+    np.testing.assert_allclose([r.objective for r in rep.trace], [t["objective"] for t in o.trace],
+                               rtol=1e-6)
+    pi, ref = rep.final_coupling.entries(), o.final
+    assert np.abs(pi - ref).max() <= 1e-6 * np.abs(ref).max()
+    # the deviation from the start is what 3 iterations produce: hold it too
+    dev, dev_ref = pi - np.outer(mu, nu), ref - np.outer(mu, nu)
+    assert np.abs(dev - dev_ref).max() <= 1e-3 * np.abs(dev_ref).max()
