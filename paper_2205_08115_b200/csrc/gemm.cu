@@ -150,18 +150,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
 
-  // Grouped rasterisation over pair tiles (split-K: one tile sweep per split).
-  const int pid_all = blockIdx.x >> 1;
+  // Persistent CTA pairs: pair `pair` processes work items pair, pair +
+  // npairs, …  (item = split · tiles + tile; tiles in grouped rasterisation,
+  // split-K: one tile sweep per split).  The stage ring and the two TMEM
+  // chunk buffers run on across items, so the epilogue's drain and store of
+  // one tile overlap the MMAs of the next and the prologue is paid once.
   const int tiles_all = p.tiles_m * p.tiles_n;
-  const int split = pid_all / tiles_all;
-  const int pid = pid_all - split * tiles_all;
+  const int items = tiles_all * p.splits;
+  const int npairs = static_cast<int>(gridDim.x >> 1);
+  const int pair = static_cast<int>(blockIdx.x >> 1);
   const int per_group = p.group_m * p.tiles_n;
-  const int group = pid / per_group;
-  const int first_m = group * p.group_m;
-  const int gsize = min(p.tiles_m - first_m, p.group_m);
-  const int in_group = pid % per_group;
-  const int tm = first_m + in_group % gsize;
-  const int tn = in_group / gsize;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&p.a_map[0]);
@@ -184,63 +182,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int kblk = p.kind ? kBK16 : kBK;  // elements per 128-B k-block
   const int kblocks_all = (p.K + kblk - 1) / kblk;
-  const int kb_begin = p.splits > 1 ? split * p.kb_per_split : 0;
-  const int kblocks = p.splits > 1 ? max(0, min(kblocks_all - kb_begin, p.kb_per_split)) : kblocks_all;
-  // Fused planes: the work item is a k-block carrying every plane pass.
-  const int total = p.fused ? kblocks : p.passes * kblocks;
   const int chunk = p.chunk;
   const uint32_t f_a_bytes = static_cast<uint32_t>(p.a_planes) * kABytes;
   const uint32_t f_stage_bytes = f_a_bytes + static_cast<uint32_t>(p.b_planes) * kBBytes;
   const int f_stages = static_cast<int>((kStages * kStageBytes) / f_stage_bytes);
-  const int nchunks = (total + chunk - 1) / chunk;
-  const int a_row = tm * kPairM + static_cast<int>(rank) * kBM;
-  const int b_row = tn * kBN + static_cast<int>(rank) * kHalfN;
+
+  // Coordinates and k-range of work item `item`.
+  struct Item {
+    int split, tm, tn, kb_begin, kblocks, total, nchunks, a_row, b_row;
+  };
+  auto item_of = [&](int item) {
+    Item t;
+    t.split = item / tiles_all;
+    const int pid = item - t.split * tiles_all;
+    const int group = pid / per_group;
+    const int first_m = group * p.group_m;
+    const int gsize = min(p.tiles_m - first_m, p.group_m);
+    const int in_group = pid % per_group;
+    t.tm = first_m + in_group % gsize;
+    t.tn = in_group / gsize;
+    t.kb_begin = p.splits > 1 ? t.split * p.kb_per_split : 0;
+    t.kblocks = p.splits > 1 ? max(0, min(kblocks_all - t.kb_begin, p.kb_per_split)) : kblocks_all;
+    // Fused planes: the work item is a k-block carrying every plane pass.
+    t.total = p.fused ? t.kblocks : p.passes * t.kblocks;
+    t.nchunks = (t.total + chunk - 1) / chunk;
+    t.a_row = t.tm * kPairM + static_cast<int>(rank) * kBM;
+    t.b_row = t.tn * kBN + static_cast<int>(rank) * kHalfN;
+    return t;
+  };
 
   if (warp == 0) {
     if (ptx::elect_one()) {
-      if (p.fused) {
-        // One stage per k-block: A once, then every B plane (A is shared by
-        // the plane passes, so it crosses L2 → SMEM once instead of per pass).
-        for (int it = 0; it < total; ++it) {
-          const int s = it % f_stages;
-          const uint32_t ph = (it / f_stages) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          const int kb = kb_begin + it;
-          const uint32_t fbar = ptx::mapa(&full[s], 0);
-          uint8_t* st = smem + s * f_stage_bytes;
-          if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
-          for (int pa = 0; pa < p.a_planes; ++pa)
-            ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, a_row);
-          for (int pl = 0; pl < p.b_planes; ++pl) {
-            void* dst = st + f_a_bytes + pl * kBBytes;
+      int g = 0;  // stage iterations issued so far (all items)
+      for (int item = pair; item < items; item += npairs) {
+        const Item t = item_of(item);
+        if (p.fused) {
+          // One stage per k-block: A once, then every B plane (A is shared by
+          // the plane passes, so it crosses L2 → SMEM once instead of per pass).
+          for (int it = 0; it < t.total; ++it, ++g) {
+            const int s = g % f_stages;
+            const uint32_t ph = (g / f_stages) & 1;
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            const int kb = t.kb_begin + it;
+            const uint32_t fbar = ptx::mapa(&full[s], 0);
+            uint8_t* st = smem + s * f_stage_bytes;
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
+            for (int pa = 0; pa < p.a_planes; ++pa)
+              ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, t.a_row);
+            for (int pl = 0; pl < p.b_planes; ++pl) {
+              void* dst = st + f_a_bytes + pl * kBBytes;
+              if (p.b_block_k > 0) {
+                const int kk = kb * kblk;
+                ptx::tma_load_3d_2sm(dst, &p.b_map[pl], fbar, kk % p.b_block_k, t.b_row,
+                                     kk / p.b_block_k);
+              } else {
+                ptx::tma_load_2d_2sm(dst, &p.b_map[pl], fbar, kb * kblk, t.b_row);
+              }
+            }
+          }
+        } else {
+          for (int it = 0; it < t.total; ++it, ++g) {
+            const int s = g % kStages;
+            const uint32_t ph = (g / kStages) & 1;
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            const int pass = it / t.kblocks;
+            const int kb = t.kb_begin + it - pass * t.kblocks;
+            const uint32_t fbar = ptx::mapa(&full[s], 0);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+            ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk,
+                                 t.a_row);
             if (p.b_block_k > 0) {
               const int kk = kb * kblk;
-              ptx::tma_load_3d_2sm(dst, &p.b_map[pl], fbar, kk % p.b_block_k, b_row,
-                                   kk / p.b_block_k);
+              ptx::tma_load_3d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
+                                   kk % p.b_block_k, t.b_row, kk / p.b_block_k);
             } else {
-              ptx::tma_load_2d_2sm(dst, &p.b_map[pl], fbar, kb * kblk, b_row);
+              ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
+                                   kb * kblk, t.b_row);
             }
           }
         }
-      } else {
-      for (int it = 0; it < total; ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        const int pass = it / kblocks;
-        const int kb = kb_begin + it - pass * kblocks;
-        const uint32_t fbar = ptx::mapa(&full[s], 0);
-        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-        ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk, a_row);
-        if (p.b_block_k > 0) {
-          const int kk = kb * kblk;
-          ptx::tma_load_3d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
-                               kk % p.b_block_k, b_row, kk / p.b_block_k);
-        } else {
-          ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar, kb * kblk,
-                               b_row);
-        }
-      }
       }
     }
   } else if (warp == 1) {
@@ -248,58 +268,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t idesc = p.kind == 2   ? ptx::idesc_f16(kPairM, kBN)
                              : p.kind == 1 ? ptx::idesc_bf16(kPairM, kBN)
                                            : ptx::idesc_tf32(kPairM, kBN);
-      for (int c = 0; c < nchunks; ++c) {
-        const int b = c & 1;
-        ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
-        const int it0 = c * chunk;
-        const int it1 = min(total, it0 + chunk);
-        if (p.fused) {
-          for (int it = it0; it < it1; ++it) {
-            const int s = it % f_stages;
-            const uint32_t ph = (it / f_stages) & 1;
-            ptx::mbar_wait(&full[s], ph);
-            ptx::tc_fence_after();
-            const uint32_t st_base = ptx::smem_u32(smem + s * f_stage_bytes);
-            // Smallest pass first (the last pass index is the smallest
-            // product): the tensor core's truncating accumulation then acts
-            // on the hi-plane terms only (as in batched.cu).
-            for (int pl = p.passes - 1; pl >= 0; --pl) {
-              const uint32_t a_base = st_base + p.a_sel[pl] * kABytes;
-              const uint32_t b_base = st_base + f_a_bytes + p.b_sel[pl] * kBBytes;
+      int g0 = 0;  // stage iterations of the previous items
+      int c = 0;   // chunks of all items so far
+      for (int item = pair; item < items; item += npairs) {
+        const Item t = item_of(item);
+        for (int cc = 0; cc < t.nchunks; ++cc, ++c) {
+          const int b = c & 1;
+          ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
+          const int it0 = cc * chunk;
+          const int it1 = min(t.total, it0 + chunk);
+          if (p.fused) {
+            for (int it = it0; it < it1; ++it) {
+              const int g = g0 + it;
+              const int s = g % f_stages;
+              const uint32_t ph = (g / f_stages) & 1;
+              ptx::mbar_wait(&full[s], ph);
+              ptx::tc_fence_after();
+              const uint32_t st_base = ptx::smem_u32(smem + s * f_stage_bytes);
+              // Smallest pass first (the last pass index is the smallest
+              // product): the tensor core's truncating accumulation then acts
+              // on the hi-plane terms only (as in batched.cu).
+              for (int pl = p.passes - 1; pl >= 0; --pl) {
+                const uint32_t a_base = st_base + p.a_sel[pl] * kABytes;
+                const uint32_t b_base = st_base + f_a_bytes + p.b_sel[pl] * kBBytes;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
+                  const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32);
+                  const uint32_t accum = (it != it0 || pl != p.passes - 1 || k != 0) ? 1u : 0u;
+                  ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
+                }
+              }
+              ptx::mma_commit_2sm(&empty[s], 0x3);
+            }
+          } else {
+            for (int it = it0; it < it1; ++it) {
+              const int g = g0 + it;
+              const int s = g % kStages;
+              const uint32_t ph = (g / kStages) & 1;
+              ptx::mbar_wait(&full[s], ph);
+              ptx::tc_fence_after();
+              const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
+              const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN * kBK));
+              // 4 MMAs per 128-B k-block: K = 8 (tf32) or 16 (bf16), +32 B each.
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
                 const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32);
-                const uint32_t accum = (it != it0 || pl != p.passes - 1 || k != 0) ? 1u : 0u;
-                ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
+                const uint32_t accum = (it != it0 || k != 0) ? 1u : 0u;
+                if (p.kind) ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
+                else ptx::mma_tf32_2sm(acc, ad, bd, idesc, accum);
               }
+              ptx::mma_commit_2sm(&empty[s], 0x3);
             }
-            ptx::mma_commit_2sm(&empty[s], 0x3);
           }
           ptx::mma_commit_2sm(&tfull[b], 0x3);
-          continue;
         }
-        for (int it = it0; it < it1; ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          ptx::mbar_wait(&full[s], ph);
-          ptx::tc_fence_after();
-          const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
-          const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN * kBK));
-          // 4 MMAs per 128-B k-block: K = 8 (tf32) or 16 (bf16), +32 B each.
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
-            const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32);
-            const uint32_t accum = (it != it0 || k != 0) ? 1u : 0u;
-            if (p.kind) ptx::mma_bf16_2sm(acc, ad, bd, idesc, accum);
-            else ptx::mma_tf32_2sm(acc, ad, bd, idesc, accum);
-          }
-          ptx::mma_commit_2sm(&empty[s], 0x3);
-        }
-        ptx::mma_commit_2sm(&tfull[b], 0x3);
+        g0 += t.total;
       }
     }
   } else {
@@ -309,91 +336,96 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t slice = (warp - 2) >> 2;
     const uint32_t lane_base = quad * 32;
     const uint32_t col_base = slice * kSliceCols;
-    float acc[kSliceCols];
-#pragma unroll
-    for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
     const uint32_t tempty_leader[2] = {ptx::mapa(&tempty[0], 0), ptx::mapa(&tempty[1], 0)};
-    for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
-      ptx::tc_fence_after();
-      const uint32_t taddr = tmem + (lane_base << 16) + static_cast<uint32_t>(b * kBN) + col_base;
+    int c = 0;
+    for (int item = pair; item < items; item += npairs) {
+      const Item t = item_of(item);
+      const int split = t.split, tn = t.tn, a_row = t.a_row;
+      float acc[kSliceCols];
 #pragma unroll
-      for (int h = 0; h < kSliceCols / 32; ++h) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(taddr + h * 32, v);
-        ptx::tmem_wait_ld();
+      for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+      for (int cc = 0; cc < t.nchunks; ++cc, ++c) {
+        const int b = c & 1;
+        ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem + (lane_base << 16) + static_cast<uint32_t>(b * kBN) + col_base;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], __uint_as_float(v[j]));
+        for (int h = 0; h < kSliceCols / 32; ++h) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(taddr + h * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], __uint_as_float(v[j]));
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
-    }
-    const int row = a_row + static_cast<int>(lane_base + lane);
-    if (p.splits > 1 && row < p.M) {
-      // Split-K partial: raw sums, the reduce kernel applies the epilogue.
-      float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
-      const int col0 = tn * kBN + static_cast<int>(col_base);
-#pragma unroll
-      for (int j = 0; j < kSliceCols; j += 4)
-        if (col0 + j < p.ldw)
-          *reinterpret_cast<float4*>(wrow + col0 + j) =
-              make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-    } else if (row < p.M) {
-      const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
-      float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
-      float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
-      const bool round_out = p.aux_mode == 1;
-      const int col0 = tn * kBN + static_cast<int>(col_base);
-#pragma unroll
-      for (int j = 0; j < kSliceCols; ++j) {
-        float x = acc[j] * rs;
-        if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
-        acc[j] = round_out ? rna_tf32(x) : x;
-      }
-      if (p.c_planes > 0) {
-        // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
-        // split-operand GEMM.
-        const int64_t off = static_cast<int64_t>(row) * p.ldc + col0;
-        const bool vec = col0 + kSliceCols <= p.N && (p.ldc & 7) == 0;
-#pragma unroll
-        for (int j0 = 0; j0 < kSliceCols; j0 += 8) {
-          __align__(16) uint16_t h[3][8];
-          split_planes8(acc + j0, p.c_f16 != 0, h);
-          for (int pl = 0; pl < p.c_planes; ++pl) {
-            uint16_t* dst = p.c_pl[pl] + off + j0;
-            if (vec) {
-              *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h[pl]);
-            } else {
-              for (int q = 0; q < 8; ++q)
-                if (col0 + j0 + q < p.N) dst[q] = h[pl][q];
+      const int row = a_row + static_cast<int>(lane_base + lane);
+      if (p.splits > 1 && row < p.M) {
+        // Split-K partial: raw sums, the reduce kernel applies the epilogue.
+        float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
+        const int col0 = tn * kBN + static_cast<int>(col_base);
+  #pragma unroll
+        for (int j = 0; j < kSliceCols; j += 4)
+          if (col0 + j < p.ldw)
+            *reinterpret_cast<float4*>(wrow + col0 + j) =
+                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+      } else if (row < p.M) {
+        const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
+        float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+        float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
+        const bool round_out = p.aux_mode == 1;
+        const int col0 = tn * kBN + static_cast<int>(col_base);
+  #pragma unroll
+        for (int j = 0; j < kSliceCols; ++j) {
+          float x = acc[j] * rs;
+          if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
+          acc[j] = round_out ? rna_tf32(x) : x;
+        }
+        if (p.c_planes > 0) {
+          // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
+          // split-operand GEMM.
+          const int64_t off = static_cast<int64_t>(row) * p.ldc + col0;
+          const bool vec = col0 + kSliceCols <= p.N && (p.ldc & 7) == 0;
+  #pragma unroll
+          for (int j0 = 0; j0 < kSliceCols; j0 += 8) {
+            __align__(16) uint16_t h[3][8];
+            split_planes8(acc + j0, p.c_f16 != 0, h);
+            for (int pl = 0; pl < p.c_planes; ++pl) {
+              uint16_t* dst = p.c_pl[pl] + off + j0;
+              if (vec) {
+                *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h[pl]);
+              } else {
+                for (int q = 0; q < 8; ++q)
+                  if (col0 + j0 + q < p.N) dst[q] = h[pl][q];
+              }
             }
           }
-        }
-      } else if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
-#pragma unroll
-        for (int j = 0; j < kSliceCols; j += 4) {
-          if (p.accumulate) {
-            const float4 o = *reinterpret_cast<const float4*>(crow + col0 + j);
-            acc[j] = __fadd_rn(o.x, acc[j]);
-            acc[j + 1] = __fadd_rn(o.y, acc[j + 1]);
-            acc[j + 2] = __fadd_rn(o.z, acc[j + 2]);
-            acc[j + 3] = __fadd_rn(o.w, acc[j + 3]);
+        } else if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
+  #pragma unroll
+          for (int j = 0; j < kSliceCols; j += 4) {
+            if (p.accumulate) {
+              const float4 o = *reinterpret_cast<const float4*>(crow + col0 + j);
+              acc[j] = __fadd_rn(o.x, acc[j]);
+              acc[j + 1] = __fadd_rn(o.y, acc[j + 1]);
+              acc[j + 2] = __fadd_rn(o.z, acc[j + 2]);
+              acc[j + 3] = __fadd_rn(o.w, acc[j + 3]);
+            }
+            *reinterpret_cast<float4*>(crow + col0 + j) =
+                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            if (clo)
+              *reinterpret_cast<float4*>(clo + col0 + j) = make_float4(
+                  tf32_lo(acc[j]), tf32_lo(acc[j + 1]), tf32_lo(acc[j + 2]), tf32_lo(acc[j + 3]));
           }
-          *reinterpret_cast<float4*>(crow + col0 + j) =
-              make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-          if (clo)
-            *reinterpret_cast<float4*>(clo + col0 + j) = make_float4(
-                tf32_lo(acc[j]), tf32_lo(acc[j + 1]), tf32_lo(acc[j + 2]), tf32_lo(acc[j + 3]));
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kSliceCols; ++j) {
-          if (col0 + j < p.N) {
-            if (p.accumulate) acc[j] = __fadd_rn(crow[col0 + j], acc[j]);
-            crow[col0 + j] = acc[j];
-            if (clo) clo[col0 + j] = tf32_lo(acc[j]);
+        } else {
+  #pragma unroll
+          for (int j = 0; j < kSliceCols; ++j) {
+            if (col0 + j < p.N) {
+              if (p.accumulate) acc[j] = __fadd_rn(crow[col0 + j], acc[j]);
+              crow[col0 + j] = acc[j];
+              if (clo) clo[col0 + j] = tf32_lo(acc[j]);
+            }
           }
         }
       }
@@ -706,7 +738,17 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       throw std::runtime_error("gemm: split-K workspace allocation failed");
     g.ws = p->ws;
   }
-  p->grid = 2 * g.tiles_m * g.tiles_n * g.splits;  // two CTAs (one cluster) per tile
+  // Persistent CTA pairs: one per SM pair (the kernel loops over its work
+  // items); GWB_GEMM_PERSISTENT=0 (A/B knob) launches one pair per item.
+  const int items = g.tiles_m * g.tiles_n * g.splits;
+  static const bool persistent = [] {
+    const char* e = std::getenv("GWB_GEMM_PERSISTENT");
+    return !(e && e[0] == '0');
+  }();
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p->grid = 2 * (persistent ? std::min(items, std::max(1, sms / 2)) : items);
   p->flops = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
   return p;
 }
