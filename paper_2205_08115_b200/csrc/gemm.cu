@@ -108,6 +108,7 @@ struct __align__(64) GemmParams {
   int32_t kb_per_split;
   float* ws;
   int64_t ldw;
+  int* counters;       // split-K: per (tile, CTA) arrival counters, in-kernel reduction
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -362,16 +363,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
       }
       const int row = a_row + static_cast<int>(lane_base + lane);
-      if (p.splits > 1 && row < p.M) {
-        // Split-K partial: raw sums, the reduce kernel applies the epilogue.
-        float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
+      if (p.splits > 1) {
+        // Split-K: raw partial sums to the workspace; the CTA that completes
+        // the tile's last split (per-tile arrival counter) then sums the
+        // partials in split order — the fixed order of the standalone reduce
+        // kernel, so results are bitwise the same — and runs the epilogue.
         const int col0 = tn * kBN + static_cast<int>(col_base);
-  #pragma unroll
-        for (int j = 0; j < kSliceCols; j += 4)
-          if (col0 + j < p.ldw)
-            *reinterpret_cast<float4*>(wrow + col0 + j) =
-                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-      } else if (row < p.M) {
+        if (row < p.M) {
+          float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
+#pragma unroll
+          for (int j = 0; j < kSliceCols; j += 4)
+            if (col0 + j < p.ldw)
+              *reinterpret_cast<float4*>(wrow + col0 + j) =
+                  make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        }
+        if (p.counters == nullptr) continue;  // standalone reduce kernel follows
+        __threadfence();
+        ptx::named_barrier_sync(1, 32 * kEpiWarps);
+        __shared__ int s_last;
+        int* cnt = p.counters + (item - split * tiles_all) * 2 + static_cast<int>(rank);
+        if (warp == 2 && lane == 0) s_last = atomicAdd(cnt, 1) == p.splits - 1;
+        ptx::named_barrier_sync(1, 32 * kEpiWarps);
+        if (!s_last) continue;
+        __threadfence();
+        if (warp == 2 && lane == 0) *cnt = 0;  // every split arrived: ready for the next launch
+        if (row < p.M) {
+#pragma unroll
+          for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+          for (int sp = 0; sp < p.splits; ++sp) {
+            const float* w = p.ws + static_cast<int64_t>(sp) * p.M * p.ldw +
+                             static_cast<int64_t>(row) * p.ldw + col0;
+#pragma unroll
+            for (int j = 0; j < kSliceCols; j += 4) {
+              if (col0 + j < p.ldw) {
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(w + j));
+                acc[j] = __fadd_rn(acc[j], v.x);
+                acc[j + 1] = __fadd_rn(acc[j + 1], v.y);
+                acc[j + 2] = __fadd_rn(acc[j + 2], v.z);
+                acc[j + 3] = __fadd_rn(acc[j + 3], v.w);
+              }
+            }
+          }
+        }
+      }
+      if (row < p.M) {
         const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
         float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
         float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
@@ -591,8 +626,10 @@ struct GemmPlan {
   int grid = 0;
   double flops = 0.0;
   float* ws = nullptr;  // split-K workspace (owned)
+  int* counters = nullptr;
   ~GemmPlan() {
     if (ws) cudaFree(ws);
+    if (counters) cudaFree(counters);
   }
 };
 
@@ -737,13 +774,26 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     if (cudaMalloc(&p->ws, sizeof(float) * static_cast<size_t>(g.splits) * d.M * g.ldw) != cudaSuccess)
       throw std::runtime_error("gemm: split-K workspace allocation failed");
     g.ws = p->ws;
+    // In-kernel reduction by the last-arriving split (GWB_GEMM_SPLITK_KERNEL=1
+    // keeps the separate reduce kernel for A/B).
+    static const bool reduce_kernel = std::getenv("GWB_GEMM_SPLITK_KERNEL") != nullptr;
+    if (!reduce_kernel) {
+      const size_t bytes = sizeof(int) * 2 * static_cast<size_t>(g.tiles_m) * g.tiles_n;
+      if (cudaMalloc(&p->counters, bytes) != cudaSuccess || cudaMemset(p->counters, 0, bytes) != cudaSuccess)
+        throw std::runtime_error("gemm: split-K counter allocation failed");
+      g.counters = p->counters;
+    }
   }
-  // Persistent CTA pairs: one per SM pair (the kernel loops over its work
-  // items); GWB_GEMM_PERSISTENT=0 (A/B knob) launches one pair per item.
+  // One CTA pair per work item by default; GWB_GEMM_PERSISTENT=1 runs one
+  // pair per SM pair looping over its items.  Measured at c4 (3 alternating
+  // runs, one box): persistent 11.40-11.44 it/s at 1590-1612 MHz vs
+  // 11.77-11.78 at 1665-1702 MHz — +2.7% per clock, but the chip is power-
+  // capped (sw_power_cap) and the persistent grid's higher draw costs more
+  // clock than it gains.
   const int items = g.tiles_m * g.tiles_n * g.splits;
   static const bool persistent = [] {
     const char* e = std::getenv("GWB_GEMM_PERSISTENT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -757,12 +807,14 @@ void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
   gemm_tf32_kernel<<<p->grid, kThreads, kSmemBytes, s>>>(p->params);
-  if (p->params.splits > 1)
+  if (p->params.splits > 1 && p->params.counters == nullptr)
     splitk_reduce_kernel<<<p->params.M, 256, 0, s>>>(p->params);
   return cudaGetLastError();
 }
 
-int gemm_launches(const GemmPlan* p) { return p->params.splits > 1 ? 2 : 1; }
+int gemm_launches(const GemmPlan* p) {
+  return p->params.splits > 1 && p->params.counters == nullptr ? 2 : 1;
+}
 
 double gemm_flops(const GemmPlan* p) { return p->flops; }
 int gemm_passes(const GemmPlan* p) { return p->params.passes; }

@@ -79,6 +79,11 @@ __device__ __forceinline__ void cluster_sync() {
                ::: "memory");
 }
 
+// Named barrier `id` over `count` threads (a multiple of 32) of this CTA.
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // shared::cluster address of `p` (a shared::cta variable) in CTA `rank`.
 __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   uint32_t r;
