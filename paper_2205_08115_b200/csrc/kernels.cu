@@ -50,6 +50,15 @@ __device__ __forceinline__ void store_d4(double* p, const double (&v)[4]) {
   *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
 }
 
+// A device error flag (DevFlag) raised at the current iteration: the first
+// raise records err_iter; the iteration's remaining projection kernels skip
+// on `flags`, and the finalize marks the solve done (no separate check
+// launches).
+__device__ __forceinline__ void raise_flag(DevStatus* st, int flag) {
+  atomicOr(&st->flags, flag);
+  atomicCAS(&st->err_iter, 0, st->iter);
+}
+
 // Half-step a: one CTA per row.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int write, int tail) {
@@ -87,9 +96,9 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   const double S = ms.s;
   const double r = ms.mx;
   if (threadIdx.x == 0) {
-    if (r > 700.0) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (r > 700.0) raise_flag(d.st, kFlagOverflowA);
     if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
-      atomicOr(&d.st->flags, kFlagZeroA);
+      raise_flag(d.st, kFlagZeroA);
       atomicMin(&d.st->zero_index, static_cast<int>(i));
     }
   }
@@ -193,9 +202,9 @@ __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d
   const double S = ms.s;
   const double r = ms.mx;
   if (lane == 0) {
-    if (r > 700.0) atomicOr(&d.st->flags, kFlagOverflowA);
+    if (r > 700.0) raise_flag(d.st, kFlagOverflowA);
     if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
-      atomicOr(&d.st->flags, kFlagZeroA);
+      raise_flag(d.st, kFlagZeroA);
       atomicMin(&d.st->zero_index, static_cast<int>(i));
     }
   }
@@ -220,7 +229,7 @@ constexpr int kColThreads = 256;
 constexpr int kColWidth = 128;  // columns per CTA (32 lanes × 4)
 
 __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int rows_per_chunk) {
-  if (d.st->done) return;
+  if (d.st->done || d.st->flags) return;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
 // Half-step b, pass 2: merge chunk partials per column, raise errors.  One
 // warp per column: lanes take the row chunks, then a fixed-order warp merge.
 __global__ void col_combine_kernel(BapgDev d) {
-  if (d.st->done) return;
+  if (d.st->done || d.st->flags) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   if (j >= d.m) return;
   const int lane = threadIdx.x & 31;
@@ -286,9 +295,9 @@ __global__ void col_combine_kernel(BapgDev d) {
   r = lse64_warp_merge(r);
   p = warp_sum(p);
   if (lane != 0) return;
-  if (r.mx > 700.0) atomicOr(&d.st->flags, kFlagOverflowB);
+  if (r.mx > 700.0) raise_flag(d.st, kFlagOverflowB);
   if (!(r.s > 0.0) || !isfinite(r.s) || isnan(r.mx)) {
-    atomicOr(&d.st->flags, kFlagZeroB);
+    raise_flag(d.st, kFlagZeroB);
     atomicMin(&d.st->zero_index, static_cast<int>(j));
   }
   d.col_max[j] = r.mx;
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   Lse64 dummy{-INFINITY, 0.0};
   block_reduce64<kRowThreads, 5>(dummy, sums);
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
-    atomicOr(&d.st->flags, kFlagNonFinite);
+    raise_flag(d.st, kFlagNonFinite);
   if (threadIdx.x == 0) {
     ColWritePart& c = d.cw_part[i];
     c.gw = sums[0];
@@ -387,7 +396,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
   }
 #pragma unroll
   for (int q = 0; q < 5; ++q) sums[q] = warp_sum(sums[q]);
-  if (!__all_sync(0xffffffffu, finite ? 1 : 0) && lane == 0) atomicOr(&d.st->flags, kFlagNonFinite);
+  if (!__all_sync(0xffffffffu, finite ? 1 : 0) && lane == 0) raise_flag(d.st, kFlagNonFinite);
   if (lane == 0) {
     ColWritePart& c = d.cw_part[i];
     c.gw = sums[0];
@@ -398,20 +407,15 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
   }
 }
 
-// Flags raised by a kernel: mark the solve finished at the current iteration.
-__global__ void flag_check_kernel(DevStatus* st) {
-  if (st->done) return;
-  if (st->flags != 0) {
-    st->done = 1;
-    st->err_iter = st->iter;
-  }
-}
-
 constexpr int kFinThreads = 512;
 
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(BapgDev d, double rel_tol, int tail) {
   DevStatus* st = d.st;
   if (tail ? st->flags != 0 : st->done != 0) return;
+  if (!tail && st->flags != 0) {  // raised this iteration (raise_flag): stop here
+    if (threadIdx.x == 0) st->done = 1;
+    return;
+  }
   const int k = tail ? st->iter - 1 : st->iter;
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // acc: 0 gw_row, 1 rowdev, 2 cw.gw, 3 split, 4 diff, 5 wold, 6 gp, 7 coldev
@@ -686,7 +690,6 @@ void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
   else if (d.n >= 1)
     row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
                                                                          write ? 0 : 1);
-  if (write) flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 
 void launch_col_update(const BapgDev& d, cudaStream_t s) {
@@ -695,9 +698,7 @@ void launch_col_update(const BapgDev& d, cudaStream_t s) {
             static_cast<unsigned>(d.chunks));
   col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
   col_combine_kernel<<<grid1d(d.m * 32, 256), 256, 0, s>>>(d);
-  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
   launch_col_write_pass(d, s);
-  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 
 void launch_col_partial(const BapgDev& d, cudaStream_t s) {
@@ -709,9 +710,7 @@ void launch_col_partial(const BapgDev& d, cudaStream_t s) {
 }
 
 void launch_col_write(const BapgDev& d, cudaStream_t s) {
-  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
   if (d.n >= 1) launch_col_write_pass(d, s);
-  flag_check_kernel<<<1, 1, 0, s>>>(d.st);
 }
 
 void launch_finalize(const BapgDev& d, double rel_tol, bool tail, cudaStream_t s) {

@@ -417,7 +417,7 @@ class ShardEngine {
       case 1:  // A2: G_r, row projection
         if (!chunked) GWB_CUDA(gemm_launch(g2_, s_));
         launch_row_update(d, true, s_);
-        launches_ += chunked ? 2 : 3;
+        launches_ += chunked ? 1 : 2;
         break;
       case 2:  // B1
         GWB_CUDA(gemm_launch(g1p_, s_));
@@ -435,7 +435,7 @@ class ShardEngine {
             d, stats_, world_);
         launch_col_write(d, s_);
         shard_diag_kernel<<<1, 512, 0, s_>>>(d, diag_, err_, rank_, row_begin_, 0);
-        launches_ += d.n >= 1 ? 5 : 4;
+        launches_ += d.n >= 1 ? 3 : 2;
         break;
       case 5:  // F: global finalize; w' becomes w
         shard_finalize_kernel<<<1, 1, 0, s_>>>(d, diag_, err_, cfg_.rel_tol, 0);

@@ -634,14 +634,14 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
       launch_row_quad(d, stream_);
     else
       launch_row_update(d, true, stream_);
-    launches += 2;
+    launches += quadratic() ? 2 : 1;  // quadratic: + its flag check
   } else {
     if (quadratic())
       launch_col_quad(d, stream_);
     else
       launch_col_update(d, stream_);
     launch_finalize(d, rel_tol, false, stream_);
-    launches += quadratic() ? 4 : 6;
+    launches += 4;  // column passes (partial, combine, write / quadratic's) + finalize
   }
   if (timing_) {
     GWB_CUDA(cudaEventRecord(e2, stream_));
