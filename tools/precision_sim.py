@@ -12,6 +12,7 @@ MODE combines (underscore-separated):
   opNN          both chain GEMM operands rounded to NN significant bits (22: f16x2)
   biasX         G scaled by (1 − X): a systematic accumulation bias
   noiseX        G scaled by (1 + X·N(0,1)) per entry: random chain error
+  dNN           D_X, D_Y rounded once to NN significant bits (a fixed model error)
 (the fp32-arithmetic variants of the projections were modelled separately
 in the round-2 study).
 """
@@ -43,6 +44,12 @@ def main():
         return None
 
     bits = val("op")
+    dbits = val("d")
+    if dbits:
+        m_, e_ = np.frexp(dx)
+        dx = np.ldexp(np.round(m_ * 2.0 ** dbits) / 2.0 ** dbits, e_)
+        m_, e_ = np.frexp(dy)
+        dy = np.ldexp(np.round(m_ * 2.0 ** dbits) / 2.0 ** dbits, e_)
 
     def rbits(x):
         m, e = np.frexp(x)
