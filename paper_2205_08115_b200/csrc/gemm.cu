@@ -109,6 +109,9 @@ struct __align__(64) GemmParams {
   float* ws;
   int64_t ldw;
   int* counters;       // split-K: per (tile, CTA) arrival counters, in-kernel reduction
+  const float* col_bias;  // [N] added before scaling (centred operands)
+  double* rs_part;        // [M][rs_stride] fp64 row partial sums of the output
+  int32_t rs_stride;      // tiles_n · 4 (one per 64-column slice), 1 with the reduce kernel
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -414,9 +417,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int col0 = tn * kBN + static_cast<int>(col_base);
   #pragma unroll
         for (int j = 0; j < kSliceCols; ++j) {
-          float x = acc[j] * rs;
+          float a = acc[j];
+          if (p.col_bias != nullptr) a = __fadd_rn(a, (col0 + j < p.N) ? __ldg(p.col_bias + col0 + j) : 0.0f);
+          float x = a * rs;
           if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
           acc[j] = round_out ? rna_tf32(x) : x;
+        }
+        if (p.rs_part != nullptr) {
+          double s = 0.0;
+  #pragma unroll
+          for (int j = 0; j < kSliceCols; ++j)
+            if (col0 + j < p.N) s += static_cast<double>(acc[j]);
+          p.rs_part[static_cast<int64_t>(row) * p.rs_stride + tn * 4 + static_cast<int>(slice)] = s;
         }
         if (p.c_planes > 0) {
           // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
@@ -481,6 +493,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
   if (p.skip != nullptr && *p.skip != 0) return;
   const int row = blockIdx.x;
   const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
+  double rsum = 0.0;  // row sum of the output (rs_part)
   // ldw (a multiple of 8) and ldc (of 32) and 256-B aligned buffers make
   // every 8-column group 16-B aligned (fp32 float4 pairs, bf16 uint4).
   for (int c0 = threadIdx.x * 8; c0 < p.N; c0 += blockDim.x * 8) {
@@ -510,9 +523,12 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float v = x[q] * rs;
+      float a = x[q];
+      if (p.col_bias != nullptr) a = __fadd_rn(a, (c0 + q < p.N) ? p.col_bias[c0 + q] : 0.0f);
+      float v = a * rs;
       if (p.col_scale != nullptr) v *= (c0 + q < p.N) ? p.col_scale[c0 + q] : 0.0f;
       x[q] = p.aux_mode == 1 ? rna_tf32(v) : v;
+      if (c0 + q < p.N) rsum += static_cast<double>(x[q]);
     }
     const int64_t off = static_cast<int64_t>(row) * p.ldc + c0;
     const bool full = c0 + 8 <= p.N;
@@ -537,6 +553,29 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
       }
     }
   }
+  if (p.rs_part != nullptr) {
+    // Fixed-order block sum: warp butterflies, then warps in order.
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+      p.rs_part[static_cast<int64_t>(row) * p.rs_stride] = t;
+    }
+  }
+}
+
+// out[i] = factor · Σ_k rs_part[i][k] (fixed order), rounded to fp32.
+__global__ void rowsum_bias_kernel(const __grid_constant__ GemmParams p, double factor, float* out) {
+  if (p.skip != nullptr && *p.skip != 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.M) return;
+  const double* r = p.rs_part + static_cast<int64_t>(i) * p.rs_stride;
+  double t = 0.0;
+  for (int k = 0; k < p.rs_stride; ++k) t += r[k];
+  out[i] = static_cast<float>(factor * t);
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -627,9 +666,11 @@ struct GemmPlan {
   double flops = 0.0;
   float* ws = nullptr;  // split-K workspace (owned)
   int* counters = nullptr;
+  double* rs_part = nullptr;  // row partial sums (owned)
   ~GemmPlan() {
     if (ws) cudaFree(ws);
     if (counters) cudaFree(counters);
+    if (rs_part) cudaFree(rs_part);
   }
 };
 
@@ -743,6 +784,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   for (int pl = 0; pl < 3; ++pl) g.c_pl[pl] = static_cast<uint16_t*>(d.c_bf16[pl]);
   g.row_scale = d.row_scale;
   g.col_scale = d.col_scale;
+  g.col_bias = d.col_bias;
   g.accumulate = d.accumulate ? 1 : 0;
   g.skip = d.skip;
   // Split-K when one sweep of pair tiles leaves most of the 74 SM pairs idle
@@ -793,6 +835,14 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // 11.77-11.78 at 1665-1702 MHz — +2.7% per clock, but the chip is power-
   // capped (sw_power_cap) and the persistent grid's higher draw costs more
   // clock than it gains.
+  if (d.rowsums) {
+    // One partial per (row, 64-column slice of a tile) from the GEMM's
+    // epilogue; the standalone split-K reduce kernel sums whole rows.
+    g.rs_stride = (g.splits > 1 && g.counters == nullptr) ? 1 : g.tiles_n * 4;
+    if (cudaMalloc(&p->rs_part, sizeof(double) * static_cast<size_t>(d.M) * g.rs_stride) != cudaSuccess)
+      throw std::runtime_error("gemm: row-sum workspace allocation failed");
+    g.rs_part = p->rs_part;
+  }
   const int items = g.tiles_m * g.tiles_n * g.splits;
   static const bool persistent = [] {
     const char* e = std::getenv("GWB_GEMM_PERSISTENT");
@@ -812,6 +862,12 @@ cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
   gemm_tf32_kernel<<<p->grid, kThreads, kSmemBytes, s>>>(p->params);
   if (p->params.splits > 1 && p->params.counters == nullptr)
     splitk_reduce_kernel<<<p->params.M, 256, 0, s>>>(p->params);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_rowsum_bias(const GemmPlan* p, double factor, float* out, cudaStream_t s) {
+  if (p->params.rs_part == nullptr) return cudaErrorInvalidValue;
+  rowsum_bias_kernel<<<(p->params.M + 255) / 256, 256, 0, s>>>(p->params, factor, out);
   return cudaGetLastError();
 }
 

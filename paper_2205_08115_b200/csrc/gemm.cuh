@@ -72,6 +72,13 @@ struct GemmDesc {
   // to a plan-owned fp32 workspace and a second kernel sums them in a fixed
   // order and applies the epilogue (scales, operand copies, planes).
   int split_k = 0;
+  // Centred structure matrices (weighted D): the caller passes
+  // A − c·J and adds the rank-1 part back through col_bias, a length-N vector
+  // added to the accumulated sum before the row / column scales.  With
+  // `rowsums` the plan also keeps fp64 partial sums of every output row
+  // (after scaling, before the plane split) for gemm_rowsum_bias.
+  const float* col_bias = nullptr;
+  bool rowsums = false;
 };
 
 // 2-D TMA descriptor of a row-major rows×cols matrix (leading dim ld
@@ -91,5 +98,9 @@ double gemm_flops(const GemmPlan* p);
 int gemm_passes(const GemmPlan* p);
 // Kernel launches per gemm_launch (2 with split-K).
 int gemm_launches(const GemmPlan* p);
+// out[i] = factor · Σ_j C[i][j] over the last launch's output rows (fp64 sum
+// of the plan's row partials in a fixed order, rounded to fp32).  Needs
+// GemmDesc::rowsums; one launch, a no-op when the plan's skip flag is set.
+cudaError_t gemm_rowsum_bias(const GemmPlan* p, double factor, float* out, cudaStream_t s);
 
 }  // namespace gwb

@@ -308,8 +308,9 @@ __global__ void col_combine_kernel(BapgDev d) {
 
 // One element of the half-step-b write: w' = scale_j · π · e^{x − max_j},
 // with the fused record partials (gw, split, diff, wold, gp).
+template <int kN>
 __device__ __forceinline__ double col_write_elem(float g, double p, double w, double mx,
-                                                 double sc, double inv_rho, double (&sums)[5],
+                                                 double sc, double inv_rho, double (&sums)[kN],
                                                  bool& finite) {
   const double o = sc * p * exp(expo(g, inv_rho) - mx);
   finite = finite && isfinite(o);
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
   double* wn = d.W64_new + i * d.ld;
   const double inv_rho = d.inv_rho64;
   const int64_t m = d.m;
-  double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
+  double sums[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp, ΣW'
   bool finite = true;
   for (int64_t j = threadIdx.x * 4; j < m; j += kRowThreads * 4) {
     const float4 g4 = *reinterpret_cast<const float4*>(g + j);
@@ -345,14 +346,16 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
     load_d4(d.col_max + j, mv);
     load_d4(d.col_scale + j, sv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q) {
       o[q] = (j + q < m) ? col_write_elem(gv[q], pv[q], wv[q], mv[q], sv[q], inv_rho, sums, finite)
                          : 0.0;
+      sums[5] += o[q];
+    }
     store_d4(wn + j, o);
     aux_store4_64(d.W_aux, d.W_new, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
   Lse64 dummy{-INFINITY, 0.0};
-  block_reduce64<kRowThreads, 5>(dummy, sums);
+  block_reduce64<kRowThreads, 6>(dummy, sums);
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
     raise_flag(d.st, kFlagNonFinite);
   if (threadIdx.x == 0) {
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
     c.diff = sums[2];
     c.wold = sums[3];
     c.gp = sums[4];
+    if (d.wsum_bias) d.wsum_bias[i] = static_cast<float>(d.wsum_factor * sums[5]);
   }
 }
 
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
   if (i >= d.n) return;
   const int64_t m = d.m;
   const double inv_rho = d.inv_rho64;
-  double sums[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp
+  double sums[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gw, split, diff, wold, gp, ΣW'
   bool finite = true;
 #pragma unroll 2
   for (int v = 0; v < kNarrowV; ++v) {
@@ -388,14 +392,16 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
     load_d4(d.col_max + j, mv);
     load_d4(d.col_scale + j, sv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q) {
       o[q] = (j + q < m) ? col_write_elem(gv[q], pv[q], wv[q], mv[q], sv[q], inv_rho, sums, finite)
                          : 0.0;
+      sums[5] += o[q];
+    }
     store_d4(d.W64_new + i * d.ld + j, o);
     aux_store4_64(d.W_aux, d.W_new, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
 #pragma unroll
-  for (int q = 0; q < 5; ++q) sums[q] = warp_sum(sums[q]);
+  for (int q = 0; q < 6; ++q) sums[q] = warp_sum(sums[q]);
   if (!__all_sync(0xffffffffu, finite ? 1 : 0) && lane == 0) raise_flag(d.st, kFlagNonFinite);
   if (lane == 0) {
     ColWritePart& c = d.cw_part[i];
@@ -404,6 +410,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
     c.diff = sums[2];
     c.wold = sums[3];
     c.gp = sums[4];
+    if (d.wsum_bias) d.wsum_bias[i] = static_cast<float>(d.wsum_factor * sums[5]);
   }
 }
 
@@ -636,6 +643,32 @@ __global__ void iterate_copies_kernel(const double* x, int64_t cols, int64_t ld,
   }
 }
 
+// Centred operand copies of a structure matrix: x = D − c in fp64.
+__global__ void center_copies_kernel(const float* D, int64_t cols, int64_t ld, double c,
+                                     float* copy32, float* aux, int mode, int64_t plane,
+                                     float scale) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x * 4; j < cols; j += blockDim.x * 4) {
+    const float4 f = *reinterpret_cast<const float4*>(D + i * ld + j);
+    const float fv[4] = {f.x, f.y, f.z, f.w};
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = j + q < cols ? static_cast<double>(fv[q]) - c : 0.0;
+    aux_store4_64(aux, copy32, mode, plane, i * ld + j, v, scale);
+  }
+}
+
+// out[i] = factor · Σ_j x[i][j], one warp per row, fixed order.
+__global__ void row_bias64_kernel(const double* x, int64_t rows, int64_t cols, int64_t ld,
+                                  double factor, float* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  if (i >= rows) return;
+  double t = 0.0;
+  for (int64_t j = threadIdx.x & 31; j < cols; j += 32) t += x[i * ld + j];
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) out[i] = static_cast<float>(factor * t);
+}
+
 __device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
   // valid for v >= 0 (structure matrices are nonnegative)
   atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
@@ -757,6 +790,19 @@ void launch_iterate_copies(const double* x, int64_t rows, int64_t cols, int64_t 
   if (rows < 1 || (!copy32 && !aux)) return;
   iterate_copies_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(x, cols, ld, copy32, aux, mode,
                                                                     rows * ld, scale);
+}
+
+void launch_center_copies(const float* D, int64_t rows, int64_t cols, int64_t ld, double c,
+                          float* copy32, float* aux, int mode, float scale, cudaStream_t s) {
+  if (rows < 1 || (!copy32 && !aux)) return;
+  center_copies_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(D, cols, ld, c, copy32, aux, mode,
+                                                                   rows * ld, scale);
+}
+
+void launch_row_bias64(const double* x, int64_t rows, int64_t cols, int64_t ld, double factor,
+                       float* out, cudaStream_t s) {
+  if (rows < 1) return;
+  row_bias64_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, cols, ld, factor, out);
 }
 
 void launch_product_coupling64(const double* mu, const double* nu, int64_t n, int64_t m, int64_t ld,

@@ -106,6 +106,11 @@ struct BapgDev {
   DevStatus* st;
   DevRecord* rec;           // [max_rec + 2]
   int max_rec;              // records beyond this iteration are not kept
+  // Centred chain (weighted D): the write pass of half-step b
+  // also stores wsum_factor · Σ_j W'_ij (fp64 sum, fp32 result), the next
+  // GEMM1's rank-1 bias (nullable).
+  float* wsum_bias;
+  double wsum_factor;
 };
 
 // Half-step a (solvers.cpp:164-170): E = G/ρ, P = diag(μ/rowsum)·(W ⊙ e^E),
@@ -148,6 +153,14 @@ void launch_colmajor64_to_rowmajor64(const double* src, int64_t rows, int64_t co
 // as BapgDev) of a row-major fp64 iterate.
 void launch_iterate_copies(const double* x, int64_t rows, int64_t cols, int64_t ld, float* copy32,
                            float* aux, int mode, float scale, cudaStream_t s);
+// Centred structure-matrix operands: from D − c (formed in
+// fp64), an optional fp32 copy (the TF32 hi operand) and the operand planes
+// of `mode` / `scale` as launch_iterate_copies.
+void launch_center_copies(const float* D, int64_t rows, int64_t cols, int64_t ld, double c,
+                          float* copy32, float* aux, int mode, float scale, cudaStream_t s);
+// out[i] = factor · Σ_j x[i][j] (row-major fp64, fixed order) in fp32.
+void launch_row_bias64(const double* x, int64_t rows, int64_t cols, int64_t ld, double factor,
+                       float* out, cudaStream_t s);
 // P = μ νᵀ in row-major fp64.
 void launch_product_coupling64(const double* mu, const double* nu, int64_t n, int64_t m, int64_t ld,
                                double* P, cudaStream_t s);

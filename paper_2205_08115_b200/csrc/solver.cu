@@ -140,7 +140,8 @@ BapgEngine::~BapgEngine() {
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], P64_, W64_[0], W64_[1], Vt_,
            Vt_aux_, G_, mu32_, nu32_, mu64_, nu64_, row_part_, cw_part_, col_pmax_, col_psum_,
-           col_max_, col_scale_, col_psump_, col_dev_, st_, rec_, f16_g1_rs_, f16_g2_cs_})
+           col_max_, col_scale_, col_psump_, col_dev_, st_, rec_, f16_g1_rs_, f16_g2_cs_,
+           cb1_pi_, cb1_w_[0], cb1_w_[1], cb2_, Dxc_, Dyc_})
     dfree(p, stream_);
   if (h_done_) cudaFreeHost(h_done_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
@@ -227,6 +228,8 @@ BapgDev BapgEngine::dev_view(int q) const {
   d.st = st_;
   d.rec = rec_;
   d.max_rec = max_iters_;
+  d.wsum_bias = center_ ? cb1_w_[1 - q] : nullptr;
+  d.wsum_factor = cb1_factor();
   return d;
 }
 
@@ -302,6 +305,19 @@ void BapgEngine::prepare_d() {
     precision_ = GWB_PREC_3XTF32;
   if (precision_ != GWB_PREC_TF32 && !Vt_aux_)
     Vt_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldn_ * 3 / 2);
+  // Weighted D (f16x3, or a TF32 chain on inexact D) runs centred, entropy
+  // geometry only (the column write pass provides rowsum(w)).
+  center_ = !quadratic() &&
+            (split_d() || ((precision_ == GWB_PREC_3XTF32 || precision_ == GWB_PREC_TF32) &&
+                           !(dx_exact_ && dy_exact_)));
+  ctr_x_ = center_ ? 0.5 * static_cast<double>(h_max[0]) : 0.0;
+  ctr_y_ = center_ ? 0.5 * static_cast<double>(h_max[1]) : 0.0;
+  if (center_) {
+    if (!cb1_pi_) cb1_pi_ = dalloc<float>(stream_, ldn_);
+    for (int q = 0; q < 2; ++q)
+      if (!cb1_w_[q]) cb1_w_[q] = dalloc<float>(stream_, ldn_);
+    if (!cb2_) cb2_ = dalloc<float>(stream_, ldm_);
+  }
   if (bf16()) {
     // One bf16 / fp16 plane per structure matrix (2 B/element), two for f16x3.
     const size_t per = split_d() ? 1 : 2;  // elements per float
@@ -315,10 +331,13 @@ void BapgEngine::prepare_d() {
         auto shift = [](float mx) {
           return mx > 0.f ? 14 - static_cast<int>(std::ceil(std::log2(static_cast<double>(mx)))) : 0;
         };
-        sdx_ = shift(h_max[0]);
-        sdy_ = shift(h_max[1]);
-        launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_bf_, 5, stream_, std::ldexp(1.0f, sdx_));
-        launch_tf32_aux(Dy_, m_, m_, ldm_, Dy_bf_, 5, stream_, std::ldexp(1.0f, sdy_));
+        // Centred: planes of (D − c)·2^s from fp64, |D − c| ≤ c.
+        sdx_ = shift(static_cast<float>(ctr_x_));
+        sdy_ = shift(static_cast<float>(ctr_y_));
+        launch_center_copies(Dx_, n_, n_, ldn_, ctr_x_, nullptr, Dx_bf_, 5, std::ldexp(1.0f, sdx_),
+                             stream_);
+        launch_center_copies(Dy_, m_, m_, ldm_, ctr_y_, nullptr, Dy_bf_, 5, std::ldexp(1.0f, sdy_),
+                             stream_);
       } else {
         sdx_ = sdy_ = 0;
         launch_to_f16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
@@ -333,10 +352,28 @@ void BapgEngine::prepare_d() {
       launch_to_bf16(Dx_, n_, n_, ldn_, Dx_bf_, stream_);
       launch_to_bf16(Dy_, m_, m_, ldm_, Dy_bf_, stream_);
     }
+    if (center_) launch_row_bias64(mu64_, n_, 1, 1, cb1_factor(), cb1_pi_, stream_);
     build_plans();
     return;
   }
   const int mode = precision_ == GWB_PREC_TF32 ? 1 : 2;
+  if (center_) {
+    // TF32 chains on centred D: hi = fp32(D − c) (3xTF32) and the residual
+    // or the rna copy (1xTF32), both from fp64 D − c.
+    if (!Dx_aux_) Dx_aux_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_);
+    if (!Dy_aux_) Dy_aux_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
+    if (mode == 2) {
+      if (!Dxc_) Dxc_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_);
+      if (!Dyc_) Dyc_ = dalloc<float>(stream_, static_cast<size_t>(m_) * ldm_);
+    }
+    launch_center_copies(Dx_, n_, n_, ldn_, ctr_x_, mode == 2 ? Dxc_ : nullptr, Dx_aux_, mode, 1.0f,
+                         stream_);
+    launch_center_copies(Dy_, m_, m_, ldm_, ctr_y_, mode == 2 ? Dyc_ : nullptr, Dy_aux_, mode, 1.0f,
+                         stream_);
+    launch_row_bias64(mu64_, n_, 1, 1, cb1_factor(), cb1_pi_, stream_);
+    build_plans();
+    return;
+  }
   if (!dx_exact_) {
     if (!Dx_aux_) Dx_aux_ = dalloc<float>(stream_, static_cast<size_t>(n_) * ldn_);
     launch_tf32_aux(Dx_, n_, n_, ldn_, Dx_aux_, mode, stream_);
@@ -371,11 +408,13 @@ void BapgEngine::build_plans() {
     auto planes_of = [](float* base, int64_t plane_elems, int k) {
       return static_cast<void*>(reinterpret_cast<uint16_t*>(base) + k * plane_elems);
     };
-    auto gemm1 = [&](float* X_aux, const int* skip) {
+    auto gemm1 = [&](float* X_aux, const float* bias, const int* skip) {
       GemmDesc d;
       d.M = m_;
       d.N = n_;
       d.K = m_;
+      d.col_bias = center_ ? bias : nullptr;
+      d.rowsums = center_;
       d.bf16_planes = planes;
       d.a_bf16 = Dy_bf_;
       if (split_d()) {
@@ -413,15 +452,16 @@ void BapgEngine::build_plans() {
       d.ldc = ldm_;
       d.skip = skip;
       d.f16 = f16;
+      d.col_bias = center_ ? cb2_ : nullptr;
       if (f16) d.col_scale = f16_g2_cs_;
       d.fuse_planes = !quadratic();
       return gemm_plan_create(d);
     };
     for (int q = 0; q < 2; ++q) {
-      g1_[q][0] = gemm1(W_aux_[q], done);
-      g1_tail_[q] = gemm1(W_aux_[q], flags);
+      g1_[q][0] = gemm1(W_aux_[q], cb1_w_[q], done);
+      g1_tail_[q] = gemm1(W_aux_[q], cb1_w_[q], flags);
     }
-    g1_[0][1] = gemm1(P_aux_, done);
+    g1_[0][1] = gemm1(P_aux_, cb1_pi_, done);
     g1_[1][1] = g1_[0][1];
     g2_ = gemm2(done);
     g2_tail_ = gemm2(flags);
@@ -433,19 +473,28 @@ void BapgEngine::build_plans() {
   const float* ax_lo = nullptr;
   const float* ay = Dy_;
   const float* ay_lo = nullptr;
-  if (!dx_exact_) {
-    if (tf32) ax = Dx_aux_;
-    else ax_lo = Dx_aux_;
+  if (center_) {
+    ax = tf32 ? Dx_aux_ : Dxc_;
+    ax_lo = tf32 ? nullptr : Dx_aux_;
+    ay = tf32 ? Dy_aux_ : Dyc_;
+    ay_lo = tf32 ? nullptr : Dy_aux_;
+  } else {
+    if (!dx_exact_) {
+      if (tf32) ax = Dx_aux_;
+      else ax_lo = Dx_aux_;
+    }
+    if (!dy_exact_) {
+      if (tf32) ay = Dy_aux_;
+      else ay_lo = Dy_aux_;
+    }
   }
-  if (!dy_exact_) {
-    if (tf32) ay = Dy_aux_;
-    else ay_lo = Dy_aux_;
-  }
-  auto gemm1 = [&](float* X, float* X_aux, const int* skip) {
+  auto gemm1 = [&](float* X, float* X_aux, const float* bias, const int* skip) {
     GemmDesc d;
     d.M = m_;
     d.N = n_;
     d.K = m_;
+    d.col_bias = center_ ? bias : nullptr;
+    d.rowsums = center_;
     d.a = ay;
     d.a_lo = ay_lo;
     d.lda = ldm_;
@@ -476,13 +525,14 @@ void BapgEngine::build_plans() {
     d.aux_mode = 0;
     d.skip = skip;
     d.three_pass = !tf32;
+    d.col_bias = center_ ? cb2_ : nullptr;
     return gemm_plan_create(d);
   };
   for (int q = 0; q < 2; ++q) {
-    g1_[q][0] = gemm1(W_[q], W_aux_[q], done);
-    g1_tail_[q] = gemm1(W_[q], W_aux_[q], flags);
+    g1_[q][0] = gemm1(W_[q], W_aux_[q], cb1_w_[q], done);
+    g1_tail_[q] = gemm1(W_[q], W_aux_[q], cb1_w_[q], flags);
   }
-  g1_[0][1] = gemm1(P_, P_aux_, done);
+  g1_[0][1] = gemm1(P_, P_aux_, cb1_pi_, done);
   g1_[1][1] = g1_[0][1];
   g2_ = gemm2(done);
   g2_tail_ = gemm2(flags);
@@ -565,6 +615,7 @@ void BapgEngine::reset(const double* w0_host) {
     }
     launch_iterate_copies(W64_[0], n_, m_, ldm_, needs_copy() ? W_[0] : nullptr,
                           no_planes() ? nullptr : W_aux_[0], aux_mode(), aux_scale(), stream_);
+    if (center_) launch_row_bias64(W64_[0], n_, m_, ldm_, cb1_factor(), cb1_w_[0], stream_);
     parity_ = 0;
     GWB_CUDA(cudaGetLastError());
     return;
@@ -624,6 +675,10 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
                   stream_);
   } else {
     GWB_CUDA(gemm_launch(g1_[q][half_b ? 1 : 0], stream_));
+    if (center_) {
+      GWB_CUDA(gemm_rowsum_bias(g1_[q][half_b ? 1 : 0], cb2_factor(), cb2_, stream_));
+      ++launches;
+    }
     GWB_CUDA(gemm_launch(g2_, stream_));
     launches += gemm_launches(g1_[q][half_b ? 1 : 0]) + gemm_launches(g2_) - 2;
   }
@@ -797,6 +852,7 @@ void BapgEngine::tail() {
                   stream_);
   } else {
     GWB_CUDA(gemm_launch(g1_tail_[parity_], stream_));
+    if (center_) GWB_CUDA(gemm_rowsum_bias(g1_tail_[parity_], cb2_factor(), cb2_, stream_));
     GWB_CUDA(gemm_launch(g2_tail_, stream_));
   }
   launch_row_update(d, false, stream_);

@@ -147,6 +147,20 @@ class BapgEngine {
   // D·2^sd_), for weighted D.
   bool split_d() const { return precision_ == GWB_PREC_F16X3; }
   int sdx_ = 0, sdy_ = 0;
+  // Centred chain for weighted D: the GEMMs run on
+  // D − c·J (c = max D / 2), whose signed terms keep the tensor core's
+  // truncating fp32 accumulation unbiased; the rank-1 parts return as
+  // GEMM biases — GEMM1: c_Y·rowsum(X) per output column (cb1_pi_ for
+  // X = π: c_Y·μ; cb1_w_[q] for X = w_q, written by the column write pass),
+  // GEMM2: c_X·colsum(V) per output column (cb2_, from GEMM1's row sums).
+  bool center_ = false;
+  double ctr_x_ = 0.0, ctr_y_ = 0.0;
+  float *cb1_pi_ = nullptr, *cb1_w_[2] = {nullptr, nullptr}, *cb2_ = nullptr;
+  float *Dxc_ = nullptr, *Dyc_ = nullptr;  // fp32 centred copies (TF32 hi operands)
+  double cb1_factor() const {  // GEMM1 accumulates 2^(s1 + sdy)·(D̃_Y Xᵀ) (f16), else D̃_Y Xᵀ
+    return f16() ? std::ldexp(ctr_y_, f16_s1_ + sdy_) : ctr_y_;
+  }
+  double cb2_factor() const { return f16() ? std::ldexp(ctr_x_, sdx_) : ctr_x_; }
   bool sparse() const { return precision_ == GWB_PREC_SPARSE; }
   bool fp32() const { return precision_ == GWB_PREC_FP32; }
   // Skinny bf16x3 chain (m ≤ 32, exact-bf16 D_X): FP32-pipe GEMM1 writing

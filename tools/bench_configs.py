@@ -54,7 +54,7 @@ def session_rate(inst, iters, prec="auto", warm=3):
     ms = e0.elapsed_time(e1)
     lib.gwb_session_destroy(s)
     return {"it_per_s": iters / (ms * 1e-3), "ms_per_it": ms / iters,
-            "precision": {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2"}[rp.value],
+            "precision": {1: "tf32", 2: "3xtf32", 3: "bf16x3", 4: "bf16x2", 5: "sparse", 6: "fp32", 7: "f16x2", 8: "f16x3"}[rp.value],
             "tflops_alg": fl.value * iters / (ms * 1e-3) / 1e12, "launches": L.value}
 
 
