@@ -749,9 +749,10 @@ def c5_variant(world, rank, local, dist, iters=500, total=4096):
             "note": "problems stop where rel_change crosses the pinned 1e-30, as in the "
                     "reference (149-350 iterations for most); batched it/s = mean iterations "
                     "executed / kernel time",
-            "kernel": "bapg_batched_kernel: one CTA per problem, D/planes in SMEM, pi/w/acc in TMEM",
+            "kernel": "bapg_batched_kernel: one CTA per problem, D and f16x2 planes in SMEM, "
+                      "accumulator / w / pi in TMEM; half-step b on G^T (column lanes)",
             "kernel_ms": ms, "tflops_alg": flops / (ms * 1e-3) / 1e12,
-            "tflops_exec_bf16": 3 * flops / (ms * 1e-3) / 1e12,
+            "tflops_exec_f16": 2 * flops / (ms * 1e-3) / 1e12,
             "e2e": {"value": used / wall, "unit": "batched it/s", "seconds": wall,
                     "h2d_bytes_per_step": r["h2d_bytes"], "d2h_bytes_per_step": r["d2h_bytes"],
                     "note": "one gwb_bapg_solve_batched call from pinned fp64 host buffers "
@@ -963,10 +964,10 @@ def config_rows(args, lib, abi, torch, device, peaks, tf32):
     try:
         rows["c5"] = c5_variant(1, 0, device, None)
         f = 4096 * 4.0 * 128 * 128 * 256
-        P = peaks["bf16_tflops"] / 3
+        P = peaks["bf16_tflops"] / 2
         rows["c5"]["roofline"] = {"its": P * 1e12 / f, "frac": rows["c5"]["value"] / (P * 1e12 / f),
                                   "peak_tflops": P, "peak_source":
-                                  f"bf16 burst {peaks['bf16_tflops']} / 3 planes (bf16x3)",
+                                  f"bf16/fp16 burst {peaks['bf16_tflops']} / 2 planes (f16x2)",
                                   "flops_per_batched_it": f, "model": "T = F_alg / P_exec "
                                   "(operands on-chip: no HBM term)"}
         if not args.no_cpu:

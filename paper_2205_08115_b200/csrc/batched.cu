@@ -4,23 +4,25 @@
 // The reference runs such a batch as independent gw::solve calls from its
 // experiment worker pool (experiment.cpp:273-304); each problem follows
 // bapg_solve (solvers.cpp:138-217).  Here a persistent CTA owns one problem
-// at a time:
-//   SMEM  D_X (GEMM1 A operand) and D_Yᵀ (GEMM2 B operand) as bf16, exact
-//         for 0/1 structure matrices (32 KB each, 128-B swizzled K-major);
-//         one 96 KB buffer holding three bf16 planes of the current GEMM
-//         operand — the iterate X (GEMM1's B, read MN-major) or V = D_X·X
-//         (GEMM2's A), both written row by row by the owning thread; 15 KB
-//         of reduction scratch and the marginals.
-//   TMEM  512 columns: [0,128) accumulator of the hi plane, [128,256) π,
-//         [256,384) w, [384,512) accumulator of the mid+lo planes (split
-//         accumulation).
-// One half-step = GEMM1 (3 planes × 8 MMAs of 128×128×16) → V planes →
-// GEMM2 → row (a) or column (b) normalisation read straight from TMEM (G is
-// folded into one TMEM block, the unnormalised kernel t cached in another),
-// which also writes the next operand planes.  Column statistics use a
-// 32-lane transpose-reduce plus a fixed-order merge of the 4 lane quadrants.  The fp64 diagnostics, trace record
-// and the stop rule are evaluated by the CTA itself; nothing leaves the SM
-// until the problem finishes.
+// at a time.  The two half-steps run in opposite orientations, so every
+// line reduction (row sums in a, column sums in b) is a per-thread loop and
+// no shuffle transposes are needed:
+//   half-step a (lane = row i):    G  = (D_X·X)·D_Y      X = w
+//   half-step b (lane = column j): Gᵀ = D_Y·(D_X·X)ᵀ     X = π
+// The operand planes are written by the lane that owns the line — w by
+// column (K-major B operand), π by row (MN-major B operand) — and the
+// iterates cross between the orientations through one fp32 buffer T[i][j]
+// that every thread reads and overwrites along its own line.
+//   SMEM  D_X, D_Y as fp16 (exact for 0/1 / small-integer D; 32 KB each,
+//         128-B swizzled K-major; D symmetric, so the D_Y tile is both
+//         GEMM2's B and GEMM2ᵀ's A); two fp16 planes (hi, lo) of the current
+//         GEMM operand (X, then V = D_X·X) with power-of-two scales (f16x2,
+//         DESIGN.md §4); T (fp32 128×132); reduction scratch, marginals.
+//   TMEM  accumulator · wᵀ · πᵀ (the unnormalised kernel t stays in
+//         registers: TMEM→register reads, 64 B/clk per SM, are the scarce
+//         resource, so each half-step reads its accumulator once).
+// The fp64 diagnostics, trace record and stop rule are evaluated by the
+// CTA; nothing leaves the SM until the problem finishes.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -49,21 +51,28 @@ double g_last_ms = 0.0;       // gwb_batched_last_kernel_ms
 int64_t g_last_problems = 0;
 
 constexpr int kT = 128;                         // padded problem side
-constexpr int kThreads = 256;                   // 8 warps: 4 lane quadrants × 2 column halves
-constexpr uint32_t kTileBytes = kT * kT * 2;    // one bf16 operand plane (32 KB)
+constexpr int kW = 64;                          // cross-line entries per thread
+constexpr int kH = kT / kW;                     // threads per line (2)
+constexpr int kThreads = 128 * kH;              // 8 warps: 4 lane quadrants × 2 column halves
+// (16 warps with 32 entries each measured 9% slower: the FP32 pipes, not
+// latency, bound the SIMT phases.)
+constexpr uint32_t kTileBytes = kT * kT * 2;    // one fp16 operand plane (32 KB)
 constexpr uint32_t kHalfTile = kTileBytes / 2;  // one 64-wide K chunk (16 KB)
-constexpr uint32_t kAccHi = 0, kPi = 128, kW = 256, kAccLo = 384;  // TMEM columns
-constexpr size_t kScratch = 16 * 1024;
-constexpr size_t kSmem = 1024 + 5 * static_cast<size_t>(kTileBytes) + kScratch;
+constexpr int kTLd = kT + 4;                    // T row pitch (floats): conflict-free rows and columns
+constexpr uint32_t kAcc = 0, kWT = 128, kPT = 256;  // TMEM columns (256 used of 512)
+constexpr size_t kScratch = 12 * 1024;
+constexpr size_t kSmem = 1024 + 4 * static_cast<size_t>(kTileBytes) +
+                         static_cast<size_t>(kT) * kTLd * 4 + kScratch;
 
 struct BatchStatus {
   int flags, err_iter, zero_index, used, converged, pad[3];
 };
 
 struct BatchArgs {
-  const uint8_t* dpack;  // [batch][2][32 KB] pre-swizzled bf16: D_X (A), D_Yᵀ (B)
+  const uint8_t* dpack;  // [batch][2][32 KB] pre-swizzled fp16: D_X, D_Y
   const double* mu;      // [batch][128], zero padded
   const double* nu;
+  const int* scl;        // [batch] s: iterates, X and V planes are held ×2^s
   float* P;              // [batch][128][128] final π
   float* W;              // [batch][128][128] final w
   DevRecord* rec;        // [batch][max_iters + 2] or null
@@ -73,7 +82,7 @@ struct BatchArgs {
   double rel_tol;
 };
 
-// Byte offset of bf16 element (row, k) in a 128×128 K-major operand stored
+// Byte offset of fp16 element (row, k) in a 128×128 K-major operand stored
 // as two 64-wide K chunks, each the canonical 128-B swizzle layout.
 __host__ __device__ __forceinline__ uint32_t sw_off(int row, int k) {
   return static_cast<uint32_t>(k >> 6) * kHalfTile + static_cast<uint32_t>(row) * 128u +
@@ -81,89 +90,72 @@ __host__ __device__ __forceinline__ uint32_t sw_off(int row, int k) {
          (static_cast<uint32_t>(k & 7) << 1);
 }
 
-// Two fp32 values → three packed bf16x2 planes whose sum is exact
-// (hi = rn(x), mid = rn(x − hi), lo = rn(x − hi − mid)).  One F2FP per plane
-// pair; a bf16 is the upper half of the fp32 with the same value.
-__device__ __forceinline__ uint32_t cvt_bf16x2(float lo_elem, float hi_elem) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
-  return r;
-}
-__device__ __forceinline__ void split3x2(float a, float b, uint32_t& p0, uint32_t& p1,
-                                         uint32_t& p2) {
-  p0 = cvt_bf16x2(a, b);
-  a -= __uint_as_float(p0 << 16);
-  b -= __uint_as_float(p0 & 0xFFFF0000u);
-  p1 = cvt_bf16x2(a, b);
-  a -= __uint_as_float(p1 << 16);
-  b -= __uint_as_float(p1 & 0xFFFF0000u);
-  p2 = cvt_bf16x2(a, b);
+// Two fp32 values (already in fp16 range) → hi and lo fp16x2 planes,
+// hi = rn(x), lo = rn(x − hi) (22-bit operand, DESIGN.md §4 f16x2).
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+  const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+  const float ra = a - hf.x, rb = b - hf.y;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(rb), "f"(ra));
 }
 
-// Transpose-reduce: lane l holds v[0..31] (one row, 32 columns); afterwards
-// v[0] of lane l is op over all 32 lanes of column l.  31 shuffles, fixed
-// combination order (deterministic).
-template <class T, class Op>
-__device__ __forceinline__ T xreduce32(T (&v)[32], int lane, Op op) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool upper = (lane & s) != 0;
-#pragma unroll
-    for (int k = 0; k < s; ++k) {
-      const T send = upper ? v[k] : v[k + s];
-      const T keep = upper ? v[k + s] : v[k];
-      const T recv = __shfl_xor_sync(0xffffffffu, send, s);
-      v[k] = op(keep, recv);
-    }
-  }
-  return v[0];
-}
-
-struct FMax {
-  __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
-};
-struct FAdd {
-  __device__ float operator()(float a, float b) const { return a + b; }
-};
-struct DAdd {
-  __device__ double operator()(double a, double b) const { return a + b; }
-};
-
-// Operand packing: fp64 column-major inputs → bf16 swizzled tiles, the
-// bf16-exactness check and zero-padded fp64 marginals.
+// Operand packing: fp64 column-major inputs → fp16 swizzled tiles, the
+// fp16-exactness check, zero-padded fp64 marginals and the power-of-two
+// scale s = 14 − ⌈log2(x_max · max(1, max_i Σ_k |D_X[i][k]|))⌉: x_max =
+// max(max μ, max ν) bounds every iterate entry (π_kl ≤ μ_k, w_kl ≤ ν_l) and
+// x_max·Σ_k|D_X[i][k]| every entry of V = D_X·X, so X·2^s and V·2^s both
+// stay inside fp16's range and GEMM1's accumulator is V's operand as is.
 __global__ void batched_pack_kernel(const double* __restrict__ dx, const double* __restrict__ dy,
                                     const double* __restrict__ mu, const double* __restrict__ nu,
                                     int n, int m, uint8_t* __restrict__ dpack,
                                     double* __restrict__ mu_p, double* __restrict__ nu_p,
-                                    int* inexact) {
+                                    int* __restrict__ scl, int* inexact) {
   const int64_t b = blockIdx.x;
-  const int op = blockIdx.y;  // 0: D_X as A[i][k];  1: D_Yᵀ as B[j][k] = D_Y(k, j)
+  const int op = blockIdx.y;  // 0: D_X, 1: D_Y
   const int dim = op == 0 ? n : m;
   const double* src = (op == 0 ? dx : dy) + b * static_cast<int64_t>(dim) * dim;
-  __nv_bfloat16* dst =
-      reinterpret_cast<__nv_bfloat16*>(dpack + (b * 2 + op) * static_cast<int64_t>(kTileBytes));
+  __half* dst = reinterpret_cast<__half*>(dpack + (b * 2 + op) * static_cast<int64_t>(kTileBytes));
   bool bad = false;
   for (int idx = threadIdx.x; idx < kT * kT; idx += blockDim.x) {
     // idx = c·128 + r walks the column-major source contiguously.
     const int c = idx / kT, r = idx % kT;
     double v = 0.0;
     if (r < dim && c < dim) v = src[static_cast<int64_t>(c) * dim + r];
-    const __nv_bfloat16 h = __float2bfloat16_rn(static_cast<float>(v));
-    if (static_cast<double>(__bfloat162float(h)) != v) bad = true;
-    // op 0: element (row r, col c) of D_X → A[r][c];  op 1: D_Y(r, c) → B[c][r].
-    const uint32_t off = op == 0 ? sw_off(r, c) : sw_off(c, r);
-    dst[off / 2] = h;
+    const __half hv = __double2half(v);
+    if (static_cast<double>(__half2float(hv)) != v) bad = true;
+    dst[sw_off(r, c) / 2] = hv;
   }
   if (bad) atomicOr(inexact, 1);
-  if (op == 0 && threadIdx.x < kT) {
-    mu_p[b * kT + threadIdx.x] = threadIdx.x < n ? mu[b * n + threadIdx.x] : 0.0;
-    nu_p[b * kT + threadIdx.x] = threadIdx.x < m ? nu[b * m + threadIdx.x] : 0.0;
+  if (op != 0) return;
+  __shared__ double s_deg[kT], s_x[kT];
+  const int t = threadIdx.x;
+  if (t < kT) {
+    double deg = 0.0;
+    if (t < n)
+      for (int c = 0; c < n; ++c) deg += fabs(src[static_cast<int64_t>(c) * n + t]);
+    s_deg[t] = deg;
+    const double a = t < n ? mu[b * n + t] : 0.0;
+    const double w = t < m ? nu[b * m + t] : 0.0;
+    mu_p[b * kT + t] = a;
+    nu_p[b * kT + t] = w;
+    s_x[t] = fmax(fabs(a), fabs(w));
+  }
+  __syncthreads();
+  if (t == 0) {
+    double deg = 1.0, x = 0.0;
+    for (int k = 0; k < kT; ++k) {
+      deg = fmax(deg, s_deg[k]);
+      x = fmax(x, s_x[k]);
+    }
+    const double vb = x * deg;
+    const int sv = vb > 0.0 ? 14 - static_cast<int>(ceil(log2(vb))) : 0;
+    scl[b] = max(-100, min(100, sv));
   }
 }
 
-// UMMA descriptor of GEMM1's B operand, the iterate X[k = i][n = j] stored
-// row-major in the same swizzled tiles as sw_off(i, j): MN-major, 64-wide N
-// blocks LBO = 16 KB apart, 8-row K groups SBO = 1024 B apart, 128-B swizzle.
+// UMMA descriptor of GEMM1's B operand π[k = i][n = j] stored row-major in
+// the same swizzled tiles as sw_off(i, j): MN-major, 64-wide N blocks
+// LBO = 16 KB apart, 8-row K groups SBO = 1024 B apart, 128-B swizzle.
 __device__ __forceinline__ uint64_t desc_mn(uint32_t addr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((addr >> 4) & 0x3FFFu);
@@ -174,34 +166,71 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t addr) {
   return d;
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Line sums of a thread's kW fp32 terms as 8-term fp32 partials added in
+// fp64 (short independent chains; the normalisers and record sums keep
+// ~1e-7 relative accuracy instead of a long fp32 chain's).  f(t) is the term.
+template <class F>
+__device__ __forceinline__ double sumw(F f) {
+  constexpr int G = kW / 8;
+  float p[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    p[g] = f(8 * g);
+#pragma unroll
+    for (int u = 1; u < 8; ++u) p[g] += f(8 * g + u);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) s += static_cast<double>(p[g]);
+  return s;
+}
+// Σ a_t·b_t the same way, as fused multiply-adds.
+template <class FA, class FB>
+__device__ __forceinline__ double dotw(FA fa, FB fb) {
+  constexpr int G = kW / 8;
+  float p[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    p[g] = fa(8 * g) * fb(8 * g);
+#pragma unroll
+    for (int u = 1; u < 8; ++u) p[g] = fmaf(fa(8 * g + u), fb(8 * g + u), p[g]);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) s += static_cast<double>(p[g]);
+  return s;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sD = smem;                    // D_X | D_Yᵀ
-  uint8_t* sPl = smem + 2 * kTileBytes;  // 3 operand planes
-  float* red_f = reinterpret_cast<float*>(sPl + 3 * kTileBytes);  // [4][128]
-  double* red_d = reinterpret_cast<double*>(red_f + 4 * kT);      // [4][128]
-  float* col_c = reinterpret_cast<float*>(red_d + 4 * kT);        // [128]
-  float* col_s = col_c + kT;                                      // [128]
-  float* row_x = col_s + kT;                                      // [2][128]
-  double* row_d = reinterpret_cast<double*>(row_x + 2 * kT);      // [2][128][2]
-  double* diag = row_d + 4 * kT;                                  // [8][8]
-  double* s_mu = diag + 64;                                       // [128]
-  double* s_nu = s_mu + kT;                                       // [128]
-  int* ctl = reinterpret_cast<int*>(s_nu + kT);                   // flags, zero_index, stop
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ctl + 8);          // load, mma
+  uint8_t* sD = smem;                                                // D_X | D_Y
+  uint8_t* sPl = smem + 2 * kTileBytes;                              // hi | lo planes
+  float* T = reinterpret_cast<float*>(sPl + 2 * kTileBytes);         // [128][kTLd]
+  float* red_m = T + kT * kTLd;                                      // [kH][128] line maxima
+  double* red_d = reinterpret_cast<double*>(red_m + kH * kT);        // [3][kH][128] line sums
+  double* diag = red_d + 3 * kH * kT;                                // [16][8]
+  double* s_mu = diag + 8 * (kThreads / 32);                         // [128]
+  double* s_nu = s_mu + kT;                                          // [128]
+  int* ctl = reinterpret_cast<int*>(s_nu + kT);                      // flags, zero_index, stop
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ctl + 8);             // load, mma
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
-  const int i = q * 32 + lane;  // row owned (TMEM lane)
-  const int c0 = h * 64;        // first of the 64 columns owned
+  const int L = q * 32 + lane;  // line owned: row i (half-step a) or column j (b); TMEM lane
+  const int c0 = h * kW;        // first of the kW cross-line entries owned
   const int n = a.n, m = a.m;
-  const bool row_ok = i < n;
   const float inv_rho = a.inv_rho;
 
-  if (warp == 0) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == 0) ptx::tmem_alloc<256>(tmem_slot);
   if (tid == 0) {
     ptx::mbar_init(&bars[0], 1);
     ptx::mbar_init(&bars[1], 1);
@@ -214,67 +243,68 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
   const uint32_t tl = tbase + (static_cast<uint32_t>(q * 32) << 16);  // this warp's lanes
   const uint32_t sD_a = ptx::smem_u32(sD), sPl_a = ptx::smem_u32(sPl);
   uint32_t load_ph = 0, mma_ph = 0;
+  // Operand row L, k-chunks of this thread's entries: sw_off(L, c0 + 8c) =
+  // (c0 / 64)·16 KB + 128·L + (((c0 / 8 + c) & 7) ^ (L & 7)) << 4.
+  uint8_t* const pl_row = sPl + (c0 >> 6) * kHalfTile + L * 128;
+  const int xg = ((c0 >> 3) & 7) ^ (L & 7);
 
-  // TMEM loads are issued back to back and waited once per phase.
-  auto ld = [&](uint32_t col, uint32_t (&r)[32]) { ptx::tmem_ld_32x32b_x32(tl + col, r); };
-  auto load_cols = [&](uint32_t col, float (&v)[32]) {
-    uint32_t r[32];
-    ptx::tmem_ld_32x32b_x32(tl + col, r);
+  // kW columns of this warp's lanes from / to TMEM, 32 columns per access.
+  auto ldw = [&](uint32_t col, float (&v)[kW]) {
+    uint32_t r[kW];
+#pragma unroll
+    for (int c = 0; c < kW; c += 32) ptx::tmem_ld_32x32b_x32(tl + col + c, *reinterpret_cast<uint32_t(*)[32]>(r + c));
     ptx::tmem_wait_ld();
 #pragma unroll
-    for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(r[t]);
+    for (int t = 0; t < kW; ++t) v[t] = __uint_as_float(r[t]);
   };
-  // G chunk from the split accumulators (hi plane + mid/lo planes).
-  auto load_acc = [&](int g, float (&v)[32]) {
-    uint32_t hi[32];
-    ptx::tmem_ld_32x32b_x32(tl + kAccHi + c0 + 32 * g, hi);
-    ptx::tmem_wait_ld();
+  auto st = [&](uint32_t col, const float (&v)[kW]) {
 #pragma unroll
-    for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(hi[t]);
-  };
-  auto store_cols = [&](uint32_t col, const float (&v)[32]) {
-    uint32_t r[32];
+    for (int c = 0; c < kW; c += 32) {
+      uint32_t r[32];
 #pragma unroll
-    for (int t = 0; t < 32; ++t) r[t] = __float_as_uint(v[t]);
-    ptx::tmem_st_32x32b_x32(tl + col, r);
-  };
-  // Row i, columns [col, col+32) of the next GEMM operand as bf16x3 planes.
-  auto store_planes = [&](const float (&v)[32], int col) {
-#pragma unroll
-    for (int c8 = 0; c8 < 4; ++c8) {
-      uint32_t pk[3][4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        split3x2(v[c8 * 8 + 2 * e], v[c8 * 8 + 2 * e + 1], pk[0][e], pk[1][e], pk[2][e]);
-      const uint32_t off = sw_off(i, col + 8 * c8);
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-        *reinterpret_cast<uint4*>(sPl + p * kTileBytes + off) =
-            make_uint4(pk[p][0], pk[p][1], pk[p][2], pk[p][3]);
+      for (int t = 0; t < 32; ++t) r[t] = __float_as_uint(v[c + t]);
+      ptx::tmem_st_32x32b_x32(tl + col + c, r);
     }
   };
-  // GEMM1: V = D_X · X (A = D_X K-major, B = X planes MN-major);
-  // GEMM2: G = V · D_Y (A = V planes K-major, B = D_Yᵀ K-major).
-  // Plane 0 accumulates into kAccHi, planes 1-2 into kAccLo.
-  auto issue = [&](bool gemm1) {
+  // This thread's entries [c0, c0 + kW) of line L (scaled units, inside fp16
+  // range) as the two fp16 planes of operand row L.
+  auto store_planes = [&](const float (&v)[kW]) {
+#pragma unroll
+    for (int c8 = 0; c8 < kW / 8; ++c8) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split_f16x2(v[c8 * 8 + 2 * e], v[c8 * 8 + 2 * e + 1], hi[e], lo[e]);
+      uint8_t* p = pl_row + ((xg ^ c8) << 4);
+      *reinterpret_cast<uint4*>(p) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(p + kTileBytes) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  };
+  // MMA issue (one thread).  GEMM1: V = D_X·X, B = X planes, K-major (X = w,
+  // written by columns) or MN-major (X = π, written by rows).  GEMM2: G =
+  // V·D_Y (A = V planes, B = D_Y) or Gᵀ = D_Y·Vᵀ (A = D_Y, B = V planes).
+  // Smallest plane first into one accumulator: the accumulator's truncation
+  // acts on the hi-plane terms only.
+  auto issue = [&](int kind) {  // 0: GEMM1 K-major X, 1: GEMM1 MN-major X, 2: G, 3: Gᵀ
     ptx::tc_fence_after();
-    constexpr uint32_t id1 = ptx::idesc_bf16(128, 128) | (1u << 16);  // B MN-major
-    constexpr uint32_t id2 = ptx::idesc_bf16(128, 128);
-    // One accumulator, smallest plane first (lo, mid, hi): the small terms
-    // are summed while the running sum is small, so the accumulator's
-    // truncation acts on the 128 hi-plane terms only — the same bound as a
-    // separate hi accumulator.
+    const uint32_t idesc = ptx::idesc_f16(128, 128) | (kind == 1 ? (1u << 16) : 0u);
 #pragma unroll 1
-    for (int pi = 0; pi < 3; ++pi) {
-      const int p = 2 - pi;
-      const uint32_t d = tbase + kAccHi;
-      const uint32_t pl = sPl_a + p * kTileBytes;
+    for (int pi = 0; pi < 2; ++pi) {
+      const uint32_t pl = sPl_a + (1 - pi) * kTileBytes;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {  // K = 128 in steps of 16
         const uint32_t koff = (kk >> 2) * kHalfTile + (kk & 3) * 32;
-        const uint64_t ad = ptx::umma_desc_sw128(gemm1 ? sD_a + koff : pl + koff);
-        const uint64_t bd = gemm1 ? desc_mn(pl + kk * 2048) : ptx::umma_desc_sw128(sD_a + kTileBytes + koff);
-        ptx::mma_bf16(d, ad, bd, gemm1 ? id1 : id2, (pi || kk) ? 1u : 0u);
+        uint64_t ad, bd;
+        if (kind <= 1) {
+          ad = ptx::umma_desc_sw128(sD_a + koff);
+          bd = kind == 1 ? desc_mn(pl + kk * 2048) : ptx::umma_desc_sw128(pl + koff);
+        } else if (kind == 2) {
+          ad = ptx::umma_desc_sw128(pl + koff);
+          bd = ptx::umma_desc_sw128(sD_a + kTileBytes + koff);
+        } else {
+          ad = ptx::umma_desc_sw128(sD_a + kTileBytes + koff);
+          bd = ptx::umma_desc_sw128(pl + koff);
+        }
+        ptx::mma_bf16(tbase + kAcc, ad, bd, idesc, (pi || kk) ? 1u : 0u);
       }
     }
     ptx::mma_commit(&bars[1]);
@@ -283,26 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
     ptx::mbar_wait(&bars[1], mma_ph);
     mma_ph ^= 1;
     ptx::tc_fence_after();
-  };
-  // G = D_X · X · D_Y for the X in the operand planes; V = D_X·X is re-split
-  // into bf16x3 planes in between.  Result in the two accumulators.
-  auto chain = [&]() {
-    ptx::fence_proxy_async();
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) issue(true);
-    mma_sync();
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
-      float v[32];
-      load_acc(g, v);
-      store_planes(v, c0 + 32 * g);
-    }
-    ptx::fence_proxy_async();
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) issue(false);
-    mma_sync();
   };
   // Block sum of up to 8 doubles per thread (fixed order); result on thread 0.
   auto block_sum8 = [&](double (&v)[8], int cnt) {
@@ -319,10 +329,26 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       }
     __syncthreads();
   };
+  // Line max over the kH threads of a line, in order.
+  auto line_max = [&](float v) {
+    red_m[h * kT + L] = v;
+    __syncthreads();
+    float r = red_m[L];
+#pragma unroll
+    for (int hh = 1; hh < kH; ++hh) r = fmaxf(r, red_m[hh * kT + L]);
+    return r;
+  };
+  // Line sum of slot `k` of red_d over the kH threads, in order.
+  auto line_sum = [&](int k) {
+    double r = red_d[(k * kH) * kT + L];
+#pragma unroll
+    for (int hh = 1; hh < kH; ++hh) r += red_d[(k * kH + hh) * kT + L];
+    return r;
+  };
 
-  // Zero padding (rows ≥ n, columns ≥ m of D, π, w) keeps every padded
-  // entry at 0 through the updates: G ≥ 0 there is never above a true
-  // maximum, t = 0·e^{≤0} = 0, and the padded scales are forced to 0.
+  // Zero padding (lines ≥ n / m, D beyond its side) keeps every padded entry
+  // at 0 through the updates: G ≥ 0 there is never above a true maximum,
+  // t = 0·e^{≤0} = 0, and the padded scales are forced to 0.
   for (int b = blockIdx.x; b < a.batch; b += gridDim.x) {
     DevRecord* rec = a.rec ? a.rec + static_cast<int64_t>(b) * (a.max_iters + 2) : nullptr;
     if (tid == 0) {
@@ -338,104 +364,110 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       s_mu[tid] = a.mu[static_cast<int64_t>(b) * kT + tid];
       s_nu[tid] = a.nu[static_cast<int64_t>(b) * kT + tid];
     }
+    // Scaled units: π̂ = π·2^s, ŵ = w·2^s (exact), so GEMM1's accumulator is
+    // V̂ = V·2^s and GEMM2's 2^s·G; every record sum is rescaled in fp64.
+    const int sc = a.scl[b];
+    const float up = ldexpf(1.0f, sc);
+    const double un64 = ldexp(1.0, -sc), un2_64 = ldexp(1.0, -2 * sc);
+    const float g_true = ldexpf(1.0f, -sc) * inv_rho;  // raw accumulator → G/ρ
+    // exp(G/ρ − r) = 2^(acc·k2 − r·k2), k2 = 2^−s/ρ·log2 e.
+    const float k2 = g_true * 1.4426950408889634f;
     const unsigned long long t0 = globaltimer();
     __syncthreads();
-    // w⁰ = μνᵀ in fp32 (product_coupling_kernel, kernels.cu).
+    // TMEM reads are the scarce resource (64 B/clk per SM): each half-step
+    // reads its accumulator once into registers (x = this thread's entries
+    // [c0, c0 + kW) of its line) and keeps the kernel t there.
+    float x[kW];
+    // ŵ⁰ = (μνᵀ)·2^s in fp32 (product_coupling_kernel), held column-wise
+    // (lane j = L): TMEM wᵀ, T[i][j] and the K-major planes of GEMM1's B.
     {
-      const float mu_i = static_cast<float>(s_mu[i]);
-#pragma unroll 1
-      for (int g = 0; g < 2; ++g) {
-        float wv[32];
+      const float nu_j = static_cast<float>(s_nu[L]);
 #pragma unroll
-        for (int t = 0; t < 32; ++t) wv[t] = mu_i * static_cast<float>(s_nu[c0 + 32 * g + t]);
-        store_cols(kW + c0 + 32 * g, wv);
-        store_planes(wv, c0 + 32 * g);
+      for (int t = 0; t < kW; ++t) {
+        x[t] = (static_cast<float>(s_mu[c0 + t]) * up) * nu_j;
+        T[(c0 + t) * kTLd + L] = x[t];
       }
+      st(kWT + c0, x);
+      store_planes(x);
       ptx::tmem_wait_st();
     }
     ptx::mbar_wait(&bars[0], load_ph);
     load_ph ^= 1;
 
+    auto load_acc = [&]() { ldw(kAcc + c0, x); };
+    auto acc_max = [&]() {
+      float m4[4] = {0.f, 0.f, 0.f, 0.f};  // G ≥ 0
+#pragma unroll
+      for (int t = 0; t < kW; ++t) m4[t & 3] = fmaxf(m4[t & 3], x[t]);
+      return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    };
+
     int k = 1, phase = 0, used = 0, converged = 0, err_iter = 0;
     for (;;) {
-      chain();
+      // ---- chain: V̂ = D_X·X̂ → planes → G (a) or Gᵀ (b), ×2^s, in kAcc.
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncthreads();
+      if (tid == 0) issue(phase == 1 ? 1 : 0);
+      mma_sync();
+      load_acc();
+      store_planes(x);
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      __syncthreads();
+      if (tid == 0) issue(phase == 1 ? 3 : 2);
+      mma_sync();
+      load_acc();  // x = 2^s·G (row L) or 2^s·Gᵀ (column L)
+
       if (phase != 1) {
-        // ---- half-step a (phase 0) / tail (phase 2): rows of G against w.
-        float rmax = -INFINITY;
-        double gw = 0.0, rw = 0.0;
-#pragma unroll 1
-        for (int g = 0; g < 2; ++g) {
-          uint32_t ha[32], wr[32];
-          ld(kAccHi + c0 + 32 * g, ha);
-          ld(kW + c0 + 32 * g, wr);
-          ptx::tmem_wait_ld();
-          float gv[32], wv[32];
+        // ---- half-step a (phase 0) / tail (phase 2), lane = row i = L ----
+        const bool row_ok = L < n;
+        const float rmax = line_max(acc_max());
+        const float rr = rmax * k2;
+        // t̂ = ŵ ⊙ e^{G/ρ − r} (into x), Ŝ = Σ_j t̂; ⟨G, w⟩ and Σ_j w for the
+        // previous record.  ŵ is row L of T.
+        float* Trow = T + L * kTLd + c0;
+        float wv[kW];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            gv[t] = __uint_as_float(ha[t]);
-            wv[t] = __uint_as_float(wr[t]);
-          }
-          float gwf = 0.f;
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            rmax = fmaxf(rmax, gv[t] * inv_rho);
-            gwf = fmaf(gv[t], wv[t], gwf);
-            rw += static_cast<double>(wv[t]);
-          }
-          gw += static_cast<double>(gwf);
+        for (int t = 0; t < kW; t += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(Trow + t);
+          wv[t] = w4.x;
+          wv[t + 1] = w4.y;
+          wv[t + 2] = w4.z;
+          wv[t + 3] = w4.w;
         }
-        row_x[h * kT + i] = rmax;
-        row_d[(h * kT + i) * 2 + 0] = gw;
-        row_d[(h * kT + i) * 2 + 1] = rw;
+        const double gw = dotw([&](int t) { return x[t]; }, [&](int t) { return wv[t]; });
+        const double rw = sumw([&](int t) { return wv[t]; });
+#pragma unroll
+        for (int t = 0; t < kW; ++t) x[t] = wv[t] * ex2(fmaf(x[t], k2, -rr));
+        const double S = sumw([&](int t) { return x[t]; });
+        red_d[(0 * kH + h) * kT + L] = S;
+        red_d[(1 * kH + h) * kT + L] = gw;
+        red_d[(2 * kH + h) * kT + L] = rw;
         __syncthreads();
         double ra[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (h == 0 && row_ok) {
-          ra[0] = row_d[i * 2 + 0] + row_d[(kT + i) * 2 + 0];
-          const double dv = row_d[i * 2 + 1] + row_d[(kT + i) * 2 + 1] - s_mu[i];
+          ra[0] = line_sum(1) * un2_64;
+          const double dv = line_sum(2) * un64 - s_mu[L];
           ra[1] = dv * dv;
         }
         if (phase == 0) {
-          // π = diag(μ / S) (w ⊙ e^{G/ρ − r}),  S = Σ_j w e^{G/ρ − r}
-          ptx::tmem_wait_st();
-          const float r = fmaxf(row_x[i], row_x[kT + i]);
-          float S = 0.f;
-#pragma unroll 1
-          for (int g = 0; g < 2; ++g) {
-            uint32_t gr[32], wr[32];
-            ld(kAccHi + c0 + 32 * g, gr);
-            ld(kW + c0 + 32 * g, wr);
-            ptx::tmem_wait_ld();
-            float gv[32];
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              gv[t] = __uint_as_float(wr[t]) * __expf(__uint_as_float(gr[t]) * inv_rho - r);
-              S += gv[t];
-            }
-            store_cols(kPi + c0 + 32 * g, gv);
-          }
-          __syncthreads();  // row_x (max) reads complete before reuse
-          row_x[h * kT + i] = S;
-          __syncthreads();
-          const float St = row_x[i] + row_x[kT + i];
+          const double St = line_sum(0);
           if (h == 0 && row_ok) {
-            if (r > 700.0f) atomicOr(&ctl[0], kFlagOverflowA);
-            if (!(St > 0.0f) || !isfinite(St) || isnan(r)) {
+            if (rmax * g_true > 700.0f) atomicOr(&ctl[0], kFlagOverflowA);
+            if (!(St > 0.0) || !isfinite(St) || isnan(rmax)) {
               atomicOr(&ctl[0], kFlagZeroA);
-              atomicMin(&ctl[1], i);
+              atomicMin(&ctl[1], L);
             }
           }
-          const float scale = row_ok ? static_cast<float>(s_mu[i] / static_cast<double>(St)) : 0.f;
-          ptx::tmem_wait_st();
-#pragma unroll 1
-          for (int g = 0; g < 2; ++g) {
-            float pv[32];
-            load_cols(kPi + c0 + 32 * g, pv);
+          // π̂ = t̂ · μ_i 2^s / Ŝ: row i of T and the MN-major planes of GEMM1's B.
+          const float scale = row_ok ? static_cast<float>(s_mu[L] * static_cast<double>(up) / St) : 0.f;
 #pragma unroll
-            for (int t = 0; t < 32; ++t) pv[t] *= scale;
-            store_cols(kPi + c0 + 32 * g, pv);
-            store_planes(pv, c0 + 32 * g);
-          }
-          ptx::tmem_wait_st();
+          for (int t = 0; t < kW; ++t) x[t] *= scale;
+#pragma unroll
+          for (int t = 0; t < kW; t += 4)
+            *reinterpret_cast<float4*>(Trow + t) = make_float4(x[t], x[t + 1], x[t + 2], x[t + 3]);
+          store_planes(x);
         }
         block_sum8(ra, 2);
         if (phase == 2) {
@@ -456,121 +488,85 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         phase = 1;
         continue;
       }
-      // ---- half-step b: w' = (π ⊙ e^{G/ρ − c}) diag(ν / C) -----------------
-      // B1: fold G, column max over rows.
-#pragma unroll 1
-      for (int g = 0; g < 2; ++g) {
-        float gv[32];
-        load_acc(g, gv);
+      // ---- half-step b, lane = column j = L: w' = (π ⊙ e^{G/ρ − c}) ν_j / C_j.
+      const bool col_ok = L < m;
+      const float cmax = line_max(acc_max());
+      const float cr = cmax * k2;
+      // t̂ = π̂ e^{G/ρ − c} (into x); Ĉ = Σ_i t̂, Σ_i π̂, ⟨G, π⟩ and Σ_i G t̂ (so
+      // ⟨G, w'⟩ = s_j Σ_i G t̂ needs no second accumulator read).  π̂ is
+      // column L of T; it also goes to TMEM for the final output.
+      double gp, gt;
+      {
+        float pv[kW];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) gv[t] *= inv_rho;
-        const float cm = xreduce32(gv, lane, FMax{});
-        red_f[q * kT + c0 + 32 * g + lane] = cm;
-      }
-      __syncthreads();
-      if (tid < kT) {
-        float c = red_f[tid];
-        for (int qq = 1; qq < 4; ++qq) c = fmaxf(c, red_f[qq * kT + tid]);
-        col_c[tid] = c;
-      }
-      ptx::tmem_wait_st();
-      __syncthreads();
-      // B2: t = π e^{G/ρ − c} (kept in kAccLo); column sums of t (fp32) and π (fp64).
-#pragma unroll 1
-      for (int g = 0; g < 2; ++g) {
-        uint32_t gr[32], pr[32];
-        ld(kAccHi + c0 + 32 * g, gr);
-        ld(kPi + c0 + 32 * g, pr);
-        ptx::tmem_wait_ld();
-        float gv[32];
-        double pd[32];
+        for (int t = 0; t < kW; ++t) pv[t] = T[(c0 + t) * kTLd + L];
+        const double P = sumw([&](int t) { return pv[t]; });
+        gp = dotw([&](int t) { return x[t]; }, [&](int t) { return pv[t]; });
+        float tv[kW];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float pv = __uint_as_float(pr[t]);
-          gv[t] = pv * __expf(__uint_as_float(gr[t]) * inv_rho - col_c[c0 + 32 * g + t]);
-          pd[t] = static_cast<double>(pv);
-        }
-        store_cols(kAccLo + c0 + 32 * g, gv);
-        const float cs = xreduce32(gv, lane, FAdd{});
-        const double ps = xreduce32(pd, lane, DAdd{});
-        red_f[q * kT + c0 + 32 * g + lane] = cs;
-        red_d[q * kT + c0 + 32 * g + lane] = ps;
+        for (int t = 0; t < kW; ++t) tv[t] = pv[t] * ex2(fmaf(x[t], k2, -cr));
+        gt = dotw([&](int t) { return x[t]; }, [&](int t) { return tv[t]; });
+#pragma unroll
+        for (int t = 0; t < kW; ++t) x[t] = tv[t];
+        const double C = sumw([&](int t) { return x[t]; });
+        st(kPT + c0, pv);
+        red_d[(0 * kH + h) * kT + L] = C;
+        red_d[(1 * kH + h) * kT + L] = P;
       }
       __syncthreads();
       double dsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // gw, split, diff, wold, gp, coldev
-      if (tid < kT) {
-        const int j = tid;
-        float C = red_f[j];
-        double P = red_d[j];
-        for (int qq = 1; qq < 4; ++qq) {
-          C += red_f[qq * kT + j];
-          P += red_d[qq * kT + j];
+      const double Ct = line_sum(0);
+      if (col_ok && h == 0) {
+        if (cmax * g_true > 700.0f) atomicOr(&ctl[0], kFlagOverflowB);
+        if (!(Ct > 0.0) || !isfinite(Ct) || isnan(cmax)) {
+          atomicOr(&ctl[0], kFlagZeroB);
+          atomicMin(&ctl[1], L);
         }
-        if (j < m) {
-          const float c = col_c[j];
-          if (c > 700.0f) atomicOr(&ctl[0], kFlagOverflowB);
-          if (!(C > 0.0f) || !isfinite(C) || isnan(c)) {
-            atomicOr(&ctl[0], kFlagZeroB);
-            atomicMin(&ctl[1], j);
-          }
-          col_s[j] = static_cast<float>(s_nu[j] / static_cast<double>(C));
-          const double dv = P - s_nu[j];
-          dsum[5] = dv * dv;
-        } else {
-          col_s[j] = 0.f;
-        }
+        const double dv = line_sum(1) * un64 - s_nu[L];
+        dsum[5] = dv * dv;
       }
+      const float sj = col_ok ? static_cast<float>(s_nu[L] * static_cast<double>(up) / Ct) : 0.f;
       ptx::tmem_wait_st();
       __syncthreads();
       if (ctl[0] != 0) {
         err_iter = used = k;
         break;
       }
-      // B3: w', fused diagnostics, next operand planes.
-      bool finite = true;
-#pragma unroll 1
-      for (int g = 0; g < 2; ++g) {
-        uint32_t gr[32], pr[32], wr[32], tr[32];
-        ld(kAccHi + c0 + 32 * g, gr);
-        ld(kPi + c0 + 32 * g, pr);
-        ld(kW + c0 + 32 * g, wr);
-        ld(kAccLo + c0 + 32 * g, tr);
-        ptx::tmem_wait_ld();
-        float tv[32];
-#define gv(t) __uint_as_float(gr[t])
-#define pv(t) __uint_as_float(pr[t])
-#define wv(t) __uint_as_float(wr[t])
-        float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+      // ŵ' = sj t̂ (into x); fused diagnostics; ŵ'ᵀ → TMEM, column L of T,
+      // K-major planes.  The old ŵ comes from TMEM, π̂ from T.
+      double f1, f3, dd;
+      {
+        float wo[kW];
+        ldw(kWT + c0, wo);
+#pragma unroll
+        for (int t = 0; t < kW; ++t) x[t] *= sj;
+        f3 = dotw([&](int t) { return wo[t]; }, [&](int t) { return wo[t]; });
         // ‖w' − w‖² in fp64: near convergence the changes are off-support
         // entries of 1e-31 and below (the pinned rel_tol = 1e-30 is crossed
         // there, as in the reference, solvers.cpp:191,208), whose squares
         // underflow fp32.
-        double dd = 0.0;
+        double d2[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float o = col_s[c0 + 32 * g + t] * __uint_as_float(tr[t]);
-          finite = finite && isfinite(o);
-          f[0] = fmaf(gv(t), o, f[0]);
-          const float sp = pv(t) - o;
-          f[1] = fmaf(sp, sp, f[1]);
-          const double df = static_cast<double>(o) - static_cast<double>(wv(t));
-          dd = __fma_rn(df, df, dd);
-          f[3] = fmaf(wv(t), wv(t), f[3]);
-          f[4] = fmaf(gv(t), pv(t), f[4]);
-          tv[t] = o;
+        for (int t = 0; t < kW; ++t) {
+          const double df = static_cast<double>(x[t] - wo[t]);
+          d2[t & 3] = __fma_rn(df, df, d2[t & 3]);
         }
-#undef gv
-#undef pv
-#undef wv
-        f[2] = 0.f;
+        dd = (d2[0] + d2[1]) + (d2[2] + d2[3]);
 #pragma unroll
-        for (int s = 0; s < 5; ++s) dsum[s] += static_cast<double>(f[s]);
-        dsum[2] += dd;
-        store_cols(kW + c0 + 32 * g, tv);
-        store_planes(tv, c0 + 32 * g);
+        for (int t = 0; t < kW; ++t) {
+          wo[t] = T[(c0 + t) * kTLd + L] - x[t];  // π̂ − ŵ'
+          T[(c0 + t) * kTLd + L] = x[t];
+        }
+        f1 = dotw([&](int t) { return wo[t]; }, [&](int t) { return wo[t]; });
       }
+      st(kWT + c0, x);
+      store_planes(x);
+      dsum[0] = gt * static_cast<double>(sj) * un2_64;
+      dsum[1] = f1 * un2_64;
+      dsum[2] = dd * un2_64;
+      dsum[3] = f3 * un2_64;
+      dsum[4] = gp * un2_64;
       ptx::tmem_wait_st();
-      if (!__syncthreads_and(finite ? 1 : 0) && tid == 0) ctl[0] |= kFlagNonFinite;
       block_sum8(dsum, 6);
       if (tid == 0) {
         if (rec) {
@@ -600,27 +596,20 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         phase = 0;
       }
     }
-    // Final π, w → HBM (fp32, padded 128×128).
+    // Final π (TMEM π̂ᵀ) and w (TMEM ŵᵀ) → HBM, fp32 padded 128×128 row-major;
+    // a warp writes 32 consecutive columns of one row.
     {
-      float* P = a.P + static_cast<int64_t>(b) * kT * kT + static_cast<int64_t>(i) * kT + c0;
-      float* W = a.W + static_cast<int64_t>(b) * kT * kT + static_cast<int64_t>(i) * kT + c0;
-#pragma unroll 1
-      for (int g = 0; g < 2; ++g) {
-        uint32_t pr[32], wr[32];
-        ld(kPi + c0 + 32 * g, pr);
-        ld(kW + c0 + 32 * g, wr);
-        ptx::tmem_wait_ld();
-        float pv[32], wv[32];
+      const float dn = ldexpf(1.0f, -sc);
+      float* P = a.P + static_cast<int64_t>(b) * kT * kT + L;
+      float* W = a.W + static_cast<int64_t>(b) * kT * kT + L;
+      float pr[kW], wr[kW];
+      ldw(kPT + c0, pr);
+      ldw(kWT + c0, wr);
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          pv[t] = __uint_as_float(pr[t]);
-          wv[t] = __uint_as_float(wr[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          *reinterpret_cast<float4*>(P + 32 * g + t) = make_float4(pv[t], pv[t + 1], pv[t + 2], pv[t + 3]);
-          *reinterpret_cast<float4*>(W + 32 * g + t) = make_float4(wv[t], wv[t + 1], wv[t + 2], wv[t + 3]);
-        }
+      for (int t = 0; t < kW; ++t) {
+        const int i = c0 + t;
+        P[i * kT] = pr[t] * dn;
+        W[i * kT] = wr[t] * dn;
       }
     }
     if (tid == 0) {
@@ -637,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 0) ptx::tmem_dealloc<512>(tbase);
+  if (warp == 0) ptx::tmem_dealloc<256>(tbase);
 }
 
 // K8 fix-up per problem: π rows rescaled to μ, w columns to ν in fp64,
@@ -814,7 +803,9 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   if (device < 0) device = api_device();
   GWB_CUDA(cudaSetDevice(device));
   const BatchedOut o{out_final, out_pi, out_w, trace, trace_cap, n_records, converged, iterations_used};
-  const bool onchip_prec = cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_BF16X3;
+  // The on-chip kernel runs the f16x2 chain (AUTO for 0/1 graphs, DESIGN.md
+  // §4); other explicit precisions take the generic engine.
+  const bool onchip_prec = cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_F16X2;
   double ms_total = 0.0;
   if (kernel_ms) *kernel_ms = 0.0;
   // The on-chip kernel implements the entropy geometry; the quadratic one
@@ -840,6 +831,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
       d_nu(chunk * m, s);
   DevBuf<uint8_t> d_pack(chunk * 2 * kTileBytes, s);
   DevBuf<double> d_mup(chunk * kT, s), d_nup(chunk * kT, s);
+  DevBuf<int> d_scl(chunk, s);
   DevBuf<float> d_P(chunk * kT * kT, s), d_W(chunk * kT * kT, s);
   DevBuf<DevRecord> d_rec(trace ? chunk * (cfg->max_iters + 2) : 0, s);
   DevBuf<BatchStatus> d_st(chunk, s);
@@ -871,14 +863,14 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
     GWB_CUDA(cudaMemsetAsync(d_inexact.p, 0, sizeof(int), s));
     batched_pack_kernel<<<dim3(static_cast<unsigned>(cb), 2), 256, 0, s>>>(
         d_dx.p, d_dy.p, d_mu.p, d_nu.p, static_cast<int>(n), static_cast<int>(m), d_pack.p,
-        d_mup.p, d_nup.p, d_inexact.p);
+        d_mup.p, d_nup.p, d_scl.p, d_inexact.p);
     GWB_CUDA(cudaGetLastError());
     int inexact = 0;
     GWB_CUDA(cudaMemcpyAsync(&inexact, d_inexact.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     GWB_CUDA(cudaStreamSynchronize(s));
     if (inexact) {
-      // Structure matrices not exact in bf16: the on-chip kernel keeps D in
-      // one bf16 plane, so these problems take the generic (3xTF32) engine.
+      // Structure matrices not exact in fp16: the on-chip kernel keeps D in
+      // one fp16 plane, so these problems take the generic engine.
       const BatchedOut sub{out_final + b0 * len, out_pi ? out_pi + b0 * len : nullptr,
                            out_w ? out_w + b0 * len : nullptr,
                            trace ? trace + b0 * trace_cap : nullptr, trace_cap,
@@ -894,6 +886,7 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
     a.dpack = d_pack.p;
     a.mu = d_mup.p;
     a.nu = d_nup.p;
+    a.scl = d_scl.p;
     a.P = d_P.p;
     a.W = d_W.p;
     a.rec = trace ? d_rec.p : nullptr;

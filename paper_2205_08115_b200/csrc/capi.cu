@@ -276,9 +276,9 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
     fail(GWB_ERR_CAPACITY, fmt("trace capacity %d < max_iters %d", o.trace_cap, cfg->max_iters));
   // Small problems (n, m ≤ 128, product-coupling start, no observer): the
   // whole solve runs on one SM in the on-chip batched kernel (batched.cu),
-  // which falls back to this engine itself for non-bf16-exact D.
+  // which falls back to this engine itself for non-fp16-exact D.
   if (!observer && !cfg->record_residual && !initial && !graphs && entropy && n <= 128 && m <= 128 &&
-      (cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_BF16X3)) {
+      (cfg->precision == GWB_PREC_AUTO || cfg->precision == GWB_PREC_F16X2)) {
     gwb::device_bapg_batched(cfg, 1, dx, n, dy, m, mu, nu, o.out_final, o.out_pi, o.out_w,
                              o.trace, o.trace_cap, o.n_records, o.converged, o.iterations_used,
                              /*name_problem=*/false);

@@ -72,8 +72,8 @@ def run(batch=4096, iters=500, n=128, trace=False, start=0):
     fn.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     fn(C.byref(ms), C.byref(cnt))
     flops = 2.0 * 2.0 * n * n * (n + n) * batch  # 4 GEMMs of n³ MACs per iteration, all problems
-    # Executed tensor work: 128-padded tiles, 3 bf16 planes per GEMM.
-    exec_flops = 4 * 3 * 2.0 * 128 ** 3 * batch
+    # Executed tensor work: 128-padded tiles, 2 fp16 planes per GEMM (f16x2).
+    exec_flops = 4 * 2 * 2.0 * 128 ** 3 * batch
     k_s = ms.value * 1e-3
     # Problems stop where rel_change crosses rel_tol (the reference's rule):
     # a batched iteration advances every problem once, so the executed count
@@ -86,7 +86,7 @@ def run(batch=4096, iters=500, n=128, trace=False, start=0):
             "h2d_bytes": int(dx.nbytes + dy.nbytes + mu.nbytes + nu.nbytes),
             "d2h_bytes": int(out.nbytes),
             "tflops_alg": flops * mean_used / k_s / 1e12,
-            "tflops_exec_bf16": exec_flops * mean_used / k_s / 1e12,
+            "tflops_exec_f16": exec_flops * mean_used / k_s / 1e12,
             "iterations_used": int(used.min()), "iterations_used_max": int(used.max()),
             "converged_any": bool(conv.any()),
             "final_sum_err": float(np.abs(out.reshape(batch, -1).sum(axis=1) - 1.0).max())}
