@@ -32,6 +32,7 @@
 #include <cuda_fp16.h>
 
 #include "gemm.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace gwb {
@@ -41,19 +42,16 @@ namespace {
 constexpr int kBM = 128;                   // rows per CTA
 constexpr int kPairM = 2 * kBM;            // rows per CTA pair (MMA M)
 constexpr int kBN = 256;                   // columns per tile (MMA N)
-constexpr int kHalfN = kBN / 2;            // B rows loaded per CTA
 constexpr int kBK = 32;                    // 32 fp32 = 128 B = one swizzle row
 constexpr int kBK16 = 64;                  // 64 bf16 = 128 B
 constexpr int kStages = 6;
 constexpr int kGroupM = 8;
 constexpr int kEpiWarps = 16;              // 4 lane quadrants × 4 column slices
-constexpr int kSliceCols = kBN / 4;        // 64 accumulator columns per thread
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kABytes = kBM * kBK * 4;
-constexpr uint32_t kBBytes = kHalfN * kBK * 4;
-constexpr uint32_t kStageBytes = kABytes + kBBytes;  // per CTA
-constexpr uint32_t kTmemCols = 2 * kBN;    // double-buffered accumulator
-constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+constexpr size_t smem_bytes(int bn) {
+  return kStages * (kABytes + static_cast<size_t>(bn / 2) * kBK * 4) + 1024 + 256;
+}
 
 // Round-to-nearest split of 8 fp32 values into three planes whose sum is x
 // (hi = rn(x), mid = rn(x − hi), lo = rn(x − hi − mid); each difference is
@@ -134,16 +132,23 @@ __device__ __forceinline__ float tf32_lo(float x) { return rna_tf32(x - trunc_tf
 // restarts accumulation every `chunk` k-blocks in one of two TMEM buffers
 // and the epilogue warps add each finished chunk into fp32 registers with
 // round-to-nearest adds ("promotion"), bounding the bias by the chunk length.
+template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ GemmParams p) {
-  if (p.skip != nullptr && *p.skip != 0) return;
+  // Tile width BN (MMA N): 256, or 128 for grids of few tiles (small n).
+  constexpr int kBN_ = BN;
+  constexpr int kHalfN_ = BN / 2;                        // B rows loaded per CTA
+  constexpr int kSlice_ = BN / 4;                        // accumulator columns per epilogue thread
+  constexpr uint32_t kBB_ = kHalfN_ * kBK * 4;
+  constexpr uint32_t kStageB_ = kABytes + kBB_;          // per CTA
+  constexpr uint32_t kTmem_ = 2 * BN;                    // double-buffered accumulator
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   float* sA = reinterpret_cast<float*>(smem);
   float* sB = reinterpret_cast<float*>(smem + kStages * kABytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageB_);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;  // [2] chunk accumulated (per CTA)
   uint64_t* tempty = tfull + 2;       // [2] chunk drained (leader's counts both CTAs)
@@ -160,7 +165,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // chunk buffers run on across items, so the epilogue's drain and store of
   // one tile overlap the MMAs of the next and the prologue is paid once.
   const int tiles_all = p.tiles_m * p.tiles_n;
-  const int items = tiles_all * p.splits;
   const int npairs = static_cast<int>(gridDim.x >> 1);
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int per_group = p.group_m * p.tiles_n;
@@ -178,18 +182,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc_2sm<kTmemCols>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc_2sm<kTmem_>(tmem_slot);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the predecessor kernel; nothing it
+  // wrote (operands, the skip flag) is read before this point.
+  ptx::griddep_wait();
+  ptx::griddep_launch();
+  const bool skip = p.skip != nullptr && *p.skip != 0;
+  const int items = skip ? 0 : tiles_all * p.splits;
 
   const int kblk = p.kind ? kBK16 : kBK;  // elements per 128-B k-block
   const int kblocks_all = (p.K + kblk - 1) / kblk;
   const int chunk = p.chunk;
   const uint32_t f_a_bytes = static_cast<uint32_t>(p.a_planes) * kABytes;
-  const uint32_t f_stage_bytes = f_a_bytes + static_cast<uint32_t>(p.b_planes) * kBBytes;
-  const int f_stages = static_cast<int>((kStages * kStageBytes) / f_stage_bytes);
+  const uint32_t f_stage_bytes = f_a_bytes + static_cast<uint32_t>(p.b_planes) * kBB_;
+  const int f_stages = static_cast<int>((kStages * kStageB_) / f_stage_bytes);
 
   // Coordinates and k-range of work item `item`.
   struct Item {
@@ -211,7 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     t.total = p.fused ? t.kblocks : p.passes * t.kblocks;
     t.nchunks = (t.total + chunk - 1) / chunk;
     t.a_row = t.tm * kPairM + static_cast<int>(rank) * kBM;
-    t.b_row = t.tn * kBN + static_cast<int>(rank) * kHalfN;
+    t.b_row = t.tn * kBN_ + static_cast<int>(rank) * kHalfN_;
     return t;
   };
 
@@ -234,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int pa = 0; pa < p.a_planes; ++pa)
               ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, t.a_row);
             for (int pl = 0; pl < p.b_planes; ++pl) {
-              void* dst = st + f_a_bytes + pl * kBBytes;
+              void* dst = st + f_a_bytes + pl * kBB_;
               if (p.b_block_k > 0) {
                 const int kk = kb * kblk;
                 ptx::tma_load_3d_2sm(dst, &p.b_map[pl], fbar, kk % p.b_block_k, t.b_row,
@@ -252,15 +262,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int pass = it / t.kblocks;
             const int kb = t.kb_begin + it - pass * t.kblocks;
             const uint32_t fbar = ptx::mapa(&full[s], 0);
-            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * kStageB_);
             ptx::tma_load_2d_2sm(sA + s * (kBM * kBK), &p.a_map[p.a_sel[pass]], fbar, kb * kblk,
                                  t.a_row);
             if (p.b_block_k > 0) {
               const int kk = kb * kblk;
-              ptx::tma_load_3d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
+              ptx::tma_load_3d_2sm(sB + s * (kHalfN_ * kBK), &p.b_map[p.b_sel[pass]], fbar,
                                    kk % p.b_block_k, t.b_row, kk / p.b_block_k);
             } else {
-              ptx::tma_load_2d_2sm(sB + s * (kHalfN * kBK), &p.b_map[p.b_sel[pass]], fbar,
+              ptx::tma_load_2d_2sm(sB + s * (kHalfN_ * kBK), &p.b_map[p.b_sel[pass]], fbar,
                                    kb * kblk, t.b_row);
             }
           }
@@ -269,9 +279,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && ptx::elect_one()) {
-      const uint32_t idesc = p.kind == 2   ? ptx::idesc_f16(kPairM, kBN)
-                             : p.kind == 1 ? ptx::idesc_bf16(kPairM, kBN)
-                                           : ptx::idesc_tf32(kPairM, kBN);
+      const uint32_t idesc = p.kind == 2   ? ptx::idesc_f16(kPairM, kBN_)
+                             : p.kind == 1 ? ptx::idesc_bf16(kPairM, kBN_)
+                                           : ptx::idesc_tf32(kPairM, kBN_);
       int g0 = 0;  // stage iterations of the previous items
       int c = 0;   // chunks of all items so far
       for (int item = pair; item < items; item += npairs) {
@@ -280,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int b = c & 1;
           ptx::mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
+          const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN_);
           const int it0 = cc * chunk;
           const int it1 = min(t.total, it0 + chunk);
           if (p.fused) {
@@ -296,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // on the hi-plane terms only (as in batched.cu).
               for (int pl = p.passes - 1; pl >= 0; --pl) {
                 const uint32_t a_base = st_base + p.a_sel[pl] * kABytes;
-                const uint32_t b_base = st_base + f_a_bytes + p.b_sel[pl] * kBBytes;
+                const uint32_t b_base = st_base + f_a_bytes + p.b_sel[pl] * kBB_;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32);
@@ -315,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::mbar_wait(&full[s], ph);
               ptx::tc_fence_after();
               const uint32_t a_base = ptx::smem_u32(sA + s * (kBM * kBK));
-              const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN * kBK));
+              const uint32_t b_base = ptx::smem_u32(sB + s * (kHalfN_ * kBK));
               // 4 MMAs per 128-B k-block: K = 8 (tf32) or 16 (bf16), +32 B each.
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -339,22 +349,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const uint32_t slice = (warp - 2) >> 2;
     const uint32_t lane_base = quad * 32;
-    const uint32_t col_base = slice * kSliceCols;
+    const uint32_t col_base = slice * kSlice_;
     const uint32_t tempty_leader[2] = {ptx::mapa(&tempty[0], 0), ptx::mapa(&tempty[1], 0)};
     int c = 0;
     for (int item = pair; item < items; item += npairs) {
       const Item t = item_of(item);
       const int split = t.split, tn = t.tn, a_row = t.a_row;
-      float acc[kSliceCols];
+      float acc[kSlice_];
 #pragma unroll
-      for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+      for (int j = 0; j < kSlice_; ++j) acc[j] = 0.0f;
       for (int cc = 0; cc < t.nchunks; ++cc, ++c) {
         const int b = c & 1;
         ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t taddr = tmem + (lane_base << 16) + static_cast<uint32_t>(b * kBN) + col_base;
+        const uint32_t taddr = tmem + (lane_base << 16) + static_cast<uint32_t>(b * kBN_) + col_base;
 #pragma unroll
-        for (int h = 0; h < kSliceCols / 32; ++h) {
+        for (int h = 0; h < kSlice_ / 32; ++h) {
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(taddr + h * 32, v);
           ptx::tmem_wait_ld();
@@ -371,11 +381,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // the tile's last split (per-tile arrival counter) then sums the
         // partials in split order — the fixed order of the standalone reduce
         // kernel, so results are bitwise the same — and runs the epilogue.
-        const int col0 = tn * kBN + static_cast<int>(col_base);
+        const int col0 = tn * kBN_ + static_cast<int>(col_base);
         if (row < p.M) {
           float* wrow = p.ws + static_cast<int64_t>(split) * p.M * p.ldw + static_cast<int64_t>(row) * p.ldw;
 #pragma unroll
-          for (int j = 0; j < kSliceCols; j += 4)
+          for (int j = 0; j < kSlice_; j += 4)
             if (col0 + j < p.ldw)
               *reinterpret_cast<float4*>(wrow + col0 + j) =
                   make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -392,12 +402,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (warp == 2 && lane == 0) *cnt = 0;  // every split arrived: ready for the next launch
         if (row < p.M) {
 #pragma unroll
-          for (int j = 0; j < kSliceCols; ++j) acc[j] = 0.0f;
+          for (int j = 0; j < kSlice_; ++j) acc[j] = 0.0f;
           for (int sp = 0; sp < p.splits; ++sp) {
             const float* w = p.ws + static_cast<int64_t>(sp) * p.M * p.ldw +
                              static_cast<int64_t>(row) * p.ldw + col0;
 #pragma unroll
-            for (int j = 0; j < kSliceCols; j += 4) {
+            for (int j = 0; j < kSlice_; j += 4) {
               if (col0 + j < p.ldw) {
                 const float4 v = __ldcg(reinterpret_cast<const float4*>(w + j));
                 acc[j] = __fadd_rn(acc[j], v.x);
@@ -414,9 +424,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
         float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
         const bool round_out = p.aux_mode == 1;
-        const int col0 = tn * kBN + static_cast<int>(col_base);
+        const int col0 = tn * kBN_ + static_cast<int>(col_base);
   #pragma unroll
-        for (int j = 0; j < kSliceCols; ++j) {
+        for (int j = 0; j < kSlice_; ++j) {
           float a = acc[j];
           if (p.col_bias != nullptr) a = __fadd_rn(a, (col0 + j < p.N) ? __ldg(p.col_bias + col0 + j) : 0.0f);
           float x = a * rs;
@@ -426,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (p.rs_part != nullptr) {
           double s = 0.0;
   #pragma unroll
-          for (int j = 0; j < kSliceCols; ++j)
+          for (int j = 0; j < kSlice_; ++j)
             if (col0 + j < p.N) s += static_cast<double>(acc[j]);
           p.rs_part[static_cast<int64_t>(row) * p.rs_stride + tn * 4 + static_cast<int>(slice)] = s;
         }
@@ -434,9 +444,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
           // split-operand GEMM.
           const int64_t off = static_cast<int64_t>(row) * p.ldc + col0;
-          const bool vec = col0 + kSliceCols <= p.N && (p.ldc & 7) == 0;
+          const bool vec = col0 + kSlice_ <= p.N && (p.ldc & 7) == 0;
   #pragma unroll
-          for (int j0 = 0; j0 < kSliceCols; j0 += 8) {
+          for (int j0 = 0; j0 < kSlice_; j0 += 8) {
             __align__(16) uint16_t h[3][8];
             split_planes8(acc + j0, p.c_f16 != 0, h);
             for (int pl = 0; pl < p.c_planes; ++pl) {
@@ -449,9 +459,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
-        } else if (col0 + kSliceCols <= p.N && (p.ldc & 3) == 0) {
+        } else if (col0 + kSlice_ <= p.N && (p.ldc & 3) == 0) {
   #pragma unroll
-          for (int j = 0; j < kSliceCols; j += 4) {
+          for (int j = 0; j < kSlice_; j += 4) {
             if (p.accumulate) {
               const float4 o = *reinterpret_cast<const float4*>(crow + col0 + j);
               acc[j] = __fadd_rn(o.x, acc[j]);
@@ -467,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         } else {
   #pragma unroll
-          for (int j = 0; j < kSliceCols; ++j) {
+          for (int j = 0; j < kSlice_; ++j) {
             if (col0 + j < p.N) {
               if (p.accumulate) acc[j] = __fadd_rn(crow[col0 + j], acc[j]);
               crow[col0 + j] = acc[j];
@@ -483,13 +493,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc_2sm<kTmemCols>(tmem);
+    ptx::tmem_dealloc_2sm<kTmem_>(tmem);
   }
 }
 
 // Split-K reduction + epilogue: one CTA per output row, fixed summation order
 // over the splits, then the same output modes as the GEMM epilogue.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ GemmParams p) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   if (p.skip != nullptr && *p.skip != 0) return;
   const int row = blockIdx.x;
   const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
@@ -569,6 +581,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
 
 // out[i] = factor · Σ_k rs_part[i][k] (fixed order), rounded to fp32.
 __global__ void rowsum_bias_kernel(const __grid_constant__ GemmParams p, double factor, float* out) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   if (p.skip != nullptr && *p.skip != 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.M) return;
@@ -663,6 +677,7 @@ CUtensorMap gemm_tensor_map(const void* ptr, int64_t rows, int64_t cols, int64_t
 struct GemmPlan {
   GemmParams params;
   int grid = 0;
+  int bn = 256;  // tile width (MMA N): 256, or 128 for grids of few tiles
   double flops = 0.0;
   float* ws = nullptr;  // split-K workspace (owned)
   int* counters = nullptr;
@@ -677,9 +692,23 @@ struct GemmPlan {
 GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // Per current device (attributes are per device context); cheap, and plans
   // are created once per solve.
-  cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kSmemBytes));
+  cudaFuncSetAttribute(gemm_tf32_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem_bytes(256)));
+  cudaFuncSetAttribute(gemm_tf32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem_bytes(128)));
   auto* p = new GemmPlan();
+  // Tile width: 128-wide tiles when even they fill at most one wave of the 74
+  // SM pairs (n ≲ 2000): twice the CTA pairs of 256-wide tiles, each with the
+  // full K, instead of splitting K.  GWB_GEMM_BN=128/256 forces (A/B).
+  {
+    static const int bn_env = [] {
+      const char* e = std::getenv("GWB_GEMM_BN");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int64_t t256 = ((d.M + kPairM - 1) / kPairM) * ((d.N + 255) / 256);
+    p->bn = bn_env == 128 || bn_env == 256 ? bn_env : (2 * t256 <= 74 ? 128 : 256);
+  }
+  const int halfn = p->bn / 2;
   GemmParams& g = p->params;
   std::memset(&g, 0, sizeof(g));
   g.M = static_cast<int32_t>(d.M);
@@ -696,8 +725,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     for (int pl = 0; pl < d.bf16_planes; ++pl) {
       g.b_map[pl] = d.b_block_k > 0
                         ? make_map_blocked(d.b_bf16[pl], d.N, d.b_block_k, d.K / d.b_block_k,
-                                           kHalfN, 2, d.b_block_stride)
-                        : make_map(d.b_bf16[pl], d.N, d.K, d.ldb, kHalfN, 2);
+                                           halfn, 2, d.b_block_stride)
+                        : make_map(d.b_bf16[pl], d.N, d.K, d.ldb, halfn, 2);
       g.a_sel[pl] = 0;
       g.b_sel[pl] = pl;
     }
@@ -716,9 +745,9 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     }
   } else {
   auto bmap = [&](const float* b) {
-    return d.b_block_k > 0 ? make_map_blocked(b, d.N, d.b_block_k, d.K / d.b_block_k, kHalfN, 4,
+    return d.b_block_k > 0 ? make_map_blocked(b, d.N, d.b_block_k, d.K / d.b_block_k, halfn, 4,
                                               d.b_block_stride)
-                           : make_map(b, d.N, d.K, d.ldb, kHalfN);
+                           : make_map(b, d.N, d.K, d.ldb, halfn);
   };
   g.a_map[0] = make_map(d.a, d.M, d.K, d.lda, kBM);
   g.b_map[0] = bmap(d.b);
@@ -741,7 +770,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   }
   }
   g.tiles_m = static_cast<int32_t>((d.M + kPairM - 1) / kPairM);
-  g.tiles_n = static_cast<int32_t>((d.N + kBN - 1) / kBN);
+  g.tiles_n = static_cast<int32_t>((d.N + p->bn - 1) / p->bn);
   g.chunk = d.promote_every > 0 ? d.promote_every : 1 << 30;
   static const int group_env = [] {
     const char* e = std::getenv("GWB_GEMM_GROUP_M");
@@ -859,16 +888,21 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
 void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
-  gemm_tf32_kernel<<<p->grid, kThreads, kSmemBytes, s>>>(p->params);
+  cudaError_t e = p->bn == 128
+                      ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
+                      : launch_pdl(gemm_tf32_kernel<256>, dim3(p->grid), dim3(kThreads), smem_bytes(256), s, p->params);
+  if (e != cudaSuccess) return e;
   if (p->params.splits > 1 && p->params.counters == nullptr)
-    splitk_reduce_kernel<<<p->params.M, 256, 0, s>>>(p->params);
+    e = launch_pdl(splitk_reduce_kernel, dim3(p->params.M), dim3(256), 0, s, p->params);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t gemm_rowsum_bias(const GemmPlan* p, double factor, float* out, cudaStream_t s) {
   if (p->params.rs_part == nullptr) return cudaErrorInvalidValue;
-  rowsum_bias_kernel<<<(p->params.M + 255) / 256, 256, 0, s>>>(p->params, factor, out);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(rowsum_bias_kernel, dim3((p->params.M + 255) / 256), dim3(256), 0, s,
+                                   p->params, factor, out);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 int gemm_launches(const GemmPlan* p) {

@@ -12,6 +12,7 @@
 #include "../../include/gwb.h"
 #include "devutil.cuh"
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace gwb {
 void check_cuda(cudaError_t e, const char* what);  // solver.cu: throws CudaError
@@ -50,6 +51,13 @@ __device__ __forceinline__ void store_d4(double* p, const double (&v)[4]) {
   *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
 }
 
+// PDL (launch.cuh): wait for the predecessor kernel's results, then let the
+// successor's CTAs be scheduled.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // A device error flag (DevFlag) raised at the current iteration: the first
 // raise records err_iter; the iteration's remaining projection kernels skip
 // on `flags`, and the finalize marks the solve done (no separate check
@@ -62,6 +70,7 @@ __device__ __forceinline__ void raise_flag(DevStatus* st, int flag) {
 // Half-step a: one CTA per row.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int write, int tail) {
+  pdl_enter();
   if (tail ? d.st->flags != 0 : d.st->done != 0) return;
   const int64_t i = blockIdx.x;
   const float* g = d.G + i * d.ld;
@@ -145,6 +154,7 @@ constexpr int kNarrowV = kNarrowM / 128;  // 4-column groups per lane
 constexpr int kWarpRows = kRowThreads / 32;
 
 __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d, int write, int tail) {
+  pdl_enter();
   if (tail ? d.st->flags != 0 : d.st->done != 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
@@ -229,6 +239,7 @@ constexpr int kColThreads = 256;
 constexpr int kColWidth = 128;  // columns per CTA (32 lanes × 4)
 
 __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int rows_per_chunk) {
+  pdl_enter();
   if (d.st->done || d.st->flags) return;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
@@ -281,6 +292,7 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
 // Half-step b, pass 2: merge chunk partials per column, raise errors.  One
 // warp per column: lanes take the row chunks, then a fixed-order warp merge.
 __global__ void col_combine_kernel(BapgDev d) {
+  pdl_enter();
   if (d.st->done || d.st->flags) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   if (j >= d.m) return;
@@ -326,6 +338,7 @@ __device__ __forceinline__ double col_write_elem(float g, double p, double w, do
 
 // Half-step b, pass 3: write W_new, fused diagnostics. One CTA per row.
 __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
+  pdl_enter();
   if (d.st->done) return;
   if (d.st->flags != 0) return;
   const int64_t i = blockIdx.x;
@@ -371,6 +384,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
 
 // col_write for narrow rows (m ≤ 128): one warp per row, as row_update_warps.
 __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d) {
+  pdl_enter();
   if (d.st->done) return;
   if (d.st->flags != 0) return;
   const int lane = threadIdx.x & 31;
@@ -417,6 +431,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_warps_kernel(BapgDev d)
 constexpr int kFinThreads = 512;
 
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(BapgDev d, double rel_tol, int tail) {
+  pdl_enter();
   DevStatus* st = d.st;
   if (tail ? st->flags != 0 : st->done != 0) return;
   if (!tail && st->flags != 0) {  // raised this iteration (raise_flag): stop here
@@ -705,10 +720,10 @@ inline unsigned grid1d(int64_t work, int threads) {
 namespace {
 void launch_col_write_pass(const BapgDev& d, cudaStream_t s) {
   if (d.m <= kNarrowM)
-    col_write_warps_kernel<<<static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows), kRowThreads,
-                             0, s>>>(d);
+    launch_pdl(col_write_warps_kernel, dim3(static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows)),
+               dim3(kRowThreads), 0, s, d);
   else
-    col_write_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
+    launch_pdl(col_write_kernel, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d);
 }
 }  // namespace
 
@@ -718,19 +733,19 @@ void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
     return;
   }
   if (d.n >= 1 && d.m <= kNarrowM)
-    row_update_warps_kernel<<<static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows), kRowThreads,
-                              0, s>>>(d, write ? 1 : 0, write ? 0 : 1);
+    launch_pdl(row_update_warps_kernel, dim3(static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows)),
+               dim3(kRowThreads), 0, s, d, write ? 1 : 0, write ? 0 : 1);
   else if (d.n >= 1)
-    row_update_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d, write ? 1 : 0,
-                                                                         write ? 0 : 1);
+    launch_pdl(row_update_kernel, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d,
+               write ? 1 : 0, write ? 0 : 1);
 }
 
 void launch_col_update(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
-  col_combine_kernel<<<grid1d(d.m * 32, 256), 256, 0, s>>>(d);
+  launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  launch_pdl(col_combine_kernel, dim3(grid1d(d.m * 32, 256)), dim3(256), 0, s, d);
   launch_col_write_pass(d, s);
 }
 
@@ -739,7 +754,7 @@ void launch_col_partial(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  col_partial_kernel<<<grid, kColThreads, 0, s>>>(d, rows_per_chunk);
+  launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
 }
 
 void launch_col_write(const BapgDev& d, cudaStream_t s) {
@@ -747,7 +762,7 @@ void launch_col_write(const BapgDev& d, cudaStream_t s) {
 }
 
 void launch_finalize(const BapgDev& d, double rel_tol, bool tail, cudaStream_t s) {
-  finalize_kernel<<<1, kFinThreads, 0, s>>>(d, rel_tol, tail ? 1 : 0);
+  launch_pdl(finalize_kernel, dim3(1), dim3(kFinThreads), 0, s, d, rel_tol, tail ? 1 : 0);
 }
 
 void launch_status_reset(DevStatus* st, cudaStream_t s) { status_reset_kernel<<<1, 1, 0, s>>>(st); }

@@ -294,6 +294,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       : "memory");
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor in the stream is still running; griddep_wait() blocks until
+// the predecessor grid has completed and its memory is visible, and
+// griddep_launch() lets the successor's CTAs be scheduled early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // UMMA shared-memory descriptor for a K-major operand tile stored in the
 // canonical 128-byte-swizzle layout that TMA (CU_TENSOR_MAP_SWIZZLE_128B)
 // writes: rows of 128 B, 8-row core groups 1024 B apart (SBO), tile base

@@ -60,8 +60,16 @@ def session_rate(inst, iters, prec="auto", warm=3):
 
 if __name__ == "__main__":
     out = {}
-    for name, inst, iters in [("c1", I.config1(), 2000), ("c2", I.config2(), 1000),
-                              ("c3", I.config3(), 500), ("c4@8192", I.config4(n=8192), 20)]:
+    only = None
+    for a in sys.argv[1:]:
+        if a.startswith("--only="):
+            only = a[len("--only="):].split(",")
+    cases = [("c1", I.config1, 2000), ("c2", I.config2, 1000), ("c3", I.config3, 500),
+             ("c4@8192", lambda: I.config4(n=8192), 20)]
+    for name, make, iters in cases:
+        if only and name not in only:
+            continue
+        inst = make()
         out[name] = session_rate(inst, iters)
         print(name, json.dumps(out[name]), flush=True)
         if name in ("c1", "c4@8192") and "--compare" in sys.argv:
