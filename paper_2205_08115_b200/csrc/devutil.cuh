@@ -286,15 +286,24 @@ __device__ __forceinline__ Lse64 lse64_merge(Lse64 a, Lse64 b) {
   const double M = a.mx > b.mx ? a.mx : b.mx;
   return Lse64{M, __fma_rn(a.s, exp(a.mx - M), __dmul_rn(b.s, exp(b.mx - M)))};
 }
+// Warp-wide merge of (max, Σ) pairs over the first `lanes` lanes (a power
+// of two; the others must hold {−inf, 0}): the max by an xor butterfly, then
+// each lane rescales its own sum once (one exp per lane instead of one per
+// butterfly step) and the rescaled sums are added by a butterfly.  NaN in
+// any max gives NaN.  The sum's butterfly rounds lane-dependently; every
+// lane returns lane 0's value (deterministic).
+template <int kLanes = 32>
 __device__ __forceinline__ Lse64 lse64_warp_merge(Lse64 a) {
+  const bool nan = __any_sync(0xffffffffu, isnan(a.mx));
+  double M = a.mx;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    Lse64 b;
-    b.mx = __shfl_xor_sync(0xffffffffu, a.mx, o);
-    b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
-    a = lse64_merge(a, b);
-  }
-  return a;
+  for (int o = kLanes / 2; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  double s = (a.mx == -INFINITY || M == -INFINITY) ? 0.0 : a.s * exp(a.mx - M);
+#pragma unroll
+  for (int o = kLanes / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  s = __shfl_sync(0xffffffffu, s, 0);
+  if (nan) return Lse64{NAN, NAN};
+  return Lse64{M, s};
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -337,13 +346,17 @@ __device__ void block_reduce(MaxSum& ms, double (&sums)[kSums]) {
 
 // block_reduce for the fp64 accumulator; lane 0 of each warp feeds a
 // fixed-order merge, the result is broadcast to all threads.
-template <int kThreads, int kSums>
+// Warp 0 merges the kWarps per-warp results (lanes < kWarps, fixed order)
+// and broadcasts them through shared memory: one exp per lane per level.
+// `with_lse` = false skips the (max, Σ) merge (sums only).
+template <int kThreads, int kSums, bool with_lse = true>
 __device__ void block_reduce64(Lse64& ms, double (&sums)[kSums]) {
   constexpr int kWarps = kThreads / 32;
+  static_assert(kWarps <= 32 && (kWarps & (kWarps - 1)) == 0, "warps: power of two ≤ 32");
   __shared__ double s_mx[kWarps], s_s[kWarps];
   __shared__ double s_d[kSums > 0 ? kSums : 1][kWarps];
   const int w = threadIdx.x / 32, l = threadIdx.x & 31;
-  ms = lse64_warp_merge(ms);
+  if (with_lse) ms = lse64_warp_merge(ms);
 #pragma unroll
   for (int k = 0; k < kSums; ++k) sums[k] = warp_sum(sums[k]);
   if (l == 0) {
@@ -353,18 +366,29 @@ __device__ void block_reduce64(Lse64& ms, double (&sums)[kSums]) {
     for (int k = 0; k < kSums; ++k) s_d[k][w] = sums[k];
   }
   __syncthreads();
-  Lse64 r{-INFINITY, 0.0};
-  double t[kSums > 0 ? kSums : 1];
+  if (w == 0) {
+    Lse64 r{-INFINITY, 0.0};
+    if (with_lse && l < kWarps) r = Lse64{s_mx[l], s_s[l]};
+    if (with_lse) r = lse64_warp_merge<kWarps>(r);
+    double t[kSums > 0 ? kSums : 1];
 #pragma unroll
-  for (int k = 0; k < kSums; ++k) t[k] = 0.0;
-  for (int q = 0; q < kWarps; ++q) {
-    r = lse64_merge(r, Lse64{s_mx[q], s_s[q]});
+    for (int k = 0; k < kSums; ++k) {
+      t[k] = 0.0;
+      if (l == 0)
+        for (int q = 0; q < kWarps; ++q) t[k] += s_d[k][q];
+    }
+    __syncwarp();
+    if (l == 0) {
+      s_mx[0] = r.mx;
+      s_s[0] = r.s;
 #pragma unroll
-    for (int k = 0; k < kSums; ++k) t[k] += s_d[k][q];
+      for (int k = 0; k < kSums; ++k) s_d[k][0] = t[k];
+    }
   }
-  ms = r;
+  __syncthreads();
+  if (with_lse) ms = Lse64{s_mx[0], s_s[0]};
 #pragma unroll
-  for (int k = 0; k < kSums; ++k) sums[k] = t[k];
+  for (int k = 0; k < kSums; ++k) sums[k] = s_d[k][0];
   __syncthreads();
 }
 

@@ -788,11 +788,13 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // Split A (f16x3) keeps separate pass stages: its fused 3-pass chunks
   // accumulate 48 MMAs per promotion and measured a 3× larger truncation
   // bias (−1.5e-6 vs −4.6e-7 relative at K = 2048, tests/test_gpu_gemm.py).
-  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env && !d.a_bf16_lo) {
+  if (d.bf16_planes >= 2 && d.fuse_planes && !unfused_env && (!d.a_bf16_lo || d.fuse_split_a)) {
     g.fused = 1;
     g.a_planes = d.a_bf16_lo ? 2 : 1;
     g.b_planes = d.bf16_planes;
-    if (d.promote_every > 0) g.chunk = 2 * d.promote_every;
+    // Split A (centred f16x3): promotion every promote_every k-blocks (c2,
+    // 2 vs 4: same speed, objective error 1.4e-7 vs 3.5e-7).
+    if (d.promote_every > 0) g.chunk = (d.a_bf16_lo ? 1 : 2) * d.promote_every;
     // A/B knob: k-blocks per promotion chunk in the fused schedule.
     static const int chunk_env = [] {
       const char* e = std::getenv("GWB_GEMM_CHUNK_KB");

@@ -79,6 +79,10 @@ struct GemmDesc {
   // (after scaling, before the plane split) for gemm_rowsum_bias.
   const float* col_bias = nullptr;
   bool rowsums = false;
+  // Split A (f16x3) in fused stages with 4-k-block promotion chunks.  Only
+  // for centred operands: on all-positive terms the 48-MMA chunks measured a
+  // 3× larger truncation bias than separate pass stages.
+  bool fuse_split_a = false;
 };
 
 // 2-D TMA descriptor of a row-major rows×cols matrix (leading dim ld

@@ -126,6 +126,107 @@ __global__ void __launch_bounds__(kRowThreads) row_update_kernel(BapgDev d, int 
   }
 }
 
+// Half-step a for rows of m ≤ 1024·V (c1, c2): the row stays in registers,
+// so it is read once, the max is found first and each exponential is
+// evaluated once (the online (max, Σ) of row_update_kernel re-scales and
+// evaluates two per element; on short rows that and the block merge, not
+// HBM, bound the pass).  Same map, fp64 throughout.
+template <int V>
+__global__ void __launch_bounds__(kRowThreads) row_update_reg_kernel(BapgDev d, int write, int tail) {
+  pdl_enter();
+  if (tail ? d.st->flags != 0 : d.st->done != 0) return;
+  const int64_t i = blockIdx.x;
+  const float* g = d.G + i * d.ld;
+  const double* w = d.W64 + i * d.ld;
+  const int64_t m = d.m;
+  const double inv_rho = d.inv_rho64;
+  float gv[V][4];
+  double wv[V][4];
+  double mx = -INFINITY;
+  bool nan = false;
+  double sums[3] = {0.0, 0.0, 0.0};  // ⟨G,W⟩, ΣW, then Σ W e^{x − max}
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int64_t j = (threadIdx.x + static_cast<int64_t>(v) * kRowThreads) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      gv[v][q] = 0.f;
+      wv[v][q] = 0.0;
+    }
+    if (j < m) {
+      const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+      gv[v][0] = g4.x;
+      gv[v][1] = g4.y;
+      gv[v][2] = g4.z;
+      gv[v][3] = g4.w;
+      load_d4(w + j, wv[v]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < m) {
+        const double x = expo(gv[v][q], inv_rho);
+        nan = nan || isnan(x);
+        mx = fmax(mx, x);
+        sums[0] = __fma_rn(static_cast<double>(gv[v][q]), wv[v][q], sums[0]);
+        sums[1] += wv[v][q];
+      }
+    }
+  }
+  // Block max (fixed-order butterfly + warp-0 merge) with the two sums.
+  __shared__ double s_m[kRowThreads / 32];
+  __shared__ int s_nan;
+  if (threadIdx.x == 0) s_nan = 0;
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (nan) s_nan = 1;
+  double r = s_m[0];
+#pragma unroll
+  for (int q = 1; q < kRowThreads / 32; ++q) r = fmax(r, s_m[q]);
+  Lse64 dummy{-INFINITY, 0.0};
+  double ds[2] = {sums[0], sums[1]};
+  block_reduce64<kRowThreads, 2, false>(dummy, ds);  // its barriers also publish s_nan
+  if (s_nan) r = NAN;
+  if (threadIdx.x == 0) {
+    d.row_part[i].gw = ds[0];
+    const double dev = ds[1] - d.mu64[i];
+    d.row_part[i].rowdev = dev * dev;
+  }
+  if (!write) return;
+  double ev[V][4];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int64_t j = (threadIdx.x + static_cast<int64_t>(v) * kRowThreads) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ev[v][q] = (j + q < m) ? exp(expo(gv[v][q], inv_rho) - r) : 0.0;
+      sums[2] = __fma_rn(wv[v][q], ev[v][q], sums[2]);
+    }
+  }
+  double ss[1] = {sums[2]};
+  block_reduce64<kRowThreads, 1, false>(dummy, ss);
+  const double S = ss[0];
+  if (threadIdx.x == 0) {
+    if (r > 700.0) raise_flag(d.st, kFlagOverflowA);
+    if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
+      raise_flag(d.st, kFlagZeroA);
+      atomicMin(&d.st->zero_index, static_cast<int>(i));
+    }
+  }
+  const double scale = d.mu64[i] / S;
+  double* p = d.P64 + i * d.ld;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int64_t j = (threadIdx.x + static_cast<int64_t>(v) * kRowThreads) * 4;
+    if (j >= m) break;
+    double o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = (j + q < m) ? scale * wv[v][q] * ev[v][q] : 0.0;
+    store_d4(p + j, o);
+    aux_store4_64(d.P_aux, d.P, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
+  }
+}
+
 // Diagnostics-only row pass on fp32 iterates (quadratic geometry's tail
 // record): ⟨G_i, W_i⟩ and (Σ_j W_ij − μ_i)².
 __global__ void __launch_bounds__(kRowThreads) row_diag32_kernel(BapgDev d) {
@@ -138,7 +239,7 @@ __global__ void __launch_bounds__(kRowThreads) row_diag32_kernel(BapgDev d) {
     sums[1] += w;
   }
   Lse64 dummy{-INFINITY, 0.0};
-  block_reduce64<kRowThreads, 2>(dummy, sums);
+  block_reduce64<kRowThreads, 2, false>(dummy, sums);
   if (threadIdx.x == 0) {
     d.row_part[i].gw = sums[0];
     const double dev = sums[1] - d.mu64[i];
@@ -368,7 +469,7 @@ __global__ void __launch_bounds__(kRowThreads) col_write_kernel(BapgDev d) {
     aux_store4_64(d.W_aux, d.W_new, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
   }
   Lse64 dummy{-INFINITY, 0.0};
-  block_reduce64<kRowThreads, 6>(dummy, sums);
+  block_reduce64<kRowThreads, 6, false>(dummy, sums);
   if (!__syncthreads_and(finite ? 1 : 0) && threadIdx.x == 0)
     raise_flag(d.st, kFlagNonFinite);
   if (threadIdx.x == 0) {
@@ -735,6 +836,15 @@ void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
   if (d.n >= 1 && d.m <= kNarrowM)
     launch_pdl(row_update_warps_kernel, dim3(static_cast<unsigned>((d.n + kWarpRows - 1) / kWarpRows)),
                dim3(kRowThreads), 0, s, d, write ? 1 : 0, write ? 0 : 1);
+  else if (d.n >= 1 && d.m <= 1024)
+    launch_pdl(row_update_reg_kernel<1>, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d,
+               write ? 1 : 0, write ? 0 : 1);
+  else if (d.n >= 1 && d.m <= 2048)
+    launch_pdl(row_update_reg_kernel<2>, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d,
+               write ? 1 : 0, write ? 0 : 1);
+  else if (d.n >= 1 && d.m <= 4096)
+    launch_pdl(row_update_reg_kernel<4>, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d,
+               write ? 1 : 0, write ? 0 : 1);
   else if (d.n >= 1)
     launch_pdl(row_update_kernel, dim3(static_cast<unsigned>(d.n)), dim3(kRowThreads), 0, s, d,
                write ? 1 : 0, write ? 0 : 1);

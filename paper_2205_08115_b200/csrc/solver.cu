@@ -433,6 +433,7 @@ void BapgEngine::build_plans() {
       d.f16 = f16;
       if (f16) d.row_scale = f16_g1_rs_;
       d.fuse_planes = !quadratic();  // separate plane passes keep exact ties (see resolve_precision)
+      d.fuse_split_a = center_;
       return gemm_plan_create(d);
     };
     auto gemm2 = [&](const int* skip) {
@@ -455,6 +456,7 @@ void BapgEngine::build_plans() {
       d.col_bias = center_ ? cb2_ : nullptr;
       if (f16) d.col_scale = f16_g2_cs_;
       d.fuse_planes = !quadratic();
+      d.fuse_split_a = center_;
       return gemm_plan_create(d);
     };
     for (int q = 0; q < 2; ++q) {
