@@ -135,13 +135,13 @@ __device__ __forceinline__ float tf32_lo(float x) { return rna_tf32(x - trunc_tf
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ GemmParams p) {
-  // Tile width BN (MMA N): 256, or 128 for grids of few tiles (small n).
+  // Tile width BN (MMA N): 256, or 192 / 128 for grids of few tiles (small n).
   constexpr int kBN_ = BN;
   constexpr int kHalfN_ = BN / 2;                        // B rows loaded per CTA
   constexpr int kSlice_ = BN / 4;                        // accumulator columns per epilogue thread
   constexpr uint32_t kBB_ = kHalfN_ * kBK * 4;
   constexpr uint32_t kStageB_ = kABytes + kBB_;          // per CTA
-  constexpr uint32_t kTmem_ = 2 * BN;                    // double-buffered accumulator
+  constexpr uint32_t kTmem_ = BN == 192 ? 512 : 2 * BN;  // double-buffered accumulator (power of 2)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -370,6 +370,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], __uint_as_float(v[j]));
+        }
+        if constexpr (kSlice_ % 32 != 0) {  // BN = 192: 48 columns = 32 + 16
+          constexpr int h0 = kSlice_ / 32 * 32;
+          uint32_t v[16];
+          ptx::tmem_ld_32x32b_x16(taddr + h0, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[h0 + j] = __fadd_rn(acc[h0 + j], __uint_as_float(v[j]));
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -696,17 +704,27 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
                        static_cast<int>(smem_bytes(256)));
   cudaFuncSetAttribute(gemm_tf32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem_bytes(128)));
+  cudaFuncSetAttribute(gemm_tf32_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem_bytes(192)));
   auto* p = new GemmPlan();
-  // Tile width: 128-wide tiles when even they fill at most one wave of the 74
-  // SM pairs (n ≲ 2000): twice the CTA pairs of 256-wide tiles, each with the
-  // full K, instead of splitting K.  GWB_GEMM_BN=128/256 forces (A/B).
+  // Tile width for grids of a few waves (n ≲ 4000): the width among 256 /
+  // 192 / 128 that minimises waves × width (the time of one pair's tiles)
+  // over the 74 SM pairs, e.g. c2's 48 tiles of 256 (65% of the pairs) become
+  // 64-66 tiles of 192 (c1: 32 tiles of 128).  Large grids keep 256 (best
+  // operand reuse).  GWB_GEMM_BN=128/192/256 forces (A/B).
   {
     static const int bn_env = [] {
       const char* e = std::getenv("GWB_GEMM_BN");
       return e ? std::atoi(e) : 0;
     }();
-    const int64_t t256 = ((d.M + kPairM - 1) / kPairM) * ((d.N + 255) / 256);
-    p->bn = bn_env == 128 || bn_env == 256 ? bn_env : (2 * t256 <= 74 ? 128 : 256);
+    const int64_t tm = (d.M + kPairM - 1) / kPairM;
+    auto cost = [&](int bn) { return (tm * ((d.N + bn - 1) / bn) + 73) / 74 * bn; };
+    int bn = 256;
+    if (tm * ((d.N + 255) / 256) <= 4 * 74) {
+      if (cost(192) < cost(bn)) bn = 192;
+      if (cost(128) < cost(bn)) bn = 128;
+    }
+    p->bn = bn_env == 128 || bn_env == 192 || bn_env == 256 ? bn_env : bn;
   }
   const int halfn = p->bn / 2;
   GemmParams& g = p->params;
@@ -890,9 +908,10 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
 void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
-  cudaError_t e = p->bn == 128
-                      ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
-                      : launch_pdl(gemm_tf32_kernel<256>, dim3(p->grid), dim3(kThreads), smem_bytes(256), s, p->params);
+  cudaError_t e =
+      p->bn == 128   ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
+      : p->bn == 192 ? launch_pdl(gemm_tf32_kernel<192>, dim3(p->grid), dim3(kThreads), smem_bytes(192), s, p->params)
+                     : launch_pdl(gemm_tf32_kernel<256>, dim3(p->grid), dim3(kThreads), smem_bytes(256), s, p->params);
   if (e != cudaSuccess) return e;
   if (p->params.splits > 1 && p->params.counters == nullptr)
     e = launch_pdl(splitk_reduce_kernel, dim3(p->params.M), dim3(256), 0, s, p->params);

@@ -30,8 +30,12 @@ def _gemm(a, b, precision, c=None):
     return Cm[:, :N].double().cpu().numpy()
 
 
+# (1536, 2048, 512) and (1500, 1900, 300) select 192-wide tiles (gemm_plan_create:
+# 48 tiles of 256 vs 60-66 of 192 on 74 SM pairs), the ragged one with a
+# partial last tile; (1000, 1000, 1000) selects 128-wide tiles with split-K.
 @pytest.mark.parametrize("M,N,K", [(128, 256, 32), (256, 512, 256), (1000, 1000, 1000),
-                                   (200, 72, 40), (20, 4000, 20), (4000, 20, 4000)])
+                                   (200, 72, 40), (20, 4000, 20), (4000, 20, 4000),
+                                   (1536, 2048, 512), (1500, 1900, 300)])
 def test_gemm_tf32_exact_operands(gpu, M, N, K):
     # Integer-valued operands are exact in TF32 and sums stay < 2^24: the
     # tensor-core result must be bit-exact.
