@@ -706,6 +706,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
                        static_cast<int>(smem_bytes(128)));
   cudaFuncSetAttribute(gemm_tf32_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem_bytes(192)));
+  cudaFuncSetAttribute(gemm_tf32_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem_bytes(64)));
   auto* p = new GemmPlan();
   // Tile width for grids of a few waves (n ≲ 4000): the width among 256 /
   // 192 / 128 that minimises waves × width (the time of one pair's tiles)
@@ -724,7 +726,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       if (cost(192) < cost(bn)) bn = 192;
       if (cost(128) < cost(bn)) bn = 128;
     }
-    p->bn = bn_env == 128 || bn_env == 192 || bn_env == 256 ? bn_env : bn;
+    p->bn = bn_env == 64 || bn_env == 128 || bn_env == 192 || bn_env == 256 ? bn_env : bn;
   }
   const int halfn = p->bn / 2;
   GemmParams& g = p->params;
@@ -909,7 +911,8 @@ void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
   cudaError_t e =
-      p->bn == 128   ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
+      p->bn == 64    ? launch_pdl(gemm_tf32_kernel<64>, dim3(p->grid), dim3(kThreads), smem_bytes(64), s, p->params)
+      : p->bn == 128 ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
       : p->bn == 192 ? launch_pdl(gemm_tf32_kernel<192>, dim3(p->grid), dim3(kThreads), smem_bytes(192), s, p->params)
                      : launch_pdl(gemm_tf32_kernel<256>, dim3(p->grid), dim3(kThreads), smem_bytes(256), s, p->params);
   if (e != cudaSuccess) return e;

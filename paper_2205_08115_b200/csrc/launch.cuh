@@ -10,7 +10,15 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 namespace gwb {
+
+// GWB_NO_PDL=1 launches everything fully serialised (A/B knob).
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("GWB_NO_PDL") == nullptr;
+  return on;
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -24,7 +32,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
