@@ -50,7 +50,8 @@ constexpr int kEpiWarps = 16;              // 4 lane quadrants × 4 column slice
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kABytes = kBM * kBK * 4;
 constexpr size_t smem_bytes(int bn) {
-  return kStages * (kABytes + static_cast<size_t>(bn / 2) * kBK * 4) + 1024 + 256;
+  // stage ring + alignment slack + barriers / TMEM slot (256) + column staging (2·bn floats)
+  return kStages * (kABytes + static_cast<size_t>(bn / 2) * kBK * 4) + 1024 + 256 + 8 * bn;
 }
 
 // Round-to-nearest split of 8 fp32 values into three planes whose sum is x
@@ -351,10 +352,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = quad * 32;
     const uint32_t col_base = slice * kSlice_;
     const uint32_t tempty_leader[2] = {ptx::mapa(&tempty[0], 0), ptx::mapa(&tempty[1], 0)};
+    // The tile's column bias / scale are staged in shared memory while the
+    // MMAs run, so the final epilogue reads them at SMEM latency instead of
+    // from L2 on the kernel's tail (named barrier 2: the 16 epilogue warps).
+    float* s_cb = reinterpret_cast<float*>(tmem_slot + 4);  // [kBN_]
+    float* s_cs = s_cb + kBN_;                              // [kBN_]
+    const bool stage_cols = p.splits == 1 && (p.col_bias != nullptr || p.col_scale != nullptr);
     int c = 0;
     for (int item = pair; item < items; item += npairs) {
       const Item t = item_of(item);
       const int split = t.split, tn = t.tn, a_row = t.a_row;
+      if (stage_cols) {
+        ptx::named_barrier_sync(2, 32 * kEpiWarps);  // previous tile's epilogue done
+        for (int j = static_cast<int>(threadIdx.x) - 64; j < kBN_; j += 32 * kEpiWarps) {
+          const int col = tn * kBN_ + j;
+          s_cb[j] = p.col_bias != nullptr && col < p.N ? __ldg(p.col_bias + col) : 0.0f;
+          s_cs[j] = p.col_scale != nullptr ? (col < p.N ? __ldg(p.col_scale + col) : 0.0f) : 1.0f;
+        }
+        ptx::named_barrier_sync(2, 32 * kEpiWarps);
+      }
       float acc[kSlice_];
 #pragma unroll
       for (int j = 0; j < kSlice_; ++j) acc[j] = 0.0f;
@@ -433,13 +449,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
         const bool round_out = p.aux_mode == 1;
         const int col0 = tn * kBN_ + static_cast<int>(col_base);
+        if (stage_cols) {
   #pragma unroll
-        for (int j = 0; j < kSlice_; ++j) {
-          float a = acc[j];
-          if (p.col_bias != nullptr) a = __fadd_rn(a, (col0 + j < p.N) ? __ldg(p.col_bias + col0 + j) : 0.0f);
-          float x = a * rs;
-          if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
-          acc[j] = round_out ? rna_tf32(x) : x;
+          for (int j = 0; j < kSlice_; ++j) {
+            float a = acc[j];
+            if (p.col_bias != nullptr) a = __fadd_rn(a, s_cb[col_base + j]);
+            float x = a * rs;
+            if (p.col_scale != nullptr) x *= s_cs[col_base + j];
+            acc[j] = round_out ? rna_tf32(x) : x;
+          }
+        } else {
+  #pragma unroll
+          for (int j = 0; j < kSlice_; ++j) {
+            float a = acc[j];
+            if (p.col_bias != nullptr) a = __fadd_rn(a, (col0 + j < p.N) ? __ldg(p.col_bias + col0 + j) : 0.0f);
+            float x = a * rs;
+            if (p.col_scale != nullptr) x *= (col0 + j < p.N) ? __ldg(p.col_scale + col0 + j) : 0.0f;
+            acc[j] = round_out ? rna_tf32(x) : x;
+          }
         }
         if (p.rs_part != nullptr) {
           double s = 0.0;
