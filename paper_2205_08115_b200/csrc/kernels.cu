@@ -390,6 +390,62 @@ __global__ void __launch_bounds__(kColThreads) col_partial_kernel(BapgDev d, int
   }
 }
 
+// Pass 1 for narrow rows (m ≤ 32, config 3): lane = column, warp w takes the
+// chunk's rows w, w+8, …; the 8 warps' partials merge in fixed order.  (The
+// 128-column layout above leaves 27 of 32 lanes idle at m = 20.)
+__global__ void __launch_bounds__(kColThreads) col_partial_narrow_kernel(BapgDev d, int rows_per_chunk) {
+  pdl_enter();
+  if (d.st->done || d.st->flags) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
+  const double inv_rho = d.inv_rho64;
+  const bool col = lane < d.m;
+  Lse64 ms{-INFINITY, 0.0};
+  double ps = 0.0;
+  if (col) {
+    int64_t i = r0 + warp;
+    for (; i + 3 * (kColThreads / 32) < r1; i += 4 * (kColThreads / 32)) {
+      float g[4];
+      double p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t r = i + u * (kColThreads / 32);
+        g[u] = d.G[r * d.ld + lane];
+        p[u] = d.P64[r * d.ld + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        lse64_add(ms, expo(g[u], inv_rho), p[u]);
+        ps += p[u];
+      }
+    }
+    for (; i < r1; i += kColThreads / 32) {
+      const double p = d.P64[i * d.ld + lane];
+      lse64_add(ms, expo(d.G[i * d.ld + lane], inv_rho), p);
+      ps += p;
+    }
+  }
+  __shared__ double s_mx[kColThreads / 32][32], s_s[kColThreads / 32][32], s_p[kColThreads / 32][32];
+  s_mx[warp][lane] = ms.mx;
+  s_s[warp][lane] = ms.s;
+  s_p[warp][lane] = ps;
+  __syncthreads();
+  if (threadIdx.x < d.m) {
+    const int c = threadIdx.x;
+    Lse64 r{-INFINITY, 0.0};
+    double p = 0.0;
+    for (int q = 0; q < kColThreads / 32; ++q) {
+      r = lse64_merge(r, Lse64{s_mx[q][c], s_s[q][c]});
+      p += s_p[q][c];
+    }
+    const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + c;
+    d.col_pmax[o] = r.mx;
+    d.col_psum[o] = r.s;
+    d.col_psump[o] = p;
+  }
+}
+
 // Half-step b, pass 2: merge chunk partials per column, raise errors.  One
 // warp per column: lanes take the row chunks, then a fixed-order warp merge.
 __global__ void col_combine_kernel(BapgDev d) {
@@ -854,7 +910,11 @@ void launch_col_update(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  if (d.m <= 32)
+    launch_pdl(col_partial_narrow_kernel, dim3(1, static_cast<unsigned>(d.chunks)), dim3(kColThreads), 0,
+               s, d, rows_per_chunk);
+  else
+    launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
   launch_pdl(col_combine_kernel, dim3(grid1d(d.m * 32, 256)), dim3(256), 0, s, d);
   launch_col_write_pass(d, s);
 }
@@ -864,7 +924,11 @@ void launch_col_partial(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  if (d.m <= 32)
+    launch_pdl(col_partial_narrow_kernel, dim3(1, static_cast<unsigned>(d.chunks)), dim3(kColThreads), 0,
+               s, d, rows_per_chunk);
+  else
+    launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
 }
 
 void launch_col_write(const BapgDev& d, cudaStream_t s) {
