@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -302,14 +303,28 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
     return;
   }
   const int device = devs[0];
+  // GWB_PHASE_TIMES=1: wall time of each phase of the call on stderr.
+  static const bool phase_times = std::getenv("GWB_PHASE_TIMES") != nullptr;
+  auto tick = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!phase_times) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "gwb_solve phase %-9s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tick).count());
+    tick = now;
+  };
   BapgEngine eng(device, n, m, cfg->rho, cfg->precision, cfg->max_iters, nullptr);
   eng.set_geometry(cfg->geometry);
+  lap("create");
   if (graphs)
     eng.load_graphs(*graphs, mu, nu);
   else
     eng.load_host(dx, dy, mu, nu);
+  lap("load");
   // Quadratic: π⁰ itself goes to the device, which projects it (reset()).
   eng.reset(initial ? (entropy ? w0.data() : initial) : nullptr);
+  lap("reset");
   gwb::DevStatus s;
   std::vector<double> residuals;
   if (!observer && !cfg->record_residual) {
@@ -330,12 +345,15 @@ void bapg(const gwb_config* cfg, const double* dx, int64_t n, const double* dy, 
     });
     raise_device_flags(s, "bapg");
   }
+  lap("run");
   const int used = s.iter - 1;
   eng.tail();
   fill_trace(o, eng.records(used), used, residuals);
   if (o.converged) *o.converged = s.converged;
   if (o.iterations_used) *o.iterations_used = used;
+  lap("tail");
   eng.outputs(o.out_final, o.out_pi, o.out_w);
+  lap("outputs");
 }
 
 int32_t solve_impl(int32_t expected, const gwb_config* cfg, const double* dx, int64_t n,
