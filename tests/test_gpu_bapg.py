@@ -64,15 +64,18 @@ def test_bapg_er_small(gpu, port, precision):
         assert abs(r.split_gap - q["split_gap"]) <= 1e-3 * q["split_gap"] + 1e-9
 
 
-@pytest.mark.parametrize("precision", ["auto", "3xtf32", "bf16x3", "f16x2", "f16x3"])
+@pytest.mark.parametrize("precision", ["auto", "3xtf32", "bf16x3", "f16x2", "f16x3", "tf32"])
 def test_bapg_gmm_small(gpu, port, precision):
     # Euclidean distances are not exact in bf16 / fp16: bf16x3 and f16x2 must
-    # fall back to 3xTF32; AUTO and f16x3 split both operands.
+    # fall back to 3xTF32; AUTO and f16x3 split both operands.  All of them
+    # run on the centred structure matrices, 1xTF32 included
+    # (the opt-in fast mode: 11-bit operands, held to looser bounds).
     inst = I.config2(seed=1, n=320, m=256)
     rep, o = run_both(port, inst, precision, max_iters=40)
-    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    tf32 = precision == "tf32"
+    assert rel_scale(rep.final_coupling.entries(), o.final) < (2e-3 if tf32 else PI_TOL)
     obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
-    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+    assert abs(obj - obj_ref) <= (2e-4 if tf32 else OBJ_TOL) * abs(obj_ref)
 
 
 def test_bapg_marginal_invariants(gpu):
