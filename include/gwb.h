@@ -40,15 +40,18 @@ enum gwb_geometry { GWB_ENTROPY = 0, GWB_QUADRATIC = 1 };
 enum gwb_axis { GWB_ROWS = 0, GWB_COLS = 1 };
 
 /* Tensor-core precision of the D_X·π·D_Y chain (B200 extension, not in
- * SolverConfig).  All modes keep fp32 iterates and fp32 accumulation.
+ * SolverConfig).  All modes accumulate in fp32; the entropy engines keep
+ * fp64 iterates.
  * AUTO picks, by the exactness of the structure matrices:
  *   - both exact in fp16 (0/1 graphs, small integer weights): F16X2 — in the
- *     BAPG, eBPG / BPG / hBPG and row-sharded engines;
- *   - exact in bf16 only: BF16X3 (also the skinny m ≤ 32 chain and the
- *     batched n, m ≤ 128 kernel for 0/1 graphs);
- *   - otherwise: F16X3 in the single-GPU BAPG engine (fp16 hi/lo planes of
- *     both operands: kind::f16's accumulation carries far less truncation
- *     bias than kind::tf32's), 3XTF32 in the other engines.
+ *     BAPG, eBPG / BPG / hBPG and row-sharded engines and the batched
+ *     n, m ≤ 128 kernel;
+ *   - exact in bf16 only: BF16X3 (also the skinny m ≤ 32 chain for 0/1 D_X);
+ *   - otherwise: F16X3 in the single-GPU BAPG engine, on the centred
+ *     structure matrices D − (max D / 2)·J with the rank-1 parts added back
+ *     exactly (the tensor core's truncating accumulation then has no sign
+ *     bias); 3XTF32 in the other engines (also centred in the single-GPU
+ *     BAPG engine).
  * An explicit split-plane request (F16X2 / BF16X3 / BF16X2) on a D that is
  * not exact in that format falls back F16X2 -> BF16X3 -> 3XTF32, as AUTO
  * would; TF32 (1 pass) and BF16X2 are faster, reduced-precision opt-ins. */
