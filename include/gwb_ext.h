@@ -16,6 +16,11 @@ extern "C" {
  * tcgen05 GEMM (precision: GWB_PREC_TF32 = 1 pass on the given operands,
  * GWB_PREC_3XTF32 = hi/lo split passes computed internally).  `stream` is a
  * cudaStream_t (NULL = legacy default).  Test hook for the K1 kernel. */
+/* Debug (GWB_GEMM_TIMING=1): per-CTA %globaltimer stamps of the last chain
+ * GEMM launch, [ctas][8] ns: entry, prologue done, PDL wait done, first
+ * stage ready, last MMA issued (leader CTA), last chunk drained, stores
+ * done, exit.  *count = CTAs written (0 when timing is off). */
+GWB_API int32_t gwb_debug_gemm_stamps(uint64_t* out, int32_t max_ctas, int32_t* count);
 GWB_API int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b,
                                int64_t ldb, float* c, int64_t ldc, int64_t M,
                                int64_t N, int64_t K, int32_t precision,

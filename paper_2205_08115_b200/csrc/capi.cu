@@ -883,6 +883,11 @@ int32_t gwb_session_destroy(gwb_session* s) {
   return GWB_OK;
 }
 
+int32_t gwb_debug_gemm_stamps(uint64_t* out, int32_t max_ctas, int32_t* count) {
+  *count = gwb::gemm_debug_stamps(reinterpret_cast<unsigned long long*>(out), max_ctas);
+  return GWB_OK;
+}
+
 int32_t gwb_debug_gemm(const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                        int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t precision,
                        void* stream, gwb_status* st) {

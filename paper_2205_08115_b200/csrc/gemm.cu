@@ -111,6 +111,8 @@ struct __align__(64) GemmParams {
   const float* col_bias;  // [N] added before scaling (centred operands)
   double* rs_part;        // [M][rs_stride] fp64 row partial sums of the output
   int32_t rs_stride;      // tiles_n · 4 (one per 64-column slice), 1 with the reduce kernel
+  unsigned long long* stamps;  // GWB_GEMM_TIMING: [grid][8] %globaltimer stamps (debug)
+  int32_t bulk_store;          // epilogue rows leave SMEM by bulk copies (else coalesced st.global)
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -183,14 +185,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     ptx::fence_barrier_init();
   }
+  unsigned long long* const stamp = p.stamps ? p.stamps + blockIdx.x * 8 : nullptr;
+  auto mark = [&](int k) {
+    if (stamp) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamp[k] = t;
+    }
+  };
+  if (threadIdx.x == 0) mark(0);
   if (warp == 1) ptx::tmem_alloc_2sm<kTmem_>(tmem_slot);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) mark(1);
   // PDL: the prologue above overlapped the predecessor kernel; nothing it
   // wrote (operands, the skip flag) is read before this point.
   ptx::griddep_wait();
+  if (threadIdx.x == 0) mark(2);
   ptx::griddep_launch();
   const bool skip = p.skip != nullptr && *p.skip != 0;
   const int items = skip ? 0 : tiles_all * p.splits;
@@ -300,6 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const int s = g % f_stages;
               const uint32_t ph = (g / f_stages) & 1;
               ptx::mbar_wait(&full[s], ph);
+              if (g == 0) mark(3);
               ptx::tc_fence_after();
               const uint32_t st_base = ptx::smem_u32(smem + s * f_stage_bytes);
               // Smallest pass first (the last pass index is the smallest
@@ -343,6 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         g0 += t.total;
       }
+      mark(4);
     }
   } else {
     // Epilogue: warp w (2..17) owns TMEM lanes 32·(w%4).. and columns
@@ -399,7 +414,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[b]);
       }
+      if (warp == 2 && lane == 0) mark(5);
       const int row = a_row + static_cast<int>(lane_base + lane);
+      // Coalesced stores (one pair per tile, i.e. the stage ring is idle once
+      // the last chunk is drained): each warp transposes its 32 rows × kSlice_
+      // columns through shared memory and writes whole row segments, instead
+      // of one 16-B piece of 32 different rows per instruction.
+      const bool staged = npairs >= items && p.counters == nullptr;
+      float* const sw = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * (kSlice_ + 4);
+      auto stage_rows = [&]() {
+        float* r = sw + lane * (kSlice_ + 4);
+#pragma unroll
+        for (int j = 0; j < kSlice_; j += 4) *reinterpret_cast<float4*>(r + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        __syncwarp();
+      };
+      if (staged && p.splits > 1) {
+        // Split-K: raw partial sums to the workspace (reduced by the next kernel).
+        stage_rows();
+        const int col0w = tn * kBN_ + static_cast<int>(col_base);
+        constexpr int cpr = kSlice_ / 4;
+        for (int idx = lane; idx < 32 * cpr; idx += 32) {
+          const int r = idx / cpr, ch = idx - r * cpr;
+          const int grow = a_row + static_cast<int>(lane_base) + r;
+          const int col = col0w + 4 * ch;
+          if (grow < p.M && col < p.ldw)
+            *reinterpret_cast<float4*>(p.ws + static_cast<int64_t>(split) * p.M * p.ldw +
+                                       static_cast<int64_t>(grow) * p.ldw + col) =
+                *reinterpret_cast<const float4*>(sw + r * (kSlice_ + 4) + 4 * ch);
+        }
+        __syncwarp();
+        continue;
+      }
       if (p.splits > 1) {
         // Split-K: raw partial sums to the workspace; the CTA that completes
         // the tile's last split (per-tile arrival counter) then sums the
@@ -445,8 +490,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       if (row < p.M) {
         const float rs = p.row_scale != nullptr ? p.row_scale[row] : 1.0f;
-        float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
-        float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
         const bool round_out = p.aux_mode == 1;
         const int col0 = tn * kBN_ + static_cast<int>(col_base);
         if (stage_cols) {
@@ -475,6 +518,118 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (col0 + j < p.N) s += static_cast<double>(acc[j]);
           p.rs_part[static_cast<int64_t>(row) * p.rs_stride + tn * 4 + static_cast<int>(slice)] = s;
         }
+      }
+      const int col0w_ = tn * kBN_ + static_cast<int>(col_base);
+      if (staged && p.bulk_store && !p.accumulate && p.c_planes <= 2 && col0w_ + kSlice_ <= p.N) {
+        // Whole row segments: each lane stages its own row (fp32, or the
+        // split planes) and one bulk copy per row and output array streams it
+        // to global memory asynchronously.
+        const bool planes = p.c_planes > 0;
+        const bool aligned = planes ? (p.ldc & 7) == 0 : (p.ldc & 3) == 0;
+        if (aligned) {
+          if (row < p.M) {
+            uint8_t* my = reinterpret_cast<uint8_t*>(sw + lane * (kSlice_ + 4));
+            if (planes) {
+              // planes back to back in the row's slot: kSlice_ fp16 each
+#pragma unroll
+              for (int j0 = 0; j0 < kSlice_; j0 += 8) {
+                __align__(16) uint16_t h[3][8];
+                split_planes8(acc + j0, p.c_f16 != 0, h);
+                for (int pl = 0; pl < p.c_planes; ++pl)
+                  *reinterpret_cast<uint4*>(my + pl * kSlice_ * 2 + j0 * 2) = *reinterpret_cast<const uint4*>(h[pl]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < kSlice_; j += 4)
+                *reinterpret_cast<float4*>(my + j * 4) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            }
+            ptx::fence_proxy_async();
+            const int64_t off = static_cast<int64_t>(row) * p.ldc + col0w_;
+            if (planes) {
+              for (int pl = 0; pl < p.c_planes; ++pl)
+                ptx::bulk_s2g(p.c_pl[pl] + off, my + pl * kSlice_ * 2, kSlice_ * 2);
+            } else {
+              ptx::bulk_s2g(p.c + off, my, kSlice_ * 4);
+            }
+            ptx::bulk_commit();
+            if (!planes && p.aux_mode == 2) {
+              // second array (3xTF32 residual operand) after the first left SMEM
+              ptx::bulk_wait_all();
+#pragma unroll
+              for (int j = 0; j < kSlice_; j += 4)
+                *reinterpret_cast<float4*>(my + j * 4) =
+                    make_float4(tf32_lo(acc[j]), tf32_lo(acc[j + 1]), tf32_lo(acc[j + 2]), tf32_lo(acc[j + 3]));
+              ptx::fence_proxy_async();
+              ptx::bulk_s2g(p.c_aux + off, my, kSlice_ * 4);
+              ptx::bulk_commit();
+            }
+            ptx::bulk_wait_all();
+          }
+          continue;
+        }
+      }
+      if (staged) {
+        stage_rows();
+        const int col0w = tn * kBN_ + static_cast<int>(col_base);
+        if (p.c_planes > 0) {
+          constexpr int cpr = kSlice_ / 8;
+          for (int idx = lane; idx < 32 * cpr; idx += 32) {
+            const int r = idx / cpr, ch = idx - r * cpr;
+            const int grow = a_row + static_cast<int>(lane_base) + r;
+            const int col = col0w + 8 * ch;
+            if (grow >= p.M || col >= p.N) continue;
+            __align__(16) uint16_t h[3][8];
+            split_planes8(sw + r * (kSlice_ + 4) + 8 * ch, p.c_f16 != 0, h);
+            const int64_t off = static_cast<int64_t>(grow) * p.ldc + col;
+            const bool vec = col + 8 <= p.N && (p.ldc & 7) == 0;
+            for (int pl = 0; pl < p.c_planes; ++pl) {
+              uint16_t* dst = p.c_pl[pl] + off;
+              if (vec) {
+                *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h[pl]);
+              } else {
+                for (int q = 0; q < 8; ++q)
+                  if (col + q < p.N) dst[q] = h[pl][q];
+              }
+            }
+          }
+        } else {
+          constexpr int cpr = kSlice_ / 4;
+          float* clo_base = p.aux_mode == 2 ? p.c_aux : nullptr;
+          for (int idx = lane; idx < 32 * cpr; idx += 32) {
+            const int r = idx / cpr, ch = idx - r * cpr;
+            const int grow = a_row + static_cast<int>(lane_base) + r;
+            const int col = col0w + 4 * ch;
+            if (grow >= p.M || col >= p.N) continue;
+            float4 v = *reinterpret_cast<const float4*>(sw + r * (kSlice_ + 4) + 4 * ch);
+            float* crow = p.c + static_cast<int64_t>(grow) * p.ldc;
+            float* clo = clo_base ? clo_base + static_cast<int64_t>(grow) * p.ldc : nullptr;
+            if (col + 4 <= p.N && (p.ldc & 3) == 0) {
+              if (p.accumulate) {
+                const float4 o = *reinterpret_cast<const float4*>(crow + col);
+                v = make_float4(__fadd_rn(o.x, v.x), __fadd_rn(o.y, v.y), __fadd_rn(o.z, v.z), __fadd_rn(o.w, v.w));
+              }
+              *reinterpret_cast<float4*>(crow + col) = v;
+              if (clo)
+                *reinterpret_cast<float4*>(clo + col) =
+                    make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+            } else {
+              const float f[4] = {v.x, v.y, v.z, v.w};
+              for (int q = 0; q < 4; ++q) {
+                if (col + q >= p.N) break;
+                const float x = p.accumulate ? __fadd_rn(crow[col + q], f[q]) : f[q];
+                crow[col + q] = x;
+                if (clo) clo[col + q] = tf32_lo(x);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      if (row < p.M) {
+        const int col0 = tn * kBN_ + static_cast<int>(col_base);
+        float* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+        float* clo = p.aux_mode == 2 ? p.c_aux + static_cast<int64_t>(row) * p.ldc : nullptr;
         if (p.c_planes > 0) {
           // Split planes (RN): x ≈ hi + mid (+ lo), bf16 or fp16, for a
           // split-operand GEMM.
@@ -524,12 +679,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp == 2 && lane == 0) mark(6);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<kTmem_>(tmem);
   }
+  if (threadIdx.x == 0) mark(7);
 }
 
 // Split-K reduction + epilogue: one CTA per output row, fixed summation order
@@ -707,6 +864,20 @@ CUtensorMap make_map_blocked(const void* ptr, int64_t rows, int64_t block_k, int
 CUtensorMap gemm_tensor_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                             int esize) {
   return make_map(ptr, rows, cols, ld, box_rows, esize);
+}
+
+// GWB_GEMM_TIMING=1 (debug): every launch writes per-CTA %globaltimer
+// stamps (entry, prologue done, PDL wait done, first stage, last MMA, last
+// chunk drained, stores done, exit) to one device buffer that
+// gwb_debug_gemm_stamps() copies out.
+unsigned long long* g_stamps = nullptr;
+int g_stamps_grid = 0;
+unsigned long long* stamps_buffer() {
+  static const bool on = std::getenv("GWB_GEMM_TIMING") != nullptr;
+  if (!on) return nullptr;
+  if (!g_stamps && cudaMalloc(&g_stamps, sizeof(unsigned long long) * 8 * 1024) != cudaSuccess)
+    g_stamps = nullptr;
+  return g_stamps;
 }
 
 struct GemmPlan {
@@ -921,6 +1092,16 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
       throw std::runtime_error("gemm: row-sum workspace allocation failed");
     g.rs_part = p->rs_part;
   }
+  g.stamps = stamps_buffer();
+  // Epilogue stores (measured A/B, one box, alternating runs): bulk copies of
+  // whole row segments win on 256-wide tiles (c4 @ 8192: 158.5 vs 156.4
+  // it/s), coalesced st.global on the smaller grids (c2, 192-wide: 4576 vs
+  // 4411).  GWB_GEMM_BULK_STORE=0/1 forces.
+  static const int bulk_env = [] {
+    const char* e = std::getenv("GWB_GEMM_BULK_STORE");
+    return e ? std::atoi(e) : -1;
+  }();
+  g.bulk_store = bulk_env >= 0 ? bulk_env : (p->bn == 256 ? 1 : 0);
   const int items = g.tiles_m * g.tiles_n * g.splits;
   static const bool persistent = [] {
     const char* e = std::getenv("GWB_GEMM_PERSISTENT");
@@ -937,6 +1118,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
 void gemm_plan_destroy(GemmPlan* p) { delete p; }
 
 cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
+  if (p->params.stamps) g_stamps_grid = p->grid;
   cudaError_t e =
       p->bn == 64    ? launch_pdl(gemm_tf32_kernel<64>, dim3(p->grid), dim3(kThreads), smem_bytes(64), s, p->params)
       : p->bn == 128 ? launch_pdl(gemm_tf32_kernel<128>, dim3(p->grid), dim3(kThreads), smem_bytes(128), s, p->params)
@@ -947,6 +1129,14 @@ cudaError_t gemm_launch(const GemmPlan* p, cudaStream_t s) {
     e = launch_pdl(splitk_reduce_kernel, dim3(p->params.M), dim3(256), 0, s, p->params);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+int gemm_debug_stamps(unsigned long long* out, int max_ctas) {
+  if (!g_stamps) return 0;
+  const int n = std::min(max_ctas, std::min(g_stamps_grid, 1024));
+  if (cudaMemcpy(out, g_stamps, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  return n;
 }
 
 cudaError_t gemm_rowsum_bias(const GemmPlan* p, double factor, float* out, cudaStream_t s) {

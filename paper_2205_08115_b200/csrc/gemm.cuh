@@ -106,5 +106,8 @@ int gemm_launches(const GemmPlan* p);
 // of the plan's row partials in a fixed order, rounded to fp32).  Needs
 // GemmDesc::rowsums; one launch, a no-op when the plan's skip flag is set.
 cudaError_t gemm_rowsum_bias(const GemmPlan* p, double factor, float* out, cudaStream_t s);
+// Debug (GWB_GEMM_TIMING=1): copies the last timed launch's per-CTA stamps
+// ([ctas][8] %globaltimer ns) to `out`; returns the CTA count (0 if none).
+int gemm_debug_stamps(unsigned long long* out, int max_ctas);
 
 }  // namespace gwb
