@@ -32,10 +32,14 @@ def _gemm(a, b, precision, c=None):
 
 # (1536, 2048, 512) and (1500, 1900, 300) select 192-wide tiles (gemm_plan_create:
 # 48 tiles of 256 vs 60-66 of 192 on 74 SM pairs), the ragged one with a
-# partial last tile; (1000, 1000, 1000) selects 128-wide tiles with split-K.
+# partial last tile; (1000, 1000, 1000) selects 128-wide tiles with split-K;
+# (5000, 5000, 64) and (4500, 4700, 96) keep 256-wide tiles (> 4 waves), whose
+# epilogue writes rows by bulk copies — the ragged one also takes the direct
+# store path on its partial last column tile.
 @pytest.mark.parametrize("M,N,K", [(128, 256, 32), (256, 512, 256), (1000, 1000, 1000),
                                    (200, 72, 40), (20, 4000, 20), (4000, 20, 4000),
-                                   (1536, 2048, 512), (1500, 1900, 300)])
+                                   (1536, 2048, 512), (1500, 1900, 300),
+                                   (5000, 5000, 64), (4500, 4700, 96)])
 def test_gemm_tf32_exact_operands(gpu, M, N, K):
     # Integer-valued operands are exact in TF32 and sums stay < 2^24: the
     # tensor-core result must be bit-exact.
