@@ -557,14 +557,36 @@ def run_sharded_e2e(args, world, rank, local, dist, edges, tgt, prec):
     from paper_2205_08115_b200 import abi
     from paper_2205_08115_b200 import dist as D
     n = args.n
-    dx = HostRows(n, edges)
-    dy = HostRows(n, tgt)[0:n]
+    # The user's inputs, in page-locked host memory before the timed region
+    # (as the single-GPU e2e): this rank's rows of D_X, and D_Y.
+    plan = D.ShardPlan(n, world)
+    rb, rv = plan.row_begin(rank), plan.rows_valid(rank)
+
+    def pinned_copy(a):
+        t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    class RankRows:
+        """dx[rb:rb + rv] of this rank, already built (solve_sharded slices it)."""
+
+        def __init__(self, rows):
+            self.rows = rows
+
+        def __getitem__(self, sl):
+            assert sl.start == rb and min(sl.stop, n) == rb + rv, (sl, rb, rv)
+            return self.rows
+
+    dx = RankRows(pinned_copy(HostRows(n, edges)[rb:rb + rv]))
+    dy = pinned_copy(HostRows(n, tgt)[0:n])
+    out_pi, out_w = (torch.empty((rv, n), dtype=torch.float64, pin_memory=True).numpy()
+                     for _ in range(2))
     u = np.full(n, 1.0 / n)
     cfg = abi.default_config(rho=0.1, max_iters=args.e2e_iters, rel_tol=1e-30, precision=prec)
     dist.barrier()
     t0 = time.perf_counter()
     r = D.solve_sharded(cfg, dx, dy, u, u, dist, rank, world, local,
-                        overlap=not args.no_overlap)
+                        overlap=not args.no_overlap, out_pi=out_pi, out_w=out_w)
     dt = time.perf_counter() - t0
     t = torch.tensor([dt], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)

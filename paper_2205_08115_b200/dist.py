@@ -202,11 +202,17 @@ class GpuShard:
         _check(st)
         return list(out[:count])
 
-    def rows(self):
+    def rows(self, out_pi=None, out_w=None):
+        """This rank's rows of π and w (fp64, rows_valid × m), into the
+        caller's arrays when given (e.g. page-locked, allocated once)."""
         import numpy as np
         st = abi.Status()
-        pi = np.zeros((self.rows_valid, self.m))
-        w = np.zeros((self.rows_valid, self.m))
+        shape = (self.rows_valid, self.m)
+        pi = out_pi if out_pi is not None else np.empty(shape)
+        w = out_w if out_w is not None else np.empty(shape)
+        for a in (pi, w):
+            if a.shape != shape or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError(f"rows: output must be a C-contiguous float64 array of shape {shape}")
         self.lib.gwb_shard_rows(self.h, pi.ctypes.data, w.ctypes.data, C.byref(st))
         _check(st)
         return pi, w
@@ -607,7 +613,8 @@ def run_sharded(shards: List, comm, iters: int, poll_every: int = 16,
 
 
 def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
-                  device: int = 0, poll_every: int = 16, overlap: bool = True) -> dict:
+                  device: int = 0, poll_every: int = 16, overlap: bool = True,
+                  out_pi=None, out_w=None) -> dict:
     """Row-sharded BAPG from HOST inputs — the public multi-GPU entry, called
     by every rank of a torch.distributed (NCCL) job with the same arguments.
 
@@ -615,8 +622,9 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
     array, a memmap, or a lazy row builder), so a rank only materialises its
     own rows of D_X; `dy`, `mu`, `nu` are full host arrays.  The rank uploads
     its rows, runs the solve (bapg_solve semantics, solvers.cpp:138-217) and
-    returns its rows of π and w (fp64), the agreed trace, convergence flag
-    and iteration count.  Errors raise the reference exception on every rank.
+    returns its rows of π and w (fp64; written into `out_pi` / `out_w` when
+    given, rows_valid × m), the agreed trace, convergence flag and iteration
+    count.  Errors raise the reference exception on every rank.
     """
     import numpy as np
     import torch
@@ -649,7 +657,7 @@ def solve_sharded(cfg: abi.Config, dx, dy, mu, nu, dist, rank: int, world: int,
         raise_shard_flags(st)
         used = st["iter"] - 1
         recs = shard.records(used)
-        pi, w = shard.rows()
+        pi, w = shard.rows(out_pi, out_w)
         return {"pi_rows": pi, "w_rows": w, "row_begin": rb, "trace": recs,
                 "converged": bool(st["converged"]), "iterations_used": used,
                 "launches": shard.launches()}
