@@ -113,6 +113,7 @@ struct __align__(64) GemmParams {
   int32_t rs_stride;      // tiles_n · 4 (one per 64-column slice), 1 with the reduce kernel
   unsigned long long* stamps;  // GWB_GEMM_TIMING: [grid][8] %globaltimer stamps (debug)
   int32_t bulk_store;          // epilogue rows leave SMEM by bulk copies (else coalesced st.global)
+  int32_t a_const;             // A tiles of the first ring fill requested before the PDL wait
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) {
@@ -200,13 +201,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) mark(1);
-  // PDL: the prologue above overlapped the predecessor kernel; nothing it
-  // wrote (operands, the skip flag) is read before this point.
-  ptx::griddep_wait();
-  if (threadIdx.x == 0) mark(2);
-  ptx::griddep_launch();
-  const bool skip = p.skip != nullptr && *p.skip != 0;
-  const int items = skip ? 0 : tiles_all * p.splits;
 
   const int kblk = p.kind ? kBK16 : kBK;  // elements per 128-B k-block
   const int kblocks_all = (p.K + kblk - 1) / kblk;
@@ -239,8 +233,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     return t;
   };
 
+  // A constant A operand (the structure matrix) does not depend on the
+  // predecessor kernel: the producer requests the A tiles of its first ring
+  // fill before the PDL wait (only the expected bytes, no arrival yet; the
+  // B tiles and the arrival follow the wait), so the first stage is not a
+  // full TMA round trip behind the predecessor's last store.
+  const bool elected0 = warp == 0 && ptx::elect_one();
+  int pre = 0;
+  if (p.a_const && p.fused && elected0 && pair < tiles_all * p.splits) {
+    const Item t0 = item_of(pair);
+    pre = min(f_stages, t0.total);
+    for (int it = 0; it < pre; ++it) {
+      const int kb = t0.kb_begin + it;
+      const uint32_t fbar = ptx::mapa(&full[it], 0);
+      if (leader) ptx::mbar_expect_tx(&full[it], 2 * f_a_bytes);
+      for (int pa = 0; pa < p.a_planes; ++pa)
+        ptx::tma_load_2d_2sm(smem + it * f_stage_bytes + pa * kABytes, &p.a_map[pa], fbar, kb * kblk,
+                             t0.a_row);
+    }
+  }
+  // PDL: the prologue above overlapped the predecessor kernel; nothing it
+  // wrote (B operands, the skip flag) is read before this point.
+  ptx::griddep_wait();
+  if (threadIdx.x == 0) mark(2);
+  ptx::griddep_launch();
+  const bool skip = p.skip != nullptr && *p.skip != 0;
+  const int items = skip ? 0 : tiles_all * p.splits;
+  if (skip && pre > 0) {
+    // Skipped launch: arrive on the prefetched stages and let their A
+    // tiles land before the CTA (and its peer) can exit.
+    for (int it = 0; it < pre; ++it) {
+      if (leader) {
+        ptx::mbar_arrive(&full[it]);
+        ptx::mbar_wait(&full[it], 0);
+      }
+    }
+  }
+
   if (warp == 0) {
-    if (ptx::elect_one()) {
+    if (elected0) {
       int g = 0;  // stage iterations issued so far (all items)
       for (int item = pair; item < items; item += npairs) {
         const Item t = item_of(item);
@@ -250,13 +281,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int it = 0; it < t.total; ++it, ++g) {
             const int s = g % f_stages;
             const uint32_t ph = (g / f_stages) & 1;
-            ptx::mbar_wait(&empty[s], ph ^ 1);
             const int kb = t.kb_begin + it;
             const uint32_t fbar = ptx::mapa(&full[s], 0);
             uint8_t* st = smem + s * f_stage_bytes;
-            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
-            for (int pa = 0; pa < p.a_planes; ++pa)
-              ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, t.a_row);
+            if (g < pre) {  // A already requested before the PDL wait
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * (f_stage_bytes - f_a_bytes));
+            } else {
+              ptx::mbar_wait(&empty[s], ph ^ 1);
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * f_stage_bytes);
+              for (int pa = 0; pa < p.a_planes; ++pa)
+                ptx::tma_load_2d_2sm(st + pa * kABytes, &p.a_map[pa], fbar, kb * kblk, t.a_row);
+            }
             for (int pl = 0; pl < p.b_planes; ++pl) {
               void* dst = st + f_a_bytes + pl * kBB_;
               if (p.b_block_k > 0) {
@@ -1102,6 +1137,8 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     return e ? std::atoi(e) : -1;
   }();
   g.bulk_store = bulk_env >= 0 ? bulk_env : (p->bn == 256 ? 1 : 0);
+  static const bool no_prefetch = std::getenv("GWB_GEMM_NO_A_PREFETCH") != nullptr;
+  g.a_const = d.a_const && !no_prefetch ? 1 : 0;
   const int items = g.tiles_m * g.tiles_n * g.splits;
   static const bool persistent = [] {
     const char* e = std::getenv("GWB_GEMM_PERSISTENT");

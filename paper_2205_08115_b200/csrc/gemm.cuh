@@ -83,6 +83,10 @@ struct GemmDesc {
   // for centred operands: on all-positive terms the 48-MMA chunks measured a
   // 3× larger truncation bias than separate pass stages.
   bool fuse_split_a = false;
+  // A is a constant operand (a structure matrix), not written by the kernel
+  // launched before this GEMM: its first stages are requested before the
+  // programmatic-dependent-launch wait (fused schedule).
+  bool a_const = false;
 };
 
 // 2-D TMA descriptor of a row-major rows×cols matrix (leading dim ld

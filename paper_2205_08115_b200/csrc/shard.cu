@@ -560,6 +560,7 @@ class ShardEngine {
 
   GemmPlan* make1(float* X, float* X_aux, const int* skip) {
     GemmDesc d;
+    d.a_const = true;  // A = a structure matrix (constant)
     d.M = m_;
     d.N = nr_;
     d.K = m_;
@@ -595,6 +596,7 @@ class ShardEngine {
   // local D_X rows starting at src·n_r, B = that rank's slot (plain 2-D).
   GemmPlan* make2_chunk(int src, const int* skip) {
     GemmDesc d;
+    d.a_const = true;  // A = a structure matrix (constant)
     d.M = nr_;
     d.N = m_;
     d.K = nr_;
@@ -626,6 +628,7 @@ class ShardEngine {
 
   GemmPlan* make2(const int* skip) {
     GemmDesc d;
+    d.a_const = true;  // A = a structure matrix (constant)
     d.M = nr_;
     d.N = m_;
     d.K = nr_ * world_;

@@ -410,6 +410,7 @@ void BapgEngine::build_plans() {
     };
     auto gemm1 = [&](float* X_aux, const float* bias, const int* skip) {
       GemmDesc d;
+      d.a_const = true;  // A = a structure matrix (constant)
       d.M = m_;
       d.N = n_;
       d.K = m_;
@@ -438,6 +439,7 @@ void BapgEngine::build_plans() {
     };
     auto gemm2 = [&](const int* skip) {
       GemmDesc d;
+      d.a_const = true;  // A = a structure matrix (constant)
       d.M = n_;
       d.N = m_;
       d.K = n_;
@@ -492,6 +494,7 @@ void BapgEngine::build_plans() {
   }
   auto gemm1 = [&](float* X, float* X_aux, const float* bias, const int* skip) {
     GemmDesc d;
+    d.a_const = true;  // A = a structure matrix (constant)
     d.M = m_;
     d.N = n_;
     d.K = m_;
@@ -513,6 +516,7 @@ void BapgEngine::build_plans() {
   };
   auto gemm2 = [&](const int* skip) {
     GemmDesc d;
+    d.a_const = true;  // A = a structure matrix (constant)
     d.M = n_;
     d.N = m_;
     d.K = n_;
