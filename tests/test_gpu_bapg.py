@@ -78,6 +78,28 @@ def test_bapg_gmm_small(gpu, port, precision):
     assert abs(obj - obj_ref) <= (2e-4 if tf32 else OBJ_TOL) * abs(obj_ref)
 
 
+@pytest.mark.parametrize("precision", ["auto", "3xtf32"])
+def test_bapg_weighted_ragged_nonuniform(gpu, port, precision):
+    # The centred chain on sizes that are not multiples of the
+    # tiles, with non-uniform marginals: the rank-1 biases use rowsum(w) from
+    # the column write pass and rowsum(π) = μ, and GEMM2's bias comes from
+    # GEMM1's row partials over ragged tiles.
+    rng = np.random.default_rng(11)
+    base = I.config2(seed=5, n=333, m=201)
+    mu = rng.uniform(0.2, 1.8, base.n)
+    nu = rng.uniform(0.2, 1.8, base.m)
+    inst = I.Instance("gmm_ragged", base.dx, base.dy, mu / mu.sum(), nu / nu.sum(), dict(base.solver))
+    rep, o = run_both(port, inst, precision, max_iters=50)
+    assert rel_scale(rep.final_coupling.entries(), o.final) < PI_TOL
+    assert rel_scale(rep.pi_half.entries(), o.pi) < PI_TOL
+    obj, obj_ref = rep.trace[-1].objective, o.trace[-1]["objective"]
+    assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref)
+    for r, q in zip(rep.trace, o.trace):
+        assert abs(r.objective - q["objective"]) <= 2e-4 * abs(q["objective"])
+        assert abs(r.marginal_infeasibility - q["marginal_infeasibility"]) <= \
+            1e-3 * q["marginal_infeasibility"] + 1e-9
+
+
 def test_bapg_marginal_invariants(gpu):
     inst = I.config1(seed=5, n=160)
     rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
