@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -826,17 +827,32 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
     return;
   }
   pool_keep(device);
-  cudaStream_t s;
+  // Streams: `s` stages the inputs (and owns the allocations), sc[0/1] run
+  // alternate sub-chunks (pack, kernel, fix-up; a sub-chunk's kernel can start
+  // while the previous one drains its last problems), `so` returns results.
+  // H2D of sub-chunk c+1 and D2H of sub-chunk c-1 overlap sub-chunk c's kernel.
+  cudaStream_t s, sc[2], so;
   GWB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  GWB_CUDA(cudaStreamCreateWithFlags(&sc[0], cudaStreamNonBlocking));
+  GWB_CUDA(cudaStreamCreateWithFlags(&sc[1], cudaStreamNonBlocking));
+  GWB_CUDA(cudaStreamCreateWithFlags(&so, cudaStreamNonBlocking));
   struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{s};
+    cudaStream_t s[4];
+    ~StreamGuard() {
+      for (auto x : s) cudaStreamDestroy(x);
+    }
+  } sg{{s, sc[0], sc[1], so}};
   int sms = 148;
   GWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   // Bound the device working set: problems are processed in chunks.
   const int64_t chunk = std::min<int64_t>(batch, 16384);
   const size_t len = static_cast<size_t>(n) * m;
+  constexpr int kSub = 8;  // max pipelined sub-chunks per chunk (each ≥ one wave)
+  static const int sub_env = [] {
+    const char* e = std::getenv("GWB_BATCHED_SUB");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
+  }();
+  const int sub_req = sub_env ? sub_env : 4;
   DevBuf<double> d_dx(chunk * n * n, s), d_dy(chunk * m * m, s), d_mu(chunk * n, s),
       d_nu(chunk * m, s);
   DevBuf<uint8_t> d_pack(chunk * 2 * kTileBytes, s);
@@ -847,40 +863,101 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
   DevBuf<BatchStatus> d_st(chunk, s);
   DevBuf<double> d_pi(out_pi ? chunk * len : 0, s), d_w(out_w ? chunk * len : 0, s),
       d_fin(chunk * len, s);
-  DevBuf<int> d_inexact(1, s), d_next(1, s);
+  DevBuf<int> d_inexact(1, s), d_next(kSub, s);
   GWB_CUDA(cudaFuncSetAttribute(bapg_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmem)));
-  cudaEvent_t ev0, ev1;
-  GWB_CUDA(cudaEventCreate(&ev0));
-  GWB_CUDA(cudaEventCreate(&ev1));
+  std::vector<cudaEvent_t> evs;
+  auto event = [&](bool timing) {
+    cudaEvent_t e;
+    GWB_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    evs.push_back(e);
+    return e;
+  };
   struct EventGuard {
-    cudaEvent_t a, b;
+    std::vector<cudaEvent_t>* v;
     ~EventGuard() {
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
+      for (auto e : *v) cudaEventDestroy(e);
     }
-  } eg{ev0, ev1};
+  } eg{&evs};
   std::vector<BatchStatus> hst(chunk);
   std::vector<DevRecord> hrec(trace ? chunk * (cfg->max_iters + 2) : 0);
   std::vector<HostRecord> hr(trace ? cfg->max_iters + 1 : 0);
   Failure first;
   for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
     const int64_t cb = std::min(chunk, batch - b0);
-    GWB_CUDA(cudaMemcpyAsync(d_dx.p, dx + b0 * n * n, sizeof(double) * cb * n * n, cudaMemcpyHostToDevice, s));
-    GWB_CUDA(cudaMemcpyAsync(d_dy.p, dy + b0 * m * m, sizeof(double) * cb * m * m, cudaMemcpyHostToDevice, s));
-    GWB_CUDA(cudaMemcpyAsync(d_mu.p, mu + b0 * n, sizeof(double) * cb * n, cudaMemcpyHostToDevice, s));
-    GWB_CUDA(cudaMemcpyAsync(d_nu.p, nu + b0 * m, sizeof(double) * cb * m, cudaMemcpyHostToDevice, s));
+    const int nsub = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sub_req, cb / sms)));
     GWB_CUDA(cudaMemsetAsync(d_inexact.p, 0, sizeof(int), s));
-    batched_pack_kernel<<<dim3(static_cast<unsigned>(cb), 2), 256, 0, s>>>(
-        d_dx.p, d_dy.p, d_mu.p, d_nu.p, static_cast<int>(n), static_cast<int>(m), d_pack.p,
-        d_mup.p, d_nup.p, d_scl.p, d_inexact.p);
-    GWB_CUDA(cudaGetLastError());
+    GWB_CUDA(cudaMemsetAsync(d_next.p, 0, sizeof(int) * kSub, s));
+    const cudaEvent_t ready = event(false);  // allocations and resets done
+    GWB_CUDA(cudaEventRecord(ready, s));
+    for (auto x : {sc[0], sc[1], so}) GWB_CUDA(cudaStreamWaitEvent(x, ready, 0));
+    const cudaEvent_t k0 = event(true);
+    std::vector<cudaEvent_t> kend(nsub);
+    for (int c = 0; c < nsub; ++c) {
+      const int64_t c0 = cb * c / nsub, c1 = cb * (c + 1) / nsub, cc = c1 - c0;
+      const int64_t g0 = b0 + c0;  // problem index of the sub-chunk's first problem
+      GWB_CUDA(cudaMemcpyAsync(d_dx.p + c0 * n * n, dx + g0 * n * n, sizeof(double) * cc * n * n, cudaMemcpyHostToDevice, s));
+      GWB_CUDA(cudaMemcpyAsync(d_dy.p + c0 * m * m, dy + g0 * m * m, sizeof(double) * cc * m * m, cudaMemcpyHostToDevice, s));
+      GWB_CUDA(cudaMemcpyAsync(d_mu.p + c0 * n, mu + g0 * n, sizeof(double) * cc * n, cudaMemcpyHostToDevice, s));
+      GWB_CUDA(cudaMemcpyAsync(d_nu.p + c0 * m, nu + g0 * m, sizeof(double) * cc * m, cudaMemcpyHostToDevice, s));
+      const cudaEvent_t in = event(false);
+      GWB_CUDA(cudaEventRecord(in, s));
+      const cudaStream_t cs = sc[c & 1];
+      GWB_CUDA(cudaStreamWaitEvent(cs, in, 0));
+      batched_pack_kernel<<<dim3(static_cast<unsigned>(cc), 2), 256, 0, cs>>>(
+          d_dx.p + c0 * n * n, d_dy.p + c0 * m * m, d_mu.p + c0 * n, d_nu.p + c0 * m, static_cast<int>(n),
+          static_cast<int>(m), d_pack.p + c0 * 2 * kTileBytes, d_mup.p + c0 * kT, d_nup.p + c0 * kT,
+          d_scl.p + c0, d_inexact.p);
+      GWB_CUDA(cudaGetLastError());
+      BatchArgs a;
+      a.dpack = d_pack.p + c0 * 2 * kTileBytes;
+      a.mu = d_mup.p + c0 * kT;
+      a.nu = d_nup.p + c0 * kT;
+      a.scl = d_scl.p + c0;
+      a.P = d_P.p + c0 * kT * kT;
+      a.W = d_W.p + c0 * kT * kT;
+      a.rec = trace ? d_rec.p + c0 * (cfg->max_iters + 2) : nullptr;
+      a.st = d_st.p + c0;
+      a.next = d_next.p + c;
+      a.batch = static_cast<int>(cc);
+      a.n = static_cast<int>(n);
+      a.m = static_cast<int>(m);
+      a.max_iters = cfg->max_iters;
+      a.inv_rho = static_cast<float>(1.0 / cfg->rho);
+      a.rel_tol = cfg->rel_tol;
+      if (c == 0) GWB_CUDA(cudaEventRecord(k0, cs));
+      bapg_batched_kernel<<<static_cast<unsigned>(std::min<int64_t>(cc, sms)), kThreads, kSmem, cs>>>(a);
+      GWB_CUDA(cudaGetLastError());
+      kend[c] = event(true);
+      GWB_CUDA(cudaEventRecord(kend[c], cs));
+      batched_fixup_kernel<<<static_cast<unsigned>(cc), kT, 0, cs>>>(
+          a.P, a.W, a.mu, a.nu, static_cast<int>(n), static_cast<int>(m),
+          out_pi ? d_pi.p + c0 * len : nullptr, out_w ? d_w.p + c0 * len : nullptr, d_fin.p + c0 * len);
+      GWB_CUDA(cudaGetLastError());
+      const cudaEvent_t done = event(false);
+      GWB_CUDA(cudaEventRecord(done, cs));
+      GWB_CUDA(cudaStreamWaitEvent(so, done, 0));
+      GWB_CUDA(cudaMemcpyAsync(out_final + g0 * len, d_fin.p + c0 * len, sizeof(double) * cc * len, cudaMemcpyDeviceToHost, so));
+      if (out_pi) GWB_CUDA(cudaMemcpyAsync(out_pi + g0 * len, d_pi.p + c0 * len, sizeof(double) * cc * len, cudaMemcpyDeviceToHost, so));
+      if (out_w) GWB_CUDA(cudaMemcpyAsync(out_w + g0 * len, d_w.p + c0 * len, sizeof(double) * cc * len, cudaMemcpyDeviceToHost, so));
+    }
+    GWB_CUDA(cudaMemcpyAsync(hst.data(), d_st.p, sizeof(BatchStatus) * cb, cudaMemcpyDeviceToHost, so));
+    if (trace)
+      GWB_CUDA(cudaMemcpyAsync(hrec.data(), d_rec.p, sizeof(DevRecord) * cb * (cfg->max_iters + 2), cudaMemcpyDeviceToHost, so));
     int inexact = 0;
-    GWB_CUDA(cudaMemcpyAsync(&inexact, d_inexact.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    GWB_CUDA(cudaStreamSynchronize(s));
+    GWB_CUDA(cudaMemcpyAsync(&inexact, d_inexact.p, sizeof(int), cudaMemcpyDeviceToHost, so));
+    for (auto x : {s, sc[0], sc[1], so}) GWB_CUDA(cudaStreamSynchronize(x));
+    // Device time of the chunk's solve: first kernel start → last kernel end.
+    float kms = 0.f;
+    for (int c = 0; c < nsub; ++c) {
+      float t = 0.f;
+      GWB_CUDA(cudaEventElapsedTime(&t, k0, kend[c]));
+      kms = std::max(kms, t);
+    }
     if (inexact) {
       // Structure matrices not exact in fp16: the on-chip kernel keeps D in
-      // one fp16 plane, so these problems take the generic engine.
+      // one fp16 plane, so these problems take the generic engine (its
+      // results overwrite the on-chip ones).
       const BatchedOut sub{out_final + b0 * len, out_pi ? out_pi + b0 * len : nullptr,
                            out_w ? out_w + b0 * len : nullptr,
                            trace ? trace + b0 * trace_cap : nullptr, trace_cap,
@@ -892,41 +969,6 @@ void device_bapg_batched(const gwb_config* cfg, int64_t batch, const double* dx,
       if (first.problem < 0 && f.problem >= 0) first = f;
       continue;
     }
-    BatchArgs a;
-    a.dpack = d_pack.p;
-    a.mu = d_mup.p;
-    a.nu = d_nup.p;
-    a.scl = d_scl.p;
-    a.P = d_P.p;
-    a.W = d_W.p;
-    a.rec = trace ? d_rec.p : nullptr;
-    a.st = d_st.p;
-    a.next = d_next.p;
-    GWB_CUDA(cudaMemsetAsync(d_next.p, 0, sizeof(int), s));
-    a.batch = static_cast<int>(cb);
-    a.n = static_cast<int>(n);
-    a.m = static_cast<int>(m);
-    a.max_iters = cfg->max_iters;
-    a.inv_rho = static_cast<float>(1.0 / cfg->rho);
-    a.rel_tol = cfg->rel_tol;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(cb, sms));
-    GWB_CUDA(cudaEventRecord(ev0, s));
-    bapg_batched_kernel<<<grid, kThreads, kSmem, s>>>(a);
-    GWB_CUDA(cudaGetLastError());
-    GWB_CUDA(cudaEventRecord(ev1, s));
-    batched_fixup_kernel<<<static_cast<unsigned>(cb), kT, 0, s>>>(
-        d_P.p, d_W.p, d_mup.p, d_nup.p, static_cast<int>(n), static_cast<int>(m),
-        out_pi ? d_pi.p : nullptr, out_w ? d_w.p : nullptr, d_fin.p);
-    GWB_CUDA(cudaGetLastError());
-    GWB_CUDA(cudaMemcpyAsync(out_final + b0 * len, d_fin.p, sizeof(double) * cb * len, cudaMemcpyDeviceToHost, s));
-    if (out_pi) GWB_CUDA(cudaMemcpyAsync(out_pi + b0 * len, d_pi.p, sizeof(double) * cb * len, cudaMemcpyDeviceToHost, s));
-    if (out_w) GWB_CUDA(cudaMemcpyAsync(out_w + b0 * len, d_w.p, sizeof(double) * cb * len, cudaMemcpyDeviceToHost, s));
-    GWB_CUDA(cudaMemcpyAsync(hst.data(), d_st.p, sizeof(BatchStatus) * cb, cudaMemcpyDeviceToHost, s));
-    if (trace)
-      GWB_CUDA(cudaMemcpyAsync(hrec.data(), d_rec.p, sizeof(DevRecord) * cb * (cfg->max_iters + 2), cudaMemcpyDeviceToHost, s));
-    GWB_CUDA(cudaStreamSynchronize(s));
-    float kms = 0.f;
-    GWB_CUDA(cudaEventElapsedTime(&kms, ev0, ev1));
     ms_total += kms;
     for (int64_t k = 0; k < cb; ++k) {
       const BatchStatus& st = hst[k];
