@@ -1005,18 +1005,42 @@ def hbpg_full(n, peaks, tf32, iters=200, switch=100):
     gw.solve from host fp64 buffers.  value = iterations ÷ the device trace
     clock (reset → last record); e2e = iterations ÷ the call's wall time
     (6.4 GB H2D of D_X, D_Y and the coupling D2H included)."""
+    import torch
     import paper_2205_08115_b200 as gw
+    from paper_2205_08115_b200 import abi
     from harness import instances as I
     inst = I.config4(n=n, algorithm="hbpg")
     s = dict(inst.solver)
     s.update(max_iters=iters, switch_iters=switch)
-    cfg = gw.SolverConfig(quiet=True, **s)
-    a = (gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
-         gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu))
+    cfg = gw.SolverConfig(quiet=True, **s).to_abi()
+
+    def pinned(a):
+        # Page-locked host buffers, filled outside the timed region (as the
+        # BAPG e2e): the user's fp64 column-major inputs and the output.
+        t = torch.empty(a.size, dtype=torch.float64, pin_memory=True)
+        v = t.numpy().reshape(a.shape, order="F")
+        v[...] = a
+        return v
+
+    dx, dy = pinned(inst.dx), pinned(inst.dy)
+    out = pinned(np.zeros((n, n)))
+    trace = (abi.Record * cfg.max_iters)()
+    nr, cv, used = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    lib = abi.load()
+    Dp = C.POINTER(C.c_double)
+    ptr = lambda a: a.ctypes.data_as(Dp)
+    st = abi.Status()
     t0 = time.perf_counter()
-    rep = gw.solve(*a, cfg)
+    lib.gwb_solve(C.byref(cfg), ptr(dx), n, ptr(dy), n, ptr(inst.mu), ptr(inst.nu), None,
+                  abi.OBSERVER(), None, ptr(out), None, None, trace, cfg.max_iters, C.byref(nr),
+                  C.byref(cv), C.byref(used), C.byref(st))
     wall = time.perf_counter() - t0
-    tr = rep.trace
+    abi.raise_for(st)
+    tr = list(trace)[:used.value]
+
+    class _Rep:
+        iterations_used = used.value
+    rep = _Rep()
     dev_s = tr[-1].elapsed_seconds
     its = rep.iterations_used / dev_s
     flops = 2.0 * n * n * (n + n)            # one chain per outer iteration
@@ -1026,6 +1050,7 @@ def hbpg_full(n, peaks, tf32, iters=200, switch=100):
     rl = roofline_its(flops, nbytes, P, bw)
     out = {"value": its, "unit": "it/s", "iterations": rep.iterations_used,
            "phases": {"ebpg": sum(r.phase == 1 for r in tr), "bpg": sum(r.phase == 2 for r in tr)},
+           "call": "gwb_solve (C-ABI), pinned fp64 host buffers",
            "device_s": dev_s, "objective": tr[-1].objective,
            "roofline": {"its": rl, "frac": its / rl, "peak_tflops": P, "hbm_gbs": bw,
                         "model": "T = F_alg / P_exec + B_alg / BW_HBM (F = one chain, B = 96nm)"},

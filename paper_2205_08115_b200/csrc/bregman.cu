@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -583,6 +584,18 @@ class BregmanEngine {
       GWB_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
       own_stream_ = true;
     }
+    pool_keep(dev_);
+    {
+      // Grow the pool once by (an upper bound of) the engine's workspace and
+      // return it, so the ~36 buffers below are carved from it instead of
+      // growing the pool one mapping at a time (cold solve at c4: 1.2 s).
+      const size_t nm_b = static_cast<size_t>(round_up(n_, 64)) * static_cast<size_t>(ldm_);
+      const size_t total = 60 * nm_b + 16 * static_cast<size_t>(ldn_) * ldn_ +
+                           16 * static_cast<size_t>(ldm_) * ldm_;
+      void* w = nullptr;
+      if (cudaMallocAsync(&w, total, s_) == cudaSuccess) cudaFreeAsync(w, s_);
+      cudaGetLastError();
+    }
     sharded_ = world > 0;
     rows_alloc_ = n_;
     if (sharded_) {
@@ -605,48 +618,49 @@ class BregmanEngine {
     const size_t nm = static_cast<size_t>(rows_alloc_) * ldm_;
     const size_t dx_elems =
         sharded_ ? static_cast<size_t>(nr_) * ldk_ : static_cast<size_t>(n_) * ldn_;
-    Dx_ = keep(dalloc<float>(dx_elems));
-    Dy_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
-    Dx_lo_ = keep(dalloc<float>(dx_elems));
-    Dy_lo_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_));
+    Dx_ = keep(salloc<float>(dx_elems));
+    Dy_ = keep(salloc<float>(static_cast<size_t>(m_) * ldm_));
+    Dx_lo_ = keep(salloc<float>(dx_elems));
+    Dy_lo_ = keep(salloc<float>(static_cast<size_t>(m_) * ldm_));
     for (int q = 0; q < 2; ++q) {
-      P_[q] = keep(dalloc<float>(nm));            // fp32 hi operand (3xTF32)
-      Pa_[q] = keep(dalloc<float>(nm * 3 / 2));  // fp32 residual or up to 3 bf16 planes
-      P64_[q] = keep(dalloc<double>(nm));         // the iterate π (fp64)
+      P_[q] = keep(salloc<float>(nm));            // fp32 hi operand (3xTF32)
+      Pa_[q] = keep(salloc<float>(nm * 3 / 2));  // fp32 residual or up to 3 bf16 planes
+      P64_[q] = keep(salloc<double>(nm));         // the iterate π (fp64)
     }
-    LK_ = keep(dalloc<double>(nm));               // row-shifted log-kernel (fp64)
-    Vt_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_));
-    Vta_ = sharded_ ? nullptr : keep(dalloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
-    G_ = sharded_ ? nullptr : keep(dalloc<float>(nm));  // sharded: caller-owned (set_comm)
-    mu_ = keep(dalloc<double>(n_));
-    nu_ = keep(dalloc<double>(m_));
-    f_ = keep(dalloc<double>(n_));
-    fn_ = keep(dalloc<double>(n_));
-    g_ = keep(dalloc<double>(m_));
-    rowmax_ = keep(dalloc<double>(n_));
-    row_err_ = keep(dalloc<double>(n_));
-    col_err_ = keep(dalloc<double>(m_));
+    LK_ = keep(salloc<double>(nm));               // row-shifted log-kernel (fp64)
+    Vt_ = sharded_ ? nullptr : keep(salloc<float>(static_cast<size_t>(m_) * ldn_));
+    Vta_ = sharded_ ? nullptr : keep(salloc<float>(static_cast<size_t>(m_) * ldn_ * 3 / 2));
+    G_ = sharded_ ? nullptr : keep(salloc<float>(nm));  // sharded: caller-owned (set_comm)
+    mu_ = keep(salloc<double>(n_));
+    nu_ = keep(salloc<double>(m_));
+    f_ = keep(salloc<double>(n_));
+    fn_ = keep(salloc<double>(n_));
+    g_ = keep(salloc<double>(m_));
+    rowmax_ = keep(salloc<double>(n_));
+    row_err_ = keep(salloc<double>(n_));
+    col_err_ = keep(salloc<double>(m_));
     colblocks_ = static_cast<int>((m_ + kColWidth - 1) / kColWidth);
     // Row chunks of the column passes: ~16 CTAs per SM — the fp64 online LSE
     // per element is latency-bound, so the column pass needs the parallelism
     // (4 per SM ran the c4 column partial at 1.96 TB/s).
     chunks_ = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>((n_ + 63) / 64, (16 * 148 + colblocks_ - 1) / colblocks_)));
-    col_pm_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
-    col_ps_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
-    col_pe_ = keep(dalloc<float>(static_cast<size_t>(chunks_) * m_));
-    col_sum_ = keep(dalloc<double>(static_cast<size_t>(chunks_) * m_));
-    row_sum_ = keep(dalloc<double>(static_cast<size_t>(colblocks_) * n_));
-    obj_part_ = keep(dalloc<double>(n_));
-    wpart_ = keep(dalloc<double>(2 * static_cast<size_t>(chunks_) * colblocks_));
-    st_ = keep(dalloc<BState>(1));
-    rec_ = keep(dalloc<BRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
+    col_pm_ = keep(salloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_ps_ = keep(salloc<double>(static_cast<size_t>(chunks_) * m_));
+    col_pe_ = keep(salloc<float>(static_cast<size_t>(chunks_) * m_));
+    col_sum_ = keep(salloc<double>(static_cast<size_t>(chunks_) * m_));
+    row_sum_ = keep(salloc<double>(static_cast<size_t>(colblocks_) * n_));
+    obj_part_ = keep(salloc<double>(n_));
+    wpart_ = keep(salloc<double>(2 * static_cast<size_t>(chunks_) * colblocks_));
+    st_ = keep(salloc<BState>(1));
+    rec_ = keep(salloc<BRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
   }
   ~BregmanEngine() {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(s_);
     for (auto* p : plans_) gemm_plan_destroy(p);
-    for (void* p : bufs_) cudaFree(p);
+    for (void* p : bufs_) cudaFreeAsync(p, s_);
+    cudaStreamSynchronize(s_);
     if (own_stream_) cudaStreamDestroy(s_);
   }
 
@@ -686,8 +700,8 @@ class BregmanEngine {
                  "bregman shard: the requested split-plane precision needs structure matrices "
                  "exact in fp16 (f16x2) / bf16 (bf16x3, bf16x2); resolve it across ranks first "
                  "(dist.resolve_precision)");
-      Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(nr_) * ldk_ / 2 + 16));
-      Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
+      Dx_bf_ = keep(salloc<float>(static_cast<size_t>(nr_) * ldk_ / 2 + 16));
+      Dy_bf_ = keep(salloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
       if (aux_mode_ == 5) {
         // f16x2: every rank holds the full μ, ν (host) and D_Y, so the
         // bound and the Vᵀ row scales agree across ranks.
@@ -697,8 +711,8 @@ class BregmanEngine {
         launch_to_f16(Dx_, nr_, ldk_, ldk_, Dx_bf_, s_);
         launch_to_f16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
         f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(std::max(x_max_, 1e-30))));
-        f16_g1_rs_ = keep(dalloc<float>(ldm_));
-        f16_g2_cs_ = keep(dalloc<float>(ldm_));
+        f16_g1_rs_ = keep(salloc<float>(ldm_));
+        f16_g2_cs_ = keep(salloc<float>(ldm_));
         launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_,
                           f16_g2_cs_, s_);
       } else {
@@ -892,6 +906,16 @@ class BregmanEngine {
     bufs_.push_back(p);
     return p;
   }
+  // Engine buffers: stream-ordered, zero-filled, from the device pool
+  // (pool_keep), so repeated solves reuse their workspace instead of paying
+  // cudaMalloc of tens of GB (c4: 279 ms per solve before).
+  template <class T>
+  T* salloc(size_t count) {
+    void* p = nullptr;
+    GWB_CUDA(cudaMallocAsync(&p, count * sizeof(T) + 256, s_));
+    GWB_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T) + 256, s_));
+    return static_cast<T*>(p);
+  }
 
   // fp32 hi operand (3xTF32 only) and GEMM planes of the initial iterate.
   void init_copies() {
@@ -989,15 +1013,15 @@ class BregmanEngine {
     else if (bf16_exact && req == GWB_PREC_BF16X2) aux_mode_ = 4;
     else aux_mode_ = 2;
     if (aux_mode_ >= 3) {
-      Dx_bf_ = keep(dalloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16));
-      Dy_bf_ = keep(dalloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
+      Dx_bf_ = keep(salloc<float>(static_cast<size_t>(n_) * ldn_ / 2 + 16));
+      Dy_bf_ = keep(salloc<float>(static_cast<size_t>(m_) * ldm_ / 2 + 16));
       if (aux_mode_ == 5) {
         // f16x2 scales as in the BAPG engine.
         launch_to_f16(Dx_, n_, n_, ldn_, Dx_bf_, s_);
         launch_to_f16(Dy_, m_, m_, ldm_, Dy_bf_, s_);
         f16_s1_ = 14 - static_cast<int>(std::ceil(std::log2(std::max(x_max_, 1e-30))));
-        f16_g1_rs_ = keep(dalloc<float>(ldm_));
-        f16_g2_cs_ = keep(dalloc<float>(ldm_));
+        f16_g1_rs_ = keep(salloc<float>(ldm_));
+        f16_g2_cs_ = keep(salloc<float>(ldm_));
         launch_f16_scales(Dy_, m_, ldm_, static_cast<float>(x_max_), f16_s1_, f16_g1_rs_,
                           f16_g2_cs_, s_);
       } else {
@@ -1234,10 +1258,24 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
   // BPG step-size warning (solvers.cpp:226-234), only if a BPG phase can run.
   const bool bpg_may_run =
       algo == GWB_BPG || (algo == GWB_HBPG && cfg->max_iters >= 1);
+  // GWB_PHASE_TIMES=1: wall time of each phase of the call on stderr.
+  static const bool phase_times = std::getenv("GWB_PHASE_TIMES") != nullptr;
+  auto tick = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!phase_times) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "bregman phase %-9s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tick).count());
+    tick = now;
+  };
   BregmanEngine eng(device, n, m, *cfg, algo);
+  lap("create");
   eng.load(dx, dy, mu, nu, initial, graphs);
+  lap("load");
   std::vector<double> host_pi;
   eng.run(observer, user, &host_pi);
+  lap("run");
   const BState s = eng.status();
   if (s.flags) raise_breg(s, cfg->log_domain != 0);
   const int used = s.iter - 1;
@@ -1277,7 +1315,9 @@ void bregman_solve(const gwb_config* cfg, int32_t algo, const double* dx, int64_
   const double p = last_bpg ? cfg->perturbation : 0.0;
   std::vector<double> target(m);
   for (int64_t j = 0; j < m; ++j) target[j] = (1.0 - p) * nu[j] + p / static_cast<double>(m);
+  lap("tail");
   eng.output(used, out_final, target);
+  lap("output");
 }
 
 // ---- row-sharded eBPG / BPG / hBPG (C-ABI in capi.cu) ---------
