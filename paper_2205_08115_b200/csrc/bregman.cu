@@ -4,19 +4,19 @@
 //   GEMM chain            G = D_X·π·D_Y                       (tcgen05, 3xTF32)
 //   form   (row pass)     ⟨G,π⟩ for record k−1's objective;
 //                         eBPG: E = (2/ε)G, BPG: E = 2t·G, log-kernel
-//                         LK = E (eBPG) or log π + E (BPG); stores the
-//                         row-shifted LKs = LK − max_j LK in place of G
+//                         LK = E (eBPG) or log π + E (BPG), stored (fp64)
+//                         in one pass; max_j LK per row for the dead-line test
 //   check                 BPG overflow (max E > 700), eBPG dead lines,
 //                         reset of the Sinkhorn potentials
 //   sweeps s=1..inner     row LSE → f (fp64), early-exit decision for sweep
 //                         s−1 (the reference's ∞-norm marginal test after a
 //                         full ROWS→COLS sweep, projections.cpp:101-113),
 //                         column LSE (chunked partials + fixed-order merge) → g
-//   write                 π' = exp(max(LKs, clamp) + f + g) (+ perturbation),
+//   write                 π' = exp(max(LK, clamp) + f + g) (+ perturbation),
 //                         row/column sums, ‖π'−π‖², ‖π‖²
 //   finalize              trace record, stop rule, hBPG phase switch.
-// The Sinkhorn runs in the log domain with fp64 potentials over an fp32
-// row-shifted log-kernel: identical to the reference's plain-domain
+// The Sinkhorn runs in the log domain with fp64 potentials over the fp64
+// log-kernel (any row shift is absorbed by the row potential f): identical to the reference's plain-domain
 // alternating scaling (rows first) whenever the latter is finite, with the
 // reference's 1e-300 kernel clamp applied as a log-space floor and its error
 // semantics (dead lines, zero-sum lines, overflow, non-finite) emulated.
@@ -99,7 +99,9 @@ struct BDev {
   double* row_sum;      // colblocks × n
   double* obj_part;     // n
   double* wpart;        // (colblocks·chunks) × 2
+  double* dev_part;     // marginal deviation partials: row blocks, then column blocks
   int chunks, colblocks;
+  int dev_rb, dev_cb;   // blocks of 256 rows / columns in dev_part
   double eb_scale;      // 2/ε
   double bp_scale;      // 2t
   int log_domain;
@@ -116,14 +118,15 @@ __device__ __forceinline__ bool skip_sink(const BDev& d) {
   return d.st->done != 0 || d.st->sink_done != 0;
 }
 
-// Per-row clamp floor in shifted log space: the reference clamps the kernel
-// at 1e-300 (solvers.cpp:252, :331); eBPG's kernel is exp(E − max E).
-__device__ __forceinline__ double clamp_floor(const BDev& d, int64_t i) {
+// Clamp floor of the log-kernel: the reference clamps the kernel at 1e-300
+// (solvers.cpp:252, :331); eBPG's kernel is exp(E − max E), so its floor on
+// LK = E sits at log(1e-300) + max E.
+__device__ __forceinline__ double clamp_floor(const BDev& d) {
   if (d.st->phase == 1) {
     if (d.log_domain) return -INFINITY;
-    return kLogClamp + static_cast<double>(__int_as_float(d.st->gmax_bits)) - d.rowmax[i];
+    return kLogClamp + static_cast<double>(__int_as_float(d.st->gmax_bits));
   }
-  return kLogClamp - d.rowmax[i];
+  return kLogClamp;
 }
 
 __device__ double block_sum(double v) {
@@ -167,40 +170,52 @@ __device__ double block_max_d(double v) {
 // (devutil.cuh), instantiated for fp64 with unit weights.
 
 // ---------------------------------------------------------------------------
-// form: one CTA per row.
+// form: one warp per row (8 rows per CTA).  A CTA per row kept too few
+// bytes in flight per SM: 78 elements per thread, a block-merge tail per row.
+constexpr int kRowsPerCta = kThreads / 32;
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __global__ void __launch_bounds__(kThreads) form_kernel(BDev d, int tail) {
   if (tail ? d.st->flags != 0 : skip(d)) return;
-  const int64_t i = blockIdx.x;
-  const float* g = d.G + i * d.ld;
-  const double* p = d.P + i * d.ld;
-  double* lkrow = d.LK + i * d.ld;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kRowsPerCta + warp;
   const bool ebpg = d.st->phase == 1;
   const double sc = ebpg ? d.eb_scale : d.bp_scale;
-  double obj = 0.0;
-  double rmax = -INFINITY;
   float emax = 0.0f;
-  for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
-    const double gv = g[j], pv = p[j];
-    obj = __fma_rn(gv, pv, obj);
-    const double e = sc * gv;
-    emax = fmaxf(emax, static_cast<float>(e));
-    const double lk = ebpg ? e : e + log(pv);
-    rmax = fmax(rmax, lk);
+  if (i < d.n) {
+    const float* g = d.G + i * d.ld;
+    const double* p = d.P + i * d.ld;
+    double* lkrow = d.LK + i * d.ld;
+    double obj = 0.0;
+    double rmax = -INFINITY;
+    // One pass: G and π are read once and LK is written unshifted (a row
+    // shift would need a second pass; the row potential f absorbs it).
+#pragma unroll 4
+    for (int64_t j = lane; j < d.m; j += 32) {
+      const double gv = g[j], pv = p[j];
+      obj = __fma_rn(gv, pv, obj);
+      if (tail) continue;
+      const double e = sc * gv;
+      emax = fmaxf(emax, static_cast<float>(e));
+      const double lk = ebpg ? e : e + log(pv);
+      rmax = fmax(rmax, lk);
+      lkrow[j] = lk;
+    }
+    obj = warp_sum(obj);
+    rmax = warp_max_d(rmax);
+    if (lane == 0) {
+      d.obj_part[i] = obj;
+      if (!tail) d.rowmax[i] = rmax;
+    }
   }
-  obj = block_sum(obj);
-  if (threadIdx.x == 0) d.obj_part[i] = obj;
   if (tail) return;
-  rmax = block_max_d(rmax);
   emax = block_max(emax);
-  if (threadIdx.x == 0) {
-    d.rowmax[i] = rmax;
-    atomicMax(&d.st->gmax_bits, __float_as_int(emax));
-  }
-  for (int64_t j = threadIdx.x; j < d.m; j += kThreads) {
-    const double e = sc * static_cast<double>(g[j]);
-    const double lk = ebpg ? e : e + log(p[j]);
-    lkrow[j] = lk - rmax;
-  }
+  if (threadIdx.x == 0) atomicMax(&d.st->gmax_bits, __float_as_int(emax));
 }
 
 // Checks after the form pass + Sinkhorn reset.  One block.
@@ -228,32 +243,64 @@ __global__ void form_check_kernel(BDev d) {
   }
 }
 
-// Sinkhorn row update for sweep s: f_new = log μ − LSE_j(max(LKs, floor) + g),
+// Adds four terms to an online (max, Σ): at most one rescale per group, then
+// four independent exponentials.  Per-term new-max branches diverge across
+// a warp on most steps of a short per-lane chain, evaluating both sides.
+// NaN in any term gives NaN.
+__device__ __forceinline__ void lse64_add4(Lse64& a, const double (&x)[4]) {
+  const bool bad = isnan(x[0]) || isnan(x[1]) || isnan(x[2]) || isnan(x[3]);
+  const double m4 = fmax(fmax(x[0], x[1]), fmax(x[2], x[3]));
+  if (m4 > a.mx) {
+    a.s = a.mx == -INFINITY ? 0.0 : a.s * exp(a.mx - m4);
+    a.mx = m4;
+  }
+  if (m4 > -INFINITY) {
+    const double e0 = exp(x[0] - a.mx), e1 = exp(x[1] - a.mx);
+    const double e2 = exp(x[2] - a.mx), e3 = exp(x[3] - a.mx);
+    a.s += (e0 + e1) + (e2 + e3);
+  }
+  if (bad) a.mx = NAN;
+}
+
+// Sinkhorn row update for sweep s: f_new = log μ − LSE_j(max(LK, floor) + g),
 // fp64 terms and exponentials (the reference's arithmetic, projections.cpp:92-163).
 __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   if (skip_sink(d)) return;
-  const int64_t i = blockIdx.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kRowsPerCta + warp;
+  if (i >= d.n) return;
   const double* lk = d.LK + i * d.ld;
-  const double floor_i = clamp_floor(d, i);
-  Lse64 a{-INFINITY, 0.0};
-  for (int64_t j = threadIdx.x * 2; j < d.m; j += kThreads * 2) {
-    const double2 v = *reinterpret_cast<const double2*>(lk + j);
-    const double2 g01 = *reinterpret_cast<const double2*>(d.g + j);
-    lse64_add(a, fmax(v.x, floor_i) + g01.x, 1.0);
-    if (j + 1 < d.m) lse64_add(a, fmax(v.y, floor_i) + g01.y, 1.0);
+  const double fl = clamp_floor(d);
+  // One warp per row.  Each step loads 8 columns per lane (four coalesced
+  // double2 loads of LK and g over a 256-column window) into two
+  // independent accumulators.  ld is a multiple of 32, so a pair that
+  // starts inside the row stays inside it.
+  Lse64 a[2] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}};
+  for (int64_t b = 0; b < d.m; b += 256) {
+    double2 v[4], gg[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int64_t j = b + 64 * h + 2 * lane;
+      if (j < d.m) {
+        v[h] = *reinterpret_cast<const double2*>(lk + j);
+        gg[h] = *reinterpret_cast<const double2*>(d.g + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      double x[4];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int h = 2 * u + h2;
+        const int64_t j = b + 64 * h + 2 * lane;
+        x[2 * h2] = j < d.m ? fmax(v[h].x, fl) + gg[h].x : -INFINITY;
+        x[2 * h2 + 1] = j + 1 < d.m ? fmax(v[h].y, fl) + gg[h].y : -INFINITY;
+      }
+      lse64_add4(a[u], x);
+    }
   }
-  // block merge (fixed order)
-  __shared__ double smx[kThreads / 32], ss[kThreads / 32];
-  a = lse64_warp_merge(a);
-  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
-  if (l == 0) {
-    smx[w] = a.mx;
-    ss[w] = a.s;
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  Lse64 r{-INFINITY, 0.0};
-  for (int q = 0; q < kThreads / 32; ++q) r = lse64_merge(r, Lse64{smx[q], ss[q]});
+  const Lse64 r = lse64_warp_merge(lse64_merge(a[0], a[1]));
+  if (lane != 0) return;
   const double lse = r.mx + log(r.s);
   const double fn = log(d.mu64[i]) - lse;
   d.f_new[i] = fn;
@@ -317,6 +364,7 @@ __global__ void __launch_bounds__(kThreads) col_lse_partial_kernel(BDev d, int r
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
   const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
   const bool want_emax = first_sweep && d.st->phase == 1 && !d.log_domain;
+  const double fl = clamp_floor(d);
   Lse64 a[4] = {{-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}, {-INFINITY, 0.0}};
   float emax[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   if (c0 < d.m) {
@@ -324,12 +372,12 @@ __global__ void __launch_bounds__(kThreads) col_lse_partial_kernel(BDev d, int r
       const double* lk = d.LK + i * d.ld + c0;
       const double2 v01 = *reinterpret_cast<const double2*>(lk);
       const double2 v23 = *reinterpret_cast<const double2*>(lk + 2);
-      const double fl = clamp_floor(d, i), fi = d.f[i];
+      const double fi = d.f[i];
       const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         lse64_add(a[q], fmax(vv[q], fl) + fi, 1.0);
-        if (want_emax) emax[q] = fmaxf(emax[q], static_cast<float>(vv[q] + d.rowmax[i]));
+        if (want_emax) emax[q] = fmaxf(emax[q], static_cast<float>(vv[q]));
       }
     }
   }
@@ -423,7 +471,7 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
     if (ok) {
       const double* lk = d.LK + i * d.ld + c0;
       const double* pp = d.P + i * d.ld + c0;
-      const double fl = clamp_floor(d, i), fi = d.f[i];
+      const double fl = clamp_floor(d), fi = d.f[i];
       double o[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -470,6 +518,32 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
   }
 }
 
+// Marginal deviations Σ_i (row sum − μ_i)² and Σ_j (column sum − ν_j)² of
+// the written coupling, one partial per block of 256 lines (fixed order).
+// (One block reading the colblocks × n row partials took 1.2 ms at c4.)
+__global__ void __launch_bounds__(256) breg_dev_partial_kernel(BDev d) {
+  if (skip(d)) return;
+  const int b = blockIdx.x;
+  double v = 0.0;
+  if (b < d.dev_rb) {
+    const int64_t i = static_cast<int64_t>(b) * 256 + threadIdx.x;
+    if (i < d.n) {
+      double s = 0.0;
+      for (int c = 0; c < d.colblocks; ++c) s += d.row_sum[static_cast<int64_t>(c) * d.n + i];
+      v = (s - d.mu64[i]) * (s - d.mu64[i]);
+    }
+  } else {
+    const int64_t j = static_cast<int64_t>(b - d.dev_rb) * 256 + threadIdx.x;
+    if (j < d.m) {
+      double s = 0.0;
+      for (int c = 0; c < d.chunks; ++c) s += d.col_sum[static_cast<int64_t>(c) * d.m + j];
+      v = (s - d.nu64[j]) * (s - d.nu64[j]);
+    }
+  }
+  v = block_sum(v);
+  if (threadIdx.x == 0) d.dev_part[b] = v;
+}
+
 // Record k, stop rule, phase logic.  One block.
 __global__ void breg_finalize_kernel(BDev d, int tail) {
   BState* st = d.st;
@@ -484,16 +558,8 @@ __global__ void breg_finalize_kernel(BDev d, int tail) {
     return;
   }
   double rowdev = 0.0, coldev = 0.0, diff = 0.0, old = 0.0;
-  for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < d.colblocks; ++b) s += d.row_sum[static_cast<int64_t>(b) * d.n + i];
-    rowdev += (s - d.mu64[i]) * (s - d.mu64[i]);
-  }
-  for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < d.chunks; ++c) s += d.col_sum[static_cast<int64_t>(c) * d.m + j];
-    coldev += (s - d.nu64[j]) * (s - d.nu64[j]);
-  }
+  for (int b = threadIdx.x; b < d.dev_rb; b += blockDim.x) rowdev += d.dev_part[b];
+  for (int b = threadIdx.x; b < d.dev_cb; b += blockDim.x) coldev += d.dev_part[d.dev_rb + b];
   const int64_t ctas = static_cast<int64_t>(d.chunks) * d.colblocks;
   for (int64_t c = threadIdx.x; c < ctas; c += blockDim.x) {
     diff += d.wpart[2 * c];
@@ -652,6 +718,9 @@ class BregmanEngine {
     row_sum_ = keep(salloc<double>(static_cast<size_t>(colblocks_) * n_));
     obj_part_ = keep(salloc<double>(n_));
     wpart_ = keep(salloc<double>(2 * static_cast<size_t>(chunks_) * colblocks_));
+    dev_rb_ = static_cast<int>((n_ + 255) / 256);
+    dev_cb_ = static_cast<int>((m_ + 255) / 256);
+    dev_part_ = keep(salloc<double>(static_cast<size_t>(dev_rb_ + dev_cb_)));
     st_ = keep(salloc<BState>(1));
     rec_ = keep(salloc<BRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
   }
@@ -800,6 +869,8 @@ class BregmanEngine {
     base_ = d;
   }
 
+  unsigned row_ctas() const { return static_cast<unsigned>((n_ + kRowsPerCta - 1) / kRowsPerCta); }
+
   // Everything of outer iteration k after the chain: the form pass, ≤
   // inner_iters Sinkhorn sweeps, the write pass and the record; returns the
   // device status after the iteration.
@@ -809,10 +880,10 @@ class BregmanEngine {
     rebind(v, q);
     const int rows_per_chunk = static_cast<int>((n_ + chunks_ - 1) / chunks_);
     {
-      form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 0);
+      form_kernel<<<row_ctas(), kThreads, 0, s_>>>(v, 0);
       form_check_kernel<<<1, 1024, 0, s_>>>(v);
       for (int sw = 1; sw <= cfg_.inner_iters; ++sw) {
-        row_lse_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, sw);
+        row_lse_kernel<<<row_ctas(), kThreads, 0, s_>>>(v, sw);
         row_decide_kernel<<<1, 1024, 0, s_>>>(v, sw);
         dim3 grid(static_cast<unsigned>(colblocks_), static_cast<unsigned>(chunks_));
         col_lse_partial_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk, sw == 1);
@@ -828,6 +899,7 @@ class BregmanEngine {
       }
       dim3 grid(static_cast<unsigned>(colblocks_), static_cast<unsigned>(chunks_));
       write_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk);
+      breg_dev_partial_kernel<<<static_cast<unsigned>(v.dev_rb + v.dev_cb), 256, 0, s_>>>(v);
       breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 0);
       GWB_CUDA(cudaGetLastError());
     }
@@ -876,7 +948,7 @@ class BregmanEngine {
   void tail_rest(int used) {
     BDev v = base_;
     rebind(v, used & 1);
-    form_kernel<<<static_cast<unsigned>(n_), kThreads, 0, s_>>>(v, 1);
+    form_kernel<<<row_ctas(), kThreads, 0, s_>>>(v, 1);
     breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 1);
     GWB_CUDA(cudaGetLastError());
   }
@@ -965,6 +1037,9 @@ class BregmanEngine {
     d.row_sum = row_sum_;
     d.obj_part = obj_part_;
     d.wpart = wpart_;
+    d.dev_part = dev_part_;
+    d.dev_rb = dev_rb_;
+    d.dev_cb = dev_cb_;
     d.chunks = chunks_;
     d.colblocks = colblocks_;
     d.eb_scale = 2.0 / cfg_.epsilon_reg;
@@ -1204,9 +1279,9 @@ class BregmanEngine {
   float* f16_g1_rs_ = nullptr;
   float* f16_g2_cs_ = nullptr;
   double *mu_, *nu_, *f_, *fn_, *g_, *row_err_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
-      *row_sum_, *obj_part_, *wpart_;
+      *row_sum_, *obj_part_, *wpart_, *dev_part_;
   float* col_pe_;
-  int chunks_ = 1, colblocks_ = 1;
+  int chunks_ = 1, colblocks_ = 1, dev_rb_ = 1, dev_cb_ = 1;
   BState* st_;
   BRecord* rec_;
   BDev base_;
