@@ -414,12 +414,15 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
     };
 
     int k = 1, phase = 0, used = 0, converged = 0, err_iter = 0;
+    // GEMM1 of the first chain (X̂ = ŵ⁰).  Every later chain's GEMM1 is
+    // issued at the end of the preceding half-step, as soon as its operand
+    // planes are written, so its MMAs run under that half-step's record sums.
+    ptx::fence_proxy_async();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) issue(0);
     for (;;) {
       // ---- chain: V̂ = D_X·X̂ → planes → G (a) or Gᵀ (b), ×2^s, in kAcc.
-      ptx::fence_proxy_async();
-      ptx::tc_fence_before();
-      __syncthreads();
-      if (tid == 0) issue(phase == 1 ? 1 : 0);
       mma_sync();
       load_acc();
       store_planes(x);
@@ -427,6 +430,24 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       ptx::tc_fence_before();
       __syncthreads();
       if (tid == 0) issue(phase == 1 ? 3 : 2);
+      // While GEMM2 runs: the current iterate's entries of line L from T
+      // (ŵ by rows for a / the tail, π̂ by columns for b) and their sum.
+      float xo[kW];
+      if (phase != 1) {
+        const float* Trow = T + L * kTLd + c0;
+#pragma unroll
+        for (int t = 0; t < kW; t += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(Trow + t);
+          xo[t] = w4.x;
+          xo[t + 1] = w4.y;
+          xo[t + 2] = w4.z;
+          xo[t + 3] = w4.w;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kW; ++t) xo[t] = T[(c0 + t) * kTLd + L];
+      }
+      const double xo_sum = sumw([&](int t) { return xo[t]; });
       mma_sync();
       load_acc();  // x = 2^s·G (row L) or 2^s·Gᵀ (column L)
 
@@ -438,17 +459,9 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         // t̂ = ŵ ⊙ e^{G/ρ − r} (into x), Ŝ = Σ_j t̂; ⟨G, w⟩ and Σ_j w for the
         // previous record.  ŵ is row L of T.
         float* Trow = T + L * kTLd + c0;
-        float wv[kW];
-#pragma unroll
-        for (int t = 0; t < kW; t += 4) {
-          const float4 w4 = *reinterpret_cast<const float4*>(Trow + t);
-          wv[t] = w4.x;
-          wv[t + 1] = w4.y;
-          wv[t + 2] = w4.z;
-          wv[t + 3] = w4.w;
-        }
+        const float (&wv)[kW] = xo;
         const double gw = dotw([&](int t) { return x[t]; }, [&](int t) { return wv[t]; });
-        const double rw = sumw([&](int t) { return wv[t]; });
+        const double rw = xo_sum;
 #pragma unroll
         for (int t = 0; t < kW; ++t) x[t] = wv[t] * ex2(fmaf(x[t], k2, -rr));
         const double S = sumw([&](int t) { return x[t]; });
@@ -479,6 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
           for (int t = 0; t < kW; t += 4)
             *reinterpret_cast<float4*>(Trow + t) = make_float4(x[t], x[t + 1], x[t + 2], x[t + 3]);
           store_planes(x);
+          // Next GEMM1 (X̂ = π̂, MN-major) now.  The flags raised above are
+          // visible after the barrier; a failing problem issues nothing.
+          ptx::fence_proxy_async();
+          ptx::tc_fence_before();
+          __syncthreads();
+          if (tid == 0 && ctl[0] == 0) issue(1);
         }
         block_sum8(ra, 2);
         if (phase == 2) {
@@ -508,10 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       // column L of T; it also goes to TMEM for the final output.
       double gp, gt;
       {
-        float pv[kW];
-#pragma unroll
-        for (int t = 0; t < kW; ++t) pv[t] = T[(c0 + t) * kTLd + L];
-        const double P = sumw([&](int t) { return pv[t]; });
+        const float (&pv)[kW] = xo;
+        const double P = xo_sum;
         gp = dotw([&](int t) { return x[t]; }, [&](int t) { return pv[t]; });
         float tv[kW];
 #pragma unroll
@@ -551,6 +568,15 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         ldw(kWT + c0, wo);
 #pragma unroll
         for (int t = 0; t < kW; ++t) x[t] *= sj;
+        st(kWT + c0, x);
+        store_planes(x);
+        ptx::tmem_wait_st();
+        // Next GEMM1 (X̂ = ŵ', K-major: the next iteration or the tail) now;
+        // the diagnostics below run under its MMAs.
+        ptx::fence_proxy_async();
+        ptx::tc_fence_before();
+        __syncthreads();
+        if (tid == 0) issue(0);
         f3 = dotw([&](int t) { return wo[t]; }, [&](int t) { return wo[t]; });
         // ‖w' − w‖² in fp64: near convergence the changes are off-support
         // entries of 1e-31 and below (the pinned rel_tol = 1e-30 is crossed
@@ -570,14 +596,11 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
         }
         f1 = dotw([&](int t) { return wo[t]; }, [&](int t) { return wo[t]; });
       }
-      st(kWT + c0, x);
-      store_planes(x);
       dsum[0] = gt * static_cast<double>(sj) * un2_64;
       dsum[1] = f1 * un2_64;
       dsum[2] = dd * un2_64;
       dsum[3] = f3 * un2_64;
       dsum[4] = gp * un2_64;
-      ptx::tmem_wait_st();
       block_sum8(dsum, 6);
       if (tid == 0) {
         if (rec) {
@@ -595,7 +618,8 @@ __global__ void __launch_bounds__(kThreads, 1) bapg_batched_kernel(BatchArgs a) 
       }
       __syncthreads();
       used = k;
-      if (ctl[0] != 0) {
+      if (ctl[0] != 0) {  // (no flag is raised after the check above)
+        mma_sync();
         err_iter = k;
         break;
       }
