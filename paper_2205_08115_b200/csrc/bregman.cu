@@ -8,12 +8,13 @@
 //                         in one pass; max_j LK per row for the dead-line test
 //   check                 BPG overflow (max E > 700), eBPG dead lines,
 //                         reset of the Sinkhorn potentials
-//   sweeps s=1..inner     row LSE → f (fp64), early-exit decision for sweep
-//                         s−1 (the reference's ∞-norm marginal test after a
-//                         full ROWS→COLS sweep, projections.cpp:101-113),
-//                         column LSE (chunked partials + fixed-order merge) → g
-//   write                 π' = exp(max(LK, clamp) + f + g) (+ perturbation),
-//                         row/column sums, ‖π'−π‖², ‖π‖²
+//   sweeps s=1..inner     row LSE → f (fp64), column LSE (chunked partials +
+//                         fixed-order merge) → g, then the write pass
+//                         π' = exp(max(LK, clamp) + f + g) (+ perturbation)
+//                         with row/column sums, ‖π'−π‖², ‖π‖², whose row sums
+//                         give the early-exit test of sweep s (the reference's
+//                         ∞-norm marginal test after a full ROWS→COLS sweep,
+//                         projections.cpp:101-113); later sweeps are skipped
 //   finalize              trace record, stop rule, hBPG phase switch.
 // The Sinkhorn runs in the log domain with fp64 potentials over the fp64
 // log-kernel (any row shift is absorbed by the row potential f): identical to the reference's plain-domain
@@ -90,7 +91,8 @@ struct BDev {
   double* f_new;
   double* g;
   double* rowmax;
-  double* row_err;
+  double* row_sum_raw;  // colblocks × n: write-pass row sums before the BPG perturbation
+  double* err_part;     // sweep marginal-error partials (max), as dev_part
   double* col_err;
   double* col_pm;       // chunks × m  (max, fp64)
   double* col_ps;       // chunks × m  (Σ exp, fp64)
@@ -304,7 +306,6 @@ __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   const double lse = r.mx + log(r.s);
   const double fn = log(d.mu64[i]) - lse;
   d.f_new[i] = fn;
-  if (s >= 2) d.row_err[i] = fabs(d.mu64[i] * expm1(d.f[i] - fn));
   if (isnan(lse) || !(r.s > 0.0) || r.mx == -INFINITY) {
     const bool plain = !(d.st->phase == 1 && d.log_domain);
     if (plain && !isnan(lse)) {
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) row_lse_kernel(BDev d, int s) {
   }
 }
 
-// Early-exit decision for sweep s−1 and f ← f_new.  One block.
+// Row-pass flags and f ← f_new.  One block.
 __global__ void row_decide_kernel(BDev d, int s) {
   BState* st = d.st;
   if (skip_sink(d)) return;
@@ -327,29 +328,6 @@ __global__ void row_decide_kernel(BDev d, int s) {
       st->err_sweep = s;
     }
     return;
-  }
-  __shared__ int conv;
-  if (s >= 2) {
-    double e = 0.0;
-    for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) e = fmax(e, d.row_err[i]);
-    for (int64_t j = threadIdx.x; j < d.m; j += blockDim.x) e = fmax(e, d.col_err[j]);
-    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
-    __shared__ double sh[32];
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = e;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < static_cast<int>(blockDim.x / 32); ++q) t = fmax(t, sh[q]);
-      conv = t <= d.inner_tol;
-    }
-    __syncthreads();
-    if (conv) {
-      if (threadIdx.x == 0) {
-        st->sink_done = 1;
-        st->sweeps = s - 1;
-      }
-      return;
-    }
   }
   for (int64_t i = threadIdx.x; i < d.n; i += blockDim.x) d.f[i] = d.f_new[i];
   if (threadIdx.x == 0) st->sweeps = s;
@@ -450,7 +428,7 @@ __global__ void col_flag_kernel(BDev d, int s) {
 
 // π' = exp(max(LKs, floor) + f + g) (+ perturbation), fused sums.
 __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_chunk) {
-  if (skip(d)) return;
+  if (skip_sink(d)) return;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
@@ -467,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
 #pragma unroll
     for (int q = 0; q < 4; ++q) gj[q] = (c0 + q < d.m) ? d.g[c0 + q] : 0.0;
   for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
-    double rs = 0.0;
+    double rs = 0.0, rr = 0.0;
     if (ok) {
       const double* lk = d.LK + i * d.ld + c0;
       const double* pp = d.P + i * d.ld + c0;
@@ -478,6 +456,7 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
         if (c0 + q < d.m) {
           const double x = fmax(lk[q], fl) + fi + gj[q];
           double val = exp(x);
+          rr += val;
           if (perturb) val = keep * val + add;
           o[q] = val;
           cs[q] += val;
@@ -496,6 +475,10 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
     }
     rs = warp_sum(rs);
     if (lane == 0) d.row_sum[static_cast<int64_t>(blockIdx.x) * d.n + i] = rs;
+    if (perturb) {
+      rr = warp_sum(rr);
+      if (lane == 0) d.row_sum_raw[static_cast<int64_t>(blockIdx.x) * d.n + i] = rr;
+    }
   }
   __shared__ double s_c[kThreads / 32][kColWidth];
 #pragma unroll
@@ -518,19 +501,28 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
   }
 }
 
-// Marginal deviations Σ_i (row sum − μ_i)² and Σ_j (column sum − ν_j)² of
-// the written coupling, one partial per block of 256 lines (fixed order).
-// (One block reading the colblocks × n row partials took 1.2 ms at c4.)
-__global__ void __launch_bounds__(256) breg_dev_partial_kernel(BDev d) {
-  if (skip(d)) return;
+// After the write pass of a sweep, per block of 256 lines (fixed order):
+// the record's marginal deviations Σ_i (row sum − μ_i)², Σ_j (column sum −
+// ν_j)² of the written coupling, and the sweep's ∞-norm marginal error
+// (|row sum − μ_i| of the coupling before the BPG perturbation, and the
+// column errors of the column step).  (One block reading the colblocks × n
+// row partials took 1.2 ms at c4.)
+__global__ void __launch_bounds__(256) sink_partial_kernel(BDev d) {
+  if (skip_sink(d)) return;
   const int b = blockIdx.x;
-  double v = 0.0;
+  const bool perturb = d.perturb > 0.0 && d.st->phase == 2;
+  double v = 0.0, e = 0.0;
   if (b < d.dev_rb) {
     const int64_t i = static_cast<int64_t>(b) * 256 + threadIdx.x;
     if (i < d.n) {
       double s = 0.0;
       for (int c = 0; c < d.colblocks; ++c) s += d.row_sum[static_cast<int64_t>(c) * d.n + i];
       v = (s - d.mu64[i]) * (s - d.mu64[i]);
+      if (perturb) {
+        s = 0.0;
+        for (int c = 0; c < d.colblocks; ++c) s += d.row_sum_raw[static_cast<int64_t>(c) * d.n + i];
+      }
+      e = fabs(s - d.mu64[i]);
     }
   } else {
     const int64_t j = static_cast<int64_t>(b - d.dev_rb) * 256 + threadIdx.x;
@@ -538,10 +530,29 @@ __global__ void __launch_bounds__(256) breg_dev_partial_kernel(BDev d) {
       double s = 0.0;
       for (int c = 0; c < d.chunks; ++c) s += d.col_sum[static_cast<int64_t>(c) * d.m + j];
       v = (s - d.nu64[j]) * (s - d.nu64[j]);
+      e = d.col_err[j];
     }
   }
   v = block_sum(v);
-  if (threadIdx.x == 0) d.dev_part[b] = v;
+  e = block_max_d(e);
+  if (threadIdx.x == 0) {
+    d.dev_part[b] = v;
+    d.err_part[b] = e;
+  }
+}
+
+// Early exit after sweep s: ∞-norm marginal error ≤ inner_tol, or the last
+// sweep.  One block.
+__global__ void sink_decide_kernel(BDev d, int s, int last) {
+  BState* st = d.st;
+  if (skip_sink(d)) return;
+  double e = 0.0;
+  for (int b = threadIdx.x; b < d.dev_rb + d.dev_cb; b += blockDim.x) e = fmax(e, d.err_part[b]);
+  e = block_max_d(e);
+  if (threadIdx.x == 0) {
+    st->sweeps = s;
+    if (last || e <= d.inner_tol) st->sink_done = 1;
+  }
 }
 
 // Record k, stop rule, phase logic.  One block.
@@ -703,7 +714,6 @@ class BregmanEngine {
     fn_ = keep(salloc<double>(n_));
     g_ = keep(salloc<double>(m_));
     rowmax_ = keep(salloc<double>(n_));
-    row_err_ = keep(salloc<double>(n_));
     col_err_ = keep(salloc<double>(m_));
     colblocks_ = static_cast<int>((m_ + kColWidth - 1) / kColWidth);
     // Row chunks of the column passes: ~16 CTAs per SM — the fp64 online LSE
@@ -721,6 +731,8 @@ class BregmanEngine {
     dev_rb_ = static_cast<int>((n_ + 255) / 256);
     dev_cb_ = static_cast<int>((m_ + 255) / 256);
     dev_part_ = keep(salloc<double>(static_cast<size_t>(dev_rb_ + dev_cb_)));
+    err_part_ = keep(salloc<double>(static_cast<size_t>(dev_rb_ + dev_cb_)));
+    row_sum_raw_ = keep(salloc<double>(static_cast<size_t>(colblocks_) * n_));
     st_ = keep(salloc<BState>(1));
     rec_ = keep(salloc<BRecord>(static_cast<size_t>(cfg_.max_iters) + 2));
   }
@@ -882,6 +894,9 @@ class BregmanEngine {
     {
       form_kernel<<<row_ctas(), kThreads, 0, s_>>>(v, 0);
       form_check_kernel<<<1, 1024, 0, s_>>>(v);
+      // Large problems poll the early exit after every sweep (one host sync,
+      // instead of enqueueing up to inner_iters sweeps of skipped launches).
+      const bool poll = n_ * m_ >= (int64_t{1} << 23);
       for (int sw = 1; sw <= cfg_.inner_iters; ++sw) {
         row_lse_kernel<<<row_ctas(), kThreads, 0, s_>>>(v, sw);
         row_decide_kernel<<<1, 1024, 0, s_>>>(v, sw);
@@ -889,7 +904,10 @@ class BregmanEngine {
         col_lse_partial_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk, sw == 1);
         col_lse_combine_kernel<<<static_cast<unsigned>((m_ + 255) / 256), 256, 0, s_>>>(v, sw == 1);
         col_flag_kernel<<<1, 1, 0, s_>>>(v, sw);
-        if (cfg_.inner_iters > 64 && (sw % 32) == 0) {
+        write_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk);
+        sink_partial_kernel<<<static_cast<unsigned>(v.dev_rb + v.dev_cb), 256, 0, s_>>>(v);
+        sink_decide_kernel<<<1, 256, 0, s_>>>(v, sw, sw == cfg_.inner_iters);
+        if (poll ? sw < cfg_.inner_iters : cfg_.inner_iters > 64 && (sw % 32) == 0) {
           // Long inner loops: stop enqueueing once the device has converged.
           BState h;
           GWB_CUDA(cudaMemcpyAsync(&h, st_, sizeof(h), cudaMemcpyDeviceToHost, s_));
@@ -897,9 +915,6 @@ class BregmanEngine {
           if (h.done || h.sink_done) break;
         }
       }
-      dim3 grid(static_cast<unsigned>(colblocks_), static_cast<unsigned>(chunks_));
-      write_kernel<<<grid, kThreads, 0, s_>>>(v, rows_per_chunk);
-      breg_dev_partial_kernel<<<static_cast<unsigned>(v.dev_rb + v.dev_cb), 256, 0, s_>>>(v);
       breg_finalize_kernel<<<1, 1024, 0, s_>>>(v, 0);
       GWB_CUDA(cudaGetLastError());
     }
@@ -1028,7 +1043,8 @@ class BregmanEngine {
     d.f_new = fn_;
     d.g = g_;
     d.rowmax = rowmax_;
-    d.row_err = row_err_;
+    d.row_sum_raw = row_sum_raw_;
+    d.err_part = err_part_;
     d.col_err = col_err_;
     d.col_pm = col_pm_;
     d.col_ps = col_ps_;
@@ -1278,7 +1294,7 @@ class BregmanEngine {
   int f16_s1_ = 0;
   float* f16_g1_rs_ = nullptr;
   float* f16_g2_cs_ = nullptr;
-  double *mu_, *nu_, *f_, *fn_, *g_, *row_err_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
+  double *mu_, *nu_, *f_, *fn_, *g_, *row_sum_raw_, *err_part_, *col_err_, *col_pm_, *col_ps_, *col_sum_,
       *row_sum_, *obj_part_, *wpart_, *dev_part_;
   float* col_pe_;
   int chunks_ = 1, colblocks_ = 1, dev_rb_ = 1, dev_cb_ = 1;
