@@ -197,16 +197,31 @@ __global__ void __launch_bounds__(kThreads) form_kernel(BDev d, int tail) {
     double rmax = -INFINITY;
     // One pass: G and π are read once and LK is written unshifted (a row
     // shift would need a second pass; the row potential f absorbs it).
-#pragma unroll 4
-    for (int64_t j = lane; j < d.m; j += 32) {
-      const double gv = g[j], pv = p[j];
-      obj = __fma_rn(gv, pv, obj);
+    // 4 consecutive columns per lane (float4 of G, double2 pairs of π and
+    // LK); ld is a multiple of 32, so a group that starts in the row stays
+    // in it, and padding columns (G = π = 0) are masked.
+#pragma unroll 2
+    for (int64_t j = 4 * lane; j < d.m; j += 128) {
+      const float4 g4 = *reinterpret_cast<const float4*>(g + j);
+      const double2 p01 = *reinterpret_cast<const double2*>(p + j);
+      const double2 p23 = *reinterpret_cast<const double2*>(p + j + 2);
+      const double gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      const double pv[4] = {p01.x, p01.y, p23.x, p23.y};
+      double lk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool in = j + q < d.m;
+        obj = __fma_rn(gv[q], pv[q], obj);
+        const double e = sc * gv[q];
+        lk[q] = ebpg ? e : e + log(pv[q]);
+        if (in) {
+          emax = fmaxf(emax, static_cast<float>(e));
+          rmax = fmax(rmax, lk[q]);
+        }
+      }
       if (tail) continue;
-      const double e = sc * gv;
-      emax = fmaxf(emax, static_cast<float>(e));
-      const double lk = ebpg ? e : e + log(pv);
-      rmax = fmax(rmax, lk);
-      lkrow[j] = lk;
+      *reinterpret_cast<double2*>(lkrow + j) = make_double2(lk[0], lk[1]);
+      *reinterpret_cast<double2*>(lkrow + j + 2) = make_double2(lk[2], lk[3]);
     }
     obj = warp_sum(obj);
     rmax = warp_max_d(rmax);
@@ -444,12 +459,19 @@ __global__ void __launch_bounds__(kThreads) write_kernel(BDev d, int rows_per_ch
   if (ok)
 #pragma unroll
     for (int q = 0; q < 4; ++q) gj[q] = (c0 + q < d.m) ? d.g[c0 + q] : 0.0;
+  const double fl = clamp_floor(d);
+#pragma unroll 2
   for (int64_t i = r0 + warp; i < r1; i += kThreads / 32) {
     double rs = 0.0, rr = 0.0;
     if (ok) {
-      const double* lk = d.LK + i * d.ld + c0;
-      const double* pp = d.P + i * d.ld + c0;
-      const double fl = clamp_floor(d), fi = d.f[i];
+      // c0 < m ≤ ld and ld is a multiple of 32: the 4 entries stay in the row.
+      const double2 lk01 = *reinterpret_cast<const double2*>(d.LK + i * d.ld + c0);
+      const double2 lk23 = *reinterpret_cast<const double2*>(d.LK + i * d.ld + c0 + 2);
+      const double2 pp01 = *reinterpret_cast<const double2*>(d.P + i * d.ld + c0);
+      const double2 pp23 = *reinterpret_cast<const double2*>(d.P + i * d.ld + c0 + 2);
+      const double lk[4] = {lk01.x, lk01.y, lk23.x, lk23.y};
+      const double pp[4] = {pp01.x, pp01.y, pp23.x, pp23.y};
+      const double fi = d.f[i];
       double o[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
