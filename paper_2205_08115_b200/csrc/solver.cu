@@ -176,9 +176,16 @@ void BapgEngine::alloc() {
   nu64_ = dalloc<double>(stream_, ldm_);
   row_part_ = dalloc<RowPart>(stream_, n_);
   cw_part_ = dalloc<ColWritePart>(stream_, n_);
-  // Column-pass chunking: enough CTAs to fill the chip (≥ 2 waves of 148).
+  // Column-pass chunking: ~16 CTAs per SM (large n), so the column-partial
+  // grid balances across the 148 SMs (4 per SM left 628 CTAs at c4: 4.24
+  // waves, the busiest SMs 18% above the mean).  GWB_COL_CTAS_PER_SM (A/B).
   const int64_t col_blocks = (m_ + 127) / 128;
-  chunks_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n_ + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks)));
+  static const int64_t col_per_sm = [] {
+    const char* e = std::getenv("GWB_COL_CTAS_PER_SM");
+    return static_cast<int64_t>(e && std::atoi(e) > 0 ? std::atoi(e) : 16);
+  }();
+  chunks_ = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((n_ + 63) / 64, (col_per_sm * 148 + col_blocks - 1) / col_blocks)));
   col_pmax_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
   col_psum_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
   col_psump_ = dalloc<double>(stream_, static_cast<size_t>(chunks_) * m_);
