@@ -19,24 +19,66 @@ namespace gwb {
 
 namespace {
 
+// The leaf entry points (device_*) each run on their own non-blocking
+// stream: a LeafStream scope creates it and points t_leaf at it, so every
+// buffer fill, copy and kernel of the call is ordered on that stream and
+// nothing touches the legacy default stream (which would serialise with
+// other work on the device).  Outside a scope (the engine-stream helpers
+// structure_product_dev / gw_objective_dev / coupling_entropy_dev) t_leaf is
+// null and buffers are filled synchronously.
+thread_local cudaStream_t t_leaf = nullptr;
+
+struct LeafStream {
+  cudaStream_t prev;
+  cudaStream_t s = nullptr;
+  LeafStream() : prev(t_leaf) {
+    GWB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    t_leaf = s;
+  }
+  ~LeafStream() {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    t_leaf = prev;
+  }
+  LeafStream(const LeafStream&) = delete;
+  LeafStream& operator=(const LeafStream&) = delete;
+};
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   explicit DBuf(size_t count) : n(count) {
-    GWB_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 256));
-    GWB_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 256));
-    // The memset runs on the legacy stream, which does not order with the
-    // engines' non-blocking streams: finish it before the buffer is used.
-    GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 256;
+    GWB_CUDA(cudaMalloc(&p, bytes));
+    if (t_leaf) {
+      GWB_CUDA(cudaMemsetAsync(p, 0, bytes, t_leaf));
+    } else {
+      // Not inside a leaf scope: fill synchronously, so the buffer is ready
+      // for the caller's (non-blocking) stream.
+      GWB_CUDA(cudaMemset(p, 0, bytes));
+      GWB_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    }
   }
   ~DBuf() {
     if (p) cudaFree(p);
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  void up(const T* h) { GWB_CUDA(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice)); }
-  void down(T* h) const { GWB_CUDA(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost)); }
+  void up(const T* h) {
+    if (t_leaf)
+      GWB_CUDA(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, t_leaf));
+    else
+      GWB_CUDA(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void down(T* h) const {
+    if (t_leaf) {
+      GWB_CUDA(cudaMemcpyAsync(h, p, n * sizeof(T), cudaMemcpyDeviceToHost, t_leaf));
+      GWB_CUDA(cudaStreamSynchronize(t_leaf));
+    } else {
+      GWB_CUDA(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    }
+  }
 };
 
 unsigned blocks(int64_t work, int threads) {
@@ -231,15 +273,15 @@ double reduce_host(const DBuf<double>& part) {
 
 double sum_sq_diff(const double* a, const double* b, int64_t len) {
   DBuf<double> part(592);
-  sq_diff_kernel<<<592, 256>>>(a, b, len, part.p);
+  sq_diff_kernel<<<592, 256, 0, t_leaf>>>(a, b, len, part.p);
   GWB_CUDA(cudaGetLastError());
   return reduce_host(part);
 }
 
 double marginal_err_inf(const DBuf<double>& c, int64_t n, int64_t m, const double* mu,
                         const double* nu, DBuf<double>& rs, DBuf<double>& cs) {
-  rowsum_kernel<<<blocks(n, 256), 256>>>(c.p, n, m, rs.p);
-  colsum_kernel<<<static_cast<unsigned>(m), 256>>>(c.p, n, m, cs.p);
+  rowsum_kernel<<<blocks(n, 256), 256, 0, t_leaf>>>(c.p, n, m, rs.p);
+  colsum_kernel<<<static_cast<unsigned>(m), 256, 0, t_leaf>>>(c.p, n, m, cs.p);
   std::vector<double> hr(n), hc(m);
   rs.down(hr.data());
   cs.down(hc.data());
@@ -252,12 +294,12 @@ double marginal_err_inf(const DBuf<double>& c, int64_t n, int64_t m, const doubl
 // kl_scale on device data; throws ZeroSumLineError for the lowest bad line.
 void kl_scale_dev(DBuf<double>& a, int64_t n, int64_t m, const DBuf<double>& target, int axis,
                   DBuf<double>& sums) {
-  if (axis == GWB_ROWS) rowsum_kernel<<<blocks(n, 256), 256>>>(a.p, n, m, sums.p);
-  else colsum_kernel<<<static_cast<unsigned>(m), 256>>>(a.p, n, m, sums.p);
+  if (axis == GWB_ROWS) rowsum_kernel<<<blocks(n, 256), 256, 0, t_leaf>>>(a.p, n, m, sums.p);
+  else colsum_kernel<<<static_cast<unsigned>(m), 256, 0, t_leaf>>>(a.p, n, m, sums.p);
   DBuf<int> bad(1);
   const int init = 0x7fffffff;
   bad.up(&init);
-  scale_lines_kernel<<<blocks(n * m, 256), 256>>>(a.p, n, m, target.p, sums.p, axis, bad.p);
+  scale_lines_kernel<<<blocks(n * m, 256), 256, 0, t_leaf>>>(a.p, n, m, target.p, sums.p, axis, bad.p);
   int hb;
   bad.down(&hb);
   if (hb != 0x7fffffff) api_zero_sum(axis, hb);
@@ -268,10 +310,11 @@ void kl_scale_dev(DBuf<double>& a, int64_t n, int64_t m, const DBuf<double>& tar
 void device_product_coupling(const double* mu, int64_t n, const double* nu, int64_t m,
                              double* out) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> dmu(n), dnu(m), o(static_cast<size_t>(n) * m);
   dmu.up(mu);
   dnu.up(nu);
-  outer_kernel<<<blocks(n * m, 256), 256>>>(dmu.p, n, dnu.p, m, o.p);
+  outer_kernel<<<blocks(n * m, 256), 256, 0, t_leaf>>>(dmu.p, n, dnu.p, m, o.p);
   GWB_CUDA(cudaGetLastError());
   o.down(out);
 }
@@ -279,6 +322,7 @@ void device_product_coupling(const double* mu, int64_t n, const double* nu, int6
 void device_kl_scale(const double* pi, int64_t n, int64_t m, const double* target, int32_t axis,
                      double* out) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> a(static_cast<size_t>(n) * m), t(axis == GWB_ROWS ? n : m),
       sums(axis == GWB_ROWS ? n : m);
   a.up(pi);
@@ -290,10 +334,11 @@ void device_kl_scale(const double* pi, int64_t n, int64_t m, const double* targe
 double device_marginal_infeasibility(const double* pi, int64_t n, int64_t m, const double* mu,
                                      const double* nu) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> a(static_cast<size_t>(n) * m), rs(n), cs(m);
   a.up(pi);
-  rowsum_kernel<<<blocks(n, 256), 256>>>(a.p, n, m, rs.p);
-  colsum_kernel<<<static_cast<unsigned>(m), 256>>>(a.p, n, m, cs.p);
+  rowsum_kernel<<<blocks(n, 256), 256, 0, t_leaf>>>(a.p, n, m, rs.p);
+  colsum_kernel<<<static_cast<unsigned>(m), 256, 0, t_leaf>>>(a.p, n, m, cs.p);
   std::vector<double> hr(n), hc(m);
   rs.down(hr.data());
   cs.down(hc.data());
@@ -305,6 +350,7 @@ double device_marginal_infeasibility(const double* pi, int64_t n, int64_t m, con
 
 double device_split_gap(const double* pi, const double* w, int64_t n, int64_t m) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> a(static_cast<size_t>(n) * m), b(static_cast<size_t>(n) * m);
   a.up(pi);
   b.up(w);
@@ -313,10 +359,11 @@ double device_split_gap(const double* pi, const double* w, int64_t n, int64_t m)
 
 void device_hard_assignment(const double* pi, int64_t n, int64_t m, int32_t* out) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> a(static_cast<size_t>(n) * m);
   DBuf<int32_t> o(n);
   a.up(pi);
-  argmax_kernel<<<blocks(n, 128), 128>>>(a.p, n, m, o.p);
+  argmax_kernel<<<blocks(n, 128), 128, 0, t_leaf>>>(a.p, n, m, o.p);
   GWB_CUDA(cudaGetLastError());
   o.down(out);
 }
@@ -329,11 +376,11 @@ static double spectral_norm_on_device(const double* d, int64_t n) {
   x.up(hx.data());
   double lambda = 0.0;
   for (int it = 0; it < 10000; ++it) {
-    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d, n, x.p, t.p);
-    symv64_kernel<<<blocks(n * 32, 256), 256>>>(d, n, t.p, y.p);
+    symv64_kernel<<<blocks(n * 32, 256), 256, 0, t_leaf>>>(d, n, x.p, t.p);
+    symv64_kernel<<<blocks(n * 32, 256), 256, 0, t_leaf>>>(d, n, t.p, y.p);
     const double est = std::sqrt(sum_sq_diff(y.p, nullptr, n));
     if (est == 0.0) return 0.0;
-    div_kernel<<<blocks(n, 256), 256>>>(y.p, n, est);
+    div_kernel<<<blocks(n, 256), 256, 0, t_leaf>>>(y.p, n, est);
     std::swap(x.p, y.p);
     const double conv = std::fabs(est - lambda);
     lambda = est;
@@ -360,11 +407,10 @@ __global__ void adjacency64_kernel(const int2* e, int64_t count, int64_t n, doub
 // ‖A‖₂ of adjacency_distance(g) (tasks.cpp:167-174) built on the device.
 static double spectral_norm_graph(const int32_t* edges, int64_t count, int64_t n) {
   DBuf<double> d(static_cast<size_t>(n) * n);
-  GWB_CUDA(cudaMemset(d.p, 0, sizeof(double) * static_cast<size_t>(n) * n));
   if (count > 0) {
     DBuf<int2> e(static_cast<size_t>(count));
-    GWB_CUDA(cudaMemcpy(e.p, edges, sizeof(int2) * count, cudaMemcpyHostToDevice));
-    adjacency64_kernel<<<static_cast<unsigned>(std::min<int64_t>(blocks(count, 256), 1184)), 256>>>(
+    GWB_CUDA(cudaMemcpyAsync(e.p, edges, sizeof(int2) * count, cudaMemcpyHostToDevice, t_leaf));
+    adjacency64_kernel<<<static_cast<unsigned>(std::min<int64_t>(blocks(count, 256), 1184)), 256, 0, t_leaf>>>(
         e.p, count, n, d.p);
     GWB_CUDA(cudaGetLastError());
   }
@@ -373,11 +419,13 @@ static double spectral_norm_graph(const int32_t* edges, int64_t count, int64_t n
 
 double device_lipschitz_bound(const double* dx, int64_t n, const double* dy, int64_t m) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   return spectral_norm_dev(dx, n) * spectral_norm_dev(dy, m);
 }
 
 double device_lipschitz_bound_graphs(const GraphInput& g, int64_t n, int64_t m) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   return spectral_norm_graph(g.ex, g.cx, n) * spectral_norm_graph(g.ey, g.cy, m);
 }
 
@@ -386,6 +434,7 @@ void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* m
                      double* out, int32_t* iterations, double* marginal_error,
                      int32_t* converged) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   const int64_t len = n * m;
   DBuf<double> c(static_cast<size_t>(len)), dmu(n), dnu(m), rs(n), cs(m);
   dmu.up(mu);
@@ -401,7 +450,7 @@ void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* m
       kl_scale_dev(c, n, m, dnu, GWB_COLS, cs);
       const int zero = 0;
       bad.up(&zero);
-      all_finite_kernel<<<592, 256>>>(c.p, len, bad.p);
+      all_finite_kernel<<<592, 256, 0, t_leaf>>>(c.p, len, bad.p);
       int hb;
       bad.down(&hb);
       if (hb) api_numerical("sinkhorn", sweep, "non-finite entries after scaling sweep");
@@ -416,12 +465,12 @@ void device_sinkhorn(const double* kernel, int64_t n, int64_t m, const double* m
     DBuf<double> e(static_cast<size_t>(len)), f(n), g(m);
     e.up(kernel);
     for (int sweep = 1; sweep <= max_iters; ++sweep) {
-      lse_rows_kernel<<<blocks(n, 128), 128>>>(e.p, n, m, g.p, dmu.p, f.p);
-      lse_cols_kernel<<<static_cast<unsigned>(m), 256>>>(e.p, n, m, f.p, dnu.p, g.p);
-      exp_fg_kernel<<<blocks(len, 256), 256>>>(e.p, n, m, f.p, g.p, c.p);
+      lse_rows_kernel<<<blocks(n, 128), 128, 0, t_leaf>>>(e.p, n, m, g.p, dmu.p, f.p);
+      lse_cols_kernel<<<static_cast<unsigned>(m), 256, 0, t_leaf>>>(e.p, n, m, f.p, dnu.p, g.p);
+      exp_fg_kernel<<<blocks(len, 256), 256, 0, t_leaf>>>(e.p, n, m, f.p, g.p, c.p);
       const int zero = 0;
       bad.up(&zero);
-      all_finite_kernel<<<592, 256>>>(c.p, len, bad.p);
+      all_finite_kernel<<<592, 256, 0, t_leaf>>>(c.p, len, bad.p);
       int hb;
       bad.down(&hb);
       if (hb) api_numerical("sinkhorn-log", sweep, "non-finite entries after scaling sweep");
@@ -483,16 +532,17 @@ double gw_objective_dev(const float* Dx_in, int64_t ldn, const float* Dy_in, int
 double device_gw_objective(const double* dx, int64_t n, const double* dy, int64_t m,
                            const double* pi) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   const int64_t ldn = round_up(n, 32), ldm = round_up(m, 32);
   const int64_t big = std::max(n * n, std::max(m * m, n * m));
   DBuf<double> stage(static_cast<size_t>(big));
   DBuf<float> Dx(n * ldn), Dy(m * ldm), P(n * ldm);
-  cudaStream_t s = nullptr;
-  GWB_CUDA(cudaMemcpy(stage.p, dx, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  cudaStream_t s = leaf.s;
+  GWB_CUDA(cudaMemcpyAsync(stage.p, dx, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   launch_colmajor64_to_rowmajor32(stage.p, n, n, Dx.p, ldn, s);
-  GWB_CUDA(cudaMemcpy(stage.p, dy, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+  GWB_CUDA(cudaMemcpyAsync(stage.p, dy, sizeof(double) * m * m, cudaMemcpyHostToDevice, s));
   launch_colmajor64_to_rowmajor32(stage.p, m, m, Dy.p, ldm, s);
-  GWB_CUDA(cudaMemcpy(stage.p, pi, sizeof(double) * n * m, cudaMemcpyHostToDevice));
+  GWB_CUDA(cudaMemcpyAsync(stage.p, pi, sizeof(double) * n * m, cudaMemcpyHostToDevice, s));
   launch_colmajor64_to_rowmajor32(stage.p, n, m, P.p, ldm, s);
   return gw_objective_dev(Dx.p, ldn, Dy.p, ldm, P.p, n, m, s);
 }
@@ -527,9 +577,10 @@ double coupling_entropy_dev(const double* pi_dev, int64_t len, cudaStream_t s) {
 
 double device_coupling_entropy(const double* pi, int64_t n, int64_t m) {
   GWB_CUDA(cudaSetDevice(api_device()));
+  LeafStream leaf;
   DBuf<double> d(static_cast<size_t>(n) * m);
   d.up(pi);
-  return coupling_entropy_dev(d.p, n * m, nullptr);
+  return coupling_entropy_dev(d.p, n * m, leaf.s);
 }
 
 }  // namespace gwb
