@@ -480,7 +480,8 @@ def run_ours(args, world, rank, local, dist):
                                  "the kind::f16 rate)" if f16_pipe else "cuBLAS TF32 measured in this run"),
         "executed_frac": (achieved * passes / exec_peak) if (achieved and exec_peak) else None,
         "algorithmic_flops_per_launch_pair": chain_flops,
-        "traffic": gemm_traffic(n),
+        "traffic": (gemm_traffic(n) or {}).get("bytes_per_launch"),
+        "traffic_detail": gemm_traffic(n),
         "scaling_kernels_ms_per_half_step": main["scal_ms"],
     }
     del dx, dy
