@@ -13,6 +13,7 @@
 #include "devutil.cuh"
 #include "kernels.cuh"
 #include "launch.cuh"
+#include "narrow.cuh"
 
 namespace gwb {
 void check_cuda(cudaError_t e, const char* what);  // solver.cu: throws CudaError
@@ -25,47 +26,6 @@ namespace {
 
 using namespace dev;
 constexpr int kRowThreads = 256;
-
-// ---------------------------------------------------------------------------
-// Entropy BAPG projections on fp64 iterates.  G arrives in
-// fp32 from the chain; the exponent x = g·(1/ρ), the online (max, Σ), the
-// exponentials and the iterates are fp64, as the reference computes them
-// (solvers.cpp:164-177, projections.cpp:12-34).  The same helper forms x
-// in the (max, Σ) pass and the write pass, so numerators and normaliser
-// agree bitwise.
-__device__ __forceinline__ double expo(float g, double inv_rho) {
-  return __dmul_rn(static_cast<double>(g), inv_rho);
-}
-
-__device__ __forceinline__ void load_d4(const double* p, double (&v)[4]) {
-  const double2 a = *reinterpret_cast<const double2*>(p);
-  const double2 b = *reinterpret_cast<const double2*>(p + 2);
-  v[0] = a.x;
-  v[1] = a.y;
-  v[2] = b.x;
-  v[3] = b.y;
-}
-
-__device__ __forceinline__ void store_d4(double* p, const double (&v)[4]) {
-  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
-}
-
-// PDL (launch.cuh): wait for the predecessor kernel's results, then let the
-// successor's CTAs be scheduled.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// A device error flag (DevFlag) raised at the current iteration: the first
-// raise records err_iter; the iteration's remaining projection kernels skip
-// on `flags`, and the finalize marks the solve done (no separate check
-// launches).
-__device__ __forceinline__ void raise_flag(DevStatus* st, int flag) {
-  atomicOr(&st->flags, flag);
-  atomicCAS(&st->err_iter, 0, st->iter);
-}
 
 // Half-step a: one CTA per row.
 // ---------------------------------------------------------------------------
@@ -247,90 +207,17 @@ __global__ void __launch_bounds__(kRowThreads) row_diag32_kernel(BapgDev d) {
   }
 }
 
-// Narrow rows (m ≤ kNarrowM, config 3): one warp per row, 8 rows per CTA,
-// lane l covering the 4-column groups at 4l + 128v — the row sits in
-// registers between the (max, Σ) pass and the write, no block barriers.
-constexpr int kNarrowM = 128;
-constexpr int kNarrowV = kNarrowM / 128;  // 4-column groups per lane
+// Narrow rows (m ≤ kNarrowM, config 3): one warp per row, 8 rows per CTA
+// (narrow.cuh: the row sits in registers between the (max, Σ) pass and the
+// write, no block barriers).
 constexpr int kWarpRows = kRowThreads / 32;
 
 __global__ void __launch_bounds__(kRowThreads) row_update_warps_kernel(BapgDev d, int write, int tail) {
   pdl_enter();
   if (tail ? d.st->flags != 0 : d.st->done != 0) return;
-  const int lane = threadIdx.x & 31;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kWarpRows + threadIdx.x / 32;
   if (i >= d.n) return;
-  const float* g = d.G + i * d.ld;
-  const double* w = d.W64 + i * d.ld;
-  const int64_t m = d.m;
-  const double inv_rho = d.inv_rho64;
-  Lse64 ms{-INFINITY, 0.0};
-  double sums[2] = {0.0, 0.0};
-  float gv[kNarrowV][4];
-  double wv[kNarrowV][4];
-#pragma unroll
-  for (int v = 0; v < kNarrowV; ++v) {
-    const int64_t j = lane * 4 + 128 * v;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      gv[v][q] = 0.f;
-      wv[v][q] = 0.0;
-    }
-    if (j < m) {
-      const float4 g4 = *reinterpret_cast<const float4*>(g + j);
-      gv[v][0] = g4.x;
-      gv[v][1] = g4.y;
-      gv[v][2] = g4.z;
-      gv[v][3] = g4.w;
-      load_d4(w + j, wv[v]);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < kNarrowV; ++v) {
-    const int64_t j = lane * 4 + 128 * v;
-    if (j >= m) break;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (j + q < m) {
-        lse64_add(ms, expo(gv[v][q], inv_rho), wv[v][q]);
-        sums[0] = __fma_rn(static_cast<double>(gv[v][q]), wv[v][q], sums[0]);
-        sums[1] += wv[v][q];
-      }
-    }
-  }
-  ms = lse64_warp_merge(ms);
-  // The xor butterfly leaves lane-dependent roundings; every lane takes lane 0's.
-  ms.mx = __shfl_sync(0xffffffffu, ms.mx, 0);
-  ms.s = __shfl_sync(0xffffffffu, ms.s, 0);
-  sums[0] = warp_sum(sums[0]);
-  sums[1] = warp_sum(sums[1]);
-  if (lane == 0) {
-    d.row_part[i].gw = sums[0];
-    const double dev = sums[1] - d.mu64[i];
-    d.row_part[i].rowdev = dev * dev;
-  }
-  if (!write) return;
-  const double S = ms.s;
-  const double r = ms.mx;
-  if (lane == 0) {
-    if (r > 700.0) raise_flag(d.st, kFlagOverflowA);
-    if (!(S > 0.0) || !isfinite(S) || isnan(r)) {
-      raise_flag(d.st, kFlagZeroA);
-      atomicMin(&d.st->zero_index, static_cast<int>(i));
-    }
-  }
-  const double scale = d.mu64[i] / S;
-#pragma unroll
-  for (int v = 0; v < kNarrowV; ++v) {
-    const int64_t j = lane * 4 + 128 * v;
-    if (j >= m) break;
-    double o[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      o[q] = (j + q < m) ? scale * wv[v][q] * exp(expo(gv[v][q], inv_rho) - r) : 0.0;
-    store_d4(d.P64 + i * d.ld + j, o);
-    aux_store4_64(d.P_aux, d.P, d.aux_mode, d.plane, i * d.ld + j, o, d.aux_scale);
-  }
+  narrow_row_update<32>(d, i, d.G + i * d.ld, threadIdx.x & 31, true, write, nullptr);
 }
 
 // ---------------------------------------------------------------------------

@@ -37,6 +37,17 @@ SkinnyTcPlan* skinny_tc_plan_create(const void* a_packed, const void* b_packed, 
                                     const int* skip, cudaStream_t s);
 void skinny_tc_plan_destroy(SkinnyTcPlan* plan, cudaStream_t s);
 void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s);
+// Half-step a in one launch (entropy BAPG, fp64 iterates; solvers.cpp:164-170
+// behind the chain): GEMM2 as above, then each cluster rank runs the row
+// update of the rows it summed (d: the engine's device view, G read from
+// shared memory) and forms half-step b's GEMM1 — the packed Vᵀ planes of
+// (new π)·D_Yᵀ — into `next_b`, a plane buffer other than the one being
+// streamed.  Replaces skinny_tc_launch + launch_row_update +
+// launch_skinny_planes; same arithmetic.  Needs skinny_tc_can_fuse(plan).
+struct BapgDev;
+bool skinny_tc_can_fuse(const SkinnyTcPlan* plan);
+void skinny_tc_launch_fused_a(const SkinnyTcPlan* plan, const BapgDev& d, const float* dyt,
+                              int64_t ld_dyt, void* next_b, int64_t next_pstride, cudaStream_t s);
 
 // dst (cols × rows, ldd) = srcᵀ (src rows × cols, lds).
 void launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst,

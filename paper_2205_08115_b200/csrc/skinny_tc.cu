@@ -29,6 +29,7 @@
 #include <stdexcept>
 
 #include "gemm.cuh"
+#include "narrow.cuh"
 #include "ptx.cuh"
 #include "skinny.cuh"
 
@@ -59,8 +60,20 @@ struct SkinnyTcParams {
   int N;
   int kblocks, splits, kb_per;
   const int* skip;
+  // Fused half-step a (kEpi == 1): the cluster rank that sums rows
+  // [rbeg, rend) of G then runs their row update (narrow.cuh) and forms the
+  // next GEMM1, Vᵀ planes of (new π)·D_Yᵀ, into `next_b` — a second packed
+  // plane buffer, since peers are still streaming `b`.
+  BapgDev d;
+  const float* dyt;  // D_Yᵀ, N×N fp32 row-major
+  int64_t ld_dyt;
+  uint16_t* next_b;
+  int64_t next_pstride;
 };
 
+constexpr int kFuseRows = 32;  // rows per cluster rank in the fused epilogue (splits ≥ 4)
+
+template <int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
     skinny_tc_kernel(const __grid_constant__ SkinnyTcParams p) {
   if (p.skip != nullptr && *p.skip != 0) return;
@@ -70,6 +83,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) float part[kBM][kBN + 4];  // split-K partial (padded rows)
+  // Fused epilogue: this rank's summed rows of G, the fp32 copy of their new
+  // π rows, D_Yᵀ.
+  __shared__ __align__(16) float gsum[kEpi ? kFuseRows : 1][kBN + 4];
+  __shared__ float xs[kEpi ? kFuseRows : 1][kBN + 1];
+  __shared__ float bs[kEpi ? kBN : 1][kBN];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
   const int kb0 = split * p.kb_per;
@@ -180,8 +198,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum = 0.f;
       for (int q = 0; q < S; ++q) sum += *cluster.map_shared_rank(&part[r][j], q);
       p.c[row * p.ldc + j] = sum;
+      if constexpr (kEpi == 1) gsum[r - rbeg][j] = sum;
+    }
+    if constexpr (kEpi == 1) {
+      for (int e = threadIdx.x; e < kBN * kBN; e += kThreads) {
+        const int k = e / kBN, c = e % kBN;
+        bs[k][c] = (k < p.N && c < p.N) ? p.dyt[static_cast<int64_t>(k) * p.ld_dyt + c] : 0.f;
+      }
     }
     cluster.sync();  // peers may still read this CTA's partials
+    if constexpr (kEpi == 1) {
+      // Half-step a on this rank's rows (the standalone
+      // row_update_warps_kernel's arithmetic, bit for bit), keeping the fp32 rows.
+      // Eight lanes per row (N ≤ 32 = 8 lanes × 4 columns), four rows per warp.
+      for (int r0 = rbeg; r0 < rend; r0 += kThreads / 8) {
+        const int r = r0 + static_cast<int>(threadIdx.x) / 8;
+        const int64_t row = static_cast<int64_t>(tile) * kBM + r;
+        const bool active = r < rend && row < p.d.n;
+        const int rl = active ? r - rbeg : 0;
+        dev::narrow_row_update<8>(p.d, row, &gsum[rl][0], lane, active, 1, &xs[rl][0]);
+      }
+      __syncthreads();
+      // GEMM1 of half-step b for the same rows: lane = row, warps over the
+      // output columns; k in order with fmaf, the bf16 planes written in
+      // GEMM2's packed order (small_k_planes_kernel's arithmetic, skinny.cu).
+      const int64_t row = static_cast<int64_t>(tile) * kBM + rbeg + lane;
+      if (rbeg + lane < rend && row < p.M) {
+        float a[kBN];
+#pragma unroll
+        for (int k = 0; k < kBN; ++k) a[k] = xs[lane][k];
+        for (int c = warp; c < p.N; c += kThreads / 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < kBN; ++k)
+            if (k < p.N) acc = fmaf(a[k], bs[k][c], acc);
+          const int64_t off =
+              (row >> 6) * 2048 + c * 64 + ((((row >> 3) & 7) ^ (c & 7)) << 3) + (row & 7);
+          float x = acc;
+          for (int q = 0; q < p.planes; ++q) {
+            const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+            p.next_b[q * p.next_pstride + off] = __bfloat16_as_ushort(hb);
+            x -= __bfloat162float(hb);
+          }
+        }
+      }
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -256,9 +317,12 @@ SkinnyTcPlan* skinny_tc_plan_create(const void* a_packed, const void* b_packed, 
   plan->grid = tiles * splits;
   static thread_local int attr_device = -1;
   if (attr_device != dev) {
-    check_cuda(cudaFuncSetAttribute(skinny_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    check_cuda(cudaFuncSetAttribute(skinny_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem)),
                "skinny_tc: smem attribute");
+    check_cuda(cudaFuncSetAttribute(skinny_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem)),
+               "skinny_tc: smem attribute (fused)");
     attr_device = dev;
   }
   return plan;
@@ -269,7 +333,9 @@ void skinny_tc_plan_destroy(SkinnyTcPlan* plan, cudaStream_t s) {
   delete plan;
 }
 
-void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s) {
+namespace {
+template <int kEpi>
+void launch_tc(const SkinnyTcPlan* plan, const SkinnyTcParams& params, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(plan->grid));
   cfg.blockDim = dim3(kThreads);
@@ -284,7 +350,28 @@ void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  check_cuda(cudaLaunchKernelEx(&cfg, skinny_tc_kernel, plan->params), "skinny_tc_kernel");
+  check_cuda(cudaLaunchKernelEx(&cfg, skinny_tc_kernel<kEpi>, params), "skinny_tc_kernel");
+}
+}  // namespace
+
+void skinny_tc_launch(const SkinnyTcPlan* plan, cudaStream_t s) { launch_tc<0>(plan, plan->params, s); }
+
+bool skinny_tc_can_fuse(const SkinnyTcPlan* plan) {
+  // Each cluster rank sums ⌈128 / splits⌉ rows; the fused epilogue holds 32.
+  return plan->params.splits > 1 &&
+         (kBM + plan->params.splits - 1) / plan->params.splits <= kFuseRows;
+}
+
+void skinny_tc_launch_fused_a(const SkinnyTcPlan* plan, const BapgDev& d, const float* dyt,
+                              int64_t ld_dyt, void* next_b, int64_t next_pstride, cudaStream_t s) {
+  if (!skinny_tc_can_fuse(plan)) throw std::logic_error("skinny_tc: fused epilogue needs ≥ 4 K splits");
+  SkinnyTcParams params = plan->params;
+  params.d = d;
+  params.dyt = dyt;
+  params.ld_dyt = ld_dyt;
+  params.next_b = static_cast<uint16_t*>(next_b);
+  params.next_pstride = next_pstride;
+  launch_tc<1>(plan, params, s);
 }
 
 }  // namespace gwb

@@ -132,10 +132,12 @@ BapgEngine::~BapgEngine() {
   csr_free(cy_);
   skinny_tc_plan_destroy(stc_, stream_);
   skinny_tc_plan_destroy(stc_tail_, stream_);
+  skinny_tc_plan_destroy(stc_b_, stream_);
   dfree(Vs_, stream_);
   dfree(DyT_, stream_);
   dfree(Dxp_, stream_);
   dfree(Vtp_, stream_);
+  dfree(Vtp2_, stream_);
   for (void* p : std::initializer_list<void*>{
            Dx_, Dx_aux_, Dy_, Dy_aux_, Dx_bf_, Dy_bf_, P_, P_aux_, W_[0], W_[1], W_aux_[0],
            W_aux_[1], P64_, W64_[0], W64_[1], Vt_,
@@ -263,7 +265,8 @@ void BapgEngine::prepare_d() {
   if (precision_ == GWB_PREC_FP32 && m_ > kSkinnyMaxN) precision_ = GWB_PREC_AUTO;
   skinny_tc_plan_destroy(stc_, stream_);
   skinny_tc_plan_destroy(stc_tail_, stream_);
-  stc_ = stc_tail_ = nullptr;
+  skinny_tc_plan_destroy(stc_b_, stream_);
+  stc_ = stc_tail_ = stc_b_ = nullptr;
   skinny_tc_ = false;
   if (m_ <= kSkinnyMaxN && (h_inexact[0] & 2) == 0 &&
       (precision_ == GWB_PREC_AUTO || precision_ == GWB_PREC_BF16X3)) {
@@ -280,6 +283,19 @@ void BapgEngine::prepare_d() {
                                  stream_);
     stc_tail_ = skinny_tc_plan_create(Dxp_, Vtp_, 3, G_, ldm_, n_, static_cast<int>(m_), n_,
                                       &st_->flags, stream_);
+    // Fused schedule (entropy geometry): half-step a's GEMM2 also runs the
+    // row update and half-step b's GEMM1 (skinny_tc_launch_fused_a), writing
+    // the second plane buffer, which half-step b's GEMM2 streams.
+    // GWB_SKINNY_UNFUSED=1 keeps one launch per stage (A/B knob).
+    static const bool unfused_env = [] {
+      const char* e = std::getenv("GWB_SKINNY_UNFUSED");
+      return e && e[0] == '1';
+    }();
+    if (!unfused_env && skinny_tc_can_fuse(stc_)) {
+      if (!Vtp2_) Vtp2_ = dalloc<uint16_t>(stream_, static_cast<size_t>(3 * vtp_plane_));
+      stc_b_ = skinny_tc_plan_create(Dxp_, Vtp2_, 3, G_, ldm_, n_, static_cast<int>(m_), n_,
+                                     &st_->done, stream_);
+    }
     GWB_CUDA(cudaStreamSynchronize(stream_));
     return;
   }
@@ -664,6 +680,7 @@ cudaEvent_t BapgEngine::ev_get() {
 int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
   const BapgDev d = dev_view(q);
   int64_t launches = 0;
+  bool row_fused = false;  // half-step a's row update ran inside the chain's last kernel
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   if (timing_) {
     e0 = ev_get();
@@ -675,6 +692,18 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
     // Uᵀ = (D_X·X)ᵀ, then G = (D_Y·Uᵀ)ᵀ: two CSR row-gathers (sparse.cu).
     launch_rowgather(cx_, half_b ? P_ : W_[q], ldm_, m_, Vt_, ldn_, true, &st_->done, stream_);
     launch_rowgather(cy_, Vt_, ldn_, n_, G_, ldm_, true, &st_->done, stream_);
+  } else if (skinny_tc_ && stc_b_ && !quadratic()) {
+    // Fused schedule: a = {GEMM1 on w, GEMM2 + row update + GEMM1 on the new
+    // π}, b = {GEMM2 on the planes half-step a left in Vtp2_}.
+    if (!half_b) {
+      launch_skinny_planes(W_[q], ldm_, DyT_, ldm_, Vtp_, 3, 0, vtp_plane_, n_,
+                           static_cast<int>(m_), m_, &st_->done, stream_);
+      skinny_tc_launch_fused_a(stc_, d, DyT_, ldm_, Vtp2_, vtp_plane_, stream_);
+      row_fused = true;
+    } else {
+      skinny_tc_launch(stc_b_, stream_);
+      launches -= 1;
+    }
   } else if (skinny_tc_) {
     // Vᵀ planes = (X·D_Yᵀ)ᵀ on the FP32 pipes, then G = D_X·V on the tensor cores.
     launch_skinny_planes(half_b ? P_ : W_[q], ldm_, DyT_, ldm_, Vtp_, 3, 0, vtp_plane_, n_,
@@ -700,9 +729,9 @@ int64_t BapgEngine::enqueue_half(int q, bool half_b, double rel_tol) {
   if (!half_b) {
     if (quadratic())
       launch_row_quad(d, stream_);
-    else
+    else if (!row_fused)
       launch_row_update(d, true, stream_);
-    launches += quadratic() ? 2 : 1;  // quadratic: + its flag check
+    launches += quadratic() ? 2 : (row_fused ? 0 : 1);  // quadratic: + its flag check
   } else {
     if (quadratic())
       launch_col_quad(d, stream_);

@@ -170,6 +170,9 @@ class BapgEngine {
   SkinnyTcPlan* stc_tail_ = nullptr;  // skip on flags
   void* Dxp_ = nullptr;               // D_X packed in GEMM2 tile order
   void* Vtp_ = nullptr;               // Vᵀ bf16 planes packed in tile order
+  void* Vtp2_ = nullptr;              // second plane buffer: half-step b's Vᵀ, written by the
+                                      // fused half-step a while Vtp_ is still being streamed
+  SkinnyTcPlan* stc_b_ = nullptr;     // GEMM2 of half-step b on Vtp2_ (fused schedule)
   int64_t vtp_plane_ = 0;             // bf16 elements per packed plane
   bool no_planes() const { return sparse() || fp32() || skinny_tc_; }  // chains read the fp32 iterates
   int aux_mode() const {
