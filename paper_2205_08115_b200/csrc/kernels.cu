@@ -8,6 +8,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/gwb.h"
 #include "devutil.cuh"
@@ -330,6 +331,124 @@ __global__ void __launch_bounds__(kColThreads) col_partial_narrow_kernel(BapgDev
     d.col_pmax[o] = r.mx;
     d.col_psum[o] = r.s;
     d.col_psump[o] = p;
+  }
+}
+
+// Pass 1 for short chunks (≤ kShortRows rows per warp) in at most one wave
+// of CTAs (c1, c3): the
+// online (max, Σ) above runs one dependent fp64 exponential per row and two
+// per warp merge, ~22 in sequence per lane, and that latency — not HBM — is
+// the pass's time at these sizes.  Here the chunk's rows sit in registers:
+// column maxima first (warp-local, then across the 8 warps through shared
+// memory, no exponentials), then Σ π·e^{x − max} with independent
+// exponentials and plain sums across warps.  Same partial (max, Σ, Σπ) per
+// (chunk, column); NaN exponents give (NaN, NaN) as lse64 does.
+constexpr int kShortRows = 8;
+
+template <bool kNarrow>
+__global__ void __launch_bounds__(kColThreads) col_partial_short_kernel(BapgDev d, int rows_per_chunk) {
+  pdl_enter();
+  if (d.st->done || d.st->flags) return;
+  constexpr int C = kNarrow ? 1 : 4;           // columns per lane
+  constexpr int kWarps = kColThreads / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t c0 = kNarrow ? lane : static_cast<int64_t>(blockIdx.x) * kColWidth + lane * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = (r0 + rows_per_chunk < d.n) ? r0 + rows_per_chunk : d.n;
+  const double inv_rho = d.inv_rho64;
+  double x[kShortRows][C], pv[kShortRows][C];
+  double mx[C], ps[C];
+  bool nan[C];
+#pragma unroll
+  for (int q = 0; q < C; ++q) {
+    mx[q] = -INFINITY;
+    ps[q] = 0.0;
+    nan[q] = false;
+  }
+  const bool live = c0 < d.m;
+#pragma unroll
+  for (int u = 0; u < kShortRows; ++u) {
+    const int64_t i = r0 + warp + static_cast<int64_t>(u) * kWarps;
+    const bool ok = live && i < r1;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      x[u][q] = -INFINITY;
+      pv[u][q] = 0.0;
+    }
+    if (ok) {
+      if constexpr (kNarrow) {
+        x[u][0] = expo(d.G[i * d.ld + c0], inv_rho);
+        pv[u][0] = d.P64[i * d.ld + c0];
+      } else {
+        const float4 g4 = *reinterpret_cast<const float4*>(d.G + i * d.ld + c0);
+        load_d4(d.P64 + i * d.ld + c0, pv[u]);
+        x[u][0] = expo(g4.x, inv_rho);
+        x[u][1] = expo(g4.y, inv_rho);
+        x[u][2] = expo(g4.z, inv_rho);
+        x[u][3] = expo(g4.w, inv_rho);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kShortRows; ++u)
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      nan[q] = nan[q] || isnan(x[u][q]);
+      mx[q] = fmax(mx[q], x[u][q]);
+      ps[q] += pv[u][q];
+    }
+  __shared__ double s_mx[kWarps][kColWidth];
+  __shared__ double s_s[kWarps][kColWidth];
+  __shared__ double s_p[kWarps][kColWidth];
+#pragma unroll
+  for (int q = 0; q < C; ++q) s_mx[warp][lane * C + q] = nan[q] ? NAN : mx[q];
+  __syncthreads();
+  double M[C], sum[C];
+#pragma unroll
+  for (int q = 0; q < C; ++q) {
+    double v = s_mx[0][lane * C + q];
+    bool bad = isnan(v);
+#pragma unroll
+    for (int k = 1; k < kWarps; ++k) {
+      const double t = s_mx[k][lane * C + q];
+      bad = bad || isnan(t);
+      v = fmax(v, t);
+    }
+    M[q] = bad ? NAN : v;
+    sum[q] = 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kShortRows; ++u)
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+      const double e = x[u][q] == -INFINITY ? 0.0 : exp(x[u][q] - M[q]);
+      sum[q] = __fma_rn(pv[u][q], e, sum[q]);
+    }
+#pragma unroll
+  for (int q = 0; q < C; ++q) {
+    s_s[warp][lane * C + q] = sum[q];
+    s_p[warp][lane * C + q] = ps[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < (kNarrow ? 32 : kColWidth)) {
+    const int c = threadIdx.x;
+    const int64_t col = kNarrow ? c : static_cast<int64_t>(blockIdx.x) * kColWidth + c;
+    if (col < d.m) {
+      double mc = s_mx[0][c];
+      bool bad = isnan(mc);
+      double sc = 0.0, p = 0.0;
+      for (int k = 0; k < kWarps; ++k) {
+        const double t = s_mx[k][c];
+        bad = bad || isnan(t);
+        mc = fmax(mc, t);
+        sc += s_s[k][c];
+        p += s_p[k][c];
+      }
+      const int64_t o = static_cast<int64_t>(blockIdx.y) * d.m + col;
+      d.col_pmax[o] = bad ? NAN : mc;
+      d.col_psum[o] = bad ? NAN : sc;
+      d.col_psump[o] = p;
+    }
   }
 }
 
@@ -771,6 +890,31 @@ void launch_col_write_pass(const BapgDev& d, cudaStream_t s) {
 }
 }  // namespace
 
+namespace {
+void launch_col_partial_pass(const BapgDev& d, dim3 grid, int rows_per_chunk, cudaStream_t s) {
+  // GWB_COL_ONLINE=1 keeps the online (max, Σ) pass at every size (A/B knob).
+  static const bool online_env = [] {
+    const char* e = std::getenv("GWB_COL_ONLINE");
+    return e && e[0] == '1';
+  }();
+  // Short form only where the pass is at most one wave of CTAs, i.e. bound by
+  // one CTA's latency (c1 +2.8%, c3 +1.2%); with several CTAs per SM the
+  // online form's streaming loads win (c2: −2.9% with the short form).
+  const int64_t ctas = static_cast<int64_t>(d.m <= 32 ? 1 : grid.x) * d.chunks;
+  const bool is_short =
+      !online_env && rows_per_chunk <= kShortRows * (kColThreads / 32) && ctas <= 148;
+  const dim3 narrow_grid(1, static_cast<unsigned>(d.chunks));
+  if (d.m <= 32 && is_short)
+    launch_pdl(col_partial_short_kernel<true>, narrow_grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  else if (d.m <= 32)
+    launch_pdl(col_partial_narrow_kernel, narrow_grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  else if (is_short)
+    launch_pdl(col_partial_short_kernel<false>, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  else
+    launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+}
+}  // namespace
+
 void launch_row_update(const BapgDev& d, bool write, cudaStream_t s) {
   if (!d.P64) {  // fp32 iterates (quadratic geometry): diagnostics only
     if (!write && d.n >= 1) row_diag32_kernel<<<static_cast<unsigned>(d.n), kRowThreads, 0, s>>>(d);
@@ -797,11 +941,7 @@ void launch_col_update(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  if (d.m <= 32)
-    launch_pdl(col_partial_narrow_kernel, dim3(1, static_cast<unsigned>(d.chunks)), dim3(kColThreads), 0,
-               s, d, rows_per_chunk);
-  else
-    launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  launch_col_partial_pass(d, grid, rows_per_chunk, s);
   launch_pdl(col_combine_kernel, dim3(grid1d(d.m * 32, 256)), dim3(256), 0, s, d);
   launch_col_write_pass(d, s);
 }
@@ -811,11 +951,7 @@ void launch_col_partial(const BapgDev& d, cudaStream_t s) {
   const int rows_per_chunk = static_cast<int>((d.n + d.chunks - 1) / d.chunks);
   dim3 grid(static_cast<unsigned>((d.m + kColWidth - 1) / kColWidth),
             static_cast<unsigned>(d.chunks));
-  if (d.m <= 32)
-    launch_pdl(col_partial_narrow_kernel, dim3(1, static_cast<unsigned>(d.chunks)), dim3(kColThreads), 0,
-               s, d, rows_per_chunk);
-  else
-    launch_pdl(col_partial_kernel, grid, dim3(kColThreads), 0, s, d, rows_per_chunk);
+  launch_col_partial_pass(d, grid, rows_per_chunk, s);
 }
 
 void launch_col_write(const BapgDev& d, cudaStream_t s) {
