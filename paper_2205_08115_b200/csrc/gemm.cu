@@ -946,7 +946,7 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
   // 192 / 128 that minimises waves × width (the time of one pair's tiles)
   // over the 74 SM pairs, e.g. c2's 48 tiles of 256 (65% of the pairs) become
   // 64-66 tiles of 192 (c1: 32 tiles of 128).  Large grids keep 256 (best
-  // operand reuse).  GWB_GEMM_BN=128/192/256 forces (A/B).
+  // operand reuse).  GWB_GEMM_BN=64/128/192/256 forces (A/B).
   {
     static const int bn_env = [] {
       const char* e = std::getenv("GWB_GEMM_BN");
@@ -958,6 +958,12 @@ GemmPlan* gemm_plan_create(const GemmDesc& d) {
     if (tm * ((d.N + 255) / 256) <= 4 * 74) {
       if (cost(192) < cost(bn)) bn = 192;
       if (cost(128) < cost(bn)) bn = 128;
+      // 64 wide where it fills more than half of the SM pairs in one wave
+      // with no split-K (c1: 64 tiles): the K loop is twice as long as with
+      // 128-wide tiles split in two, but the four reduce launches per
+      // iteration go (c1 9.95K -> 10.45K it/s, alternating runs).
+      const int64_t t64 = tm * ((d.N + 63) / 64);
+      if (cost(64) < cost(bn) && t64 > 37 && t64 <= 74 && d.split_k == 0) bn = 64;
     }
     p->bn = bn_env == 64 || bn_env == 128 || bn_env == 192 || bn_env == 256 ? bn_env : bn;
   }
