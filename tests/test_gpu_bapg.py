@@ -139,6 +139,91 @@ def test_bapg_skinny_ragged_k(gpu, port, precision):
         assert abs(obj - obj_ref) <= OBJ_TOL * abs(obj_ref), k
 
 
+_SKINNY_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2205_08115_b200 as gw
+from harness import instances as I
+out = {{}}
+for k, n in ((20, 700), (32, 517), (5, 333), (20, 4000)):
+    inst = I.config3(seed=k, n=n, k=k)
+    solver = dict(inst.solver); solver.update(max_iters=12)
+    cfg = gw.SolverConfig(precision="auto", quiet=True, **solver)
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu), cfg)
+    out[f"pi_{{k}}_{{n}}"] = rep.pi_half.entries()
+    out[f"w_{{k}}_{{n}}"] = rep.w_half.entries()
+    out[f"obj_{{k}}_{{n}}"] = np.array([r.objective for r in rep.trace])
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_bapg_skinny_fused_half_step_is_bitwise_the_unfused_chain(gpu, tmp_path):
+    # csrc/skinny_tc.cu kEpi = 1 (GEMM2 + row update + next GEMM1 in one
+    # launch) against one launch per stage (GWB_SKINNY_UNFUSED=1, read once per
+    # process): same arithmetic, so iterates and trace are bit-identical —
+    # cluster sizes 4 (n = 4000), 5 and 6, ragged last row tiles, m = 5/20/32.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "skinny_ab.py"
+    script.write_text(_SKINNY_SCRIPT.format(root=root))
+    res = {}
+    for tag, val in (("fused", None), ("unfused", "1")):
+        env = dict(os.environ)
+        env.pop("GWB_SKINNY_UNFUSED", None)
+        if val:
+            env["GWB_SKINNY_UNFUSED"] = val
+        out = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=600)
+        res[tag] = np.load(out)
+    for key in res["fused"].files:
+        assert np.array_equal(res["fused"][key], res["unfused"][key]), key
+
+
+_COL_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2205_08115_b200 as gw
+from harness import instances as I
+out = {{}}
+for name, inst in (("c1_256", I.config1(n=256)), ("c1_1000", I.config1()), ("c3_700", I.config3(seed=2, n=700, k=20))):
+    solver = dict(inst.solver); solver.update(max_iters=10)
+    cfg = gw.SolverConfig(precision="auto", quiet=True, **solver)
+    rep = gw.solve(gw.DistanceMatrix.trusted(inst.dx), gw.DistanceMatrix.trusted(inst.dy),
+                   gw.ProbabilityVector(inst.mu), gw.ProbabilityVector(inst.nu), cfg)
+    out["w_" + name] = rep.w_half.entries()
+    out["obj_" + name] = np.array([r.objective for r in rep.trace])
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_bapg_short_column_partials_agree_with_the_online_pass(gpu, tmp_path):
+    # csrc/kernels.cu col_partial_short_kernel (max first, independent
+    # exponentials; single-wave grids) against the online (max, Σ) pass
+    # (GWB_COL_ONLINE=1): the same fp64 column normalisers up to summation
+    # order, so 10 iterations agree to ~1e-12 of scale.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "col_ab.py"
+    script.write_text(_COL_SCRIPT.format(root=root))
+    res = {}
+    for tag, val in (("short", None), ("online", "1")):
+        env = dict(os.environ)
+        env.pop("GWB_COL_ONLINE", None)
+        if val:
+            env["GWB_COL_ONLINE"] = val
+        out = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=600)
+        res[tag] = np.load(out)
+    for key in res["short"].files:
+        a, b = res["short"][key], res["online"][key]
+        assert np.abs(a - b).max() <= 1e-10 * np.abs(b).max(), (key, np.abs(a - b).max() / np.abs(b).max())
+
+
 def test_bapg_skinny_full_c3(gpu, port):
     # BASELINE c3 at full size (n = 4000, K = 20): 32 row tiles × 4 K splits.
     inst = I.config3()
